@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 H^2 mat-vec hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one single-vector H^2 mat-vec y = A x (hmv.hpp:175-188) over the
+n = 2^22 2D exponential-covariance matrix (leaf 64, Chebyshev order 8 -> rank
+64, eta 2, ell 0.1, perturbation 0.25, seed 1; BASELINE.json configs[3], the
+"n=2^22" the metric is quoted at), built directly in HBM (76.98 GB, > L2).
+
+value  = reference bytes (memory_footprint(A).total(), h2kit.cpp:131-132) / device
+         time per step, whole job (sum over ranks of bytes / max-over-ranks time).
+e2e    = the same metric through the public API with pinned HOST x/y: each step
+         copies x H2D and y D2H inside h2b_hmv (counted in the timed region).
+roofline = the dominant kernel (k_bsr: coupling + dense blocks) from per-phase
+         CUDA events recorded on the launching stream during the timed region.
+cpu_baseline = the unmodified reference (oracle/_ref, OpenMP, all host cores)
+         on a bounded sample (2D n=2^18, same structure family).
+
+N > 1 (torchrun): every rank holds its own replica of the matrix on its GPU and
+runs the full mat-vec ("replicas"; see DESIGN.md §6 for the subtree-partitioned
+plan), scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "H2 mat-vec GB/s (% of HBM peak) & ms at n=2^22; compression GFLOP/s"
+WORKLOAD = dict(workload="H2 single-vector mat-vec, 2D exponential covariance", dim=2,
+                n=1 << 22, leaf_size=64, grid_order=8, rank=64, eta=2.0, ell=0.1,
+                perturbation=0.25, seed=1)
+CPU_SAMPLE_N = 1 << 18
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per k_bsr launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        if d.get("workload_n") == WORKLOAD["n"]:
+            return float(d["k_bsr_dram_bytes"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_sample(steps: int | None = None, budget_s: float = 20.0):
+    """The unmodified reference hmv on the host cores (bounded sample)."""
+    import numpy as np
+
+    import oracle
+    kind = "reference" if oracle.reference_available() else "port"
+    be = oracle.best()
+    cores = os.cpu_count() or 1
+    be.set_threads(cores)
+    t0 = time.time()
+    A = be.construct(2, CPU_SAMPLE_N, grid_order=8)
+    build_s = time.time() - t0
+    x = be.random_vector(CPU_SAMPLE_N, 1)
+    A.hmv(x)  # warm-up
+    fp = A.footprint()
+    times = []
+    t_all = time.time()
+    while True:
+        t = time.perf_counter()
+        A.hmv(x)
+        times.append(time.perf_counter() - t)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and (time.time() - t_all > budget_s or len(times) >= 200):
+            break
+    mean = sum(times) / len(times)
+    return {"value": fp / mean / 1e9, "unit": "GB/s", "cores": be.max_threads(), "kind": kind,
+            "ms_per_step": mean * 1e3,
+            "sample": f"reference hmv (OpenMP, {be.max_threads()} threads) on 2D n=2^18 k=64 "
+                      f"({fp / 1e9:.3f} GB footprint), {len(times)} reps after 1 warm-up; "
+                      f"host construct {build_s:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if rank != 0:
+        return
+    cb = cpu_reference_sample(steps=max(1, args.steps))
+    line = {"metric": METRIC, "value": round(cb["value"], 3), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cb["ms_per_step"], 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": dict(WORKLOAD, n=CPU_SAMPLE_N,
+                           note="CPU sample of the n=2^22 workload (77 GB does not fit a bounded "
+                                "CPU run); same structure family, same metric"),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": round(cb["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=WORKLOAD["n"], help="override n (testing only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    args.warmup = max(3, args.warmup)
+
+    import numpy as np
+    import torch
+
+    import paper_1902_01829_b200 as h2
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    cfg = dict(WORKLOAD, n=args.n)
+    t0 = time.time()
+    A = h2.H2Matrix.construct(cfg["dim"], cfg["n"], leaf_size=cfg["leaf_size"],
+                              grid_order=cfg["grid_order"], eta=cfg["eta"], ell=cfg["ell"],
+                              perturbation=cfg["perturbation"], seed=cfg["seed"], device=local)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    info = A.info()
+    fp = info.footprint_bytes
+    n = info.n
+    gen = torch.Generator(device="cuda").manual_seed(1 + rank)
+    xt = torch.rand(n, dtype=torch.float64, device="cuda", generator=gen)
+    yt = torch.zeros(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    # launches per step: up_leaf + per-level up + bsr + per-level down + down_leaf
+    r = info.ranks
+    launches = 1 + sum(1 for l in range(1, info.depth + 1) if r[l - 1] > 0 and r[l] > 0) + 1 \
+        + sum(1 for l in range(1, info.depth + 1) if r[l] > 0 and r[l - 1] > 0) + 1
+
+    for _ in range(args.warmup):
+        h2.hmv(A, xt, yt, stream=sp)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region --------------------------------
+    A.set_phase_timing(True)
+    A.last_hmv_timing()  # reset
+    sampler = ClockSampler(local) if rank == 0 else None
+    barrier(world)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        h2.hmv(A, xt, yt, stream=sp)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop() if sampler else None
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    phases = A.last_hmv_timing()
+    A.set_phase_timing(False)
+    ms = max_over_ranks(ms_local, world)
+    value = world * fp / (ms * 1e-3) / 1e9
+
+    # ---- end-to-end through the public API with pinned host buffers ----
+    xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xh.copy_(xt.cpu())
+    xn, yn = xh.numpy(), yh.numpy()
+    for _ in range(2):
+        h2.hmv(A, xn, yn, stream=sp)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        h2.hmv(A, xn, yn, stream=sp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    e2e_value = world * fp / (e2e_ms * 1e-3) / 1e9
+    # correctness spot check of the e2e result against the device result
+    assert np.allclose(yn, yt.cpu().numpy(), rtol=1e-13, atol=0)
+
+    if rank != 0:
+        return
+    peak, peak_src = load_peaks()
+    bsr_bytes = 8 * (sum(info.cpl_blocks[l] * r[l] * r[l] for l in range(info.depth + 1))
+                     + info.dense_blocks * info.m * info.m)
+    bsr_ms = phases[1]
+    achieved = bsr_bytes / (bsr_ms * 1e-3) / 1e9 if bsr_ms > 0 else None
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(budget_s=15.0)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": dict(cfg, parallelism=f"replicas{world}" if world > 1 else "single",
+                       footprint_bytes=fp, l2="inputs larger than L2 (76.98 GB matrix per step)",
+                       build_s=round(build_s, 2)),
+        "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
+        "phase_ms": {"upsweep": round(phases[0], 4), "coupling_dense_bsr": round(phases[1], 4),
+                     "downsweep_scatter": round(phases[2], 4)},
+        "roofline": {"bound": "hbm", "kernel": "k_bsr (coupling + dense blocks)",
+                     "achieved": round(achieved, 1) if achieved else None, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4) if achieved else None,
+                     "traffic": load_traffic(), "algorithmic_bytes_per_launch": bsr_bytes},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

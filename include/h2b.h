@@ -1,0 +1,187 @@
+/*
+ * h2b.h — C-ABI of the B200-native H^2-matrix hot path (libh2b.so).
+ *
+ * Drop-in boundary for the reference library h2kit (arXiv 1902.01829 reference,
+ * /root/reference/proj).  The reference has no FFI layer of its own: its seams
+ * are C++ function templates over H2Matrix<T>.  Each entry
+ * point below replaces one of them; the header-only C++ shim
+ * include/h2kit_b200.hpp re-exposes them under the reference's own names and
+ * signatures (h2kit_b200::hmv, ::compress, ...), and INTEGRATION.md shows the
+ * binding a maintainer adds.
+ *
+ *   h2b_hmv              <- h2kit::hmv(A, x, y, alpha, beta[, ctx])   include/h2kit/hmv.hpp:175-194
+ *   h2b_hmv_multi        <- (no reference API; SPEC.md:497 non-goal) column-wise hmv
+ *   h2b_upsweep          <- h2kit::upsweep(V, xc, n, xhat)            hmv.hpp:79-111
+ *   h2b_tree_multiply    <- h2kit::tree_multiply(S, xhat, yhat)       hmv.hpp:114-125
+ *   h2b_downsweep        <- h2kit::downsweep(U, yhat, yc, n)          hmv.hpp:129-157
+ *   h2b_dense_mv         <- h2kit::block_sparse_mv(A.dense, xc, yc, alpha, beta)  bsr.hpp:79-82
+ *   h2b_compress         <- h2kit::compress(A, eps)                   include/h2kit/compression.hpp:466-551
+ *   h2b_orthogonalize    <- h2kit::orthogonalize_basis(B)             compression.hpp:69-126
+ *   h2b_matrix_build     <- h2kit::construct<double>(points, spec, cfg)  include/h2kit/construction.hpp:179-200
+ *   h2b_matrix_create    <- (host H2Matrix<double> -> device mirror; the HmvContext analogue hmv.hpp:161-172)
+ *   h2b_matrix_export    <- (device -> host H2Matrix<double> arrays, e.g. after compress)
+ *   h2b_matrix_footprint <- h2kit::memory_footprint(A).total()       include/h2kit/h2_matrix.hpp:90-102
+ *
+ * Conventions
+ *  - All scalars are FP64, all matrices column-major, index type int32
+ *    (h2kit::index_t, include/h2kit/defs.hpp:15); offsets/sizes are int64.
+ *  - The flat host layout ("export layout") is the reference's own pool
+ *    layout concatenated over levels:
+ *      perm[n]; ranks[depth+1];
+ *      leaf: 2^depth blocks of m x ranks[depth]            (BasisTree::leaf_pool)
+ *      transfer: for l = 1..depth, 2^l blocks of ranks[l] x ranks[l-1]  (BasisTree::transfer[l])
+ *      cpl_row_ptr: for l = 0..depth, 2^l + 1 entries      (BSRLayer::row_ptr, level-local)
+ *      cpl_col_idx / cpl_values: for l = 0..depth, nb_l entries / nb_l blocks of ranks[l]^2
+ *      dense_row_ptr[2^depth + 1], dense_col_idx[nbd], dense_values[nbd * m * m]
+ *  - Errors: every function returns an h2b_status; H2B_INVALID_ARGUMENT is
+ *    the reference's std::invalid_argument (defs.hpp:20-22), with the same
+ *    message text, retrievable through h2b_last_error() (thread-local).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns H2B_NO_DEVICE.
+ */
+#ifndef H2B_H
+#define H2B_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define H2B_API __attribute__((visibility("default")))
+#else
+#define H2B_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  H2B_OK = 0,
+  H2B_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  H2B_CUDA_ERROR = 2,
+  H2B_OUT_OF_MEMORY = 3,
+  H2B_UNSUPPORTED = 4,      /* shape outside the compiled kernel envelope */
+  H2B_NO_DEVICE = 5,
+  H2B_INTERNAL = 6
+} h2b_status;
+
+typedef enum {
+  H2B_PTR_AUTO = 0,   /* detect with cudaPointerGetAttributes */
+  H2B_PTR_HOST = 1,   /* host memory (pinned or pageable); copies happen inside the call */
+  H2B_PTR_DEVICE = 2  /* device memory on the matrix's device */
+} h2b_ptr_kind;
+
+typedef struct h2b_matrix h2b_matrix;
+
+/* Host description of a symmetric H^2 matrix in the export layout. */
+typedef struct {
+  int32_t n;          /* points; n == m * 2^depth */
+  int32_t m;          /* leaf size (BasisTree::leaf_dim) */
+  int32_t depth;      /* q */
+  int32_t symmetric;  /* must be 1 (construct() always produces symmetric matrices) */
+  const int32_t* perm;
+  const int32_t* ranks;
+  const double* leaf;
+  const double* transfer;
+  const int32_t* cpl_row_ptr;
+  const int32_t* cpl_col_idx;
+  const double* cpl_values;
+  const int32_t* dense_row_ptr;
+  const int32_t* dense_col_idx;
+  const double* dense_values;
+} h2b_matrix_desc;
+
+/* Parameters of the reference's ab-initio construction (ConstructionConfig +
+ * KernelSpec + generate_perturbed_grid, construction.hpp:15-25, kernels.hpp:10-22,
+ * geometry.hpp:41-45). */
+typedef struct {
+  int32_t dim;          /* 2 or 3 */
+  int32_t n;            /* points */
+  int32_t leaf_size;    /* m (64) */
+  int32_t grid_order;   /* Chebyshev order per axis; rank = order^dim */
+  double eta;           /* admissibility (2.0) */
+  double ell;           /* correlation length of exp(-r/ell) */
+  double perturbation;  /* grid jitter (0.25) */
+  uint64_t seed;        /* mt19937_64 seed (1) */
+} h2b_build_config;
+
+/* Sizes of a matrix in the export layout. */
+typedef struct {
+  int32_t n, m, depth, symmetric;
+  int32_t ranks[32];
+  int64_t cpl_blocks[32];     /* blocks per coupling level */
+  int32_t cpl_max_row[32];    /* max blocks in one block row, per level */
+  int64_t dense_blocks;
+  int32_t dense_max_row;
+  uint64_t footprint_bytes;   /* memory_footprint(A).total(): reference byte convention */
+  uint64_t device_bytes;      /* HBM actually held by the handle (pools + workspace) */
+  double hmv_flops;           /* reference analytic flop model of one hmv (flops.hpp) */
+} h2b_matrix_info;
+
+/* compress() report (CompressionReport, compression.hpp:422-441). Times are
+ * device-measured (CUDA events); flops follow the reference analytic model. */
+typedef struct {
+  int32_t old_ranks[32];
+  int32_t new_ranks[32];
+  uint64_t bytes_before, bytes_after;
+  double frobenius_error;
+  double frobenius_norm;
+  double time_orthogonalize_ms, time_project_orth_ms, time_weights_ms,
+         time_truncate_ms, time_project_trunc_ms;
+  double flops_orthogonalize, flops_project_orth, flops_weights,
+         flops_truncate, flops_project_trunc;
+} h2b_compress_report;
+
+H2B_API const char* h2b_last_error(void);
+H2B_API const char* h2b_version(void);
+
+/* Device count visible to the library; 0 means no usable sm_100 device. */
+H2B_API int h2b_device_count(void);
+
+H2B_API h2b_status h2b_matrix_create(const h2b_matrix_desc* desc, int device, h2b_matrix** out);
+H2B_API h2b_status h2b_matrix_build(const h2b_build_config* cfg, int device, h2b_matrix** out);
+H2B_API h2b_status h2b_matrix_destroy(h2b_matrix* A);
+H2B_API h2b_status h2b_matrix_info_get(const h2b_matrix* A, h2b_matrix_info* info);
+/* Copy the device matrix into caller-allocated host arrays (export layout,
+ * sizes from h2b_matrix_info_get). Any pointer may be NULL to skip it. */
+H2B_API h2b_status h2b_matrix_export(const h2b_matrix* A, int32_t* perm, double* leaf, double* transfer,
+                             int32_t* cpl_row_ptr, int32_t* cpl_col_idx, double* cpl_values,
+                             int32_t* dense_row_ptr, int32_t* dense_col_idx, double* dense_values);
+H2B_API uint64_t h2b_matrix_footprint(const h2b_matrix* A);
+
+/* y <- alpha (A_D + A_LR) x + beta y, x and y in original point order.
+ * beta == 0 never reads y (hmv.hpp:186). stream is a cudaStream_t (NULL =
+ * the matrix's own stream). Host pointers: the call is synchronous. */
+H2B_API h2b_status h2b_hmv(h2b_matrix* A, const double* x, double* y, double alpha, double beta,
+                   h2b_ptr_kind kind, void* stream);
+/* nvec columns, leading dimensions ldx/ldy (>= n). */
+H2B_API h2b_status h2b_hmv_multi(h2b_matrix* A, int nvec, const double* X, int64_t ldx, double* Y,
+                         int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream);
+
+/* Phase entry points (device or host pointers, cluster order; node vectors
+ * are level-concatenated: level l holds 2^l * ranks[l] doubles). */
+H2B_API h2b_status h2b_upsweep(h2b_matrix* A, const double* xc, double* xhat, h2b_ptr_kind kind);
+H2B_API h2b_status h2b_tree_multiply(h2b_matrix* A, const double* xhat, double* yhat, h2b_ptr_kind kind);
+H2B_API h2b_status h2b_downsweep(h2b_matrix* A, const double* yhat, double* yc, h2b_ptr_kind kind);
+H2B_API h2b_status h2b_dense_mv(h2b_matrix* A, const double* xc, double* yc, double alpha, double beta,
+                        h2b_ptr_kind kind);
+
+/* Algebraic recompression in place (orthogonalize, project, weights,
+ * truncate at relative eps, project).  Exclusive access required. */
+H2B_API h2b_status h2b_compress(h2b_matrix* A, double eps, h2b_compress_report* report);
+/* Orthogonalize only (in place); projection tree written to t_out (host,
+ * level-concatenated ranks[l]^2 per node) when non-NULL. */
+H2B_API h2b_status h2b_orthogonalize(h2b_matrix* A, double* t_out);
+
+/* Per-phase device time of the h2b_hmv calls made since phase timing was
+ * enabled or last read, averaged per call (ms; CUDA events recorded on the
+ * launching stream, no host syncs inside h2b_hmv):
+ * [0]=upsweep [1]=coupling+dense BSR [2]=downsweep+scatter [3]=total.  Resets. */
+H2B_API h2b_status h2b_last_hmv_timing(h2b_matrix* A, double* ms4);
+/* Enable/disable per-phase event timing inside h2b_hmv (default off). */
+H2B_API h2b_status h2b_set_phase_timing(h2b_matrix* A, int on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2B_H */

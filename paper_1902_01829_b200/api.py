@@ -1,0 +1,260 @@
+"""Python mirror of the reference h2kit operator API for the hot path.
+
+Same names, argument meaning and error behaviour as the reference C++ templates
+(include/h2kit/hmv.hpp, compression.hpp, construction.hpp), over the B200
+C-ABI (include/h2b.h).  Invalid arguments raise ``H2bInvalidArgument`` (a
+``ValueError``), the Python face of the reference's ``std::invalid_argument``.
+
+Vectors may be numpy arrays (host; copies happen inside the call) or CUDA
+tensors / any object exposing ``data_ptr()`` on the matrix's device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .host import HostMatrix
+
+
+def _ptr(a):
+    if a is None:
+        return None, _lib.PTR_AUTO
+    if isinstance(a, np.ndarray):
+        if a.dtype not in (np.float64, np.int32) or not a.flags.c_contiguous:
+            raise ValueError("arrays must be C-contiguous float64/int32")
+        return a.ctypes.data, _lib.PTR_HOST
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr(), (_lib.PTR_DEVICE if getattr(a, "is_cuda", False) else _lib.PTR_HOST)
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+@dataclass
+class MatrixInfo:
+    n: int
+    m: int
+    depth: int
+    ranks: list
+    cpl_blocks: list
+    cpl_max_row: list
+    dense_blocks: int
+    dense_max_row: int
+    footprint_bytes: int
+    device_bytes: int
+    hmv_flops: float
+
+
+class H2Matrix:
+    """Device-resident symmetric H^2 matrix (the reference's H2Matrix<double>,
+    h2_matrix.hpp:62-80, plus its HmvContext workspace, hmv.hpp:161-172)."""
+
+    def __init__(self, handle: int, device: int):
+        self._h = C.c_void_p(handle)
+        self.device = device
+
+    # -- construction -------------------------------------------------
+    @classmethod
+    def from_host(cls, hm: HostMatrix, device: int = 0) -> "H2Matrix":
+        lib = _lib.load()
+        keep = [np.ascontiguousarray(a) for a in (hm.perm, hm.ranks, hm.leaf, hm.transfer,
+                                                    hm.cpl_row_ptr, hm.cpl_col_idx, hm.cpl_values,
+                                                    hm.dense_row_ptr, hm.dense_col_idx,
+                                                    hm.dense_values)]
+        d = _lib.MatrixDesc(hm.n, hm.m, hm.depth, 1, *[a.ctypes.data for a in keep])
+        out = C.c_void_p()
+        _lib.check(lib.h2b_matrix_create(C.byref(d), device, C.byref(out)))
+        return cls(out.value, device)
+
+    @classmethod
+    def construct(cls, dim: int, n: int, leaf_size: int = 64, grid_order: int | None = None,
+                  eta: float = 2.0, ell: float | None = None, perturbation: float = 0.25,
+                  seed: int = 1, device: int = 0) -> "H2Matrix":
+        """construct<double>(generate_perturbed_grid(dim, n, perturbation, seed),
+        KernelSpec{ell}, ConstructionConfig{leaf_size, grid_order, eta}) built on the
+        device (construction.hpp:179-200; defaults of tools/h2kit.cpp:55-58)."""
+        lib = _lib.load()
+        if grid_order is None:
+            grid_order = 8 if dim == 2 else 4
+        if ell is None:
+            ell = 0.1 if dim == 2 else 0.2
+        cfg = _lib.BuildConfig(dim, n, leaf_size, grid_order, eta, ell, perturbation, seed)
+        out = C.c_void_p()
+        _lib.check(lib.h2b_matrix_build(C.byref(cfg), device, C.byref(out)))
+        A = cls(out.value, device)
+        A.build_config = dict(dim=dim, n=n, leaf_size=leaf_size, grid_order=grid_order, eta=eta,
+                              ell=ell, perturbation=perturbation, seed=seed)
+        return A
+
+    def close(self):
+        if self._h and self._h.value:
+            _lib.check(_lib.load().h2b_matrix_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- queries --------------------------------------------------------
+    def info(self) -> MatrixInfo:
+        inf = _lib.MatrixInfo()
+        _lib.check(_lib.load().h2b_matrix_info_get(self._h, C.byref(inf)))
+        q = inf.depth
+        return MatrixInfo(inf.n, inf.m, q, list(inf.ranks[:q + 1]), list(inf.cpl_blocks[:q + 1]),
+                          list(inf.cpl_max_row[:q + 1]), inf.dense_blocks, inf.dense_max_row,
+                          inf.footprint_bytes, inf.device_bytes, inf.hmv_flops)
+
+    @property
+    def n(self) -> int:
+        return self.info().n
+
+    def memory_footprint(self) -> int:
+        """memory_footprint(A).total() (h2_matrix.hpp:90-102)."""
+        return int(_lib.load().h2b_matrix_footprint(self._h))
+
+    def to_host(self) -> HostMatrix:
+        inf = self.info()
+        hm = HostMatrix.empty(inf.n, inf.m, inf.depth, inf.ranks, inf.cpl_blocks,
+                              inf.dense_blocks)
+        _lib.check(_lib.load().h2b_matrix_export(self._h, *[a.ctypes.data for a in hm.arrays()]))
+        return hm
+
+    def vec_size(self) -> int:
+        inf = self.info()
+        return sum((1 << l) * r for l, r in enumerate(inf.ranks))
+
+    # -- hot path -------------------------------------------------------
+    def set_phase_timing(self, on: bool = True):
+        _lib.check(_lib.load().h2b_set_phase_timing(self._h, int(on)))
+
+    def last_hmv_timing(self):
+        buf = (C.c_double * 4)()
+        _lib.check(_lib.load().h2b_last_hmv_timing(self._h, buf))
+        return list(buf)
+
+
+def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=None):
+    """y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-194). Returns y."""
+    if y is None:
+        if isinstance(x, np.ndarray):
+            y = np.zeros_like(x)
+        else:
+            import torch
+            y = torch.zeros_like(x)
+    px, kx = _ptr(x)
+    py, ky = _ptr(y)
+    kind = _lib.PTR_DEVICE if (kx == ky == _lib.PTR_DEVICE) else (
+        _lib.PTR_HOST if (kx == ky == _lib.PTR_HOST) else _lib.PTR_AUTO)
+    _lib.check(_lib.load().h2b_hmv(A._h, px, py, float(alpha), float(beta), kind,
+                                   None if stream is None else C.c_void_p(stream)))
+    return y
+
+
+def hmv_multi(A: H2Matrix, X: np.ndarray, alpha: float = 1.0, beta: float = 0.0, Y=None):
+    """Column-wise hmv of X (n x nvec, column-major i.e. X[:, v] contiguous when
+    passed as a (nvec, n) C array)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    nvec, n = X.shape
+    if Y is None:
+        Y = np.zeros_like(X)
+    _lib.check(_lib.load().h2b_hmv_multi(A._h, nvec, X.ctypes.data, n, Y.ctypes.data, n,
+                                         float(alpha), float(beta), _lib.PTR_HOST, None))
+    return Y
+
+
+def upsweep(A: H2Matrix, xc: np.ndarray) -> np.ndarray:
+    """upsweep(V, xc, n, xhat) (hmv.hpp:79-111); xc in cluster order."""
+    xc = np.ascontiguousarray(xc, dtype=np.float64)
+    out = np.zeros(A.vec_size(), np.float64)
+    _lib.check(_lib.load().h2b_upsweep(A._h, xc.ctypes.data, out.ctypes.data, _lib.PTR_HOST))
+    return out
+
+
+def tree_multiply(A: H2Matrix, xhat: np.ndarray) -> np.ndarray:
+    """tree_multiply(S, xhat, yhat) (hmv.hpp:114-125)."""
+    xhat = np.ascontiguousarray(xhat, dtype=np.float64)
+    out = np.zeros_like(xhat)
+    _lib.check(_lib.load().h2b_tree_multiply(A._h, xhat.ctypes.data, out.ctypes.data,
+                                             _lib.PTR_HOST))
+    return out
+
+
+def downsweep(A: H2Matrix, yhat: np.ndarray, yc: np.ndarray) -> np.ndarray:
+    """downsweep(U, yhat, yc, n) (hmv.hpp:129-157): returns yc + U-expansion."""
+    yhat = np.ascontiguousarray(yhat, dtype=np.float64)
+    yc = np.array(yc, dtype=np.float64, copy=True)
+    _lib.check(_lib.load().h2b_downsweep(A._h, yhat.ctypes.data, yc.ctypes.data, _lib.PTR_HOST))
+    return yc
+
+
+def dense_mv(A: H2Matrix, xc: np.ndarray) -> np.ndarray:
+    """block_sparse_mv(A.dense, xc, yc, 1, 0) (bsr.hpp:79-82)."""
+    xc = np.ascontiguousarray(xc, dtype=np.float64)
+    out = np.zeros_like(xc)
+    _lib.check(_lib.load().h2b_dense_mv(A._h, xc.ctypes.data, out.ctypes.data, 1.0, 0.0,
+                                        _lib.PTR_HOST))
+    return out
+
+
+@dataclass
+class CompressionReport:
+    """CompressionReport (compression.hpp:422-441)."""
+    old_ranks: list
+    new_ranks: list
+    bytes_before: int
+    bytes_after: int
+    frobenius_error: float
+    frobenius_norm: float
+    time_orthogonalize_ms: float
+    time_project_orth_ms: float
+    time_weights_ms: float
+    time_truncate_ms: float
+    time_project_trunc_ms: float
+    flops_orthogonalize: float
+    flops_project_orth: float
+    flops_weights: float
+    flops_truncate: float
+    flops_project_trunc: float
+
+    def total_flops(self) -> float:
+        return (self.flops_orthogonalize + self.flops_project_orth + self.flops_weights
+                + self.flops_truncate + self.flops_project_trunc)
+
+    def total_ms(self) -> float:
+        return (self.time_orthogonalize_ms + self.time_project_orth_ms + self.time_weights_ms
+                + self.time_truncate_ms + self.time_project_trunc_ms)
+
+
+def compress(A: H2Matrix, eps: float) -> CompressionReport:
+    """compress(A, eps) (compression.hpp:466-551), in place on the device."""
+    depth = A.info().depth
+    rep = _lib.CompressReport()
+    _lib.check(_lib.load().h2b_compress(A._h, float(eps), C.byref(rep)))
+    return CompressionReport(
+        list(rep.old_ranks[:depth + 1]), list(rep.new_ranks[:depth + 1]), rep.bytes_before,
+        rep.bytes_after, rep.frobenius_error, rep.frobenius_norm, rep.time_orthogonalize_ms,
+        rep.time_project_orth_ms, rep.time_weights_ms, rep.time_truncate_ms,
+        rep.time_project_trunc_ms, rep.flops_orthogonalize, rep.flops_project_orth,
+        rep.flops_weights, rep.flops_truncate, rep.flops_project_trunc)
+
+
+def orthogonalize_basis(A: H2Matrix) -> np.ndarray:
+    """orthogonalize_basis(B) (compression.hpp:69-126): returns the projection tree
+    (level-concatenated k_l x k_l blocks)."""
+    inf = A.info()
+    out = np.zeros(sum((1 << l) * r * r for l, r in enumerate(inf.ranks)), np.float64)
+    _lib.check(_lib.load().h2b_orthogonalize(A._h, out.ctypes.data))
+    return out
+
+
+def device_count() -> int:
+    return int(_lib.load().h2b_device_count())

@@ -1,0 +1,662 @@
+// C-ABI implementation (include/h2b.h): host orchestration of the device
+// H^2 matrix.  The reference's call sequence (hmv.hpp:175-188) is kept phase
+// for phase; marshaling, pool management and OpenMP fork/joins are replaced
+// by the kernels in k_hmv.cu acting on HBM-resident pools.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "h2b_internal.hpp"
+
+namespace h2b {
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+h2b_status guarded(F&& f) {
+  try {
+    f();
+    return H2B_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return H2B_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return H2B_INTERNAL;
+  }
+}
+
+int usable_devices() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < n; ++d) {
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d);
+    if (major >= 10) ++ok;
+  }
+  return ok;
+}
+
+void need_device(int device) {
+  const int n = usable_devices();
+  if (n == 0) throw Error(H2B_NO_DEVICE, "no sm_100 CUDA device available (libh2b has no CPU fallback)");
+  require(device >= 0 && device < n, "device index out of range");
+  H2B_CUDA(cudaSetDevice(device));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    H2B_CUDA(cudaSetDevice(d));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+bool resolve_device(h2b_ptr_kind kind, const void* p) {
+  if (kind == H2B_PTR_DEVICE) return true;
+  if (kind == H2B_PTR_HOST) return false;
+  return p && is_device_ptr(p);
+}
+
+// Upload `count` column-major blocks of rows x cols stored densely
+// (stride rows*cols) into a padded device pool (ld = pad2(rows)).
+void upload_blocks(const double* h, double* d, int rows, int cols, int64_t count,
+                   cudaStream_t s) {
+  const int ld = pad2(rows);
+  const size_t packed = size_t(rows) * cols * count;
+  if (packed == 0) return;
+  if (ld == rows) {
+    H2B_CUDA(cudaMemcpyAsync(d, h, packed * sizeof(double), cudaMemcpyHostToDevice, s));
+    return;
+  }
+  DevBuf<double> tmp;
+  tmp.alloc(packed);
+  H2B_CUDA(cudaMemcpyAsync(tmp.p, h, packed * sizeof(double), cudaMemcpyHostToDevice, s));
+  launch_repack(tmp.p, int64_t(rows) * cols, rows, d, int64_t(ld) * cols, ld, rows, cols, count, s);
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+void download_blocks(const double* d, double* h, int rows, int cols, int64_t count,
+                     cudaStream_t s) {
+  const int ld = pad2(rows);
+  const size_t packed = size_t(rows) * cols * count;
+  if (packed == 0) return;
+  if (ld == rows) {
+    H2B_CUDA(cudaMemcpyAsync(h, d, packed * sizeof(double), cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  DevBuf<double> tmp;
+  tmp.alloc(packed);
+  launch_repack(d, int64_t(ld) * cols, ld, tmp.p, int64_t(rows) * cols, rows, rows, cols, count, s);
+  H2B_CUDA(cudaMemcpyAsync(h, tmp.p, packed * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+Matrix::~Matrix() {
+  if (h_stage) cudaFreeHost(h_stage);
+  for (auto& e : ev_pool)
+    if (e) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+uint64_t Matrix::footprint() const {
+  // memory_footprint(A) (h2_matrix.hpp:90-102): unpadded entries * 8 bytes.
+  uint64_t e = uint64_t(dense.nb) * dense.br * dense.bc + uint64_t(nodes(q)) * m * rank[q];
+  for (int l = 0; l <= q; ++l) e += uint64_t(cpl[l].nb) * cpl[l].br * cpl[l].bc;
+  for (int l = 1; l <= q; ++l) e += uint64_t(nodes(l)) * rank[l] * rank[l - 1];
+  return e * sizeof(double);
+}
+
+uint64_t Matrix::device_bytes() const {
+  return perm.bytes() + leaf.bytes() + transfer.bytes() + cpl_val.bytes() + dense_val.bytes() +
+         cpl_rp.bytes() + cpl_ci.bytes() + dense_rp.bytes() + dense_ci.bytes() + work.bytes() +
+         xc.bytes() + yc.bytes() + xhat.bytes() + yhat.bytes() + xs.bytes() + ys.bytes();
+}
+
+double Matrix::hmv_flops() const {
+  // flops.hpp:29-47 over the call sequence of hmv.hpp:175-188.
+  double f = 2.0 * dense.br * dense.bc * double(dense.nb);
+  f += 2.0 * m * rank[q] * double(nodes(q)) * 2;  // leaf gemv up + down
+  for (int l = 1; l <= q; ++l) f += 2.0 * rank[l] * rank[l - 1] * double(nodes(l)) * 2;
+  for (int l = 0; l <= q; ++l)
+    if (cpl[l].nb) f += 2.0 * cpl[l].br * cpl[l].bc * double(cpl[l].nb);
+  return f;
+}
+
+// Allocate pools and the workspace for the structure already set in A
+// (n, m, q, rank, layers' host CSR).  Values are left uninitialised.
+void allocate(Matrix& A) {
+  const int q = A.q;
+  A.ldm = pad2(A.m);
+  A.perm.alloc(A.n);
+  A.leaf.alloc(size_t(A.nodes(q)) * A.leaf_stride());
+  A.tr_off.assign(q + 2, 0);
+  int64_t t = 0;
+  for (int l = 1; l <= q; ++l) {
+    A.tr_off[l] = t;
+    t += A.nodes(l) * A.tr_stride(l);
+  }
+  A.tr_off[q + 1] = t;
+  A.transfer.alloc(t);
+  int64_t nv = 0, nrp = 0, nci = 0;
+  for (int l = 0; l <= q; ++l) {
+    Layer& L = A.cpl[l];
+    L.ld = pad2(L.br);
+    nv += L.nb * L.block_stride();
+    nrp += L.rows + 1;
+    nci += L.nb;
+  }
+  A.cpl_val.alloc(nv);
+  A.cpl_rp.alloc(nrp);
+  A.cpl_ci.alloc(nci);
+  nv = nrp = nci = 0;
+  for (int l = 0; l <= q; ++l) {
+    Layer& L = A.cpl[l];
+    L.val = A.cpl_val.p + nv;
+    L.rp = A.cpl_rp.p + nrp;
+    L.ci = A.cpl_ci.p + nci;
+    nv += L.nb * L.block_stride();
+    nrp += L.rows + 1;
+    nci += L.nb;
+  }
+  Layer& D = A.dense;
+  D.ld = pad2(D.br);
+  A.dense_val.alloc(size_t(D.nb) * D.block_stride());
+  A.dense_rp.alloc(D.rows + 1);
+  A.dense_ci.alloc(D.nb);
+  D.val = A.dense_val.p;
+  D.rp = A.dense_rp.p;
+  D.ci = A.dense_ci.p;
+
+  A.vec_off.assign(q + 2, 0);
+  for (int l = 0; l <= q; ++l) A.vec_off[l + 1] = A.vec_off[l] + A.nodes(l) * A.rank[l];
+  A.xc.alloc(A.n);
+  A.yc.alloc(A.n);
+  A.xhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
+  A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
+  A.xs.alloc(A.n);
+  A.ys.alloc(A.n);
+}
+
+// Upload the CSR structure of every layer and build the fused work list.
+void upload_structure(Matrix& A) {
+  cudaStream_t s = A.stream;
+  for (int l = 0; l <= A.q; ++l) {
+    Layer& L = A.cpl[l];
+    L.max_row = 0;
+    for (int64_t r = 0; r < L.rows; ++r) L.max_row = std::max(L.max_row, L.h_rp[r + 1] - L.h_rp[r]);
+    H2B_CUDA(cudaMemcpyAsync(L.rp, L.h_rp.data(), (L.rows + 1) * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, s));
+    if (L.nb)
+      H2B_CUDA(cudaMemcpyAsync(L.ci, L.h_ci.data(), L.nb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  }
+  Layer& D = A.dense;
+  D.max_row = 0;
+  for (int64_t r = 0; r < D.rows; ++r) D.max_row = std::max(D.max_row, D.h_rp[r + 1] - D.h_rp[r]);
+  H2B_CUDA(cudaMemcpyAsync(D.rp, D.h_rp.data(), (D.rows + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (D.nb) H2B_CUDA(cudaMemcpyAsync(D.ci, D.h_ci.data(), D.nb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  std::vector<const Layer*> layers;
+  for (int l = 0; l <= A.q; ++l) layers.push_back(&A.cpl[l]);
+  layers.push_back(&A.dense);
+  const std::vector<uint32_t> w = make_work_list(layers);
+  A.nwork = int64_t(w.size());
+  A.work.alloc(w.size());
+  if (!w.empty())
+    H2B_CUDA(cudaMemcpyAsync(A.work.p, w.data(), w.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+void check_shape(int n, int m, int depth, const int32_t* ranks) {
+  require(depth >= 0 && depth <= kMaxLevels - 1, "depth out of range");
+  require(m >= 1, "leaf size must be positive");
+  require(int64_t(m) << depth == n, "n must equal m * 2^depth");
+  if (m > kMaxDim) throw Error(H2B_UNSUPPORTED, "leaf size > 64 not supported by the compiled kernels");
+  for (int l = 0; l <= depth; ++l) {
+    require(ranks[l] >= 0, "ranks must be non-negative");
+    if (ranks[l] > kMaxDim) throw Error(H2B_UNSUPPORTED, "rank > 64 not supported by the compiled kernels");
+  }
+  require(int64_t(1) << (depth + 1) < (int64_t(1) << kLayerShift), "tree too deep for the work-list encoding");
+}
+
+void set_layer_structure(Layer& L, int64_t rows, int br, int bc, const int32_t* rp,
+                         const int32_t* ci) {
+  L.rows = rows;
+  L.br = br;
+  L.bc = bc;
+  L.h_rp.assign(rp, rp + rows + 1);
+  require(L.h_rp[0] == 0, "row_ptr must start at 0");
+  for (int64_t r = 0; r < rows; ++r) require(L.h_rp[r] <= L.h_rp[r + 1], "row_ptr must be non-decreasing");
+  L.nb = L.h_rp[rows];
+  L.h_ci.assign(ci, ci + L.nb);
+  for (int64_t r = 0; r < rows; ++r)
+    for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1]; ++b)
+      require(L.h_ci[b] >= 0 && L.h_ci[b] < rows, "col_idx out of range");
+}
+
+h2b_matrix* create_from_desc(const h2b_matrix_desc& d, int device) {
+  require(d.symmetric == 1, "only symmetric H2 matrices are supported (construct() is always symmetric)");
+  require(d.perm && d.ranks && d.leaf && d.cpl_row_ptr && d.dense_row_ptr, "null pointer in descriptor");
+  check_shape(d.n, d.m, d.depth, d.ranks);
+  need_device(device);
+  std::unique_ptr<h2b_matrix> A(new h2b_matrix);
+  A->device = device;
+  H2B_CUDA(cudaStreamCreateWithFlags(&A->stream, cudaStreamNonBlocking));
+  A->n = d.n;
+  A->m = d.m;
+  A->q = d.depth;
+  A->rank.assign(d.ranks, d.ranks + d.depth + 1);
+  const int q = A->q;
+  A->cpl.resize(q + 1);
+  const int32_t* rp = d.cpl_row_ptr;
+  const int32_t* ci = d.cpl_col_idx;
+  for (int l = 0; l <= q; ++l) {
+    set_layer_structure(A->cpl[l], A->nodes(l), A->rank[l], A->rank[l], rp, ci);
+    rp += A->nodes(l) + 1;
+    ci += A->cpl[l].nb;
+  }
+  set_layer_structure(A->dense, A->nodes(q), A->m, A->m, d.dense_row_ptr, d.dense_col_idx);
+  for (int t = 0; t < d.n; ++t) require(d.perm[t] >= 0 && d.perm[t] < d.n, "perm out of range");
+  allocate(*A);
+  cudaStream_t s = A->stream;
+  H2B_CUDA(cudaMemcpyAsync(A->perm.p, d.perm, size_t(d.n) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  upload_blocks(d.leaf, A->leaf.p, A->m, A->rank[q], A->nodes(q), s);
+  const double* tr = d.transfer;
+  for (int l = 1; l <= q; ++l) {
+    upload_blocks(tr, A->transfer.p + A->tr_off[l], A->rank[l], A->rank[l - 1], A->nodes(l), s);
+    tr += A->nodes(l) * A->rank[l] * A->rank[l - 1];
+  }
+  const double* sv = d.cpl_values;
+  for (int l = 0; l <= q; ++l) {
+    const Layer& L = A->cpl[l];
+    upload_blocks(sv, L.val, L.br, L.bc, L.nb, s);
+    sv += L.nb * L.br * L.bc;
+  }
+  upload_blocks(d.dense_values, A->dense.val, A->m, A->m, A->dense.nb, s);
+  upload_structure(*A);
+  return A.release();
+}
+
+// ---------------------------------------------------------------- HMV driver
+cudaEvent_t* timing_slots(Matrix& A) {
+  if (!A.timing) return nullptr;
+  if (A.ev_used + 4 > A.ev_pool.size()) {
+    const size_t old = A.ev_pool.size();
+    A.ev_pool.resize(std::max<size_t>(64, 2 * old));
+    for (size_t i = old; i < A.ev_pool.size(); ++i) H2B_CUDA(cudaEventCreate(&A.ev_pool[i]));
+  }
+  cudaEvent_t* e = A.ev_pool.data() + A.ev_used;
+  A.ev_used += 4;
+  return e;
+}
+
+void hmv_device(Matrix& A, const double* x, double* y, double alpha, double beta, cudaStream_t s) {
+  const int q = A.q;
+  cudaEvent_t* ev = timing_slots(A);
+  if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
+  launch_up_leaf(A, x, s);
+  for (int l = q; l >= 1; --l) launch_up_level(A, l, s);
+  if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
+  launch_bsr(A, A.work.p, A.nwork, A.xc.p, A.yc.p, A.xhat.p, A.yhat.p, s);
+  if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
+  for (int l = 1; l <= q; ++l) launch_down_level(A, l, s);
+  launch_down_leaf(A, y, alpha, beta, true, s);
+  if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
+}
+
+void ensure_host_stage(Matrix& A, size_t n) {
+  if (A.h_stage_n >= n) return;
+  if (A.h_stage) cudaFreeHost(A.h_stage);
+  A.h_stage = nullptr;
+  A.h_stage_n = 0;
+  H2B_CUDA(cudaMallocHost(&A.h_stage, n * sizeof(double)));
+  A.h_stage_n = n;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+void copy_in(Matrix& A, double* dst, const double* src, size_t n, cudaStream_t s) {
+  H2B_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, s));
+}
+
+void copy_out(Matrix& A, double* dst, const double* src, size_t n, cudaStream_t s) {
+  H2B_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+}
+
+void hmv(Matrix& A, const double* x, double* y, double alpha, double beta, h2b_ptr_kind kind,
+         cudaStream_t s) {
+  require(x && y, "hmv: null vector");
+  DeviceGuard g(A.device);
+  if (!s) s = A.stream;
+  const bool dx = resolve_device(kind, x), dy = resolve_device(kind, y);
+  const double* xd = x;
+  double* yd = y;
+  if (!dx) {
+    copy_in(A, A.xs.p, x, A.n, s);
+    xd = A.xs.p;
+  }
+  if (!dy) {
+    if (beta != 0.0) copy_in(A, A.ys.p, y, A.n, s);
+    yd = A.ys.p;
+  }
+  hmv_device(A, xd, yd, alpha, beta, s);
+  if (!dy) copy_out(A, y, A.ys.p, A.n, s);
+  if (!dx || !dy) H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+// Phase helpers take host or device pointers; host data goes through
+// temporary device buffers.
+struct Staged {
+  DevBuf<double> buf;
+  double* d = nullptr;
+  double* host = nullptr;
+  size_t n = 0;
+};
+
+const double* stage_in(Staged& st, const double* p, size_t n, bool dev, cudaStream_t s) {
+  if (dev) return p;
+  st.buf.alloc(std::max<size_t>(n, 1));
+  if (n) H2B_CUDA(cudaMemcpyAsync(st.buf.p, p, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  return st.buf.p;
+}
+
+double* stage_out(Staged& st, double* p, size_t n, bool dev, bool copy_existing, cudaStream_t s) {
+  if (dev) return p;
+  st.buf.alloc(std::max<size_t>(n, 1));
+  st.host = p;
+  st.n = n;
+  if (copy_existing && n)
+    H2B_CUDA(cudaMemcpyAsync(st.buf.p, p, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  return st.buf.p;
+}
+
+void finish_out(Staged& st, cudaStream_t s) {
+  if (st.host && st.n)
+    H2B_CUDA(cudaMemcpyAsync(st.host, st.buf.p, st.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace h2b
+
+using namespace h2b;
+
+// Implemented in build.cu / compress.cu.
+namespace h2b {
+h2b_matrix* build_matrix(const h2b_build_config& cfg, int device);
+void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep);
+void orthogonalize_matrix(Matrix& A, double* t_out);
+}  // namespace h2b
+
+extern "C" {
+
+const char* h2b_last_error(void) { return g_err.c_str(); }
+const char* h2b_version(void) { return "h2b 0.1 (sm_100a, fp64)"; }
+int h2b_device_count(void) { return usable_devices(); }
+
+h2b_status h2b_matrix_create(const h2b_matrix_desc* desc, int device, h2b_matrix** out) {
+  return guarded([&] {
+    require(desc && out, "null argument");
+    *out = create_from_desc(*desc, device);
+  });
+}
+
+h2b_status h2b_matrix_build(const h2b_build_config* cfg, int device, h2b_matrix** out) {
+  return guarded([&] {
+    require(cfg && out, "null argument");
+    *out = build_matrix(*cfg, device);
+  });
+}
+
+h2b_status h2b_matrix_destroy(h2b_matrix* A) {
+  return guarded([&] {
+    if (!A) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(A->device);
+    delete A;
+    cudaSetDevice(prev);
+  });
+}
+
+h2b_status h2b_matrix_info_get(const h2b_matrix* Ah, h2b_matrix_info* info) {
+  return guarded([&] {
+    require(Ah && info, "null argument");
+    const Matrix& A = *Ah;
+    std::memset(info, 0, sizeof(*info));
+    info->n = A.n;
+    info->m = A.m;
+    info->depth = A.q;
+    info->symmetric = 1;
+    for (int l = 0; l <= A.q; ++l) {
+      info->ranks[l] = A.rank[l];
+      info->cpl_blocks[l] = A.cpl[l].nb;
+      info->cpl_max_row[l] = A.cpl[l].max_row;
+    }
+    info->dense_blocks = A.dense.nb;
+    info->dense_max_row = A.dense.max_row;
+    info->footprint_bytes = A.footprint();
+    info->device_bytes = A.device_bytes();
+    info->hmv_flops = A.hmv_flops();
+  });
+}
+
+uint64_t h2b_matrix_footprint(const h2b_matrix* A) {
+  return A ? reinterpret_cast<const Matrix*>(A)->footprint() : 0;
+}
+
+h2b_status h2b_matrix_export(const h2b_matrix* Ah, int32_t* perm, double* leaf, double* transfer,
+                             int32_t* cpl_row_ptr, int32_t* cpl_col_idx, double* cpl_values,
+                             int32_t* dense_row_ptr, int32_t* dense_col_idx,
+                             double* dense_values) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    const Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    cudaStream_t s = A.stream;
+    const int q = A.q;
+    if (perm) {
+      H2B_CUDA(cudaMemcpyAsync(perm, A.perm.p, size_t(A.n) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      H2B_CUDA(cudaStreamSynchronize(s));
+    }
+    if (leaf) download_blocks(A.leaf.p, leaf, A.m, A.rank[q], A.nodes(q), s);
+    if (transfer)
+      for (int l = 1; l <= q; ++l) {
+        download_blocks(A.transfer.p + A.tr_off[l], transfer, A.rank[l], A.rank[l - 1], A.nodes(l), s);
+        transfer += A.nodes(l) * A.rank[l] * A.rank[l - 1];
+      }
+    for (int l = 0; l <= q; ++l) {
+      const Layer& L = A.cpl[l];
+      if (cpl_row_ptr) cpl_row_ptr = std::copy(L.h_rp.begin(), L.h_rp.end(), cpl_row_ptr);
+      if (cpl_col_idx) cpl_col_idx = std::copy(L.h_ci.begin(), L.h_ci.end(), cpl_col_idx);
+      if (cpl_values) {
+        download_blocks(L.val, cpl_values, L.br, L.bc, L.nb, s);
+        cpl_values += L.nb * L.br * L.bc;
+      }
+    }
+    if (dense_row_ptr) std::copy(A.dense.h_rp.begin(), A.dense.h_rp.end(), dense_row_ptr);
+    if (dense_col_idx) std::copy(A.dense.h_ci.begin(), A.dense.h_ci.end(), dense_col_idx);
+    if (dense_values) download_blocks(A.dense.val, dense_values, A.m, A.m, A.dense.nb, s);
+  });
+}
+
+h2b_status h2b_hmv(h2b_matrix* Ah, const double* x, double* y, double alpha, double beta,
+                   h2b_ptr_kind kind, void* stream) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    hmv(*Ah, x, y, alpha, beta, kind, static_cast<cudaStream_t>(stream));
+  });
+}
+
+h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx, double* Y,
+                         int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    Matrix& A = *Ah;
+    require(nvec >= 0 && ldx >= A.n && ldy >= A.n, "hmv_multi: bad leading dimension");
+    for (int v = 0; v < nvec; ++v)
+      hmv(A, X + v * ldx, Y + v * ldy, alpha, beta, kind, static_cast<cudaStream_t>(stream));
+  });
+}
+
+h2b_status h2b_upsweep(h2b_matrix* Ah, const double* xc, double* xhat, h2b_ptr_kind kind) {
+  return guarded([&] {
+    require(Ah && xc && xhat, "null argument");
+    Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    cudaStream_t s = A.stream;
+    const bool dev = resolve_device(kind, xc);
+    Staged si, so;
+    const double* xin = stage_in(si, xc, A.n, dev, s);
+    launch_up_leaf(A, xin, s, /*cluster_order=*/true);
+    for (int l = A.q; l >= 1; --l) launch_up_level(A, l, s);
+    double* out = stage_out(so, xhat, A.vec_off[A.q + 1], resolve_device(kind, xhat), false, s);
+    if (A.vec_off[A.q + 1])
+      H2B_CUDA(cudaMemcpyAsync(out, A.xhat.p, A.vec_off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    finish_out(so, s);
+  });
+}
+
+h2b_status h2b_tree_multiply(h2b_matrix* Ah, const double* xhat, double* yhat, h2b_ptr_kind kind) {
+  return guarded([&] {
+    require(Ah && xhat && yhat, "null argument");
+    Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    cudaStream_t s = A.stream;
+    const size_t nv = A.vec_off[A.q + 1];
+    Staged si, so;
+    const double* xin = stage_in(si, xhat, nv, resolve_device(kind, xhat), s);
+    double* out = stage_out(so, yhat, nv, resolve_device(kind, yhat), false, s);
+    // coupling layers only: work items with layer index <= q
+    std::vector<const Layer*> layers;
+    for (int l = 0; l <= A.q; ++l) layers.push_back(&A.cpl[l]);
+    const auto w = make_work_list(layers);
+    DevBuf<uint32_t> dw;
+    dw.alloc(w.size());
+    if (!w.empty())
+      H2B_CUDA(cudaMemcpyAsync(dw.p, w.data(), w.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    launch_bsr(A, dw.p, int64_t(w.size()), nullptr, nullptr, xin, out, s);
+    finish_out(so, s);
+  });
+}
+
+h2b_status h2b_downsweep(h2b_matrix* Ah, const double* yhat, double* yc, h2b_ptr_kind kind) {
+  return guarded([&] {
+    require(Ah && yhat && yc, "null argument");
+    Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    cudaStream_t s = A.stream;
+    const size_t nv = A.vec_off[A.q + 1];
+    Staged si, so;
+    const double* yin = stage_in(si, yhat, nv, resolve_device(kind, yhat), s);
+    if (nv) H2B_CUDA(cudaMemcpyAsync(A.yhat.p, yin, nv * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double* out = stage_out(so, yc, A.n, resolve_device(kind, yc), true, s);
+    H2B_CUDA(cudaMemcpyAsync(A.yc.p, out, A.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    for (int l = 1; l <= A.q; ++l) launch_down_level(A, l, s);
+    launch_down_leaf(A, out, 1.0, 0.0, false, s);
+    finish_out(so, s);
+  });
+}
+
+h2b_status h2b_dense_mv(h2b_matrix* Ah, const double* xc, double* yc, double alpha, double beta,
+                        h2b_ptr_kind kind) {
+  return guarded([&] {
+    require(Ah && xc && yc, "null argument");
+    Matrix& A = *Ah;
+    require(alpha == 1.0 && beta == 0.0, "h2b_dense_mv: only alpha = 1, beta = 0 (the hmv call site) is implemented");
+    DeviceGuard g(A.device);
+    cudaStream_t s = A.stream;
+    Staged si, so;
+    const double* xin = stage_in(si, xc, A.n, resolve_device(kind, xc), s);
+    double* out = stage_out(so, yc, A.n, resolve_device(kind, yc), false, s);
+    std::vector<const Layer*> layers(A.q + 1, nullptr);
+    layers.push_back(&A.dense);
+    const auto w = make_work_list(layers);
+    DevBuf<uint32_t> dw;
+    dw.alloc(w.size());
+    if (!w.empty())
+      H2B_CUDA(cudaMemcpyAsync(dw.p, w.data(), w.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    launch_bsr(A, dw.p, int64_t(w.size()), xin, out, A.xhat.p, A.yhat.p, s);
+    finish_out(so, s);
+  });
+}
+
+h2b_status h2b_compress(h2b_matrix* Ah, double eps, h2b_compress_report* report) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    compress_matrix(*Ah, eps, report);
+  });
+}
+
+h2b_status h2b_orthogonalize(h2b_matrix* Ah, double* t_out) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    orthogonalize_matrix(*Ah, t_out);
+  });
+}
+
+h2b_status h2b_last_hmv_timing(h2b_matrix* Ah, double* ms4) {
+  return guarded([&] {
+    require(Ah && ms4, "null argument");
+    Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    for (int i = 0; i < 4; ++i) ms4[i] = 0.0;
+    const size_t calls = A.ev_used / 4;
+    for (size_t c = 0; c < calls; ++c) {
+      cudaEvent_t* e = A.ev_pool.data() + 4 * c;
+      H2B_CUDA(cudaEventSynchronize(e[3]));
+      for (int i = 0; i < 3; ++i) {
+        float t = 0;
+        H2B_CUDA(cudaEventElapsedTime(&t, e[i], e[i + 1]));
+        ms4[i] += t;
+        ms4[3] += t;
+      }
+    }
+    if (calls)
+      for (int i = 0; i < 4; ++i) ms4[i] /= double(calls);
+    A.ev_used = 0;
+  });
+}
+
+h2b_status h2b_set_phase_timing(h2b_matrix* Ah, int on) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    Matrix& A = *Ah;
+    A.timing = on != 0;
+    A.ev_used = 0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+// Internal types of libh2b.so: the HBM-resident H^2 matrix and its workspace.
+//
+// Device layout.  Everything the reference keeps in
+// std::vector pools (BasisTree::leaf_pool / transfer[l], BSRLayer::values,
+// LevelVectors::pool[l]; include/h2kit/h2_matrix.hpp:17-80, hmv.hpp:13-22)
+// lives in a few large cudaMalloc'd pools:
+//   * every matrix block is column-major with an EVEN leading dimension
+//     ld = pad2(rows) (a zero row is appended when rows is odd), so every
+//     column starts 16-byte aligned and the kernels can use 128-bit loads;
+//   * block strides are ld * cols doubles, 64-bit offsets throughout;
+//   * node vectors x^ / y^ are unpadded, level-concatenated (vec_off[l]).
+// Marshaling (hmv.hpp:33-74, compression.hpp:47-64,185-209) is replaced by
+// closed-form complete-binary-tree index arithmetic inside the kernels:
+// children of level-local node i are 2i, 2i+1; the parent is i >> 1.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "h2b.h"
+
+namespace h2b {
+
+struct Error : std::runtime_error {
+  h2b_status code;
+  Error(h2b_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// The reference's require() (include/h2kit/defs.hpp:20-22).
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(H2B_INVALID_ARGUMENT, msg);
+}
+
+#define H2B_CUDA(expr)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      throw ::h2b::Error(e_ == cudaErrorMemoryAllocation ? H2B_OUT_OF_MEMORY        \
+                                                         : H2B_CUDA_ERROR,          \
+                         std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+inline int pad2(int r) { return r + (r & 1); }
+
+// Largest block dimension the compiled warp kernels cover (rows owned by a
+// lane pair: 2 * 32 lanes).
+constexpr int kMaxDim = 64;
+constexpr int kMaxLevels = 31;
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t cnt) {
+    release();
+    if (cnt == 0) return;
+    H2B_CUDA(cudaMalloc(&p, cnt * sizeof(T)));
+    n = cnt;
+  }
+  void zero(cudaStream_t s) {
+    if (n) H2B_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// One uniform-block BSR layer (a coupling level or the dense layer),
+// bsr.hpp:13-31.  row_ptr/col_idx are level-local like the reference.
+struct Layer {
+  int br = 0, bc = 0, ld = 0;     // block dims, padded leading dim
+  int64_t rows = 0, nb = 0;
+  int max_row = 0;
+  std::vector<int32_t> h_rp, h_ci;  // host copy of the structure
+  int32_t* rp = nullptr;            // device (views into Matrix pools)
+  int32_t* ci = nullptr;
+  double* val = nullptr;
+  int64_t block_stride() const { return int64_t(ld) * bc; }
+};
+
+// Work item of the fused BSR kernel: (layer << 26) | block_row.
+constexpr int kLayerShift = 26;
+
+struct Matrix {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int n = 0, m = 0, q = 0, ldm = 0;
+  std::vector<int> rank;            // per level (row basis == column basis)
+
+  DevBuf<int32_t> perm;
+  DevBuf<double> leaf;              // 2^q blocks, ldm x rank[q]
+  DevBuf<double> transfer;          // level-concatenated, block ld = pad2(rank[l])
+  std::vector<int64_t> tr_off;      // [l] offset into transfer (l >= 1)
+
+  std::vector<Layer> cpl;           // q + 1 coupling levels
+  Layer dense;
+  DevBuf<double> cpl_val, dense_val;
+  DevBuf<int32_t> cpl_rp, cpl_ci, dense_rp, dense_ci;
+
+  std::vector<int64_t> vec_off;     // node-vector level offsets, size q + 2
+  DevBuf<uint32_t> work;            // BSR work list (dense + coupling rows)
+  int64_t nwork = 0;
+
+  // HmvContext analogue (hmv.hpp:161-172): one workspace per handle.
+  DevBuf<double> xc, yc, xhat, yhat, xs, ys;
+  double* h_stage = nullptr;        // pinned host staging for host-pointer calls
+  size_t h_stage_n = 0;
+
+  // Per-phase CUDA-event timing (h2b_set_phase_timing): four events per
+  // hmv call, recorded on the launching stream without host syncs; read and
+  // reset by h2b_last_hmv_timing.
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+
+  ~Matrix();
+  int64_t nodes(int l) const { return int64_t(1) << l; }
+  int ld(int l) const { return pad2(rank[l]); }
+  int64_t leaf_stride() const { return int64_t(ldm) * rank[q]; }
+  int64_t tr_stride(int l) const { return int64_t(ld(l)) * rank[l - 1]; }
+  uint64_t footprint() const;       // reference byte convention
+  uint64_t device_bytes() const;
+  double hmv_flops() const;         // reference analytic model
+};
+
+// ---- launchers (k_hmv.cu) ----
+void launch_up_leaf(const Matrix& A, const double* x, cudaStream_t s, bool cluster_order = false);
+void launch_up_level(const Matrix& A, int l, cudaStream_t s);
+void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
+                double* ydense, const double* xh, double* yh, cudaStream_t s);
+void launch_down_level(const Matrix& A, int l, cudaStream_t s);
+void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
+                      cudaStream_t s);
+void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s);
+
+// Build the fused BSR work list for the given layers (rows sorted by
+// decreasing block count so the round-robin warp assignment is balanced).
+std::vector<uint32_t> make_work_list(const std::vector<const Layer*>& layers);
+
+// ---- padded <-> packed block copies (k_hmv.cu) ----
+// dst (ld_dst x cols, stride sd) <- src (ld_src x cols, stride ss), rows valid.
+void launch_repack(const double* src, int64_t ss, int ld_src, double* dst, int64_t sd, int ld_dst,
+                   int rows, int cols, int64_t count, cudaStream_t s);
+
+}  // namespace h2b
+
+// The opaque handle of include/h2b.h is the device matrix itself.
+struct h2b_matrix : h2b::Matrix {};

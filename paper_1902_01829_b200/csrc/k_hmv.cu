@@ -1,0 +1,475 @@
+// HMV kernels for sm_100a (FP64).  One warp owns one small matrix at a time;
+// lane L owns the row pair (2L, 2L+1) of every block it touches, so a column
+// of a 64-row block is one fully coalesced 512-byte warp load (32 x 128-bit).
+//
+// Phase map (reference include/h2kit/hmv.hpp, Appendix B of SURVEY.md):
+//   k_up_leaf    : xc = x[perm] (hmv.hpp:179) fused with x^q = V^T xc (hmv.hpp:86-97)
+//   k_up_level   : x^{l-1}_p = F_2p^T x^l_2p + F_2p+1^T x^l_2p+1 (hmv.hpp:98-110)
+//   k_bsr        : yc = D xc (hmv.hpp:180) and y^l = S^l x^l for every level
+//                  (hmv.hpp:114-125) in ONE launch over a flattened row list
+//   k_down_level : y^l_c += E_c y^{l-1}_{c/2} (hmv.hpp:136-146)
+//   k_down_leaf  : yc += U y^q (hmv.hpp:147-156) fused with the alpha/beta
+//                  scatter y[perm[t]] = alpha yc[t] + beta y[perm[t]] (hmv.hpp:184-187)
+// All matrix bytes are read exactly once per phase with streaming
+// (evict-first) 128-bit loads; node vectors stay L2-resident.
+#include "h2b_internal.hpp"
+
+#include <algorithm>
+#include <numeric>
+
+namespace h2b {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 256;  // 8 warps per CTA
+
+__device__ __forceinline__ double2 ld_stream(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int64_t warp_global() {
+  return (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+}
+__device__ __forceinline__ int64_t warp_count() {
+  return (int64_t(gridDim.x) * blockDim.x) >> 5;
+}
+
+// Butterfly reduce-scatter: lane L returns sum over all lanes of p[L].
+// 31 double shuffles for 32 independent dot products.
+__device__ __forceinline__ double reduce_scatter32(double (&p)[32]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = up ? p[i] : p[i + s];
+      const double keep = up ? p[i + s] : p[i];
+      p[i] = keep + __shfl_xor_sync(kFull, send, s);
+    }
+  }
+  return p[0];
+}
+
+// Transposed product for the column group g in {0,1}:
+//   returns out[2*lane + g] = sum_r A[r, 2*lane+g] * v[r]  (+ B^T w when TWO)
+// A, B: column-major, leading dim ld (even), `cols` columns; the lane's row
+// pair (2*lane, 2*lane+1) is valid when row_ok.
+template <bool TWO>
+__device__ __forceinline__ double gemvT_group(const double* __restrict__ A,
+                                              const double* __restrict__ B, int ld, int cols,
+                                              int g, double v0, double v1, double w0, double w1,
+                                              bool row_ok) {
+  const int lane = lane_id();
+  const int r = 2 * lane;
+  // Streaming reduce-scatter: each chunk of 8 columns is reduced over lane
+  // bits 0..2 right away (7 shuffles), leaving one value per chunk; the 4
+  // chunk values are then reduced over lane bits 3..4 (3 shuffles).  Lane L
+  // ends with column index L of the group; 31 shuffles per 32 columns, and
+  // only one chunk of loads is live at a time.
+  double hv[4] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t step = 2 * int64_t(ld);
+  const double* pa = A + int64_t(g) * ld + r;
+  const double* pb = TWO ? B + int64_t(g) * ld + r : nullptr;
+#pragma unroll 1
+  for (int h = 0; h < 4; ++h) {
+    double p[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int c = 2 * (8 * h + t) + g;
+      const bool ok = c < cols && row_ok;
+      const double2 a = ok ? ld_stream(pa) : make_double2(0.0, 0.0);
+      pa += step;
+      double acc = a.x * v0 + a.y * v1;
+      if (TWO) {
+        const double2 b = ok ? ld_stream(pb) : make_double2(0.0, 0.0);
+        pb += step;
+        acc += b.x * w0 + b.y * w1;
+      }
+      p[t] = acc;
+    }
+#pragma unroll
+    for (int s = 1, n = 8; s <= 4; s <<= 1, n >>= 1) {
+      const bool up = (lane & s) != 0;
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        const double keep = up ? p[2 * i + 1] : p[2 * i];
+        const double send = up ? p[2 * i] : p[2 * i + 1];
+        p[i] = keep + __shfl_xor_sync(kFull, send, s);
+      }
+    }
+    hv[0] = h == 0 ? p[0] : hv[0];
+    hv[1] = h == 1 ? p[0] : hv[1];
+    hv[2] = h == 2 ? p[0] : hv[2];
+    hv[3] = h == 3 ? p[0] : hv[3];
+    if (2 * (8 * h + 8) + g >= cols) break;  // remaining chunks are all padding
+  }
+#pragma unroll
+  for (int s = 8, n = 4; s <= 16; s <<= 1, n >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const double keep = up ? hv[2 * i + 1] : hv[2 * i];
+      const double send = up ? hv[2 * i] : hv[2 * i + 1];
+      hv[i] = keep + __shfl_xor_sync(kFull, send, s);
+    }
+  }
+  return hv[0];
+}
+
+// Non-transposed product: returns (acc0, acc1) for rows (2*lane, 2*lane+1)
+// of A (ld x cols) times v, where v is held in pair layout (lane L has
+// v[2L], v[2L+1]) and broadcast with shuffles.
+__device__ __forceinline__ void gemvN_pair(const double* __restrict__ A, int ld, int cols,
+                                           double a0, double a1, bool row_ok, double& acc0,
+                                           double& acc1) {
+  const int r = 2 * lane_id();
+  acc0 = 0.0;
+  acc1 = 0.0;
+  for (int c0 = 0; c0 < cols; c0 += 8) {
+    double2 col[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u;
+      col[u] = (c < cols && row_ok) ? ld_stream(A + int64_t(c) * ld + r) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u;  // warp-uniform
+      if (c < cols) {
+        const double s = __shfl_sync(kFull, (c & 1) ? a1 : a0, c >> 1);
+        acc0 += col[u].x * s;
+        acc1 += col[u].y * s;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_up_leaf(const double* __restrict__ x,
+                                                      const int32_t* __restrict__ perm,
+                                                      const double* __restrict__ leaf, int m,
+                                                      int ldm, int k, int64_t nleaves,
+                                                      double* __restrict__ xc,
+                                                      double* __restrict__ xh) {
+  const int r = 2 * lane_id();
+  const int64_t stride = int64_t(ldm) * k;
+  for (int64_t i = warp_global(); i < nleaves; i += warp_count()) {
+    const int64_t base = i * m;
+    double v0 = 0.0, v1 = 0.0;
+    // perm == nullptr: x is already in cluster order (phase API).
+    if (r < m) {
+      v0 = __ldg(x + (perm ? __ldg(perm + base + r) : base + r));
+      xc[base + r] = v0;
+    }
+    if (r + 1 < m) {
+      v1 = __ldg(x + (perm ? __ldg(perm + base + r + 1) : base + r + 1));
+      xc[base + r + 1] = v1;
+    }
+    if (k == 0) continue;
+    const double* V = leaf + i * stride;
+    const double o0 = gemvT_group<false>(V, nullptr, ldm, k, 0, v0, v1, 0, 0, r < ldm);
+    const double o1 = gemvT_group<false>(V, nullptr, ldm, k, 1, v0, v1, 0, 0, r < ldm);
+    if (r < k) xh[i * k + r] = o0;
+    if (r + 1 < k) xh[i * k + r + 1] = o1;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_up_level(const double* __restrict__ F, int ldc,
+                                                       int kc, int kp, int64_t nparents,
+                                                       const double* __restrict__ xl,
+                                                       double* __restrict__ xp) {
+  const int r = 2 * lane_id();
+  const int64_t stride = int64_t(ldc) * kp;
+  for (int64_t p = warp_global(); p < nparents; p += warp_count()) {
+    const double* x0 = xl + (2 * p) * kc;
+    const double* x1 = x0 + kc;
+    const double v0 = r < kc ? x0[r] : 0.0, v1 = r + 1 < kc ? x0[r + 1] : 0.0;
+    const double w0 = r < kc ? x1[r] : 0.0, w1 = r + 1 < kc ? x1[r + 1] : 0.0;
+    const double* A = F + (2 * p) * stride;
+    const double o0 = gemvT_group<true>(A, A + stride, ldc, kp, 0, v0, v1, w0, w1, r < ldc);
+    const double o1 = gemvT_group<true>(A, A + stride, ldc, kp, 1, v0, v1, w0, w1, r < ldc);
+    if (r < kp) xp[p * kp + r] = o0;
+    if (r + 1 < kp) xp[p * kp + r + 1] = o1;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_down_level(const double* __restrict__ E, int ldc,
+                                                         int kc, int kp, int64_t nchildren,
+                                                         const double* __restrict__ yp_all,
+                                                         double* __restrict__ yl) {
+  const int r = 2 * lane_id();
+  const int64_t stride = int64_t(ldc) * kp;
+  for (int64_t c = warp_global(); c < nchildren; c += warp_count()) {
+    const double* yp = yp_all + (c >> 1) * kp;
+    const double a0 = r < kp ? yp[r] : 0.0, a1 = r + 1 < kp ? yp[r + 1] : 0.0;
+    double acc0, acc1;
+    gemvN_pair(E + c * stride, ldc, kp, a0, a1, r < ldc, acc0, acc1);
+    double* y = yl + c * kc;
+    if (r < kc) y[r] = acc0 + y[r];
+    if (r + 1 < kc) y[r + 1] = acc1 + y[r + 1];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_down_leaf(
+    const double* __restrict__ U, int ldm, int m, int k, int64_t nleaves,
+    const double* __restrict__ yh, const double* __restrict__ yc,
+    const int32_t* __restrict__ perm, double* __restrict__ y, double alpha, double beta,
+    int to_user) {
+  const int r = 2 * lane_id();
+  const int64_t stride = int64_t(ldm) * k;
+  for (int64_t i = warp_global(); i < nleaves; i += warp_count()) {
+    const double* yq = yh + i * k;
+    const double a0 = r < k ? yq[r] : 0.0, a1 = r + 1 < k ? yq[r + 1] : 0.0;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (k > 0) gemvN_pair(U + i * stride, ldm, k, a0, a1, r < ldm, acc0, acc1);
+    const int64_t base = i * m;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rr = r + h;
+      if (rr >= m) continue;
+      const double v = (h ? acc1 : acc0) + yc[base + rr];
+      if (to_user) {
+        const int64_t o = perm[base + rr];
+        y[o] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[o]);
+      } else {
+        y[base + rr] = v;  // phase API: cluster-order yc += U y^
+      }
+    }
+  }
+}
+
+struct LayerDesc {
+  const double* val;
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* x;
+  double* y;
+  int64_t stride;
+  int br, bc, ld, pad;
+};
+struct LayerTable {
+  LayerDesc L[kMaxLevels + 2];
+};
+
+// Fused block-sparse multiply over every (layer, block row) work item:
+// y_r = sum_b B_b x_{col(b)} in col_idx order (bsr.hpp:50-73, beta = 0).
+// A row of ld/2 lanes covers one block column; small blocks put
+// G = 32 / (ld/2) column groups side by side and reduce them at the end.
+__global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerTable T,
+                                                  const uint32_t* __restrict__ work,
+                                                  int64_t nwork) {
+  const int lane = lane_id();
+  for (int64_t it = warp_global(); it < nwork; it += warp_count()) {
+    const uint32_t u = __ldg(work + it);
+    const LayerDesc& D = T.L[u >> kLayerShift];
+    const int row = int(u & ((1u << kLayerShift) - 1));
+    const int lpc = D.ld >> 1;
+    const int G = 32 / lpc;
+    const int grp = lane / lpc;
+    const int pr = lane - grp * lpc;
+    const bool act = grp < G;
+    const int r = 2 * pr;
+    int b = __ldg(D.rp + row);
+    const int b1 = __ldg(D.rp + row + 1);
+    double y0 = 0.0, y1 = 0.0;
+    int col = b < b1 ? __ldg(D.ci + b) : 0;
+    for (; b < b1; ++b) {
+      const double* xs = D.x + int64_t(col) * D.bc;
+      const double xr0 = lane < D.bc ? __ldg(xs + lane) : 0.0;
+      const double xr1 = lane + 32 < D.bc ? __ldg(xs + lane + 32) : 0.0;
+      col = b + 1 < b1 ? __ldg(D.ci + b + 1) : 0;
+      const double* blk = D.val + int64_t(b) * D.stride + r;
+      for (int j0 = 0; j0 < D.bc; j0 += 8 * G) {
+        double2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = j0 + q * G + grp;
+          v[q] = (act && j < D.bc) ? ld_stream(blk + int64_t(j) * D.ld) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = j0 + q * G + grp;
+          // bc > 32 implies G == 1, so j (and the xr0/xr1 choice) is warp-uniform.
+          const double xj = __shfl_sync(kFull, j < 32 ? xr0 : xr1, j & 31);
+          if (j < D.bc) {
+            y0 += v[q].x * xj;
+            y1 += v[q].y * xj;
+          }
+        }
+      }
+    }
+    if (G > 1) {
+      double t0 = y0, t1 = y1;
+      for (int g = 1; g < G; ++g) {
+        t0 += __shfl_down_sync(kFull, y0, g * lpc);
+        t1 += __shfl_down_sync(kFull, y1, g * lpc);
+      }
+      y0 = t0;
+      y1 = t1;
+    }
+    if (act && grp == 0) {
+      double* yr = D.y + int64_t(row) * D.br;
+      if (r < D.br) yr[r] = y0;
+      if (r + 1 < D.br) yr[r + 1] = y1;
+    }
+  }
+}
+
+__global__ void k_gather(const int32_t* __restrict__ perm, const double* __restrict__ x,
+                         double* __restrict__ xc, int64_t n) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n;
+       t += int64_t(gridDim.x) * blockDim.x)
+    xc[t] = x[perm[t]];
+}
+
+__global__ void k_repack(const double* __restrict__ src, int64_t ss, int ld_src,
+                         double* __restrict__ dst, int64_t sd, int ld_dst, int rows, int cols,
+                         int64_t count) {
+  const int64_t per = int64_t(ld_dst) * cols;
+  const int64_t total = per * count;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = e / per;
+    const int64_t w = e - b * per;
+    const int j = int(w / ld_dst);
+    const int i = int(w - int64_t(j) * ld_dst);
+    dst[b * sd + int64_t(j) * ld_dst + i] = i < rows ? src[b * ss + int64_t(j) * ld_src + i] : 0.0;
+  }
+}
+
+int sm_count() {
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return sms;
+}
+
+// Grid for a grid-stride warp loop over `items` warps of work: at most 8
+// resident 256-thread CTAs per SM.
+unsigned warp_grid(int64_t items) {
+  const int64_t want = (items + 7) / 8;
+  const int64_t cap = int64_t(sm_count()) * 8;
+  return unsigned(std::max<int64_t>(1, std::min(want, cap)));
+}
+
+unsigned flat_grid(int64_t n) {
+  const int64_t want = (n + kThreads - 1) / kThreads;
+  const int64_t cap = int64_t(sm_count()) * 16;
+  return unsigned(std::max<int64_t>(1, std::min(want, cap)));
+}
+
+}  // namespace
+
+void launch_up_leaf(const Matrix& A, const double* x, cudaStream_t s, bool cluster_order) {
+  const int64_t nl = A.nodes(A.q);
+  k_up_leaf<<<warp_grid(nl), kThreads, 0, s>>>(x, cluster_order ? nullptr : A.perm.p, A.leaf.p, A.m, A.ldm, A.rank[A.q], nl,
+                                               A.xc.p, A.xhat.p + A.vec_off[A.q]);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_up_level(const Matrix& A, int l, cudaStream_t s) {
+  const int kc = A.rank[l], kp = A.rank[l - 1];
+  double* xp = A.xhat.p + A.vec_off[l - 1];
+  const int64_t np = A.nodes(l - 1);
+  if (kp == 0) return;
+  if (kc == 0) {
+    H2B_CUDA(cudaMemsetAsync(xp, 0, size_t(np) * kp * sizeof(double), s));
+    return;
+  }
+  k_up_level<<<warp_grid(np), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, np,
+                                                A.xhat.p + A.vec_off[l], xp);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_down_level(const Matrix& A, int l, cudaStream_t s) {
+  const int kc = A.rank[l], kp = A.rank[l - 1];
+  if (kc == 0 || kp == 0) return;
+  const int64_t nc = A.nodes(l);
+  k_down_level<<<warp_grid(nc), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
+                                                  nc, A.yhat.p + A.vec_off[l - 1],
+                                                  A.yhat.p + A.vec_off[l]);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
+                      cudaStream_t s) {
+  const int64_t nl = A.nodes(A.q);
+  k_down_leaf<<<warp_grid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[A.q], nl,
+                                                 A.yhat.p + A.vec_off[A.q], A.yc.p, A.perm.p, y,
+                                                 alpha, beta, to_user ? 1 : 0);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
+                double* ydense, const double* xh, double* yh, cudaStream_t s) {
+  if (nwork == 0) return;
+  LayerTable T{};
+  for (int l = 0; l <= A.q; ++l) {
+    const Layer& L = A.cpl[l];
+    LayerDesc& d = T.L[l];
+    d.val = L.val;
+    d.rp = L.rp;
+    d.ci = L.ci;
+    d.x = xh + A.vec_off[l];
+    d.y = yh + A.vec_off[l];
+    d.stride = L.block_stride();
+    d.br = L.br;
+    d.bc = L.bc;
+    d.ld = std::max(2, L.ld);
+  }
+  LayerDesc& d = T.L[A.q + 1];
+  d.val = A.dense.val;
+  d.rp = A.dense.rp;
+  d.ci = A.dense.ci;
+  d.x = xdense;
+  d.y = ydense;
+  d.stride = A.dense.block_stride();
+  d.br = A.dense.br;
+  d.bc = A.dense.bc;
+  d.ld = std::max(2, A.dense.ld);
+  k_bsr<<<warp_grid(nwork), kThreads, 0, s>>>(T, work, nwork);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s) {
+  k_gather<<<flat_grid(n), kThreads, 0, s>>>(perm, x, xc, n);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_repack(const double* src, int64_t ss, int ld_src, double* dst, int64_t sd, int ld_dst,
+                   int rows, int cols, int64_t count, cudaStream_t s) {
+  const int64_t total = int64_t(ld_dst) * cols * count;
+  if (total == 0) return;
+  k_repack<<<flat_grid(total), kThreads, 0, s>>>(src, ss, ld_src, dst, sd, ld_dst, rows, cols,
+                                                 count);
+  H2B_CUDA(cudaGetLastError());
+}
+
+std::vector<uint32_t> make_work_list(const std::vector<const Layer*>& layers) {
+  struct Item {
+    uint32_t code;
+    int32_t cost;
+  };
+  std::vector<Item> items;
+  for (size_t li = 0; li < layers.size(); ++li) {
+    const Layer* L = layers[li];
+    if (!L) continue;
+    for (int64_t r = 0; r < L->rows; ++r) {
+      const int32_t nb = L->h_rp.empty() ? 0 : L->h_rp[r + 1] - L->h_rp[r];
+      // cost ~ bytes of the row; empty rows still write zeros
+      const int64_t bytes = int64_t(nb) * L->ld * L->bc;
+      items.push_back({uint32_t(li) << kLayerShift | uint32_t(r), int32_t(std::min<int64_t>(bytes, 1 << 30))});
+    }
+  }
+  std::stable_sort(items.begin(), items.end(),
+                   [](const Item& a, const Item& b) { return a.cost > b.cost; });
+  std::vector<uint32_t> out(items.size());
+  for (size_t i = 0; i < items.size(); ++i) out[i] = items[i].code;
+  return out;
+}
+
+}  // namespace h2b
