@@ -232,7 +232,8 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(1 + rank)
     xt = torch.rand(n, dtype=torch.float64, device="cuda", generator=gen)
     yt = torch.zeros(n, dtype=torch.float64, device="cuda")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # explicit stream: NULL would mean the matrix's own stream
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
     # launches per step: up_leaf + per-level up + bsr + per-level down + down_leaf

@@ -289,9 +289,11 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const int j = j0 + q * G + grp;
-          // bc > 32 implies G == 1, so j (and the xr0/xr1 choice) is warp-uniform.
-          const double xj = __shfl_sync(kFull, j < 32 ? xr0 : xr1, j & 31);
+          const int jb = j0 + q * G;  // warp-uniform
+          const int j = jb + grp;
+          // bc > 32 implies G == 1: active lanes have j == jb, and the source
+          // lane's register choice must depend on the uniform jb only.
+          const double xj = __shfl_sync(kFull, jb < 32 ? xr0 : xr1, j & 31);
           if (j < D.bc) {
             y0 += v[q].x * xj;
             y1 += v[q].y * xj;
