@@ -1,16 +1,749 @@
-// Algebraic recompression on the device (compression.hpp:466-551).
+// Algebraic recompression on the device (include/h2kit/compression.hpp:466-551).
+//
+//   orthogonalize (QR upsweep)   k_orth_leaf, k_orth_level          compression.hpp:69-126
+//   project S <- T S T^T         k_project (one CTA per block row)  :130-169
+//   ||A||_F^2                    k_sumsq                            :453-460
+//   weight tree (R-only QR)      k_weights (streaming TSQR, unpadded stacks)  :184-256
+//   truncate (SVD upsweep)       k_trunc_leaf_svd / _apply, k_trunc_level_svd / _apply  :267-420
+//   project with rectangular T   k_project                          :542
+//
+// One 256-thread CTA owns one batch entry; its matrices live in shared memory
+// (cta_linalg.cuh).  The per-level rank max (compression.hpp:301,375) is a
+// device atomicMax; the host reads one int per level.  Pools change shape
+// after truncation, so the matrix is re-laid out (new leaf/transfer/coupling
+// pools, x^/y^ workspace, BSR work list) at the end.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "cta_linalg.cuh"
 #include "h2b_internal.hpp"
 
 namespace h2b {
 
+void upload_structure(Matrix& A);
+
+namespace {
+
+using cta::kThreads;
+
+// ------------------------------------------------------------------ kernels
+__global__ void __launch_bounds__(kThreads) k_orth_leaf(double* __restrict__ leaf, int ldm, int m,
+                                                        int k, double* __restrict__ T) {
+  extern __shared__ double sm[];
+  double* A = sm;                 // m x k, ld m
+  double* Q = A + m * k;          // m x k, ld m
+  double* tau = Q + m * k;        // 64
+  double* red = tau + 64;         // 16
+  int* flip = reinterpret_cast<int*>(red + 16);
+  const int64_t i = blockIdx.x;
+  double* U = leaf + i * int64_t(ldm) * k;
+  cta::copy_block(A, m, U, ldm, m, k);
+  __syncthreads();
+  cta::householder(A, m, m, k, tau, red);
+  cta::form_q(A, m, m, k, tau, Q, m);
+  __syncthreads();
+  cta::extract_r(A, m, k, T + i * int64_t(k) * k, k, flip);
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * k; e += kThreads) {
+    const int j = e / m, r = e - j * m;
+    U[r + int64_t(j) * ldm] = flip[j] ? -Q[r + j * m] : Q[r + j * m];
+  }
+}
+
+// Parent p at level l-1: Z = [T_2p F_2p; T_2p+1 F_2p+1] (2kc x kp) -> QR.
+__global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F, int ldf, int kc,
+                                                         int kp, const double* __restrict__ Tl,
+                                                         double* __restrict__ Tp) {
+  extern __shared__ double sm[];
+  const int zr = 2 * kc;
+  double* Z = sm;                    // zr x kp
+  double* Q = Z + zr * kp;           // zr x kp
+  double* tau = Q + zr * kp;
+  double* red = tau + 64;
+  int* flip = reinterpret_cast<int*>(red + 16);
+  const int64_t p = blockIdx.x;
+  const int64_t fs = int64_t(ldf) * kp;
+  for (int ci = 0; ci < 2; ++ci) {
+    const int64_t c = 2 * p + ci;
+    cta::gemm<false, false>(Z + ci * kc, zr, Tl + c * int64_t(kc) * kc, kc, F + c * fs, ldf, kc, kp, kc);
+  }
+  __syncthreads();
+  cta::householder(Z, zr, zr, kp, tau, red);
+  cta::form_q(Z, zr, zr, kp, tau, Q, zr);
+  __syncthreads();
+  cta::extract_r(Z, zr, kp, Tp + p * int64_t(kp) * kp, kp, flip);
+  __syncthreads();
+  for (int ci = 0; ci < 2; ++ci) {
+    double* dst = F + (2 * p + ci) * fs;
+    for (int e = threadIdx.x; e < kc * kp; e += kThreads) {
+      const int j = e / kc, r = e - j * kc;
+      const double v = Q[ci * kc + r + j * zr];
+      dst[r + int64_t(j) * ldf] = flip[j] ? -v : v;
+    }
+  }
+}
+
+struct ProjRow {
+  int32_t level;
+  int32_t row;
+};
+
+struct ProjLevel {
+  const double* S;    // old blocks (ld_old x co)
+  double* out;        // new blocks (ld_new x cn)
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* T;    // rn x ro per node, ld rn
+  int ro, rn, ld_old, ld_new;
+};
+struct ProjTable {
+  ProjLevel L[kMaxLevels + 1];
+};
+
+// S_b <- T_row S_b T_col^T for every block of one block row (compression.hpp:160-168).
+__global__ void __launch_bounds__(kThreads) k_project(const __grid_constant__ ProjTable P,
+                                                      const ProjRow* __restrict__ rows) {
+  extern __shared__ double sm[];
+  const ProjRow pr = rows[blockIdx.x];
+  const ProjLevel& L = P.L[pr.level];
+  const int ro = L.ro, rn = L.rn;
+  double* Tr = sm;              // rn x ro
+  double* Sb = Tr + rn * ro;    // ro x ro  (then T_col)
+  double* TS = Sb + ro * ro;    // rn x ro
+  cta::copy_block(Tr, rn, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
+  const int b0 = L.rp[pr.row], b1 = L.rp[pr.row + 1];
+  for (int b = b0; b < b1; ++b) {
+    __syncthreads();
+    cta::copy_block(Sb, ro, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
+    __syncthreads();
+    cta::gemm<false, false>(TS, rn, Tr, rn, Sb, ro, rn, ro, ro);
+    __syncthreads();
+    const int c = L.ci[b];
+    cta::copy_block(Sb, rn, L.T + int64_t(c) * rn * ro, rn, rn, ro);
+    __syncthreads();
+    double* out = L.out + int64_t(b) * L.ld_new * rn;
+    cta::gemm<false, true>(out, L.ld_new, TS, rn, Sb, rn, rn, rn, ro);
+    if (L.ld_new > rn)
+      for (int j = threadIdx.x; j < rn; j += kThreads) out[rn + int64_t(j) * L.ld_new] = 0.0;
+  }
+}
+
+__global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restrict__ part) {
+  __shared__ double red[16];
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    s += v[e] * v[e];
+  s = cta::cta_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// R^l_r = R-factor of [R^{l-1}_{r/2} E_r^T ; S_rb^T ...] by streaming
+// Householder TSQR over chunks of <= kChunk coupling blocks (no padding).
+constexpr int kChunk = 2;
+__global__ void __launch_bounds__(kThreads) k_weights(const double* __restrict__ E, int lde, int kc,
+                                                      int kp, const double* __restrict__ Rpar,
+                                                      const int32_t* __restrict__ rp,
+                                                      const int32_t* __restrict__ ci,
+                                                      const double* __restrict__ S, int lds,
+                                                      double* __restrict__ Rout) {
+  extern __shared__ double sm[];
+  const int ldb = kc + (kp > kChunk * kc ? kp : kChunk * kc);  // Racc + one chunk
+  double* B = sm;                                             // ldb x kc
+  double* tau = B + ldb * kc;
+  double* red = tau + 64;
+  int* flip = reinterpret_cast<int*>(red + 16);
+  const int64_t r = blockIdx.x;
+  cta::zero_block(B, ldb, ldb, kc);
+  __syncthreads();
+  int rows = kc;  // rows [0, kc) hold the running R factor (zero initially)
+  if (kp > 0) {   // parent contribution R_p E_r^T (kp x kc)
+    cta::gemm<false, true>(B + kc, ldb, Rpar + (r >> 1) * int64_t(kp) * kp, kp,
+                           E + r * int64_t(lde) * kp, lde, kp, kc, kp);
+    rows += kp;
+  }
+  const int b1 = rp[r + 1];
+  int b = rp[r];
+  for (;;) {
+    for (; b < b1 && rows + kc <= ldb; ++b, rows += kc) {  // append S_rb^T
+      const double* Sb = S + int64_t(b) * lds * kc;
+      for (int e = threadIdx.x; e < kc * kc; e += kThreads) {
+        const int j = e / kc, i = e - j * kc;  // S(i, j) -> B(rows + j, i)
+        B[rows + j + i * ldb] = Sb[i + int64_t(j) * lds];
+      }
+    }
+    __syncthreads();
+    if (rows > kc) {
+      cta::householder(B, ldb, rows, kc, tau, red);
+      for (int e = threadIdx.x; e < rows * kc; e += kThreads) {  // keep R only
+        const int j = e / rows, i = e - j * rows;
+        if (i > j) B[i + j * ldb] = 0.0;
+      }
+      __syncthreads();
+      rows = kc;
+    }
+    if (b >= b1) break;
+  }
+  cta::extract_r(B, ldb, kc, Rout + r * int64_t(kc) * kc, kc, flip);
+}
+
+// One-sided Jacobi SVD of W (rows x cols, smem, ld = rows) into Uout (global,
+// rows x s) + sigma; `work` holds >= cols*rows + 64 doubles when rows < cols.
+__device__ int svd_to(double* W, int rows, int cols, double* work, double* Uout, int ldu,
+                      double* sig, double eps, double* nrm, int* ord, int* flag, double* tau,
+                      double* red) {
+  const int s = rows < cols ? rows : cols;
+  if (s == 0) return 0;
+  if (rows >= cols) {
+    int n = cols;
+    if (n & 1) {  // zero pad column
+      for (int i = threadIdx.x; i < rows; i += kThreads) W[i + cols * rows] = 0.0;
+      ++n;
+    }
+    __syncthreads();
+    cta::jacobi(W, rows, rows, n, flag);
+    cta::jacobi_finish(W, rows, rows, n, s, Uout, ldu, sig, nrm, ord);
+  } else {
+    // wide: QR of W^T (cols x rows), Jacobi on R^T (linalg.hpp:195-207)
+    double* At = work;  // cols x rows, ld cols
+    for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
+      const int j = e / rows, i = e - j * rows;
+      At[j + i * cols] = W[i + j * rows];
+    }
+    __syncthreads();
+    cta::householder(At, cols, cols, rows, tau, red);
+    int* flip = ord;  // reuse as scratch, overwritten by jacobi_finish
+    cta::extract_r(At, cols, rows, W, rows, flip);  // R (rows x rows) into W
+    __syncthreads();
+    double* G = work;  // rows x (rows + 1)
+    for (int e = threadIdx.x; e < rows * rows; e += kThreads) {
+      const int j = e / rows, i = e - j * rows;
+      G[i + j * rows] = W[j + i * rows];
+    }
+    int n = rows;
+    if (n & 1) {
+      for (int i = threadIdx.x; i < rows; i += kThreads) G[i + rows * rows] = 0.0;
+      ++n;
+    }
+    __syncthreads();
+    cta::jacobi(G, rows, rows, n, flag);
+    cta::jacobi_finish(G, rows, rows, n, s, Uout, ldu, sig, nrm, ord);
+  }
+  int rank = 0;
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < s; ++j)
+      if (sig[0] > 0.0 && sig[j] >= eps * sig[0]) ++rank;
+  }
+  return rank;
+}
+
+__device__ void check_finite(const double* W, int n, int* bad) {
+  for (int e = threadIdx.x; e < n; e += kThreads)
+    if (!isfinite(W[e])) *bad = 1;
+}
+
+// Leaves: W = U R^T (m x k), truncated SVD (compression.hpp:285-300).
+__global__ void __launch_bounds__(kThreads) k_trunc_leaf_svd(const double* __restrict__ leaf, int ldm,
+                                                             int m, int k, const double* __restrict__ R,
+                                                             double* __restrict__ Uout,
+                                                             double* __restrict__ sig_out, double eps,
+                                                             int* __restrict__ kmax, int* __restrict__ bad) {
+  extern __shared__ double sm[];
+  const int s = m < k ? m : k;
+  double* W = sm;                       // m x (k+1)
+  double* work = W + m * (k + 1);       // (k x m) + pad for the wide case
+  double* nrm = work + (k + 1) * (m + 1);
+  double* tau = nrm + 128;
+  double* red = tau + 64;
+  int* ord = reinterpret_cast<int*>(red + 16);
+  int* flag = ord + 128;
+  const int64_t i = blockIdx.x;
+  cta::gemm<false, true>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
+  __syncthreads();
+  check_finite(W, m * k, bad);
+  double* sg = sig_out + i * s;
+  const int rank = svd_to(W, m, k, work, Uout + i * int64_t(m) * s, m, sg, eps, nrm, ord, flag, tau, red);
+  if (threadIdx.x == 0) atomicMax(kmax, rank);
+}
+
+// T^q = Q^T U_old (kt x k), new leaf = Q (m x kt), discarded energy (:309-324).
+__global__ void __launch_bounds__(kThreads) k_trunc_leaf_apply(const double* __restrict__ leaf, int ldm,
+                                                               int m, int k, int s, int kt,
+                                                               const double* __restrict__ Uq,
+                                                               const double* __restrict__ sig,
+                                                               double* __restrict__ Tq,
+                                                               double* __restrict__ newleaf, int ldn,
+                                                               double* __restrict__ energy) {
+  const int64_t i = blockIdx.x;
+  const double* Q = Uq + i * int64_t(m) * s;
+  if (kt > 0)
+    cta::gemm<true, false>(Tq + i * int64_t(kt) * k, kt, Q, m, leaf + i * int64_t(ldm) * k, ldm, kt, k, m);
+  double* nl = newleaf + i * int64_t(ldn) * kt;
+  for (int e = threadIdx.x; e < ldn * kt; e += kThreads) {
+    const int j = e / ldn, r = e - j * ldn;
+    nl[e] = r < m ? Q[r + int64_t(j) * m] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int j = kt; j < s; ++j) acc += sig[i * s + j] * sig[i * s + j];
+    energy[i] = acc;
+  }
+}
+
+// Parent p: Z = [Tt_c E_c] (2kt_c x kp), W = Z R^{l-1,T}, SVD (:327-376).
+__global__ void __launch_bounds__(kThreads) k_trunc_level_svd(
+    const double* __restrict__ E, int lde, int kc, int kp, int ktc, const double* __restrict__ Tt,
+    const double* __restrict__ Rp, double* __restrict__ Zout, double* __restrict__ Uout,
+    double* __restrict__ sig_out, double eps, int* __restrict__ kmax, int* __restrict__ bad) {
+  extern __shared__ double sm[];
+  const int zr = 2 * ktc;
+  const int s = zr < kp ? zr : kp;
+  double* Z = sm;                        // zr x kp
+  double* W = Z + zr * kp;               // zr x (kp + 1)
+  double* work = W + zr * (kp + 1);      // (kp x zr) or G (zr x zr+1)
+  double* nrm = work + (kp + 1) * (zr + 1);
+  double* tau = nrm + 128;
+  double* red = tau + 64;
+  int* ord = reinterpret_cast<int*>(red + 16);
+  int* flag = ord + 128;
+  const int64_t p = blockIdx.x;
+  const int64_t es = int64_t(lde) * kp;
+  for (int ci = 0; ci < 2; ++ci) {
+    const int64_t c = 2 * p + ci;
+    cta::gemm<false, false>(Z + ci * ktc, zr, Tt + c * int64_t(ktc) * kc, ktc, E + c * es, lde, ktc, kp, kc);
+  }
+  __syncthreads();
+  cta::copy_block(Zout + p * int64_t(zr) * kp, zr, Z, zr, zr, kp);
+  cta::gemm<false, true>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
+  __syncthreads();
+  check_finite(W, zr * kp, bad);
+  const int rank = svd_to(W, zr, kp, work, Uout + p * int64_t(zr) * s, zr, sig_out + p * s, eps, nrm,
+                          ord, flag, tau, red);
+  if (threadIdx.x == 0) atomicMax(kmax, rank);
+}
+
+// T^{l-1}_p = Q^T Z (kt_p x kp); new transfers = Q row blocks (:382-415).
+__global__ void __launch_bounds__(kThreads) k_trunc_level_apply(
+    int ktc, int kp, int s, int ktp, const double* __restrict__ Zin, const double* __restrict__ Uin,
+    const double* __restrict__ sig, double* __restrict__ Tp, double* __restrict__ Enew, int ldn,
+    double* __restrict__ energy) {
+  const int zr = 2 * ktc;
+  const int64_t p = blockIdx.x;
+  const double* Q = Uin + p * int64_t(zr) * s;
+  if (ktp > 0)
+    cta::gemm<true, false>(Tp + p * int64_t(ktp) * kp, ktp, Q, zr, Zin + p * int64_t(zr) * kp, zr, ktp,
+                           kp, zr);
+  for (int ci = 0; ci < 2; ++ci) {
+    double* dst = Enew + (2 * p + ci) * int64_t(ldn) * ktp;
+    for (int e = threadIdx.x; e < ldn * ktp; e += kThreads) {
+      const int j = e / ldn, r = e - j * ldn;
+      dst[e] = r < ktc ? Q[ci * ktc + r + int64_t(j) * zr] : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int j = ktp; j < s; ++j) acc += sig[p * s + j] * sig[p * s + j];
+    energy[p] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ host helpers
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    H2B_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+constexpr size_t kSmemCap = 227 * 1024;
+
+void check_smem(size_t bytes, const char* what) {
+  if (bytes > kSmemCap) throw Error(H2B_UNSUPPORTED, std::string(what) + ": shared-memory footprint too large");
+}
+
+struct Flops {
+  double gemm(double c, double m, double n, double k) { return 2.0 * m * n * k * c; }
+  double qr(double c, double r, double k) { return 2.0 * k * k * (r - k / 3.0) * c; }
+  double svd(double c, double r, double k) {
+    const double s = std::min(r, k);
+    return (2.0 * s * s * (std::max(r, k) - s / 3.0) + 60.0 * s * s * s) * c;
+  }
+};
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    H2B_CUDA(cudaEventCreate(&a));
+    H2B_CUDA(cudaEventCreate(&b));
+    H2B_CUDA(cudaEventRecord(a, s));
+  }
+  double stop() {
+    H2B_CUDA(cudaEventRecord(b, s));
+    H2B_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    H2B_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+  }
+};
+
+// Level-concatenated pool of per-node (rows[l] x cols[l]) matrices, ld = rows.
+struct TreePool {
+  DevBuf<double> buf;
+  std::vector<int64_t> off;
+  std::vector<int> rows, cols;
+  void alloc(const Matrix& A, const std::vector<int>& r, const std::vector<int>& c) {
+    rows = r;
+    cols = c;
+    off.assign(A.q + 2, 0);
+    for (int l = 0; l <= A.q; ++l) off[l + 1] = off[l] + A.nodes(l) * int64_t(r[l]) * c[l];
+    buf.alloc(std::max<int64_t>(1, off[A.q + 1]));
+  }
+  double* at(int l) { return buf.p + off[l]; }
+};
+
+// ---------------------------------------------------------------- phases
+void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops) {
+  const int q = A.q, m = A.m, kq = A.rank[q];
+  require(m >= kq, "orthogonalize_basis: leaf_dim must be >= leaf rank");
+  T.alloc(A, A.rank, A.rank);
+  const int64_t nl = A.nodes(q);
+  if (kq > 0) {
+    const size_t sm = (2 * size_t(m) * kq + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    check_smem(sm, "orthogonalize");
+    set_smem(k_orth_leaf, sm);
+    k_orth_leaf<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, T.at(q));
+    H2B_CUDA(cudaGetLastError());
+  }
+  flops += fl.qr(double(nl), m, kq);
+  for (int l = q; l >= 1; --l) {
+    const int kc = A.rank[l], kp = A.rank[l - 1];
+    const int64_t np = A.nodes(l - 1);
+    flops += fl.gemm(double(A.nodes(l)), kc, kp, kc) + fl.qr(double(np), 2 * kc, kp);
+    require(2 * kc >= kp, "qr_batched: requires rows >= cols");
+    if (kp == 0) continue;
+    const size_t sm = (2 * size_t(2 * kc) * kp + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    check_smem(sm, "orthogonalize");
+    set_smem(k_orth_level, sm);
+    k_orth_level<<<unsigned(np), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
+                                                   T.at(l), T.at(l - 1));
+    H2B_CUDA(cudaGetLastError());
+  }
+}
+
+// Project every coupling level with T (rows x cols per node): blocks become
+// T.rows[l] x T.rows[l].  Writes into `out_pool` (may alias the current pool
+// when the shapes agree).
+void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place) {
+  const int q = A.q;
+  ProjTable P{};
+  std::vector<ProjRow> rows;
+  std::vector<int64_t> new_off(q + 2, 0);
+  for (int l = 0; l <= q; ++l) {
+    const Layer& L = A.cpl[l];
+    const int rn = T.rows[l];
+    new_off[l + 1] = new_off[l] + L.nb * int64_t(pad2(rn)) * rn;
+  }
+  DevBuf<double> fresh;
+  if (!in_place) fresh.alloc(std::max<int64_t>(1, new_off[q + 1]));
+  double* base = in_place ? A.cpl_val.p : fresh.p;
+  size_t smax = 0;
+  for (int l = 0; l <= q; ++l) {
+    Layer& L = A.cpl[l];
+    const int rn = T.rows[l], ro = T.cols[l];
+    if (L.nb == 0) continue;
+    require(ro == L.br && ro == L.bc, "project_coupling: dim mismatch");
+    flops += fl.gemm(double(L.nb), rn, ro, ro) + fl.gemm(double(L.nb), rn, rn, ro);
+    ProjLevel& d = P.L[l];
+    d.S = L.val;
+    d.out = base + new_off[l];
+    d.rp = L.rp;
+    d.ci = L.ci;
+    d.T = T.at(l);
+    d.ro = ro;
+    d.rn = rn;
+    d.ld_old = L.ld;
+    d.ld_new = pad2(rn);
+    if (rn == 0) continue;
+    for (int64_t r = 0; r < L.rows; ++r)
+      if (L.h_rp[r + 1] > L.h_rp[r]) rows.push_back({l, int32_t(r)});
+    smax = std::max(smax, (size_t(rn) * ro * 2 + size_t(ro) * ro) * sizeof(double));
+  }
+  if (!rows.empty()) {
+    check_smem(smax, "project_coupling");
+    DevBuf<ProjRow> drows;
+    drows.alloc(rows.size());
+    H2B_CUDA(cudaMemcpyAsync(drows.p, rows.data(), rows.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
+    set_smem(k_project, smax);
+    k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows.p);
+    H2B_CUDA(cudaGetLastError());
+    H2B_CUDA(cudaStreamSynchronize(s));
+  }
+  if (!in_place) A.cpl_val = std::move(fresh);
+  for (int l = 0; l <= q; ++l) {
+    Layer& L = A.cpl[l];
+    L.br = L.bc = T.rows[l];
+    L.ld = pad2(L.br);
+    L.val = A.cpl_val.p + new_off[l];
+  }
+}
+
+double sumsq(const double* v, int64_t n, cudaStream_t s) {
+  if (n == 0) return 0.0;
+  const int blocks = 1024;
+  DevBuf<double> part;
+  part.alloc(blocks);
+  k_sumsq<<<blocks, kThreads, 0, s>>>(v, n, part.p);
+  H2B_CUDA(cudaGetLastError());
+  std::vector<double> h(blocks);
+  H2B_CUDA(cudaMemcpyAsync(h.data(), part.p, blocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+  double acc = 0.0;
+  for (double v2 : h) acc += v2;
+  return acc;
+}
+
+void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
+  const int q = A.q;
+  R.alloc(A, A.rank, A.rank);
+  H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * A.rank[0] * A.rank[0], s));
+  for (int l = 1; l <= q; ++l) {
+    const int kc = A.rank[l], kp = A.rank[l - 1];
+    const Layer& L = A.cpl[l];
+    const int ld_ref = kp + L.max_row * kc;  // the reference's padded stack height
+    flops += fl.gemm(double(A.nodes(l)), kp, kc, kp) + fl.qr(double(A.nodes(l)), ld_ref, kc);
+    require(ld_ref >= kc, "qr_r_only_batched: requires rows >= cols");
+    if (kc == 0) continue;
+    const int ldb = kc + std::max(kp, kChunk * kc);
+    const size_t sm = (size_t(ldb) * kc + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    check_smem(sm, "generate_weight_tree");
+    set_smem(k_weights, sm);
+    k_weights<<<unsigned(A.nodes(l)), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
+                                                        R.at(l - 1), L.rp, L.ci, L.val, L.ld, R.at(l));
+    H2B_CUDA(cudaGetLastError());
+  }
+}
+
+int read_kmax(int* d, cudaStream_t s) {
+  int h = 0;
+  H2B_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+double sum_host(const DevBuf<double>& d, int64_t n, cudaStream_t s) {
+  std::vector<double> h(n);
+  if (n) H2B_CUDA(cudaMemcpyAsync(h.data(), d.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+  double acc = 0.0;
+  for (double v : h) acc += v;
+  return acc;
+}
+
+// Returns the discarded energy; fills Tt (new x old per node) and replaces
+// the leaf / transfer pools and ranks.
+double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s, Flops& fl,
+                double& flops) {
+  require(eps >= 0.0, "truncate_basis: eps must be non-negative");
+  const int q = A.q, m = A.m;
+  const std::vector<int> old = A.rank;
+  std::vector<int> nr(q + 1, 0);
+  std::vector<double> lev_e(q + 1, 0.0);
+  DevBuf<int> dk;
+  dk.alloc(2);  // [0] = kmax, [1] = non-finite flag
+  std::vector<DevBuf<double>> newtr(q + 1);
+  std::vector<int> trows(q + 1, 0);
+  // projection pool sized after the fact per level
+  std::vector<DevBuf<double>> Tlev(q + 1);
+  const int64_t nl = A.nodes(q);
+  DevBuf<double> newleaf;
+  {
+    const int kq = old[q];
+    const int sl = std::min(m, kq);
+    flops += fl.gemm(double(nl), m, kq, kq) + fl.svd(double(nl), m, kq);
+    DevBuf<double> Uq, sg, en;
+    Uq.alloc(std::max<int64_t>(1, nl * m * sl));
+    sg.alloc(std::max<int64_t>(1, nl * sl));
+    en.alloc(nl);
+    H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
+    if (sl > 0) {
+      const size_t sm = (size_t(m) * (kq + 1) + size_t(kq + 1) * (m + 1) + 128 + 64 + 16) * sizeof(double) +
+                        256 * sizeof(int) + 64;
+      check_smem(sm, "truncate_basis");
+      set_smem(k_trunc_leaf_svd, sm);
+      k_trunc_leaf_svd<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, R.at(q), Uq.p, sg.p, eps,
+                                                          dk.p, dk.p + 1);
+      H2B_CUDA(cudaGetLastError());
+    }
+    int flags[2] = {0, 0};
+    H2B_CUDA(cudaMemcpyAsync(flags, dk.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaStreamSynchronize(s));
+    require(flags[1] == 0, "svd_truncated_batched: non-finite input");
+    const int kt = std::min(flags[0], sl);
+    nr[q] = kt;
+    flops += fl.gemm(double(nl), kt, kq, m);
+    Tlev[q].alloc(std::max<int64_t>(1, nl * kt * kq));
+    const int ldn = pad2(m);
+    newleaf.alloc(std::max<int64_t>(1, nl * ldn * kt));
+    k_trunc_leaf_apply<<<unsigned(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq.p, sg.p,
+                                                         Tlev[q].p, newleaf.p, ldn, en.p);
+    H2B_CUDA(cudaGetLastError());
+    lev_e[q] = sum_host(en, nl, s);
+  }
+  for (int l = q; l >= 1; --l) {
+    const int ktc = nr[l], kc = old[l], kp = old[l - 1];
+    const int64_t np = A.nodes(l - 1);
+    const int zr = 2 * ktc;
+    const int sl = std::min(zr, kp);
+    flops += fl.gemm(double(A.nodes(l)), ktc, kp, kc) + fl.gemm(double(np), zr, kp, kp) +
+             fl.svd(double(np), zr, kp);
+    DevBuf<double> Z, U, sg, en;
+    Z.alloc(std::max<int64_t>(1, np * zr * kp));
+    U.alloc(std::max<int64_t>(1, np * zr * sl));
+    sg.alloc(std::max<int64_t>(1, np * sl));
+    en.alloc(np);
+    H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
+    if (sl > 0) {
+      const size_t sm = (size_t(zr) * kp + size_t(zr) * (kp + 1) + size_t(kp + 1) * (zr + 1) + 128 + 64 + 16) *
+                            sizeof(double) + 256 * sizeof(int) + 64;
+      check_smem(sm, "truncate_basis");
+      set_smem(k_trunc_level_svd, sm);
+      k_trunc_level_svd<<<unsigned(np), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, ktc,
+                                                           Tlev[l].p, R.at(l - 1), Z.p, U.p, sg.p, eps, dk.p,
+                                                           dk.p + 1);
+      H2B_CUDA(cudaGetLastError());
+    }
+    int flags[2] = {0, 0};
+    H2B_CUDA(cudaMemcpyAsync(flags, dk.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaStreamSynchronize(s));
+    require(flags[1] == 0, "svd_truncated_batched: non-finite input");
+    const int ktp = std::min(flags[0], sl);
+    nr[l - 1] = ktp;
+    flops += fl.gemm(double(np), ktp, kp, zr);
+    Tlev[l - 1].alloc(std::max<int64_t>(1, np * ktp * kp));
+    const int ldn = pad2(ktc);
+    newtr[l].alloc(std::max<int64_t>(1, A.nodes(l) * ldn * ktp));
+    k_trunc_level_apply<<<unsigned(np), kThreads, 0, s>>>(ktc, kp, sl, ktp, Z.p, U.p, sg.p, Tlev[l - 1].p,
+                                                          newtr[l].p, ldn, en.p);
+    H2B_CUDA(cudaGetLastError());
+    lev_e[l - 1] = sum_host(en, np, s);
+  }
+  // gather Tt into one pool (rows = new rank, cols = old rank)
+  Tt.alloc(A, nr, old);
+  for (int l = 0; l <= q; ++l) {
+    const int64_t sz = A.nodes(l) * int64_t(nr[l]) * old[l];
+    if (sz) H2B_CUDA(cudaMemcpyAsync(Tt.at(l), Tlev[l].p, sz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  // new transfer pool with padded ld for the new ranks
+  A.rank = nr;
+  std::vector<int64_t> toff(q + 2, 0);
+  int64_t t = 0;
+  for (int l = 1; l <= q; ++l) {
+    toff[l] = t;
+    t += A.nodes(l) * A.tr_stride(l);
+  }
+  toff[q + 1] = t;
+  DevBuf<double> trpool;
+  trpool.alloc(std::max<int64_t>(1, t));
+  for (int l = 1; l <= q; ++l) {
+    const int64_t sz = A.nodes(l) * A.tr_stride(l);
+    if (sz) H2B_CUDA(cudaMemcpyAsync(trpool.p + toff[l], newtr[l].p, sz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  H2B_CUDA(cudaStreamSynchronize(s));
+  A.transfer = std::move(trpool);
+  A.tr_off = toff;
+  A.leaf = std::move(newleaf);
+  double energy = 0.0;
+  for (double e : lev_e) energy += e;
+  return energy;
+}
+
+// Resize the workspace and rebuild the BSR work list after ranks changed.
+void relayout(Matrix& A) {
+  const int q = A.q;
+  A.vec_off.assign(q + 2, 0);
+  for (int l = 0; l <= q; ++l) A.vec_off[l + 1] = A.vec_off[l] + A.nodes(l) * A.rank[l];
+  A.xhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
+  A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
+  upload_structure(A);
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    H2B_CUDA(cudaSetDevice(d));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
 void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep) {
-  (void)A; (void)eps; (void)rep;
-  throw Error(H2B_UNSUPPORTED, "compress: not implemented yet");
+  require(eps >= 0.0, "truncate_basis: eps must be non-negative");
+  DeviceGuard g(A.device);
+  cudaStream_t s = A.stream;
+  Flops fl;
+  h2b_compress_report r{};
+  for (int l = 0; l <= A.q; ++l) r.old_ranks[l] = A.rank[l];
+  r.bytes_before = A.footprint();
+
+  TreePool To, R, Tt;
+  {
+    Timer t(s);
+    orthogonalize(A, To, s, fl, r.flops_orthogonalize);
+    r.time_orthogonalize_ms = t.stop();
+  }
+  {
+    Timer t(s);
+    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true);
+    r.time_project_orth_ms = t.stop();
+  }
+  To.buf.release();
+  double n2 = 0.0;
+  for (int l = 0; l <= A.q; ++l) n2 += sumsq(A.cpl[l].val, A.cpl[l].nb * A.cpl[l].block_stride(), s);
+  n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s);
+  r.frobenius_norm = std::sqrt(n2);
+  {
+    Timer t(s);
+    weights(A, R, s, fl, r.flops_weights);
+    r.time_weights_ms = t.stop();
+  }
+  double energy = 0.0;
+  {
+    Timer t(s);
+    energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate);
+    r.time_truncate_ms = t.stop();
+  }
+  R.buf.release();
+  {
+    Timer t(s);
+    project(A, Tt, s, fl, r.flops_project_trunc, /*in_place=*/false);
+    r.time_project_trunc_ms = t.stop();
+  }
+  relayout(A);
+  for (int l = 0; l <= A.q; ++l) r.new_ranks[l] = A.rank[l];
+  r.bytes_after = A.footprint();
+  r.frobenius_error = r.frobenius_norm > 0 ? std::sqrt(energy) / r.frobenius_norm : 0.0;
+  if (rep) *rep = r;
 }
 
 void orthogonalize_matrix(Matrix& A, double* t_out) {
-  (void)A; (void)t_out;
-  throw Error(H2B_UNSUPPORTED, "orthogonalize: not implemented yet");
+  DeviceGuard g(A.device);
+  cudaStream_t s = A.stream;
+  Flops fl;
+  double f = 0;
+  TreePool T;
+  orthogonalize(A, T, s, fl, f);
+  if (t_out && T.off[A.q + 1])
+    H2B_CUDA(cudaMemcpyAsync(t_out, T.buf.p, T.off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace h2b

@@ -1,0 +1,273 @@
+// CTA-cooperative FP64 small dense linear algebra in shared memory (the
+// per-entry bodies of the reference's batched engine, include/h2kit/linalg.hpp
+// and batch.hpp, re-designed for one 256-thread CTA per batch entry).
+//
+// Conventions follow the reference exactly where results are defined by them:
+//  * Householder QR with beta = -sign(alpha)||x||, tau = (beta-alpha)/beta,
+//    zero columns get tau = 0 (linalg.hpp:48-75); R is returned with a
+//    non-negative diagonal and the matching Q columns negated (:100-131).
+//  * One-sided Jacobi SVD with the skip rule |a_pq| <= 16 eps sqrt(a_pp a_qq)
+//    or a_pq == 0 and at most 60 sweeps (:142-176); sigma are the column norms,
+//    stable-sorted descending; zero columns give zero vectors (:178-232).
+//    The pair order is the parallel round-robin (tournament) ordering instead
+//    of the cyclic row order, so n/2 rotations run concurrently.
+// All matrices are column-major with explicit leading dimensions.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace h2b {
+namespace cta {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ int lane() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp() { return threadIdx.x >> 5; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) v += __shfl_xor_sync(kFull, v, s);
+  return v;
+}
+
+// Deterministic CTA-wide sum; `red` is >= 9 doubles of scratch smem.
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane() == 0) red[warp()] = v;
+  __syncthreads();
+  if (warp() == 0) {
+    double t = lane() < kWarps ? red[lane()] : 0.0;
+    t = warp_sum(t);
+    if (lane() == 0) red[kWarps] = t;
+  }
+  __syncthreads();
+  return red[kWarps];
+}
+
+// Copy a rows x cols block between column-major buffers (global or smem).
+__device__ __forceinline__ void copy_block(double* dst, int ldd, const double* src, int lds,
+                                          int rows, int cols) {
+  for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
+    const int j = e / rows, i = e - j * rows;
+    dst[i + j * ldd] = src[i + j * lds];
+  }
+}
+
+__device__ __forceinline__ void zero_block(double* dst, int ldd, int rows, int cols) {
+  for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
+    const int j = e / rows, i = e - j * rows;
+    dst[i + j * ldd] = 0.0;
+  }
+}
+
+// C (m x n) = op(A) (m x k) * op(B) (k x n); all operands in smem (or any
+// memory).  Each thread owns a 4 x 4 register tile of a 64 x 64 output tile.
+template <bool TA, bool TB>
+__device__ void gemm(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
+                     int m, int n, int k) {
+  const int tr = (threadIdx.x & 15) * 4;   // row offset in the 64x64 tile
+  const int tc = (threadIdx.x >> 4) * 4;   // col offset
+  for (int i0 = 0; i0 < m; i0 += 64)
+    for (int j0 = 0; j0 < n; j0 += 64) {
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int p = 0; p < k; ++p) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int i = i0 + tr + a;
+          av[a] = i < m ? (TA ? A[p + i * lda] : A[i + p * lda]) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = j0 + tc + b;
+          bv[b] = j < n ? (TB ? B[j + p * ldb] : B[p + j * ldb]) : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = i0 + tr + a, j = j0 + tc + b;
+          if (i < m && j < n) C[i + j * ldc] = acc[a][b];
+        }
+    }
+}
+
+// In-place Householder factorisation (linalg.hpp:48-75): reflectors below the
+// diagonal, R on and above it; tau[cols] in smem; red: >= 9 doubles scratch.
+__device__ void householder(double* A, int lda, int rows, int cols, double* tau, double* red) {
+  for (int j = 0; j < cols; ++j) {
+    double* v = A + j * lda;
+    double part = 0.0;
+    for (int i = j + threadIdx.x; i < rows; i += kThreads) part += v[i] * v[i];
+    const double nx = sqrt(cta_sum(part, red));
+    if (nx == 0.0) {
+      if (threadIdx.x == 0) tau[j] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    const double al = v[j];
+    const double be = al >= 0.0 ? -nx : nx;
+    const double tj = (be - al) / be;
+    const double sc = 1.0 / (al - be);
+    __syncthreads();  // everyone has read v[j]
+    for (int i = j + 1 + threadIdx.x; i < rows; i += kThreads) v[i] *= sc;
+    if (threadIdx.x == 0) {
+      v[j] = be;
+      tau[j] = tj;
+    }
+    __syncthreads();
+    for (int kk = j + 1 + warp(); kk < cols; kk += kWarps) {
+      double* w = A + kk * lda;
+      double s = 0.0;
+      for (int i = j + 1 + lane(); i < rows; i += 32) s += v[i] * w[i];
+      s = warp_sum(s);
+      const double d = (w[j] + s) * tj;
+      __syncwarp();
+      if (lane() == 0) w[j] -= d;
+      for (int i = j + 1 + lane(); i < rows; i += 32) w[i] -= v[i] * d;
+    }
+    __syncthreads();
+  }
+}
+
+// Thin Q (rows x cols) from the factored form (linalg.hpp:77-98).
+__device__ void form_q(const double* A, int lda, int rows, int cols, const double* tau,
+                       double* Q, int ldq) {
+  for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
+    const int j = e / rows, i = e - j * rows;
+    Q[i + j * ldq] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = cols - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double* v = A + j * lda;
+    for (int kk = j + warp(); kk < cols; kk += kWarps) {
+      double* w = Q + kk * ldq;
+      double s = 0.0;
+      for (int i = j + 1 + lane(); i < rows; i += 32) s += v[i] * w[i];
+      s = warp_sum(s);
+      const double d = (w[j] + s) * tj;
+      __syncwarp();
+      if (lane() == 0) w[j] -= d;
+      for (int i = j + 1 + lane(); i < rows; i += 32) w[i] -= v[i] * d;
+    }
+    __syncthreads();
+  }
+}
+
+// R (cols x cols, non-negative diagonal) to R_out; flip[j] (smem ints) marks
+// negated rows (linalg.hpp:100-113).
+__device__ void extract_r(const double* A, int lda, int cols, double* R, int ldr, int* flip) {
+  for (int j = threadIdx.x; j < cols; j += kThreads) flip[j] = A[j + j * lda] < 0.0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < cols * cols; e += kThreads) {
+    const int j = e / cols, i = e - j * cols;
+    const double v = i <= j ? A[i + j * lda] : 0.0;
+    R[i + j * ldr] = flip[i] ? -v : v;
+  }
+}
+
+// Round-robin (circle method) pairing of n (even) columns: round r in
+// [0, n-1), slot s in [0, n/2).
+__device__ __forceinline__ void rr_pair(int n, int r, int s, int& p, int& q) {
+  const int m = n - 1;
+  if (s == 0) {
+    p = r;
+    q = m;
+  } else {
+    p = (r + s) % m;
+    q = (r - s + m) % m;
+  }
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
+// One-sided Jacobi on the columns of G (rows x n, n even; pad with a zero
+// column for odd counts).  flag: one int of smem.
+__device__ void jacobi(double* G, int ldg, int rows, int n, int* flag) {
+  const double tol = 2.220446049250313e-16 * 16.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < n - 1; ++r) {
+      for (int s = warp(); s < n / 2; s += kWarps) {
+        int p, q;
+        rr_pair(n, r, s, p, q);
+        double* gp = G + p * ldg;
+        double* gq = G + q * ldg;
+        double a = 0.0, b = 0.0, d = 0.0;
+        for (int i = lane(); i < rows; i += 32) {
+          const double u = gp[i], w = gq[i];
+          a += u * u;
+          b += w * w;
+          d += u * w;
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        d = warp_sum(d);
+        if (fabs(d) <= tol * sqrt(a * b) || d == 0.0) continue;
+        if (lane() == 0) *flag = 1;
+        const double z = (b - a) / (2.0 * d);
+        const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
+        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double sn = cs * t;
+        for (int i = lane(); i < rows; i += 32) {
+          const double u = gp[i], w = gq[i];
+          gp[i] = cs * u - sn * w;
+          gq[i] = sn * u + cs * w;
+        }
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) break;
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+// After jacobi(): sigma[j] (descending, stable) and U (rows x s) with unit (or
+// zero) columns.  nrm/ord: smem scratch of n doubles / ints.
+__device__ void jacobi_finish(const double* G, int ldg, int rows, int n, int s, double* U, int ldu,
+                              double* sigma, double* nrm, int* ord) {
+  for (int j = warp(); j < n; j += kWarps) {
+    double t = 0.0;
+    for (int i = lane(); i < rows; i += 32) t += G[i + j * ldg] * G[i + j * ldg];
+    t = warp_sum(t);
+    if (lane() == 0) nrm[j] = sqrt(t);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += kThreads) {
+    int rank = 0;
+    const double v = nrm[j];
+    for (int i = 0; i < n; ++i) rank += (nrm[i] > v) || (nrm[i] == v && i < j);
+    ord[rank] = j;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < s; j += kThreads) sigma[j] = nrm[ord[j]];
+  for (int e = threadIdx.x; e < rows * s; e += kThreads) {
+    const int j = e / rows, i = e - j * rows;
+    const int src = ord[j];
+    const double nv = nrm[src];
+    U[i + j * ldu] = nv > 0.0 ? G[i + src * ldg] * (1.0 / nv) : 0.0;
+  }
+  __syncthreads();
+}
+
+}  // namespace cta
+}  // namespace h2b

@@ -1,0 +1,175 @@
+"""GPU parity of the B200 compression (orthogonalize, project, weight tree,
+truncate, project) against the reference CPU implementation.
+
+Bar (BASELINE.json north_star / BASELINE.md §2): per-level truncated ranks
+within +-1 of the reference, Frobenius error estimate within [0.5x, 2x] of the
+reference's, post-compression operator change <= 10 eps."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+import paper_1902_01829_b200 as h2
+from paper_1902_01829_b200.host import HostMatrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _ranks_close(a, b):
+    return len(a) == len(b) and all(abs(int(x) - int(y)) <= 1 for x, y in zip(a, b))
+
+
+def test_compress_matches_reference_golden(gpu, golden):
+    for name, (meta, arr) in sorted(golden.items()):
+        A = h2.H2Matrix.construct(meta["dim"], meta["n"], grid_order=meta["grid_order"])
+        rep = h2.compress(A, meta["eps"])
+        g = meta["compress"]
+        assert _ranks_close(rep.new_ranks, g["new_ranks"]), (name, rep.new_ranks, g["new_ranks"])
+        assert rep.frobenius_norm == pytest.approx(g["frobenius_norm"], rel=1e-12), name
+        if g["frobenius_error"] > 0:
+            assert 0.5 <= rep.frobenius_error / g["frobenius_error"] <= 2.0, (name, rep.frobenius_error)
+        else:
+            assert rep.frobenius_error <= 1e-13
+        assert rep.bytes_after == A.memory_footprint()
+        if rep.new_ranks == g["new_ranks"]:
+            assert rep.bytes_after == g["bytes_after"], name
+            assert rep.total_flops() == pytest.approx(g["total_flops"], rel=1e-12), name
+        yc = h2.hmv(A, arr["x"])
+        assert rel_err(yc, arr["yc"]) <= 10 * meta["eps"], name
+        assert rel_err(yc, arr["y"]) <= 10 * meta["eps"], name
+
+
+def test_compress_uploaded_matches_oracle(gpu, orc):
+    for dim, n, order, eps in [(2, 4096, 8, 1e-7), (3, 4096, 4, 1e-6), (2, 2048, 6, 1e-9)]:
+        O = orc.construct(dim, n, grid_order=order)
+        A = h2.H2Matrix.from_host(O.to_host())
+        x = np.random.default_rng(9).random(n)
+        y0 = O.hmv(x)
+        ro = O.compress(eps)
+        rg = h2.compress(A, eps)
+        assert _ranks_close(rg.new_ranks, ro["new_ranks"]), (rg.new_ranks, ro["new_ranks"])
+        assert 0.5 <= rg.frobenius_error / ro["frobenius_error"] <= 2.0
+        assert rel_err(h2.hmv(A, x), O.hmv(x)) <= 10 * eps
+        assert rel_err(h2.hmv(A, x), y0) <= 10 * eps
+
+
+def test_orthogonalize_matches_oracle(gpu, orc):
+    O = orc.construct(2, 2048)
+    hm = O.to_host()
+    A = h2.H2Matrix.from_host(hm)
+    t_gpu = h2.orthogonalize_basis(A)
+    t_ref = O.orthogonalize()
+    assert rel_err(t_gpu, t_ref) <= 1e-11
+    q_gpu, q_ref = A.to_host(), O.to_host()
+    assert rel_err(q_gpu.leaf, q_ref.leaf) <= 1e-11
+    assert rel_err(q_gpu.transfer, q_ref.transfer) <= 1e-11
+    # V^T V = I at the leaves (acceptance c3)
+    V = q_gpu.leaves()
+    G = np.einsum("bij,bik->bjk", V, V)
+    assert np.max(np.abs(G - np.eye(V.shape[2]))) <= 1e-12
+
+
+def test_eps_zero_preserves_operator(gpu):
+    # test_compression.cpp:217-223
+    A = h2.H2Matrix.construct(2, 1 << 9)
+    x = np.random.default_rng(5).random(1 << 9)
+    y0 = h2.hmv(A, x)
+    rep = h2.compress(A, 0.0)
+    assert rel_err(h2.hmv(A, x), y0) <= 1e-12
+    assert rep.frobenius_error <= 1e-13
+
+
+def test_compression_reports_and_shrinks(gpu):
+    # test_compression.cpp:225-258
+    A = h2.H2Matrix.construct(2, 1 << 10)
+    before = A.memory_footprint()
+    info0 = A.info()
+    x = np.random.default_rng(7).random(1 << 10)
+    y0 = h2.hmv(A, x)
+    rep = h2.compress(A, 1e-7)
+    assert rep.bytes_before == before and rep.bytes_after == A.memory_footprint() < before
+    info = A.info()
+    assert info.cpl_blocks == info0.cpl_blocks  # structure untouched
+    assert all(a <= b for a, b in zip(rep.new_ranks, rep.old_ranks))
+    assert info.ranks == rep.new_ranks
+    assert rel_err(h2.hmv(A, x), y0) <= 1e-5
+    assert 0 < rep.frobenius_error <= 1e-5
+
+
+def test_recompression_nearly_idempotent(gpu):
+    # test_compression.cpp:260-269
+    A = h2.H2Matrix.construct(2, 1 << 10)
+    r1 = h2.compress(A, 1e-7)
+    x = np.random.default_rng(11).random(1 << 10)
+    y1 = h2.hmv(A, x)
+    r2 = h2.compress(A, 1e-7)
+    assert all(a <= b for a, b in zip(r2.new_ranks, r1.new_ranks))
+    assert rel_err(h2.hmv(A, x), y1) <= 1e-6
+    assert r2.bytes_after <= r2.bytes_before
+
+
+def test_tighter_tolerance_keeps_more(gpu):
+    # test_compression.cpp:271-287
+    x = np.random.default_rng(13).random(1 << 10)
+    prev_err, prev_bytes = None, 0
+    base = h2.H2Matrix.construct(2, 1 << 10)
+    y0 = h2.hmv(base, x)
+    for eps in (1e-3, 1e-7, 1e-11):
+        A = h2.H2Matrix.construct(2, 1 << 10)
+        h2.compress(A, eps)
+        err = rel_err(h2.hmv(A, x), y0)
+        if prev_err is not None:
+            assert err <= prev_err + 1e-15
+            assert A.memory_footprint() >= prev_bytes
+        prev_err, prev_bytes = err, A.memory_footprint()
+
+
+def synthetic_rank(q=4, m=64, k=64, r=12, seed=2024) -> HostMatrix:
+    """Stored at rank k, every basis/coupling in an r-dim subspace per level
+    (the acceptance suite's synthetic_rank12, acceptance_test.cpp:205-294)."""
+    rng = np.random.default_rng(seed)
+    Q = [np.linalg.qr(rng.uniform(-1, 1, (k, r)))[0] for _ in range(q + 1)]
+    nl = 1 << q
+    leaves = [rng.uniform(-1, 1, (m, r)) @ Q[q].T for _ in range(nl)]
+    trs = []
+    for l in range(1, q + 1):
+        for _ in range(1 << l):
+            trs.append(Q[l] @ rng.uniform(-1, 1, (r, r)) @ Q[l - 1].T)
+    rp, ci, sv = [], [], []
+    for l in range(q + 1):
+        nb = 1 << l
+        if l < 2:
+            rp.extend([0] * (nb + 1))
+            continue
+        rp.extend(range(nb + 1))
+        for b in range(nb):
+            ci.append(b ^ 1)
+            sv.append(Q[l] @ rng.uniform(-1, 1, (r, r)) @ Q[l].T)
+    D = [rng.uniform(-1, 1, (m, m)) for _ in range(nl)]
+    f = lambda blocks: np.concatenate([b.T.ravel() for b in blocks]) if blocks else np.zeros(0)
+    return HostMatrix(
+        n=m << q, m=m, depth=q, ranks=np.full(q + 1, k, np.int32),
+        perm=np.arange(m << q, dtype=np.int32), leaf=f(leaves), transfer=f(trs),
+        cpl_row_ptr=np.array(rp, np.int32), cpl_col_idx=np.array(ci, np.int32),
+        cpl_values=f(sv), dense_row_ptr=np.arange(nl + 1, dtype=np.int32),
+        dense_col_idx=np.arange(nl, dtype=np.int32), dense_values=f(D))
+
+
+def test_rank12_recovery(gpu, orc):
+    # acceptance criterion c5: ranks [0, 0, 12, 12, 12], operator preserved.
+    hm = synthetic_rank()
+    O = orc.from_host(hm)
+    x = np.random.default_rng(1).random(hm.n)
+    y0 = O.hmv(x)
+    ro = O.compress(1e-8)
+    A = h2.H2Matrix.from_host(hm)
+    rep = h2.compress(A, 1e-8)
+    assert ro["new_ranks"] == [0, 0, 12, 12, 12]
+    assert rep.new_ranks == [0, 0, 12, 12, 12]
+    assert rel_err(h2.hmv(A, x), y0) <= 1e-12
+
+
+def test_compress_errors(gpu):
+    A = h2.H2Matrix.construct(2, 1 << 10)
+    with pytest.raises(h2.H2bInvalidArgument, match="eps must be non-negative"):
+        h2.compress(A, -1.0)
