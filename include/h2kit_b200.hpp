@@ -1,0 +1,270 @@
+// h2kit_b200.hpp — header-only C++ drop-in for the reference h2kit hot path.
+//
+// Include it next to the reference headers (it needs h2kit/compression.hpp,
+// h2kit/hmv.hpp from /root/reference/proj/include) and link libh2b.so.  It
+// re-exposes the reference's own signatures in namespace h2kit_b200, so a
+// caller switches by changing the namespace qualifier:
+//
+//   h2kit::hmv(A, x, y, alpha, beta, ctx)   ->  h2kit_b200::hmv(A, x, y, alpha, beta, ctx)
+//        (include/h2kit/hmv.hpp:175-188)
+//   h2kit::hmv(A, x, y, alpha, beta)        ->  h2kit_b200::hmv(A, x, y, alpha, beta)   (:190-194)
+//   h2kit::upsweep / tree_multiply / downsweep  (:79-157)
+//   h2kit::compress(A, eps)                 ->  h2kit_b200::compress(A, eps)
+//        (include/h2kit/compression.hpp:466-551)
+//   h2kit::orthogonalize_basis(B)           ->  h2kit_b200::orthogonalize_basis(A)   (:69-126)
+//
+// Semantics match the reference: alpha/beta (beta == 0 never reads y), x/y
+// in original point order, compress() mutates A in place and returns a
+// CompressionReport (device-measured times, reference-model flops), and
+// invalid arguments throw std::invalid_argument with the reference's message.
+//
+// Device residency: the first call on a matrix uploads it once into HBM and
+// keeps the device mirror in a per-process cache keyed by the H2Matrix
+// address (the role HmvContext plays on the CPU).  compress() refreshes the
+// host object from the device.  A caller that mutates A by other means must
+// call h2kit_b200::invalidate(A).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "h2b.h"
+#include "h2kit/compression.hpp"
+#include "h2kit/hmv.hpp"
+
+namespace h2kit_b200 {
+
+using h2kit::BasisTree;
+using h2kit::BSRLayer;
+using h2kit::CompressionReport;
+using h2kit::H2Matrix;
+using h2kit::HmvContext;
+using h2kit::index_t;
+using h2kit::LevelVectors;
+using h2kit::MatrixTree;
+
+namespace detail {
+
+inline void check(h2b_status st) {
+  if (st == H2B_OK) return;
+  const std::string msg = h2b_last_error();
+  if (st == H2B_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error("h2b: " + msg);
+}
+
+// Flattened export-layout copy of a reference H2Matrix<double>.
+struct Flat {
+  std::vector<int32_t> ranks, rp, ci, drp, dci;
+  std::vector<double> transfer, values;
+  h2b_matrix_desc desc{};
+};
+
+inline std::unique_ptr<Flat> flatten(const H2Matrix<double>& A) {
+  if (!A.symmetric) throw std::invalid_argument("h2kit_b200: only symmetric H2 matrices are supported");
+  auto f = std::make_unique<Flat>();
+  const int q = A.depth();
+  f->ranks.assign(A.row_basis.ranks.begin(), A.row_basis.ranks.end());
+  for (int l = 1; l <= q; ++l)
+    f->transfer.insert(f->transfer.end(), A.row_basis.transfer[l].begin(), A.row_basis.transfer[l].end());
+  for (int l = 0; l <= q; ++l) {
+    const auto& L = A.coupling.levels[l];
+    if (L.row_ptr.empty())
+      f->rp.insert(f->rp.end(), size_t(index_t(1) << l) + 1, 0);
+    else
+      f->rp.insert(f->rp.end(), L.row_ptr.begin(), L.row_ptr.end());
+    f->ci.insert(f->ci.end(), L.col_idx.begin(), L.col_idx.end());
+    f->values.insert(f->values.end(), L.values.begin(), L.values.end());
+  }
+  h2b_matrix_desc& d = f->desc;
+  d.n = A.n;
+  d.m = A.m;
+  d.depth = q;
+  d.symmetric = 1;
+  d.perm = A.perm.data();
+  d.ranks = f->ranks.data();
+  d.leaf = A.row_basis.leaf_pool.data();
+  d.transfer = f->transfer.data();
+  d.cpl_row_ptr = f->rp.data();
+  d.cpl_col_idx = f->ci.data();
+  d.cpl_values = f->values.data();
+  d.dense_row_ptr = A.dense.row_ptr.data();
+  d.dense_col_idx = A.dense.col_idx.data();
+  d.dense_values = A.dense.values.data();
+  return f;
+}
+
+class Mirror {
+ public:
+  explicit Mirror(const H2Matrix<double>& A, int device = 0) {
+    auto f = flatten(A);
+    check(h2b_matrix_create(&f->desc, device, &h_));
+  }
+  ~Mirror() {
+    if (h_) h2b_matrix_destroy(h_);
+  }
+  Mirror(const Mirror&) = delete;
+  Mirror& operator=(const Mirror&) = delete;
+  h2b_matrix* get() const { return h_; }
+
+ private:
+  h2b_matrix* h_ = nullptr;
+};
+
+inline std::mutex& cache_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<const void*, std::shared_ptr<Mirror>>& cache() {
+  static std::map<const void*, std::shared_ptr<Mirror>> c;
+  return c;
+}
+
+inline std::shared_ptr<Mirror> mirror_of(const H2Matrix<double>& A) {
+  std::lock_guard<std::mutex> g(cache_mutex());
+  auto& c = cache();
+  auto it = c.find(&A);
+  if (it != c.end()) return it->second;
+  auto m = std::make_shared<Mirror>(A);
+  c[&A] = m;
+  return m;
+}
+
+// Copy the device matrix back into the reference object (after compress).
+inline void pull(h2b_matrix* h, H2Matrix<double>& A) {
+  h2b_matrix_info inf{};
+  check(h2b_matrix_info_get(h, &inf));
+  const int q = inf.depth;
+  auto& B = A.row_basis;
+  B.ranks.assign(inf.ranks, inf.ranks + q + 1);
+  std::vector<double> tr;
+  size_t ntr = 0, nsv = 0;
+  for (int l = 1; l <= q; ++l) ntr += (size_t(1) << l) * inf.ranks[l] * inf.ranks[l - 1];
+  for (int l = 0; l <= q; ++l) nsv += size_t(inf.cpl_blocks[l]) * inf.ranks[l] * inf.ranks[l];
+  B.leaf_pool.assign((size_t(1) << q) * inf.m * inf.ranks[q], 0.0);
+  tr.resize(ntr);
+  std::vector<double> sv(nsv);
+  check(h2b_matrix_export(h, nullptr, B.leaf_pool.data(), tr.data(), nullptr, nullptr, sv.data(),
+                          nullptr, nullptr, nullptr));
+  size_t o = 0;
+  for (int l = 1; l <= q; ++l) {
+    const size_t sz = (size_t(1) << l) * inf.ranks[l] * inf.ranks[l - 1];
+    B.transfer[l].assign(tr.begin() + o, tr.begin() + o + sz);
+    o += sz;
+  }
+  o = 0;
+  for (int l = 0; l <= q; ++l) {
+    auto& L = A.coupling.levels[l];
+    const size_t sz = size_t(inf.cpl_blocks[l]) * inf.ranks[l] * inf.ranks[l];
+    L.values.assign(sv.begin() + o, sv.begin() + o + sz);
+    L.brows = L.bcols = inf.ranks[l];
+    o += sz;
+  }
+}
+
+}  // namespace detail
+
+// Drop the cached device mirror of A (call after mutating A on the host).
+inline void invalidate(const H2Matrix<double>& A) {
+  std::lock_guard<std::mutex> g(detail::cache_mutex());
+  detail::cache().erase(&A);
+}
+
+// y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-188).  ctx is accepted for
+// signature compatibility; the device workspace lives in the mirror.
+inline void hmv(const H2Matrix<double>& A, const double* x, double* y, double alpha, double beta,
+                HmvContext<double>& ctx) {
+  (void)ctx;
+  auto m = detail::mirror_of(A);
+  detail::check(h2b_hmv(m->get(), x, y, alpha, beta, H2B_PTR_AUTO, nullptr));
+}
+
+inline void hmv(const H2Matrix<double>& A, const double* x, double* y, double alpha = 1.0,
+                double beta = 0.0) {
+  auto m = detail::mirror_of(A);
+  detail::check(h2b_hmv(m->get(), x, y, alpha, beta, H2B_PTR_AUTO, nullptr));
+}
+
+// Phase entry points (hmv.hpp:79-157) on the mirror of A; node vectors use
+// the reference's LevelVectors layout.
+inline void upsweep(const H2Matrix<double>& A, const double* xc, LevelVectors<double>& xhat) {
+  auto m = detail::mirror_of(A);
+  xhat.resize(A.col_basis());
+  std::vector<double> flat;
+  for (auto& p : xhat.pool) flat.insert(flat.end(), p.size(), 0.0);
+  detail::check(h2b_upsweep(m->get(), xc, flat.data(), H2B_PTR_HOST));
+  size_t o = 0;
+  for (auto& p : xhat.pool) {
+    std::copy(flat.begin() + o, flat.begin() + o + p.size(), p.begin());
+    o += p.size();
+  }
+}
+
+inline void tree_multiply(const H2Matrix<double>& A, const LevelVectors<double>& xhat,
+                          LevelVectors<double>& yhat) {
+  auto m = detail::mirror_of(A);
+  std::vector<double> xf, yf;
+  for (auto& p : xhat.pool) xf.insert(xf.end(), p.begin(), p.end());
+  yf.assign(xf.size(), 0.0);
+  detail::check(h2b_tree_multiply(m->get(), xf.data(), yf.data(), H2B_PTR_HOST));
+  yhat.resize(A.row_basis);
+  size_t o = 0;
+  for (auto& p : yhat.pool) {
+    std::copy(yf.begin() + o, yf.begin() + o + p.size(), p.begin());
+    o += p.size();
+  }
+}
+
+inline void downsweep(const H2Matrix<double>& A, LevelVectors<double>& yhat, double* yc) {
+  auto m = detail::mirror_of(A);
+  std::vector<double> yf;
+  for (auto& p : yhat.pool) yf.insert(yf.end(), p.begin(), p.end());
+  detail::check(h2b_downsweep(m->get(), yf.data(), yc, H2B_PTR_HOST));
+}
+
+// compress(A, eps) (compression.hpp:466-551): runs on the device mirror and
+// writes the recompressed bases / coupling blocks back into A.
+inline CompressionReport compress(H2Matrix<double>& A, double eps) {
+  auto m = detail::mirror_of(A);
+  h2b_compress_report r{};
+  detail::check(h2b_compress(m->get(), eps, &r));
+  detail::pull(m->get(), A);
+  CompressionReport rep;
+  const int q = A.depth();
+  rep.old_ranks.assign(r.old_ranks, r.old_ranks + q + 1);
+  rep.new_ranks.assign(r.new_ranks, r.new_ranks + q + 1);
+  rep.bytes_before = r.bytes_before;
+  rep.bytes_after = r.bytes_after;
+  rep.frobenius_error = r.frobenius_error;
+  rep.frobenius_norm = r.frobenius_norm;
+  rep.time_orthogonalize_ms = r.time_orthogonalize_ms;
+  rep.time_project_orth_ms = r.time_project_orth_ms;
+  rep.time_weights_ms = r.time_weights_ms;
+  rep.time_truncate_ms = r.time_truncate_ms;
+  rep.time_project_trunc_ms = r.time_project_trunc_ms;
+  rep.flops_orthogonalize = r.flops_orthogonalize;
+  rep.flops_project_orth = r.flops_project_orth;
+  rep.flops_weights = r.flops_weights;
+  rep.flops_truncate = r.flops_truncate;
+  rep.flops_project_trunc = r.flops_project_trunc;
+  return rep;
+}
+
+// orthogonalize_basis (compression.hpp:69-126) on A's basis, in place; the
+// coupling blocks are NOT projected (same contract as the reference).
+inline std::vector<double> orthogonalize_basis(H2Matrix<double>& A) {
+  auto m = detail::mirror_of(A);
+  size_t nt = 0;
+  for (int l = 0; l <= A.depth(); ++l)
+    nt += (size_t(1) << l) * A.row_basis.ranks[l] * A.row_basis.ranks[l];
+  std::vector<double> T(nt);
+  detail::check(h2b_orthogonalize(m->get(), T.data()));
+  detail::pull(m->get(), A);
+  return T;
+}
+
+}  // namespace h2kit_b200
