@@ -20,12 +20,14 @@
 //
 // Device residency: the first call on a matrix uploads it once into HBM and
 // keeps the device mirror in a per-process cache keyed by the H2Matrix
-// address (the role HmvContext plays on the CPU).  compress() refreshes the
-// host object from the device.  A caller that mutates A by other means must
-// call h2kit_b200::invalidate(A).
+// address plus a fingerprint (shape, pool addresses, sampled values) -- the
+// role HmvContext plays on the CPU.  compress() refreshes the host object
+// from the device.  A caller that mutates unsampled entries of A in place
+// must call h2kit_b200::invalidate(A).
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -119,19 +121,59 @@ inline std::mutex& cache_mutex() {
   static std::mutex m;
   return m;
 }
-inline std::map<const void*, std::shared_ptr<Mirror>>& cache() {
-  static std::map<const void*, std::shared_ptr<Mirror>> c;
+
+// Fingerprint of a matrix: shape, pool sizes and addresses, and a sample of
+// values, so a different matrix constructed at a recycled address (or a
+// host-side mutation of sampled entries) never hits a stale mirror.
+inline uint64_t fingerprint(const H2Matrix<double>& A) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+  auto sample = [&](const std::vector<double>& v) {
+    mix(v.size());
+    mix(reinterpret_cast<uintptr_t>(v.data()));
+    const size_t step = v.size() / 61 + 1;
+    for (size_t i = 0; i < v.size(); i += step) {
+      uint64_t b;
+      std::memcpy(&b, &v[i], sizeof(b));
+      mix(b);
+    }
+  };
+  mix(uint64_t(A.n));
+  mix(uint64_t(A.m));
+  mix(uint64_t(A.depth()));
+  for (int r : A.row_basis.ranks) mix(uint64_t(r));
+  sample(A.row_basis.leaf_pool);
+  for (const auto& t : A.row_basis.transfer) sample(t);
+  for (const auto& L : A.coupling.levels) sample(L.values);
+  sample(A.dense.values);
+  return h;
+}
+
+struct Entry {
+  uint64_t fp;
+  std::shared_ptr<Mirror> m;
+};
+inline std::map<const void*, Entry>& cache() {
+  static std::map<const void*, Entry> c;
   return c;
 }
 
 inline std::shared_ptr<Mirror> mirror_of(const H2Matrix<double>& A) {
+  const uint64_t fp = fingerprint(A);
   std::lock_guard<std::mutex> g(cache_mutex());
   auto& c = cache();
   auto it = c.find(&A);
-  if (it != c.end()) return it->second;
+  if (it != c.end() && it->second.fp == fp) return it->second.m;
   auto m = std::make_shared<Mirror>(A);
-  c[&A] = m;
+  c[&A] = Entry{fp, m};
   return m;
+}
+
+// Re-key the cache entry of A after A was refreshed from its mirror.
+inline void rekey(const H2Matrix<double>& A, const std::shared_ptr<Mirror>& m) {
+  const uint64_t fp = fingerprint(A);
+  std::lock_guard<std::mutex> g(cache_mutex());
+  cache()[&A] = Entry{fp, m};
 }
 
 // Copy the device matrix back into the reference object (after compress).
@@ -233,6 +275,7 @@ inline CompressionReport compress(H2Matrix<double>& A, double eps) {
   h2b_compress_report r{};
   detail::check(h2b_compress(m->get(), eps, &r));
   detail::pull(m->get(), A);
+  detail::rekey(A, m);
   CompressionReport rep;
   const int q = A.depth();
   rep.old_ranks.assign(r.old_ranks, r.old_ranks + q + 1);
@@ -264,6 +307,7 @@ inline std::vector<double> orthogonalize_basis(H2Matrix<double>& A) {
   std::vector<double> T(nt);
   detail::check(h2b_orthogonalize(m->get(), T.data()));
   detail::pull(m->get(), A);
+  detail::rekey(A, m);
   return T;
 }
 

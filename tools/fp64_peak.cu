@@ -1,0 +1,66 @@
+// FP64 throughput microbenchmark on the B200: DFMA (CUDA cores) vs DMMA
+// (mma.sync.m8n8k4.f64 tensor path).  Prints TFLOP/s for each.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void k_dfma(double* out, int iters) {
+  double a[8], b = 1.0000001, c = 0.9999999;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.0) out[0] = s;
+}
+
+__global__ void k_dmma(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 0.999;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[0] = s;
+}
+
+int main() {
+  double* d;
+  cudaMalloc(&d, 8);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int iters = 20000;
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = sms * 8, threads = 256;
+    cudaEventRecord(a);
+    k_dfma<<<blocks, threads>>>(d, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double fl = 2.0 * 8 * iters * double(blocks) * threads;
+    printf("DFMA: %.2f TFLOP/s\n", fl / ms / 1e9);
+    cudaEventRecord(a);
+    k_dmma<<<blocks, threads>>>(d, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    // each warp-level m8n8k4 = 8*8*4 FMAs = 512 FMA = 1024 flops
+    const double fm = 1024.0 * 8 * iters * double(blocks) * (threads / 32);
+    printf("DMMA m8n8k4: %.2f TFLOP/s\n", fm / ms / 1e9);
+  }
+  return 0;
+}
