@@ -181,6 +181,43 @@ def cpu_reference_sample(steps: int | None = None, budget_s: float = 20.0):
                       f"host construct {build_s:.1f} s"}
 
 
+FP64_PEAK_TFLOPS = 74.3  # DMMA m8n8k4 measured on this pool's B200 (tools/fp64_peak.cu); DFMA 36.4
+COMPRESS_CFG = dict(dim=3, n=1 << 20, grid_order=4, eps=1e-6)
+
+
+def compression_run(h2, torch, device, reps):
+    """compress() of the C3 matrix (3D exponential covariance n=2^20, rank 64,
+    eps 1e-6): model GFLOP/s = reference analytic flops (flops.hpp) / device time."""
+    warm = h2.H2Matrix.construct(2, 1 << 14, device=device)
+    h2.compress(warm, 1e-7)
+    warm.close()
+    times, rep = [], None
+    for _ in range(max(1, reps)):
+        A = h2.H2Matrix.construct(COMPRESS_CFG["dim"], COMPRESS_CFG["n"],
+                                  grid_order=COMPRESS_CFG["grid_order"], device=device)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = h2.compress(A, COMPRESS_CFG["eps"])
+        torch.cuda.synchronize()
+        times.append((time.perf_counter() - t0) * 1e3)
+        dev_ms = rep.total_ms()
+        A.close()
+    dev_ms = rep.total_ms()
+    gflops = rep.total_flops() / (dev_ms * 1e-3) / 1e9
+    return {"config": "3D exponential covariance n=2^20, leaf 64, order 4 (rank 64), eps 1e-6 (C3)",
+            "ms": round(dev_ms, 1), "wall_ms": round(min(times), 1), "reps": len(times),
+            "model_flops": rep.total_flops(), "gflops": round(gflops, 1),
+            "pct_fp64_peak": round(100 * gflops / 1e3 / FP64_PEAK_TFLOPS, 2),
+            "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+            "phase_ms": {"orthogonalize": round(rep.time_orthogonalize_ms, 1),
+                         "project_orth": round(rep.time_project_orth_ms, 1),
+                         "weights": round(rep.time_weights_ms, 1),
+                         "truncate": round(rep.time_truncate_ms, 1),
+                         "project_trunc": round(rep.time_project_trunc_ms, 1)},
+            "new_ranks": rep.new_ranks, "frobenius_error": rep.frobenius_error,
+            "bytes": [rep.bytes_before, rep.bytes_after]}
+
+
 def run_reference(args):
     world, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
     if rank != 0:
@@ -207,6 +244,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=WORKLOAD["n"], help="override n (testing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compress", action="store_true")
+    ap.add_argument("--compress-reps", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -289,6 +328,14 @@ def main():
     # correctness spot check of the e2e result against the device result
     assert np.allclose(yn, yt.cpu().numpy(), rtol=1e-13, atol=0)
 
+    # ---- compression GFLOP/s (metric's second half): C3, 3D n=2^20 k=64, eps 1e-6 ----
+    A.close()
+    del A
+    torch.cuda.synchronize()
+    comp = None
+    if not args.no_compress:
+        comp = compression_run(h2, torch, local, args.compress_reps)
+
     if rank != 0:
         return
     peak, peak_src = load_peaks()
@@ -333,6 +380,7 @@ def main():
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
+        "compression": comp,
     }
     print(json.dumps(line), flush=True)
 
