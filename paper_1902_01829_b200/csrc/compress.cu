@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
   const int64_t fs = int64_t(ldf) * kp;
   for (int ci = 0; ci < 2; ++ci) {
     const int64_t c = 2 * p + ci;
-    cta::gemm<false, false>(Z + ci * kc, zr, Tl + c * int64_t(kc) * kc, kc, F + c * fs, ldf, kc, kp, kc);
+    cta::gemm_tc<false, false>(Z + ci * kc, zr, Tl + c * int64_t(kc) * kc, kc, F + c * fs, ldf, kc, kp, kc);
   }
   __syncthreads();
   cta::householder(Z, zr, zr, kp, tau, red);
@@ -110,22 +110,23 @@ __global__ void __launch_bounds__(kThreads) k_project(const __grid_constant__ Pr
   const ProjRow pr = rows[blockIdx.x];
   const ProjLevel& L = P.L[pr.level];
   const int ro = L.ro, rn = L.rn;
-  double* Tr = sm;              // rn x ro
-  double* Sb = Tr + rn * ro;    // ro x ro  (then T_col)
-  double* TS = Sb + ro * ro;    // rn x ro
-  cta::copy_block(Tr, rn, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
+  const int lr = cta::sld(rn), lo = cta::sld(ro);
+  double* Tr = sm;              // rn x ro   (ld lr)
+  double* Sb = Tr + lr * ro;    // ro x ro   (ld lo), then T_col (rn x ro, ld lr <= lo)
+  double* TS = Sb + lo * ro;    // rn x ro   (ld lr)
+  cta::copy_block(Tr, lr, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
   const int b0 = L.rp[pr.row], b1 = L.rp[pr.row + 1];
   for (int b = b0; b < b1; ++b) {
     __syncthreads();
-    cta::copy_block(Sb, ro, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
+    cta::copy_block(Sb, lo, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
     __syncthreads();
-    cta::gemm<false, false>(TS, rn, Tr, rn, Sb, ro, rn, ro, ro);
+    cta::gemm_tc<false, false>(TS, lr, Tr, lr, Sb, lo, rn, ro, ro);
     __syncthreads();
     const int c = L.ci[b];
-    cta::copy_block(Sb, rn, L.T + int64_t(c) * rn * ro, rn, rn, ro);
+    cta::copy_block(Sb, lr, L.T + int64_t(c) * rn * ro, rn, rn, ro);
     __syncthreads();
     double* out = L.out + int64_t(b) * L.ld_new * rn;
-    cta::gemm<false, true>(out, L.ld_new, TS, rn, Sb, rn, rn, rn, ro);
+    cta::gemm_tc<false, true>(out, L.ld_new, TS, lr, Sb, lr, rn, rn, ro);
     if (L.ld_new > rn)
       for (int j = threadIdx.x; j < rn; j += kThreads) out[rn + int64_t(j) * L.ld_new] = 0.0;
   }
@@ -141,53 +142,109 @@ __global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restr
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// R^l_r = R-factor of [R^{l-1}_{r/2} E_r^T ; S_rb^T ...] by streaming
-// Householder TSQR over chunks of <= kChunk coupling blocks (no padding).
-constexpr int kChunk = 2;
-__global__ void __launch_bounds__(kThreads) k_weights(const double* __restrict__ E, int lde, int kc,
-                                                      int kp, const double* __restrict__ Rpar,
-                                                      const int32_t* __restrict__ rp,
-                                                      const int32_t* __restrict__ ci,
-                                                      const double* __restrict__ S, int lds,
-                                                      double* __restrict__ Rout) {
+// R^l_r = R-factor of [R^{l-1}_{r/2} E_r^T ; S_rb^T ...] (compression.hpp:213-256)
+// by streaming TSQR over the UNPADDED stack.  The running R (kc x kc, upper
+// triangular) stays in smem; each chunk of <= kChunkRows stack rows lives in
+// registers -- thread (warp w, lane t) owns column c = 8w + t/4 and rows
+// g + 4r (g = t%4) -- and [R; chunk] is re-triangularised by a structured
+// Householder pass whose reflectors touch one row of R plus the chunk.
+constexpr int kChunkRows = 128;
+constexpr int kRowsPerThread = kChunkRows / 4;
+__global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restrict__ E, int lde,
+                                                         int kc, int kp,
+                                                         const double* __restrict__ Rpar,
+                                                         const int32_t* __restrict__ rp,
+                                                         const double* __restrict__ S, int lds,
+                                                         double* __restrict__ Rout) {
   extern __shared__ double sm[];
-  const int ldb = kc + (kp > kChunk * kc ? kp : kChunk * kc);  // Racc + one chunk
-  double* B = sm;                                             // ldb x kc
-  double* tau = B + ldb * kc;
-  double* red = tau + 64;
-  int* flip = reinterpret_cast<int*>(red + 16);
-  const int64_t r = blockIdx.x;
-  cta::zero_block(B, ldb, ldb, kc);
-  __syncthreads();
-  int rows = kc;  // rows [0, kc) hold the running R factor (zero initially)
-  if (kp > 0) {   // parent contribution R_p E_r^T (kp x kc)
-    cta::gemm<false, true>(B + kc, ldb, Rpar + (r >> 1) * int64_t(kp) * kp, kp,
-                           E + r * int64_t(lde) * kp, lde, kp, kc, kp);
-    rows += kp;
-  }
-  const int b1 = rp[r + 1];
-  int b = rp[r];
-  for (;;) {
-    for (; b < b1 && rows + kc <= ldb; ++b, rows += kc) {  // append S_rb^T
+  const int ldr = cta::sld(kc);
+  const int ldst = cta::sld(kChunkRows);
+  double* Rs = sm;                       // ldr x kc, running R
+  double* st = Rs + ldr * kc;            // ldst x kc chunk staging
+  double* vb = st + ldst * kc;           // kChunkRows reflector entries
+  double* misc = vb + kChunkRows;        // [0] = tau, [1..16] red
+  int* flip = reinterpret_cast<int*>(misc + 32);
+  const int lane = cta::lane();
+  const int c = cta::warp() * 8 + (lane >> 2);  // owned column
+  const int g = lane & 3;                        // row group
+  const bool own = c < kc;
+  const int64_t node = blockIdx.x;
+  cta::zero_block(Rs, ldr, kc, kc);
+  const int b1 = rp[node + 1];
+  int b = rp[node];
+  bool parent = kp > 0;
+  const int per_chunk_blocks = kChunkRows / kc;
+  while (parent || b < b1) {
+    // ---- stage one chunk: [parent rows][blocks ...] ----
+    int rows = 0;
+    __syncthreads();
+    if (parent) {
+      cta::gemm_tc<false, true>(st, ldst, Rpar + (node >> 1) * int64_t(kp) * kp, kp,
+                                E + node * int64_t(lde) * kp, lde, kp, kc, kp);
+      rows = kp;
+      parent = false;
+    }
+    for (int nb = 0; b < b1 && rows + kc <= kChunkRows && nb < per_chunk_blocks; ++b, ++nb) {
       const double* Sb = S + int64_t(b) * lds * kc;
       for (int e = threadIdx.x; e < kc * kc; e += kThreads) {
-        const int j = e / kc, i = e - j * kc;  // S(i, j) -> B(rows + j, i)
-        B[rows + j + i * ldb] = Sb[i + int64_t(j) * lds];
+        const int j = e / kc, i = e - j * kc;  // S(i, j) -> stack row rows + j, column i
+        st[rows + j + i * ldst] = Sb[i + int64_t(j) * lds];
       }
+      rows += kc;
     }
     __syncthreads();
-    if (rows > kc) {
-      cta::householder(B, ldb, rows, kc, tau, red);
-      for (int e = threadIdx.x; e < rows * kc; e += kThreads) {  // keep R only
-        const int j = e / rows, i = e - j * rows;
-        if (i > j) B[i + j * ldb] = 0.0;
+    double B[kRowsPerThread];
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) {
+      const int i = g + 4 * r;
+      B[r] = (own && i < rows) ? st[i + c * ldst] : 0.0;
+    }
+    // ---- structured Householder on [R; B] ----
+    for (int j = 0; j < kc; ++j) {
+      if (c == j) {
+        double sq = 0.0;
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) sq += B[r] * B[r];
+        sq += __shfl_xor_sync(0xfu << (lane & ~3), sq, 1, 4);
+        sq += __shfl_xor_sync(0xfu << (lane & ~3), sq, 2, 4);
+        const double al = Rs[j + j * ldr];
+        const double nx = sqrt(al * al + sq);
+        double tj = 0.0, sc = 0.0, be = al;
+        if (nx != 0.0) {
+          be = al >= 0.0 ? -nx : nx;
+          tj = (be - al) / be;
+          sc = 1.0 / (al - be);
+        }
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) {
+          const int i = g + 4 * r;
+          if (i < kChunkRows) vb[i] = B[r] * sc;
+          B[r] = 0.0;  // below the new diagonal: the reflector, not part of R
+        }
+        if (g == 0) {
+          misc[0] = tj;
+          Rs[j + j * ldr] = be;
+        }
       }
       __syncthreads();
-      rows = kc;
+      const double tj = misc[0];
+      if (own && c > j && tj != 0.0) {
+        double w = 0.0;
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) w += vb[g + 4 * r] * B[r];
+        w += __shfl_xor_sync(0xfu << (lane & ~3), w, 1, 4);
+        w += __shfl_xor_sync(0xfu << (lane & ~3), w, 2, 4);
+        const double d = (Rs[j + c * ldr] + w) * tj;
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) B[r] -= vb[g + 4 * r] * d;
+        __syncwarp(0xfu << (lane & ~3));
+        if (g == 0) Rs[j + c * ldr] -= d;
+      }
+      __syncthreads();
     }
-    if (b >= b1) break;
   }
-  cta::extract_r(B, ldb, kc, Rout + r * int64_t(kc) * kc, kc, flip);
+  __syncthreads();
+  cta::extract_r(Rs, ldr, kc, Rout + node * int64_t(kc) * kc, kc, flip);
 }
 
 // One-sided Jacobi SVD of W (rows x cols, smem, ld = rows) into Uout (global,
@@ -261,7 +318,7 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_svd(const double* __res
   int* ord = reinterpret_cast<int*>(red + 16);
   int* flag = ord + 128;
   const int64_t i = blockIdx.x;
-  cta::gemm<false, true>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
+  cta::gemm_tc<false, true>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
   __syncthreads();
   check_finite(W, m * k, bad);
   double* sg = sig_out + i * s;
@@ -280,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_apply(const double* __r
   const int64_t i = blockIdx.x;
   const double* Q = Uq + i * int64_t(m) * s;
   if (kt > 0)
-    cta::gemm<true, false>(Tq + i * int64_t(kt) * k, kt, Q, m, leaf + i * int64_t(ldm) * k, ldm, kt, k, m);
+    cta::gemm_tc<true, false>(Tq + i * int64_t(kt) * k, kt, Q, m, leaf + i * int64_t(ldm) * k, ldm, kt, k, m);
   double* nl = newleaf + i * int64_t(ldn) * kt;
   for (int e = threadIdx.x; e < ldn * kt; e += kThreads) {
     const int j = e / ldn, r = e - j * ldn;
@@ -313,11 +370,11 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_svd(
   const int64_t es = int64_t(lde) * kp;
   for (int ci = 0; ci < 2; ++ci) {
     const int64_t c = 2 * p + ci;
-    cta::gemm<false, false>(Z + ci * ktc, zr, Tt + c * int64_t(ktc) * kc, ktc, E + c * es, lde, ktc, kp, kc);
+    cta::gemm_tc<false, false>(Z + ci * ktc, zr, Tt + c * int64_t(ktc) * kc, ktc, E + c * es, lde, ktc, kp, kc);
   }
   __syncthreads();
   cta::copy_block(Zout + p * int64_t(zr) * kp, zr, Z, zr, zr, kp);
-  cta::gemm<false, true>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
+  cta::gemm_tc<false, true>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
   __syncthreads();
   check_finite(W, zr * kp, bad);
   const int rank = svd_to(W, zr, kp, work, Uout + p * int64_t(zr) * s, zr, sig_out + p * s, eps, nrm,
@@ -334,7 +391,7 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_apply(
   const int64_t p = blockIdx.x;
   const double* Q = Uin + p * int64_t(zr) * s;
   if (ktp > 0)
-    cta::gemm<true, false>(Tp + p * int64_t(ktp) * kp, ktp, Q, zr, Zin + p * int64_t(zr) * kp, zr, ktp,
+    cta::gemm_tc<true, false>(Tp + p * int64_t(ktp) * kp, ktp, Q, zr, Zin + p * int64_t(zr) * kp, zr, ktp,
                            kp, zr);
   for (int ci = 0; ci < 2; ++ci) {
     double* dst = Enew + (2 * p + ci) * int64_t(ldn) * ktp;
@@ -471,7 +528,7 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     if (rn == 0) continue;
     for (int64_t r = 0; r < L.rows; ++r)
       if (L.h_rp[r + 1] > L.h_rp[r]) rows.push_back({l, int32_t(r)});
-    smax = std::max(smax, (size_t(rn) * ro * 2 + size_t(ro) * ro) * sizeof(double));
+    smax = std::max(smax, (size_t(cta::sld(rn)) * ro * 2 + size_t(cta::sld(ro)) * ro) * sizeof(double));
   }
   if (!rows.empty()) {
     check_smem(smax, "project_coupling");
@@ -518,12 +575,12 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
     flops += fl.gemm(double(A.nodes(l)), kp, kc, kp) + fl.qr(double(A.nodes(l)), ld_ref, kc);
     require(ld_ref >= kc, "qr_r_only_batched: requires rows >= cols");
     if (kc == 0) continue;
-    const int ldb = kc + std::max(kp, kChunk * kc);
-    const size_t sm = (size_t(ldb) * kc + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    const size_t sm = (size_t(cta::sld(kc)) * kc + size_t(cta::sld(kChunkRows)) * kc + kChunkRows + 32) *
+                          sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "generate_weight_tree");
     set_smem(k_weights, sm);
     k_weights<<<unsigned(A.nodes(l)), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
-                                                        R.at(l - 1), L.rp, L.ci, L.val, L.ld, R.at(l));
+                                                        R.at(l - 1), L.rp, L.val, L.ld, R.at(l));
     H2B_CUDA(cudaGetLastError());
   }
 }

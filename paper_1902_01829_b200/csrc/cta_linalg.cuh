@@ -104,6 +104,65 @@ __device__ void gemm(double* C, int ldc, const double* A, int lda, const double*
     }
 }
 
+// Smallest leading dimension >= rows that is == 4 (mod 16) doubles: makes the
+// 8x4 / 4x8 DMMA fragment loads below 2-way (optimal) bank-conflicted.
+__host__ __device__ __forceinline__ int sld(int rows) { return ((rows + 11) / 16) * 16 + 4; }
+
+// FP64 tensor-core MMA (SASS DMMA.8x8x4): D(8x8) += A(8x4) B(4x8).
+// Fragments: A[lane>>2][lane&3], B[lane&3][lane>>2], C[lane>>2][2(lane&3)+{0,1}].
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// C (m x n) = op(A) (m x k) * op(B) (k x n) on the FP64 tensor cores.  Each
+// warp owns 32 x 16 output tiles (4 x 2 DMMA tiles, 16 accumulators); any
+// m, n, k (edges predicated to zero).  Operands may live in smem or global.
+template <bool TA, bool TB>
+__device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
+                        int m, int n, int k) {
+  const int t = lane();
+  const int fr = t >> 2, fk = t & 3;  // fragment row (A) / col (B), k index
+  const int mt = (m + 31) >> 5, nt = (n + 15) >> 4;
+  for (int wt = warp(); wt < mt * nt; wt += kWarps) {
+    const int i0 = (wt % mt) * 32, j0 = (wt / mt) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int p0 = 0; p0 < k; p0 += 4) {
+      const int p = p0 + fk;
+      const bool pk = p < k;
+      double a[4], b[2];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int i = i0 + 8 * x + fr;
+        a[x] = (pk && i < m) ? (TA ? A[p + i * lda] : A[i + p * lda]) : 0.0;
+      }
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const int j = j0 + 8 * y + fr;
+        b[y] = (pk && j < n) ? (TB ? B[j + p * ldb] : B[p + j * ldb]) : 0.0;
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) dmma(acc[x][y][0], acc[x][y][1], a[x], b[y]);
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int i = i0 + 8 * x + fr, j = j0 + 8 * y + 2 * fk + v;
+          if (i < m && j < n) C[i + j * ldc] = acc[x][y][v];
+        }
+  }
+}
+
 // In-place Householder factorisation (linalg.hpp:48-75): reflectors below the
 // diagonal, R on and above it; tau[cols] in smem; red: >= 9 doubles scratch.
 __device__ void householder(double* A, int lda, int rows, int cols, double* tau, double* red) {
