@@ -202,9 +202,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restric
     // ---- structured Householder on [R; B] ----
     for (int j = 0; j < kc; ++j) {
       if (c == j) {
-        double sq = 0.0;
+        double q4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) sq += B[r] * B[r];
+        for (int r = 0; r < kRowsPerThread; ++r) q4[r & 3] += B[r] * B[r];
+        double sq = (q4[0] + q4[1]) + (q4[2] + q4[3]);
         sq += __shfl_xor_sync(0xfu << (lane & ~3), sq, 1, 4);
         sq += __shfl_xor_sync(0xfu << (lane & ~3), sq, 2, 4);
         const double al = Rs[j + j * ldr];
@@ -229,9 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restric
       __syncthreads();
       const double tj = misc[0];
       if (own && c > j && tj != 0.0) {
-        double w = 0.0;
+        double w4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) w += vb[g + 4 * r] * B[r];
+        for (int r = 0; r < kRowsPerThread; ++r) w4[r & 3] += vb[g + 4 * r] * B[r];
+        double w = (w4[0] + w4[1]) + (w4[2] + w4[3]);
         w += __shfl_xor_sync(0xfu << (lane & ~3), w, 1, 4);
         w += __shfl_xor_sync(0xfu << (lane & ~3), w, 2, 4);
         const double d = (Rs[j + c * ldr] + w) * tj;

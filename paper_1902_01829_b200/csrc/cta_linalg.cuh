@@ -258,8 +258,11 @@ __device__ __forceinline__ void rr_pair(int n, int r, int s, int& p, int& q) {
 }
 
 // One-sided Jacobi on the columns of G (rows x n, n even; pad with a zero
-// column for odd counts).  flag: one int of smem.
-__device__ void jacobi(double* G, int ldg, int rows, int n, int* flag) {
+// column for odd counts).  flag: one int of smem.  A warp owns one column pair
+// per step and keeps it in registers (RPL rows per lane) between the three
+// dot products and the rotation.
+template <int RPL>
+__device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag) {
   const double tol = 2.220446049250313e-16 * 16.0;
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
@@ -270,12 +273,16 @@ __device__ void jacobi(double* G, int ldg, int rows, int n, int* flag) {
         rr_pair(n, r, s, p, q);
         double* gp = G + p * ldg;
         double* gq = G + q * ldg;
+        double u[RPL], w[RPL];
         double a = 0.0, b = 0.0, d = 0.0;
-        for (int i = lane(); i < rows; i += 32) {
-          const double u = gp[i], w = gq[i];
-          a += u * u;
-          b += w * w;
-          d += u * w;
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int i = lane() + 32 * t;
+          u[t] = i < rows ? gp[i] : 0.0;
+          w[t] = i < rows ? gq[i] : 0.0;
+          a += u[t] * u[t];
+          b += w[t] * w[t];
+          d += u[t] * w[t];
         }
         a = warp_sum(a);
         b = warp_sum(b);
@@ -286,10 +293,13 @@ __device__ void jacobi(double* G, int ldg, int rows, int n, int* flag) {
         const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
         const double cs = 1.0 / sqrt(1.0 + t * t);
         const double sn = cs * t;
-        for (int i = lane(); i < rows; i += 32) {
-          const double u = gp[i], w = gq[i];
-          gp[i] = cs * u - sn * w;
-          gq[i] = sn * u + cs * w;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) {
+          const int i = lane() + 32 * k;
+          if (i < rows) {
+            gp[i] = cs * u[k] - sn * w[k];
+            gq[i] = sn * u[k] + cs * w[k];
+          }
         }
       }
       __syncthreads();
@@ -298,6 +308,17 @@ __device__ void jacobi(double* G, int ldg, int rows, int n, int* flag) {
     __syncthreads();
   }
   __syncthreads();
+}
+
+__device__ inline void jacobi(double* G, int ldg, int rows, int n, int* flag) {
+  if (rows <= 32)
+    jacobi_t<1>(G, ldg, rows, n, flag);
+  else if (rows <= 64)
+    jacobi_t<2>(G, ldg, rows, n, flag);
+  else if (rows <= 128)
+    jacobi_t<4>(G, ldg, rows, n, flag);
+  else
+    jacobi_t<8>(G, ldg, rows, n, flag);
 }
 
 // After jacobi(): sigma[j] (descending, stable) and U (rows x s) with unit (or
