@@ -116,7 +116,13 @@ typedef struct {
   uint64_t footprint_bytes;   /* memory_footprint(A).total(): reference byte convention */
   uint64_t device_bytes;      /* HBM actually held by the handle (pools + workspace) */
   double hmv_flops;           /* reference analytic flop model of one hmv (flops.hpp) */
+  uint64_t global_footprint_bytes; /* whole matrix (== footprint_bytes unless partitioned) */
+  int32_t part_log2;          /* 2^part_log2 subtree partitions (0: whole matrix) */
+  int32_t part_index;         /* partition owned by this handle */
 } h2b_matrix_info;
+
+/* Workspace buffers of a handle (device pointers, see h2b_workspace). */
+typedef enum { H2B_WS_XHAT = 0, H2B_WS_YHAT = 1, H2B_WS_XC = 2, H2B_WS_PERM = 3 } h2b_workspace_id;
 
 /* compress() report (CompressionReport, compression.hpp:422-441). Times are
  * device-measured (CUDA events); flops follow the reference analytic model. */
@@ -172,6 +178,24 @@ H2B_API h2b_status h2b_compress(h2b_matrix* A, double eps, h2b_compress_report* 
 /* Orthogonalize only (in place); projection tree written to t_out (host,
  * level-concatenated ranks[l]^2 per node) when non-NULL. */
 H2B_API h2b_status h2b_orthogonalize(h2b_matrix* A, double* t_out);
+
+/* ---- subtree-partitioned multi-GPU mat-vec ----
+ * nparts = 2^s GPUs; partition `part` owns the leaves [part n/nparts, (part+1) n/nparts)
+ * in cluster order, the basis nodes and coupling/dense block rows of its top-level
+ * subtree at levels >= s; levels < s (and the transfers up to level s) are
+ * replicated.  One mat-vec on every rank:
+ *   h2b_part_upsweep(A, x)           x: full x (original order, device)
+ *   all-gather x^ at levels >= s     (caller: NCCL; the owned slice of level l is
+ *                                     nodes [part 2^(l-s), (part+1) 2^(l-s)) of the
+ *                                     H2B_WS_XHAT buffer, level-concatenated)
+ *   h2b_part_finish(A, y_slice)      y_slice: n/nparts doubles, cluster order
+ *   all-gather y_slice; y[perm[t]] = alpha y_cluster[t] + beta y[perm[t]]. */
+H2B_API h2b_status h2b_matrix_build_part(const h2b_build_config* cfg, int device, int nparts,
+                                         int part, h2b_matrix** out);
+/* Device pointer + element count of a workspace buffer (double, PERM: int32). */
+H2B_API h2b_status h2b_workspace(h2b_matrix* A, int which, void** ptr, int64_t* count);
+H2B_API h2b_status h2b_part_upsweep(h2b_matrix* A, const double* x, void* stream);
+H2B_API h2b_status h2b_part_finish(h2b_matrix* A, double* y_slice, void* stream);
 
 /* Per-phase device time of the h2b_hmv calls made since phase timing was
  * enabled or last read, averaged per call (ms; CUDA events recorded on the

@@ -20,6 +20,8 @@ H2B_NO_DEVICE = 5
 H2B_INTERNAL = 6
 
 PTR_AUTO, PTR_HOST, PTR_DEVICE = 0, 1, 2
+WS_XHAT, WS_YHAT, WS_XC, WS_PERM = 0, 1, 2, 3
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
 
 
 class H2bError(RuntimeError):
@@ -55,7 +57,9 @@ class MatrixInfo(C.Structure):
                 ("ranks", C.c_int32 * 32), ("cpl_blocks", C.c_int64 * 32),
                 ("cpl_max_row", C.c_int32 * 32), ("dense_blocks", C.c_int64),
                 ("dense_max_row", C.c_int32), ("footprint_bytes", C.c_uint64),
-                ("device_bytes", C.c_uint64), ("hmv_flops", C.c_double)]
+                ("device_bytes", C.c_uint64), ("hmv_flops", C.c_double),
+                ("global_footprint_bytes", C.c_uint64), ("part_log2", C.c_int32),
+                ("part_index", C.c_int32)]
 
 
 class CompressReport(C.Structure):
@@ -91,6 +95,11 @@ _SIGS = {
     "h2b_compress": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(CompressReport)]),
     "h2b_orthogonalize": (C.c_int, [C.c_void_p, C.c_void_p]),
     "h2b_last_hmv_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    "h2b_matrix_build_part": (C.c_int, [C.POINTER(BuildConfig), C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_void_p)]),
+    "h2b_workspace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "h2b_part_upsweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "h2b_part_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "h2b_set_phase_timing": (C.c_int, [C.c_void_p, C.c_int]),
 }
 

@@ -154,6 +154,11 @@ def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=No
     py, ky = _ptr(y)
     kind = _lib.PTR_DEVICE if (kx == ky == _lib.PTR_DEVICE) else (
         _lib.PTR_HOST if (kx == ky == _lib.PTR_HOST) else _lib.PTR_AUTO)
+    if stream is None and _lib.PTR_DEVICE in (kx, ky):
+        # device tensors: run on torch's current stream (NULL would mean the
+        # matrix's own non-blocking stream, unordered with torch's work)
+        from .dist import torch_stream_handle
+        stream = torch_stream_handle()
     _lib.check(_lib.load().h2b_hmv(A._h, px, py, float(alpha), float(beta), kind,
                                    None if stream is None else C.c_void_p(stream)))
     return y

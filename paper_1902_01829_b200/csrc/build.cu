@@ -265,9 +265,10 @@ __global__ void k_leaf_basis(const ChebTables C, int order, int dim, const Box3*
   }
 }
 
+// child_box / E start at the first stored child c0 (global index c0 + c).
 __global__ void k_transfer(const ChebTables C, int order, int dim, const Box3* __restrict__ child_box,
                            const Box3* __restrict__ parent_box, int k, int ldk, int64_t nchild,
-                           double* __restrict__ E) {
+                           int64_t c0, double* __restrict__ E) {
   const int64_t total = nchild * ldk;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -280,7 +281,7 @@ __global__ void k_transfer(const ChebTables C, int order, int dim, const Box3* _
     }
     double node[3];
     cheb_node(C, order, dim, child_box[c], ac, node);
-    lagrange_tensor_dev(C, order, dim, parent_box[c >> 1], node, out, ldk, k);
+    lagrange_tensor_dev(C, order, dim, parent_box[(c0 + c) >> 1], node, out, ldk, k);
   }
 }
 
@@ -342,7 +343,7 @@ std::vector<int32_t> block_rows(const Layer& L) {
 
 }  // namespace
 
-h2b_matrix* build_matrix(const h2b_build_config& cfg, int device) {
+h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, int part) {
   require(cfg.dim == 2 || cfg.dim == 3, "generate_perturbed_grid: dim must be 2 or 3");
   require(cfg.grid_order >= 1, "chebyshev_points: order must be >= 1");
   require(cfg.eta > 0, "dual_traversal_partition: eta must be positive");
@@ -357,6 +358,11 @@ h2b_matrix* build_matrix(const h2b_build_config& cfg, int device) {
   const Tree T = cluster_tree(X, cfg.dim, cfg.n, cfg.leaf_size);
   const int q = T.q;
   require(q <= kMaxLevels - 1, "tree too deep");
+  require(nparts >= 1 && (nparts & (nparts - 1)) == 0, "partition count must be a power of two");
+  int ps = 0;
+  while ((1 << ps) < nparts) ++ps;
+  require(ps <= q, "more partitions than leaves");
+  require(part >= 0 && part < nparts, "partition index out of range");
   Pairs P;
   P.far.resize(q + 1);
   traverse(T, cfg.dim, cfg.eta, 0, 0, 0, P);
@@ -377,9 +383,33 @@ h2b_matrix* build_matrix(const h2b_build_config& cfg, int device) {
   A->m = cfg.leaf_size;
   A->q = q;
   A->rank.assign(q + 1, k);
+  A->part_s = ps;
+  A->part_g = part;
+  {  // memory_footprint of the whole matrix (h2_matrix.hpp:90-102)
+    uint64_t e = uint64_t(P.near.size()) * A->m * A->m + uint64_t(A->nodes(q)) * A->m * k;
+    for (int l = 0; l <= q; ++l) e += uint64_t(P.far[l].size()) * k * k;
+    for (int l = 1; l <= q; ++l) e += uint64_t(A->nodes(l)) * k * k;
+    A->global_footprint = 8 * e;
+  }
+  // keep only the block rows this partition computes (levels >= ps split)
+  auto keep = [&](std::vector<std::pair<int32_t, int32_t>>& v, int l) {
+    if (ps == 0 || l < ps) return;
+    const int64_t b0 = A->own_begin(l), b1 = A->own_end(l);
+    v.erase(std::remove_if(v.begin(), v.end(),
+                           [&](const std::pair<int32_t, int32_t>& e) { return e.first < b0 || e.first >= b1; }),
+            v.end());
+  };
   A->cpl.resize(q + 1);
-  for (int l = 0; l <= q; ++l) to_csr(P.far[l], A->nodes(l), k, k, A->cpl[l]);
+  for (int l = 0; l <= q; ++l) {
+    keep(P.far[l], l);
+    to_csr(P.far[l], A->nodes(l), k, k, A->cpl[l]);
+    A->cpl[l].row0 = A->own_begin(l);
+    A->cpl[l].row1 = A->own_end(l);
+  }
+  keep(P.near, q);
   to_csr(P.near, A->nodes(q), A->m, A->m, A->dense);
+  A->dense.row0 = A->own_begin(q);
+  A->dense.row1 = A->own_end(q);
   P = Pairs{};
   allocate(*A);
   upload_structure(*A);
@@ -406,14 +436,15 @@ h2b_matrix* build_matrix(const h2b_build_config& cfg, int device) {
   if (order == 1) C.t[0] = 0.0;
   auto box_of = [&](int l) { return dbox.p + ((int64_t(1) << l) - 1); };
 
-  const int64_t nleaf = A->nodes(q);
-  k_leaf_basis<<<grid_of(nleaf * A->ldm), 256, 0, s>>>(C, order, cfg.dim, box_of(q), dpts.p, A->m,
-                                                       A->ldm, k, nleaf, A->leaf.p);
+  const int64_t nleaf = A->own_count(q), leaf0 = A->own_begin(q);
+  k_leaf_basis<<<grid_of(nleaf * A->ldm), 256, 0, s>>>(C, order, cfg.dim, box_of(q) + leaf0,
+                                                       dpts.p + leaf0 * A->m * cfg.dim, A->m, A->ldm, k,
+                                                       nleaf, A->leaf.p);
   H2B_CUDA(cudaGetLastError());
   for (int l = 1; l <= q; ++l) {
-    k_transfer<<<grid_of(A->nodes(l) * A->ld(l)), 256, 0, s>>>(
-        C, order, cfg.dim, box_of(l), box_of(l - 1), k, A->ld(l), A->nodes(l),
-        A->transfer.p + A->tr_off[l]);
+    const int64_t c0 = A->tr_begin(l), nc = A->tr_count(l);
+    k_transfer<<<grid_of(nc * A->ld(l)), 256, 0, s>>>(C, order, cfg.dim, box_of(l) + c0, box_of(l - 1), k,
+                                                      A->ld(l), nc, c0, A->transfer.p + A->tr_off[l]);
     H2B_CUDA(cudaGetLastError());
   }
   for (int l = 0; l <= q; ++l) {

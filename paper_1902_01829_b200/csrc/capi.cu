@@ -128,9 +128,10 @@ Matrix::~Matrix() {
 
 uint64_t Matrix::footprint() const {
   // memory_footprint(A) (h2_matrix.hpp:90-102): unpadded entries * 8 bytes.
-  uint64_t e = uint64_t(dense.nb) * dense.br * dense.bc + uint64_t(nodes(q)) * m * rank[q];
+  // (a partition handle counts the blocks it stores)
+  uint64_t e = uint64_t(dense.nb) * dense.br * dense.bc + uint64_t(own_count(q)) * m * rank[q];
   for (int l = 0; l <= q; ++l) e += uint64_t(cpl[l].nb) * cpl[l].br * cpl[l].bc;
-  for (int l = 1; l <= q; ++l) e += uint64_t(nodes(l)) * rank[l] * rank[l - 1];
+  for (int l = 1; l <= q; ++l) e += uint64_t(tr_count(l)) * rank[l] * rank[l - 1];
   return e * sizeof(double);
 }
 
@@ -156,12 +157,12 @@ void allocate(Matrix& A) {
   const int q = A.q;
   A.ldm = pad2(A.m);
   A.perm.alloc(A.n);
-  A.leaf.alloc(size_t(A.nodes(q)) * A.leaf_stride());
+  A.leaf.alloc(size_t(A.own_count(q)) * A.leaf_stride());
   A.tr_off.assign(q + 2, 0);
   int64_t t = 0;
   for (int l = 1; l <= q; ++l) {
     A.tr_off[l] = t;
-    t += A.nodes(l) * A.tr_stride(l);
+    t += A.tr_count(l) * A.tr_stride(l);
   }
   A.tr_off[q + 1] = t;
   A.transfer.alloc(t);
@@ -359,6 +360,7 @@ void copy_out(Matrix& A, double* dst, const double* src, size_t n, cudaStream_t 
 void hmv(Matrix& A, const double* x, double* y, double alpha, double beta, h2b_ptr_kind kind,
          cudaStream_t s) {
   require(x && y, "hmv: null vector");
+  require(A.part_s == 0, "hmv: partition handles use h2b_part_upsweep / h2b_part_finish");
   DeviceGuard g(A.device);
   if (!s) s = A.stream;
   const bool dx = resolve_device(kind, x), dy = resolve_device(kind, y);
@@ -375,6 +377,10 @@ void hmv(Matrix& A, const double* x, double* y, double alpha, double beta, h2b_p
   hmv_device(A, xd, yd, alpha, beta, s);
   if (!dy) copy_out(A, y, A.ys.p, A.n, s);
   if (!dx || !dy) H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+void whole(const Matrix& A, const char* what) {
+  require(A.part_s == 0, std::string(what) + ": not supported on a partition handle");
 }
 
 // Phase helpers take host or device pointers; host data goes through
@@ -415,7 +421,7 @@ using namespace h2b;
 
 // Implemented in build.cu / compress.cu.
 namespace h2b {
-h2b_matrix* build_matrix(const h2b_build_config& cfg, int device);
+h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, int part);
 void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep);
 void orthogonalize_matrix(Matrix& A, double* t_out);
 }  // namespace h2b
@@ -436,7 +442,7 @@ h2b_status h2b_matrix_create(const h2b_matrix_desc* desc, int device, h2b_matrix
 h2b_status h2b_matrix_build(const h2b_build_config* cfg, int device, h2b_matrix** out) {
   return guarded([&] {
     require(cfg && out, "null argument");
-    *out = build_matrix(*cfg, device);
+    *out = build_matrix(*cfg, device, 1, 0);
   });
 }
 
@@ -468,6 +474,9 @@ h2b_status h2b_matrix_info_get(const h2b_matrix* Ah, h2b_matrix_info* info) {
     info->dense_blocks = A.dense.nb;
     info->dense_max_row = A.dense.max_row;
     info->footprint_bytes = A.footprint();
+    info->global_footprint_bytes = A.part_s ? A.global_footprint : A.footprint();
+    info->part_log2 = A.part_s;
+    info->part_index = A.part_g;
     info->device_bytes = A.device_bytes();
     info->hmv_flops = A.hmv_flops();
   });
@@ -484,6 +493,7 @@ h2b_status h2b_matrix_export(const h2b_matrix* Ah, int32_t* perm, double* leaf, 
   return guarded([&] {
     require(Ah, "null matrix");
     const Matrix& A = *Ah;
+    whole(A, "h2b_matrix_export");
     DeviceGuard g(A.device);
     cudaStream_t s = A.stream;
     const int q = A.q;
@@ -535,6 +545,7 @@ h2b_status h2b_upsweep(h2b_matrix* Ah, const double* xc, double* xhat, h2b_ptr_k
   return guarded([&] {
     require(Ah && xc && xhat, "null argument");
     Matrix& A = *Ah;
+    whole(A, "h2b_upsweep");
     DeviceGuard g(A.device);
     cudaStream_t s = A.stream;
     const bool dev = resolve_device(kind, xc);
@@ -553,6 +564,7 @@ h2b_status h2b_tree_multiply(h2b_matrix* Ah, const double* xhat, double* yhat, h
   return guarded([&] {
     require(Ah && xhat && yhat, "null argument");
     Matrix& A = *Ah;
+    whole(A, "h2b_tree_multiply");
     DeviceGuard g(A.device);
     cudaStream_t s = A.stream;
     const size_t nv = A.vec_off[A.q + 1];
@@ -576,6 +588,7 @@ h2b_status h2b_downsweep(h2b_matrix* Ah, const double* yhat, double* yc, h2b_ptr
   return guarded([&] {
     require(Ah && yhat && yc, "null argument");
     Matrix& A = *Ah;
+    whole(A, "h2b_downsweep");
     DeviceGuard g(A.device);
     cudaStream_t s = A.stream;
     const size_t nv = A.vec_off[A.q + 1];
@@ -595,6 +608,7 @@ h2b_status h2b_dense_mv(h2b_matrix* Ah, const double* xc, double* yc, double alp
   return guarded([&] {
     require(Ah && xc && yc, "null argument");
     Matrix& A = *Ah;
+    whole(A, "h2b_dense_mv");
     require(alpha == 1.0 && beta == 0.0, "h2b_dense_mv: only alpha = 1, beta = 0 (the hmv call site) is implemented");
     DeviceGuard g(A.device);
     cudaStream_t s = A.stream;
@@ -616,6 +630,7 @@ h2b_status h2b_dense_mv(h2b_matrix* Ah, const double* xc, double* yc, double alp
 h2b_status h2b_compress(h2b_matrix* Ah, double eps, h2b_compress_report* report) {
   return guarded([&] {
     require(Ah, "null matrix");
+    whole(*Ah, "h2b_compress");
     compress_matrix(*Ah, eps, report);
   });
 }
@@ -623,7 +638,55 @@ h2b_status h2b_compress(h2b_matrix* Ah, double eps, h2b_compress_report* report)
 h2b_status h2b_orthogonalize(h2b_matrix* Ah, double* t_out) {
   return guarded([&] {
     require(Ah, "null matrix");
+    whole(*Ah, "h2b_orthogonalize");
     orthogonalize_matrix(*Ah, t_out);
+  });
+}
+
+h2b_status h2b_matrix_build_part(const h2b_build_config* cfg, int device, int nparts, int part,
+                                  h2b_matrix** out) {
+  return guarded([&] {
+    require(cfg && out, "null argument");
+    *out = build_matrix(*cfg, device, nparts, part);
+  });
+}
+
+h2b_status h2b_workspace(h2b_matrix* Ah, int which, void** ptr, int64_t* count) {
+  return guarded([&] {
+    require(Ah && ptr && count, "null argument");
+    Matrix& A = *Ah;
+    switch (which) {
+      case H2B_WS_XHAT: *ptr = A.xhat.p; *count = A.vec_off[A.q + 1]; break;
+      case H2B_WS_YHAT: *ptr = A.yhat.p; *count = A.vec_off[A.q + 1]; break;
+      case H2B_WS_XC: *ptr = A.xc.p; *count = A.n; break;
+      case H2B_WS_PERM: *ptr = A.perm.p; *count = A.n; break;
+      default: require(false, "h2b_workspace: unknown buffer");
+    }
+  });
+}
+
+h2b_status h2b_part_upsweep(h2b_matrix* Ah, const double* x, void* stream) {
+  return guarded([&] {
+    require(Ah && x, "null argument");
+    Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    launch_up_leaf(A, x, s);
+    launch_gather(A.perm.p, x, A.xc.p, A.n, s);  // dense blocks read remote columns
+    for (int l = A.q; l > A.part_s; --l) launch_up_level(A, l, s, A.own_begin(l - 1), A.own_end(l - 1));
+  });
+}
+
+h2b_status h2b_part_finish(h2b_matrix* Ah, double* y_slice, void* stream) {
+  return guarded([&] {
+    require(Ah && y_slice, "null argument");
+    Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    for (int l = A.part_s; l >= 1; --l) launch_up_level(A, l, s);  // replicated top
+    launch_bsr(A, A.work.p, A.nwork, A.xc.p, A.yc.p, A.xhat.p, A.yhat.p, s);
+    for (int l = 1; l <= A.q; ++l) launch_down_level(A, l, s, A.own_begin(l), A.own_end(l));
+    launch_down_leaf(A, y_slice, 1.0, 0.0, false, s);
   });
 }
 

@@ -93,6 +93,7 @@ struct DevBuf {
 struct Layer {
   int br = 0, bc = 0, ld = 0;     // block dims, padded leading dim
   int64_t rows = 0, nb = 0;
+  int64_t row0 = 0, row1 = -1;      // block rows this handle computes (-1: all)
   int max_row = 0;
   std::vector<int32_t> h_rp, h_ci;  // host copy of the structure
   int32_t* rp = nullptr;            // device (views into Matrix pools)
@@ -136,8 +137,19 @@ struct Matrix {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
 
+  // Subtree partition: 2^part_s partitions, this handle owns
+  // part_g.  Levels >= part_s are split by top subtree; levels < part_s (and
+  // the transfers up to level part_s) are replicated.  part_s = 0: whole matrix.
+  int part_s = 0, part_g = 0;
+  uint64_t global_footprint = 0;    // memory_footprint of the whole matrix
+
   ~Matrix();
   int64_t nodes(int l) const { return int64_t(1) << l; }
+  int64_t own_begin(int l) const { return l < part_s ? 0 : int64_t(part_g) << (l - part_s); }
+  int64_t own_end(int l) const { return l < part_s ? nodes(l) : int64_t(part_g + 1) << (l - part_s); }
+  int64_t own_count(int l) const { return own_end(l) - own_begin(l); }
+  int64_t tr_begin(int l) const { return l <= part_s ? 0 : own_begin(l); }
+  int64_t tr_count(int l) const { return l <= part_s ? nodes(l) : own_count(l); }
   int ld(int l) const { return pad2(rank[l]); }
   int64_t leaf_stride() const { return int64_t(ldm) * rank[q]; }
   int64_t tr_stride(int l) const { return int64_t(ld(l)) * rank[l - 1]; }
@@ -148,10 +160,14 @@ struct Matrix {
 
 // ---- launchers (k_hmv.cu) ----
 void launch_up_leaf(const Matrix& A, const double* x, cudaStream_t s, bool cluster_order = false);
-void launch_up_level(const Matrix& A, int l, cudaStream_t s);
+// parents at level l-1 in [p0, p1) (children in the transfer pool)
+void launch_up_level(const Matrix& A, int l, cudaStream_t s, int64_t p0 = 0, int64_t p1 = -1);
 void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
                 double* ydense, const double* xh, double* yh, cudaStream_t s);
-void launch_down_level(const Matrix& A, int l, cudaStream_t s);
+// children at level l in [c0, c1)
+void launch_down_level(const Matrix& A, int l, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1);
+// to_user: y[perm[t]] = alpha v + beta y[perm[t]] (original order); else y[t] = v
+// with t relative to the first owned leaf (cluster-order slice).
 void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
                       cudaStream_t s);
 void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s);

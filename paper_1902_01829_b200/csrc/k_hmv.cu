@@ -149,12 +149,13 @@ __device__ __forceinline__ void gemvN_pair(const double* __restrict__ A, int ld,
 __global__ void __launch_bounds__(kThreads, 2) k_up_leaf(const double* __restrict__ x,
                                                       const int32_t* __restrict__ perm,
                                                       const double* __restrict__ leaf, int m,
-                                                      int ldm, int k, int64_t nleaves,
+                                                      int ldm, int k, int64_t nleaves, int64_t leaf0,
                                                       double* __restrict__ xc,
                                                       double* __restrict__ xh) {
   const int r = 2 * lane_id();
   const int64_t stride = int64_t(ldm) * k;
-  for (int64_t i = warp_global(); i < nleaves; i += warp_count()) {
+  for (int64_t il = warp_global(); il < nleaves; il += warp_count()) {
+    const int64_t i = leaf0 + il;  // global leaf index; the pool holds owned leaves only
     const int64_t base = i * m;
     double v0 = 0.0, v1 = 0.0;
     // perm == nullptr: x is already in cluster order (phase API).
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_leaf(const double* __restric
       xc[base + r + 1] = v1;
     }
     if (k == 0) continue;
-    const double* V = leaf + i * stride;
+    const double* V = leaf + il * stride;
     const double o0 = gemvT_group<false>(V, nullptr, ldm, k, 0, v0, v1, 0, 0, r < ldm);
     const double o1 = gemvT_group<false>(V, nullptr, ldm, k, 1, v0, v1, 0, 0, r < ldm);
     if (r < k) xh[i * k + r] = o0;
@@ -176,17 +177,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_leaf(const double* __restric
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_up_level(const double* __restrict__ F, int ldc,
-                                                       int kc, int kp, int64_t nparents,
+                                                       int kc, int kp, int64_t p0, int64_t p1,
+                                                       int64_t cbegin,
                                                        const double* __restrict__ xl,
                                                        double* __restrict__ xp) {
   const int r = 2 * lane_id();
   const int64_t stride = int64_t(ldc) * kp;
-  for (int64_t p = warp_global(); p < nparents; p += warp_count()) {
+  for (int64_t p = p0 + warp_global(); p < p1; p += warp_count()) {
     const double* x0 = xl + (2 * p) * kc;
     const double* x1 = x0 + kc;
     const double v0 = r < kc ? x0[r] : 0.0, v1 = r + 1 < kc ? x0[r + 1] : 0.0;
     const double w0 = r < kc ? x1[r] : 0.0, w1 = r + 1 < kc ? x1[r + 1] : 0.0;
-    const double* A = F + (2 * p) * stride;
+    const double* A = F + (2 * p - cbegin) * stride;
     const double o0 = gemvT_group<true>(A, A + stride, ldc, kp, 0, v0, v1, w0, w1, r < ldc);
     const double o1 = gemvT_group<true>(A, A + stride, ldc, kp, 1, v0, v1, w0, w1, r < ldc);
     if (r < kp) xp[p * kp + r] = o0;
@@ -195,16 +197,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_level(const double* __restri
 }
 
 __global__ void __launch_bounds__(kThreads) k_down_level(const double* __restrict__ E, int ldc,
-                                                         int kc, int kp, int64_t nchildren,
+                                                         int kc, int kp, int64_t c0, int64_t c1,
+                                                         int64_t cbegin,
                                                          const double* __restrict__ yp_all,
                                                          double* __restrict__ yl) {
   const int r = 2 * lane_id();
   const int64_t stride = int64_t(ldc) * kp;
-  for (int64_t c = warp_global(); c < nchildren; c += warp_count()) {
+  for (int64_t c = c0 + warp_global(); c < c1; c += warp_count()) {
     const double* yp = yp_all + (c >> 1) * kp;
     const double a0 = r < kp ? yp[r] : 0.0, a1 = r + 1 < kp ? yp[r + 1] : 0.0;
     double acc0, acc1;
-    gemvN_pair(E + c * stride, ldc, kp, a0, a1, r < ldc, acc0, acc1);
+    gemvN_pair(E + (c - cbegin) * stride, ldc, kp, a0, a1, r < ldc, acc0, acc1);
     double* y = yl + c * kc;
     if (r < kc) y[r] = acc0 + y[r];
     if (r + 1 < kc) y[r + 1] = acc1 + y[r + 1];
@@ -212,17 +215,18 @@ __global__ void __launch_bounds__(kThreads) k_down_level(const double* __restric
 }
 
 __global__ void __launch_bounds__(kThreads) k_down_leaf(
-    const double* __restrict__ U, int ldm, int m, int k, int64_t nleaves,
+    const double* __restrict__ U, int ldm, int m, int k, int64_t nleaves, int64_t leaf0,
     const double* __restrict__ yh, const double* __restrict__ yc,
     const int32_t* __restrict__ perm, double* __restrict__ y, double alpha, double beta,
     int to_user) {
   const int r = 2 * lane_id();
   const int64_t stride = int64_t(ldm) * k;
-  for (int64_t i = warp_global(); i < nleaves; i += warp_count()) {
+  for (int64_t il = warp_global(); il < nleaves; il += warp_count()) {
+    const int64_t i = leaf0 + il;  // global leaf index; the pool holds owned leaves only
     const double* yq = yh + i * k;
     const double a0 = r < k ? yq[r] : 0.0, a1 = r + 1 < k ? yq[r + 1] : 0.0;
     double acc0 = 0.0, acc1 = 0.0;
-    if (k > 0) gemvN_pair(U + i * stride, ldm, k, a0, a1, r < ldm, acc0, acc1);
+    if (k > 0) gemvN_pair(U + il * stride, ldm, k, a0, a1, r < ldm, acc0, acc1);
     const int64_t base = i * m;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) k_down_leaf(
         const int64_t o = perm[base + rr];
         y[o] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[o]);
       } else {
-        y[base + rr] = v;  // phase API: cluster-order yc += U y^
+        y[il * m + rr] = v;  // cluster-order slice starting at the first owned leaf
       }
     }
   }
@@ -367,41 +371,44 @@ unsigned flat_grid(int64_t n) {
 }  // namespace
 
 void launch_up_leaf(const Matrix& A, const double* x, cudaStream_t s, bool cluster_order) {
-  const int64_t nl = A.nodes(A.q);
-  k_up_leaf<<<warp_grid(nl), kThreads, 0, s>>>(x, cluster_order ? nullptr : A.perm.p, A.leaf.p, A.m, A.ldm, A.rank[A.q], nl,
-                                               A.xc.p, A.xhat.p + A.vec_off[A.q]);
+  const int64_t nl = A.own_count(A.q);
+  k_up_leaf<<<warp_grid(nl), kThreads, 0, s>>>(x, cluster_order ? nullptr : A.perm.p, A.leaf.p, A.m, A.ldm,
+                                               A.rank[A.q], nl, A.own_begin(A.q), A.xc.p,
+                                               A.xhat.p + A.vec_off[A.q]);
   H2B_CUDA(cudaGetLastError());
 }
 
-void launch_up_level(const Matrix& A, int l, cudaStream_t s) {
+void launch_up_level(const Matrix& A, int l, cudaStream_t s, int64_t p0, int64_t p1) {
   const int kc = A.rank[l], kp = A.rank[l - 1];
+  if (p1 < 0) p1 = A.nodes(l - 1);
   double* xp = A.xhat.p + A.vec_off[l - 1];
-  const int64_t np = A.nodes(l - 1);
-  if (kp == 0) return;
+  const int64_t np = p1 - p0;
+  if (kp == 0 || np <= 0) return;
   if (kc == 0) {
-    H2B_CUDA(cudaMemsetAsync(xp, 0, size_t(np) * kp * sizeof(double), s));
+    H2B_CUDA(cudaMemsetAsync(xp + p0 * kp, 0, size_t(np) * kp * sizeof(double), s));
     return;
   }
-  k_up_level<<<warp_grid(np), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, np,
-                                                A.xhat.p + A.vec_off[l], xp);
+  k_up_level<<<warp_grid(np), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, p0, p1,
+                                                A.tr_begin(l), A.xhat.p + A.vec_off[l], xp);
   H2B_CUDA(cudaGetLastError());
 }
 
-void launch_down_level(const Matrix& A, int l, cudaStream_t s) {
+void launch_down_level(const Matrix& A, int l, cudaStream_t s, int64_t c0, int64_t c1) {
   const int kc = A.rank[l], kp = A.rank[l - 1];
-  if (kc == 0 || kp == 0) return;
-  const int64_t nc = A.nodes(l);
+  if (c1 < 0) c1 = A.nodes(l);
+  const int64_t nc = c1 - c0;
+  if (kc == 0 || kp == 0 || nc <= 0) return;
   k_down_level<<<warp_grid(nc), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
-                                                  nc, A.yhat.p + A.vec_off[l - 1],
+                                                  c0, c1, A.tr_begin(l), A.yhat.p + A.vec_off[l - 1],
                                                   A.yhat.p + A.vec_off[l]);
   H2B_CUDA(cudaGetLastError());
 }
 
 void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
                       cudaStream_t s) {
-  const int64_t nl = A.nodes(A.q);
+  const int64_t nl = A.own_count(A.q);
   k_down_leaf<<<warp_grid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[A.q], nl,
-                                                 A.yhat.p + A.vec_off[A.q], A.yc.p, A.perm.p, y,
+                                                 A.own_begin(A.q), A.yhat.p + A.vec_off[A.q], A.yc.p, A.perm.p, y,
                                                  alpha, beta, to_user ? 1 : 0);
   H2B_CUDA(cudaGetLastError());
 }
@@ -460,7 +467,8 @@ std::vector<uint32_t> make_work_list(const std::vector<const Layer*>& layers) {
   for (size_t li = 0; li < layers.size(); ++li) {
     const Layer* L = layers[li];
     if (!L) continue;
-    for (int64_t r = 0; r < L->rows; ++r) {
+    const int64_t r1 = L->row1 < 0 ? L->rows : L->row1;
+    for (int64_t r = L->row0; r < r1; ++r) {
       const int32_t nb = L->h_rp.empty() ? 0 : L->h_rp[r + 1] - L->h_rp[r];
       // cost ~ bytes of the row; empty rows still write zeros
       const int64_t bytes = int64_t(nb) * L->ld * L->bc;
