@@ -17,9 +17,9 @@ roofline = the dominant kernel (k_bsr: coupling + dense blocks) from per-phase
 cpu_baseline = the unmodified reference (oracle/_ref, OpenMP, all host cores)
          on a bounded sample (2D n=2^18, same structure family).
 
-N > 1 (torchrun): every rank holds its own replica of the matrix on its GPU and
-runs the full mat-vec ("replicas"; see DESIGN.md §6 for the subtree-partitioned
-plan), scaling "weak".
+N > 1 (torchrun): the same n=2^22 matrix is partitioned by top-level subtrees
+across the ranks (1/N of the matrix per GPU) and one mat-vec exchanges x^ and
+the y slices with NCCL all-gathers; scaling "strong".
 """
 from __future__ import annotations
 
@@ -120,11 +120,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup():
+def dist_setup(force: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or force:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -236,6 +240,114 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_distributed(args, cfg, world, rank, local):
+    """N > 1: subtree-partitioned mat-vec of the SAME n=2^22 matrix (strong
+    scaling): every rank holds 1/N of the matrix (its top-level subtree plus
+    the replicated levels above the split) and exchanges x^ / y slices with
+    NCCL all-gathers (paper_1902_01829_b200/dist.py)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1902_01829_b200 import _lib
+    from paper_1902_01829_b200.dist import DistributedH2Matrix
+    import ctypes as C
+
+    t0 = time.time()
+    D = DistributedH2Matrix(cfg["dim"], cfg["n"], leaf_size=cfg["leaf_size"],
+                            grid_order=cfg["grid_order"], eta=cfg["eta"], ell=cfg["ell"],
+                            perturbation=cfg["perturbation"], seed=cfg["seed"], device=local)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    n = D.n
+    fp = D.footprint_global
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    gen = torch.Generator(device="cuda").manual_seed(1)  # same x on every rank
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=gen)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        D.hmv(x, y)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+    _lib.check(lib.h2b_set_phase_timing(D._h, 1))
+    buf = (C.c_double * 4)()
+    lib.h2b_last_hmv_timing(D._h, buf)
+    sampler = ClockSampler(local) if rank == 0 else None
+    barrier(world)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        D.hmv(x, y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop() if sampler else None
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    _lib.check(lib.h2b_last_hmv_timing(D._h, buf))
+    phases = list(buf)
+    _lib.check(lib.h2b_set_phase_timing(D._h, 0))
+    value = fp / (ms * 1e-3) / 1e9
+
+    # e2e: pinned host x -> device, mat-vec, full y -> pinned host, every rank
+    xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x.cpu())
+    xd = torch.empty_like(x)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        D.hmv(xd, y)
+        yh.copy_(y, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    # parity spot check against the replicated-input result
+    assert torch.allclose(yh, y.cpu(), rtol=0, atol=0)
+    if rank != 0:
+        D.close()
+        return
+    peak, peak_src = load_peaks()
+    inf = D.info
+    q = inf.depth
+    bsr_bytes = 8 * (sum(inf.cpl_blocks[l] * inf.ranks[l] ** 2 for l in range(q + 1))
+                     + inf.dense_blocks * inf.m * inf.m)
+    achieved = bsr_bytes / (phases[1] * 1e-3) / 1e9 if phases[1] > 0 else None
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": dict(cfg, parallelism=f"subtree{world}", footprint_bytes=fp,
+                       footprint_per_gpu=D.footprint_local,
+                       l2="inputs larger than L2", build_s=round(build_s, 2)),
+        "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
+        "phase_ms_rank0": {"top_upsweep": round(phases[0], 4), "coupling_dense_bsr": round(phases[1], 4),
+                           "downsweep": round(phases[2], 4)},
+        "roofline": {"bound": "hbm", "kernel": "k_bsr (rank 0 partition)",
+                     "achieved": round(achieved, 1) if achieved else None, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                     "algorithmic_bytes_per_launch": bsr_bytes},
+        "cpu_baseline": None,
+        "e2e": {"value": round(fp / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": 8 * n * world,
+                "d2h_bytes_per_step": 8 * n * world},
+        # ours per step: up_leaf, gather, per-level up (q), bsr, per-level down (q), down_leaf
+        "gpu_launches": (2 * q + 4) * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    D.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -246,6 +358,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compress", action="store_true")
     ap.add_argument("--compress-reps", type=int, default=2)
+    ap.add_argument("--dist", action="store_true",
+                    help="use the subtree-partitioned path even at N=1 (testing)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -256,9 +370,11 @@ def main():
 
     import paper_1902_01829_b200 as h2
 
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(force=args.dist)
     torch.cuda.set_device(local)
     cfg = dict(WORKLOAD, n=args.n)
+    if world > 1 or args.dist:
+        return run_distributed(args, cfg, world, rank, local)
     t0 = time.time()
     A = h2.H2Matrix.construct(cfg["dim"], cfg["n"], leaf_size=cfg["leaf_size"],
                               grid_order=cfg["grid_order"], eta=cfg["eta"], ell=cfg["ell"],

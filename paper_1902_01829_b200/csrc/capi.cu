@@ -683,10 +683,15 @@ h2b_status h2b_part_finish(h2b_matrix* Ah, double* y_slice, void* stream) {
     Matrix& A = *Ah;
     DeviceGuard g(A.device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    cudaEvent_t* ev = timing_slots(A);
+    if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
     for (int l = A.part_s; l >= 1; --l) launch_up_level(A, l, s);  // replicated top
+    if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
     launch_bsr(A, A.work.p, A.nwork, A.xc.p, A.yc.p, A.xhat.p, A.yhat.p, s);
+    if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
     for (int l = 1; l <= A.q; ++l) launch_down_level(A, l, s, A.own_begin(l), A.own_end(l));
     launch_down_leaf(A, y_slice, 1.0, 0.0, false, s);
+    if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
   });
 }
 

@@ -53,6 +53,15 @@ def torch_stream_handle() -> int:
     return h if h else _lib.CUDA_STREAM_LEGACY
 
 
+def gather_xhat(plan: PartitionPlan, xhat, allgather):
+    """All-gather the owned x^ slices of every level >= s, in place in the
+    level-concatenated pool `xhat` (any tensor type the callback accepts)."""
+    for l in plan.gather_levels():
+        off, length, chunk = plan.level_slice(l)
+        level = xhat[off:off + length]
+        allgather(level, level[plan.part * chunk:(plan.part + 1) * chunk])
+
+
 class DistributedH2Matrix:
     """Rank-local partition of construct<double>(...) (construction.hpp:179-200)."""
 
@@ -110,11 +119,7 @@ class DistributedH2Matrix:
             pass
 
     def gather_xhat(self, allgather):
-        """All-gather the owned x^ slices of every level >= s (in place)."""
-        for l in self.plan.gather_levels():
-            off, length, chunk = self.plan.level_slice(l)
-            level = self.xhat[off:off + length]
-            allgather(level, level[self.part * chunk:(self.part + 1) * chunk])
+        gather_xhat(self.plan, self.xhat, allgather)
 
     def hmv(self, x, y=None, alpha: float = 1.0, beta: float = 0.0, allgather=None):
         """y <- alpha A x + beta y for the full vectors x, y (original order,
