@@ -222,6 +222,41 @@ def compression_run(h2, torch, device, reps):
             "bytes": [rep.bytes_before, rep.bytes_after]}
 
 
+def multi16_run(A, torch, steps):
+    """16 right-hand sides per pass through h2b_hmv_multi (device pointers):
+    every block is read once per 16 vectors and multiplied on the FP64 tensor
+    cores (mma.sync m8n8k4, k_hmv_mv.cu)."""
+    import ctypes as C
+
+    from paper_1902_01829_b200 import _lib
+    n = A.info().n
+    fp = A.memory_footprint()
+    flops = A.info().hmv_flops
+    X = torch.rand(16, n, dtype=torch.float64, device="cuda")
+    Y = torch.zeros_like(X)
+    s = torch.cuda.current_stream()
+    lib = _lib.load()
+
+    def run():
+        _lib.check(lib.h2b_hmv_multi(A._h, 16, C.c_void_p(X.data_ptr()), n, C.c_void_p(Y.data_ptr()),
+                                     n, 1.0, 0.0, _lib.PTR_DEVICE, C.c_void_p(s.cuda_stream or 1)))
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        run()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"vectors": 16, "ms_per_pass": round(ms, 3), "ms_per_vector": round(ms / 16, 4),
+            "effective_GBs": round(16 * fp / ms / 1e6, 1),
+            "matrix_stream_GBs": round(fp / ms / 1e6, 1),
+            "model_tflops": round(16 * flops / ms / 1e9, 2)}
+
+
 def run_reference(args):
     world, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
     if rank != 0:
@@ -444,6 +479,9 @@ def main():
     # correctness spot check of the e2e result against the device result
     assert np.allclose(yn, yt.cpu().numpy(), rtol=1e-13, atol=0)
 
+    # ---- 16-vector FP64-MMA mat-vec on the same matrix (BASELINE configs[3]) ----
+    multi = multi16_run(A, torch, args.steps)
+
     # ---- compression GFLOP/s (metric's second half): C3, 3D n=2^20 k=64, eps 1e-6 ----
     A.close()
     del A
@@ -496,6 +534,7 @@ def main():
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
+        "multi16": multi,
         "compression": comp,
     }
     print(json.dumps(line), flush=True)

@@ -535,9 +535,38 @@ h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx,
   return guarded([&] {
     require(Ah, "null matrix");
     Matrix& A = *Ah;
+    whole(A, "h2b_hmv_multi");
     require(nvec >= 0 && ldx >= A.n && ldy >= A.n, "hmv_multi: bad leading dimension");
-    for (int v = 0; v < nvec; ++v)
-      hmv(A, X + v * ldx, Y + v * ldy, alpha, beta, kind, static_cast<cudaStream_t>(stream));
+    require(X && Y, "hmv_multi: null vector");
+    if (nvec == 0) return;
+    DeviceGuard g(A.device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    const bool dx = resolve_device(kind, X), dy = resolve_device(kind, Y);
+    DevBuf<double> xs, ys;
+    const double* xd = X;
+    double* yd = Y;
+    int64_t lx = ldx, ly = ldy;
+    if (!dx) {
+      xs.alloc(size_t(A.n) * nvec);
+      H2B_CUDA(cudaMemcpy2DAsync(xs.p, A.n * sizeof(double), X, ldx * sizeof(double), A.n * sizeof(double),
+                                 nvec, cudaMemcpyHostToDevice, s));
+      xd = xs.p;
+      lx = A.n;
+    }
+    if (!dy) {
+      ys.alloc(size_t(A.n) * nvec);
+      if (beta != 0.0)
+        H2B_CUDA(cudaMemcpy2DAsync(ys.p, A.n * sizeof(double), Y, ldy * sizeof(double),
+                                   A.n * sizeof(double), nvec, cudaMemcpyHostToDevice, s));
+      yd = ys.p;
+      ly = A.n;
+    }
+    for (int v0 = 0; v0 < nvec; v0 += 16)
+      hmv_multi_device(A, xd + v0 * lx, lx, yd + v0 * ly, ly, std::min(16, nvec - v0), alpha, beta, s);
+    if (!dy)
+      H2B_CUDA(cudaMemcpy2DAsync(Y, ldy * sizeof(double), ys.p, A.n * sizeof(double), A.n * sizeof(double),
+                                 nvec, cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaStreamSynchronize(s));
   });
 }
 

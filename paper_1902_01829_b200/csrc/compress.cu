@@ -728,6 +728,8 @@ void relayout(Matrix& A) {
   for (int l = 0; l <= q; ++l) A.vec_off[l + 1] = A.vec_off[l] + A.nodes(l) * A.rank[l];
   A.xhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
   A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
+  A.xh16.release();
+  A.yh16.release();
   upload_structure(A);
 }
 

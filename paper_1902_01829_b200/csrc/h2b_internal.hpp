@@ -127,6 +127,7 @@ struct Matrix {
 
   // HmvContext analogue (hmv.hpp:161-172): one workspace per handle.
   DevBuf<double> xc, yc, xhat, yhat, xs, ys;
+  DevBuf<double> xc16, yc16, xh16, yh16;  // 16-vector panels (k_hmv_mv.cu), lazily allocated
   double* h_stage = nullptr;        // pinned host staging for host-pointer calls
   size_t h_stage_n = 0;
 
@@ -171,6 +172,10 @@ void launch_down_level(const Matrix& A, int l, cudaStream_t s, int64_t c0 = 0, i
 void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
                       cudaStream_t s);
 void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s);
+
+// 16-vector FP64-MMA mat-vec, device pointers (k_hmv_mv.cu).
+void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
+                      double alpha, double beta, cudaStream_t s);
 
 // Build the fused BSR work list for the given layers (rows sorted by
 // decreasing block count so the round-robin warp assignment is balanced).

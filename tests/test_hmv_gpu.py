@@ -154,3 +154,34 @@ def test_large_matches_reference(gpu, ref):
     A = h2.H2Matrix.construct(2, n)
     assert A.memory_footprint() == R.footprint()
     assert rel_err(h2.hmv(A, x), R.hmv(x)) <= TOL
+
+
+def test_hmv_multi_16_and_ragged(gpu, orc):
+    """16-vector FP64-MMA path (k_hmv_mv.cu): every column equals the oracle's
+    single-vector hmv; 20 vectors exercise a full pass + a ragged one; alpha/beta."""
+    for dim, n, order in [(2, 4096, 8), (3, 4096, 4), (2, 4096, 6)]:
+        O = orc.construct(dim, n, grid_order=order)
+        A = h2.H2Matrix.from_host(O.to_host())
+        rng = np.random.default_rng(8)
+        X = rng.random((20, n))
+        Y0 = rng.random((20, n))
+        Y = h2.hmv_multi(A, X, 2.0, 0.5, Y0.copy())
+        for v in range(20):
+            assert rel_err(Y[v], O.hmv(X[v], Y0[v], 2.0, 0.5)) <= TOL, (dim, order, v)
+
+
+def test_hmv_multi_device_pointers(gpu, orc):
+    import ctypes as C
+    import torch
+    from paper_1902_01829_b200 import _lib
+    O = orc.construct(2, 4096)
+    A = h2.H2Matrix.from_host(O.to_host())
+    X = torch.rand(16, 4096, dtype=torch.float64, device="cuda")
+    Y = torch.zeros_like(X)
+    _lib.check(_lib.load().h2b_hmv_multi(A._h, 16, C.c_void_p(X.data_ptr()), 4096,
+                                         C.c_void_p(Y.data_ptr()), 4096, 1.0, 0.0, _lib.PTR_DEVICE,
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream or 1)))
+    torch.cuda.synchronize()
+    Xn, Yn = X.cpu().numpy(), Y.cpu().numpy()
+    for v in range(16):
+        assert rel_err(Yn[v], O.hmv(Xn[v])) <= TOL
