@@ -142,34 +142,46 @@ __global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restr
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// R^l_r = R-factor of [R^{l-1}_{r/2} E_r^T ; S_rb^T ...] (compression.hpp:213-256)
-// by streaming TSQR over the UNPADDED stack.  The running R (kc x kc, upper
+// Parent contributions P_r = R^{l-1}_{r/2} E_r^T (kp x kc) for every node of
+// level l (the first rows of the weight stack, compression.hpp:228-235).
+__global__ void __launch_bounds__(kThreads) k_weights_parent(const double* __restrict__ E, int lde,
+                                                             int kc, int kp,
+                                                             const double* __restrict__ Rpar,
+                                                             double* __restrict__ P) {
+  const int64_t r = blockIdx.x;
+  cta::gemm_tc<false, true>(P + r * int64_t(kp) * kc, kp, Rpar + (r >> 1) * int64_t(kp) * kp, kp,
+                            E + r * int64_t(lde) * kp, lde, kp, kc, kp);
+}
+
+// R^l_r = R-factor of [P_r ; S_rb^T ...] (compression.hpp:213-256) by
+// streaming TSQR over the UNPADDED stack.  The running R (kc x kc, upper
 // triangular) stays in smem; each chunk of <= kChunkRows stack rows lives in
-// registers -- thread (warp w, lane t) owns column c = 8w + t/4 and rows
-// g + 4r (g = t%4) -- and [R; chunk] is re-triangularised by a structured
-// Householder pass whose reflectors touch one row of R plus the chunk.
+// registers -- thread (warp w, lane t) of a 512-thread CTA owns column
+// c = 4w + t/8 and rows g + 8r (g = t%8) -- and [R; chunk] is
+// re-triangularised by a structured Householder pass whose reflectors touch
+// one row of R plus the chunk.
+constexpr int kWThreads = 512;
 constexpr int kChunkRows = 128;
-constexpr int kRowsPerThread = kChunkRows / 4;
-__global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restrict__ E, int lde,
-                                                         int kc, int kp,
-                                                         const double* __restrict__ Rpar,
-                                                         const int32_t* __restrict__ rp,
-                                                         const double* __restrict__ S, int lds,
-                                                         double* __restrict__ Rout) {
+constexpr int kRowsPerThread = kChunkRows / 8;
+__global__ void __launch_bounds__(kWThreads, 1) k_weights(const double* __restrict__ P, int kc, int kp,
+                                                          const int32_t* __restrict__ rp,
+                                                          const double* __restrict__ S, int lds,
+                                                          double* __restrict__ Rout) {
   extern __shared__ double sm[];
   const int ldr = cta::sld(kc);
   const int ldst = cta::sld(kChunkRows);
   double* Rs = sm;                       // ldr x kc, running R
   double* st = Rs + ldr * kc;            // ldst x kc chunk staging
   double* vb = st + ldst * kc;           // kChunkRows reflector entries
-  double* misc = vb + kChunkRows;        // [0] = tau, [1..16] red
-  int* flip = reinterpret_cast<int*>(misc + 32);
-  const int lane = cta::lane();
-  const int c = cta::warp() * 8 + (lane >> 2);  // owned column
-  const int g = lane & 3;                        // row group
+  double* misc = vb + kChunkRows;        // [0] = tau
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int c = (tid >> 5) * 4 + (lane >> 3);  // owned column
+  const int g = lane & 7;                       // row group
+  const unsigned gmask = 0xffu << (lane & ~7);
   const bool own = c < kc;
   const int64_t node = blockIdx.x;
-  cta::zero_block(Rs, ldr, kc, kc);
+  for (int e = tid; e < ldr * kc; e += kWThreads) Rs[e] = 0.0;
   const int b1 = rp[node + 1];
   int b = rp[node];
   bool parent = kp > 0;
@@ -179,14 +191,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restric
     int rows = 0;
     __syncthreads();
     if (parent) {
-      cta::gemm_tc<false, true>(st, ldst, Rpar + (node >> 1) * int64_t(kp) * kp, kp,
-                                E + node * int64_t(lde) * kp, lde, kp, kc, kp);
+      const double* Pr = P + node * int64_t(kp) * kc;
+      for (int e = tid; e < kp * kc; e += kWThreads) {
+        const int j = e / kp, i = e - j * kp;
+        st[i + j * ldst] = Pr[e];
+      }
       rows = kp;
       parent = false;
     }
     for (int nb = 0; b < b1 && rows + kc <= kChunkRows && nb < per_chunk_blocks; ++b, ++nb) {
       const double* Sb = S + int64_t(b) * lds * kc;
-      for (int e = threadIdx.x; e < kc * kc; e += kThreads) {
+      for (int e = tid; e < kc * kc; e += kWThreads) {
         const int j = e / kc, i = e - j * kc;  // S(i, j) -> stack row rows + j, column i
         st[rows + j + i * ldst] = Sb[i + int64_t(j) * lds];
       }
@@ -196,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restric
     double B[kRowsPerThread];
 #pragma unroll
     for (int r = 0; r < kRowsPerThread; ++r) {
-      const int i = g + 4 * r;
+      const int i = g + 8 * r;
       B[r] = (own && i < rows) ? st[i + c * ldst] : 0.0;
     }
     // ---- structured Householder on [R; B] ----
@@ -206,8 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restric
 #pragma unroll
         for (int r = 0; r < kRowsPerThread; ++r) q4[r & 3] += B[r] * B[r];
         double sq = (q4[0] + q4[1]) + (q4[2] + q4[3]);
-        sq += __shfl_xor_sync(0xfu << (lane & ~3), sq, 1, 4);
-        sq += __shfl_xor_sync(0xfu << (lane & ~3), sq, 2, 4);
+        sq += __shfl_xor_sync(gmask, sq, 1, 8);
+        sq += __shfl_xor_sync(gmask, sq, 2, 8);
+        sq += __shfl_xor_sync(gmask, sq, 4, 8);
         const double al = Rs[j + j * ldr];
         const double nx = sqrt(al * al + sq);
         double tj = 0.0, sc = 0.0, be = al;
@@ -218,8 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restric
         }
 #pragma unroll
         for (int r = 0; r < kRowsPerThread; ++r) {
-          const int i = g + 4 * r;
-          if (i < kChunkRows) vb[i] = B[r] * sc;
+          vb[g + 8 * r] = B[r] * sc;
           B[r] = 0.0;  // below the new diagonal: the reflector, not part of R
         }
         if (g == 0) {
@@ -232,21 +247,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_weights(const double* __restric
       if (own && c > j && tj != 0.0) {
         double w4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) w4[r & 3] += vb[g + 4 * r] * B[r];
+        for (int r = 0; r < kRowsPerThread; ++r) w4[r & 3] += vb[g + 8 * r] * B[r];
         double w = (w4[0] + w4[1]) + (w4[2] + w4[3]);
-        w += __shfl_xor_sync(0xfu << (lane & ~3), w, 1, 4);
-        w += __shfl_xor_sync(0xfu << (lane & ~3), w, 2, 4);
+        w += __shfl_xor_sync(gmask, w, 1, 8);
+        w += __shfl_xor_sync(gmask, w, 2, 8);
+        w += __shfl_xor_sync(gmask, w, 4, 8);
         const double d = (Rs[j + c * ldr] + w) * tj;
 #pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) B[r] -= vb[g + 4 * r] * d;
-        __syncwarp(0xfu << (lane & ~3));
+        for (int r = 0; r < kRowsPerThread; ++r) B[r] -= vb[g + 8 * r] * d;
+        __syncwarp(gmask);
         if (g == 0) Rs[j + c * ldr] -= d;
       }
       __syncthreads();
     }
   }
   __syncthreads();
-  cta::extract_r(Rs, ldr, kc, Rout + node * int64_t(kc) * kc, kc, flip);
+  // R with non-negative diagonal (linalg.hpp:100-113)
+  double* Ro = Rout + node * int64_t(kc) * kc;
+  for (int e = tid; e < kc * kc; e += kWThreads) {
+    const int j = e / kc, i = e - j * kc;
+    const double v = i <= j ? Rs[i + j * ldr] : 0.0;
+    Ro[i + j * kc] = Rs[i + i * ldr] < 0.0 ? -v : v;
+  }
 }
 
 // One-sided Jacobi SVD of W (rows x cols, smem, ld = rows) into Uout (global,
@@ -299,6 +321,8 @@ __device__ int svd_to(double* W, int rows, int cols, double* work, double* Uout,
   return rank;
 }
 
+constexpr int kSvdScratch = 128 + 64 + 16 + 72;  // nrm, tau, red, ord/flag (ints)
+
 __device__ void check_finite(const double* W, int n, int* bad) {
   for (int e = threadIdx.x; e < n; e += kThreads)
     if (!isfinite(W[e])) *bad = 1;
@@ -312,13 +336,13 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_svd(const double* __res
                                                              int* __restrict__ kmax, int* __restrict__ bad) {
   extern __shared__ double sm[];
   const int s = m < k ? m : k;
-  double* W = sm;                       // m x (k+1)
-  double* work = W + m * (k + 1);       // (k x m) + pad for the wide case
-  double* nrm = work + (k + 1) * (m + 1);
+  double* nrm = sm;                     // scratch first (kSvdScratch doubles)
   double* tau = nrm + 128;
   double* red = tau + 64;
   int* ord = reinterpret_cast<int*>(red + 16);
   int* flag = ord + 128;
+  double* W = sm + kSvdScratch;         // m x (k+1)
+  double* work = W + m * (k + 1);       // wide case only: (k+1) x (m+1)
   const int64_t i = blockIdx.x;
   cta::gemm_tc<false, true>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
   __syncthreads();
@@ -360,22 +384,21 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_svd(
   extern __shared__ double sm[];
   const int zr = 2 * ktc;
   const int s = zr < kp ? zr : kp;
-  double* Z = sm;                        // zr x kp
-  double* W = Z + zr * kp;               // zr x (kp + 1)
-  double* work = W + zr * (kp + 1);      // (kp x zr) or G (zr x zr+1)
-  double* nrm = work + (kp + 1) * (zr + 1);
+  double* nrm = sm;                      // scratch first (kSvdScratch doubles)
   double* tau = nrm + 128;
   double* red = tau + 64;
   int* ord = reinterpret_cast<int*>(red + 16);
   int* flag = ord + 128;
+  double* W = sm + kSvdScratch;          // zr x (kp + 1)
+  double* work = W + zr * (kp + 1);      // wide case only: (kp+1) x (zr+1)
   const int64_t p = blockIdx.x;
   const int64_t es = int64_t(lde) * kp;
+  double* Z = Zout + p * int64_t(zr) * kp;  // Z lives in global memory (L2)
   for (int ci = 0; ci < 2; ++ci) {
     const int64_t c = 2 * p + ci;
     cta::gemm_tc<false, false>(Z + ci * ktc, zr, Tt + c * int64_t(ktc) * kc, ktc, E + c * es, lde, ktc, kp, kc);
   }
   __syncthreads();
-  cta::copy_block(Zout + p * int64_t(zr) * kp, zr, Z, zr, zr, kp);
   cta::gemm_tc<false, true>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
   __syncthreads();
   check_finite(W, zr * kp, bad);
@@ -577,12 +600,18 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
     flops += fl.gemm(double(A.nodes(l)), kp, kc, kp) + fl.qr(double(A.nodes(l)), ld_ref, kc);
     require(ld_ref >= kc, "qr_r_only_batched: requires rows >= cols");
     if (kc == 0) continue;
-    const size_t sm = (size_t(cta::sld(kc)) * kc + size_t(cta::sld(kChunkRows)) * kc + kChunkRows + 32) *
-                          sizeof(double) + 64 * sizeof(int);
+    DevBuf<double> Pbuf;
+    if (kp > 0) {
+      Pbuf.alloc(size_t(A.nodes(l)) * kp * kc);
+      k_weights_parent<<<unsigned(A.nodes(l)), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
+                                                                  R.at(l - 1), Pbuf.p);
+      H2B_CUDA(cudaGetLastError());
+    }
+    const size_t sm = (size_t(cta::sld(kc)) * kc + size_t(cta::sld(kChunkRows)) * kc + kChunkRows + 8) *
+                      sizeof(double);
     check_smem(sm, "generate_weight_tree");
     set_smem(k_weights, sm);
-    k_weights<<<unsigned(A.nodes(l)), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
-                                                        R.at(l - 1), L.rp, L.val, L.ld, R.at(l));
+    k_weights<<<unsigned(A.nodes(l)), kWThreads, sm, s>>>(Pbuf.p, kc, kp, L.rp, L.val, L.ld, R.at(l));
     H2B_CUDA(cudaGetLastError());
   }
 }
@@ -630,8 +659,8 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     en.alloc(nl);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
-      const size_t sm = (size_t(m) * (kq + 1) + size_t(kq + 1) * (m + 1) + 128 + 64 + 16) * sizeof(double) +
-                        256 * sizeof(int) + 64;
+      const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + (m < kq ? size_t(kq + 1) * (m + 1) : 0)) *
+                        sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_leaf_svd, sm);
       k_trunc_leaf_svd<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, R.at(q), Uq.p, sg.p, eps,
@@ -667,8 +696,8 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     en.alloc(np);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
-      const size_t sm = (size_t(zr) * kp + size_t(zr) * (kp + 1) + size_t(kp + 1) * (zr + 1) + 128 + 64 + 16) *
-                            sizeof(double) + 256 * sizeof(int) + 64;
+      const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + (zr < kp ? size_t(kp + 1) * (zr + 1) : 0)) *
+                        sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_level_svd, sm);
       k_trunc_level_svd<<<unsigned(np), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, ktc,
