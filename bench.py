@@ -481,6 +481,12 @@ def main():
 
     # ---- 16-vector FP64-MMA mat-vec on the same matrix (BASELINE configs[3]) ----
     multi = multi16_run(A, torch, args.steps)
+    # ---- accuracy of the device-built matrix: exact-kernel sampled validation
+    #      (validate.hpp:26-62; acceptance c1 bound 1e-7 in 2D) ----
+    t0 = time.time()
+    acc = {"sampled_rel_err": h2.validate_sampled(A, 1e-3, 1), "fraction": 1e-3,
+           "bound_2d": 1e-7}
+    acc["seconds"] = round(time.time() - t0, 2)
 
     # ---- compression GFLOP/s (metric's second half): C3, 3D n=2^20 k=64, eps 1e-6 ----
     A.close()
@@ -535,6 +541,7 @@ def main():
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
         "multi16": multi,
+        "accuracy": acc,
         "compression": comp,
     }
     print(json.dumps(line), flush=True)

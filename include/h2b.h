@@ -179,6 +179,13 @@ H2B_API h2b_status h2b_compress(h2b_matrix* A, double eps, h2b_compress_report* 
  * level-concatenated ranks[l]^2 per node) when non-NULL. */
 H2B_API h2b_status h2b_orthogonalize(h2b_matrix* A, double* t_out);
 
+/* validate_sampled (validate.hpp:26-62) on the device: relative mat-vec error
+ * against the exact kernel exp(-|p_i - p_j|/ell) on ceil(fraction n) sampled
+ * rows, x = random_vector(n, seed).  points: n x dim, original order (NULL:
+ * the points h2b_matrix_build generated; dim/ell <= 0 then mean "stored"). */
+H2B_API h2b_status h2b_validate_sampled(h2b_matrix* A, const double* points, int dim, double ell,
+                                        double fraction, uint64_t seed, double* err);
+
 /* ---- subtree-partitioned multi-GPU mat-vec ----
  * nparts = 2^s GPUs; partition `part` owns the leaves [part n/nparts, (part+1) n/nparts)
  * in cluster order, the basis nodes and coupling/dense block rows of its top-level

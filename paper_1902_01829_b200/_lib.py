@@ -100,6 +100,8 @@ _SIGS = {
     "h2b_workspace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "h2b_part_upsweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "h2b_part_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "h2b_validate_sampled": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double,
+                                       C.c_uint64, C.POINTER(C.c_double)]),
     "h2b_set_phase_timing": (C.c_int, [C.c_void_p, C.c_int]),
 }
 

@@ -261,5 +261,20 @@ def orthogonalize_basis(A: H2Matrix) -> np.ndarray:
     return out
 
 
+def validate_sampled(A: H2Matrix, fraction: float, seed: int = 1, points=None, dim: int = 0,
+                     ell: float = 0.0) -> float:
+    """validate_sampled(A, points, spec, fraction, seed) (validate.hpp:26-62) on the
+    device; points default to the ones construct() generated on the device."""
+    pp = None
+    if points is not None:
+        points = np.ascontiguousarray(points, dtype=np.float64)
+        dim = points.shape[1]
+        pp = points.ctypes.data
+    err = C.c_double()
+    _lib.check(_lib.load().h2b_validate_sampled(A._h, pp, int(dim), float(ell), float(fraction),
+                                                int(seed), C.byref(err)))
+    return err.value
+
+
 def device_count() -> int:
     return int(_lib.load().h2b_device_count())

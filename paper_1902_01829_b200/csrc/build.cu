@@ -420,6 +420,10 @@ h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, in
   std::vector<double> pc(size_t(cfg.n) * cfg.dim);
   for (int64_t t = 0; t < cfg.n; ++t)
     for (int a = 0; a < cfg.dim; ++a) pc[t * cfg.dim + a] = X[int64_t(T.perm[t]) * cfg.dim + a];
+  A->pts_orig.alloc(X.size());
+  H2B_CUDA(cudaMemcpyAsync(A->pts_orig.p, X.data(), X.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  A->pts_dim = cfg.dim;
+  A->ell = cfg.ell;
   DevBuf<double> dpts;
   dpts.alloc(pc.size());
   H2B_CUDA(cudaMemcpyAsync(dpts.p, pc.data(), pc.size() * sizeof(double), cudaMemcpyHostToDevice, s));

@@ -331,6 +331,13 @@ void hmv_device(Matrix& A, const double* x, double* y, double alpha, double beta
   if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
 }
 
+void hmv_for_validation(Matrix& A, const double* x, double* y, cudaStream_t s) {
+  hmv_device(A, x, y, 1.0, 0.0, s);
+}
+
+double validate_sampled_device(Matrix& A, const double* points_host, int dim, double ell,
+                               double fraction, uint64_t seed);
+
 void ensure_host_stage(Matrix& A, size_t n) {
   if (A.h_stage_n >= n) return;
   if (A.h_stage) cudaFreeHost(A.h_stage);
@@ -721,6 +728,21 @@ h2b_status h2b_part_finish(h2b_matrix* Ah, double* y_slice, void* stream) {
     for (int l = 1; l <= A.q; ++l) launch_down_level(A, l, s, A.own_begin(l), A.own_end(l));
     launch_down_leaf(A, y_slice, 1.0, 0.0, false, s);
     if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
+  });
+}
+
+h2b_status h2b_validate_sampled(h2b_matrix* Ah, const double* points, int dim, double ell,
+                                double fraction, uint64_t seed, double* err) {
+  return guarded([&] {
+    require(Ah && err, "null argument");
+    Matrix& A = *Ah;
+    whole(A, "h2b_validate_sampled");
+    DeviceGuard g(A.device);
+    if (!points) {
+      if (dim <= 0) dim = A.pts_dim;
+      if (ell <= 0) ell = A.ell;
+    }
+    *err = validate_sampled_device(A, points, dim, ell, fraction, seed);
   });
 }
 

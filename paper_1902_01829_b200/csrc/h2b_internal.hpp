@@ -128,6 +128,11 @@ struct Matrix {
   // HmvContext analogue (hmv.hpp:161-172): one workspace per handle.
   DevBuf<double> xc, yc, xhat, yhat, xs, ys;
   DevBuf<double> xc16, yc16, xh16, yh16;  // 16-vector panels (k_hmv_mv.cu), lazily allocated
+  // Points (original order) + kernel of a device-built matrix, for
+  // h2b_validate_sampled (validate.cu).
+  DevBuf<double> pts_orig;
+  int pts_dim = 0;
+  double ell = 0.0;
   double* h_stage = nullptr;        // pinned host staging for host-pointer calls
   size_t h_stage_n = 0;
 

@@ -67,3 +67,18 @@ def test_invalid_arguments(gpu):
     A = h2.H2Matrix.construct(2, 1024)
     with pytest.raises(h2.H2bInvalidArgument, match="leading dimension"):
         h2.hmv_multi(A, np.zeros((2, 512)))  # columns shorter than n
+
+
+def test_validate_sampled_matches_reference(gpu, ref):
+    """validate_sampled on the device == the reference's (acceptance c1:
+    2D n=2^14 fraction 0.1 -> 3.44e-8; 3D -> 5.16e-5)."""
+    for dim, n in [(2, 1 << 14), (3, 1 << 14)]:
+        R = ref.construct(dim, n)
+        import ctypes as C
+        err_ref = C.c_double()
+        assert ref.lib.ref_validate_sampled(R.h, 0.1, 1, C.byref(err_ref)) == 0
+        A = h2.H2Matrix.construct(dim, n)
+        err = h2.validate_sampled(A, 0.1, 1)
+        assert err == pytest.approx(err_ref.value, rel=1e-6), (dim, err, err_ref.value)
+        pts = ref.points(dim, n)
+        assert h2.validate_sampled(A, 0.1, 1, points=pts, ell=0.1 if dim == 2 else 0.2) == pytest.approx(err, rel=1e-12)
