@@ -59,7 +59,9 @@ def gather_xhat(plan: PartitionPlan, xhat, allgather):
     for l in plan.gather_levels():
         off, length, chunk = plan.level_slice(l)
         level = xhat[off:off + length]
-        allgather(level, level[plan.part * chunk:(plan.part + 1) * chunk])
+        # the owned slice is copied out first: no reliance on in-place
+        # all-gather semantics of the backend (the slice is <= 1/P of a level)
+        allgather(level, level[plan.part * chunk:(plan.part + 1) * chunk].clone())
 
 
 class DistributedH2Matrix:
