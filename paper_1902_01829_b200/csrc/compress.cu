@@ -288,30 +288,45 @@ __device__ int svd_to(double* W, int rows, int cols, double* work, double* Uout,
     cta::jacobi(W, rows, rows, n, flag);
     cta::jacobi_finish(W, rows, rows, n, s, Uout, ldu, sig, nrm, ord);
   } else {
-    // wide: QR of W^T (cols x rows), Jacobi on R^T (linalg.hpp:195-207)
-    double* At = work;  // cols x rows, ld cols
-    for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
-      const int j = e / rows, i = e - j * rows;
-      At[j + i * cols] = W[i + j * rows];
-    }
-    __syncthreads();
-    cta::householder(At, cols, cols, rows, tau, red);
-    int* flip = ord;  // reuse as scratch, overwritten by jacobi_finish
-    cta::extract_r(At, cols, rows, W, rows, flip);  // R (rows x rows) into W
-    __syncthreads();
-    double* G = work;  // rows x (rows + 1)
-    for (int e = threadIdx.x; e < rows * rows; e += kThreads) {
-      const int j = e / rows, i = e - j * rows;
-      G[i + j * rows] = W[j + i * rows];
+    // wide (rows < cols): the left singular vectors of W are the accumulated
+    // right rotations of one-sided Jacobi on W^T.  Run it on [W^T; I_rows]
+    // (dots over the first `cols` rows only) -- no QR needed (the reference
+    // takes the QR-of-W^T route, linalg.hpp:195-207; same subspaces/sigmas).
+    const int ldg = cols + rows;
+    double* G = work;  // (cols + rows) x (rows + 1)
+    for (int e = threadIdx.x; e < ldg * rows; e += kThreads) {
+      const int j = e / ldg, i = e - j * ldg;
+      G[i + j * ldg] = i < cols ? W[j + i * rows] : (i - cols == j ? 1.0 : 0.0);
     }
     int n = rows;
     if (n & 1) {
-      for (int i = threadIdx.x; i < rows; i += kThreads) G[i + rows * rows] = 0.0;
+      for (int i = threadIdx.x; i < ldg; i += kThreads) G[i + rows * ldg] = 0.0;
       ++n;
     }
     __syncthreads();
-    cta::jacobi(G, rows, rows, n, flag);
-    cta::jacobi_finish(G, rows, rows, n, s, Uout, ldu, sig, nrm, ord);
+    cta::jacobi(G, ldg, ldg, n, flag, cols);
+    // sigma = column norms over the W^T part; U column j = accumulated rotation
+    for (int j = cta::warp(); j < n; j += cta::kWarps) {
+      double t = 0.0;
+      for (int i = cta::lane(); i < cols; i += 32) t += G[i + j * ldg] * G[i + j * ldg];
+      t = cta::warp_sum(t);
+      if (cta::lane() == 0) nrm[j] = sqrt(t);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += kThreads) {
+      int rk = 0;
+      const double v = nrm[j];
+      for (int i = 0; i < n; ++i) rk += (nrm[i] > v) || (nrm[i] == v && i < j);
+      ord[rk] = j;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < s; j += kThreads) sig[j] = nrm[ord[j]];
+    for (int e = threadIdx.x; e < rows * s; e += kThreads) {
+      const int j = e / rows, i = e - j * rows;
+      const int src = ord[j];
+      Uout[i + int64_t(j) * ldu] = nrm[src] > 0.0 ? G[cols + i + src * ldg] : 0.0;
+    }
+    __syncthreads();
   }
   int rank = 0;
   if (threadIdx.x == 0) {
@@ -659,7 +674,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     en.alloc(nl);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
-      const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + (m < kq ? size_t(kq + 1) * (m + 1) : 0)) *
+      const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + (m < kq ? size_t(kq + m) * (m + 1) : 0)) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_leaf_svd, sm);
@@ -696,7 +711,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     en.alloc(np);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
-      const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + (zr < kp ? size_t(kp + 1) * (zr + 1) : 0)) *
+      const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + (zr < kp ? size_t(kp + zr) * (zr + 1) : 0)) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_level_svd, sm);

@@ -258,44 +258,53 @@ __device__ __forceinline__ void rr_pair(int n, int r, int s, int& p, int& q) {
 }
 
 // One-sided Jacobi on the columns of G (rows x n, n even; pad with a zero
-// column for odd counts).  flag: one int of smem.  A warp owns one column pair
-// per step and keeps it in registers (RPL rows per lane) between the three
-// dot products and the rotation.
-template <int RPL>
-__device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag) {
+// column for odd counts).  flag: one int of smem.  Eight lanes own one
+// column pair (four pairs per warp, 32 pairs per CTA step) and keep it in
+// registers (RPT rows per lane) between the three dot products (reduced with
+// width-8 shuffles) and the rotation.
+template <int RPT>
+__device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag, int rows_dot) {
   const double tol = 2.220446049250313e-16 * 16.0;
+  const int sub = lane() & 7;
+  const int slot0 = warp() * 4 + (lane() >> 3);
+  const unsigned gmask = 0xffu << (lane() & 24);
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int r = 0; r < n - 1; ++r) {
-      for (int s = warp(); s < n / 2; s += kWarps) {
+      for (int s = slot0; s < n / 2; s += kWarps * 4) {
         int p, q;
         rr_pair(n, r, s, p, q);
         double* gp = G + p * ldg;
         double* gq = G + q * ldg;
-        double u[RPL], w[RPL];
+        double u[RPT], w[RPT];
         double a = 0.0, b = 0.0, d = 0.0;
 #pragma unroll
-        for (int t = 0; t < RPL; ++t) {
-          const int i = lane() + 32 * t;
+        for (int t = 0; t < RPT; ++t) {
+          const int i = sub + 8 * t;
           u[t] = i < rows ? gp[i] : 0.0;
           w[t] = i < rows ? gq[i] : 0.0;
-          a += u[t] * u[t];
-          b += w[t] * w[t];
-          d += u[t] * w[t];
+          if (i < rows_dot) {  // rows beyond rows_dot only accumulate rotations
+            a += u[t] * u[t];
+            b += w[t] * w[t];
+            d += u[t] * w[t];
+          }
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        d = warp_sum(d);
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) {
+          a += __shfl_xor_sync(gmask, a, m, 8);
+          b += __shfl_xor_sync(gmask, b, m, 8);
+          d += __shfl_xor_sync(gmask, d, m, 8);
+        }
         if (fabs(d) <= tol * sqrt(a * b) || d == 0.0) continue;
-        if (lane() == 0) *flag = 1;
+        if (sub == 0) *flag = 1;
         const double z = (b - a) / (2.0 * d);
         const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
         const double cs = 1.0 / sqrt(1.0 + t * t);
         const double sn = cs * t;
 #pragma unroll
-        for (int k = 0; k < RPL; ++k) {
-          const int i = lane() + 32 * k;
+        for (int k = 0; k < RPT; ++k) {
+          const int i = sub + 8 * k;
           if (i < rows) {
             gp[i] = cs * u[k] - sn * w[k];
             gq[i] = sn * u[k] + cs * w[k];
@@ -310,15 +319,19 @@ __device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag) {
   __syncthreads();
 }
 
-__device__ inline void jacobi(double* G, int ldg, int rows, int n, int* flag) {
+// rows_dot < rows: the dot products (and hence the rotations) are defined by
+// the first rows_dot rows; the remaining rows (e.g. an appended identity)
+// only accumulate the rotations.
+__device__ inline void jacobi(double* G, int ldg, int rows, int n, int* flag, int rows_dot = -1) {
+  if (rows_dot < 0) rows_dot = rows;
   if (rows <= 32)
-    jacobi_t<1>(G, ldg, rows, n, flag);
+    jacobi_t<4>(G, ldg, rows, n, flag, rows_dot);
   else if (rows <= 64)
-    jacobi_t<2>(G, ldg, rows, n, flag);
+    jacobi_t<8>(G, ldg, rows, n, flag, rows_dot);
   else if (rows <= 128)
-    jacobi_t<4>(G, ldg, rows, n, flag);
+    jacobi_t<16>(G, ldg, rows, n, flag, rows_dot);
   else
-    jacobi_t<8>(G, ldg, rows, n, flag);
+    jacobi_t<32>(G, ldg, rows, n, flag, rows_dot);
 }
 
 // After jacobi(): sigma[j] (descending, stable) and U (rows x s) with unit (or
