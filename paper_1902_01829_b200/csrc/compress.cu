@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <vector>
 
@@ -154,120 +155,167 @@ __global__ void __launch_bounds__(kThreads) k_weights_parent(const double* __res
 }
 
 // R^l_r = R-factor of [P_r ; S_rb^T ...] (compression.hpp:213-256) by
-// streaming TSQR over the UNPADDED stack.  The running R (kc x kc, upper
-// triangular) stays in smem; each chunk of <= kChunkRows stack rows lives in
-// registers -- thread (warp w, lane t) of a 512-thread CTA owns column
-// c = 4w + t/8 and rows g + 8r (g = t%8) -- and [R; chunk] is
-// re-triangularised by a structured Householder pass whose reflectors touch
-// one row of R plus the chunk.
-constexpr int kWThreads = 512;
-constexpr int kChunkRows = 128;
-constexpr int kRowsPerThread = kChunkRows / 8;
-__global__ void __launch_bounds__(kWThreads, 1) k_weights(const double* __restrict__ P, int kc, int kp,
+// streaming TSQR over the UNPADDED stack, ONE WARP PER NODE (no block
+// barriers).  Lane L owns stack columns c_t = L + 32 t (t < NCOL); the
+// current chunk -- CR consecutive rows of the stack: the parent rows P_r,
+// then each transposed coupling block S_rb^T in CR-row pieces (the warp walks
+// rows c of S_rb, so every load instruction covers 32 consecutive doubles) --
+// lives in registers, the running R (upper triangular, packed column-wise) in
+// shared memory.  [R; chunk] is re-triangularised by a structured
+// Householder pass whose reflector j touches row j of R plus the chunk.
+//
+// Per reflector the owner of column j publishes its RAW chunk column and
+// alpha = R[j,j] to shared memory; every lane then forms the Householder
+// scalars itself (||x||^2, one sqrt, one division) in parallel with its dot
+// products and applies the reflector to its own columns.  Arithmetic as
+// linalg.hpp:48-75: beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta,
+// v = x / (alpha - beta) below the unit entry.
+constexpr int kWWarps = 4;  // nodes (warps) per CTA
+template <int NCOL, int CR>
+__global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __restrict__ P, int kc, int kp,
                                                           const int32_t* __restrict__ rp,
                                                           const double* __restrict__ S, int lds,
-                                                          double* __restrict__ Rout) {
+                                                          double* __restrict__ Rout, int64_t nnodes) {
+  constexpr int XS = CR + 2;  // publish slot: raw column, alpha
   extern __shared__ double sm[];
-  const int ldr = cta::sld(kc);
-  const int ldst = cta::sld(kChunkRows);
-  double* Rs = sm;                       // ldr x kc, running R
-  double* st = Rs + ldr * kc;            // ldst x kc chunk staging
-  double* vb = st + ldst * kc;           // kChunkRows reflector entries
-  double* misc = vb + kChunkRows;        // [0] = tau
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int c = (tid >> 5) * 4 + (lane >> 3);  // owned column
-  const int g = lane & 7;                       // row group
-  const unsigned gmask = 0xffu << (lane & ~7);
-  const bool own = c < kc;
-  const int64_t node = blockIdx.x;
-  for (int e = tid; e < ldr * kc; e += kWThreads) Rs[e] = 0.0;
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int rsz = (((kc * (kc + 1)) / 2 + 1) & ~1);
+  double* Rp = sm + wid * (rsz + 2 * XS);  // packed R: column c at c(c+1)/2
+  double* xb = Rp + rsz;                   // 2 x XS
+  const int64_t node = int64_t(blockIdx.x) * kWWarps + wid;
+  if (node >= nnodes) return;
+  for (int e = lane; e < rsz; e += 32) Rp[e] = 0.0;
+  int coff[NCOL];
+#pragma unroll
+  for (int t = 0; t < NCOL; ++t) {
+    const int c = lane + 32 * t;
+    coff[t] = (c * (c + 1)) >> 1;
+  }
   const int b1 = rp[node + 1];
   int b = rp[node];
-  bool parent = kp > 0;
-  const int per_chunk_blocks = kChunkRows / kc;
-  while (parent || b < b1) {
-    // ---- stage one chunk: [parent rows][blocks ...] ----
-    int rows = 0;
-    __syncthreads();
-    if (parent) {
-      const double* Pr = P + node * int64_t(kp) * kc;
-      for (int e = tid; e < kp * kc; e += kWThreads) {
-        const int j = e / kp, i = e - j * kp;
-        st[i + j * ldst] = Pr[e];
+  int prow = 0;  // next parent row
+  int brow = 0;  // next row of block b's transpose
+  double B[NCOL][CR];
+  int jg = 0;    // reflector counter (selects the publish slot)
+  __syncwarp();
+  while (prow < kp || b < b1) {
+    // ---- load the next CR-row chunk ----
+    if (prow < kp) {
+      const int nr = min(CR, kp - prow);
+#pragma unroll
+      for (int t = 0; t < NCOL; ++t) {
+        const int c = lane + 32 * t;
+        const double* src = P + node * int64_t(kp) * kc + int64_t(c) * kp + prow;
+#pragma unroll
+        for (int i = 0; i < CR; ++i) B[t][i] = (c < kc && i < nr) ? src[i] : 0.0;
       }
-      rows = kp;
-      parent = false;
-    }
-    for (int nb = 0; b < b1 && rows + kc <= kChunkRows && nb < per_chunk_blocks; ++b, ++nb) {
-      const double* Sb = S + int64_t(b) * lds * kc;
-      for (int e = tid; e < kc * kc; e += kWThreads) {
-        const int j = e / kc, i = e - j * kc;  // S(i, j) -> stack row rows + j, column i
-        st[rows + j + i * ldst] = Sb[i + int64_t(j) * lds];
-      }
-      rows += kc;
-    }
-    __syncthreads();
-    double B[kRowsPerThread];
+      prow += nr;
+    } else {
+      const int nr = min(CR, kc - brow);
 #pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r) {
-      const int i = g + 8 * r;
-      B[r] = (own && i < rows) ? st[i + c * ldst] : 0.0;
-    }
-    // ---- structured Householder on [R; B] ----
-    for (int j = 0; j < kc; ++j) {
-      if (c == j) {
-        double q4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int t = 0; t < NCOL; ++t) {
+        const int c = lane + 32 * t;
+        const double* src = S + int64_t(b) * lds * kc + c + int64_t(brow) * lds;
 #pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) q4[r & 3] += B[r] * B[r];
-        double sq = (q4[0] + q4[1]) + (q4[2] + q4[3]);
-        sq += __shfl_xor_sync(gmask, sq, 1, 8);
-        sq += __shfl_xor_sync(gmask, sq, 2, 8);
-        sq += __shfl_xor_sync(gmask, sq, 4, 8);
-        const double al = Rs[j + j * ldr];
-        const double nx = sqrt(al * al + sq);
-        double tj = 0.0, sc = 0.0, be = al;
-        if (nx != 0.0) {
-          be = al >= 0.0 ? -nx : nx;
-          tj = (be - al) / be;
-          sc = 1.0 / (al - be);
-        }
-#pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) {
-          vb[g + 8 * r] = B[r] * sc;
-          B[r] = 0.0;  // below the new diagonal: the reflector, not part of R
-        }
-        if (g == 0) {
-          misc[0] = tj;
-          Rs[j + j * ldr] = be;
+        for (int i = 0; i < CR; ++i) {
+          B[t][i] = (c < kc && i < nr) ? __ldcs(src) : 0.0;
+          src += lds;
         }
       }
-      __syncthreads();
-      const double tj = misc[0];
-      if (own && c > j && tj != 0.0) {
-        double w4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) w4[r & 3] += vb[g + 8 * r] * B[r];
-        double w = (w4[0] + w4[1]) + (w4[2] + w4[3]);
-        w += __shfl_xor_sync(gmask, w, 1, 8);
-        w += __shfl_xor_sync(gmask, w, 2, 8);
-        w += __shfl_xor_sync(gmask, w, 4, 8);
-        const double d = (Rs[j + c * ldr] + w) * tj;
-#pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) B[r] -= vb[g + 8 * r] * d;
-        __syncwarp(gmask);
-        if (g == 0) Rs[j + c * ldr] -= d;
+      brow += nr;
+      if (brow >= kc) {
+        brow = 0;
+        ++b;
       }
-      __syncthreads();
+    }
+    if (lane == 0) {  // column 0 opens the chunk
+      double* x = xb + (jg & 1) * XS;
+#pragma unroll
+      for (int i = 0; i < CR; i += 2) *reinterpret_cast<double2*>(x + i) = make_double2(B[0][i], B[0][i + 1]);
+      x[CR] = Rp[0];
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < kc; ++j, ++jg) {
+      const double* x = xb + (jg & 1) * XS;
+      double* xn = xb + ((jg + 1) & 1) * XS;
+      // ||x||^2 and the dot products with the raw column (branch-free: every
+      // lane runs the same straight-line code, dead columns get f = 0)
+      double q[4] = {0.0, 0.0, 0.0, 0.0};
+      double w[NCOL][2];
+#pragma unroll
+      for (int t = 0; t < NCOL; ++t) w[t][0] = w[t][1] = 0.0;
+#pragma unroll
+      for (int i = 0; i < CR; i += 2) {
+        const double2 xx = *reinterpret_cast<const double2*>(x + i);
+        q[i & 3] = fma(xx.x, xx.x, q[i & 3]);
+        q[(i + 1) & 3] = fma(xx.y, xx.y, q[(i + 1) & 3]);
+#pragma unroll
+        for (int t = 0; t < NCOL; ++t) {
+          w[t][0] = fma(xx.x, B[t][i], w[t][0]);
+          w[t][1] = fma(xx.y, B[t][i + 1], w[t][1]);
+        }
+      }
+      const double al = x[CR];
+      const double nx = sqrt(fma(al, al, (q[0] + q[1]) + (q[2] + q[3])));
+      const double be = al >= 0.0 ? -nx : nx;
+      const double am = al - be;
+      const double r = 1.0 / (be * am);  // sc = 1/(al-be) = be r, tau = (be-al)/be = -am^2 r
+      const double sc = be * r;
+      const double tau = -(am * am) * r;
+      double f[NCOL];
+#pragma unroll
+      for (int t = 0; t < NCOL; ++t) {
+        const int c = lane + 32 * t;
+        f[t] = 0.0;
+        if (c > j && c < kc && nx != 0.0) {
+          const double d = fma(sc, w[t][0] + w[t][1], Rp[coff[t] + j]) * tau;
+          Rp[coff[t] + j] -= d;
+          f[t] = sc * d;
+        }
+        if (c == j && nx != 0.0) {
+          Rp[coff[t] + j] = be;
+          f[t] = 1.0;  // x == this column: B - x = 0 exactly (it becomes the reflector)
+        }
+      }
+      asm volatile("" ::: "memory");  // re-read x below instead of holding CR more registers
+#pragma unroll
+      for (int i = 0; i < CR; i += 2) {
+        const double2 xx = *reinterpret_cast<const double2*>(x + i);
+#pragma unroll
+        for (int t = 0; t < NCOL; ++t) {
+          B[t][i] = fma(-xx.x, f[t], B[t][i]);
+          B[t][i + 1] = fma(-xx.y, f[t], B[t][i + 1]);
+        }
+      }
+      // next owner hands over its updated column
+      const int jn = j + 1;
+      if (jn < kc && lane == (jn & 31)) {
+        if (jn < 32) {
+#pragma unroll
+          for (int i = 0; i < CR; i += 2)
+            *reinterpret_cast<double2*>(xn + i) = make_double2(B[0][i], B[0][i + 1]);
+          xn[CR] = Rp[coff[0] + jn];
+        } else {
+#pragma unroll
+          for (int i = 0; i < CR; i += 2)
+            *reinterpret_cast<double2*>(xn + i) = make_double2(B[NCOL - 1][i], B[NCOL - 1][i + 1]);
+          xn[CR] = Rp[coff[NCOL - 1] + jn];
+        }
+      }
+      __syncwarp();
     }
   }
-  __syncthreads();
-  // R with non-negative diagonal (linalg.hpp:100-113)
+  // R with non-negative diagonal (linalg.hpp:100-113); row i by lane, so the
+  // stores of one column are coalesced
   double* Ro = Rout + node * int64_t(kc) * kc;
-  for (int e = tid; e < kc * kc; e += kWThreads) {
-    const int j = e / kc, i = e - j * kc;
-    const double v = i <= j ? Rs[i + j * ldr] : 0.0;
-    Ro[i + j * kc] = Rs[i + i * ldr] < 0.0 ? -v : v;
+  for (int cc = 0; cc < kc; ++cc) {
+    const int ccoff = (cc * (cc + 1)) >> 1;
+    for (int i = lane; i < kc; i += 32) {
+      const double v = i <= cc ? Rp[ccoff + i] : 0.0;
+      Ro[i + int64_t(cc) * kc] = Rp[((i * (i + 1)) >> 1) + i] < 0.0 ? -v : v;
+    }
   }
 }
 
@@ -490,15 +538,15 @@ struct Timer {
 
 // Level-concatenated pool of per-node (rows[l] x cols[l]) matrices, ld = rows.
 struct TreePool {
-  DevBuf<double> buf;
+  TmpBuf<double> buf;
   std::vector<int64_t> off;
   std::vector<int> rows, cols;
-  void alloc(const Matrix& A, const std::vector<int>& r, const std::vector<int>& c) {
+  void alloc(const Matrix& A, const std::vector<int>& r, const std::vector<int>& c, cudaStream_t s) {
     rows = r;
     cols = c;
     off.assign(A.q + 2, 0);
     for (int l = 0; l <= A.q; ++l) off[l + 1] = off[l] + A.nodes(l) * int64_t(r[l]) * c[l];
-    buf.alloc(std::max<int64_t>(1, off[A.q + 1]));
+    buf.alloc(std::max<int64_t>(1, off[A.q + 1]), s);
   }
   double* at(int l) { return buf.p + off[l]; }
 };
@@ -507,7 +555,7 @@ struct TreePool {
 void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops) {
   const int q = A.q, m = A.m, kq = A.rank[q];
   require(m >= kq, "orthogonalize_basis: leaf_dim must be >= leaf rank");
-  T.alloc(A, A.rank, A.rank);
+  T.alloc(A, A.rank, A.rank, s);
   const int64_t nl = A.nodes(q);
   if (kq > 0) {
     const size_t sm = (2 * size_t(m) * kq + 64 + 16) * sizeof(double) + 64 * sizeof(int);
@@ -572,8 +620,8 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
   }
   if (!rows.empty()) {
     check_smem(smax, "project_coupling");
-    DevBuf<ProjRow> drows;
-    drows.alloc(rows.size());
+    TmpBuf<ProjRow> drows;
+    drows.alloc(rows.size(), s);
     H2B_CUDA(cudaMemcpyAsync(drows.p, rows.data(), rows.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
     set_smem(k_project, smax);
     k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows.p);
@@ -592,8 +640,8 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
 double sumsq(const double* v, int64_t n, cudaStream_t s) {
   if (n == 0) return 0.0;
   const int blocks = 1024;
-  DevBuf<double> part;
-  part.alloc(blocks);
+  TmpBuf<double> part;
+  part.alloc(blocks, s);
   k_sumsq<<<blocks, kThreads, 0, s>>>(v, n, part.p);
   H2B_CUDA(cudaGetLastError());
   std::vector<double> h(blocks);
@@ -606,7 +654,7 @@ double sumsq(const double* v, int64_t n, cudaStream_t s) {
 
 void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
   const int q = A.q;
-  R.alloc(A, A.rank, A.rank);
+  R.alloc(A, A.rank, A.rank, s);
   H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * A.rank[0] * A.rank[0], s));
   for (int l = 1; l <= q; ++l) {
     const int kc = A.rank[l], kp = A.rank[l - 1];
@@ -615,18 +663,24 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
     flops += fl.gemm(double(A.nodes(l)), kp, kc, kp) + fl.qr(double(A.nodes(l)), ld_ref, kc);
     require(ld_ref >= kc, "qr_r_only_batched: requires rows >= cols");
     if (kc == 0) continue;
-    DevBuf<double> Pbuf;
+    TmpBuf<double> Pbuf;
     if (kp > 0) {
-      Pbuf.alloc(size_t(A.nodes(l)) * kp * kc);
+      Pbuf.alloc(size_t(A.nodes(l)) * kp * kc, s);
       k_weights_parent<<<unsigned(A.nodes(l)), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
                                                                   R.at(l - 1), Pbuf.p);
       H2B_CUDA(cudaGetLastError());
     }
-    const size_t sm = (size_t(cta::sld(kc)) * kc + size_t(cta::sld(kChunkRows)) * kc + kChunkRows + 8) *
-                      sizeof(double);
-    check_smem(sm, "generate_weight_tree");
-    set_smem(k_weights, sm);
-    k_weights<<<unsigned(A.nodes(l)), kWThreads, sm, s>>>(Pbuf.p, kc, kp, L.rp, L.val, L.ld, R.at(l));
+    constexpr int CR = 32;
+    const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
+    const int64_t nn = A.nodes(l);
+    const unsigned grid = unsigned((nn + kWWarps - 1) / kWWarps);
+#define H2B_WEIGHTS(NCOL)                                                                          \
+  if ((kc > 32 ? 2 : 1) == NCOL) {                                                                 \
+    set_smem(k_weights<NCOL, CR>, sm);                                                             \
+    k_weights<NCOL, CR><<<grid, 32 * kWWarps, sm, s>>>(Pbuf.p, kc, kp, L.rp, L.val, L.ld, R.at(l), nn); \
+  }
+    H2B_WEIGHTS(1) H2B_WEIGHTS(2)
+#undef H2B_WEIGHTS
     H2B_CUDA(cudaGetLastError());
   }
 }
@@ -638,7 +692,7 @@ int read_kmax(int* d, cudaStream_t s) {
   return h;
 }
 
-double sum_host(const DevBuf<double>& d, int64_t n, cudaStream_t s) {
+double sum_host(const TmpBuf<double>& d, int64_t n, cudaStream_t s) {
   std::vector<double> h(n);
   if (n) H2B_CUDA(cudaMemcpyAsync(h.data(), d.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   H2B_CUDA(cudaStreamSynchronize(s));
@@ -656,22 +710,22 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   const std::vector<int> old = A.rank;
   std::vector<int> nr(q + 1, 0);
   std::vector<double> lev_e(q + 1, 0.0);
-  DevBuf<int> dk;
-  dk.alloc(2);  // [0] = kmax, [1] = non-finite flag
-  std::vector<DevBuf<double>> newtr(q + 1);
+  TmpBuf<int> dk;
+  dk.alloc(2, s);  // [0] = kmax, [1] = non-finite flag
+  std::vector<TmpBuf<double>> newtr(q + 1);
   std::vector<int> trows(q + 1, 0);
   // projection pool sized after the fact per level
-  std::vector<DevBuf<double>> Tlev(q + 1);
+  std::vector<TmpBuf<double>> Tlev(q + 1);
   const int64_t nl = A.nodes(q);
   DevBuf<double> newleaf;
   {
     const int kq = old[q];
     const int sl = std::min(m, kq);
     flops += fl.gemm(double(nl), m, kq, kq) + fl.svd(double(nl), m, kq);
-    DevBuf<double> Uq, sg, en;
-    Uq.alloc(std::max<int64_t>(1, nl * m * sl));
-    sg.alloc(std::max<int64_t>(1, nl * sl));
-    en.alloc(nl);
+    TmpBuf<double> Uq, sg, en;
+    Uq.alloc(std::max<int64_t>(1, nl * m * sl), s);
+    sg.alloc(std::max<int64_t>(1, nl * sl), s);
+    en.alloc(nl, s);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
       const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + (m < kq ? size_t(kq + m) * (m + 1) : 0)) *
@@ -689,7 +743,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     const int kt = std::min(flags[0], sl);
     nr[q] = kt;
     flops += fl.gemm(double(nl), kt, kq, m);
-    Tlev[q].alloc(std::max<int64_t>(1, nl * kt * kq));
+    Tlev[q].alloc(std::max<int64_t>(1, nl * kt * kq), s);
     const int ldn = pad2(m);
     newleaf.alloc(std::max<int64_t>(1, nl * ldn * kt));
     k_trunc_leaf_apply<<<unsigned(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq.p, sg.p,
@@ -704,11 +758,11 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     const int sl = std::min(zr, kp);
     flops += fl.gemm(double(A.nodes(l)), ktc, kp, kc) + fl.gemm(double(np), zr, kp, kp) +
              fl.svd(double(np), zr, kp);
-    DevBuf<double> Z, U, sg, en;
-    Z.alloc(std::max<int64_t>(1, np * zr * kp));
-    U.alloc(std::max<int64_t>(1, np * zr * sl));
-    sg.alloc(std::max<int64_t>(1, np * sl));
-    en.alloc(np);
+    TmpBuf<double> Z, U, sg, en;
+    Z.alloc(std::max<int64_t>(1, np * zr * kp), s);
+    U.alloc(std::max<int64_t>(1, np * zr * sl), s);
+    sg.alloc(std::max<int64_t>(1, np * sl), s);
+    en.alloc(np, s);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
       const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + (zr < kp ? size_t(kp + zr) * (zr + 1) : 0)) *
@@ -727,16 +781,16 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     const int ktp = std::min(flags[0], sl);
     nr[l - 1] = ktp;
     flops += fl.gemm(double(np), ktp, kp, zr);
-    Tlev[l - 1].alloc(std::max<int64_t>(1, np * ktp * kp));
+    Tlev[l - 1].alloc(std::max<int64_t>(1, np * ktp * kp), s);
     const int ldn = pad2(ktc);
-    newtr[l].alloc(std::max<int64_t>(1, A.nodes(l) * ldn * ktp));
+    newtr[l].alloc(std::max<int64_t>(1, A.nodes(l) * ldn * ktp), s);
     k_trunc_level_apply<<<unsigned(np), kThreads, 0, s>>>(ktc, kp, sl, ktp, Z.p, U.p, sg.p, Tlev[l - 1].p,
                                                           newtr[l].p, ldn, en.p);
     H2B_CUDA(cudaGetLastError());
     lev_e[l - 1] = sum_host(en, np, s);
   }
   // gather Tt into one pool (rows = new rank, cols = old rank)
-  Tt.alloc(A, nr, old);
+  Tt.alloc(A, nr, old, s);
   for (int l = 0; l <= q; ++l) {
     const int64_t sz = A.nodes(l) * int64_t(nr[l]) * old[l];
     if (sz) H2B_CUDA(cudaMemcpyAsync(Tt.at(l), Tlev[l].p, sz * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -794,6 +848,19 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   DeviceGuard g(A.device);
   cudaStream_t s = A.stream;
+  // keep freed scratch in the pool for the whole call; handed back at the end
+  cudaMemPool_t pool;
+  H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, A.device));
+  uint64_t keep = ~uint64_t(0);
+  H2B_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  struct Trim {
+    cudaMemPool_t p;
+    cudaStream_t s;
+    ~Trim() {
+      cudaStreamSynchronize(s);
+      cudaMemPoolTrimTo(p, 0);
+    }
+  } trim{pool, s};
   Flops fl;
   h2b_compress_report r{};
   for (int l = 0; l <= A.q; ++l) r.old_ranks[l] = A.rank[l];
@@ -837,6 +904,16 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep) {
   r.bytes_after = A.footprint();
   r.frobenius_error = r.frobenius_norm > 0 ? std::sqrt(energy) / r.frobenius_norm : 0.0;
   if (rep) *rep = r;
+#ifdef H2B_SWEEP_HIST
+  int hist[64];
+  H2B_CUDA(cudaMemcpyFromSymbol(hist, cta::g_sweep_hist, sizeof(hist)));
+  fprintf(stderr, "jacobi sweeps:");
+  for (int i = 0; i <= 60; ++i)
+    if (hist[i]) fprintf(stderr, " %d:%d", i + 1, hist[i]);
+  fprintf(stderr, "\n");
+  std::fill(hist, hist + 64, 0);
+  H2B_CUDA(cudaMemcpyToSymbol(cta::g_sweep_hist, hist, sizeof(hist)));
+#endif
 }
 
 void orthogonalize_matrix(Matrix& A, double* t_out) {

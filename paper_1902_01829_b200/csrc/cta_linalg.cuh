@@ -262,6 +262,9 @@ __device__ __forceinline__ void rr_pair(int n, int r, int s, int& p, int& q) {
 // column pair (four pairs per warp, 32 pairs per CTA step) and keep it in
 // registers (RPT rows per lane) between the three dot products (reduced with
 // width-8 shuffles) and the rotation.
+#ifdef H2B_SWEEP_HIST
+__device__ int g_sweep_hist[64];
+#endif
 template <int RPT>
 __device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag, int rows_dot) {
   const double tol = 2.220446049250313e-16 * 16.0;
@@ -296,10 +299,14 @@ __device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag, int row
           b += __shfl_xor_sync(gmask, b, m, 8);
           d += __shfl_xor_sync(gmask, d, m, 8);
         }
-        if (fabs(d) <= tol * sqrt(a * b) || d == 0.0) continue;
+        // sqrt(a) sqrt(b) and hypot(1, z): the reference's rule and rotation
+        // (linalg.hpp:155-170) without the under/overflow of a*b and z*z,
+        // which turn tiny-column pairs into no-op rotations that never
+        // satisfy the convergence test
+        if (fabs(d) <= tol * (sqrt(a) * sqrt(b)) || d == 0.0) continue;
         if (sub == 0) *flag = 1;
         const double z = (b - a) / (2.0 * d);
-        const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
+        const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + hypot(1.0, z));
         const double cs = 1.0 / sqrt(1.0 + t * t);
         const double sn = cs * t;
 #pragma unroll
@@ -313,8 +320,16 @@ __device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag, int row
       }
       __syncthreads();
     }
-    if (*flag == 0) break;
+    if (*flag == 0) {
+#ifdef H2B_SWEEP_HIST
+      if (threadIdx.x == 0) atomicAdd(&g_sweep_hist[sweep], 1);
+#endif
+      break;
+    }
     __syncthreads();
+#ifdef H2B_SWEEP_HIST
+    if (sweep == 59 && threadIdx.x == 0) atomicAdd(&g_sweep_hist[60], 1);
+#endif
   }
   __syncthreads();
 }

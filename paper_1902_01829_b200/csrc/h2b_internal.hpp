@@ -88,6 +88,33 @@ struct DevBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// Stream-ordered scratch (cudaMallocAsync from the device's default pool):
+// compression temporaries are recycled by the pool instead of going through
+// cudaMalloc/cudaFree (each a device-wide synchronisation plus page mapping).
+template <class T>
+struct TmpBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  TmpBuf() = default;
+  TmpBuf(const TmpBuf&) = delete;
+  TmpBuf& operator=(const TmpBuf&) = delete;
+  TmpBuf(TmpBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  ~TmpBuf() { release(); }
+  void alloc(size_t cnt, cudaStream_t st) {
+    release();
+    s = st;
+    if (cnt == 0) return;
+    H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), s));
+    n = cnt;
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+};
+
 // One uniform-block BSR layer (a coupling level or the dense layer),
 // bsr.hpp:13-31.  row_ptr/col_idx are level-local like the reference.
 struct Layer {

@@ -58,8 +58,8 @@ int main() {
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b);
-    // each warp-level m8n8k4 = 8*8*4 FMAs = 512 FMA = 1024 flops
-    const double fm = 1024.0 * 8 * iters * double(blocks) * (threads / 32);
+    // each warp-level m8n8k4 = 8*8*4 = 256 FMA = 512 flops
+    const double fm = 512.0 * 8 * iters * double(blocks) * (threads / 32);
     printf("DMMA m8n8k4: %.2f TFLOP/s\n", fm / ms / 1e9);
   }
   return 0;
