@@ -503,6 +503,7 @@ def main():
     comp = None
     if not args.no_compress:
         comp = compression_run(h2, torch, local, args.compress_reps)
+    h2.release_cached_memory(local)
 
     if rank != 0:
         return

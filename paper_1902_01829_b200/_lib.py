@@ -78,6 +78,7 @@ _SIGS = {
     "h2b_last_error": (C.c_char_p, []),
     "h2b_version": (C.c_char_p, []),
     "h2b_device_count": (C.c_int, []),
+    "h2b_release_cached_memory": (C.c_int, [C.c_int]),
     "h2b_matrix_create": (C.c_int, [C.POINTER(MatrixDesc), C.c_int, C.POINTER(C.c_void_p)]),
     "h2b_matrix_build": (C.c_int, [C.POINTER(BuildConfig), C.c_int, C.POINTER(C.c_void_p)]),
     "h2b_matrix_destroy": (C.c_int, [C.c_void_p]),

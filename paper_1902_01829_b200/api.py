@@ -278,3 +278,9 @@ def validate_sampled(A: H2Matrix, fraction: float, seed: int = 1, points=None, d
 
 def device_count() -> int:
     return int(_lib.load().h2b_device_count())
+
+
+def release_cached_memory(device: int = 0) -> None:
+    """Hand the memory compress() cached in the device's stream-ordered pool back
+    to the device (h2b_release_cached_memory)."""
+    _lib.check(_lib.load().h2b_release_cached_memory(int(device)))

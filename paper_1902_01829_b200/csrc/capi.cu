@@ -120,6 +120,13 @@ void download_blocks(const double* d, double* h, int rows, int cols, int64_t cou
 }  // namespace
 
 Matrix::~Matrix() {
+  // pools re-laid out by compress() come from the stream-ordered pool and are
+  // freed on this stream: release them before the stream goes away
+  if (stream) cudaStreamSynchronize(stream);
+  leaf.release();
+  transfer.release();
+  cpl_val.release();
+  dense_val.release();
   if (h_stage) cudaFreeHost(h_stage);
   for (auto& e : ev_pool)
     if (e) cudaEventDestroy(e);
@@ -155,9 +162,19 @@ double Matrix::hmv_flops() const {
 // (n, m, q, rank, layers' host CSR).  Values are left uninitialised.
 void allocate(Matrix& A) {
   const int q = A.q;
+  // The device's default stream-ordered pool keeps freed memory cached (a
+  // caching allocator: rebuilding / compressing matrices does not re-map
+  // pages); h2b_release_cached_memory hands it back.
+  {
+    cudaMemPool_t pool;
+    H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, A.device));
+    uint64_t keep = ~uint64_t(0);
+    H2B_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   A.ldm = pad2(A.m);
   A.perm.alloc(A.n);
-  A.leaf.alloc(size_t(A.own_count(q)) * A.leaf_stride());
+  // the big pools come from the stream-ordered pool (see compress_matrix)
+  A.leaf.alloc_pooled(size_t(A.own_count(q)) * A.leaf_stride(), A.stream);
   A.tr_off.assign(q + 2, 0);
   int64_t t = 0;
   for (int l = 1; l <= q; ++l) {
@@ -165,7 +182,7 @@ void allocate(Matrix& A) {
     t += A.tr_count(l) * A.tr_stride(l);
   }
   A.tr_off[q + 1] = t;
-  A.transfer.alloc(t);
+  A.transfer.alloc_pooled(t, A.stream);
   int64_t nv = 0, nrp = 0, nci = 0;
   for (int l = 0; l <= q; ++l) {
     Layer& L = A.cpl[l];
@@ -174,7 +191,7 @@ void allocate(Matrix& A) {
     nrp += L.rows + 1;
     nci += L.nb;
   }
-  A.cpl_val.alloc(nv);
+  A.cpl_val.alloc_pooled(nv, A.stream);
   A.cpl_rp.alloc(nrp);
   A.cpl_ci.alloc(nci);
   nv = nrp = nci = 0;
@@ -189,7 +206,7 @@ void allocate(Matrix& A) {
   }
   Layer& D = A.dense;
   D.ld = pad2(D.br);
-  A.dense_val.alloc(size_t(D.nb) * D.block_stride());
+  A.dense_val.alloc_pooled(size_t(D.nb) * D.block_stride(), A.stream);
   A.dense_rp.alloc(D.rows + 1);
   A.dense_ci.alloc(D.nb);
   D.val = A.dense_val.p;
@@ -204,6 +221,9 @@ void allocate(Matrix& A) {
   A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
   A.xs.alloc(A.n);
   A.ys.alloc(A.n);
+  // pooled allocations are stream-ordered on A.stream: complete them before
+  // the pools are used from any other stream
+  H2B_CUDA(cudaStreamSynchronize(A.stream));
 }
 
 // Upload the CSR structure of every layer and build the fused work list.
@@ -438,6 +458,20 @@ extern "C" {
 const char* h2b_last_error(void) { return g_err.c_str(); }
 const char* h2b_version(void) { return "h2b 0.1 (sm_100a, fp64)"; }
 int h2b_device_count(void) { return usable_devices(); }
+
+h2b_status h2b_release_cached_memory(int device) {
+  return guarded([&] {
+    require(device >= 0 && device < usable_devices(), "invalid device");
+    int prev = 0;
+    H2B_CUDA(cudaGetDevice(&prev));
+    H2B_CUDA(cudaSetDevice(device));
+    cudaMemPool_t pool;
+    H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    H2B_CUDA(cudaDeviceSynchronize());
+    H2B_CUDA(cudaMemPoolTrimTo(pool, 0));
+    H2B_CUDA(cudaSetDevice(prev));
+  });
+}
 
 h2b_status h2b_matrix_create(const h2b_matrix_desc* desc, int device, h2b_matrix** out) {
   return guarded([&] {

@@ -15,7 +15,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
   const int64_t fs = int64_t(ldf) * kp;
   for (int ci = 0; ci < 2; ++ci) {
     const int64_t c = 2 * p + ci;
-    cta::gemm_tc<false, false>(Z + ci * kc, zr, Tl + c * int64_t(kc) * kc, kc, F + c * fs, ldf, kc, kp, kc);
+    cta::gemm_tc<false, false, 1>(Z + ci * kc, zr, Tl + c * int64_t(kc) * kc, kc, F + c * fs, ldf, kc, kp, kc);
   }
   __syncthreads();
   cta::householder(Z, zr, zr, kp, tau, red);
@@ -102,34 +104,125 @@ struct ProjLevel {
 };
 struct ProjTable {
   ProjLevel L[kMaxLevels + 1];
+  int tri;  // T upper triangular (orthogonalization's R factors)
 };
 
-// S_b <- T_row S_b T_col^T for every block of one block row (compression.hpp:160-168).
-__global__ void __launch_bounds__(kThreads) k_project(const __grid_constant__ ProjTable P,
-                                                      const ProjRow* __restrict__ rows) {
+// S_b <- T_row S_b T_col^T for every block of one block row (compression.hpp:160-168),
+// ranks <= 64.  T_row stays in smem for the row; per block, S_b and T_col are
+// staged in smem (cp.async) and warp w computes the 8-row strip [8w, 8w+8) of
+//   TS  = T_row S_b    (DMMA, the strip's accumulators stay in registers) and
+//   out = TS T_col^T   (DMMA; TS's A fragments come from the accumulators by
+//                       two quad shuffles per k-step -- TS never touches smem).
+// With TRI (orthogonalization: T are upper-triangular R factors) the
+// structurally zero fragments of both products are skipped.
+constexpr int kPLd = 68;  // smem leading dimension (== 4 mod 16: conflict-free fragments)
+template <bool TRI>
+__device__ __forceinline__ void project_block(const double* Tr, const double* Sb, const double* Tc, double* out,
+                                              int ld_new, int ro, int rn) {
+  const int w = cta::warp(), t = cta::lane();
+  const int fr = t >> 2, fk = t & 3;
+  const int i0 = 8 * w;
+  if (i0 >= rn) return;
+  // ---- TS strip = Tr[i0:i0+8, :] S (8 x ro), 8 column tiles ----
+  double acc[8][2];
+#pragma unroll
+  for (int y = 0; y < 8; ++y) acc[y][0] = acc[y][1] = 0.0;
+  const int kc_end = (ro + 3) >> 2;
+#pragma unroll
+  for (int kc = 0; kc < 16; ++kc) {
+    if (kc < kc_end && (!TRI || 4 * kc + 3 >= i0)) {
+      const int p = 4 * kc + fk;
+      const double a = Tr[i0 + fr + p * kPLd];
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        if (8 * y < ro) {
+          const double b = Sb[p + (8 * y + fr) * kPLd];
+          cta::dmma(acc[y][0], acc[y][1], a, b);
+        }
+      }
+    }
+  }
+  // ---- out strip = TS strip (8 x ro) T_col^T (ro x rn) ----
+  double o[8][2];
+#pragma unroll
+  for (int y = 0; y < 8; ++y) o[y][0] = o[y][1] = 0.0;
+  const int src = fr * 4 + (fk >> 1);
+#pragma unroll
+  for (int kc = 0; kc < 16; ++kc) {
+    if (kc < kc_end) {
+      // A fragment TS[i0 + fr, 4 kc + fk] lives in acc[kc / 2][(fk & 1)] of
+      // lane fr * 4 + 2 (kc & 1) + fk / 2
+      const int sl = src + 2 * (kc & 1);
+      const double s0 = __shfl_sync(0xffffffffu, acc[kc >> 1][0], sl);
+      const double s1 = __shfl_sync(0xffffffffu, acc[kc >> 1][1], sl);
+      const double a = (fk & 1) ? s1 : s0;
+      const int p = 4 * kc + fk;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        if (8 * y < rn && (!TRI || 4 * kc + 3 >= 8 * y)) {
+          const double b = Tc[8 * y + fr + p * kPLd];  // T_col[j, p]
+          cta::dmma(o[y][0], o[y][1], a, b);
+        }
+      }
+    }
+  }
+  const int i = i0 + fr;
+  if (i < rn) {
+#pragma unroll
+    for (int y = 0; y < 8; ++y)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = 8 * y + 2 * fk + v;
+        if (j < rn) out[i + int64_t(j) * ld_new] = o[y][v];
+      }
+  }
+  if (ld_new > rn && w == 0)
+    for (int j = t; j < rn; j += 32) out[rn + int64_t(j) * ld_new] = 0.0;
+}
+
+// 8-byte asynchronous global -> shared copies (cp.async.ca), grouped.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// rows x cols block (ld lds, global) into a zero-padded 64 x 64 smem tile (ld kPLd)
+__device__ __forceinline__ void stage64(double* dst, const double* src, int lds, int rows, int cols) {
+  for (int e = threadIdx.x; e < 64 * 64; e += kThreads) {
+    const int j = e >> 6, i = e & 63;
+    if (i < rows && j < cols)
+      cp_async8(dst + i + j * kPLd, src + i + int64_t(j) * lds);
+    else
+      dst[i + j * kPLd] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__ ProjTable P,
+                                                         const ProjRow* __restrict__ rows) {
   extern __shared__ double sm[];
   const ProjRow pr = rows[blockIdx.x];
   const ProjLevel& L = P.L[pr.level];
   const int ro = L.ro, rn = L.rn;
-  const int lr = cta::sld(rn), lo = cta::sld(ro);
-  double* Tr = sm;              // rn x ro   (ld lr)
-  double* Sb = Tr + lr * ro;    // ro x ro   (ld lo), then T_col (rn x ro, ld lr <= lo)
-  double* TS = Sb + lo * ro;    // rn x ro   (ld lr)
-  cta::copy_block(Tr, lr, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
+  double* Tr = sm;                // rn x ro
+  double* Sb = Tr + 64 * kPLd;    // ro x ro
+  double* Tc = Sb + 64 * kPLd;    // rn x ro
+  stage64(Tr, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
   const int b0 = L.rp[pr.row], b1 = L.rp[pr.row + 1];
   for (int b = b0; b < b1; ++b) {
-    __syncthreads();
-    cta::copy_block(Sb, lo, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
-    __syncthreads();
-    cta::gemm_tc<false, false>(TS, lr, Tr, lr, Sb, lo, rn, ro, ro);
-    __syncthreads();
-    const int c = L.ci[b];
-    cta::copy_block(Sb, lr, L.T + int64_t(c) * rn * ro, rn, rn, ro);
+    __syncthreads();  // previous block done with Sb / Tc
+    stage64(Sb, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
+    stage64(Tc, L.T + int64_t(L.ci[b]) * rn * ro, rn, rn, ro);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     double* out = L.out + int64_t(b) * L.ld_new * rn;
-    cta::gemm_tc<false, true>(out, L.ld_new, TS, lr, Sb, lr, rn, rn, ro);
-    if (L.ld_new > rn)
-      for (int j = threadIdx.x; j < rn; j += kThreads) out[rn + int64_t(j) * L.ld_new] = 0.0;
+    if (P.tri)
+      project_block<true>(Tr, Sb, Tc, out, L.ld_new, ro, rn);
+    else
+      project_block<false>(Tr, Sb, Tc, out, L.ld_new, ro, rn);
   }
 }
 
@@ -150,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_weights_parent(const double* __res
                                                              const double* __restrict__ Rpar,
                                                              double* __restrict__ P) {
   const int64_t r = blockIdx.x;
-  cta::gemm_tc<false, true>(P + r * int64_t(kp) * kc, kp, Rpar + (r >> 1) * int64_t(kp) * kp, kp,
+  cta::gemm_tc<false, true, 1>(P + r * int64_t(kp) * kc, kp, Rpar + (r >> 1) * int64_t(kp) * kp, kp,
                             E + r * int64_t(lde) * kp, lde, kp, kc, kp);
 }
 
@@ -170,12 +263,83 @@ __global__ void __launch_bounds__(kThreads) k_weights_parent(const double* __res
 // products and applies the reflector to its own columns.  Arithmetic as
 // linalg.hpp:48-75: beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta,
 // v = x / (alpha - beta) below the unit entry.
+// One reflector of k_weights (see below) on column slots [T0, NCOL).
+template <int T0, int NCOL, int CR>
+__device__ __forceinline__ void weights_step(double (&B)[NCOL][CR], const double* x, double* xn, double* Rp,
+                                             const int (&coff)[NCOL], int lane, int j, int kc) {
+  // ||x||^2 and the dot products with the raw column (branch-free: every
+  // lane runs the same straight-line code, dead columns get f = 0)
+  double q[4] = {0.0, 0.0, 0.0, 0.0};
+  double w[NCOL][2];
+#pragma unroll
+  for (int t = T0; t < NCOL; ++t) w[t][0] = w[t][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < CR; i += 2) {
+    const double2 xx = *reinterpret_cast<const double2*>(x + i);
+    q[i & 3] = fma(xx.x, xx.x, q[i & 3]);
+    q[(i + 1) & 3] = fma(xx.y, xx.y, q[(i + 1) & 3]);
+#pragma unroll
+    for (int t = T0; t < NCOL; ++t) {
+      w[t][0] = fma(xx.x, B[t][i], w[t][0]);
+      w[t][1] = fma(xx.y, B[t][i + 1], w[t][1]);
+    }
+  }
+  const double al = x[CR];
+  const double nx = sqrt(fma(al, al, (q[0] + q[1]) + (q[2] + q[3])));
+  const double be = al >= 0.0 ? -nx : nx;
+  const double am = al - be;
+  const double r = 1.0 / (be * am);  // sc = 1/(al-be) = be r, tau = (be-al)/be = -am^2 r
+  const double sc = be * r;
+  const double tau = -(am * am) * r;
+  double f[NCOL];
+#pragma unroll
+  for (int t = T0; t < NCOL; ++t) {
+    const int c = lane + 32 * t;
+    f[t] = 0.0;
+    if (c > j && c < kc && nx != 0.0) {
+      const double d = fma(sc, w[t][0] + w[t][1], Rp[coff[t] + j]) * tau;
+      Rp[coff[t] + j] -= d;
+      f[t] = sc * d;
+    }
+    if (c == j && nx != 0.0) {
+      Rp[coff[t] + j] = be;
+      f[t] = 1.0;  // x == this column: B - x = 0 exactly (it becomes the reflector)
+    }
+  }
+  asm volatile("" ::: "memory");  // re-read x below instead of holding CR more registers
+#pragma unroll
+  for (int i = 0; i < CR; i += 2) {
+    const double2 xx = *reinterpret_cast<const double2*>(x + i);
+#pragma unroll
+    for (int t = T0; t < NCOL; ++t) {
+      B[t][i] = fma(-xx.x, f[t], B[t][i]);
+      B[t][i + 1] = fma(-xx.y, f[t], B[t][i + 1]);
+    }
+  }
+  // next owner hands over its updated column
+  const int jn = j + 1;
+  if (jn < kc && lane == (jn & 31)) {
+    if (jn < 32) {
+#pragma unroll
+      for (int i = 0; i < CR; i += 2) *reinterpret_cast<double2*>(xn + i) = make_double2(B[0][i], B[0][i + 1]);
+      xn[CR] = Rp[coff[0] + jn];
+    } else {
+#pragma unroll
+      for (int i = 0; i < CR; i += 2)
+        *reinterpret_cast<double2*>(xn + i) = make_double2(B[NCOL - 1][i], B[NCOL - 1][i + 1]);
+      xn[CR] = Rp[coff[NCOL - 1] + jn];
+    }
+  }
+}
+
 constexpr int kWWarps = 4;  // nodes (warps) per CTA
 template <int NCOL, int CR>
 __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __restrict__ P, int kc, int kp,
                                                           const int32_t* __restrict__ rp,
                                                           const double* __restrict__ S, int lds,
-                                                          double* __restrict__ Rout, int64_t nnodes) {
+                                                          double* __restrict__ Rout, int64_t nnodes,
+                                                          const int32_t* __restrict__ order,
+                                                          int* __restrict__ next) {
   constexpr int XS = CR + 2;  // publish slot: raw column, alpha
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31;
@@ -183,8 +347,13 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
   const int rsz = (((kc * (kc + 1)) / 2 + 1) & ~1);
   double* Rp = sm + wid * (rsz + 2 * XS);  // packed R: column c at c(c+1)/2
   double* xb = Rp + rsz;                   // 2 x XS
-  const int64_t node = int64_t(blockIdx.x) * kWWarps + wid;
-  if (node >= nnodes) return;
+  // persistent warps: nodes are claimed in decreasing-work order (LPT)
+  for (;;) {
+  int idx = 0;
+  if (lane == 0) idx = atomicAdd(next, 1);
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+  if (idx >= nnodes) break;
+  const int64_t node = order[idx];
   for (int e = lane; e < rsz; e += 32) Rp[e] = 0.0;
   int coff[NCOL];
 #pragma unroll
@@ -240,70 +409,11 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
     for (int j = 0; j < kc; ++j, ++jg) {
       const double* x = xb + (jg & 1) * XS;
       double* xn = xb + ((jg + 1) & 1) * XS;
-      // ||x||^2 and the dot products with the raw column (branch-free: every
-      // lane runs the same straight-line code, dead columns get f = 0)
-      double q[4] = {0.0, 0.0, 0.0, 0.0};
-      double w[NCOL][2];
-#pragma unroll
-      for (int t = 0; t < NCOL; ++t) w[t][0] = w[t][1] = 0.0;
-#pragma unroll
-      for (int i = 0; i < CR; i += 2) {
-        const double2 xx = *reinterpret_cast<const double2*>(x + i);
-        q[i & 3] = fma(xx.x, xx.x, q[i & 3]);
-        q[(i + 1) & 3] = fma(xx.y, xx.y, q[(i + 1) & 3]);
-#pragma unroll
-        for (int t = 0; t < NCOL; ++t) {
-          w[t][0] = fma(xx.x, B[t][i], w[t][0]);
-          w[t][1] = fma(xx.y, B[t][i + 1], w[t][1]);
-        }
-      }
-      const double al = x[CR];
-      const double nx = sqrt(fma(al, al, (q[0] + q[1]) + (q[2] + q[3])));
-      const double be = al >= 0.0 ? -nx : nx;
-      const double am = al - be;
-      const double r = 1.0 / (be * am);  // sc = 1/(al-be) = be r, tau = (be-al)/be = -am^2 r
-      const double sc = be * r;
-      const double tau = -(am * am) * r;
-      double f[NCOL];
-#pragma unroll
-      for (int t = 0; t < NCOL; ++t) {
-        const int c = lane + 32 * t;
-        f[t] = 0.0;
-        if (c > j && c < kc && nx != 0.0) {
-          const double d = fma(sc, w[t][0] + w[t][1], Rp[coff[t] + j]) * tau;
-          Rp[coff[t] + j] -= d;
-          f[t] = sc * d;
-        }
-        if (c == j && nx != 0.0) {
-          Rp[coff[t] + j] = be;
-          f[t] = 1.0;  // x == this column: B - x = 0 exactly (it becomes the reflector)
-        }
-      }
-      asm volatile("" ::: "memory");  // re-read x below instead of holding CR more registers
-#pragma unroll
-      for (int i = 0; i < CR; i += 2) {
-        const double2 xx = *reinterpret_cast<const double2*>(x + i);
-#pragma unroll
-        for (int t = 0; t < NCOL; ++t) {
-          B[t][i] = fma(-xx.x, f[t], B[t][i]);
-          B[t][i + 1] = fma(-xx.y, f[t], B[t][i + 1]);
-        }
-      }
-      // next owner hands over its updated column
-      const int jn = j + 1;
-      if (jn < kc && lane == (jn & 31)) {
-        if (jn < 32) {
-#pragma unroll
-          for (int i = 0; i < CR; i += 2)
-            *reinterpret_cast<double2*>(xn + i) = make_double2(B[0][i], B[0][i + 1]);
-          xn[CR] = Rp[coff[0] + jn];
-        } else {
-#pragma unroll
-          for (int i = 0; i < CR; i += 2)
-            *reinterpret_cast<double2*>(xn + i) = make_double2(B[NCOL - 1][i], B[NCOL - 1][i + 1]);
-          xn[CR] = Rp[coff[NCOL - 1] + jn];
-        }
-      }
+      // column slot 0 holds only dead columns once j >= 32: skip it (uniform)
+      if (NCOL == 2 && j >= 32)
+        weights_step<1, NCOL, CR>(B, x, xn, Rp, coff, lane, j, kc);
+      else
+        weights_step<0, NCOL, CR>(B, x, xn, Rp, coff, lane, j, kc);
       __syncwarp();
     }
   }
@@ -317,62 +427,93 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
       Ro[i + int64_t(cc) * kc] = Rp[((i * (i + 1)) >> 1) + i] < 0.0 ? -v : v;
     }
   }
+  __syncwarp();
+  }
 }
 
-// One-sided Jacobi SVD of W (rows x cols, smem, ld = rows) into Uout (global,
-// rows x s) + sigma; `work` holds >= cols*rows + 64 doubles when rows < cols.
-__device__ int svd_to(double* W, int rows, int cols, double* work, double* Uout, int ldu,
-                      double* sig, double eps, double* nrm, int* ord, int* flag, double* tau,
-                      double* red) {
+// Shared-memory scratch of the truncation SVDs.
+struct SvdScratch {
+  double nrm[128];
+  double tau[64];
+  double tau2[64];
+  double red[16];
+  int ord[128];
+  int perm[128];
+  int flag, sel;
+};
+constexpr int kSvdScratch = int((sizeof(SvdScratch) + 15) / 16) * 2;  // in doubles, 16 B aligned
+
+// Left singular vectors (Uout, global, rows x s) and singular values (sig) of
+// W (rows x cols, smem, ld rows; destroyed), s = min(rows, cols); returns
+// #{sigma_j >= eps sigma_1} (0 if sigma_1 = 0) -- svd_truncated_batched,
+// batch.hpp:107-140 / linalg.hpp:142-232.
+//
+// Preconditioned one-sided Jacobi (Drmac-Veselic): instead of rotating W's
+// columns directly (10-26 sweeps on these graded spectra), factor
+//   tall  W P = Q1 R1 (QR with column pivoting), R1^T = Q2 R2, Jacobi on R2^T:
+//         U = Q1 U_X, where U_X = normalised columns of the rotated R2^T;
+//   wide  W^T P = Q1 R1, Jacobi on R1^T: U = P U_X;
+// which converges in a few sweeps.  Same singular values, same subspaces
+// (the reference runs Jacobi on W, or on R^T of an unpivoted QR of W^T when
+// wide); columns of U may differ in sign.  The Jacobi rule, tolerance, sweep
+// cap, sigma = column norms and stable descending sort are the reference's.
+// X: smem, >= s * (s + 1) doubles (and >= cols * rows when wide).
+__device__ int svd_pre(double* W, int rows, int cols, double* X, double* Uout, int ldu, double* sig,
+                       double eps, SvdScratch& sc) {
   const int s = rows < cols ? rows : cols;
   if (s == 0) return 0;
+  const int n = s + (s & 1);  // Jacobi columns (zero pad column when odd)
   if (rows >= cols) {
-    int n = cols;
-    if (n & 1) {  // zero pad column
-      for (int i = threadIdx.x; i < rows; i += kThreads) W[i + cols * rows] = 0.0;
-      ++n;
+    const int c = cols;
+    cta::qrcp(W, rows, rows, c, sc.tau, sc.perm, sc.nrm, sc.red, &sc.sel);
+    // X = R1^T (c x c, lower), then QR of it: R2 in the upper triangle
+    for (int e = threadIdx.x; e < c * c; e += kThreads) {
+      const int j = e / c, i = e - j * c;
+      X[i + j * c] = i >= j ? W[j + i * rows] : 0.0;
     }
     __syncthreads();
-    cta::jacobi(W, rows, rows, n, flag);
-    cta::jacobi_finish(W, rows, rows, n, s, Uout, ldu, sig, nrm, ord);
+    cta::householder(X, c, c, c, sc.tau2, sc.red);
+    // in-place transpose to R2^T (lower), zero pad column
+    for (int e = threadIdx.x; e < c * c; e += kThreads) {
+      const int j = e / c, i = e - j * c;
+      if (i < j) {
+        X[j + i * c] = X[i + j * c];
+        X[i + j * c] = 0.0;
+      }
+    }
+    if (n > c)
+      for (int i = threadIdx.x; i < c; i += kThreads) X[i + c * c] = 0.0;
+    __syncthreads();
+    cta::jacobi(X, c, c, n, &sc.flag);
+    // U_X into the top c rows of Uout, zero below, then U = Q1 [U_X; 0]
+    cta::jacobi_finish(X, c, c, n, s, Uout, ldu, sig, sc.nrm, sc.ord);
+    for (int e = threadIdx.x; e < (rows - c) * s; e += kThreads) {
+      const int j = e / (rows - c), i = e - j * (rows - c);
+      Uout[c + i + int64_t(j) * ldu] = 0.0;
+    }
+    __syncthreads();
+    cta::apply_q(W, rows, rows, c, sc.tau, Uout, ldu, s);
   } else {
-    // wide (rows < cols): the left singular vectors of W are the accumulated
-    // right rotations of one-sided Jacobi on W^T.  Run it on [W^T; I_rows]
-    // (dots over the first `cols` rows only) -- no QR needed (the reference
-    // takes the QR-of-W^T route, linalg.hpp:195-207; same subspaces/sigmas).
-    const int ldg = cols + rows;
-    double* G = work;  // (cols + rows) x (rows + 1)
-    for (int e = threadIdx.x; e < ldg * rows; e += kThreads) {
-      const int j = e / ldg, i = e - j * ldg;
-      G[i + j * ldg] = i < cols ? W[j + i * rows] : (i - cols == j ? 1.0 : 0.0);
-    }
-    int n = rows;
-    if (n & 1) {
-      for (int i = threadIdx.x; i < ldg; i += kThreads) G[i + rows * ldg] = 0.0;
-      ++n;
+    const int r = rows;
+    double* G = X;  // W^T (cols x r)
+    for (int e = threadIdx.x; e < cols * r; e += kThreads) {
+      const int j = e / cols, i = e - j * cols;
+      G[i + j * cols] = W[j + i * rows];
     }
     __syncthreads();
-    cta::jacobi(G, ldg, ldg, n, flag, cols);
-    // sigma = column norms over the W^T part; U column j = accumulated rotation
-    for (int j = cta::warp(); j < n; j += cta::kWarps) {
-      double t = 0.0;
-      for (int i = cta::lane(); i < cols; i += 32) t += G[i + j * ldg] * G[i + j * ldg];
-      t = cta::warp_sum(t);
-      if (cta::lane() == 0) nrm[j] = sqrt(t);
+    cta::qrcp(G, cols, cols, r, sc.tau, sc.perm, sc.nrm, sc.red, &sc.sel);
+    // J = R1^T (r x n, lower) in W's storage (W is dead)
+    double* J = W;
+    for (int e = threadIdx.x; e < r * n; e += kThreads) {
+      const int j = e / r, i = e - j * r;
+      J[i + j * r] = (j < r && i >= j) ? G[j + i * cols] : 0.0;
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < n; j += kThreads) {
-      int rk = 0;
-      const double v = nrm[j];
-      for (int i = 0; i < n; ++i) rk += (nrm[i] > v) || (nrm[i] == v && i < j);
-      ord[rk] = j;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < s; j += kThreads) sig[j] = nrm[ord[j]];
-    for (int e = threadIdx.x; e < rows * s; e += kThreads) {
-      const int j = e / rows, i = e - j * rows;
-      const int src = ord[j];
-      Uout[i + int64_t(j) * ldu] = nrm[src] > 0.0 ? G[cols + i + src * ldg] : 0.0;
+    cta::jacobi(J, r, r, n, &sc.flag);
+    cta::jacobi_finish(J, r, r, n, s, X, r, sig, sc.nrm, sc.ord);
+    for (int e = threadIdx.x; e < r * s; e += kThreads) {
+      const int j = e / r, i = e - j * r;
+      Uout[sc.perm[i] + int64_t(j) * ldu] = X[i + j * r];
     }
     __syncthreads();
   }
@@ -383,8 +524,6 @@ __device__ int svd_to(double* W, int rows, int cols, double* work, double* Uout,
   }
   return rank;
 }
-
-constexpr int kSvdScratch = 128 + 64 + 16 + 72;  // nrm, tau, red, ord/flag (ints)
 
 __device__ void check_finite(const double* W, int n, int* bad) {
   for (int e = threadIdx.x; e < n; e += kThreads)
@@ -399,19 +538,15 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_svd(const double* __res
                                                              int* __restrict__ kmax, int* __restrict__ bad) {
   extern __shared__ double sm[];
   const int s = m < k ? m : k;
-  double* nrm = sm;                     // scratch first (kSvdScratch doubles)
-  double* tau = nrm + 128;
-  double* red = tau + 64;
-  int* ord = reinterpret_cast<int*>(red + 16);
-  int* flag = ord + 128;
-  double* W = sm + kSvdScratch;         // m x (k+1)
-  double* work = W + m * (k + 1);       // wide case only: (k+1) x (m+1)
+  SvdScratch& sc = *reinterpret_cast<SvdScratch*>(sm);
+  double* W = sm + kSvdScratch;        // m x (k + 1)
+  double* X = W + m * (k + 1);         // >= s (s + 1), >= k m
   const int64_t i = blockIdx.x;
-  cta::gemm_tc<false, true>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
+  cta::gemm_tc<false, true, 2>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
   __syncthreads();
   check_finite(W, m * k, bad);
   double* sg = sig_out + i * s;
-  const int rank = svd_to(W, m, k, work, Uout + i * int64_t(m) * s, m, sg, eps, nrm, ord, flag, tau, red);
+  const int rank = svd_pre(W, m, k, X, Uout + i * int64_t(m) * s, m, sg, eps, sc);
   if (threadIdx.x == 0) atomicMax(kmax, rank);
 }
 
@@ -447,13 +582,9 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_svd(
   extern __shared__ double sm[];
   const int zr = 2 * ktc;
   const int s = zr < kp ? zr : kp;
-  double* nrm = sm;                      // scratch first (kSvdScratch doubles)
-  double* tau = nrm + 128;
-  double* red = tau + 64;
-  int* ord = reinterpret_cast<int*>(red + 16);
-  int* flag = ord + 128;
+  SvdScratch& sc = *reinterpret_cast<SvdScratch*>(sm);
   double* W = sm + kSvdScratch;          // zr x (kp + 1)
-  double* work = W + zr * (kp + 1);      // wide case only: (kp+1) x (zr+1)
+  double* X = W + zr * (kp + 1);         // >= s (s + 1), >= kp zr
   const int64_t p = blockIdx.x;
   const int64_t es = int64_t(lde) * kp;
   double* Z = Zout + p * int64_t(zr) * kp;  // Z lives in global memory (L2)
@@ -462,11 +593,10 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_svd(
     cta::gemm_tc<false, false>(Z + ci * ktc, zr, Tt + c * int64_t(ktc) * kc, ktc, E + c * es, lde, ktc, kp, kc);
   }
   __syncthreads();
-  cta::gemm_tc<false, true>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
+  cta::gemm_tc<false, true, 2>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
   __syncthreads();
   check_finite(W, zr * kp, bad);
-  const int rank = svd_to(W, zr, kp, work, Uout + p * int64_t(zr) * s, zr, sig_out + p * s, eps, nrm,
-                          ord, flag, tau, red);
+  const int rank = svd_pre(W, zr, kp, X, Uout + p * int64_t(zr) * s, zr, sig_out + p * s, eps, sc);
   if (threadIdx.x == 0) atomicMax(kmax, rank);
 }
 
@@ -586,6 +716,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
 void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place) {
   const int q = A.q;
   ProjTable P{};
+  P.tri = in_place ? 1 : 0;
   std::vector<ProjRow> rows;
   std::vector<int64_t> new_off(q + 2, 0);
   for (int l = 0; l <= q; ++l) {
@@ -594,7 +725,7 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     new_off[l + 1] = new_off[l] + L.nb * int64_t(pad2(rn)) * rn;
   }
   DevBuf<double> fresh;
-  if (!in_place) fresh.alloc(std::max<int64_t>(1, new_off[q + 1]));
+  if (!in_place) fresh.alloc_pooled(std::max<int64_t>(1, new_off[q + 1]), s);
   double* base = in_place ? A.cpl_val.p : fresh.p;
   size_t smax = 0;
   for (int l = 0; l <= q; ++l) {
@@ -616,7 +747,7 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     if (rn == 0) continue;
     for (int64_t r = 0; r < L.rows; ++r)
       if (L.h_rp[r + 1] > L.h_rp[r]) rows.push_back({l, int32_t(r)});
-    smax = std::max(smax, (size_t(cta::sld(rn)) * ro * 2 + size_t(cta::sld(ro)) * ro) * sizeof(double));
+    smax = size_t(3) * 64 * kPLd * sizeof(double);
   }
   if (!rows.empty()) {
     check_smem(smax, "project_coupling");
@@ -673,11 +804,28 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
     constexpr int CR = 32;
     const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
     const int64_t nn = A.nodes(l);
-    const unsigned grid = unsigned((nn + kWWarps - 1) / kWWarps);
-#define H2B_WEIGHTS(NCOL)                                                                          \
-  if ((kc > 32 ? 2 : 1) == NCOL) {                                                                 \
-    set_smem(k_weights<NCOL, CR>, sm);                                                             \
-    k_weights<NCOL, CR><<<grid, 32 * kWWarps, sm, s>>>(Pbuf.p, kc, kp, L.rp, L.val, L.ld, R.at(l), nn); \
+    // LPT order: nodes by decreasing stack height
+    std::vector<int32_t> ord(nn);
+    for (int64_t i = 0; i < nn; ++i) ord[i] = int32_t(i);
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+      return L.h_rp[a + 1] - L.h_rp[a] > L.h_rp[b + 1] - L.h_rp[b];
+    });
+    TmpBuf<int32_t> dord;
+    dord.alloc(nn + 1, s);  // [nn] = work counter
+    H2B_CUDA(cudaMemcpyAsync(dord.p, ord.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    H2B_CUDA(cudaMemsetAsync(dord.p + nn, 0, sizeof(int32_t), s));
+    int dev_sms = 0;
+    H2B_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, A.device));
+#define H2B_WEIGHTS(NCOL)                                                                           \
+  if ((kc > 32 ? 2 : 1) == NCOL) {                                                                  \
+    set_smem(k_weights<NCOL, CR>, sm);                                                              \
+    int per_sm = 0;                                                                                 \
+    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<NCOL, CR>,            \
+                                                           32 * kWWarps, sm));                      \
+    const int64_t want = (nn + kWWarps - 1) / kWWarps;                                              \
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(dev_sms) * std::max(1, per_sm)))); \
+    k_weights<NCOL, CR><<<grid, 32 * kWWarps, sm, s>>>(Pbuf.p, kc, kp, L.rp, L.val, L.ld, R.at(l), nn, \
+                                                       dord.p, reinterpret_cast<int*>(dord.p + nn)); \
   }
     H2B_WEIGHTS(1) H2B_WEIGHTS(2)
 #undef H2B_WEIGHTS
@@ -701,11 +849,24 @@ double sum_host(const TmpBuf<double>& d, int64_t n, cudaStream_t s) {
   return acc;
 }
 
+// H2B_TRACE=1: per-level wall-clock trace of the truncation on stderr.
+struct Trace {
+  bool on = std::getenv("H2B_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void at(cudaStream_t s, const char* tag, int l) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "  [trace] %8.2f ms %s l=%d\n", ms, tag, l);
+  }
+};
+
 // Returns the discarded energy; fills Tt (new x old per node) and replaces
 // the leaf / transfer pools and ranks.
 double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s, Flops& fl,
                 double& flops) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
+  Trace tr;
   const int q = A.q, m = A.m;
   const std::vector<int> old = A.rank;
   std::vector<int> nr(q + 1, 0);
@@ -728,7 +889,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     en.alloc(nl, s);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
-      const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + (m < kq ? size_t(kq + m) * (m + 1) : 0)) *
+      const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + size_t(std::max(sl * (sl + 1), kq * m))) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_leaf_svd, sm);
@@ -736,6 +897,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
                                                           dk.p, dk.p + 1);
       H2B_CUDA(cudaGetLastError());
     }
+    tr.at(s, "leaf svd", q);
     int flags[2] = {0, 0};
     H2B_CUDA(cudaMemcpyAsync(flags, dk.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2B_CUDA(cudaStreamSynchronize(s));
@@ -745,11 +907,12 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     flops += fl.gemm(double(nl), kt, kq, m);
     Tlev[q].alloc(std::max<int64_t>(1, nl * kt * kq), s);
     const int ldn = pad2(m);
-    newleaf.alloc(std::max<int64_t>(1, nl * ldn * kt));
+    newleaf.alloc_pooled(std::max<int64_t>(1, nl * ldn * kt), s);
     k_trunc_leaf_apply<<<unsigned(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq.p, sg.p,
                                                          Tlev[q].p, newleaf.p, ldn, en.p);
     H2B_CUDA(cudaGetLastError());
     lev_e[q] = sum_host(en, nl, s);
+    tr.at(s, "leaf apply", q);
   }
   for (int l = q; l >= 1; --l) {
     const int ktc = nr[l], kc = old[l], kp = old[l - 1];
@@ -765,7 +928,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     en.alloc(np, s);
     H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
     if (sl > 0) {
-      const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + (zr < kp ? size_t(kp + zr) * (zr + 1) : 0)) *
+      const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + size_t(std::max(sl * (sl + 1), kp * zr))) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_level_svd, sm);
@@ -774,6 +937,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
                                                            dk.p + 1);
       H2B_CUDA(cudaGetLastError());
     }
+    tr.at(s, "level svd", l);
     int flags[2] = {0, 0};
     H2B_CUDA(cudaMemcpyAsync(flags, dk.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2B_CUDA(cudaStreamSynchronize(s));
@@ -788,6 +952,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
                                                           newtr[l].p, ldn, en.p);
     H2B_CUDA(cudaGetLastError());
     lev_e[l - 1] = sum_host(en, np, s);
+    tr.at(s, "level apply", l);
   }
   // gather Tt into one pool (rows = new rank, cols = old rank)
   Tt.alloc(A, nr, old, s);
@@ -805,7 +970,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   }
   toff[q + 1] = t;
   DevBuf<double> trpool;
-  trpool.alloc(std::max<int64_t>(1, t));
+  trpool.alloc_pooled(std::max<int64_t>(1, t), s);
   for (int l = 1; l <= q; ++l) {
     const int64_t sz = A.nodes(l) * A.tr_stride(l);
     if (sz) H2B_CUDA(cudaMemcpyAsync(trpool.p + toff[l], newtr[l].p, sz * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -848,19 +1013,14 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   DeviceGuard g(A.device);
   cudaStream_t s = A.stream;
-  // keep freed scratch in the pool for the whole call; handed back at the end
+  // scratch and the re-laid-out pools come from the device's default
+  // stream-ordered pool, which keeps freed memory cached (like a caching
+  // allocator) so repeated compressions do not re-map pages; h2b_trim_pool /
+  // a failing cudaMalloc hand it back
   cudaMemPool_t pool;
   H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, A.device));
   uint64_t keep = ~uint64_t(0);
   H2B_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  struct Trim {
-    cudaMemPool_t p;
-    cudaStream_t s;
-    ~Trim() {
-      cudaStreamSynchronize(s);
-      cudaMemPoolTrimTo(p, 0);
-    }
-  } trim{pool, s};
   Flops fl;
   h2b_compress_report r{};
   for (int l = 0; l <= A.q; ++l) r.old_ranks[l] = A.rank[l];

@@ -119,7 +119,11 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // C (m x n) = op(A) (m x k) * op(B) (k x n) on the FP64 tensor cores.  Each
 // warp owns 32 x 16 output tiles (4 x 2 DMMA tiles, 16 accumulators); any
 // m, n, k (edges predicated to zero).  Operands may live in smem or global.
-template <bool TA, bool TB>
+// TRI = 1: op(A)(i, p) == 0 for p < i (upper triangular A, e.g. an R factor);
+// TRI = 2: op(B)(p, j) == 0 for p < j (B = R^T with R upper triangular).  The
+// DMMAs whose fragments are structurally zero are skipped; skipped terms are
+// exact zeros, so the result is bitwise that of the full product.
+template <bool TA, bool TB, int TRI = 0>
 __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
                         int m, int n, int k) {
   const int t = lane();
@@ -132,24 +136,30 @@ __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const doub
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-    for (int p0 = 0; p0 < k; p0 += 4) {
+    const int p_begin = TRI == 1 ? (i0 & ~3) : TRI == 2 ? (j0 & ~3) : 0;
+    for (int p0 = p_begin; p0 < k; p0 += 4) {
       const int p = p0 + fk;
       const bool pk = p < k;
       double a[4], b[2];
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
         const int i = i0 + 8 * x + fr;
-        a[x] = (pk && i < m) ? (TA ? A[p + i * lda] : A[i + p * lda]) : 0.0;
+        a[x] = (pk && i < m && (TRI != 1 || p >= i)) ? (TA ? A[p + i * lda] : A[i + p * lda]) : 0.0;
       }
 #pragma unroll
       for (int y = 0; y < 2; ++y) {
         const int j = j0 + 8 * y + fr;
-        b[y] = (pk && j < n) ? (TB ? B[j + p * ldb] : B[p + j * ldb]) : 0.0;
+        b[y] = (pk && j < n && (TRI != 2 || p >= j)) ? (TB ? B[j + p * ldb] : B[p + j * ldb]) : 0.0;
       }
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 2; ++y) dmma(acc[x][y][0], acc[x][y][1], a[x], b[y]);
+        for (int y = 0; y < 2; ++y) {
+          // structurally zero fragments (warp-uniform test)
+          if (TRI == 1 && p0 + 3 < i0 + 8 * x) continue;
+          if (TRI == 2 && p0 + 3 < j0 + 8 * y) continue;
+          dmma(acc[x][y][0], acc[x][y][1], a[x], b[y]);
+        }
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x)
@@ -196,6 +206,127 @@ __device__ void householder(double* A, int lda, int rows, int cols, double* tau,
       __syncwarp();
       if (lane() == 0) w[j] -= d;
       for (int i = j + 1 + lane(); i < rows; i += 32) w[i] -= v[i] * d;
+    }
+    __syncthreads();
+  }
+}
+
+// Householder QR with column pivoting (largest remaining column norm, first
+// index on ties), in place: reflectors below the diagonal, R on and above it,
+// perm[j] = original index of the column now at position j.  The remaining
+// column norms are recomputed exactly inside every trailing update (one extra
+// FMA per element), so no norm downdating.  Same reflector convention as
+// householder().  nrm: cols doubles, red: >= 16 doubles, sel: 1 int (smem).
+__device__ void qrcp(double* A, int lda, int rows, int cols, double* tau, int* perm, double* nrm,
+                     double* red, int* sel) {
+  for (int kk = warp(); kk < cols; kk += kWarps) {
+    const double* w = A + kk * lda;
+    double t = 0.0;
+    for (int i = lane(); i < rows; i += 32) t = fma(w[i], w[i], t);
+    t = warp_sum(t);
+    if (lane() == 0) {
+      nrm[kk] = t;
+      perm[kk] = kk;
+    }
+  }
+  __syncthreads();
+  const int steps = rows < cols ? rows : cols;
+  for (int j = 0; j < steps; ++j) {
+    if (warp() == 0) {  // argmax of the remaining norms
+      double bv = -1.0;
+      int bi = cols;
+      for (int kk = j + lane(); kk < cols; kk += 32)
+        if (nrm[kk] > bv) {
+          bv = nrm[kk];
+          bi = kk;
+        }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, bv, o);
+        const int oi = __shfl_xor_sync(kFull, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane() == 0) *sel = bi;
+    }
+    __syncthreads();
+    const int pj = *sel;
+    if (pj != j) {
+      double* a = A + j * lda;
+      double* b = A + pj * lda;
+      for (int i = threadIdx.x; i < rows; i += kThreads) {
+        const double t = a[i];
+        a[i] = b[i];
+        b[i] = t;
+      }
+      if (threadIdx.x == 0) {
+        const double tn = nrm[j];
+        nrm[j] = nrm[pj];
+        nrm[pj] = tn;
+        const int tp = perm[j];
+        perm[j] = perm[pj];
+        perm[pj] = tp;
+      }
+      __syncthreads();
+    }
+    double* v = A + j * lda;
+    const double nx = sqrt(nrm[j]);  // exact: recomputed by the previous update
+    if (nx == 0.0) {  // all remaining columns are zero
+      if (threadIdx.x == 0) tau[j] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    const double al = v[j];
+    const double be = al >= 0.0 ? -nx : nx;
+    const double tj = (be - al) / be;
+    const double sc = 1.0 / (al - be);
+    __syncthreads();  // everyone has read v[j]
+    for (int i = j + 1 + threadIdx.x; i < rows; i += kThreads) v[i] *= sc;
+    if (threadIdx.x == 0) {
+      v[j] = be;
+      tau[j] = tj;
+    }
+    __syncthreads();
+    for (int kk = j + 1 + warp(); kk < cols; kk += kWarps) {
+      double* w = A + kk * lda;
+      double s = 0.0;
+      for (int i = j + 1 + lane(); i < rows; i += 32) s = fma(v[i], w[i], s);
+      s = warp_sum(s);
+      const double d = (w[j] + s) * tj;
+      __syncwarp();
+      if (lane() == 0) w[j] -= d;
+      double t = 0.0;
+      for (int i = j + 1 + lane(); i < rows; i += 32) {
+        const double nv = fma(-v[i], d, w[i]);
+        w[i] = nv;
+        t = fma(nv, nv, t);
+      }
+      t = warp_sum(t);
+      if (lane() == 0) nrm[kk] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// Y (rows x ncols, ld ldy) <- H_0 H_1 ... H_{k-1} Y for the k reflectors
+// stored below the diagonal of A (unit leading entry, tau[j]).
+__device__ void apply_q(const double* A, int lda, int rows, int k, const double* tau, double* Y,
+                        int ldy, int ncols) {
+  for (int j = k - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double* v = A + j * lda;
+    for (int kk = warp(); kk < ncols; kk += kWarps) {
+      double* w = Y + kk * ldy;
+      double s = 0.0;
+      for (int i = j + 1 + lane(); i < rows; i += 32) s = fma(v[i], w[i], s);
+      s = warp_sum(s);
+      const double d = (w[j] + s) * tj;
+      __syncwarp();
+      if (lane() == 0) w[j] -= d;
+      for (int i = j + 1 + lane(); i < rows; i += 32) w[i] = fma(-v[i], d, w[i]);
     }
     __syncthreads();
   }
@@ -339,14 +470,11 @@ __device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag, int row
 // only accumulate the rotations.
 __device__ inline void jacobi(double* G, int ldg, int rows, int n, int* flag, int rows_dot = -1) {
   if (rows_dot < 0) rows_dot = rows;
+  // rows <= 64: the preconditioned SVD only rotates square triangular factors
   if (rows <= 32)
     jacobi_t<4>(G, ldg, rows, n, flag, rows_dot);
-  else if (rows <= 64)
-    jacobi_t<8>(G, ldg, rows, n, flag, rows_dot);
-  else if (rows <= 128)
-    jacobi_t<16>(G, ldg, rows, n, flag, rows_dot);
   else
-    jacobi_t<32>(G, ldg, rows, n, flag, rows_dot);
+    jacobi_t<8>(G, ldg, rows, n, flag, rows_dot);
 }
 
 // After jacobi(): sigma[j] (descending, stable) and U (rows x s) with unit (or

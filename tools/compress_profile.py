@@ -9,8 +9,14 @@ import paper_1902_01829_b200 as h2
 
 dim, n, order, eps = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), float(sys.argv[4])
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+settle = float(sys.argv[6]) if len(sys.argv) > 6 else 0.0
 for _ in range(reps):
     A = h2.H2Matrix.construct(dim, n, grid_order=order)
+    if settle:
+        import time
+        import torch
+        torch.cuda.synchronize()
+        time.sleep(settle)
     rep = h2.compress(A, eps)
     ph = [rep.time_orthogonalize_ms, rep.time_project_orth_ms, rep.time_weights_ms,
           rep.time_truncate_ms, rep.time_project_trunc_ms]
