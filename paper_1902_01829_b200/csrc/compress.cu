@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(kThreads) k_orth_leaf(double* __restrict__ lea
   extern __shared__ double sm[];
   double* A = sm;                 // m x k, ld m
   double* Q = A + m * k;          // m x k, ld m
-  double* tau = Q + m * k;        // 64
+  double* Zw = Q + m * k;         // k x k
+  double* tau = Zw + k * k;       // 64
   double* red = tau + 64;         // 16
   int* flip = reinterpret_cast<int*>(red + 16);
   const int64_t i = blockIdx.x;
@@ -46,10 +47,13 @@ __global__ void __launch_bounds__(kThreads) k_orth_leaf(double* __restrict__ lea
   cta::copy_block(A, m, U, ldm, m, k);
   __syncthreads();
   cta::householder(A, m, m, k, tau, red);
-  cta::form_q(A, m, m, k, tau, Q, m);
-  __syncthreads();
   cta::extract_r(A, m, k, T + i * int64_t(k) * k, k, flip);
+  for (int e = threadIdx.x; e < k * k; e += kThreads) {
+    const int j = e / k, r = e - j * k;
+    Q[r + j * m] = r == j ? 1.0 : 0.0;
+  }
   __syncthreads();
+  cta::apply_q_wy(A, m, m, k, tau, Q, m, k, Zw, /*y0_identity=*/true);  // Q = H_0..H_{k-1} [I; 0]
   for (int e = threadIdx.x; e < m * k; e += kThreads) {
     const int j = e / m, r = e - j * m;
     U[r + int64_t(j) * ldm] = flip[j] ? -Q[r + j * m] : Q[r + j * m];
@@ -64,7 +68,8 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
   const int zr = 2 * kc;
   double* Z = sm;                    // zr x kp
   double* Q = Z + zr * kp;           // zr x kp
-  double* tau = Q + zr * kp;
+  double* Zw = Q + zr * kp;          // kp x kp
+  double* tau = Zw + kp * kp;
   double* red = tau + 64;
   int* flip = reinterpret_cast<int*>(red + 16);
   const int64_t p = blockIdx.x;
@@ -75,10 +80,13 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
   }
   __syncthreads();
   cta::householder(Z, zr, zr, kp, tau, red);
-  cta::form_q(Z, zr, zr, kp, tau, Q, zr);
-  __syncthreads();
   cta::extract_r(Z, zr, kp, Tp + p * int64_t(kp) * kp, kp, flip);
+  for (int e = threadIdx.x; e < kp * kp; e += kThreads) {
+    const int j = e / kp, r = e - j * kp;
+    Q[r + j * zr] = r == j ? 1.0 : 0.0;
+  }
   __syncthreads();
+  cta::apply_q_wy(Z, zr, zr, kp, tau, Q, zr, kp, Zw, /*y0_identity=*/true);
   for (int ci = 0; ci < 2; ++ci) {
     double* dst = F + (2 * p + ci) * fs;
     for (int e = threadIdx.x; e < kc * kp; e += kThreads) {
@@ -487,12 +495,7 @@ __device__ int svd_pre(double* W, int rows, int cols, double* X, double* Uout, i
     cta::jacobi(X, c, c, n, &sc.flag);
     // U_X into the top c rows of Uout, zero below, then U = Q1 [U_X; 0]
     cta::jacobi_finish(X, c, c, n, s, Uout, ldu, sig, sc.nrm, sc.ord);
-    for (int e = threadIdx.x; e < (rows - c) * s; e += kThreads) {
-      const int j = e / (rows - c), i = e - j * (rows - c);
-      Uout[c + i + int64_t(j) * ldu] = 0.0;
-    }
-    __syncthreads();
-    cta::apply_q(W, rows, rows, c, sc.tau, Uout, ldu, s);
+    cta::apply_q_wy(W, rows, rows, c, sc.tau, Uout, ldu, s, X);
   } else {
     const int r = rows;
     double* G = X;  // W^T (cols x r)
@@ -681,6 +684,26 @@ struct TreePool {
   double* at(int l) { return buf.p + off[l]; }
 };
 
+// One stream-ordered allocation carved into sub-buffers: the phases size all
+// their scratch up front instead of allocating per level.
+struct Arena {
+  TmpBuf<double> buf;
+  size_t off = 0;
+  void reserve(size_t doubles, cudaStream_t s) {
+    buf.alloc(std::max<size_t>(1, doubles), s);
+    off = 0;
+  }
+  template <class T>
+  T* take(size_t n) {
+    const size_t d = ((n * sizeof(T) + 255) / 256) * 32;  // 256-byte granules, in doubles
+    if (off + d > buf.n) throw Error(H2B_CUDA_ERROR, "scratch arena overflow");
+    T* p = reinterpret_cast<T*>(buf.p + off);
+    off += d;
+    return p;
+  }
+  static size_t need(size_t n, size_t elem) { return ((n * elem + 255) / 256) * 32; }
+};
+
 // ---------------------------------------------------------------- phases
 void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops) {
   const int q = A.q, m = A.m, kq = A.rank[q];
@@ -688,7 +711,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
   T.alloc(A, A.rank, A.rank, s);
   const int64_t nl = A.nodes(q);
   if (kq > 0) {
-    const size_t sm = (2 * size_t(m) * kq + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    const size_t sm = (2 * size_t(m) * kq + size_t(kq) * kq + 64 + 16) * sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "orthogonalize");
     set_smem(k_orth_leaf, sm);
     k_orth_leaf<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, T.at(q));
@@ -701,7 +724,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
     flops += fl.gemm(double(A.nodes(l)), kc, kp, kc) + fl.qr(double(np), 2 * kc, kp);
     require(2 * kc >= kp, "qr_batched: requires rows >= cols");
     if (kp == 0) continue;
-    const size_t sm = (2 * size_t(2 * kc) * kp + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    const size_t sm = (2 * size_t(2 * kc) * kp + size_t(kp) * kp + 64 + 16) * sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "orthogonalize");
     set_smem(k_orth_level, sm);
     k_orth_level<<<unsigned(np), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
@@ -787,6 +810,30 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
   const int q = A.q;
   R.alloc(A, A.rank, A.rank, s);
   H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * A.rank[0] * A.rank[0], s));
+  // LPT order of every level (nodes by decreasing stack height) plus one work
+  // counter per level, uploaded once
+  size_t pmax = 1;
+  std::vector<int64_t> ooff(q + 2, 0);
+  for (int l = 1; l <= q; ++l) {
+    pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
+    ooff[l + 1] = ooff[l] + A.nodes(l) + 1;
+  }
+  std::vector<int32_t> ord(std::max<int64_t>(1, ooff[q + 1]), 0);
+  for (int l = 1; l <= q; ++l) {
+    const Layer& L = A.cpl[l];
+    int32_t* o = ord.data() + ooff[l];
+    const int64_t nn = A.nodes(l);
+    for (int64_t i = 0; i < nn; ++i) o[i] = int32_t(i);
+    std::stable_sort(o, o + nn, [&](int32_t a, int32_t b) {
+      return L.h_rp[a + 1] - L.h_rp[a] > L.h_rp[b + 1] - L.h_rp[b];
+    });
+    o[nn] = 0;
+  }
+  Arena ar;
+  ar.reserve(Arena::need(pmax, sizeof(double)) + Arena::need(ord.size(), sizeof(int32_t)), s);
+  double* Pall = ar.take<double>(pmax);
+  int32_t* dord_all = ar.take<int32_t>(ord.size());
+  H2B_CUDA(cudaMemcpyAsync(dord_all, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   for (int l = 1; l <= q; ++l) {
     const int kc = A.rank[l], kp = A.rank[l - 1];
     const Layer& L = A.cpl[l];
@@ -794,9 +841,10 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
     flops += fl.gemm(double(A.nodes(l)), kp, kc, kp) + fl.qr(double(A.nodes(l)), ld_ref, kc);
     require(ld_ref >= kc, "qr_r_only_batched: requires rows >= cols");
     if (kc == 0) continue;
-    TmpBuf<double> Pbuf;
+    struct {
+      double* p;
+    } Pbuf{Pall};
     if (kp > 0) {
-      Pbuf.alloc(size_t(A.nodes(l)) * kp * kc, s);
       k_weights_parent<<<unsigned(A.nodes(l)), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
                                                                   R.at(l - 1), Pbuf.p);
       H2B_CUDA(cudaGetLastError());
@@ -805,15 +853,9 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
     const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
     const int64_t nn = A.nodes(l);
     // LPT order: nodes by decreasing stack height
-    std::vector<int32_t> ord(nn);
-    for (int64_t i = 0; i < nn; ++i) ord[i] = int32_t(i);
-    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
-      return L.h_rp[a + 1] - L.h_rp[a] > L.h_rp[b + 1] - L.h_rp[b];
-    });
-    TmpBuf<int32_t> dord;
-    dord.alloc(nn + 1, s);  // [nn] = work counter
-    H2B_CUDA(cudaMemcpyAsync(dord.p, ord.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    H2B_CUDA(cudaMemsetAsync(dord.p + nn, 0, sizeof(int32_t), s));
+    struct {
+      int32_t* p;
+    } dord{dord_all + ooff[l]};  // [nn] = work counter
     int dev_sms = 0;
     H2B_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, A.device));
 #define H2B_WEIGHTS(NCOL)                                                                           \
@@ -840,9 +882,9 @@ int read_kmax(int* d, cudaStream_t s) {
   return h;
 }
 
-double sum_host(const TmpBuf<double>& d, int64_t n, cudaStream_t s) {
+double sum_host(const double* d, int64_t n, cudaStream_t s) {
   std::vector<double> h(n);
-  if (n) H2B_CUDA(cudaMemcpyAsync(h.data(), d.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (n) H2B_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   H2B_CUDA(cudaStreamSynchronize(s));
   double acc = 0.0;
   for (double v : h) acc += v;
@@ -871,45 +913,58 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   const std::vector<int> old = A.rank;
   std::vector<int> nr(q + 1, 0);
   std::vector<double> lev_e(q + 1, 0.0);
-  TmpBuf<int> dk;
-  dk.alloc(2, s);  // [0] = kmax, [1] = non-finite flag
-  std::vector<TmpBuf<double>> newtr(q + 1);
-  std::vector<int> trows(q + 1, 0);
-  // projection pool sized after the fact per level
-  std::vector<TmpBuf<double>> Tlev(q + 1);
   const int64_t nl = A.nodes(q);
+  // ---- all scratch up front (new ranks are bounded by the old ones) ----
+  // Tt (new x old per node): level offsets sized for the old ranks, filled
+  // in place; the new transfers: one region per level, compacted at the end.
+  Tt.alloc(A, old, old, s);
+  std::vector<int64_t> ntoff(q + 2, 0);
+  for (int l = 1; l <= q; ++l) ntoff[l + 1] = ntoff[l] + A.nodes(l) * int64_t(pad2(old[l])) * old[l - 1];
+  const int sl_leaf = std::min(m, old[q]);
+  size_t lvl = Arena::need(size_t(nl) * m * sl_leaf, 8) + Arena::need(size_t(nl) * sl_leaf, 8) +
+               Arena::need(size_t(nl), 8);
+  for (int l = q; l >= 1; --l) {
+    const int64_t np = A.nodes(l - 1);
+    const int zr = 2 * old[l], kp = old[l - 1], sl = std::min(zr, kp);
+    lvl = std::max(lvl, Arena::need(size_t(np) * zr * kp, 8) + Arena::need(size_t(np) * zr * sl, 8) +
+                            Arena::need(size_t(np) * sl, 8) + Arena::need(size_t(np), 8));
+  }
+  Arena ar;
+  ar.reserve(lvl + Arena::need(size_t(std::max<int64_t>(1, ntoff[q + 1])), 8) + Arena::need(2, 4), s);
+  double* newtr = ar.take<double>(std::max<int64_t>(1, ntoff[q + 1]));
+  int* dk = ar.take<int>(2);  // [0] = kmax, [1] = non-finite flag
+  const size_t lvl_base = ar.off;
   DevBuf<double> newleaf;
   {
     const int kq = old[q];
-    const int sl = std::min(m, kq);
+    const int sl = sl_leaf;
     flops += fl.gemm(double(nl), m, kq, kq) + fl.svd(double(nl), m, kq);
-    TmpBuf<double> Uq, sg, en;
-    Uq.alloc(std::max<int64_t>(1, nl * m * sl), s);
-    sg.alloc(std::max<int64_t>(1, nl * sl), s);
-    en.alloc(nl, s);
-    H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
+    ar.off = lvl_base;
+    double* Uq = ar.take<double>(size_t(nl) * m * sl);
+    double* sg = ar.take<double>(size_t(nl) * sl);
+    double* en = ar.take<double>(size_t(nl));
+    H2B_CUDA(cudaMemsetAsync(dk, 0, 2 * sizeof(int), s));
     if (sl > 0) {
       const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + size_t(std::max(sl * (sl + 1), kq * m))) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_leaf_svd, sm);
-      k_trunc_leaf_svd<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, R.at(q), Uq.p, sg.p, eps,
-                                                          dk.p, dk.p + 1);
+      k_trunc_leaf_svd<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, R.at(q), Uq, sg, eps,
+                                                          dk, dk + 1);
       H2B_CUDA(cudaGetLastError());
     }
     tr.at(s, "leaf svd", q);
     int flags[2] = {0, 0};
-    H2B_CUDA(cudaMemcpyAsync(flags, dk.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaMemcpyAsync(flags, dk, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2B_CUDA(cudaStreamSynchronize(s));
     require(flags[1] == 0, "svd_truncated_batched: non-finite input");
     const int kt = std::min(flags[0], sl);
     nr[q] = kt;
     flops += fl.gemm(double(nl), kt, kq, m);
-    Tlev[q].alloc(std::max<int64_t>(1, nl * kt * kq), s);
     const int ldn = pad2(m);
     newleaf.alloc_pooled(std::max<int64_t>(1, nl * ldn * kt), s);
-    k_trunc_leaf_apply<<<unsigned(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq.p, sg.p,
-                                                         Tlev[q].p, newleaf.p, ldn, en.p);
+    k_trunc_leaf_apply<<<unsigned(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq, sg, Tt.at(q),
+                                                         newleaf.p, ldn, en);
     H2B_CUDA(cudaGetLastError());
     lev_e[q] = sum_host(en, nl, s);
     tr.at(s, "leaf apply", q);
@@ -921,45 +976,37 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     const int sl = std::min(zr, kp);
     flops += fl.gemm(double(A.nodes(l)), ktc, kp, kc) + fl.gemm(double(np), zr, kp, kp) +
              fl.svd(double(np), zr, kp);
-    TmpBuf<double> Z, U, sg, en;
-    Z.alloc(std::max<int64_t>(1, np * zr * kp), s);
-    U.alloc(std::max<int64_t>(1, np * zr * sl), s);
-    sg.alloc(std::max<int64_t>(1, np * sl), s);
-    en.alloc(np, s);
-    H2B_CUDA(cudaMemsetAsync(dk.p, 0, 2 * sizeof(int), s));
+    ar.off = lvl_base;
+    double* Z = ar.take<double>(size_t(np) * zr * kp);
+    double* U = ar.take<double>(size_t(np) * zr * sl);
+    double* sg = ar.take<double>(size_t(np) * sl);
+    double* en = ar.take<double>(size_t(np));
+    H2B_CUDA(cudaMemsetAsync(dk, 0, 2 * sizeof(int), s));
     if (sl > 0) {
       const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + size_t(std::max(sl * (sl + 1), kp * zr))) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_level_svd, sm);
       k_trunc_level_svd<<<unsigned(np), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, ktc,
-                                                           Tlev[l].p, R.at(l - 1), Z.p, U.p, sg.p, eps, dk.p,
-                                                           dk.p + 1);
+                                                           Tt.at(l), R.at(l - 1), Z, U, sg, eps, dk, dk + 1);
       H2B_CUDA(cudaGetLastError());
     }
     tr.at(s, "level svd", l);
     int flags[2] = {0, 0};
-    H2B_CUDA(cudaMemcpyAsync(flags, dk.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaMemcpyAsync(flags, dk, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2B_CUDA(cudaStreamSynchronize(s));
     require(flags[1] == 0, "svd_truncated_batched: non-finite input");
     const int ktp = std::min(flags[0], sl);
     nr[l - 1] = ktp;
     flops += fl.gemm(double(np), ktp, kp, zr);
-    Tlev[l - 1].alloc(std::max<int64_t>(1, np * ktp * kp), s);
     const int ldn = pad2(ktc);
-    newtr[l].alloc(std::max<int64_t>(1, A.nodes(l) * ldn * ktp), s);
-    k_trunc_level_apply<<<unsigned(np), kThreads, 0, s>>>(ktc, kp, sl, ktp, Z.p, U.p, sg.p, Tlev[l - 1].p,
-                                                          newtr[l].p, ldn, en.p);
+    k_trunc_level_apply<<<unsigned(np), kThreads, 0, s>>>(ktc, kp, sl, ktp, Z, U, sg, Tt.at(l - 1),
+                                                          newtr + ntoff[l], ldn, en);
     H2B_CUDA(cudaGetLastError());
     lev_e[l - 1] = sum_host(en, np, s);
     tr.at(s, "level apply", l);
   }
-  // gather Tt into one pool (rows = new rank, cols = old rank)
-  Tt.alloc(A, nr, old, s);
-  for (int l = 0; l <= q; ++l) {
-    const int64_t sz = A.nodes(l) * int64_t(nr[l]) * old[l];
-    if (sz) H2B_CUDA(cudaMemcpyAsync(Tt.at(l), Tlev[l].p, sz * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  }
+  Tt.rows = nr;  // per node: new x old, at the old-rank level offsets
   // new transfer pool with padded ld for the new ranks
   A.rank = nr;
   std::vector<int64_t> toff(q + 2, 0);
@@ -973,7 +1020,8 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   trpool.alloc_pooled(std::max<int64_t>(1, t), s);
   for (int l = 1; l <= q; ++l) {
     const int64_t sz = A.nodes(l) * A.tr_stride(l);
-    if (sz) H2B_CUDA(cudaMemcpyAsync(trpool.p + toff[l], newtr[l].p, sz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (sz) H2B_CUDA(cudaMemcpyAsync(trpool.p + toff[l], newtr + ntoff[l], sz * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
   }
   H2B_CUDA(cudaStreamSynchronize(s));
   A.transfer = std::move(trpool);
@@ -1021,6 +1069,15 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep) {
   H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, A.device));
   uint64_t keep = ~uint64_t(0);
   H2B_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  if (std::getenv("H2B_TRACE")) {
+    uint64_t res = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    fprintf(stderr, "  [trace] compress start: pool reserved %.2f GB used %.2f GB, device free %.2f GB\n",
+            res / 1e9, used / 1e9, fr / 1e9);
+  }
   Flops fl;
   h2b_compress_report r{};
   for (int l = 0; l <= A.q; ++l) r.old_ranks[l] = A.rank[l];

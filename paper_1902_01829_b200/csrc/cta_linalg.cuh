@@ -123,9 +123,12 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // TRI = 2: op(B)(p, j) == 0 for p < j (B = R^T with R upper triangular).  The
 // DMMAs whose fragments are structurally zero are skipped; skipped terms are
 // exact zeros, so the result is bitwise that of the full product.
-template <bool TA, bool TB, int TRI = 0>
+// VM bit 1 (2): A's (B's) storage holds Householder vectors below its
+// diagonal (V with an implicit unit diagonal, zero above; the storage on and
+// above the diagonal is NOT read).  EPI = 1: C <- (i < epi_rows ? C : 0) - op(A) op(B).
+template <bool TA, bool TB, int TRI = 0, int VM = 0, int EPI = 0>
 __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
-                        int m, int n, int k) {
+                        int m, int n, int k, int epi_rows = 0) {
   const int t = lane();
   const int fr = t >> 2, fk = t & 3;  // fragment row (A) / col (B), k index
   const int mt = (m + 31) >> 5, nt = (n + 15) >> 4;
@@ -144,12 +147,22 @@ __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const doub
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
         const int i = i0 + 8 * x + fr;
-        a[x] = (pk && i < m && (TRI != 1 || p >= i)) ? (TA ? A[p + i * lda] : A[i + p * lda]) : 0.0;
+        if (VM & 1) {
+          const int r = TA ? p : i, c = TA ? i : p;  // storage coordinates
+          a[x] = (pk && i < m) ? (r > c ? A[r + c * lda] : (r == c ? 1.0 : 0.0)) : 0.0;
+        } else {
+          a[x] = (pk && i < m && (TRI != 1 || p >= i)) ? (TA ? A[p + i * lda] : A[i + p * lda]) : 0.0;
+        }
       }
 #pragma unroll
       for (int y = 0; y < 2; ++y) {
         const int j = j0 + 8 * y + fr;
-        b[y] = (pk && j < n && (TRI != 2 || p >= j)) ? (TB ? B[j + p * ldb] : B[p + j * ldb]) : 0.0;
+        if (VM & 2) {
+          const int r = TB ? j : p, c = TB ? p : j;  // storage coordinates
+          b[y] = (pk && j < n) ? (r > c ? B[r + c * ldb] : (r == c ? 1.0 : 0.0)) : 0.0;
+        } else {
+          b[y] = (pk && j < n && (TRI != 2 || p >= j)) ? (TB ? B[j + p * ldb] : B[p + j * ldb]) : 0.0;
+        }
       }
 #pragma unroll
       for (int x = 0; x < 4; ++x)
@@ -168,7 +181,12 @@ __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const doub
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int i = i0 + 8 * x + fr, j = j0 + 8 * y + 2 * fk + v;
-          if (i < m && j < n) C[i + j * ldc] = acc[x][y][v];
+          if (i < m && j < n) {
+            if (EPI == 1)
+              C[i + j * ldc] = (i < epi_rows ? C[i + j * ldc] : 0.0) - acc[x][y][v];
+            else
+              C[i + j * ldc] = acc[x][y][v];
+          }
         }
   }
 }
@@ -330,6 +348,71 @@ __device__ void apply_q(const double* A, int lda, int rows, int k, const double*
     }
     __syncthreads();
   }
+}
+
+// Y <- H_0 H_1 ... H_{k-1} [Y0; 0] for the k reflectors below the diagonal
+// of A (rows x k, unit leading entries, tau[j]; tau = 0 marks an identity),
+// Y0 = the top k x ncols of Y (global or smem, ld ldy; rows k.. of Y are
+// written).  Compact WY on the FP64 tensor cores:
+//   Q = I - V T V^T,  T^{-1} = diag(1/tau) + triu(V^T V, 1)   (so no T build)
+//   Z = V^T [Y0; 0] = V(0:k,:)^T Y0,  solve T^{-1} W = Z,  Y = [Y0; 0] - V W.
+// A's strict upper triangle (the R factor, dead by now) is overwritten with
+// triu(V^T V, 1); Zw (smem, k x ncols, ld k) holds Z then W.
+__device__ void apply_q_wy(double* A, int lda, int rows, int k, const double* tau, double* Y, int ldy,
+                           int ncols, double* Zw, bool y0_identity = false) {
+  // G = V^T V, strict upper triangle into A's upper triangle: computed into Zw
+  // first (A's upper triangle is still being read as structural zeros)
+  gemm_tc<true, false, 0, 3>(Zw, k, A, lda, A, lda, k, k, rows);
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += kThreads) {
+    const int j = e / k, i = e - j * k;
+    if (i < j) A[i + j * lda] = Zw[i + j * k];
+  }
+  __syncthreads();
+  // Z = V(0:k, :)^T Y0  (Y0 = I: Z = V(0:k, :)^T, unit upper triangular)
+  if (y0_identity) {
+    for (int e = threadIdx.x; e < k * ncols; e += kThreads) {
+      const int j = e / k, i = e - j * k;
+      Zw[i + j * k] = j > i ? A[j + i * lda] : (i == j ? 1.0 : 0.0);
+    }
+  } else {
+    gemm_tc<true, false, 0, 1>(Zw, k, A, lda, Y, ldy, k, ncols, k);
+  }
+  __syncthreads();
+  // solve T^{-1} W = Z column by column: 4 lanes per column, lane t owns rows
+  // i = t (mod 4) and keeps their running sums s_i = sum_{j > i} G_ij W_j
+  {
+    const int q4 = threadIdx.x & 3;
+    for (int col = threadIdx.x >> 2; col < ncols; col += kThreads / 4) {
+      double* z = Zw + col * k;
+      double sacc[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) sacc[r] = 0.0;
+      const unsigned gm = 0xfu << (threadIdx.x & 28);
+      for (int j = k - 1; j >= 0; --j) {
+        double wj = 0.0;
+        if ((j & 3) == q4) {
+          const double tj = tau[j];
+          double sj = 0.0;
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            if (4 * r + q4 == j) sj = sacc[r];
+          wj = tj == 0.0 ? 0.0 : tj * (z[j] - sj);
+          z[j] = wj;
+        }
+        wj = __shfl_sync(gm, wj, j & 3, 4);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int i = 4 * r + q4;
+          if (i < j) sacc[r] = fma(A[i + j * lda], wj, sacc[r]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // Y = [Y0; 0] - V W
+  gemm_tc<false, false, 0, 1, 1>(Y, ldy, A, lda, Zw, k, rows, ncols, k, k);
+  __syncthreads();
 }
 
 // Thin Q (rows x cols) from the factored form (linalg.hpp:77-98).

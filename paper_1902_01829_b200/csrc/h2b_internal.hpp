@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -61,6 +63,7 @@ inline cudaError_t malloc_retry(void** p, size_t bytes) {
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      if (std::getenv("H2B_TRACE")) fprintf(stderr, "  [trace] cudaMalloc(%zu) failed: trimming the pool\n", bytes);
       cudaDeviceSynchronize();
       cudaMemPoolTrimTo(pool, 0);
       e = cudaMalloc(p, bytes);
