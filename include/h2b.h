@@ -208,6 +208,28 @@ H2B_API h2b_status h2b_workspace(h2b_matrix* A, int which, void** ptr, int64_t* 
 H2B_API h2b_status h2b_part_upsweep(h2b_matrix* A, const double* x, void* stream);
 H2B_API h2b_status h2b_part_finish(h2b_matrix* A, double* y_slice, void* stream);
 
+/* ---- subtree-partitioned compression (compression.hpp:466-551 on 2^s GPUs) ----
+ * Every rank calls h2b_part_compress on its partition handle with the same eps;
+ * the library runs the phases on the rank's subtree and calls back into the
+ * host communicator at fixed points (same order on every rank):
+ *   allgather   in place on DEVICE memory: buf holds nparts slices of `count`
+ *               doubles, slice `part` is this rank's (NCCL all-gather); used for
+ *               the projection trees T of the levels >= s (orthogonalisation and
+ *               truncation) -- remote column bases of the coupling blocks;
+ *   allreduce_max_i32 / allreduce_sum_f64   element-wise on HOST memory: the
+ *               per-level truncated rank (compression.hpp:301,375), the
+ *               non-finite flag, ||A||_F^2 and the discarded energy.
+ * Levels < s are computed redundantly on every rank.  Callbacks return 0 on
+ * success.  The report is global (identical on every rank). */
+typedef struct h2b_comm {
+  void* ctx;
+  int (*allgather)(void* ctx, double* buf, int64_t count);
+  int (*allreduce_max_i32)(void* ctx, int32_t* v, int n);
+  int (*allreduce_sum_f64)(void* ctx, double* v, int n);
+} h2b_comm;
+H2B_API h2b_status h2b_part_compress(h2b_matrix* A, double eps, const h2b_comm* comm,
+                                     h2b_compress_report* report);
+
 /* Per-phase device time of the h2b_hmv calls made since phase timing was
  * enabled or last read, averaged per call (ms; CUDA events recorded on the
  * launching stream, no host syncs inside h2b_hmv):

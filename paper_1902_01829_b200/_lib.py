@@ -73,6 +73,17 @@ class CompressReport(C.Structure):
                 ("flops_truncate", C.c_double), ("flops_project_trunc", C.c_double)]
 
 
+# h2b_comm (include/h2b.h): host communicator callbacks of h2b_part_compress
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+ALLREDUCE_I32_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int32), C.c_int)
+ALLREDUCE_F64_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
+
+
+class Comm(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", ALLGATHER_FN),
+                ("allreduce_max_i32", ALLREDUCE_I32_FN), ("allreduce_sum_f64", ALLREDUCE_F64_FN)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "h2b_last_error": (C.c_char_p, []),
@@ -94,6 +105,7 @@ _SIGS = {
     "h2b_downsweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "h2b_dense_mv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int]),
     "h2b_compress": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(CompressReport)]),
+    "h2b_part_compress": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(Comm), C.POINTER(CompressReport)]),
     "h2b_orthogonalize": (C.c_int, [C.c_void_p, C.c_void_p]),
     "h2b_last_hmv_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "h2b_matrix_build_part": (C.c_int, [C.POINTER(BuildConfig), C.c_int, C.c_int, C.c_int,

@@ -239,17 +239,21 @@ class CompressionReport:
                 + self.time_truncate_ms + self.time_project_trunc_ms)
 
 
-def compress(A: H2Matrix, eps: float) -> CompressionReport:
-    """compress(A, eps) (compression.hpp:466-551), in place on the device."""
-    depth = A.info().depth
-    rep = _lib.CompressReport()
-    _lib.check(_lib.load().h2b_compress(A._h, float(eps), C.byref(rep)))
+def report_from_c(rep, depth: int) -> CompressionReport:
     return CompressionReport(
         list(rep.old_ranks[:depth + 1]), list(rep.new_ranks[:depth + 1]), rep.bytes_before,
         rep.bytes_after, rep.frobenius_error, rep.frobenius_norm, rep.time_orthogonalize_ms,
         rep.time_project_orth_ms, rep.time_weights_ms, rep.time_truncate_ms,
         rep.time_project_trunc_ms, rep.flops_orthogonalize, rep.flops_project_orth,
         rep.flops_weights, rep.flops_truncate, rep.flops_project_trunc)
+
+
+def compress(A: H2Matrix, eps: float) -> CompressionReport:
+    """compress(A, eps) (compression.hpp:466-551), in place on the device."""
+    depth = A.info().depth
+    rep = _lib.CompressReport()
+    _lib.check(_lib.load().h2b_compress(A._h, float(eps), C.byref(rep)))
+    return report_from_c(rep, depth)
 
 
 def orthogonalize_basis(A: H2Matrix) -> np.ndarray:

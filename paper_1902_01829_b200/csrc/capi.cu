@@ -449,7 +449,7 @@ using namespace h2b;
 // Implemented in build.cu / compress.cu.
 namespace h2b {
 h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, int part);
-void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep);
+void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_comm* comm = nullptr);
 void orthogonalize_matrix(Matrix& A, double* t_out);
 }  // namespace h2b
 
@@ -702,6 +702,16 @@ h2b_status h2b_compress(h2b_matrix* Ah, double eps, h2b_compress_report* report)
     require(Ah, "null matrix");
     whole(*Ah, "h2b_compress");
     compress_matrix(*Ah, eps, report);
+  });
+}
+
+h2b_status h2b_part_compress(h2b_matrix* Ah, double eps, const h2b_comm* comm, h2b_compress_report* report) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    if (Ah->part_s > 0)
+      require(comm && comm->allgather && comm->allreduce_max_i32 && comm->allreduce_sum_f64,
+              "h2b_part_compress: a partition handle needs a communicator");
+    compress_matrix(*Ah, eps, report, Ah->part_s > 0 ? comm : nullptr);
   });
 }
 

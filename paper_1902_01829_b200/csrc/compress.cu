@@ -704,8 +704,34 @@ struct Arena {
   static size_t need(size_t n, size_t elem) { return ((n * elem + 255) / 256) * 32; }
 };
 
+// Subtree partition of the compression: 2^s ranks, this one
+// owns the nodes [own_begin(l), own_end(l)) of every level l >= s (levels < s
+// replicated, computed redundantly).  Trees indexed by global node (T, R, Tt)
+// are allocated full-size; leaf / transfer pools are the handle's local ones.
+struct Part {
+  const h2b_comm* comm = nullptr;
+  int s = 0, g = 0;
+  bool dist() const { return comm != nullptr; }
+  // slice of level l >= s owned by this rank: contiguous in a per-level pool
+  void allgather(double* buf, int64_t count, cudaStream_t st) const {
+    if (!comm || count == 0) return;
+    H2B_CUDA(cudaStreamSynchronize(st));
+    if (comm->allgather(comm->ctx, buf, count) != 0) throw Error(H2B_CUDA_ERROR, "communicator: allgather failed");
+  }
+  void max_i32(int32_t* v, int n) const {
+    if (comm && comm->allreduce_max_i32(comm->ctx, v, n) != 0)
+      throw Error(H2B_CUDA_ERROR, "communicator: allreduce(max) failed");
+  }
+  void sum_f64(double* v, int n) const {
+    if (comm && comm->allreduce_sum_f64(comm->ctx, v, n) != 0)
+      throw Error(H2B_CUDA_ERROR, "communicator: allreduce(sum) failed");
+  }
+  // replicated levels are counted by rank 0 only in global sums
+  bool counts(int l) const { return !comm || l >= s || g == 0; }
+};
+
 // ---------------------------------------------------------------- phases
-void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops) {
+void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, const Part& pt) {
   const int q = A.q, m = A.m, kq = A.rank[q];
   require(m >= kq, "orthogonalize_basis: leaf_dim must be >= leaf rank");
   T.alloc(A, A.rank, A.rank, s);
@@ -714,29 +740,40 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
     const size_t sm = (2 * size_t(m) * kq + size_t(kq) * kq + 64 + 16) * sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "orthogonalize");
     set_smem(k_orth_leaf, sm);
-    k_orth_leaf<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, T.at(q));
+    if (A.own_count(q) > 0)
+      k_orth_leaf<<<unsigned(A.own_count(q)), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq,
+                                                                 T.at(q) + A.own_begin(q) * int64_t(kq) * kq);
     H2B_CUDA(cudaGetLastError());
   }
   flops += fl.qr(double(nl), m, kq);
-  for (int l = q; l >= 1; --l) {
+  auto level = [&](int l) {
     const int kc = A.rank[l], kp = A.rank[l - 1];
     const int64_t np = A.nodes(l - 1);
     flops += fl.gemm(double(A.nodes(l)), kc, kp, kc) + fl.qr(double(np), 2 * kc, kp);
     require(2 * kc >= kp, "qr_batched: requires rows >= cols");
-    if (kp == 0) continue;
+    if (kp == 0) return;
     const size_t sm = (2 * size_t(2 * kc) * kp + size_t(kp) * kp + 64 + 16) * sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "orthogonalize");
     set_smem(k_orth_level, sm);
-    k_orth_level<<<unsigned(np), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
-                                                   T.at(l), T.at(l - 1));
+    // parents [p0, p1) at level l-1; children 2p0.. in the (local) transfer pool
+    const int64_t p0 = A.own_begin(l - 1), p1 = A.own_end(l - 1);
+    k_orth_level<<<unsigned(p1 - p0), kThreads, sm, s>>>(
+        A.transfer.p + A.tr_off[l] + (2 * p0 - A.tr_begin(l)) * A.tr_stride(l), A.ld(l), kc, kp,
+        T.at(l) + 2 * p0 * int64_t(kc) * kc, T.at(l - 1) + p0 * int64_t(kp) * kp);
     H2B_CUDA(cudaGetLastError());
-  }
+  };
+  for (int l = q; l > pt.s; --l) level(l);
+  // the projection tree of the partitioned levels: remote column bases for
+  // the projection, the level-s roots for the replicated top
+  for (int l = pt.s; l <= q; ++l)
+    pt.allgather(T.at(l), (int64_t(1) << (l - pt.s)) * A.rank[l] * A.rank[l], s);
+  for (int l = pt.s; l >= 1; --l) level(l);
 }
 
 // Project every coupling level with T (rows x cols per node): blocks become
 // T.rows[l] x T.rows[l].  Writes into `out_pool` (may alias the current pool
 // when the shapes agree).
-void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place) {
+void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place, const Part& pt) {
   const int q = A.q;
   ProjTable P{};
   P.tri = in_place ? 1 : 0;
@@ -756,7 +793,7 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     const int rn = T.rows[l], ro = T.cols[l];
     if (L.nb == 0) continue;
     require(ro == L.br && ro == L.bc, "project_coupling: dim mismatch");
-    flops += fl.gemm(double(L.nb), rn, ro, ro) + fl.gemm(double(L.nb), rn, rn, ro);
+    if (pt.counts(l)) flops += fl.gemm(double(L.nb), rn, ro, ro) + fl.gemm(double(L.nb), rn, rn, ro);
     ProjLevel& d = P.L[l];
     d.S = L.val;
     d.out = base + new_off[l];
@@ -806,7 +843,7 @@ double sumsq(const double* v, int64_t n, cudaStream_t s) {
   return acc;
 }
 
-void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
+void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, const Part& pt) {
   const int q = A.q;
   R.alloc(A, A.rank, A.rank, s);
   H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * A.rank[0] * A.rank[0], s));
@@ -816,16 +853,16 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
   std::vector<int64_t> ooff(q + 2, 0);
   for (int l = 1; l <= q; ++l) {
     pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
-    ooff[l + 1] = ooff[l] + A.nodes(l) + 1;
+    ooff[l + 1] = ooff[l] + A.own_count(l) + 1;
   }
   std::vector<int32_t> ord(std::max<int64_t>(1, ooff[q + 1]), 0);
-  for (int l = 1; l <= q; ++l) {
+  for (int l = 1; l <= q; ++l) {  // node indices relative to own_begin(l)
     const Layer& L = A.cpl[l];
     int32_t* o = ord.data() + ooff[l];
-    const int64_t nn = A.nodes(l);
+    const int64_t nn = A.own_count(l), r0 = A.own_begin(l);
     for (int64_t i = 0; i < nn; ++i) o[i] = int32_t(i);
     std::stable_sort(o, o + nn, [&](int32_t a, int32_t b) {
-      return L.h_rp[a + 1] - L.h_rp[a] > L.h_rp[b + 1] - L.h_rp[b];
+      return L.h_rp[r0 + a + 1] - L.h_rp[r0 + a] > L.h_rp[r0 + b + 1] - L.h_rp[r0 + b];
     });
     o[nn] = 0;
   }
@@ -844,14 +881,16 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
     struct {
       double* p;
     } Pbuf{Pall};
-    if (kp > 0) {
-      k_weights_parent<<<unsigned(A.nodes(l)), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
-                                                                  R.at(l - 1), Pbuf.p);
+    const int64_t r0 = A.own_begin(l), nn = A.own_count(l);  // r0 is even unless l == s (one node)
+    if (kp > 0 && nn > 0) {
+      k_weights_parent<<<unsigned(nn), kThreads, 0, s>>>(
+          A.transfer.p + A.tr_off[l] + (r0 - A.tr_begin(l)) * A.tr_stride(l), A.ld(l), kc, kp,
+          R.at(l - 1) + (r0 >> 1) * int64_t(kp) * kp, Pbuf.p);
       H2B_CUDA(cudaGetLastError());
     }
+    if (nn == 0) continue;
     constexpr int CR = 32;
     const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
-    const int64_t nn = A.nodes(l);
     // LPT order: nodes by decreasing stack height
     struct {
       int32_t* p;
@@ -866,7 +905,8 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops) {
                                                            32 * kWWarps, sm));                      \
     const int64_t want = (nn + kWWarps - 1) / kWWarps;                                              \
     const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(dev_sms) * std::max(1, per_sm)))); \
-    k_weights<NCOL, CR><<<grid, 32 * kWWarps, sm, s>>>(Pbuf.p, kc, kp, L.rp, L.val, L.ld, R.at(l), nn, \
+    k_weights<NCOL, CR><<<grid, 32 * kWWarps, sm, s>>>(Pbuf.p, kc, kp, L.rp + r0, L.val, L.ld,          \
+                                                       R.at(l) + r0 * int64_t(kc) * kc, nn,            \
                                                        dord.p, reinterpret_cast<int*>(dord.p + nn)); \
   }
     H2B_WEIGHTS(1) H2B_WEIGHTS(2)
@@ -906,7 +946,7 @@ struct Trace {
 // Returns the discarded energy; fills Tt (new x old per node) and replaces
 // the leaf / transfer pools and ranks.
 double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s, Flops& fl,
-                double& flops) {
+                double& flops, const Part& pt) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   Trace tr;
   const int q = A.q, m = A.m;
@@ -919,10 +959,11 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   // in place; the new transfers: one region per level, compacted at the end.
   Tt.alloc(A, old, old, s);
   std::vector<int64_t> ntoff(q + 2, 0);
-  for (int l = 1; l <= q; ++l) ntoff[l + 1] = ntoff[l] + A.nodes(l) * int64_t(pad2(old[l])) * old[l - 1];
+  for (int l = 1; l <= q; ++l) ntoff[l + 1] = ntoff[l] + A.tr_count(l) * int64_t(pad2(old[l])) * old[l - 1];
   const int sl_leaf = std::min(m, old[q]);
-  size_t lvl = Arena::need(size_t(nl) * m * sl_leaf, 8) + Arena::need(size_t(nl) * sl_leaf, 8) +
-               Arena::need(size_t(nl), 8);
+  const int64_t nlo = std::max<int64_t>(1, A.own_count(q)), l0 = A.own_begin(q);  // owned leaves
+  size_t lvl = Arena::need(size_t(nlo) * m * sl_leaf, 8) + Arena::need(size_t(nlo) * sl_leaf, 8) +
+               Arena::need(size_t(nlo), 8);
   for (int l = q; l >= 1; --l) {
     const int64_t np = A.nodes(l - 1);
     const int zr = 2 * old[l], kp = old[l - 1], sl = std::min(zr, kp);
@@ -940,33 +981,38 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     const int sl = sl_leaf;
     flops += fl.gemm(double(nl), m, kq, kq) + fl.svd(double(nl), m, kq);
     ar.off = lvl_base;
-    double* Uq = ar.take<double>(size_t(nl) * m * sl);
-    double* sg = ar.take<double>(size_t(nl) * sl);
-    double* en = ar.take<double>(size_t(nl));
+    const int64_t no = A.own_count(q);
+    double* Uq = ar.take<double>(size_t(nlo) * m * sl);
+    double* sg = ar.take<double>(size_t(nlo) * sl);
+    double* en = ar.take<double>(size_t(nlo));
     H2B_CUDA(cudaMemsetAsync(dk, 0, 2 * sizeof(int), s));
-    if (sl > 0) {
+    if (sl > 0 && no > 0) {
       const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + size_t(std::max(sl * (sl + 1), kq * m))) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_leaf_svd, sm);
-      k_trunc_leaf_svd<<<unsigned(nl), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, R.at(q), Uq, sg, eps,
-                                                          dk, dk + 1);
+      k_trunc_leaf_svd<<<unsigned(no), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq,
+                                                          R.at(q) + l0 * int64_t(kq) * kq, Uq, sg, eps, dk,
+                                                          dk + 1);
       H2B_CUDA(cudaGetLastError());
     }
     tr.at(s, "leaf svd", q);
     int flags[2] = {0, 0};
     H2B_CUDA(cudaMemcpyAsync(flags, dk, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2B_CUDA(cudaStreamSynchronize(s));
+    pt.max_i32(flags, 2);  // the level rank is the max over ALL leaves
     require(flags[1] == 0, "svd_truncated_batched: non-finite input");
     const int kt = std::min(flags[0], sl);
     nr[q] = kt;
     flops += fl.gemm(double(nl), kt, kq, m);
     const int ldn = pad2(m);
-    newleaf.alloc_pooled(std::max<int64_t>(1, nl * ldn * kt), s);
-    k_trunc_leaf_apply<<<unsigned(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq, sg, Tt.at(q),
-                                                         newleaf.p, ldn, en);
-    H2B_CUDA(cudaGetLastError());
-    lev_e[q] = sum_host(en, nl, s);
+    newleaf.alloc_pooled(std::max<int64_t>(1, no * ldn * kt), s);
+    if (no > 0) {
+      k_trunc_leaf_apply<<<unsigned(no), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq, sg,
+                                                           Tt.at(q) + l0 * int64_t(kt) * kq, newleaf.p, ldn, en);
+      H2B_CUDA(cudaGetLastError());
+    }
+    lev_e[q] = sum_host(en, no, s);
     tr.at(s, "leaf apply", q);
   }
   for (int l = q; l >= 1; --l) {
@@ -976,36 +1022,49 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     const int sl = std::min(zr, kp);
     flops += fl.gemm(double(A.nodes(l)), ktc, kp, kc) + fl.gemm(double(np), zr, kp, kp) +
              fl.svd(double(np), zr, kp);
+    if (l == pt.s)  // the replicated top needs every level-s child's T
+      pt.allgather(Tt.at(l), int64_t(ktc) * kc, s);
+    const int64_t p0 = A.own_begin(l - 1), npo = A.own_count(l - 1);  // parents here
     ar.off = lvl_base;
-    double* Z = ar.take<double>(size_t(np) * zr * kp);
-    double* U = ar.take<double>(size_t(np) * zr * sl);
-    double* sg = ar.take<double>(size_t(np) * sl);
-    double* en = ar.take<double>(size_t(np));
+    double* Z = ar.take<double>(size_t(npo) * zr * kp);
+    double* U = ar.take<double>(size_t(npo) * zr * sl);
+    double* sg = ar.take<double>(size_t(npo) * sl);
+    double* en = ar.take<double>(size_t(npo));
     H2B_CUDA(cudaMemsetAsync(dk, 0, 2 * sizeof(int), s));
-    if (sl > 0) {
+    const int64_t es = A.tr_stride(l);
+    if (sl > 0 && npo > 0) {
       const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + size_t(std::max(sl * (sl + 1), kp * zr))) *
                         sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_level_svd, sm);
-      k_trunc_level_svd<<<unsigned(np), kThreads, sm, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, ktc,
-                                                           Tt.at(l), R.at(l - 1), Z, U, sg, eps, dk, dk + 1);
+      k_trunc_level_svd<<<unsigned(npo), kThreads, sm, s>>>(
+          A.transfer.p + A.tr_off[l] + (2 * p0 - A.tr_begin(l)) * es, A.ld(l), kc, kp, ktc,
+          Tt.at(l) + 2 * p0 * int64_t(ktc) * kc, R.at(l - 1) + p0 * int64_t(kp) * kp, Z, U, sg, eps, dk, dk + 1);
       H2B_CUDA(cudaGetLastError());
     }
     tr.at(s, "level svd", l);
     int flags[2] = {0, 0};
     H2B_CUDA(cudaMemcpyAsync(flags, dk, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2B_CUDA(cudaStreamSynchronize(s));
+    if (l - 1 >= pt.s) pt.max_i32(flags, 2);  // (replicated parents agree already)
     require(flags[1] == 0, "svd_truncated_batched: non-finite input");
     const int ktp = std::min(flags[0], sl);
     nr[l - 1] = ktp;
     flops += fl.gemm(double(np), ktp, kp, zr);
     const int ldn = pad2(ktc);
-    k_trunc_level_apply<<<unsigned(np), kThreads, 0, s>>>(ktc, kp, sl, ktp, Z, U, sg, Tt.at(l - 1),
-                                                          newtr + ntoff[l], ldn, en);
-    H2B_CUDA(cudaGetLastError());
-    lev_e[l - 1] = sum_host(en, np, s);
+    if (npo > 0) {
+      k_trunc_level_apply<<<unsigned(npo), kThreads, 0, s>>>(
+          ktc, kp, sl, ktp, Z, U, sg, Tt.at(l - 1) + p0 * int64_t(ktp) * kp,
+          newtr + ntoff[l] + (2 * p0 - A.tr_begin(l)) * int64_t(ldn) * ktp, ldn, en);
+      H2B_CUDA(cudaGetLastError());
+    }
+    const double el = sum_host(en, npo, s);
+    lev_e[l - 1] = pt.counts(l - 1) ? el : 0.0;
     tr.at(s, "level apply", l);
   }
+  // the projection with the rectangular T needs remote column bases too
+  for (int l = pt.s + 1; l <= q; ++l)
+    pt.allgather(Tt.at(l), (int64_t(1) << (l - pt.s)) * nr[l] * old[l], s);
   Tt.rows = nr;  // per node: new x old, at the old-rank level offsets
   // new transfer pool with padded ld for the new ranks
   A.rank = nr;
@@ -1013,13 +1072,13 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   int64_t t = 0;
   for (int l = 1; l <= q; ++l) {
     toff[l] = t;
-    t += A.nodes(l) * A.tr_stride(l);
+    t += A.tr_count(l) * A.tr_stride(l);
   }
   toff[q + 1] = t;
   DevBuf<double> trpool;
   trpool.alloc_pooled(std::max<int64_t>(1, t), s);
   for (int l = 1; l <= q; ++l) {
-    const int64_t sz = A.nodes(l) * A.tr_stride(l);
+    const int64_t sz = A.tr_count(l) * A.tr_stride(l);
     if (sz) H2B_CUDA(cudaMemcpyAsync(trpool.p + toff[l], newtr + ntoff[l], sz * sizeof(double),
                                      cudaMemcpyDeviceToDevice, s));
   }
@@ -1057,7 +1116,18 @@ struct DeviceGuard {
 
 }  // namespace
 
-void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep) {
+// memory_footprint (h2_matrix.hpp:90-102) of the part of the matrix this
+// rank accounts for: its own blocks, replicated top levels on rank 0 only
+uint64_t counted_footprint(const Matrix& A, const Part& pt) {
+  uint64_t e = uint64_t(A.dense.nb) * A.dense.br * A.dense.bc + uint64_t(A.own_count(A.q)) * A.m * A.rank[A.q];
+  for (int l = 0; l <= A.q; ++l)
+    if (pt.counts(l)) e += uint64_t(A.cpl[l].nb) * A.cpl[l].br * A.cpl[l].bc;
+  for (int l = 1; l <= A.q; ++l)
+    if (l > pt.s || pt.counts(0)) e += uint64_t(A.tr_count(l)) * A.rank[l] * A.rank[l - 1];
+  return e * sizeof(double);
+}
+
+void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_comm* comm) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   DeviceGuard g(A.device);
   cudaStream_t s = A.stream;
@@ -1078,48 +1148,72 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep) {
     fprintf(stderr, "  [trace] compress start: pool reserved %.2f GB used %.2f GB, device free %.2f GB\n",
             res / 1e9, used / 1e9, fr / 1e9);
   }
+  Part pt;
+  pt.comm = comm;
+  pt.s = comm ? A.part_s : 0;
+  pt.g = comm ? A.part_g : 0;
   Flops fl;
   h2b_compress_report r{};
   for (int l = 0; l <= A.q; ++l) r.old_ranks[l] = A.rank[l];
-  r.bytes_before = A.footprint();
+  // the reference's padded weight-stack height uses the GLOBAL longest block row
+  std::vector<int32_t> mrow(A.q + 1);
+  for (int l = 0; l <= A.q; ++l) mrow[l] = A.cpl[l].max_row;
+  pt.max_i32(mrow.data(), A.q + 1);
+  std::vector<int> saved_max(A.q + 1);
+  for (int l = 0; l <= A.q; ++l) {
+    saved_max[l] = A.cpl[l].max_row;
+    A.cpl[l].max_row = mrow[l];
+  }
+  double sums[3] = {double(counted_footprint(A, pt)), 0.0, 0.0};
 
   TreePool To, R, Tt;
   {
     Timer t(s);
-    orthogonalize(A, To, s, fl, r.flops_orthogonalize);
+    orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt);
     r.time_orthogonalize_ms = t.stop();
   }
   {
     Timer t(s);
-    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true);
+    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true, pt);
     r.time_project_orth_ms = t.stop();
   }
   To.buf.release();
   double n2 = 0.0;
-  for (int l = 0; l <= A.q; ++l) n2 += sumsq(A.cpl[l].val, A.cpl[l].nb * A.cpl[l].block_stride(), s);
+  for (int l = 0; l <= A.q; ++l)
+    if (pt.counts(l)) n2 += sumsq(A.cpl[l].val, A.cpl[l].nb * A.cpl[l].block_stride(), s);
   n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s);
+  pt.sum_f64(&n2, 1);
   r.frobenius_norm = std::sqrt(n2);
   {
     Timer t(s);
-    weights(A, R, s, fl, r.flops_weights);
+    weights(A, R, s, fl, r.flops_weights, pt);
     r.time_weights_ms = t.stop();
   }
+  for (int l = 0; l <= A.q; ++l) A.cpl[l].max_row = saved_max[l];
   double energy = 0.0;
   {
     Timer t(s);
-    energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate);
+    energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate, pt);
     r.time_truncate_ms = t.stop();
   }
   R.buf.release();
   {
     Timer t(s);
-    project(A, Tt, s, fl, r.flops_project_trunc, /*in_place=*/false);
+    project(A, Tt, s, fl, r.flops_project_trunc, /*in_place=*/false, pt);
     r.time_project_trunc_ms = t.stop();
   }
   relayout(A);
   for (int l = 0; l <= A.q; ++l) r.new_ranks[l] = A.rank[l];
-  r.bytes_after = A.footprint();
+  // global sums: footprints, discarded energy, projection flops (local rows)
+  double g5[5] = {sums[0], double(counted_footprint(A, pt)), energy, r.flops_project_orth, r.flops_project_trunc};
+  pt.sum_f64(g5, 5);
+  r.bytes_before = uint64_t(g5[0]);
+  r.bytes_after = uint64_t(g5[1]);
+  energy = g5[2];
+  r.flops_project_orth = g5[3];
+  r.flops_project_trunc = g5[4];
   r.frobenius_error = r.frobenius_norm > 0 ? std::sqrt(energy) / r.frobenius_norm : 0.0;
+  if (A.part_s > 0) A.global_footprint = r.bytes_after;
   if (rep) *rep = r;
 #ifdef H2B_SWEEP_HIST
   int hist[64];
@@ -1139,7 +1233,7 @@ void orthogonalize_matrix(Matrix& A, double* t_out) {
   Flops fl;
   double f = 0;
   TreePool T;
-  orthogonalize(A, T, s, fl, f);
+  orthogonalize(A, T, s, fl, f, Part{});
   if (t_out && T.off[A.q + 1])
     H2B_CUDA(cudaMemcpyAsync(t_out, T.buf.p, T.off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToHost, s));
   H2B_CUDA(cudaStreamSynchronize(s));

@@ -64,6 +64,166 @@ def gather_xhat(plan: PartitionPlan, xhat, allgather):
         allgather(level, level[plan.part * chunk:(plan.part + 1) * chunk].clone())
 
 
+# ------------------------------------------------------------------ communicators
+def _wrap(ptr: int, count: int, device):
+    """Zero-copy torch view of `count` doubles at `ptr` (device memory when
+    `device` is an int, host memory when None)."""
+    import numpy as np
+    import torch
+    if device is None:
+        arr = np.ctypeslib.as_array((C.c_double * int(count)).from_address(int(ptr)))
+        return torch.from_numpy(arr)
+    return torch.as_tensor(_CudaView(ptr, count, "<f8", device), device=f"cuda:{device}")
+
+
+class Communicator:
+    """Host side of h2b_comm (include/h2b.h) for h2b_part_compress: the library
+    calls allgather / allreduce at fixed points of the compression, in the
+    same order on every rank.  Subclasses implement the three collectives on
+    torch tensors:
+      allgather(buf)     buf holds nparts equal slices (device memory); slice
+                         `part` is this rank's; fill the others in place
+      allreduce_max(t)   element-wise, in place (host int32 tensor)
+      allreduce_sum(t)   element-wise, in place (host float64 tensor)"""
+
+    def __init__(self, nparts: int, part: int, device):
+        self.nparts, self.part, self.device = nparts, part, device
+        self._c = None
+
+    def allgather(self, buf):
+        raise NotImplementedError
+
+    def allreduce_max(self, t):
+        raise NotImplementedError
+
+    def allreduce_sum(self, t):
+        raise NotImplementedError
+
+    def as_c(self) -> "_lib.Comm":
+        """ctypes h2b_comm whose callbacks call this object (kept alive by it)."""
+        import numpy as np
+        import torch
+
+        def ag(ctx, ptr, count):
+            try:
+                self.allgather(_wrap(ptr, int(count) * self.nparts, self.device))
+                return 0
+            except Exception as e:  # noqa: BLE001  (cannot propagate through C)
+                self.error = e
+                return 1
+
+        def mx(ctx, v, n):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(v, shape=(int(n),)))
+                self.allreduce_max(t)
+                return 0
+            except Exception as e:  # noqa: BLE001
+                self.error = e
+                return 1
+
+        def sm(ctx, v, n):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(v, shape=(int(n),)))
+                self.allreduce_sum(t)
+                return 0
+            except Exception as e:  # noqa: BLE001
+                self.error = e
+                return 1
+
+        self.error = None
+        self._fns = (_lib.ALLGATHER_FN(ag), _lib.ALLREDUCE_I32_FN(mx), _lib.ALLREDUCE_F64_FN(sm))
+        self._c = _lib.Comm(None, *self._fns)
+        return self._c
+
+
+class TorchComm(Communicator):
+    """torch.distributed collectives (NCCL over NVLink for the device
+    all-gathers; the small host all-reduces go through the same group)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        super().__init__(dist.get_world_size(group), dist.get_rank(group), device)
+        self.group = group
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def allgather(self, buf):
+        import torch
+        import torch.distributed as dist
+        chunk = buf.numel() // self.nparts
+        mine = buf[self.part * chunk:(self.part + 1) * chunk].clone()
+        if buf.is_cuda:
+            dist.all_gather_into_tensor(buf, mine, group=self.group)
+            torch.cuda.synchronize()
+        else:
+            parts = [torch.empty_like(mine) for _ in range(self.nparts)]
+            dist.all_gather(parts, mine, group=self.group)
+            buf.copy_(torch.cat(parts))
+
+    def _allreduce(self, t, op):
+        import torch
+        import torch.distributed as dist
+        if self.nccl:
+            d = t.to(f"cuda:{self.device}")
+            dist.all_reduce(d, op=op, group=self.group)
+            t.copy_(d.cpu())
+        else:
+            dist.all_reduce(t, op=op, group=self.group)
+
+    def allreduce_max(self, t):
+        import torch.distributed as dist
+        self._allreduce(t, dist.ReduceOp.MAX)
+
+    def allreduce_sum(self, t):
+        import torch.distributed as dist
+        self._allreduce(t, dist.ReduceOp.SUM)
+
+
+class ThreadComm:
+    """In-process communicator for P partitions driven by P threads (one GPU
+    emulating P ranks): rank(part) returns the Communicator of one thread."""
+
+    def __init__(self, nparts: int, device=0):
+        import threading
+        self.nparts, self.device = nparts, device
+        self.barrier = threading.Barrier(nparts)
+        self.slots = [None] * nparts
+
+    def rank(self, part: int) -> Communicator:
+        outer = self
+
+        class _R(Communicator):
+            def _exchange(self, value):
+                outer.slots[self.part] = value
+                outer.barrier.wait()
+                vals = list(outer.slots)
+                outer.barrier.wait()
+                return vals
+
+            def allgather(self, buf):
+                import torch
+                chunk = buf.numel() // outer.nparts
+                vals = self._exchange(buf[self.part * chunk:(self.part + 1) * chunk].clone())
+                for g, v in enumerate(vals):
+                    if g != self.part:
+                        buf[g * chunk:(g + 1) * chunk].copy_(v)
+                if buf.is_cuda:
+                    torch.cuda.synchronize()
+
+            def allreduce_max(self, t):
+                import torch
+                vals = self._exchange(t.clone())
+                t.copy_(torch.stack(vals).max(dim=0).values)
+
+            def allreduce_sum(self, t):
+                vals = self._exchange(t.clone())
+                acc = vals[0].clone()
+                for v in vals[1:]:  # fixed order: identical sums on every rank
+                    acc += v
+                t.copy_(acc)
+
+        return _R(self.nparts, part, self.device)
+
+
 class DistributedH2Matrix:
     """Rank-local partition of construct<double>(...) (construction.hpp:179-200)."""
 
@@ -119,6 +279,33 @@ class DistributedH2Matrix:
             self.close()
         except Exception:
             pass
+
+    def _refresh(self):
+        """Re-read shapes and workspace views (compression changes the ranks)."""
+        import torch
+        inf = _lib.MatrixInfo()
+        _lib.check(_lib.load().h2b_matrix_info_get(self._h, C.byref(inf)))
+        self.info = inf
+        self.ranks = list(inf.ranks[:self.depth + 1])
+        self.plan = PartitionPlan(self.depth, self.ranks, self.m, self.nparts, self.part)
+        self.xhat = device_view(self._h, _lib.WS_XHAT, self.device)
+
+    def compress(self, eps: float, comm: Communicator | None = None):
+        """compress(A, eps) (compression.hpp:466-551) of the whole partitioned
+        matrix: every rank calls it with the same eps; the collectives go through
+        `comm` (default: TorchComm over this matrix's process group).  Returns
+        the global CompressionReport (identical on every rank)."""
+        from .api import report_from_c
+        if comm is None:
+            comm = TorchComm(self.group, self.device)
+        rep = _lib.CompressReport()
+        cs = comm.as_c()
+        st = _lib.load().h2b_part_compress(self._h, float(eps), C.byref(cs), C.byref(rep))
+        if st != _lib.H2B_OK and getattr(comm, "error", None) is not None:
+            raise RuntimeError(f"communicator failed: {comm.error!r}")
+        _lib.check(st)
+        self._refresh()
+        return report_from_c(rep, self.depth)
 
     def gather_xhat(self, allgather):
         gather_xhat(self.plan, self.xhat, allgather)

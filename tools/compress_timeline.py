@@ -28,8 +28,13 @@ for _ in range(reps):
     big = [(round(g, 2), a, b) for g, a, b in gaps if g > 1.0]
     gaps.sort(reverse=True)
     slow = sorted(((e.time_range.elapsed_us() / 1e3, e.name[:50]) for e in ev), reverse=True)[:6]
+    agg = {}
+    for e in ev:
+        k = e.name.replace("h2b::(anonymous namespace)::", "").replace("void ", "").split("(")[0][:30]
+        agg[k] = agg.get(k, 0.0) + e.time_range.elapsed_us() / 1e3
     print(json.dumps(dict(ms=round(rep.total_ms(), 1), kernels_busy_ms=round(busy, 1), span_ms=round(span, 1),
                           gaps_over_1ms=big, gap_total_ms=round(sum(g for g, _, _ in gaps), 1),
-                          top_kernels=[(round(t, 2), k) for t, k in slow])), flush=True)
+                          top_kernels=[(round(t, 2), k) for t, k in slow],
+                          per_kernel={k: round(v, 1) for k, v in sorted(agg.items(), key=lambda kv: -kv[1])})), flush=True)
     A.close()
     del A
