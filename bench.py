@@ -185,7 +185,7 @@ def cpu_reference_sample(steps: int | None = None, budget_s: float = 20.0):
                       f"host construct {build_s:.1f} s"}
 
 
-FP64_PEAK_TFLOPS = 74.3  # DMMA m8n8k4 measured on this pool's B200 (tools/fp64_peak.cu); DFMA 36.4
+FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 measured on this pool's B200 (tools/fp64_peak.cu: 37.07); DFMA 36.4
 COMPRESS_CFG = dict(dim=3, n=1 << 20, grid_order=4, eps=1e-6)
 
 
@@ -195,21 +195,24 @@ def compression_run(h2, torch, device, reps):
     warm = h2.H2Matrix.construct(2, 1 << 14, device=device)
     h2.compress(warm, 1e-7)
     warm.close()
-    times, rep = [], None
+    times, dev, rep = [], [], None
     for _ in range(max(1, reps)):
         A = h2.H2Matrix.construct(COMPRESS_CFG["dim"], COMPRESS_CFG["n"],
                                   grid_order=COMPRESS_CFG["grid_order"], device=device)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep = h2.compress(A, COMPRESS_CFG["eps"])
+        r = h2.compress(A, COMPRESS_CFG["eps"])
         torch.cuda.synchronize()
         times.append((time.perf_counter() - t0) * 1e3)
-        dev_ms = rep.total_ms()
+        dev.append(r.total_ms())
+        if rep is None or r.total_ms() <= rep.total_ms():
+            rep = r
         A.close()
-    dev_ms = rep.total_ms()
+    dev_ms = rep.total_ms()  # best rep: the first one also pays the memory pool's growth
     gflops = rep.total_flops() / (dev_ms * 1e-3) / 1e9
     return {"config": "3D exponential covariance n=2^20, leaf 64, order 4 (rank 64), eps 1e-6 (C3)",
-            "ms": round(dev_ms, 1), "wall_ms": round(min(times), 1), "reps": len(times),
+            "ms": round(dev_ms, 1), "ms_all_reps": [round(v, 1) for v in dev],
+            "wall_ms": round(min(times), 1), "reps": len(times),
             "model_flops": rep.total_flops(), "gflops": round(gflops, 1),
             "pct_fp64_peak": round(100 * gflops / 1e3 / FP64_PEAK_TFLOPS, 2),
             "fp64_peak_tflops": FP64_PEAK_TFLOPS,
@@ -220,6 +223,35 @@ def compression_run(h2, torch, device, reps):
                          "project_trunc": round(rep.time_project_trunc_ms, 1)},
             "new_ranks": rep.new_ranks, "frobenius_error": rep.frobenius_error,
             "bytes": [rep.bytes_before, rep.bytes_after]}
+
+
+def compression_run_dist(torch, device, reps, world):
+    """Subtree-partitioned compress() of C3 across the ranks (h2b_part_compress,
+    NCCL all-gathers of the projection trees): device time = max over ranks of
+    the per-rank phase times (collective waits included)."""
+    import paper_1902_01829_b200 as h2
+    from paper_1902_01829_b200.dist import DistributedH2Matrix
+    warm = DistributedH2Matrix(2, 1 << 14, device=device)
+    warm.compress(1e-7)
+    warm.close()
+    best, rep = None, None
+    for _ in range(max(1, reps)):
+        D = DistributedH2Matrix(COMPRESS_CFG["dim"], COMPRESS_CFG["n"], grid_order=COMPRESS_CFG["grid_order"],
+                                device=device)
+        torch.cuda.synchronize()
+        barrier(world)
+        rep = D.compress(COMPRESS_CFG["eps"])
+        ms = max_over_ranks(rep.total_ms(), world)
+        best = ms if best is None else min(best, ms)
+        D.close()
+    h2.release_cached_memory(device)
+    gflops = rep.total_flops() / (best * 1e-3) / 1e9
+    return {"config": "3D exponential covariance n=2^20, leaf 64, order 4 (rank 64), eps 1e-6 (C3), "
+                      f"subtree-partitioned over {world} GPUs",
+            "ms": round(best, 1), "reps": reps, "model_flops": rep.total_flops(), "gflops": round(gflops, 1),
+            "pct_fp64_peak_per_gpu": round(100 * gflops / 1e3 / FP64_PEAK_TFLOPS / world, 2),
+            "fp64_peak_tflops": FP64_PEAK_TFLOPS, "new_ranks": rep.new_ranks,
+            "frobenius_error": rep.frobenius_error, "bytes": [rep.bytes_before, rep.bytes_after]}
 
 
 def multi16_run(A, torch, steps):
@@ -352,12 +384,15 @@ def run_distributed(args, cfg, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     # parity spot check against the replicated-input result
     assert torch.allclose(yh, y.cpu(), rtol=0, atol=0)
+    inf = D.info
+    D.close()
+    comp = None
+    if not args.no_compress:
+        comp = compression_run_dist(torch, local, args.compress_reps, world)
     if rank != 0:
-        D.close()
         dist.destroy_process_group()
         return
     peak, peak_src = load_peaks()
-    inf = D.info
     q = inf.depth
     bsr_bytes = 8 * (sum(inf.cpl_blocks[l] * inf.ranks[l] ** 2 for l in range(q + 1))
                      + inf.dense_blocks * inf.m * inf.m)
@@ -385,9 +420,9 @@ def run_distributed(args, cfg, world, rank, local):
         # ours per step: up_leaf, gather, per-level up (q), bsr, per-level down (q), down_leaf
         "gpu_launches": (2 * q + 4) * args.steps,
         "clocks": clocks,
+        "compression": comp,
     }
     print(json.dumps(line), flush=True)
-    D.close()
     dist.destroy_process_group()
 
 
@@ -400,7 +435,7 @@ def main():
     ap.add_argument("--n", type=int, default=WORKLOAD["n"], help="override n (testing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compress", action="store_true")
-    ap.add_argument("--compress-reps", type=int, default=2)
+    ap.add_argument("--compress-reps", type=int, default=3)
     ap.add_argument("--dist", action="store_true",
                     help="use the subtree-partitioned path even at N=1 (testing)")
     args = ap.parse_args()
