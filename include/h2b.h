@@ -178,9 +178,8 @@ H2B_API h2b_status h2b_compress(h2b_matrix* A, double eps, h2b_compress_report* 
 /* Orthogonalize only (in place); projection tree written to t_out (host,
  * level-concatenated ranks[l]^2 per node) when non-NULL. */
 H2B_API h2b_status h2b_orthogonalize(h2b_matrix* A, double* t_out);
-/* compress() takes its scratch (and the re-laid-out pools) from the device's
- * default stream-ordered memory pool, which caches freed memory for the next
- * call; this hands the cached, unused memory back to the device. */
+/* compress() keeps its device workspace (projection / weight trees and
+ * scratch, a few GB) cached per device for the next call; this frees it. */
 H2B_API h2b_status h2b_release_cached_memory(int device);
 
 /* validate_sampled (validate.hpp:26-62) on the device: relative mat-vec error

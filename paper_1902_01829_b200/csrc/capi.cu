@@ -120,13 +120,7 @@ void download_blocks(const double* d, double* h, int rows, int cols, int64_t cou
 }  // namespace
 
 Matrix::~Matrix() {
-  // pools re-laid out by compress() come from the stream-ordered pool and are
-  // freed on this stream: release them before the stream goes away
   if (stream) cudaStreamSynchronize(stream);
-  leaf.release();
-  transfer.release();
-  cpl_val.release();
-  dense_val.release();
   if (h_stage) cudaFreeHost(h_stage);
   for (auto& e : ev_pool)
     if (e) cudaEventDestroy(e);
@@ -162,19 +156,9 @@ double Matrix::hmv_flops() const {
 // (n, m, q, rank, layers' host CSR).  Values are left uninitialised.
 void allocate(Matrix& A) {
   const int q = A.q;
-  // The device's default stream-ordered pool keeps freed memory cached (a
-  // caching allocator: rebuilding / compressing matrices does not re-map
-  // pages); h2b_release_cached_memory hands it back.
-  {
-    cudaMemPool_t pool;
-    H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, A.device));
-    uint64_t keep = ~uint64_t(0);
-    H2B_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  }
   A.ldm = pad2(A.m);
   A.perm.alloc(A.n);
-  // the big pools come from the stream-ordered pool (see compress_matrix)
-  A.leaf.alloc_pooled(size_t(A.own_count(q)) * A.leaf_stride(), A.stream);
+  A.leaf.alloc(size_t(A.own_count(q)) * A.leaf_stride());
   A.tr_off.assign(q + 2, 0);
   int64_t t = 0;
   for (int l = 1; l <= q; ++l) {
@@ -182,7 +166,7 @@ void allocate(Matrix& A) {
     t += A.tr_count(l) * A.tr_stride(l);
   }
   A.tr_off[q + 1] = t;
-  A.transfer.alloc_pooled(t, A.stream);
+  A.transfer.alloc(t);
   int64_t nv = 0, nrp = 0, nci = 0;
   for (int l = 0; l <= q; ++l) {
     Layer& L = A.cpl[l];
@@ -191,7 +175,7 @@ void allocate(Matrix& A) {
     nrp += L.rows + 1;
     nci += L.nb;
   }
-  A.cpl_val.alloc_pooled(nv, A.stream);
+  A.cpl_val.alloc(nv);
   A.cpl_rp.alloc(nrp);
   A.cpl_ci.alloc(nci);
   nv = nrp = nci = 0;
@@ -206,7 +190,7 @@ void allocate(Matrix& A) {
   }
   Layer& D = A.dense;
   D.ld = pad2(D.br);
-  A.dense_val.alloc_pooled(size_t(D.nb) * D.block_stride(), A.stream);
+  A.dense_val.alloc(size_t(D.nb) * D.block_stride());
   A.dense_rp.alloc(D.rows + 1);
   A.dense_ci.alloc(D.nb);
   D.val = A.dense_val.p;
@@ -221,9 +205,6 @@ void allocate(Matrix& A) {
   A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
   A.xs.alloc(A.n);
   A.ys.alloc(A.n);
-  // pooled allocations are stream-ordered on A.stream: complete them before
-  // the pools are used from any other stream
-  H2B_CUDA(cudaStreamSynchronize(A.stream));
 }
 
 // Upload the CSR structure of every layer and build the fused work list.
@@ -450,6 +431,7 @@ using namespace h2b;
 namespace h2b {
 h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, int part);
 void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_comm* comm = nullptr);
+void release_workspaces(int device);
 void orthogonalize_matrix(Matrix& A, double* t_out);
 }  // namespace h2b
 
@@ -465,10 +447,8 @@ h2b_status h2b_release_cached_memory(int device) {
     int prev = 0;
     H2B_CUDA(cudaGetDevice(&prev));
     H2B_CUDA(cudaSetDevice(device));
-    cudaMemPool_t pool;
-    H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     H2B_CUDA(cudaDeviceSynchronize());
-    H2B_CUDA(cudaMemPoolTrimTo(pool, 0));
+    release_workspaces(device);
     H2B_CUDA(cudaSetDevice(prev));
   });
 }

@@ -4,7 +4,7 @@
 //   project S <- T S T^T         k_project (one CTA per block row)  :130-169
 //   ||A||_F^2                    k_sumsq                            :453-460
 //   weight tree (R-only QR)      k_weights (streaming TSQR, unpadded stacks)  :184-256
-//   truncate (SVD upsweep)       k_trunc_leaf_svd / _apply, k_trunc_level_svd / _apply  :267-420
+//   truncate (SVD upsweep)       k_trunc_{leaf,level}_pre, k_jacobi64, k_svd_apply, k_trunc_*_apply  :267-420
 //   project with rectangular T   k_project                          :542
 //
 // One 256-thread CTA owns one batch entry; its matrices live in shared memory
@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "cta_linalg.cuh"
@@ -439,41 +440,44 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
   }
 }
 
-// Shared-memory scratch of the truncation SVDs.
+// Truncation SVDs (svd_truncated_batched, batch.hpp:107-140 / linalg.hpp:142-232):
+// left singular vectors U (rows x s), singular values, and the count
+// #{sigma_j >= eps sigma_1} of W (rows x cols), s = min(rows, cols), in three
+// stages over the whole batch:
+//   A  (256 threads)  precondition (Drmac-Veselic):
+//        tall  W = Q1 R1 (Householder), R1^T = Q2 R2  ->  J = R2^T,  U = Q1 [U_J; 0]
+//        wide  W^T = Q1 R1                            ->  J = R1^T,  U = U_J
+//      J (s x s) and Q1's reflectors go to global scratch;
+//   B  (64 threads, k_jacobi64)  one-sided Jacobi on J with lane c owning
+//      column c in registers (no reductions: dot products are lane-local, the
+//      partner column is read from shared memory), sigma = column norms,
+//      stable descending sort, U_J normalised -> the top rows of U;
+//   C  (256 threads, tall only)  U = Q1 [U_J; 0] by compact WY on the FP64
+//      tensor cores (apply_q_wy).
+// Same singular values and subspaces as the reference's Jacobi on W (which
+// takes 10-26 sweeps on these graded spectra; J converges in ~6); columns of U
+// may differ in sign.  The Jacobi rule (|a_pq| <= 16 eps sqrt(a_pp a_qq) or
+// a_pq == 0), 60-sweep cap, sigma = column norms and stable descending sort
+// are the reference's; the pair order is the parallel round-robin ordering.
 struct SvdScratch {
-  double nrm[128];
   double tau[64];
   double tau2[64];
   double red[16];
-  int ord[128];
-  int perm[128];
-  int flag, sel;
 };
 constexpr int kSvdScratch = int((sizeof(SvdScratch) + 15) / 16) * 2;  // in doubles, 16 B aligned
 
-// Left singular vectors (Uout, global, rows x s) and singular values (sig) of
-// W (rows x cols, smem, ld rows; destroyed), s = min(rows, cols); returns
-// #{sigma_j >= eps sigma_1} (0 if sigma_1 = 0) -- svd_truncated_batched,
-// batch.hpp:107-140 / linalg.hpp:142-232.
-//
-// Preconditioned one-sided Jacobi (Drmac-Veselic): instead of rotating W's
-// columns directly (10-26 sweeps on these graded spectra), factor
-//   tall  W P = Q1 R1 (QR with column pivoting), R1^T = Q2 R2, Jacobi on R2^T:
-//         U = Q1 U_X, where U_X = normalised columns of the rotated R2^T;
-//   wide  W^T P = Q1 R1, Jacobi on R1^T: U = P U_X;
-// which converges in a few sweeps.  Same singular values, same subspaces
-// (the reference runs Jacobi on W, or on R^T of an unpivoted QR of W^T when
-// wide); columns of U may differ in sign.  The Jacobi rule, tolerance, sweep
-// cap, sigma = column norms and stable descending sort are the reference's.
-// X: smem, >= s * (s + 1) doubles (and >= cols * rows when wide).
-__device__ int svd_pre(double* W, int rows, int cols, double* X, double* Uout, int ldu, double* sig,
-                       double eps, SvdScratch& sc) {
+// Stage A on W (rows x cols, smem, ld rows; destroyed).  X: smem >= s*s and
+// >= cols*rows.  Writes J (s x s, ld s) and, when tall, the factored Q1 (V:
+// rows x cols, ld rows; tau: cols) to global.
+__device__ void svd_precondition(double* W, int rows, int cols, double* X, double* J, double* V,
+                                 double* tau, SvdScratch& sc) {
   const int s = rows < cols ? rows : cols;
-  if (s == 0) return 0;
-  const int n = s + (s & 1);  // Jacobi columns (zero pad column when odd)
+  if (s == 0) return;
   if (rows >= cols) {
     const int c = cols;
-    cta::qrcp(W, rows, rows, c, sc.tau, sc.perm, sc.nrm, sc.red, &sc.sel);
+    cta::householder(W, rows, rows, c, sc.tau, sc.red);
+    for (int e = threadIdx.x; e < rows * c; e += kThreads) V[e] = W[e];
+    for (int j = threadIdx.x; j < c; j += kThreads) tau[j] = sc.tau[j];
     // X = R1^T (c x c, lower), then QR of it: R2 in the upper triangle
     for (int e = threadIdx.x; e < c * c; e += kThreads) {
       const int j = e / c, i = e - j * c;
@@ -481,21 +485,10 @@ __device__ int svd_pre(double* W, int rows, int cols, double* X, double* Uout, i
     }
     __syncthreads();
     cta::householder(X, c, c, c, sc.tau2, sc.red);
-    // in-place transpose to R2^T (lower), zero pad column
-    for (int e = threadIdx.x; e < c * c; e += kThreads) {
+    for (int e = threadIdx.x; e < c * c; e += kThreads) {  // J = R2^T
       const int j = e / c, i = e - j * c;
-      if (i < j) {
-        X[j + i * c] = X[i + j * c];
-        X[i + j * c] = 0.0;
-      }
+      J[i + j * c] = i >= j ? X[j + i * c] : 0.0;
     }
-    if (n > c)
-      for (int i = threadIdx.x; i < c; i += kThreads) X[i + c * c] = 0.0;
-    __syncthreads();
-    cta::jacobi(X, c, c, n, &sc.flag);
-    // U_X into the top c rows of Uout, zero below, then U = Q1 [U_X; 0]
-    cta::jacobi_finish(X, c, c, n, s, Uout, ldu, sig, sc.nrm, sc.ord);
-    cta::apply_q_wy(W, rows, rows, c, sc.tau, Uout, ldu, s, X);
   } else {
     const int r = rows;
     double* G = X;  // W^T (cols x r)
@@ -504,28 +497,13 @@ __device__ int svd_pre(double* W, int rows, int cols, double* X, double* Uout, i
       G[i + j * cols] = W[j + i * rows];
     }
     __syncthreads();
-    cta::qrcp(G, cols, cols, r, sc.tau, sc.perm, sc.nrm, sc.red, &sc.sel);
-    // J = R1^T (r x n, lower) in W's storage (W is dead)
-    double* J = W;
-    for (int e = threadIdx.x; e < r * n; e += kThreads) {
+    cta::householder(G, cols, cols, r, sc.tau, sc.red);
+    for (int e = threadIdx.x; e < r * r; e += kThreads) {  // J = R1^T
       const int j = e / r, i = e - j * r;
-      J[i + j * r] = (j < r && i >= j) ? G[j + i * cols] : 0.0;
+      J[i + j * r] = i >= j ? G[j + i * cols] : 0.0;
     }
-    __syncthreads();
-    cta::jacobi(J, r, r, n, &sc.flag);
-    cta::jacobi_finish(J, r, r, n, s, X, r, sig, sc.nrm, sc.ord);
-    for (int e = threadIdx.x; e < r * s; e += kThreads) {
-      const int j = e / r, i = e - j * r;
-      Uout[sc.perm[i] + int64_t(j) * ldu] = X[i + j * r];
-    }
-    __syncthreads();
   }
-  int rank = 0;
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < s; ++j)
-      if (sig[0] > 0.0 && sig[j] >= eps * sig[0]) ++rank;
-  }
-  return rank;
+  __syncthreads();
 }
 
 __device__ void check_finite(const double* W, int n, int* bad) {
@@ -533,24 +511,180 @@ __device__ void check_finite(const double* W, int n, int* bad) {
     if (!isfinite(W[e])) *bad = 1;
 }
 
-// Leaves: W = U R^T (m x k), truncated SVD (compression.hpp:285-300).
-__global__ void __launch_bounds__(kThreads) k_trunc_leaf_svd(const double* __restrict__ leaf, int ldm,
-                                                             int m, int k, const double* __restrict__ R,
-                                                             double* __restrict__ Uout,
-                                                             double* __restrict__ sig_out, double eps,
-                                                             int* __restrict__ kmax, int* __restrict__ bad) {
+// Stage A, leaves: W = U R^T (m x k) (compression.hpp:285-300).
+__global__ void __launch_bounds__(kThreads) k_trunc_leaf_pre(const double* __restrict__ leaf, int ldm, int m,
+                                                             int k, const double* __restrict__ R,
+                                                             double* __restrict__ Jout, double* __restrict__ Vout,
+                                                             double* __restrict__ tauout, int* __restrict__ bad) {
   extern __shared__ double sm[];
   const int s = m < k ? m : k;
   SvdScratch& sc = *reinterpret_cast<SvdScratch*>(sm);
-  double* W = sm + kSvdScratch;        // m x (k + 1)
-  double* X = W + m * (k + 1);         // >= s (s + 1), >= k m
+  double* W = sm + kSvdScratch;  // m x k
+  double* X = W + m * k;         // >= s s, >= k m
   const int64_t i = blockIdx.x;
   cta::gemm_tc<false, true, 2>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
   __syncthreads();
   check_finite(W, m * k, bad);
-  double* sg = sig_out + i * s;
-  const int rank = svd_pre(W, m, k, X, Uout + i * int64_t(m) * s, m, sg, eps, sc);
-  if (threadIdx.x == 0) atomicMax(kmax, rank);
+  svd_precondition(W, m, k, X, Jout + i * int64_t(s) * s, Vout + i * int64_t(m) * k, tauout + i * 64, sc);
+}
+
+// Stage A, parent p: Z = [Tt_c E_c] (2kt_c x kp), W = Z R^{l-1,T} (:327-376).
+__global__ void __launch_bounds__(kThreads) k_trunc_level_pre(
+    const double* __restrict__ E, int lde, int kc, int kp, int ktc, const double* __restrict__ Tt,
+    const double* __restrict__ Rp, double* __restrict__ Zout, double* __restrict__ Jout,
+    double* __restrict__ Vout, double* __restrict__ tauout, int* __restrict__ bad) {
+  extern __shared__ double sm[];
+  const int zr = 2 * ktc;
+  const int s = zr < kp ? zr : kp;
+  SvdScratch& sc = *reinterpret_cast<SvdScratch*>(sm);
+  double* W = sm + kSvdScratch;  // zr x kp
+  double* X = W + zr * kp;       // >= s s, >= kp zr
+  const int64_t p = blockIdx.x;
+  const int64_t es = int64_t(lde) * kp;
+  double* Z = Zout + p * int64_t(zr) * kp;  // Z lives in global memory (L2)
+  for (int ci = 0; ci < 2; ++ci) {
+    const int64_t c = 2 * p + ci;
+    cta::gemm_tc<false, false>(Z + ci * ktc, zr, Tt + c * int64_t(ktc) * kc, ktc, E + c * es, lde, ktc, kp, kc);
+  }
+  __syncthreads();
+  cta::gemm_tc<false, true, 2>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
+  __syncthreads();
+  check_finite(W, zr * kp, bad);
+  svd_precondition(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
+}
+
+// Stage B: one-sided Jacobi on J (r x r, r <= 64), one 64-thread CTA per
+// matrix, lane c owns column c in registers.  Per round-robin round every lane
+// publishes its column to shared memory, reads its partner's, forms the three
+// dot products itself (both lanes of a pair get bitwise the same values) and
+// rotates its own column.  Output: U_J (normalised, sorted) into the top r
+// rows of U (ld ldu), sigma (s = r values), atomicMax of the truncation rank.
+__global__ void __launch_bounds__(64) k_jacobi64(const double* __restrict__ Jall, int r,
+                                                 double* __restrict__ Uall, int ldu, int64_t ustride,
+                                                 double* __restrict__ sig_all, double eps,
+                                                 int* __restrict__ kmax) {
+  constexpr int LD = 66;  // even: 16-byte aligned columns (128-bit, conflict-free quarter-warps)
+  __shared__ __align__(16) double cols[64 * LD];
+  __shared__ double nrm2[64];
+  __shared__ double nrm[64];
+  __shared__ int flag;
+  const int c = threadIdx.x;
+  const int n = r + (r & 1);  // zero pad column when odd
+  const double* J = Jall + blockIdx.x * int64_t(r) * r;
+  double g[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) g[i] = (c < r && i < r) ? J[i + c * r] : 0.0;
+  // published copy of every column and its squared norm (the reference
+  // recomputes the norms at every pair visit; so does this kernel, once per
+  // rotated column, and both lanes of a pair read the same published values)
+  auto norm2 = [&]() {
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      t0 = fma(g[i], g[i], t0);
+      t1 = fma(g[i + 1], g[i + 1], t1);
+    }
+    return t0 + t1;
+  };
+  auto publish = [&](double a) {
+    double2* dst = reinterpret_cast<double2*>(cols + c * LD);
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) dst[i / 2] = make_double2(g[i], g[i + 1]);
+    nrm2[c] = a;
+  };
+  double a = norm2();
+  if (c < n) publish(a);
+  if (c == 0) flag = 0;
+  const double tol = 2.220446049250313e-16 * 16.0;
+  const int m1 = n - 1;
+  for (int sweep = 0; sweep < 60 && r > 1; ++sweep) {
+    for (int rd = 0; rd < m1; ++rd) {
+      __syncthreads();  // this round's columns are published
+      bool rot = false;
+      if (c < n) {
+        // round-robin (circle) partner of column c in round rd
+        const int pt = c == m1 ? rd : (c == rd ? m1 : (2 * rd - c + 2 * m1) % m1);
+        const double2* pc = reinterpret_cast<const double2*>(cols + pt * LD);
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          const double2 x = pc[i / 2];
+          d0 = fma(g[i], x.x, d0);
+          d1 = fma(g[i + 1], x.y, d1);
+        }
+        const double d = d0 + d1;
+        asm volatile("" ::: "memory");  // re-read the partner below: 64 registers saved
+        const double b = nrm2[pt];
+        const bool is_p = c < pt;
+        const double ap = is_p ? a : b, aq = is_p ? b : a;
+        // skip rule of linalg.hpp:155-160 (sqrt(a) sqrt(b): no underflow)
+        if (!(fabs(d) <= tol * (sqrt(ap) * sqrt(aq)) || d == 0.0)) {
+          rot = true;
+          flag = 1;
+          const double z = (aq - ap) / (2.0 * d);
+          const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + hypot(1.0, z));
+          const double cs = 1.0 / sqrt(1.0 + t * t);
+          const double sn = cs * t;
+          // new_p = cs u - sn w, new_q = sn u + cs w  (u = column p, w = column q)
+          const double fp = is_p ? -sn : sn;
+#pragma unroll
+          for (int i = 0; i < 64; i += 2) {
+            const double2 x = pc[i / 2];
+            g[i] = fma(cs, g[i], fp * x.x);
+            g[i + 1] = fma(cs, g[i + 1], fp * x.y);
+          }
+          a = norm2();
+        }
+      }
+      __syncthreads();  // everyone has read the partners
+      if (rot) publish(a);
+    }
+    __syncthreads();
+    const int f = flag;
+    __syncthreads();
+    if (c == 0) flag = 0;
+#ifdef H2B_SWEEP_HIST
+    if (c == 0 && (!f || sweep == 59)) atomicAdd(&cta::g_sweep_hist[f ? 60 : sweep], 1);
+#endif
+    if (!f) break;
+  }
+  // sigma = column norms, stable descending order
+  const double sg = sqrt(norm2());
+  nrm[c] = c < n ? sg : -1.0;
+  __syncthreads();
+  int pos = 0;
+  double smax = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double v = nrm[i];
+    pos += (v > sg) || (v == sg && i < c);
+    smax = fmax(smax, v);
+  }
+  const bool keep = smax > 0.0 && c < n && sg >= eps * smax && pos < r;
+  const int rank = __syncthreads_count(keep);
+  if (c < n && pos < r) {
+    sig_all[blockIdx.x * int64_t(r) + pos] = sg;
+    double* U = Uall + blockIdx.x * ustride + int64_t(pos) * ldu;
+    const double inv = sg > 0.0 ? 1.0 / sg : 0.0;
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      if (i < r) U[i] = sg > 0.0 ? g[i] * inv : 0.0;
+  }
+  if (c == 0) atomicMax(kmax, rank);
+}
+
+// Stage C (tall): U = Q1 [U_J; 0] (rows x s) in place in global memory.
+__global__ void __launch_bounds__(kThreads) k_svd_apply(const double* __restrict__ Vall, const double* __restrict__ tauall,
+                                                        int rows, int c, double* __restrict__ Uall) {
+  extern __shared__ double sm[];
+  double* V = sm;            // rows x c
+  double* Zw = V + rows * c; // c x c
+  double* tau = Zw + c * c;  // 64
+  const int64_t i = blockIdx.x;
+  const double* Vg = Vall + i * int64_t(rows) * c;
+  for (int e = threadIdx.x; e < rows * c; e += kThreads) V[e] = Vg[e];
+  for (int j = threadIdx.x; j < c; j += kThreads) tau[j] = tauall[i * 64 + j];
+  __syncthreads();
+  cta::apply_q_wy(V, rows, rows, c, tau, Uall + i * int64_t(rows) * c, rows, c, Zw);
 }
 
 // T^q = Q^T U_old (kt x k), new leaf = Q (m x kt), discarded energy (:309-324).
@@ -575,32 +709,6 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_apply(const double* __r
     for (int j = kt; j < s; ++j) acc += sig[i * s + j] * sig[i * s + j];
     energy[i] = acc;
   }
-}
-
-// Parent p: Z = [Tt_c E_c] (2kt_c x kp), W = Z R^{l-1,T}, SVD (:327-376).
-__global__ void __launch_bounds__(kThreads) k_trunc_level_svd(
-    const double* __restrict__ E, int lde, int kc, int kp, int ktc, const double* __restrict__ Tt,
-    const double* __restrict__ Rp, double* __restrict__ Zout, double* __restrict__ Uout,
-    double* __restrict__ sig_out, double eps, int* __restrict__ kmax, int* __restrict__ bad) {
-  extern __shared__ double sm[];
-  const int zr = 2 * ktc;
-  const int s = zr < kp ? zr : kp;
-  SvdScratch& sc = *reinterpret_cast<SvdScratch*>(sm);
-  double* W = sm + kSvdScratch;          // zr x (kp + 1)
-  double* X = W + zr * (kp + 1);         // >= s (s + 1), >= kp zr
-  const int64_t p = blockIdx.x;
-  const int64_t es = int64_t(lde) * kp;
-  double* Z = Zout + p * int64_t(zr) * kp;  // Z lives in global memory (L2)
-  for (int ci = 0; ci < 2; ++ci) {
-    const int64_t c = 2 * p + ci;
-    cta::gemm_tc<false, false>(Z + ci * ktc, zr, Tt + c * int64_t(ktc) * kc, ktc, E + c * es, lde, ktc, kp, kc);
-  }
-  __syncthreads();
-  cta::gemm_tc<false, true, 2>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
-  __syncthreads();
-  check_finite(W, zr * kp, bad);
-  const int rank = svd_pre(W, zr, kp, X, Uout + p * int64_t(zr) * s, zr, sig_out + p * s, eps, sc);
-  if (threadIdx.x == 0) atomicMax(kmax, rank);
 }
 
 // T^{l-1}_p = Q^T Z (kt_p x kp); new transfers = Q row blocks (:382-415).
@@ -669,39 +777,98 @@ struct Timer {
   }
 };
 
-// Level-concatenated pool of per-node (rows[l] x cols[l]) matrices, ld = rows.
+// Level-concatenated pool of per-node (rows[l] x cols[l]) matrices, ld = rows,
+// carved from the compression workspace.
 struct TreePool {
-  TmpBuf<double> buf;
+  double* p = nullptr;
   std::vector<int64_t> off;
   std::vector<int> rows, cols;
-  void alloc(const Matrix& A, const std::vector<int>& r, const std::vector<int>& c, cudaStream_t s) {
+  static size_t need(const Matrix& A, const std::vector<int>& r, const std::vector<int>& c) {
+    size_t t = 0;
+    for (int l = 0; l <= A.q; ++l) t += size_t(A.nodes(l)) * r[l] * c[l];
+    return std::max<size_t>(1, t);
+  }
+  void alloc(const Matrix& A, const std::vector<int>& r, const std::vector<int>& c, double* base) {
     rows = r;
     cols = c;
     off.assign(A.q + 2, 0);
     for (int l = 0; l <= A.q; ++l) off[l + 1] = off[l] + A.nodes(l) * int64_t(r[l]) * c[l];
-    buf.alloc(std::max<int64_t>(1, off[A.q + 1]), s);
+    p = base;
   }
-  double* at(int l) { return buf.p + off[l]; }
+  double* at(int l) { return p + off[l]; }
 };
 
-// One stream-ordered allocation carved into sub-buffers: the phases size all
-// their scratch up front instead of allocating per level.
+// Bump allocator over one workspace region: the phases size their scratch up
+// front instead of allocating per level.
 struct Arena {
-  TmpBuf<double> buf;
-  size_t off = 0;
-  void reserve(size_t doubles, cudaStream_t s) {
-    buf.alloc(std::max<size_t>(1, doubles), s);
+  double* base = nullptr;
+  size_t cap = 0, off = 0;
+  void reserve(double* b, size_t doubles) {
+    base = b;
+    cap = doubles;
     off = 0;
   }
   template <class T>
   T* take(size_t n) {
     const size_t d = ((n * sizeof(T) + 255) / 256) * 32;  // 256-byte granules, in doubles
-    if (off + d > buf.n) throw Error(H2B_CUDA_ERROR, "scratch arena overflow");
-    T* p = reinterpret_cast<T*>(buf.p + off);
+    if (off + d > cap) throw Error(H2B_CUDA_ERROR, "scratch arena overflow");
+    T* p = reinterpret_cast<T*>(base + off);
     off += d;
     return p;
   }
   static size_t need(size_t n, size_t elem) { return ((n * elem + 255) / 256) * 32; }
+};
+
+// Per-device cache of compression workspaces: plain cudaMalloc, grow-only,
+// reused by the next compress() (mapping tens of GB of fresh device memory,
+// or re-mapping it through a stream-ordered pool, costs 0.1-5 s -- more than
+// the compression itself); h2b_release_cached_memory frees it.  Concurrent
+// compressions (one per partition handle) check out separate buffers.
+struct WsCache {
+  std::mutex mu;
+  std::vector<std::vector<DevBuf<double>>> free;  // per device
+};
+WsCache& ws_cache() {
+  static WsCache c;
+  return c;
+}
+DevBuf<double> ws_checkout(int dev, size_t doubles) {
+  DevBuf<double> b;
+  {
+    std::lock_guard<std::mutex> lk(ws_cache().mu);
+    auto& fr = ws_cache().free;
+    if (int(fr.size()) <= dev) fr.resize(dev + 1);
+    auto& v = fr[dev];
+    if (!v.empty()) {
+      auto it = std::max_element(v.begin(), v.end(), [](const DevBuf<double>& x, const DevBuf<double>& y) {
+        return x.n < y.n;
+      });
+      b = std::move(*it);
+      v.erase(it);
+    }
+  }
+  if (b.n < doubles) {
+    b.release();
+    b.alloc(doubles + doubles / 8);  // headroom for the next, slightly larger matrix
+  }
+  return b;
+}
+void ws_return(int dev, DevBuf<double>&& b) {
+  std::lock_guard<std::mutex> lk(ws_cache().mu);
+  auto& fr = ws_cache().free;
+  if (int(fr.size()) <= dev) fr.resize(dev + 1);
+  fr[dev].push_back(std::move(b));
+}
+struct Workspace {
+  int dev;
+  DevBuf<double> buf;
+  double* trees;  // region A: To, later Tt
+  double* rtree;  // region B: R
+  double* arena;  // region C: per-phase scratch
+  size_t arena_cap;
+  ~Workspace() {
+    if (buf.p) ws_return(dev, std::move(buf));
+  }
 };
 
 // Subtree partition of the compression: 2^s ranks, this one
@@ -731,10 +898,11 @@ struct Part {
 };
 
 // ---------------------------------------------------------------- phases
-void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, const Part& pt) {
+void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, const Part& pt,
+                   double* tree_mem) {
   const int q = A.q, m = A.m, kq = A.rank[q];
   require(m >= kq, "orthogonalize_basis: leaf_dim must be >= leaf rank");
-  T.alloc(A, A.rank, A.rank, s);
+  T.alloc(A, A.rank, A.rank, tree_mem);
   const int64_t nl = A.nodes(q);
   if (kq > 0) {
     const size_t sm = (2 * size_t(m) * kq + size_t(kq) * kq + 64 + 16) * sizeof(double) + 64 * sizeof(int);
@@ -773,21 +941,26 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
 // Project every coupling level with T (rows x cols per node): blocks become
 // T.rows[l] x T.rows[l].  Writes into `out_pool` (may alias the current pool
 // when the shapes agree).
-void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place, const Part& pt) {
+// Project every coupling level with T (rows x cols per node, compression.hpp:
+// 130-169): blocks become T.rows[l] x T.rows[l].  Square T (orthogonalization)
+// projects in place.  Rectangular T (truncation) shrinks every block: the new,
+// compacted pool is written over the old one in block-order chunks staged in
+// the workspace arena -- chunk k's destination ends where chunk k+1's source
+// starts or earlier (every block only shrinks), so nothing unread is clobbered
+// and no second coupling pool is ever allocated.
+void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place, const Part& pt,
+             Arena& ar) {
   const int q = A.q;
   ProjTable P{};
   P.tri = in_place ? 1 : 0;
-  std::vector<ProjRow> rows;
   std::vector<int64_t> new_off(q + 2, 0);
   for (int l = 0; l <= q; ++l) {
     const Layer& L = A.cpl[l];
     const int rn = T.rows[l];
     new_off[l + 1] = new_off[l] + L.nb * int64_t(pad2(rn)) * rn;
   }
-  DevBuf<double> fresh;
-  if (!in_place) fresh.alloc_pooled(std::max<int64_t>(1, new_off[q + 1]), s);
-  double* base = in_place ? A.cpl_val.p : fresh.p;
-  size_t smax = 0;
+  // block rows in pool order (level, row)
+  std::vector<ProjRow> rows;
   for (int l = 0; l <= q; ++l) {
     Layer& L = A.cpl[l];
     const int rn = T.rows[l], ro = T.cols[l];
@@ -796,7 +969,6 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     if (pt.counts(l)) flops += fl.gemm(double(L.nb), rn, ro, ro) + fl.gemm(double(L.nb), rn, rn, ro);
     ProjLevel& d = P.L[l];
     d.S = L.val;
-    d.out = base + new_off[l];
     d.rp = L.rp;
     d.ci = L.ci;
     d.T = T.at(l);
@@ -804,22 +976,47 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     d.rn = rn;
     d.ld_old = L.ld;
     d.ld_new = pad2(rn);
+    d.out = in_place ? L.val : nullptr;
     if (rn == 0) continue;
     for (int64_t r = 0; r < L.rows; ++r)
       if (L.h_rp[r + 1] > L.h_rp[r]) rows.push_back({l, int32_t(r)});
-    smax = size_t(3) * 64 * kPLd * sizeof(double);
   }
-  if (!rows.empty()) {
-    check_smem(smax, "project_coupling");
-    TmpBuf<ProjRow> drows;
-    drows.alloc(rows.size(), s);
-    H2B_CUDA(cudaMemcpyAsync(drows.p, rows.data(), rows.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
-    set_smem(k_project, smax);
-    k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows.p);
-    H2B_CUDA(cudaGetLastError());
-    H2B_CUDA(cudaStreamSynchronize(s));
+  const size_t smax = size_t(3) * 64 * kPLd * sizeof(double);
+  check_smem(smax, "project_coupling");
+  set_smem(k_project, smax);
+  ar.off = 0;
+  ProjRow* drows = ar.take<ProjRow>(std::max<size_t>(1, rows.size()));
+  if (!rows.empty())
+    H2B_CUDA(cudaMemcpyAsync(drows, rows.data(), rows.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
+  if (in_place) {
+    if (!rows.empty()) {
+      k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows);
+      H2B_CUDA(cudaGetLastError());
+    }
+  } else {
+    double* temp = ar.base + ar.off;
+    const int64_t cap = int64_t(ar.cap - ar.off);
+    size_t i = 0;
+    while (i < rows.size()) {
+      // one chunk: consecutive rows of one level whose new blocks fit in temp
+      const int l = rows[i].level;
+      const Layer& L = A.cpl[l];
+      const int64_t bs = int64_t(pad2(T.rows[l])) * T.rows[l];
+      const int64_t b0 = L.h_rp[rows[i].row];
+      size_t j = i;
+      while (j < rows.size() && rows[j].level == l && (L.h_rp[rows[j].row + 1] - b0) * bs <= cap) ++j;
+      require(j > i, "project_coupling: workspace smaller than one block row");
+      const int64_t b1 = L.h_rp[rows[j - 1].row + 1];
+      ProjTable Pc = P;
+      Pc.L[l].out = temp - b0 * bs;  // block b lands at temp + (b - b0) * bs
+      k_project<<<unsigned(j - i), kThreads, smax, s>>>(Pc, drows + i);
+      H2B_CUDA(cudaGetLastError());
+      H2B_CUDA(cudaMemcpyAsync(A.cpl_val.p + new_off[l] + b0 * bs, temp, (b1 - b0) * bs * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
+      i = j;
+    }
   }
-  if (!in_place) A.cpl_val = std::move(fresh);
+  H2B_CUDA(cudaStreamSynchronize(s));
   for (int l = 0; l <= q; ++l) {
     Layer& L = A.cpl[l];
     L.br = L.bc = T.rows[l];
@@ -828,24 +1025,32 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
   }
 }
 
-double sumsq(const double* v, int64_t n, cudaStream_t s) {
+double sumsq(const double* v, int64_t n, cudaStream_t s, double* part) {
   if (n == 0) return 0.0;
   const int blocks = 1024;
-  TmpBuf<double> part;
-  part.alloc(blocks, s);
-  k_sumsq<<<blocks, kThreads, 0, s>>>(v, n, part.p);
+  k_sumsq<<<blocks, kThreads, 0, s>>>(v, n, part);
   H2B_CUDA(cudaGetLastError());
   std::vector<double> h(blocks);
-  H2B_CUDA(cudaMemcpyAsync(h.data(), part.p, blocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaMemcpyAsync(h.data(), part, blocks * sizeof(double), cudaMemcpyDeviceToHost, s));
   H2B_CUDA(cudaStreamSynchronize(s));
   double acc = 0.0;
   for (double v2 : h) acc += v2;
   return acc;
 }
 
-void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, const Part& pt) {
+size_t weights_arena_need(const Matrix& A) {
+  size_t pmax = 1, nord = 1;
+  for (int l = 1; l <= A.q; ++l) {
+    pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
+    nord += A.own_count(l) + 1;
+  }
+  return Arena::need(pmax, sizeof(double)) + Arena::need(nord, sizeof(int32_t));
+}
+
+void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, const Part& pt, double* tree_mem,
+             Arena& ar) {
   const int q = A.q;
-  R.alloc(A, A.rank, A.rank, s);
+  R.alloc(A, A.rank, A.rank, tree_mem);
   H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * A.rank[0] * A.rank[0], s));
   // LPT order of every level (nodes by decreasing stack height) plus one work
   // counter per level, uploaded once
@@ -866,8 +1071,7 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, c
     });
     o[nn] = 0;
   }
-  Arena ar;
-  ar.reserve(Arena::need(pmax, sizeof(double)) + Arena::need(ord.size(), sizeof(int32_t)), s);
+  ar.off = 0;
   double* Pall = ar.take<double>(pmax);
   int32_t* dord_all = ar.take<int32_t>(ord.size());
   H2B_CUDA(cudaMemcpyAsync(dord_all, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
@@ -931,6 +1135,22 @@ double sum_host(const double* d, int64_t n, cudaStream_t s) {
   return acc;
 }
 
+// Stages B (Jacobi) and C (Q1 application, tall) of a batch of nb SVDs of
+// rows x cols matrices whose stage A wrote J, V, tau.
+void svd_finish(const double* J, const double* V, const double* tau, int rows, int cols, double* U,
+                double* sig, double eps, int* kmax, int64_t nb, cudaStream_t s) {
+  const int sl = std::min(rows, cols);
+  k_jacobi64<<<unsigned(nb), 64, 0, s>>>(J, sl, U, rows, int64_t(rows) * sl, sig, eps, kmax);
+  H2B_CUDA(cudaGetLastError());
+  if (rows >= cols) {
+    const size_t sm = (size_t(rows) * cols + size_t(cols) * cols + 64) * sizeof(double);
+    check_smem(sm, "truncate_basis");
+    set_smem(k_svd_apply, sm);
+    k_svd_apply<<<unsigned(nb), kThreads, sm, s>>>(V, tau, rows, cols, U);
+    H2B_CUDA(cudaGetLastError());
+  }
+}
+
 // H2B_TRACE=1: per-level wall-clock trace of the truncation on stderr.
 struct Trace {
   bool on = std::getenv("H2B_TRACE") != nullptr;
@@ -945,8 +1165,39 @@ struct Trace {
 
 // Returns the discarded energy; fills Tt (new x old per node) and replaces
 // the leaf / transfer pools and ranks.
+// Scratch of truncate() (new ranks bounded by the old ones): the new
+// transfers of every level, the per-level SVD batch (reused level to level)
+// and the new leaf pool.
+struct TruncSizes {
+  std::vector<int64_t> ntoff;
+  size_t lvl = 0, total = 0;
+};
+TruncSizes truncate_sizes(const Matrix& A) {
+  TruncSizes z;
+  const int q = A.q, m = A.m;
+  const std::vector<int>& old = A.rank;
+  z.ntoff.assign(q + 2, 0);
+  for (int l = 1; l <= q; ++l) z.ntoff[l + 1] = z.ntoff[l] + A.tr_count(l) * int64_t(pad2(old[l])) * old[l - 1];
+  const int64_t nlo = std::max<int64_t>(1, A.own_count(q));
+  // per batch entry: U (rows x s), sigma, energy, J (s x s), Q1 (rows x cols + 64 tau)
+  auto svd_need = [](size_t nb, int rows, int cols) {
+    const int sl = std::min(rows, cols);
+    return Arena::need(nb * rows * sl, 8) + Arena::need(nb * sl, 8) + Arena::need(nb, 8) +
+           Arena::need(nb * sl * sl, 8) + Arena::need(nb * rows * cols, 8) + Arena::need(nb * 64, 8);
+  };
+  z.lvl = svd_need(size_t(nlo), m, old[q]);
+  for (int l = q; l >= 1; --l) {
+    const int64_t np = std::max<int64_t>(1, A.own_count(l - 1));
+    const int zr = 2 * old[l], kp = old[l - 1];
+    z.lvl = std::max(z.lvl, Arena::need(size_t(np) * zr * kp, 8) + svd_need(size_t(np), zr, kp));
+  }
+  z.total = Arena::need(size_t(std::max<int64_t>(1, z.ntoff[q + 1])), 8) + Arena::need(2, 4) +
+            Arena::need(size_t(nlo) * pad2(m) * old[q], 8) + z.lvl;
+  return z;
+}
+
 double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s, Flops& fl,
-                double& flops, const Part& pt) {
+                double& flops, const Part& pt, double* tree_mem, Arena& ar) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   Trace tr;
   const int q = A.q, m = A.m;
@@ -957,25 +1208,16 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   // ---- all scratch up front (new ranks are bounded by the old ones) ----
   // Tt (new x old per node): level offsets sized for the old ranks, filled
   // in place; the new transfers: one region per level, compacted at the end.
-  Tt.alloc(A, old, old, s);
-  std::vector<int64_t> ntoff(q + 2, 0);
-  for (int l = 1; l <= q; ++l) ntoff[l + 1] = ntoff[l] + A.tr_count(l) * int64_t(pad2(old[l])) * old[l - 1];
+  Tt.alloc(A, old, old, tree_mem);
+  const TruncSizes sz = truncate_sizes(A);
+  const std::vector<int64_t>& ntoff = sz.ntoff;
   const int sl_leaf = std::min(m, old[q]);
   const int64_t nlo = std::max<int64_t>(1, A.own_count(q)), l0 = A.own_begin(q);  // owned leaves
-  size_t lvl = Arena::need(size_t(nlo) * m * sl_leaf, 8) + Arena::need(size_t(nlo) * sl_leaf, 8) +
-               Arena::need(size_t(nlo), 8);
-  for (int l = q; l >= 1; --l) {
-    const int64_t np = A.nodes(l - 1);
-    const int zr = 2 * old[l], kp = old[l - 1], sl = std::min(zr, kp);
-    lvl = std::max(lvl, Arena::need(size_t(np) * zr * kp, 8) + Arena::need(size_t(np) * zr * sl, 8) +
-                            Arena::need(size_t(np) * sl, 8) + Arena::need(size_t(np), 8));
-  }
-  Arena ar;
-  ar.reserve(lvl + Arena::need(size_t(std::max<int64_t>(1, ntoff[q + 1])), 8) + Arena::need(2, 4), s);
+  ar.off = 0;
   double* newtr = ar.take<double>(std::max<int64_t>(1, ntoff[q + 1]));
   int* dk = ar.take<int>(2);  // [0] = kmax, [1] = non-finite flag
+  double* newleaf = ar.take<double>(size_t(nlo) * pad2(m) * old[q]);
   const size_t lvl_base = ar.off;
-  DevBuf<double> newleaf;
   {
     const int kq = old[q];
     const int sl = sl_leaf;
@@ -985,16 +1227,18 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     double* Uq = ar.take<double>(size_t(nlo) * m * sl);
     double* sg = ar.take<double>(size_t(nlo) * sl);
     double* en = ar.take<double>(size_t(nlo));
+    double* Js = ar.take<double>(size_t(nlo) * sl * sl);
+    double* Vs = ar.take<double>(size_t(nlo) * m * kq);
+    double* ts = ar.take<double>(size_t(nlo) * 64);
     H2B_CUDA(cudaMemsetAsync(dk, 0, 2 * sizeof(int), s));
     if (sl > 0 && no > 0) {
-      const size_t sm = (kSvdScratch + size_t(m) * (kq + 1) + size_t(std::max(sl * (sl + 1), kq * m))) *
-                        sizeof(double);
+      const size_t sm = (kSvdScratch + size_t(m) * kq + size_t(std::max(sl * sl, kq * m))) * sizeof(double);
       check_smem(sm, "truncate_basis");
-      set_smem(k_trunc_leaf_svd, sm);
-      k_trunc_leaf_svd<<<unsigned(no), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq,
-                                                          R.at(q) + l0 * int64_t(kq) * kq, Uq, sg, eps, dk,
-                                                          dk + 1);
+      set_smem(k_trunc_leaf_pre, sm);
+      k_trunc_leaf_pre<<<unsigned(no), kThreads, sm, s>>>(A.leaf.p, A.ldm, m, kq, R.at(q) + l0 * int64_t(kq) * kq,
+                                                          Js, Vs, ts, dk + 1);
       H2B_CUDA(cudaGetLastError());
+      svd_finish(Js, Vs, ts, m, kq, Uq, sg, eps, dk, no, s);
     }
     tr.at(s, "leaf svd", q);
     int flags[2] = {0, 0};
@@ -1006,10 +1250,9 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     nr[q] = kt;
     flops += fl.gemm(double(nl), kt, kq, m);
     const int ldn = pad2(m);
-    newleaf.alloc_pooled(std::max<int64_t>(1, no * ldn * kt), s);
     if (no > 0) {
       k_trunc_leaf_apply<<<unsigned(no), kThreads, 0, s>>>(A.leaf.p, A.ldm, m, kq, sl, kt, Uq, sg,
-                                                           Tt.at(q) + l0 * int64_t(kt) * kq, newleaf.p, ldn, en);
+                                                           Tt.at(q) + l0 * int64_t(kt) * kq, newleaf, ldn, en);
       H2B_CUDA(cudaGetLastError());
     }
     lev_e[q] = sum_host(en, no, s);
@@ -1030,17 +1273,20 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     double* U = ar.take<double>(size_t(npo) * zr * sl);
     double* sg = ar.take<double>(size_t(npo) * sl);
     double* en = ar.take<double>(size_t(npo));
+    double* Js = ar.take<double>(size_t(npo) * sl * sl);
+    double* Vs = ar.take<double>(size_t(npo) * zr * kp);
+    double* ts = ar.take<double>(size_t(npo) * 64);
     H2B_CUDA(cudaMemsetAsync(dk, 0, 2 * sizeof(int), s));
     const int64_t es = A.tr_stride(l);
     if (sl > 0 && npo > 0) {
-      const size_t sm = (kSvdScratch + size_t(zr) * (kp + 1) + size_t(std::max(sl * (sl + 1), kp * zr))) *
-                        sizeof(double);
+      const size_t sm = (kSvdScratch + size_t(zr) * kp + size_t(std::max(sl * sl, kp * zr))) * sizeof(double);
       check_smem(sm, "truncate_basis");
-      set_smem(k_trunc_level_svd, sm);
-      k_trunc_level_svd<<<unsigned(npo), kThreads, sm, s>>>(
+      set_smem(k_trunc_level_pre, sm);
+      k_trunc_level_pre<<<unsigned(npo), kThreads, sm, s>>>(
           A.transfer.p + A.tr_off[l] + (2 * p0 - A.tr_begin(l)) * es, A.ld(l), kc, kp, ktc,
-          Tt.at(l) + 2 * p0 * int64_t(ktc) * kc, R.at(l - 1) + p0 * int64_t(kp) * kp, Z, U, sg, eps, dk, dk + 1);
+          Tt.at(l) + 2 * p0 * int64_t(ktc) * kc, R.at(l - 1) + p0 * int64_t(kp) * kp, Z, Js, Vs, ts, dk + 1);
       H2B_CUDA(cudaGetLastError());
+      svd_finish(Js, Vs, ts, zr, kp, U, sg, eps, dk, npo, s);
     }
     tr.at(s, "level svd", l);
     int flags[2] = {0, 0};
@@ -1075,17 +1321,17 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     t += A.tr_count(l) * A.tr_stride(l);
   }
   toff[q + 1] = t;
-  DevBuf<double> trpool;
-  trpool.alloc_pooled(std::max<int64_t>(1, t), s);
+  // the new (smaller) pools overwrite the old allocations
+  require(size_t(t) <= std::max<size_t>(A.transfer.n, 1), "truncate: transfer pool grew");
   for (int l = 1; l <= q; ++l) {
-    const int64_t sz = A.tr_count(l) * A.tr_stride(l);
-    if (sz) H2B_CUDA(cudaMemcpyAsync(trpool.p + toff[l], newtr + ntoff[l], sz * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, s));
+    const int64_t n = A.tr_count(l) * A.tr_stride(l);
+    if (n) H2B_CUDA(cudaMemcpyAsync(A.transfer.p + toff[l], newtr + ntoff[l], n * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
   }
+  const int64_t nleaf = A.own_count(q) * int64_t(pad2(m)) * nr[q];
+  if (nleaf) H2B_CUDA(cudaMemcpyAsync(A.leaf.p, newleaf, nleaf * sizeof(double), cudaMemcpyDeviceToDevice, s));
   H2B_CUDA(cudaStreamSynchronize(s));
-  A.transfer = std::move(trpool);
   A.tr_off = toff;
-  A.leaf = std::move(newleaf);
   double energy = 0.0;
   for (double e : lev_e) energy += e;
   return energy;
@@ -1116,6 +1362,13 @@ struct DeviceGuard {
 
 }  // namespace
 
+// Free the cached compression workspaces of a device (h2b_release_cached_memory).
+void release_workspaces(int device) {
+  std::lock_guard<std::mutex> lk(ws_cache().mu);
+  auto& fr = ws_cache().free;
+  if (device >= 0 && device < int(fr.size())) fr[device].clear();
+}
+
 // memory_footprint (h2_matrix.hpp:90-102) of the part of the matrix this
 // rank accounts for: its own blocks, replicated top levels on rank 0 only
 uint64_t counted_footprint(const Matrix& A, const Part& pt) {
@@ -1131,23 +1384,23 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   DeviceGuard g(A.device);
   cudaStream_t s = A.stream;
-  // scratch and the re-laid-out pools come from the device's default
-  // stream-ordered pool, which keeps freed memory cached (like a caching
-  // allocator) so repeated compressions do not re-map pages; h2b_trim_pool /
-  // a failing cudaMalloc hand it back
-  cudaMemPool_t pool;
-  H2B_CUDA(cudaDeviceGetDefaultMemPool(&pool, A.device));
-  uint64_t keep = ~uint64_t(0);
-  H2B_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  if (std::getenv("H2B_TRACE")) {
-    uint64_t res = 0, used = 0;
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    fprintf(stderr, "  [trace] compress start: pool reserved %.2f GB used %.2f GB, device free %.2f GB\n",
-            res / 1e9, used / 1e9, fr / 1e9);
-  }
+  // One workspace for the whole call (cached per device, see WsCache):
+  // region A holds the projection trees (To, then Tt), region B the weight
+  // tree R, region C the phase scratch (weights, truncation, the chunked
+  // compaction of the coupling pool).
+  const size_t tree_need = TreePool::need(A, A.rank, A.rank);
+  const size_t arena_need = std::max({weights_arena_need(A), truncate_sizes(A).total, size_t(1) << 25});
+  Workspace ws{A.device};
+  ws.buf = ws_checkout(A.device, 2 * tree_need + arena_need);
+  ws.trees = ws.buf.p;
+  ws.rtree = ws.buf.p + tree_need;
+  ws.arena = ws.buf.p + 2 * tree_need;
+  ws.arena_cap = ws.buf.n - 2 * tree_need;  // all the rest (projection chunks)
+  Arena ar;
+  ar.reserve(ws.arena, ws.arena_cap);
+  if (std::getenv("H2B_TRACE"))
+    fprintf(stderr, "  [trace] compress workspace %.2f GB (arena %.2f GB)\n", ws.buf.n * 8e-9,
+            ws.arena_cap * 8e-9);
   Part pt;
   pt.comm = comm;
   pt.s = comm ? A.part_s : 0;
@@ -1169,37 +1422,35 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   TreePool To, R, Tt;
   {
     Timer t(s);
-    orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt);
+    orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt, ws.trees);
     r.time_orthogonalize_ms = t.stop();
   }
   {
     Timer t(s);
-    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true, pt);
+    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true, pt, ar);
     r.time_project_orth_ms = t.stop();
   }
-  To.buf.release();
   double n2 = 0.0;
   for (int l = 0; l <= A.q; ++l)
-    if (pt.counts(l)) n2 += sumsq(A.cpl[l].val, A.cpl[l].nb * A.cpl[l].block_stride(), s);
-  n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s);
+    if (pt.counts(l)) n2 += sumsq(A.cpl[l].val, A.cpl[l].nb * A.cpl[l].block_stride(), s, ws.arena);
+  n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s, ws.arena);
   pt.sum_f64(&n2, 1);
   r.frobenius_norm = std::sqrt(n2);
   {
     Timer t(s);
-    weights(A, R, s, fl, r.flops_weights, pt);
+    weights(A, R, s, fl, r.flops_weights, pt, ws.rtree, ar);
     r.time_weights_ms = t.stop();
   }
   for (int l = 0; l <= A.q; ++l) A.cpl[l].max_row = saved_max[l];
   double energy = 0.0;
   {
     Timer t(s);
-    energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate, pt);
+    energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate, pt, ws.trees, ar);
     r.time_truncate_ms = t.stop();
   }
-  R.buf.release();
   {
     Timer t(s);
-    project(A, Tt, s, fl, r.flops_project_trunc, /*in_place=*/false, pt);
+    project(A, Tt, s, fl, r.flops_project_trunc, /*in_place=*/false, pt, ar);
     r.time_project_trunc_ms = t.stop();
   }
   relayout(A);
@@ -1214,6 +1465,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   r.flops_project_trunc = g5[4];
   r.frobenius_error = r.frobenius_norm > 0 ? std::sqrt(energy) / r.frobenius_norm : 0.0;
   if (A.part_s > 0) A.global_footprint = r.bytes_after;
+
   if (rep) *rep = r;
 #ifdef H2B_SWEEP_HIST
   int hist[64];
@@ -1233,9 +1485,11 @@ void orthogonalize_matrix(Matrix& A, double* t_out) {
   Flops fl;
   double f = 0;
   TreePool T;
-  orthogonalize(A, T, s, fl, f, Part{});
+  Workspace ws{A.device};
+  ws.buf = ws_checkout(A.device, TreePool::need(A, A.rank, A.rank));
+  orthogonalize(A, T, s, fl, f, Part{}, ws.buf.p);
   if (t_out && T.off[A.q + 1])
-    H2B_CUDA(cudaMemcpyAsync(t_out, T.buf.p, T.off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaMemcpyAsync(t_out, T.p, T.off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToHost, s));
   H2B_CUDA(cudaStreamSynchronize(s));
 }
 

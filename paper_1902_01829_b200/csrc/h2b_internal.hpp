@@ -17,8 +17,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdio>
-#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -54,37 +52,15 @@ inline int pad2(int r) { return r + (r & 1); }
 constexpr int kMaxDim = 64;
 constexpr int kMaxLevels = 31;
 
-// cudaMalloc; on failure hand the default pool's cached (freed) memory back
-// to the device and retry once.
-inline cudaError_t malloc_retry(void** p, size_t bytes) {
-  cudaError_t e = cudaMalloc(p, bytes);
-  if (e == cudaErrorMemoryAllocation) {
-    cudaGetLastError();
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      if (std::getenv("H2B_TRACE")) fprintf(stderr, "  [trace] cudaMalloc(%zu) failed: trimming the pool\n", bytes);
-      cudaDeviceSynchronize();
-      cudaMemPoolTrimTo(pool, 0);
-      e = cudaMalloc(p, bytes);
-    }
-  }
-  return e;
-}
-
-// Device buffer.  alloc(): cudaMalloc.  alloc_pooled(): stream-ordered from
-// the device's default pool (recycled memory, no device-wide sync); freed
-// with cudaFreeAsync on the same stream, which must outlive the buffer.
+// Device buffer (cudaMalloc / cudaFree).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
-  cudaStream_t ps = nullptr;
-  bool pooled = false;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), ps(o.ps), pooled(o.pooled) {
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
     o.p = nullptr;
     o.n = 0;
   }
@@ -93,8 +69,6 @@ struct DevBuf {
       release();
       p = o.p;
       n = o.n;
-      ps = o.ps;
-      pooled = o.pooled;
       o.p = nullptr;
       o.n = 0;
     }
@@ -104,59 +78,18 @@ struct DevBuf {
   void alloc(size_t cnt) {
     release();
     if (cnt == 0) return;
-    H2B_CUDA(malloc_retry(reinterpret_cast<void**>(&p), cnt * sizeof(T)));
+    H2B_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), cnt * sizeof(T)));
     n = cnt;
-    pooled = false;
-  }
-  void alloc_pooled(size_t cnt, cudaStream_t s) {
-    release();
-    if (cnt == 0) return;
-    H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), s));
-    n = cnt;
-    ps = s;
-    pooled = true;
   }
   void zero(cudaStream_t s) {
     if (n) H2B_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
   void release() {
-    if (p) {
-      if (pooled)
-        cudaFreeAsync(p, ps);
-      else
-        cudaFree(p);
-    }
+    if (p) cudaFree(p);
     p = nullptr;
     n = 0;
   }
   size_t bytes() const { return n * sizeof(T); }
-};
-
-// Stream-ordered scratch (cudaMallocAsync from the device's default pool):
-// compression temporaries are recycled by the pool instead of going through
-// cudaMalloc/cudaFree (each a device-wide synchronisation plus page mapping).
-template <class T>
-struct TmpBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  cudaStream_t s = nullptr;
-  TmpBuf() = default;
-  TmpBuf(const TmpBuf&) = delete;
-  TmpBuf& operator=(const TmpBuf&) = delete;
-  TmpBuf(TmpBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
-  ~TmpBuf() { release(); }
-  void alloc(size_t cnt, cudaStream_t st) {
-    release();
-    s = st;
-    if (cnt == 0) return;
-    H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), s));
-    n = cnt;
-  }
-  void release() {
-    if (p) cudaFreeAsync(p, s);
-    p = nullptr;
-    n = 0;
-  }
 };
 
 // One uniform-block BSR layer (a coupling level or the dense layer),
