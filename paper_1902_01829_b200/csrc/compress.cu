@@ -33,6 +33,8 @@ namespace {
 
 using cta::kThreads;
 
+constexpr int kXb = 2 * (4 * 32 + 8);  // cta::householder scratch (doubles)
+
 // ------------------------------------------------------------------ kernels
 __global__ void __launch_bounds__(kThreads) k_orth_leaf(double* __restrict__ leaf, int ldm, int m,
                                                         int k, double* __restrict__ T) {
@@ -41,13 +43,13 @@ __global__ void __launch_bounds__(kThreads) k_orth_leaf(double* __restrict__ lea
   double* Q = A + m * k;          // m x k, ld m
   double* Zw = Q + m * k;         // k x k
   double* tau = Zw + k * k;       // 64
-  double* red = tau + 64;         // 16
-  int* flip = reinterpret_cast<int*>(red + 16);
+  double* xb = tau + 64;          // householder publish slots
+  int* flip = reinterpret_cast<int*>(xb + kXb);
   const int64_t i = blockIdx.x;
   double* U = leaf + i * int64_t(ldm) * k;
   cta::copy_block(A, m, U, ldm, m, k);
   __syncthreads();
-  cta::householder(A, m, m, k, tau, red);
+  cta::householder_regs<16>(A, m, m, k, tau, xb);  // m <= 64
   cta::extract_r(A, m, k, T + i * int64_t(k) * k, k, flip);
   for (int e = threadIdx.x; e < k * k; e += kThreads) {
     const int j = e / k, r = e - j * k;
@@ -71,8 +73,8 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
   double* Q = Z + zr * kp;           // zr x kp
   double* Zw = Q + zr * kp;          // kp x kp
   double* tau = Zw + kp * kp;
-  double* red = tau + 64;
-  int* flip = reinterpret_cast<int*>(red + 16);
+  double* xb = tau + 64;             // householder publish slots
+  int* flip = reinterpret_cast<int*>(xb + kXb);
   const int64_t p = blockIdx.x;
   const int64_t fs = int64_t(ldf) * kp;
   for (int ci = 0; ci < 2; ++ci) {
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
     cta::gemm_tc<false, false, 1>(Z + ci * kc, zr, Tl + c * int64_t(kc) * kc, kc, F + c * fs, ldf, kc, kp, kc);
   }
   __syncthreads();
-  cta::householder(Z, zr, zr, kp, tau, red);
+  cta::householder(Z, zr, zr, kp, tau, xb);
   cta::extract_r(Z, zr, kp, Tp + p * int64_t(kp) * kp, kp, flip);
   for (int e = threadIdx.x; e < kp * kp; e += kThreads) {
     const int j = e / kp, r = e - j * kp;
@@ -113,7 +115,8 @@ struct ProjLevel {
 };
 struct ProjTable {
   ProjLevel L[kMaxLevels + 1];
-  int tri;  // T upper triangular (orthogonalization's R factors)
+  int tri;          // T upper triangular (orthogonalization's R factors)
+  double* rowsum;   // per block row: sum of squares of the projected blocks (or null)
 };
 
 // S_b <- T_row S_b T_col^T for every block of one block row (compression.hpp:160-168),
@@ -127,7 +130,7 @@ struct ProjTable {
 constexpr int kPLd = 68;  // smem leading dimension (== 4 mod 16: conflict-free fragments)
 template <bool TRI>
 __device__ __forceinline__ void project_block(const double* Tr, const double* Sb, const double* Tc, double* out,
-                                              int ld_new, int ro, int rn) {
+                                              int ld_new, int ro, int rn, double& sumsq) {
   const int w = cta::warp(), t = cta::lane();
   const int fr = t >> 2, fk = t & 3;
   const int i0 = 8 * w;
@@ -182,7 +185,10 @@ __device__ __forceinline__ void project_block(const double* Tr, const double* Sb
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int j = 8 * y + 2 * fk + v;
-        if (j < rn) out[i + int64_t(j) * ld_new] = o[y][v];
+        if (j < rn) {
+          out[i + int64_t(j) * ld_new] = o[y][v];
+          sumsq = fma(o[y][v], o[y][v], sumsq);
+        }
       }
   }
   if (ld_new > rn && w == 0)
@@ -220,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   double* Tc = Sb + 64 * kPLd;    // rn x ro
   stage64(Tr, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
   const int b0 = L.rp[pr.row], b1 = L.rp[pr.row + 1];
+  double ss = 0.0;
   for (int b = b0; b < b1; ++b) {
     __syncthreads();  // previous block done with Sb / Tc
     stage64(Sb, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
@@ -229,9 +236,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
     __syncthreads();
     double* out = L.out + int64_t(b) * L.ld_new * rn;
     if (P.tri)
-      project_block<true>(Tr, Sb, Tc, out, L.ld_new, ro, rn);
+      project_block<true>(Tr, Sb, Tc, out, L.ld_new, ro, rn, ss);
     else
-      project_block<false>(Tr, Sb, Tc, out, L.ld_new, ro, rn);
+      project_block<false>(Tr, Sb, Tc, out, L.ld_new, ro, rn, ss);
+  }
+  // ||S||_F^2 of the projected row, fused (compression.hpp:487, frob_norm_sq)
+  if (P.rowsum) {
+    double* red = sm;  // Tr is dead
+    __syncthreads();
+    ss = cta::cta_sum(ss, red);
+    if (threadIdx.x == 0) P.rowsum[blockIdx.x] = ss;
   }
 }
 
@@ -462,20 +476,21 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
 struct SvdScratch {
   double tau[64];
   double tau2[64];
-  double red[16];
+  double xb[2 * (4 * 32 + 8)];  // householder publish slots
 };
 constexpr int kSvdScratch = int((sizeof(SvdScratch) + 15) / 16) * 2;  // in doubles, 16 B aligned
 
 // Stage A on W (rows x cols, smem, ld rows; destroyed).  X: smem >= s*s and
 // >= cols*rows.  Writes J (s x s, ld s) and, when tall, the factored Q1 (V:
 // rows x cols, ld rows; tau: cols) to global.
+template <int RQW>  // register rows per thread of W's QR (rows <= 4 RQW)
 __device__ void svd_precondition(double* W, int rows, int cols, double* X, double* J, double* V,
                                  double* tau, SvdScratch& sc) {
   const int s = rows < cols ? rows : cols;
   if (s == 0) return;
   if (rows >= cols) {
     const int c = cols;
-    cta::householder(W, rows, rows, c, sc.tau, sc.red);
+    cta::householder_regs<RQW>(W, rows, rows, c, sc.tau, sc.xb);
     for (int e = threadIdx.x; e < rows * c; e += kThreads) V[e] = W[e];
     for (int j = threadIdx.x; j < c; j += kThreads) tau[j] = sc.tau[j];
     // X = R1^T (c x c, lower), then QR of it: R2 in the upper triangle
@@ -484,7 +499,7 @@ __device__ void svd_precondition(double* W, int rows, int cols, double* X, doubl
       X[i + j * c] = i >= j ? W[j + i * rows] : 0.0;
     }
     __syncthreads();
-    cta::householder(X, c, c, c, sc.tau2, sc.red);
+    cta::householder_regs<16>(X, c, c, c, sc.tau2, sc.xb);
     for (int e = threadIdx.x; e < c * c; e += kThreads) {  // J = R2^T
       const int j = e / c, i = e - j * c;
       J[i + j * c] = i >= j ? X[j + i * c] : 0.0;
@@ -497,7 +512,7 @@ __device__ void svd_precondition(double* W, int rows, int cols, double* X, doubl
       G[i + j * cols] = W[j + i * rows];
     }
     __syncthreads();
-    cta::householder(G, cols, cols, r, sc.tau, sc.red);
+    cta::householder_regs<16>(G, cols, cols, r, sc.tau, sc.xb);  // cols <= 64 rows
     for (int e = threadIdx.x; e < r * r; e += kThreads) {  // J = R1^T
       const int j = e / r, i = e - j * r;
       J[i + j * r] = i >= j ? G[j + i * cols] : 0.0;
@@ -525,7 +540,7 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_pre(const double* __res
   cta::gemm_tc<false, true, 2>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
   __syncthreads();
   check_finite(W, m * k, bad);
-  svd_precondition(W, m, k, X, Jout + i * int64_t(s) * s, Vout + i * int64_t(m) * k, tauout + i * 64, sc);
+  svd_precondition<16>(W, m, k, X, Jout + i * int64_t(s) * s, Vout + i * int64_t(m) * k, tauout + i * 64, sc);
 }
 
 // Stage A, parent p: Z = [Tt_c E_c] (2kt_c x kp), W = Z R^{l-1,T} (:327-376).
@@ -550,7 +565,10 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_pre(
   cta::gemm_tc<false, true, 2>(W, zr, Z, zr, Rp + p * int64_t(kp) * kp, kp, zr, kp, kp);
   __syncthreads();
   check_finite(W, zr * kp, bad);
-  svd_precondition(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
+  if (zr <= 64)
+    svd_precondition<16>(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
+  else
+    svd_precondition<32>(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
 }
 
 // Stage B: one-sided Jacobi on J (r x r, r <= 64), one 64-thread CTA per
@@ -905,7 +923,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
   T.alloc(A, A.rank, A.rank, tree_mem);
   const int64_t nl = A.nodes(q);
   if (kq > 0) {
-    const size_t sm = (2 * size_t(m) * kq + size_t(kq) * kq + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    const size_t sm = (2 * size_t(m) * kq + size_t(kq) * kq + 64 + kXb) * sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "orthogonalize");
     set_smem(k_orth_leaf, sm);
     if (A.own_count(q) > 0)
@@ -920,7 +938,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
     flops += fl.gemm(double(A.nodes(l)), kc, kp, kc) + fl.qr(double(np), 2 * kc, kp);
     require(2 * kc >= kp, "qr_batched: requires rows >= cols");
     if (kp == 0) return;
-    const size_t sm = (2 * size_t(2 * kc) * kp + size_t(kp) * kp + 64 + 16) * sizeof(double) + 64 * sizeof(int);
+    const size_t sm = (2 * size_t(2 * kc) * kp + size_t(kp) * kp + 64 + kXb) * sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "orthogonalize");
     set_smem(k_orth_level, sm);
     // parents [p0, p1) at level l-1; children 2p0.. in the (local) transfer pool
@@ -949,7 +967,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
 // starts or earlier (every block only shrinks), so nothing unread is clobbered
 // and no second coupling pool is ever allocated.
 void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place, const Part& pt,
-             Arena& ar) {
+             Arena& ar, double* frob2 = nullptr) {
   const int q = A.q;
   ProjTable P{};
   P.tri = in_place ? 1 : 0;
@@ -989,9 +1007,21 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
   if (!rows.empty())
     H2B_CUDA(cudaMemcpyAsync(drows, rows.data(), rows.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
   if (in_place) {
+    double* rsum = ar.take<double>(std::max<size_t>(1, rows.size()));
+    P.rowsum = frob2 ? rsum : nullptr;
     if (!rows.empty()) {
       k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows);
       H2B_CUDA(cudaGetLastError());
+    }
+    if (frob2) {  // sum of the counted rows (replicated top levels: rank 0 only)
+      std::vector<double> h(rows.size());
+      if (!rows.empty())
+        H2B_CUDA(cudaMemcpyAsync(h.data(), rsum, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+      H2B_CUDA(cudaStreamSynchronize(s));
+      double acc = 0.0;
+      for (size_t i = 0; i < rows.size(); ++i)
+        if (pt.counts(rows[i].level)) acc += h[i];
+      *frob2 = acc;
     }
   } else {
     double* temp = ar.base + ar.off;
@@ -1420,6 +1450,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   double sums[3] = {double(counted_footprint(A, pt)), 0.0, 0.0};
 
   TreePool To, R, Tt;
+  double n2 = 0.0;  // ||A||_F^2 after the orthogonal projection (compression.hpp:487)
   {
     Timer t(s);
     orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt, ws.trees);
@@ -1427,12 +1458,9 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   }
   {
     Timer t(s);
-    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true, pt, ar);
+    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true, pt, ar, &n2);
     r.time_project_orth_ms = t.stop();
   }
-  double n2 = 0.0;
-  for (int l = 0; l <= A.q; ++l)
-    if (pt.counts(l)) n2 += sumsq(A.cpl[l].val, A.cpl[l].nb * A.cpl[l].block_stride(), s, ws.arena);
   n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s, ws.arena);
   pt.sum_f64(&n2, 1);
   r.frobenius_norm = std::sqrt(n2);

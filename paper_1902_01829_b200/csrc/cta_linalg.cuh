@@ -192,41 +192,96 @@ __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const doub
 }
 
 // In-place Householder factorisation (linalg.hpp:48-75): reflectors below the
-// diagonal, R on and above it; tau[cols] in smem; red: >= 9 doubles scratch.
-__device__ void householder(double* A, int lda, int rows, int cols, double* tau, double* red) {
-  for (int j = 0; j < cols; ++j) {
-    double* v = A + j * lda;
-    double part = 0.0;
-    for (int i = j + threadIdx.x; i < rows; i += kThreads) part += v[i] * v[i];
-    const double nx = sqrt(cta_sum(part, red));
-    if (nx == 0.0) {
-      if (threadIdx.x == 0) tau[j] = 0.0;
+// diagonal, R on and above it; tau[cols] in smem.  Register-resident: thread
+// (c = tid / 4, quarter = tid % 4) of the 256-thread CTA holds rows
+// [quarter RQ, (quarter + 1) RQ) of column c (cols <= 64, rows <= 4 RQ).  For
+// reflector j the owner column publishes its RAW entries below the diagonal
+// (and alpha = A[j,j], the squared norm partials) to shared memory; every
+// column then forms the Householder scalars itself -- sqrt and one division,
+// in parallel with its dot product (2 quad shuffles) -- and updates its own
+// registers.  One barrier per reflector (double-buffered publish slot).
+// Same arithmetic as the reference: beta = -sign(alpha) ||x||,
+// tau = (beta - alpha) / beta, v = x / (alpha - beta), zero column -> tau = 0.
+// xb: smem scratch, >= 2 * (4 RQ + 8) doubles.
+template <int RQ>
+__device__ void householder_regs(double* A, int lda, int rows, int cols, double* tau, double* xb) {
+  constexpr int XS = 4 * RQ + 8;
+  const int c = threadIdx.x >> 2, qd = threadIdx.x & 3;
+  const int r0 = qd * RQ;
+  const unsigned qmask = 0xfu << (lane() & 28);
+  const bool live = c < cols;
+  double col[RQ];
+#pragma unroll
+  for (int i = 0; i < RQ; ++i) col[i] = (live && r0 + i < rows) ? A[r0 + i + c * lda] : 0.0;
+  const int steps = rows < cols ? rows : cols;
+  const int nb = (steps + RQ - 1) / RQ;
+  for (int jb = 0; jb < nb; ++jb) {
+#pragma unroll
+    for (int jj = 0; jj < RQ; ++jj) {
+      const int j = jb * RQ + jj;
+      if (j >= steps) break;  // uniform
+      double* x = xb + (j & 1) * XS;
+      if (c == j) {  // owner: publish raw x (rows > j), alpha, norm^2 partial
+        double q2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < RQ; ++i) {
+          const double v = (r0 + i > j) ? col[i] : 0.0;
+          x[r0 + i] = v;
+          q2 = fma(v, v, q2);
+        }
+        x[4 * RQ + qd] = q2;
+        if (qd == jb) x[4 * RQ + 4] = col[jj];
+      }
       __syncthreads();
-      continue;
+      const double al = x[4 * RQ + 4];
+      const double nx = sqrt(fma(al, al, (x[4 * RQ] + x[4 * RQ + 1]) + (x[4 * RQ + 2] + x[4 * RQ + 3])));
+      if (nx != 0.0) {
+        const double be = al >= 0.0 ? -nx : nx;
+        const double am = al - be;
+        const double rr = 1.0 / (be * am);  // sc = 1/(al-be) = be rr, tau = (be-al)/be = -am^2 rr
+        const double sc = be * rr;
+        if (c == j) {
+#pragma unroll
+          for (int i = 0; i < RQ; ++i)
+            if (r0 + i > j) col[i] *= sc;
+          if (qd == jb) col[jj] = be;
+          if (threadIdx.x == 4 * j) tau[j] = -(am * am) * rr;
+        } else if (c > j && live) {
+          double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+          for (int i = 0; i < RQ; i += 2) {
+            w0 = fma(x[r0 + i], col[i], w0);
+            w1 = fma(x[r0 + i + 1], col[i + 1], w1);
+          }
+          double w = w0 + w1;
+          w += __shfl_xor_sync(qmask, w, 1);
+          w += __shfl_xor_sync(qmask, w, 2);
+          // column c's entry in row j lives in quarter jb
+          const double cj = __shfl_sync(qmask, col[jj], (lane() & 28) | jb);
+          const double d = fma(sc, w, cj) * (-(am * am) * rr);
+          const double f = sc * d;
+          asm volatile("" ::: "memory");  // re-read x: RQ registers saved
+#pragma unroll
+          for (int i = 0; i < RQ; ++i) col[i] = fma(-x[r0 + i], f, col[i]);
+          if (qd == jb) col[jj] -= d;
+        }
+      } else if (threadIdx.x == 4 * j) {
+        tau[j] = 0.0;
+      }
     }
-    const double al = v[j];
-    const double be = al >= 0.0 ? -nx : nx;
-    const double tj = (be - al) / be;
-    const double sc = 1.0 / (al - be);
-    __syncthreads();  // everyone has read v[j]
-    for (int i = j + 1 + threadIdx.x; i < rows; i += kThreads) v[i] *= sc;
-    if (threadIdx.x == 0) {
-      v[j] = be;
-      tau[j] = tj;
-    }
-    __syncthreads();
-    for (int kk = j + 1 + warp(); kk < cols; kk += kWarps) {
-      double* w = A + kk * lda;
-      double s = 0.0;
-      for (int i = j + 1 + lane(); i < rows; i += 32) s += v[i] * w[i];
-      s = warp_sum(s);
-      const double d = (w[j] + s) * tj;
-      __syncwarp();
-      if (lane() == 0) w[j] -= d;
-      for (int i = j + 1 + lane(); i < rows; i += 32) w[i] -= v[i] * d;
-    }
-    __syncthreads();
   }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < RQ; ++i)
+    if (live && r0 + i < rows) A[r0 + i + c * lda] = col[i];
+  __syncthreads();
+}
+
+__device__ inline void householder(double* A, int lda, int rows, int cols, double* tau, double* xb) {
+  if (rows <= 64)
+    householder_regs<16>(A, lda, rows, cols, tau, xb);
+  else
+    householder_regs<32>(A, lda, rows, cols, tau, xb);  // rows <= 128 (2 k_child, m <= 64)
 }
 
 // Householder QR with column pivoting (largest remaining column norm, first
