@@ -292,23 +292,28 @@ __device__ __forceinline__ void weights_step(double (&B)[NCOL][CR], const double
                                              const int (&coff)[NCOL], int lane, int j, int kc) {
   // ||x||^2 and the dot products with the raw column (branch-free: every
   // lane runs the same straight-line code, dead columns get f = 0)
-  double q[4] = {0.0, 0.0, 0.0, 0.0};
   double w[NCOL][2];
 #pragma unroll
   for (int t = T0; t < NCOL; ++t) w[t][0] = w[t][1] = 0.0;
 #pragma unroll
   for (int i = 0; i < CR; i += 2) {
     const double2 xx = *reinterpret_cast<const double2*>(x + i);
-    q[i & 3] = fma(xx.x, xx.x, q[i & 3]);
-    q[(i + 1) & 3] = fma(xx.y, xx.y, q[(i + 1) & 3]);
 #pragma unroll
     for (int t = T0; t < NCOL; ++t) {
       w[t][0] = fma(xx.x, B[t][i], w[t][0]);
       w[t][1] = fma(xx.y, B[t][i + 1], w[t][1]);
     }
   }
+  // ||x||^2 by a butterfly over the warp (lane L squares rows L, L + 32, ...):
+  // off the FP64 pipe, and shorter than the dot-product chains above; every
+  // lane ends with the same value
+  double q = 0.0;
+#pragma unroll
+  for (int i = lane; i < CR; i += 32) q = fma(x[i], x[i], q);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
   const double al = x[CR];
-  const double nx = sqrt(fma(al, al, (q[0] + q[1]) + (q[2] + q[3])));
+  const double nx = sqrt(fma(al, al, q));
   const double be = al >= 0.0 ? -nx : nx;
   const double am = al - be;
   const double r = 1.0 / (be * am);  // sc = 1/(al-be) = be r, tau = (be-al)/be = -am^2 r
