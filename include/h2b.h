@@ -62,7 +62,8 @@ typedef enum {
   H2B_OUT_OF_MEMORY = 3,
   H2B_UNSUPPORTED = 4,      /* shape outside the compiled kernel envelope */
   H2B_NO_DEVICE = 5,
-  H2B_INTERNAL = 6
+  H2B_INTERNAL = 6,
+  H2B_IO_ERROR = 7          /* reference: h2kit::IOError (io.hpp:19-21) */
 } h2b_status;
 
 typedef enum {
@@ -104,6 +105,14 @@ typedef struct {
   double perturbation;  /* grid jitter (0.25) */
   uint64_t seed;        /* mt19937_64 seed (1) */
 } h2b_build_config;
+
+/* BuildInfo (h2_matrix.hpp:53-60): construction parameters stored in containers. */
+typedef struct {
+  int32_t dim;
+  uint64_t seed;
+  double perturbation, ell, eta;
+  int32_t grid_order;
+} h2b_build_info;
 
 /* Sizes of a matrix in the export layout. */
 typedef struct {
@@ -154,6 +163,17 @@ H2B_API h2b_status h2b_matrix_export(const h2b_matrix* A, int32_t* perm, double*
                              int32_t* cpl_row_ptr, int32_t* cpl_col_idx, double* cpl_values,
                              int32_t* dense_row_ptr, int32_t* dense_col_idx, double* dense_values);
 H2B_API uint64_t h2b_matrix_footprint(const h2b_matrix* A);
+/* h2kit::save / h2kit::load (io.hpp:183-282): the reference's ".h2" container
+ * ("H2KT" v1, FP64, CRC-32 per section), byte-compatible in both directions;
+ * the pools stream straight from / into HBM.  info: BuildInfo to store (NULL:
+ * the matrix's own -- set by h2b_matrix_build / h2b_matrix_load, zeros for
+ * h2b_matrix_create); info_out may be NULL.  Errors: H2B_IO_ERROR with the
+ * reference's messages; non-symmetric containers: H2B_UNSUPPORTED. */
+H2B_API h2b_status h2b_matrix_save(const h2b_matrix* A, const char* path, const h2b_build_info* info);
+H2B_API h2b_status h2b_matrix_load(const char* path, int device, h2b_matrix** out, h2b_build_info* info_out);
+/* h2kit::crc32 (crc32.cpp:6-20, seed 0): the containers' section checksum
+ * (host memory; slicing-by-8, chunk-parallel with CRC combination). */
+H2B_API uint32_t h2b_crc32(const void* data, uint64_t len);
 
 /* y <- alpha (A_D + A_LR) x + beta y, x and y in original point order.
  * beta == 0 never reads y (hmv.hpp:186). stream is a cudaStream_t (NULL =

@@ -132,6 +132,18 @@ class Backend:
                                      C.byref(h)))
         return OracleMatrix(self, h.value)
 
+    # -- container I/O (reference backend only: h2kit::save / load, crc32) --
+    def load(self, path: str) -> "OracleMatrix":
+        h = _P()
+        self.lib.ref_load.argtypes = [C.c_char_p, C.POINTER(_P)]
+        self.check(self.lib.ref_load(path.encode(), C.byref(h)))
+        return OracleMatrix(self, h.value)
+
+    def crc32(self, data: bytes) -> int:
+        self.lib.ref_crc32.argtypes = [C.c_char_p, C.c_uint64]
+        self.lib.ref_crc32.restype = C.c_uint32
+        return int(self.lib.ref_crc32(data, len(data)))
+
     def set_threads(self, n):
         if self.prefix == "ref_":
             self.lib.ref_set_threads(int(n))
@@ -151,6 +163,10 @@ class OracleMatrix:
                 self.be.fn("destroy")(self.h)
         except Exception:
             pass
+
+    def save(self, path: str):
+        self.be.lib.ref_save.argtypes = [_P, C.c_char_p]
+        self.be.check(self.be.lib.ref_save(self.h, path.encode()))
 
     def clone(self) -> "OracleMatrix":
         return OracleMatrix(self.be, self.be.fn("clone")(self.h))

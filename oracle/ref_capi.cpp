@@ -24,6 +24,7 @@
 #include "h2kit/compression.hpp"
 #include "h2kit/construction.hpp"
 #include "h2kit/hmv.hpp"
+#include "h2kit/io.hpp"
 #include "h2kit/validate.hpp"
 
 #ifdef _OPENMP
@@ -340,5 +341,16 @@ int ref_validate_sampled(void* h, double fraction, uint64_t seed, double* err) {
     *err = validate_sampled(A, ps, spec, fraction, seed);
   });
 }
+
+// h2kit::save / h2kit::load (io.hpp:183-282) and crc32 (crc32.cpp:6-20).
+int ref_save(void* h, const char* path) {
+  return guarded([&] { save(*static_cast<Mat*>(h), std::string(path)); });
+}
+
+int ref_load(const char* path, void** out) {
+  return guarded([&] { *out = new Mat(load<double>(std::string(path))); });
+}
+
+uint32_t ref_crc32(const void* data, uint64_t len) { return crc32(data, size_t(len)); }
 
 }  // extern "C"

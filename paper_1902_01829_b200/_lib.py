@@ -18,6 +18,7 @@ H2B_OUT_OF_MEMORY = 3
 H2B_UNSUPPORTED = 4
 H2B_NO_DEVICE = 5
 H2B_INTERNAL = 6
+H2B_IO_ERROR = 7
 
 PTR_AUTO, PTR_HOST, PTR_DEVICE = 0, 1, 2
 WS_XHAT, WS_YHAT, WS_XC, WS_PERM = 0, 1, 2, 3
@@ -34,6 +35,10 @@ class H2bInvalidArgument(H2bError, ValueError):
     """The reference's std::invalid_argument (include/h2kit/defs.hpp:20-22)."""
 
 
+class H2bIOError(H2bError, OSError):
+    """h2kit::IOError (io.hpp:19-21): container open / format / checksum errors."""
+
+
 class H2bNoDevice(H2bError):
     pass
 
@@ -44,6 +49,11 @@ class MatrixDesc(C.Structure):
                 ("transfer", C.c_void_p), ("cpl_row_ptr", C.c_void_p), ("cpl_col_idx", C.c_void_p),
                 ("cpl_values", C.c_void_p), ("dense_row_ptr", C.c_void_p),
                 ("dense_col_idx", C.c_void_p), ("dense_values", C.c_void_p)]
+
+
+class BuildInfo(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("seed", C.c_uint64), ("perturbation", C.c_double),
+                ("ell", C.c_double), ("eta", C.c_double), ("grid_order", C.c_int32)]
 
 
 class BuildConfig(C.Structure):
@@ -96,6 +106,9 @@ _SIGS = {
     "h2b_matrix_info_get": (C.c_int, [C.c_void_p, C.POINTER(MatrixInfo)]),
     "h2b_matrix_export": (C.c_int, [C.c_void_p] + [C.c_void_p] * 9),
     "h2b_matrix_footprint": (C.c_uint64, [C.c_void_p]),
+    "h2b_matrix_save": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p]),
+    "h2b_matrix_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p), C.c_void_p]),
+    "h2b_crc32": (C.c_uint32, [C.c_void_p, C.c_uint64]),
     "h2b_hmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int,
                           C.c_void_p]),
     "h2b_hmv_multi": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
@@ -146,6 +159,8 @@ def check(status: int):
     msg = load().h2b_last_error().decode(errors="replace")
     if status == H2B_INVALID_ARGUMENT:
         raise H2bInvalidArgument(status, msg)
+    if status == H2B_IO_ERROR:
+        raise H2bIOError(status, msg)
     if status == H2B_NO_DEVICE:
         raise H2bNoDevice(status, msg)
     raise H2bError(status, msg)

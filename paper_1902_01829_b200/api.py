@@ -11,6 +11,7 @@ tensors / any object exposing ``data_ptr()`` on the matrix's device.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -86,6 +87,28 @@ class H2Matrix:
         A.build_config = dict(dim=dim, n=n, leaf_size=leaf_size, grid_order=grid_order, eta=eta,
                               ell=ell, perturbation=perturbation, seed=seed)
         return A
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "H2Matrix":
+        """h2kit::load<double>(path) (io.hpp:247-282) straight into HBM; the stored
+        BuildInfo is available as .build_info."""
+        out = C.c_void_p()
+        bi = _lib.BuildInfo()
+        _lib.check(_lib.load().h2b_matrix_load(os.fspath(path).encode(), device, C.byref(out),
+                                               C.byref(bi)))
+        A = cls(out.value, device)
+        A.build_info = {k: getattr(bi, k) for k, _ in bi._fields_}
+        return A
+
+    def save(self, path: str, build_info: dict | None = None):
+        """h2kit::save(A, path) (io.hpp:183-229): the reference's container, byte for
+        byte.  build_info overrides the stored BuildInfo (dim, seed, perturbation,
+        ell, eta, grid_order)."""
+        bi = None
+        if build_info is not None:
+            bi = _lib.BuildInfo(**build_info)
+        _lib.check(_lib.load().h2b_matrix_save(self._h, os.fspath(path).encode(),
+                                               C.byref(bi) if bi is not None else None))
 
     def close(self):
         if self._h and self._h.value:
@@ -288,3 +311,10 @@ def release_cached_memory(device: int = 0) -> None:
     """Hand the memory compress() cached in the device's stream-ordered pool back
     to the device (h2b_release_cached_memory)."""
     _lib.check(_lib.load().h2b_release_cached_memory(int(device)))
+
+
+def crc32(data) -> int:
+    """h2kit::crc32 (crc32.cpp:6-20) of a bytes-like object (host)."""
+    mv = memoryview(data).cast("B")
+    buf = (C.c_char * len(mv)).from_buffer_copy(mv) if mv.readonly else (C.c_char * len(mv)).from_buffer(mv)
+    return int(_lib.load().h2b_crc32(C.addressof(buf), len(mv)))

@@ -424,6 +424,12 @@ h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, in
   H2B_CUDA(cudaMemcpyAsync(A->pts_orig.p, X.data(), X.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   A->pts_dim = cfg.dim;
   A->ell = cfg.ell;
+  A->info.dim = cfg.dim;
+  A->info.seed = cfg.seed;
+  A->info.perturbation = cfg.perturbation;
+  A->info.ell = cfg.ell;
+  A->info.eta = cfg.eta;
+  A->info.grid_order = cfg.grid_order;
   DevBuf<double> dpts;
   dpts.alloc(pc.size());
   H2B_CUDA(cudaMemcpyAsync(dpts.p, pc.data(), pc.size() * sizeof(double), cudaMemcpyHostToDevice, s));

@@ -100,6 +100,9 @@ void upload_blocks(const double* h, double* d, int rows, int cols, int64_t count
   H2B_CUDA(cudaStreamSynchronize(s));
 }
 
+}  // namespace
+
+// padded device blocks -> unpadded host blocks (also used by io.cu)
 void download_blocks(const double* d, double* h, int rows, int cols, int64_t count,
                      cudaStream_t s) {
   const int ld = pad2(rows);
@@ -117,7 +120,6 @@ void download_blocks(const double* d, double* h, int rows, int cols, int64_t cou
   H2B_CUDA(cudaStreamSynchronize(s));
 }
 
-}  // namespace
 
 Matrix::~Matrix() {
   if (stream) cudaStreamSynchronize(stream);
@@ -430,6 +432,9 @@ using namespace h2b;
 // Implemented in build.cu / compress.cu.
 namespace h2b {
 h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, int part);
+void save_matrix(const Matrix& A, const std::string& path, const h2b_build_info* info);
+h2b_matrix* load_matrix(const std::string& path, int device, h2b_build_info* info_out);
+uint32_t crc32_bytes(const void* p, size_t n);
 void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_comm* comm = nullptr);
 void release_workspaces(int device);
 void orthogonalize_matrix(Matrix& A, double* t_out);
@@ -682,6 +687,23 @@ h2b_status h2b_compress(h2b_matrix* Ah, double eps, h2b_compress_report* report)
     require(Ah, "null matrix");
     whole(*Ah, "h2b_compress");
     compress_matrix(*Ah, eps, report);
+  });
+}
+
+uint32_t h2b_crc32(const void* data, uint64_t len) { return crc32_bytes(data, size_t(len)); }
+
+h2b_status h2b_matrix_save(const h2b_matrix* Ah, const char* path, const h2b_build_info* info) {
+  return guarded([&] {
+    require(Ah && path, "null argument");
+    DeviceGuard g(Ah->device);
+    save_matrix(*Ah, path, info);
+  });
+}
+
+h2b_status h2b_matrix_load(const char* path, int device, h2b_matrix** out, h2b_build_info* info) {
+  return guarded([&] {
+    require(path && out, "null argument");
+    *out = load_matrix(path, device, info);
   });
 }
 

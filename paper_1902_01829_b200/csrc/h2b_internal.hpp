@@ -137,6 +137,7 @@ struct Matrix {
   DevBuf<double> pts_orig;
   int pts_dim = 0;
   double ell = 0.0;
+  h2b_build_info info{};            // BuildInfo of the container format (h2_matrix.hpp:53-60)
   double* h_stage = nullptr;        // pinned host staging for host-pointer calls
   size_t h_stage_n = 0;
 
