@@ -26,6 +26,7 @@
 namespace h2b {
 
 void allocate(Matrix& A);
+void check_value_symmetry(Matrix& A);
 void upload_structure(Matrix& A);
 
 namespace {
@@ -483,6 +484,7 @@ h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, in
     }
     H2B_CUDA(cudaStreamSynchronize(s));
   }
+  check_value_symmetry(*A);
   return A.release();
 }
 

@@ -210,8 +210,107 @@ void allocate(Matrix& A) {
 }
 
 // Upload the CSR structure of every layer and build the fused work list.
+// Mirror map of the coupling levels (used by the symmetric projection of
+// compress()): mirror[b] = index of block (col, row) for block b = (row, col)
+// when the level's block pattern is symmetric (always, for construct()), -1
+// everywhere otherwise.  O(nb log k) per level: every row's (col, block)
+// pairs sorted, merged with the transposed pattern built by a counting pass.
+void build_mirror(Matrix& A) {
+  const int q = A.q;
+  std::vector<int32_t> all;
+  A.mirror_sym.assign(q + 1, 0);
+  A.mirror_off.assign(q + 2, 0);
+  for (int l = 0; l <= q; ++l) {
+    const Layer& L = A.cpl[l];
+    std::vector<int32_t> mir(L.nb, -1);
+    bool ok = A.part_s == 0 && L.nb > 0;  // a partition handle does not hold the mirror rows
+    if (ok) {
+      // transposed pattern: for row c, the blocks (r, c) in increasing r
+      std::vector<int64_t> tp(L.rows + 1, 0);
+      for (int64_t b = 0; b < L.nb; ++b) ++tp[L.h_ci[b] + 1];
+      for (int64_t r = 0; r < L.rows; ++r) tp[r + 1] += tp[r];
+      std::vector<std::pair<int32_t, int32_t>> tr(L.nb);  // (row, block)
+      std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
+      for (int64_t r = 0; r < L.rows && ok; ++r)
+        for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1]; ++b) {
+          if (L.h_ci[b] == r) ok = false;
+          tr[fill[L.h_ci[b]]++] = {int32_t(r), b};
+        }
+      std::vector<std::pair<int32_t, int32_t>> row;  // (col, block) of row c, sorted
+      for (int64_t c = 0; c < L.rows && ok; ++c) {
+        row.clear();
+        for (int32_t b = L.h_rp[c]; b < L.h_rp[c + 1]; ++b) row.push_back({L.h_ci[b], b});
+        std::sort(row.begin(), row.end());
+        const int64_t t0 = tp[c], t1 = tp[c + 1];
+        if (t1 - t0 != int64_t(row.size())) {
+          ok = false;
+          break;
+        }
+        // block (r, c) = tr[t] mirrors block (c, r) = row[k]
+        for (int64_t t = t0, k = 0; t < t1; ++t, ++k) {
+          if (tr[t].first != row[k].first) {
+            ok = false;
+            break;
+          }
+          mir[tr[t].second] = row[k].second;
+        }
+      }
+    }
+    if (!ok) std::fill(mir.begin(), mir.end(), -1);
+    A.mirror_sym[l] = ok;
+    A.mirror_off[l + 1] = A.mirror_off[l] + L.nb;
+    all.insert(all.end(), mir.begin(), mir.end());
+  }
+  A.mirror.alloc(std::max<size_t>(1, all.size()));
+  if (!all.empty())
+    H2B_CUDA(cudaMemcpyAsync(A.mirror.p, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice, A.stream));
+  A.mirror_ready = true;
+}
+
+// Value symmetry of the mirrored coupling blocks: S_(c,r) == S_(r,c)^T bit for
+// bit.  The reference's "symmetric" means row basis == column basis; a
+// construct() matrix (kernel evaluations) is symmetric in its blocks too, a
+// user's h2b_matrix_create matrix need not be.  One pass over the coupling
+// pool at creation; the symmetric projection of compress() is used only on
+// levels that pass (and keeps them exactly symmetric).
+__global__ void k_sym_check(const double* __restrict__ val, int64_t bstride, int ld, int k, const int32_t* __restrict__ rp,
+                            const int32_t* __restrict__ ci, const int32_t* __restrict__ mirror, int64_t rows,
+                            int* __restrict__ bad) {
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  for (int b = rp[r]; b < rp[r + 1]; ++b) {
+    if (ci[b] <= r) continue;
+    const double* S = val + int64_t(b) * bstride;
+    const double* M = val + int64_t(mirror[b]) * bstride;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+      const int j = e / k, i = e - j * k;
+      if (S[i + j * ld] != M[j + i * ld]) *bad = 1;
+    }
+  }
+}
+
+void check_value_symmetry(Matrix& A) {
+  cudaStream_t s = A.stream;
+  A.value_sym.assign(A.q + 1, 0);
+  DevBuf<int> bad;
+  bad.alloc(A.q + 1);
+  bad.zero(s);
+  for (int l = 0; l <= A.q; ++l) {
+    const Layer& L = A.cpl[l];
+    if (!A.mirror_sym[l] || L.nb == 0) continue;
+    k_sym_check<<<unsigned(L.rows), 128, 0, s>>>(L.val, L.block_stride(), L.ld, L.br, L.rp, L.ci,
+                                                 A.mirror.p + A.mirror_off[l], L.rows, bad.p + l);
+    H2B_CUDA(cudaGetLastError());
+  }
+  std::vector<int> h(A.q + 1);
+  H2B_CUDA(cudaMemcpyAsync(h.data(), bad.p, (A.q + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+  for (int l = 0; l <= A.q; ++l) A.value_sym[l] = A.mirror_sym[l] && !h[l];
+}
+
 void upload_structure(Matrix& A) {
   cudaStream_t s = A.stream;
+  build_mirror(A);
   for (int l = 0; l <= A.q; ++l) {
     Layer& L = A.cpl[l];
     L.max_row = 0;
@@ -304,6 +403,7 @@ h2b_matrix* create_from_desc(const h2b_matrix_desc& d, int device) {
   }
   upload_blocks(d.dense_values, A->dense.val, A->m, A->m, A->dense.nb, s);
   upload_structure(*A);
+  check_value_symmetry(*A);
   return A.release();
 }
 

@@ -107,11 +107,13 @@ struct ProjRow {
 
 struct ProjLevel {
   const double* S;    // old blocks (ld_old x co)
-  double* out;        // new blocks (ld_new x cn)
+  double* out;        // new blocks (ld_new x cn), block b at out + b * ostride
   const int32_t* rp;
   const int32_t* ci;
+  const int32_t* mirror;  // symmetric levels: block index of (col, row), or null
   const double* T;    // rn x ro per node, ld rn
   int ro, rn, ld_old, ld_new;
+  int64_t ostride;
 };
 struct ProjTable {
   ProjLevel L[kMaxLevels + 1];
@@ -130,7 +132,7 @@ struct ProjTable {
 constexpr int kPLd = 68;  // smem leading dimension (== 4 mod 16: conflict-free fragments)
 template <bool TRI>
 __device__ __forceinline__ void project_block(const double* Tr, const double* Sb, const double* Tc, double* out,
-                                              int ld_new, int ro, int rn, double& sumsq) {
+                                              double* outT, int ld_new, int ro, int rn, double& sumsq) {
   const int w = cta::warp(), t = cta::lane();
   const int fr = t >> 2, fk = t & 3;
   const int i0 = 8 * w;
@@ -187,12 +189,16 @@ __device__ __forceinline__ void project_block(const double* Tr, const double* Sb
         const int j = 8 * y + 2 * fk + v;
         if (j < rn) {
           out[i + int64_t(j) * ld_new] = o[y][v];
+          if (outT) outT[j + int64_t(i) * ld_new] = o[y][v];  // mirror block (col, row)
           sumsq = fma(o[y][v], o[y][v], sumsq);
         }
       }
   }
   if (ld_new > rn && w == 0)
-    for (int j = t; j < rn; j += 32) out[rn + int64_t(j) * ld_new] = 0.0;
+    for (int j = t; j < rn; j += 32) {
+      out[rn + int64_t(j) * ld_new] = 0.0;
+      if (outT) outT[rn + int64_t(j) * ld_new] = 0.0;
+    }
 }
 
 // 8-byte asynchronous global -> shared copies (cp.async.ca), grouped.
@@ -228,17 +234,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   const int b0 = L.rp[pr.row], b1 = L.rp[pr.row + 1];
   double ss = 0.0;
   for (int b = b0; b < b1; ++b) {
+    // symmetric level: (col, row) is the transpose of (row, col); the upper
+    // block computes both (S_ji' = T_j S_ij^T T_i^T = (T_i S_ij T_j^T)^T)
+    const int mb = L.mirror ? L.mirror[b] : -1;
+    if (L.mirror && L.ci[b] < pr.row && mb >= 0) continue;
     __syncthreads();  // previous block done with Sb / Tc
     stage64(Sb, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
     stage64(Tc, L.T + int64_t(L.ci[b]) * rn * ro, rn, rn, ro);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    double* out = L.out + int64_t(b) * L.ld_new * rn;
+    double* out = L.out + int64_t(b) * L.ostride;
+    double* outT = (mb >= 0 && L.ci[b] > pr.row) ? L.out + int64_t(mb) * L.ostride : nullptr;
+    double s1 = 0.0;
     if (P.tri)
-      project_block<true>(Tr, Sb, Tc, out, L.ld_new, ro, rn, ss);
+      project_block<true>(Tr, Sb, Tc, out, outT, L.ld_new, ro, rn, s1);
     else
-      project_block<false>(Tr, Sb, Tc, out, L.ld_new, ro, rn, ss);
+      project_block<false>(Tr, Sb, Tc, out, outT, L.ld_new, ro, rn, s1);
+    ss += outT ? 2.0 * s1 : s1;
   }
   // ||S||_F^2 of the projected row, fused (compression.hpp:487, frob_norm_sq)
   if (P.rowsum) {
@@ -971,9 +984,17 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
 // the workspace arena -- chunk k's destination ends where chunk k+1's source
 // starts or earlier (every block only shrinks), so nothing unread is clobbered
 // and no second coupling pool is ever allocated.
+// Project every coupling level with T (rows x cols per node, compression.hpp:
+// 130-169): blocks become T.rows[l] x T.rows[l].  On symmetric levels only the
+// upper blocks are multiplied; each also writes its mirror (the transpose).
+// The new blocks are written into the OLD block slots (they only shrink), then
+// -- for the truncation's rectangular T -- compacted in block order through
+// the workspace arena: chunk k's destination ends at or before chunk k+1's
+// source, so nothing unread is clobbered and no second pool is allocated.
 void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place, const Part& pt,
              Arena& ar, double* frob2 = nullptr) {
   const int q = A.q;
+  require(A.mirror_ready, "project_coupling: mirror map missing");
   ProjTable P{};
   P.tri = in_place ? 1 : 0;
   std::vector<int64_t> new_off(q + 2, 0);
@@ -982,7 +1003,6 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     const int rn = T.rows[l];
     new_off[l + 1] = new_off[l] + L.nb * int64_t(pad2(rn)) * rn;
   }
-  // block rows in pool order (level, row)
   std::vector<ProjRow> rows;
   for (int l = 0; l <= q; ++l) {
     Layer& L = A.cpl[l];
@@ -994,61 +1014,72 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
     d.S = L.val;
     d.rp = L.rp;
     d.ci = L.ci;
+    d.mirror = (A.mirror_sym[l] && l < int(A.value_sym.size()) && A.value_sym[l]) ? A.mirror.p + A.mirror_off[l]
+                                                                                    : nullptr;
     d.T = T.at(l);
     d.ro = ro;
     d.rn = rn;
     d.ld_old = L.ld;
     d.ld_new = pad2(rn);
-    d.out = in_place ? L.val : nullptr;
+    d.out = L.val;  // in the old slots
+    d.ostride = L.block_stride();
     if (rn == 0) continue;
-    for (int64_t r = 0; r < L.rows; ++r)
-      if (L.h_rp[r + 1] > L.h_rp[r]) rows.push_back({l, int32_t(r)});
+    for (int64_t r = 0; r < L.rows; ++r) {
+      bool any = false;
+      for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1] && !any; ++b) any = !d.mirror || L.h_ci[b] > r;
+      if (any) rows.push_back({l, int32_t(r)});
+    }
   }
   const size_t smax = size_t(3) * 64 * kPLd * sizeof(double);
   check_smem(smax, "project_coupling");
   set_smem(k_project, smax);
   ar.off = 0;
   ProjRow* drows = ar.take<ProjRow>(std::max<size_t>(1, rows.size()));
-  if (!rows.empty())
+  double* rsum = ar.take<double>(std::max<size_t>(1, rows.size()));
+  P.rowsum = frob2 ? rsum : nullptr;
+  if (!rows.empty()) {
     H2B_CUDA(cudaMemcpyAsync(drows, rows.data(), rows.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
-  if (in_place) {
-    double* rsum = ar.take<double>(std::max<size_t>(1, rows.size()));
-    P.rowsum = frob2 ? rsum : nullptr;
-    if (!rows.empty()) {
-      k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows);
-      H2B_CUDA(cudaGetLastError());
-    }
-    if (frob2) {  // sum of the counted rows (replicated top levels: rank 0 only)
-      std::vector<double> h(rows.size());
-      if (!rows.empty())
-        H2B_CUDA(cudaMemcpyAsync(h.data(), rsum, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-      H2B_CUDA(cudaStreamSynchronize(s));
-      double acc = 0.0;
-      for (size_t i = 0; i < rows.size(); ++i)
-        if (pt.counts(rows[i].level)) acc += h[i];
-      *frob2 = acc;
-    }
-  } else {
+    k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows);
+    H2B_CUDA(cudaGetLastError());
+  }
+  if (frob2) {  // sum of the counted rows (replicated top levels: rank 0 only)
+    std::vector<double> h(rows.size());
+    if (!rows.empty())
+      H2B_CUDA(cudaMemcpyAsync(h.data(), rsum, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    H2B_CUDA(cudaStreamSynchronize(s));
+    double acc = 0.0;
+    for (size_t i = 0; i < rows.size(); ++i)
+      if (pt.counts(rows[i].level)) acc += h[i];
+    *frob2 = acc;
+  }
+  if (!in_place) {
+    // compaction: level by level, block order, chunks staged in the arena
     double* temp = ar.base + ar.off;
     const int64_t cap = int64_t(ar.cap - ar.off);
-    size_t i = 0;
-    while (i < rows.size()) {
-      // one chunk: consecutive rows of one level whose new blocks fit in temp
-      const int l = rows[i].level;
+    for (int l = 0; l <= q; ++l) {
       const Layer& L = A.cpl[l];
-      const int64_t bs = int64_t(pad2(T.rows[l])) * T.rows[l];
-      const int64_t b0 = L.h_rp[rows[i].row];
-      size_t j = i;
-      while (j < rows.size() && rows[j].level == l && (L.h_rp[rows[j].row + 1] - b0) * bs <= cap) ++j;
-      require(j > i, "project_coupling: workspace smaller than one block row");
-      const int64_t b1 = L.h_rp[rows[j - 1].row + 1];
-      ProjTable Pc = P;
-      Pc.L[l].out = temp - b0 * bs;  // block b lands at temp + (b - b0) * bs
-      k_project<<<unsigned(j - i), kThreads, smax, s>>>(Pc, drows + i);
-      H2B_CUDA(cudaGetLastError());
-      H2B_CUDA(cudaMemcpyAsync(A.cpl_val.p + new_off[l] + b0 * bs, temp, (b1 - b0) * bs * sizeof(double),
-                               cudaMemcpyDeviceToDevice, s));
-      i = j;
+      const int64_t bs_new = int64_t(pad2(T.rows[l])) * T.rows[l], bs_old = L.block_stride();
+      if (L.nb == 0 || bs_new == 0) continue;
+      const int64_t per = std::max<int64_t>(1, cap / bs_new);
+      const int64_t old_off = L.val - A.cpl_val.p;
+      for (int64_t b0 = 0; b0 < L.nb;) {
+        double* dst = A.cpl_val.p + new_off[l] + b0 * bs_new;
+        const double* src = L.val + b0 * bs_old;
+        // room between this chunk's destination and its (unread) sources:
+        // chunks that fit in it are copied directly, the rest through temp
+        const int64_t gap = (old_off + b0 * bs_old) - (new_off[l] + b0 * bs_new);
+        int64_t nb = std::min(L.nb - b0, gap / bs_new);
+        if (nb >= 1) {
+          H2B_CUDA(cudaMemcpy2DAsync(dst, bs_new * sizeof(double), src, bs_old * sizeof(double),
+                                     bs_new * sizeof(double), nb, cudaMemcpyDeviceToDevice, s));
+        } else {
+          nb = std::min(per, L.nb - b0);
+          H2B_CUDA(cudaMemcpy2DAsync(temp, bs_new * sizeof(double), src, bs_old * sizeof(double),
+                                     bs_new * sizeof(double), nb, cudaMemcpyDeviceToDevice, s));
+          H2B_CUDA(cudaMemcpyAsync(dst, temp, nb * bs_new * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        }
+        b0 += nb;
+      }
     }
   }
   H2B_CUDA(cudaStreamSynchronize(s));

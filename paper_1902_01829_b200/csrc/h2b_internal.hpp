@@ -138,6 +138,13 @@ struct Matrix {
   int pts_dim = 0;
   double ell = 0.0;
   h2b_build_info info{};            // BuildInfo of the container format (h2_matrix.hpp:53-60)
+  // coupling mirror map (block (col,row) of block (row,col)) for the symmetric
+  // projection in compress(); structure only, built on first use
+  bool mirror_ready = false;
+  std::vector<char> mirror_sym;     // per level: pattern symmetric
+  std::vector<char> value_sym;      // per level: blocks symmetric too (set at creation)
+  std::vector<int64_t> mirror_off;
+  DevBuf<int32_t> mirror;
   double* h_stage = nullptr;        // pinned host staging for host-pointer calls
   size_t h_stage_n = 0;
 
