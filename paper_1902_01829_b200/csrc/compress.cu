@@ -374,12 +374,18 @@ __device__ __forceinline__ void weights_step(double (&B)[NCOL][CR], const double
 }
 
 constexpr int kWWarps = 4;  // nodes (warps) per CTA
+// A work item of k_weights: the stack rows [parent rows if par][blocks b0..b1)
+// of node `node`, R written to slot `out` (transposed when the launch's out_t
+// is set, so a merge launch can read the partial R's as "blocks").
+struct WItem {
+  int32_t node, b0, b1, out, par;
+};
+
 template <int NCOL, int CR>
 __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __restrict__ P, int kc, int kp,
-                                                          const int32_t* __restrict__ rp,
                                                           const double* __restrict__ S, int lds,
-                                                          double* __restrict__ Rout, int64_t nnodes,
-                                                          const int32_t* __restrict__ order,
+                                                          double* __restrict__ Rout, int out_t,
+                                                          const WItem* __restrict__ items, int64_t nitems,
                                                           int* __restrict__ next) {
   constexpr int XS = CR + 2;  // publish slot: raw column, alpha
   extern __shared__ double sm[];
@@ -393,8 +399,9 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
   int idx = 0;
   if (lane == 0) idx = atomicAdd(next, 1);
   idx = __shfl_sync(0xffffffffu, idx, 0);
-  if (idx >= nnodes) break;
-  const int64_t node = order[idx];
+  if (idx >= nitems) break;
+  const WItem it = items[idx];
+  const int64_t node = it.node;
   for (int e = lane; e < rsz; e += 32) Rp[e] = 0.0;
   int coff[NCOL];
 #pragma unroll
@@ -402,9 +409,9 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
     const int c = lane + 32 * t;
     coff[t] = (c * (c + 1)) >> 1;
   }
-  const int b1 = rp[node + 1];
-  int b = rp[node];
-  int prow = 0;  // next parent row
+  const int b1 = it.b1;
+  int b = it.b0;
+  int prow = it.par ? 0 : kp;  // next parent row
   int brow = 0;  // next row of block b's transpose
   double B[NCOL][CR];
   int jg = 0;    // reflector counter (selects the publish slot)
@@ -460,12 +467,16 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
   }
   // R with non-negative diagonal (linalg.hpp:100-113); row i by lane, so the
   // stores of one column are coalesced
-  double* Ro = Rout + node * int64_t(kc) * kc;
+  double* Ro = Rout + int64_t(it.out) * kc * kc;
   for (int cc = 0; cc < kc; ++cc) {
     const int ccoff = (cc * (cc + 1)) >> 1;
     for (int i = lane; i < kc; i += 32) {
       const double v = i <= cc ? Rp[ccoff + i] : 0.0;
-      Ro[i + int64_t(cc) * kc] = Rp[((i * (i + 1)) >> 1) + i] < 0.0 ? -v : v;
+      const double o = Rp[((i * (i + 1)) >> 1) + i] < 0.0 ? -v : v;
+      if (out_t)
+        Ro[cc + int64_t(i) * kc] = o;
+      else
+        Ro[i + int64_t(cc) * kc] = o;
     }
   }
   __syncwarp();
@@ -1104,43 +1115,57 @@ double sumsq(const double* v, int64_t n, cudaStream_t s, double* part) {
   return acc;
 }
 
-size_t weights_arena_need(const Matrix& A) {
-  size_t pmax = 1, nord = 1;
-  for (int l = 1; l <= A.q; ++l) {
-    pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
-    nord += A.own_count(l) + 1;
+// Warps the weight-tree kernel keeps resident on the device (persistent).
+int weights_slots(int device, int kc) {
+  int sms = 0, per_sm = 0;
+  H2B_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  constexpr int CR = 32;
+  const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
+  if (kc > 32) {
+    set_smem(k_weights<2, CR>, sm);
+    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<2, CR>, 32 * kWWarps, sm));
+  } else {
+    set_smem(k_weights<1, CR>, sm);
+    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<1, CR>, 32 * kWWarps, sm));
   }
-  return Arena::need(pmax, sizeof(double)) + Arena::need(nord, sizeof(int32_t));
+  return sms * std::max(1, per_sm) * kWWarps;
 }
 
+size_t weights_arena_need(const Matrix& A) {
+  size_t pmax = 1, items = 2;
+  const int slots = weights_slots(A.device, 64);
+  for (int l = 1; l <= A.q; ++l) {
+    pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
+    items = std::max(items, size_t(std::max<int64_t>(A.own_count(l), slots)) + 2);
+  }
+  // P, segment R's (<= slots + nodes), two item lists + counters
+  return Arena::need(pmax, sizeof(double)) + Arena::need(size_t(2 * items) * 64 * 64, sizeof(double)) +
+         2 * Arena::need(items * sizeof(WItem) / sizeof(int32_t) + 4, sizeof(int32_t));
+}
+
+// Weight tree (generate_weight_tree, compression.hpp:213-256), level by level
+// top-down.  A level with fewer nodes than resident warps is split: every
+// node's stack is cut into nseg contiguous segments processed by separate
+// warps (partial R's, stored transposed), then a merge launch re-triangularises
+// [R_0; ...; R_{nseg-1}] per node -- the same kernel, reading the partial R's
+// as blocks.  Items are issued longest first (LPT).
 void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, const Part& pt, double* tree_mem,
              Arena& ar) {
   const int q = A.q;
   R.alloc(A, A.rank, A.rank, tree_mem);
   H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * A.rank[0] * A.rank[0], s));
-  // LPT order of every level (nodes by decreasing stack height) plus one work
-  // counter per level, uploaded once
   size_t pmax = 1;
-  std::vector<int64_t> ooff(q + 2, 0);
-  for (int l = 1; l <= q; ++l) {
-    pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
-    ooff[l + 1] = ooff[l] + A.own_count(l) + 1;
-  }
-  std::vector<int32_t> ord(std::max<int64_t>(1, ooff[q + 1]), 0);
-  for (int l = 1; l <= q; ++l) {  // node indices relative to own_begin(l)
-    const Layer& L = A.cpl[l];
-    int32_t* o = ord.data() + ooff[l];
-    const int64_t nn = A.own_count(l), r0 = A.own_begin(l);
-    for (int64_t i = 0; i < nn; ++i) o[i] = int32_t(i);
-    std::stable_sort(o, o + nn, [&](int32_t a, int32_t b) {
-      return L.h_rp[r0 + a + 1] - L.h_rp[r0 + a] > L.h_rp[r0 + b + 1] - L.h_rp[r0 + b];
-    });
-    o[nn] = 0;
-  }
+  for (int l = 1; l <= q; ++l) pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
   ar.off = 0;
   double* Pall = ar.take<double>(pmax);
-  int32_t* dord_all = ar.take<int32_t>(ord.size());
-  H2B_CUDA(cudaMemcpyAsync(dord_all, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  const int slots = weights_slots(A.device, 64);
+  size_t maxitems = 2;
+  for (int l = 1; l <= q; ++l) maxitems = std::max(maxitems, size_t(std::max<int64_t>(A.own_count(l), slots)) + 2);
+  double* segR = ar.take<double>(2 * maxitems * 64 * 64);
+  WItem* ditems = ar.take<WItem>(maxitems);
+  WItem* dmerge = ar.take<WItem>(maxitems);
+  int* counters = ar.take<int>(4);
+  std::vector<WItem> items, merge;
   for (int l = 1; l <= q; ++l) {
     const int kc = A.rank[l], kp = A.rank[l - 1];
     const Layer& L = A.cpl[l];
@@ -1148,40 +1173,58 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, c
     flops += fl.gemm(double(A.nodes(l)), kp, kc, kp) + fl.qr(double(A.nodes(l)), ld_ref, kc);
     require(ld_ref >= kc, "qr_r_only_batched: requires rows >= cols");
     if (kc == 0) continue;
-    struct {
-      double* p;
-    } Pbuf{Pall};
     const int64_t r0 = A.own_begin(l), nn = A.own_count(l);  // r0 is even unless l == s (one node)
-    if (kp > 0 && nn > 0) {
+    if (nn == 0) continue;
+    if (kp > 0) {
       k_weights_parent<<<unsigned(nn), kThreads, 0, s>>>(
           A.transfer.p + A.tr_off[l] + (r0 - A.tr_begin(l)) * A.tr_stride(l), A.ld(l), kc, kp,
-          R.at(l - 1) + (r0 >> 1) * int64_t(kp) * kp, Pbuf.p);
+          R.at(l - 1) + (r0 >> 1) * int64_t(kp) * kp, Pall);
       H2B_CUDA(cudaGetLastError());
     }
-    if (nn == 0) continue;
+    const int lslots = weights_slots(A.device, kc);
+    int nseg = 1;
+    if (nn < lslots) nseg = int(std::min<int64_t>((lslots + nn - 1) / nn, std::max(1, L.max_row / 4)));
+    nseg = std::max(1, std::min(nseg, int(maxitems / std::max<int64_t>(1, nn))));
+    items.clear();
+    merge.clear();
+    for (int64_t i = 0; i < nn; ++i) {
+      const int32_t b0 = L.h_rp[r0 + i], b1 = L.h_rp[r0 + i + 1];
+      if (nseg == 1) {
+        items.push_back({int32_t(i), b0, b1, int32_t(i), 1});
+      } else {
+        for (int g = 0; g < nseg; ++g)
+          items.push_back({int32_t(i), b0 + int32_t((int64_t(b1 - b0) * g) / nseg),
+                           b0 + int32_t((int64_t(b1 - b0) * (g + 1)) / nseg), int32_t(i * nseg + g), g == 0});
+        merge.push_back({int32_t(i), int32_t(i * nseg), int32_t((i + 1) * nseg), int32_t(i), 0});
+      }
+    }
+    std::stable_sort(items.begin(), items.end(), [](const WItem& x, const WItem& y) {
+      return (x.b1 - x.b0) + x.par > (y.b1 - y.b0) + y.par;
+    });
+    H2B_CUDA(cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(WItem), cudaMemcpyHostToDevice, s));
+    H2B_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int), s));
+    if (!merge.empty())
+      H2B_CUDA(cudaMemcpyAsync(dmerge, merge.data(), merge.size() * sizeof(WItem), cudaMemcpyHostToDevice, s));
     constexpr int CR = 32;
     const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
-    // LPT order: nodes by decreasing stack height
-    struct {
-      int32_t* p;
-    } dord{dord_all + ooff[l]};  // [nn] = work counter
-    int dev_sms = 0;
-    H2B_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, A.device));
-#define H2B_WEIGHTS(NCOL)                                                                           \
-  if ((kc > 32 ? 2 : 1) == NCOL) {                                                                  \
-    set_smem(k_weights<NCOL, CR>, sm);                                                              \
-    int per_sm = 0;                                                                                 \
-    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<NCOL, CR>,            \
-                                                           32 * kWWarps, sm));                      \
-    const int64_t want = (nn + kWWarps - 1) / kWWarps;                                              \
-    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(dev_sms) * std::max(1, per_sm)))); \
-    k_weights<NCOL, CR><<<grid, 32 * kWWarps, sm, s>>>(Pbuf.p, kc, kp, L.rp + r0, L.val, L.ld,          \
-                                                       R.at(l) + r0 * int64_t(kc) * kc, nn,            \
-                                                       dord.p, reinterpret_cast<int*>(dord.p + nn)); \
-  }
-    H2B_WEIGHTS(1) H2B_WEIGHTS(2)
-#undef H2B_WEIGHTS
-    H2B_CUDA(cudaGetLastError());
+    double* Rl = R.at(l) + r0 * int64_t(kc) * kc;
+    auto launch = [&](const double* S, int lds, double* Rout, int out_t, const WItem* it, int64_t n, int* next) {
+      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((n + kWWarps - 1) / kWWarps,
+                                                                          lslots / kWWarps)));
+      if (kc > 32)
+        k_weights<2, CR><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, S, lds, Rout, out_t, it, n, next);
+      else
+        k_weights<1, CR><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, S, lds, Rout, out_t, it, n, next);
+      H2B_CUDA(cudaGetLastError());
+    };
+    if (nseg == 1) {
+      launch(L.val, L.ld, Rl, 0, ditems, int64_t(items.size()), counters);
+    } else {
+      launch(L.val, L.ld, segR, 1, ditems, int64_t(items.size()), counters);
+      launch(segR, kc, Rl, 0, dmerge, int64_t(merge.size()), counters + 1);
+    }
+    // the next level's uploads reuse the item buffers: keep stream order
+    H2B_CUDA(cudaStreamSynchronize(s));
   }
 }
 
