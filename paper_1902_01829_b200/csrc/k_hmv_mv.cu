@@ -43,12 +43,12 @@ struct Acc {
 
 // acc (M x 16) += op(A) (M x K) * B (K x 16), B vector-minor (B[p * 16 + v]).
 // op(A)(i, p) = TA ? A[p + i * lda] : A[i + p * lda]; A streamed (evict-first).
-template <bool TA>
+template <bool TA, int UNROLL = 2>
 __device__ __forceinline__ void mma_panel(Acc& acc, const double* __restrict__ A, int lda, int M,
                                           int K, const double* __restrict__ B) {
   const int lane = lane_id();
   const int fr = lane >> 2, fk = lane & 3;
-#pragma unroll 2
+#pragma unroll UNROLL
   for (int p0 = 0; p0 < K; p0 += 4) {
     const int p = p0 + fk;
     const bool pk = p < K;
@@ -145,7 +145,7 @@ struct LayerTableMV {
 };
 
 // Y_r = sum_b B_b X_{col(b)} for every work item (row of one layer).
-__global__ void __launch_bounds__(kThreads) k_bsr_mv(const __grid_constant__ LayerTableMV T,
+__global__ void __launch_bounds__(kThreads, 1) k_bsr_mv(const __grid_constant__ LayerTableMV T,
                                                      const uint32_t* __restrict__ work,
                                                      int64_t nwork) {
   for (int64_t it = warp_global(); it < nwork; it += warp_count()) {
@@ -157,8 +157,10 @@ __global__ void __launch_bounds__(kThreads) k_bsr_mv(const __grid_constant__ Lay
     acc.zero();
     for (int b = b0; b < b1; ++b) {
       const int col = __ldg(D.ci + b);
-      mma_panel<false>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc,
-                       D.x + int64_t(col) * D.bc * NV);
+      // 4 k-steps (32 fragment loads per lane) in flight: the block stream is
+      // latency-bound at 2
+      mma_panel<false, 8>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc,
+                          D.x + int64_t(col) * D.bc * NV);
     }
     store_panel(acc, D.y + int64_t(row) * D.br * NV, D.br, false);
   }
