@@ -52,6 +52,16 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def load_pipes():
+    """FP64 / DMMA pipe utilisation of the compression and 16-vector kernels
+    from the committed ncu captures (profiles/tensor_pipe.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "tensor_pipe.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def load_traffic():
     """dram bytes per k_bsr launch from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -222,7 +232,8 @@ def compression_run(h2, torch, device, reps):
                          "truncate": round(rep.time_truncate_ms, 1),
                          "project_trunc": round(rep.time_project_trunc_ms, 1)},
             "new_ranks": rep.new_ranks, "frobenius_error": rep.frobenius_error,
-            "bytes": [rep.bytes_before, rep.bytes_after]}
+            "bytes": [rep.bytes_before, rep.bytes_after],
+            "pipe_utilisation_ncu": (load_pipes() or {}).get("compression_C3")}
 
 
 def compression_run_dist(torch, device, reps, world):
@@ -286,7 +297,9 @@ def multi16_run(A, torch, steps):
     return {"vectors": 16, "ms_per_pass": round(ms, 3), "ms_per_vector": round(ms / 16, 4),
             "effective_GBs": round(16 * fp / ms / 1e6, 1),
             "matrix_stream_GBs": round(fp / ms / 1e6, 1),
-            "model_tflops": round(16 * flops / ms / 1e9, 2)}
+            "model_tflops": round(16 * flops / ms / 1e9, 2),
+            "pct_fp64_peak": round(100 * 16 * flops / ms / 1e9 / FP64_PEAK_TFLOPS, 2),
+            "pipe_utilisation_ncu": (load_pipes() or {}).get("multi16_C4")}
 
 
 def run_reference(args):
