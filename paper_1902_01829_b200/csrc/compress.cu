@@ -33,7 +33,7 @@ namespace {
 
 using cta::kThreads;
 
-constexpr int kXb = 2 * (4 * 32 + 8);  // cta::householder scratch (doubles)
+constexpr int kXb = cta::kHhScratch;  // cta::householder scratch (doubles)
 
 // ------------------------------------------------------------------ kernels
 __global__ void __launch_bounds__(kThreads) k_orth_leaf(double* __restrict__ leaf, int ldm, int m,
@@ -51,20 +51,22 @@ __global__ void __launch_bounds__(kThreads) k_orth_leaf(double* __restrict__ lea
   __syncthreads();
   cta::householder_regs<16>(A, m, m, k, tau, xb);  // m <= 64
   cta::extract_r(A, m, k, T + i * int64_t(k) * k, k, flip);
-  for (int e = threadIdx.x; e < k * k; e += kThreads) {
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     const int j = e / k, r = e - j * k;
     Q[r + j * m] = r == j ? 1.0 : 0.0;
   }
   __syncthreads();
   cta::apply_q_wy(A, m, m, k, tau, Q, m, k, Zw, /*y0_identity=*/true);  // Q = H_0..H_{k-1} [I; 0]
-  for (int e = threadIdx.x; e < m * k; e += kThreads) {
+  for (int e = threadIdx.x; e < m * k; e += blockDim.x) {
     const int j = e / m, r = e - j * m;
     U[r + int64_t(j) * ldm] = flip[j] ? -Q[r + j * m] : Q[r + j * m];
   }
 }
 
 // Parent p at level l-1: Z = [T_2p F_2p; T_2p+1 F_2p+1] (2kc x kp) -> QR.
-__global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F, int ldf, int kc,
+constexpr int kLevelThreads = 512;  // level QR kernels: 16 warps (one 164 KB CTA per SM)
+
+__global__ void __launch_bounds__(kLevelThreads) k_orth_level(double* __restrict__ F, int ldf, int kc,
                                                          int kp, const double* __restrict__ Tl,
                                                          double* __restrict__ Tp) {
   extern __shared__ double sm[];
@@ -82,9 +84,12 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
     cta::gemm_tc<false, false, 1>(Z + ci * kc, zr, Tl + c * int64_t(kc) * kc, kc, F + c * fs, ldf, kc, kp, kc);
   }
   __syncthreads();
-  cta::householder(Z, zr, zr, kp, tau, xb);
+  if (zr <= 64)
+    cta::householder_regs<8, 8>(Z, zr, zr, kp, tau, xb);
+  else
+    cta::householder_regs<16, 8>(Z, zr, zr, kp, tau, xb);  // zr <= 128
   cta::extract_r(Z, zr, kp, Tp + p * int64_t(kp) * kp, kp, flip);
-  for (int e = threadIdx.x; e < kp * kp; e += kThreads) {
+  for (int e = threadIdx.x; e < kp * kp; e += blockDim.x) {
     const int j = e / kp, r = e - j * kp;
     Q[r + j * zr] = r == j ? 1.0 : 0.0;
   }
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) k_orth_level(double* __restrict__ F,
   cta::apply_q_wy(Z, zr, zr, kp, tau, Q, zr, kp, Zw, /*y0_identity=*/true);
   for (int ci = 0; ci < 2; ++ci) {
     double* dst = F + (2 * p + ci) * fs;
-    for (int e = threadIdx.x; e < kc * kp; e += kThreads) {
+    for (int e = threadIdx.x; e < kc * kp; e += blockDim.x) {
       const int j = e / kc, r = e - j * kc;
       const double v = Q[ci * kc + r + j * zr];
       dst[r + int64_t(j) * ldf] = flip[j] ? -v : v;
@@ -212,7 +217,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // rows x cols block (ld lds, global) into a zero-padded 64 x 64 smem tile (ld kPLd)
 __device__ __forceinline__ void stage64(double* dst, const double* src, int lds, int rows, int cols) {
-  for (int e = threadIdx.x; e < 64 * 64; e += kThreads) {
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
     const int j = e >> 6, i = e & 63;
     if (i < rows && j < cols)
       cp_async8(dst + i + j * kPLd, src + i + int64_t(j) * lds);
@@ -505,53 +510,53 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
 struct SvdScratch {
   double tau[64];
   double tau2[64];
-  double xb[2 * (4 * 32 + 8)];  // householder publish slots
+  double xb[cta::kHhScratch];  // householder publish slots
 };
 constexpr int kSvdScratch = int((sizeof(SvdScratch) + 15) / 16) * 2;  // in doubles, 16 B aligned
 
 // Stage A on W (rows x cols, smem, ld rows; destroyed).  X: smem >= s*s and
 // >= cols*rows.  Writes J (s x s, ld s) and, when tall, the factored Q1 (V:
 // rows x cols, ld rows; tau: cols) to global.
-template <int RQW>  // register rows per thread of W's QR (rows <= 4 RQW)
+template <int RQW, int G>  // W's QR: G threads per column, RQW rows each (rows <= G RQW)
 __device__ void svd_precondition(double* W, int rows, int cols, double* X, double* J, double* V,
                                  double* tau, SvdScratch& sc) {
   const int s = rows < cols ? rows : cols;
   if (s == 0) return;
   if (rows >= cols) {
     const int c = cols;
-    cta::householder_regs<RQW>(W, rows, rows, c, sc.tau, sc.xb);
-    for (int e = threadIdx.x; e < rows * c; e += kThreads) V[e] = W[e];
-    for (int j = threadIdx.x; j < c; j += kThreads) tau[j] = sc.tau[j];
+    cta::householder_regs<RQW, G>(W, rows, rows, c, sc.tau, sc.xb);
+    for (int e = threadIdx.x; e < rows * c; e += blockDim.x) V[e] = W[e];
+    for (int j = threadIdx.x; j < c; j += blockDim.x) tau[j] = sc.tau[j];
     // X = R1^T (c x c, lower), then QR of it: R2 in the upper triangle
-    for (int e = threadIdx.x; e < c * c; e += kThreads) {
+    for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
       const int j = e / c, i = e - j * c;
       X[i + j * c] = i >= j ? W[j + i * rows] : 0.0;
     }
     __syncthreads();
-    cta::householder_regs<16>(X, c, c, c, sc.tau2, sc.xb);
-    for (int e = threadIdx.x; e < c * c; e += kThreads) {  // J = R2^T
+    cta::householder_regs<64 / G, G>(X, c, c, c, sc.tau2, sc.xb);
+    for (int e = threadIdx.x; e < c * c; e += blockDim.x) {  // J = R2^T
       const int j = e / c, i = e - j * c;
       J[i + j * c] = i >= j ? X[j + i * c] : 0.0;
     }
   } else {
     const int r = rows;
-    double* G = X;  // W^T (cols x r)
-    for (int e = threadIdx.x; e < cols * r; e += kThreads) {
+    double* Gt = X;  // W^T (cols x r)
+    for (int e = threadIdx.x; e < cols * r; e += blockDim.x) {
       const int j = e / cols, i = e - j * cols;
-      G[i + j * cols] = W[j + i * rows];
+      Gt[i + j * cols] = W[j + i * rows];
     }
     __syncthreads();
-    cta::householder_regs<16>(G, cols, cols, r, sc.tau, sc.xb);  // cols <= 64 rows
-    for (int e = threadIdx.x; e < r * r; e += kThreads) {  // J = R1^T
+    cta::householder_regs<64 / G, G>(Gt, cols, cols, r, sc.tau, sc.xb);  // cols <= 64 rows
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {  // J = R1^T
       const int j = e / r, i = e - j * r;
-      J[i + j * r] = i >= j ? G[j + i * cols] : 0.0;
+      J[i + j * r] = i >= j ? Gt[j + i * cols] : 0.0;
     }
   }
   __syncthreads();
 }
 
 __device__ void check_finite(const double* W, int n, int* bad) {
-  for (int e = threadIdx.x; e < n; e += kThreads)
+  for (int e = threadIdx.x; e < n; e += blockDim.x)
     if (!isfinite(W[e])) *bad = 1;
 }
 
@@ -569,11 +574,11 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_pre(const double* __res
   cta::gemm_tc<false, true, 2>(W, m, leaf + i * int64_t(ldm) * k, ldm, R + i * int64_t(k) * k, k, m, k, k);
   __syncthreads();
   check_finite(W, m * k, bad);
-  svd_precondition<16>(W, m, k, X, Jout + i * int64_t(s) * s, Vout + i * int64_t(m) * k, tauout + i * 64, sc);
+  svd_precondition<16, 4>(W, m, k, X, Jout + i * int64_t(s) * s, Vout + i * int64_t(m) * k, tauout + i * 64, sc);
 }
 
 // Stage A, parent p: Z = [Tt_c E_c] (2kt_c x kp), W = Z R^{l-1,T} (:327-376).
-__global__ void __launch_bounds__(kThreads) k_trunc_level_pre(
+__global__ void __launch_bounds__(kLevelThreads) k_trunc_level_pre(
     const double* __restrict__ E, int lde, int kc, int kp, int ktc, const double* __restrict__ Tt,
     const double* __restrict__ Rp, double* __restrict__ Zout, double* __restrict__ Jout,
     double* __restrict__ Vout, double* __restrict__ tauout, int* __restrict__ bad) {
@@ -595,9 +600,9 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_pre(
   __syncthreads();
   check_finite(W, zr * kp, bad);
   if (zr <= 64)
-    svd_precondition<16>(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
+    svd_precondition<8, 8>(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
   else
-    svd_precondition<32>(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
+    svd_precondition<16, 8>(W, zr, kp, X, Jout + p * int64_t(s) * s, Vout + p * int64_t(zr) * kp, tauout + p * 64, sc);
 }
 
 // Stage B: one-sided Jacobi on J (r x r, r <= 64), one 64-thread CTA per
@@ -728,8 +733,8 @@ __global__ void __launch_bounds__(kThreads) k_svd_apply(const double* __restrict
   double* tau = Zw + c * c;  // 64
   const int64_t i = blockIdx.x;
   const double* Vg = Vall + i * int64_t(rows) * c;
-  for (int e = threadIdx.x; e < rows * c; e += kThreads) V[e] = Vg[e];
-  for (int j = threadIdx.x; j < c; j += kThreads) tau[j] = tauall[i * 64 + j];
+  for (int e = threadIdx.x; e < rows * c; e += blockDim.x) V[e] = Vg[e];
+  for (int j = threadIdx.x; j < c; j += blockDim.x) tau[j] = tauall[i * 64 + j];
   __syncthreads();
   cta::apply_q_wy(V, rows, rows, c, tau, Uall + i * int64_t(rows) * c, rows, c, Zw);
 }
@@ -747,7 +752,7 @@ __global__ void __launch_bounds__(kThreads) k_trunc_leaf_apply(const double* __r
   if (kt > 0)
     cta::gemm_tc<true, false>(Tq + i * int64_t(kt) * k, kt, Q, m, leaf + i * int64_t(ldm) * k, ldm, kt, k, m);
   double* nl = newleaf + i * int64_t(ldn) * kt;
-  for (int e = threadIdx.x; e < ldn * kt; e += kThreads) {
+  for (int e = threadIdx.x; e < ldn * kt; e += blockDim.x) {
     const int j = e / ldn, r = e - j * ldn;
     nl[e] = r < m ? Q[r + int64_t(j) * m] : 0.0;
   }
@@ -771,7 +776,7 @@ __global__ void __launch_bounds__(kThreads) k_trunc_level_apply(
                            kp, zr);
   for (int ci = 0; ci < 2; ++ci) {
     double* dst = Enew + (2 * p + ci) * int64_t(ldn) * ktp;
-    for (int e = threadIdx.x; e < ldn * ktp; e += kThreads) {
+    for (int e = threadIdx.x; e < ldn * ktp; e += blockDim.x) {
       const int j = e / ldn, r = e - j * ldn;
       dst[e] = r < ktc ? Q[ci * ktc + r + int64_t(j) * zr] : 0.0;
     }
@@ -972,7 +977,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
     set_smem(k_orth_level, sm);
     // parents [p0, p1) at level l-1; children 2p0.. in the (local) transfer pool
     const int64_t p0 = A.own_begin(l - 1), p1 = A.own_end(l - 1);
-    k_orth_level<<<unsigned(p1 - p0), kThreads, sm, s>>>(
+    k_orth_level<<<unsigned(p1 - p0), kLevelThreads, sm, s>>>(
         A.transfer.p + A.tr_off[l] + (2 * p0 - A.tr_begin(l)) * A.tr_stride(l), A.ld(l), kc, kp,
         T.at(l) + 2 * p0 * int64_t(kc) * kc, T.at(l - 1) + p0 * int64_t(kp) * kp);
     H2B_CUDA(cudaGetLastError());
@@ -1391,7 +1396,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
       const size_t sm = (kSvdScratch + size_t(zr) * kp + size_t(std::max(sl * sl, kp * zr))) * sizeof(double);
       check_smem(sm, "truncate_basis");
       set_smem(k_trunc_level_pre, sm);
-      k_trunc_level_pre<<<unsigned(npo), kThreads, sm, s>>>(
+      k_trunc_level_pre<<<unsigned(npo), kLevelThreads, sm, s>>>(
           A.transfer.p + A.tr_off[l] + (2 * p0 - A.tr_begin(l)) * es, A.ld(l), kc, kp, ktc,
           Tt.at(l) + 2 * p0 * int64_t(ktc) * kc, R.at(l - 1) + p0 * int64_t(kp) * kp, Z, Js, Vs, ts, dk + 1);
       H2B_CUDA(cudaGetLastError());

@@ -25,6 +25,8 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ int lane() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int nthreads() { return blockDim.x; }
+__device__ __forceinline__ int nwarps() { return blockDim.x >> 5; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -32,32 +34,32 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Deterministic CTA-wide sum; `red` is >= 9 doubles of scratch smem.
+// Deterministic CTA-wide sum; `red` is >= nwarps() + 1 doubles of scratch smem.
 __device__ __forceinline__ double cta_sum(double v, double* red) {
   v = warp_sum(v);
   __syncthreads();
   if (lane() == 0) red[warp()] = v;
   __syncthreads();
   if (warp() == 0) {
-    double t = lane() < kWarps ? red[lane()] : 0.0;
+    double t = lane() < nwarps() ? red[lane()] : 0.0;
     t = warp_sum(t);
-    if (lane() == 0) red[kWarps] = t;
+    if (lane() == 0) red[nwarps()] = t;
   }
   __syncthreads();
-  return red[kWarps];
+  return red[nwarps()];
 }
 
 // Copy a rows x cols block between column-major buffers (global or smem).
 __device__ __forceinline__ void copy_block(double* dst, int ldd, const double* src, int lds,
                                           int rows, int cols) {
-  for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
+  for (int e = threadIdx.x; e < rows * cols; e += nthreads()) {
     const int j = e / rows, i = e - j * rows;
     dst[i + j * ldd] = src[i + j * lds];
   }
 }
 
 __device__ __forceinline__ void zero_block(double* dst, int ldd, int rows, int cols) {
-  for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
+  for (int e = threadIdx.x; e < rows * cols; e += nthreads()) {
     const int j = e / rows, i = e - j * rows;
     dst[i + j * ldd] = 0.0;
   }
@@ -132,7 +134,7 @@ __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const doub
   const int t = lane();
   const int fr = t >> 2, fk = t & 3;  // fragment row (A) / col (B), k index
   const int mt = (m + 31) >> 5, nt = (n + 15) >> 4;
-  for (int wt = warp(); wt < mt * nt; wt += kWarps) {
+  for (int wt = warp(); wt < mt * nt; wt += nwarps()) {
     const int i0 = (wt % mt) * 32, j0 = (wt / mt) * 16;
     double acc[4][2][2];
 #pragma unroll
@@ -193,22 +195,30 @@ __device__ void gemm_tc(double* C, int ldc, const double* A, int lda, const doub
 
 // In-place Householder factorisation (linalg.hpp:48-75): reflectors below the
 // diagonal, R on and above it; tau[cols] in smem.  Register-resident: thread
-// (c = tid / 4, quarter = tid % 4) of the 256-thread CTA holds rows
-// [quarter RQ, (quarter + 1) RQ) of column c (cols <= 64, rows <= 4 RQ).  For
+// (c = tid / G, group = tid % G) of the 64 G-thread CTA holds rows
+// [group RQ, (group + 1) RQ) of column c (cols <= 64, rows <= G RQ).  For
 // reflector j the owner column publishes its RAW entries below the diagonal
 // (and alpha = A[j,j], the squared norm partials) to shared memory; every
 // column then forms the Householder scalars itself -- sqrt and one division,
-// in parallel with its dot product (2 quad shuffles) -- and updates its own
+// in parallel with its dot product (log2 G shuffles) -- and updates its own
 // registers.  One barrier per reflector (double-buffered publish slot).
+// Group g's rows sit at x[g XQ + i]: XQ is padded so that the G groups of a
+// warp (same i) read disjoint banks with 128-bit loads (a stride of RQ
+// doubles puts them all in one bank).
 // Same arithmetic as the reference: beta = -sign(alpha) ||x||,
 // tau = (beta - alpha) / beta, v = x / (alpha - beta), zero column -> tau = 0.
-// xb: smem scratch, >= 2 * (4 RQ + 8) doubles.
-template <int RQ>
+// xb: smem scratch, >= kHhScratch doubles (aligned to 16 bytes here).
+constexpr int kHhScratch = 2 * (144 + 16) + 2;
+template <int RQ, int G = 4>
 __device__ void householder_regs(double* A, int lda, int rows, int cols, double* tau, double* xb) {
-  constexpr int XS = 4 * RQ + 8;
-  const int c = threadIdx.x >> 2, qd = threadIdx.x & 3;
+  static_assert((G == 4 && (RQ == 16 || RQ == 32)) || (G == 8 && (RQ == 8 || RQ == 16)), "householder_regs");
+  constexpr int XQ = G == 8 ? RQ + 2 : RQ + 4;
+  constexpr int XS = G * XQ + 16;
+  static_assert(2 * XS + 2 <= kHhScratch, "householder_regs: scratch");
+  xb = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(xb) + 15) & ~uintptr_t(15));
+  const int c = threadIdx.x / G, qd = threadIdx.x % G;
   const int r0 = qd * RQ;
-  const unsigned qmask = 0xfu << (lane() & 28);
+  const unsigned qmask = ((1u << G) - 1u) << (lane() & ~(G - 1));
   const bool live = c < cols;
   double col[RQ];
 #pragma unroll
@@ -221,20 +231,31 @@ __device__ void householder_regs(double* A, int lda, int rows, int cols, double*
       const int j = jb * RQ + jj;
       if (j >= steps) break;  // uniform
       double* x = xb + (j & 1) * XS;
+      const double* xq = x + qd * XQ;  // this group's rows
       if (c == j) {  // owner: publish raw x (rows > j), alpha, norm^2 partial
         double q2 = 0.0;
 #pragma unroll
-        for (int i = 0; i < RQ; ++i) {
-          const double v = (r0 + i > j) ? col[i] : 0.0;
-          x[r0 + i] = v;
-          q2 = fma(v, v, q2);
+        for (int i = 0; i < RQ; i += 2) {
+          const double v0 = (r0 + i > j) ? col[i] : 0.0;
+          const double v1 = (r0 + i + 1 > j) ? col[i + 1] : 0.0;
+          *reinterpret_cast<double2*>(x + qd * XQ + i) = make_double2(v0, v1);
+          q2 = fma(v0, v0, q2);
+          q2 = fma(v1, v1, q2);
         }
-        x[4 * RQ + qd] = q2;
-        if (qd == jb) x[4 * RQ + 4] = col[jj];
+        x[G * XQ + qd] = q2;
+        if (qd == jb) x[G * XQ + 8] = col[jj];
       }
       __syncthreads();
-      const double al = x[4 * RQ + 4];
-      const double nx = sqrt(fma(al, al, (x[4 * RQ] + x[4 * RQ + 1]) + (x[4 * RQ + 2] + x[4 * RQ + 3])));
+      const double al = x[G * XQ + 8];
+      double qs;
+      {
+        const double* qp = x + G * XQ;
+        if (G == 8)
+          qs = ((qp[0] + qp[1]) + (qp[2] + qp[3])) + ((qp[4] + qp[5]) + (qp[6] + qp[7]));
+        else
+          qs = (qp[0] + qp[1]) + (qp[2] + qp[3]);
+      }
+      const double nx = sqrt(fma(al, al, qs));
       if (nx != 0.0) {
         const double be = al >= 0.0 ? -nx : nx;
         const double am = al - be;
@@ -245,27 +266,32 @@ __device__ void householder_regs(double* A, int lda, int rows, int cols, double*
           for (int i = 0; i < RQ; ++i)
             if (r0 + i > j) col[i] *= sc;
           if (qd == jb) col[jj] = be;
-          if (threadIdx.x == 4 * j) tau[j] = -(am * am) * rr;
+          if (threadIdx.x == G * j) tau[j] = -(am * am) * rr;
         } else if (c > j && live) {
           double w0 = 0.0, w1 = 0.0;
 #pragma unroll
           for (int i = 0; i < RQ; i += 2) {
-            w0 = fma(x[r0 + i], col[i], w0);
-            w1 = fma(x[r0 + i + 1], col[i + 1], w1);
+            const double2 xx = *reinterpret_cast<const double2*>(xq + i);
+            w0 = fma(xx.x, col[i], w0);
+            w1 = fma(xx.y, col[i + 1], w1);
           }
           double w = w0 + w1;
-          w += __shfl_xor_sync(qmask, w, 1);
-          w += __shfl_xor_sync(qmask, w, 2);
-          // column c's entry in row j lives in quarter jb
-          const double cj = __shfl_sync(qmask, col[jj], (lane() & 28) | jb);
+#pragma unroll
+          for (int o = 1; o < G; o <<= 1) w += __shfl_xor_sync(qmask, w, o);
+          // column c's entry in row j lives in group jb
+          const double cj = __shfl_sync(qmask, col[jj], (lane() & ~(G - 1)) | jb);
           const double d = fma(sc, w, cj) * (-(am * am) * rr);
           const double f = sc * d;
           asm volatile("" ::: "memory");  // re-read x: RQ registers saved
 #pragma unroll
-          for (int i = 0; i < RQ; ++i) col[i] = fma(-x[r0 + i], f, col[i]);
+          for (int i = 0; i < RQ; i += 2) {
+            const double2 xx = *reinterpret_cast<const double2*>(xq + i);
+            col[i] = fma(-xx.x, f, col[i]);
+            col[i + 1] = fma(-xx.y, f, col[i + 1]);
+          }
           if (qd == jb) col[jj] -= d;
         }
-      } else if (threadIdx.x == 4 * j) {
+      } else if (threadIdx.x == G * j) {
         tau[j] = 0.0;
       }
     }
@@ -292,7 +318,7 @@ __device__ inline void householder(double* A, int lda, int rows, int cols, doubl
 // householder().  nrm: cols doubles, red: >= 16 doubles, sel: 1 int (smem).
 __device__ void qrcp(double* A, int lda, int rows, int cols, double* tau, int* perm, double* nrm,
                      double* red, int* sel) {
-  for (int kk = warp(); kk < cols; kk += kWarps) {
+  for (int kk = warp(); kk < cols; kk += nwarps()) {
     const double* w = A + kk * lda;
     double t = 0.0;
     for (int i = lane(); i < rows; i += 32) t = fma(w[i], w[i], t);
@@ -329,7 +355,7 @@ __device__ void qrcp(double* A, int lda, int rows, int cols, double* tau, int* p
     if (pj != j) {
       double* a = A + j * lda;
       double* b = A + pj * lda;
-      for (int i = threadIdx.x; i < rows; i += kThreads) {
+      for (int i = threadIdx.x; i < rows; i += nthreads()) {
         const double t = a[i];
         a[i] = b[i];
         b[i] = t;
@@ -356,13 +382,13 @@ __device__ void qrcp(double* A, int lda, int rows, int cols, double* tau, int* p
     const double tj = (be - al) / be;
     const double sc = 1.0 / (al - be);
     __syncthreads();  // everyone has read v[j]
-    for (int i = j + 1 + threadIdx.x; i < rows; i += kThreads) v[i] *= sc;
+    for (int i = j + 1 + threadIdx.x; i < rows; i += nthreads()) v[i] *= sc;
     if (threadIdx.x == 0) {
       v[j] = be;
       tau[j] = tj;
     }
     __syncthreads();
-    for (int kk = j + 1 + warp(); kk < cols; kk += kWarps) {
+    for (int kk = j + 1 + warp(); kk < cols; kk += nwarps()) {
       double* w = A + kk * lda;
       double s = 0.0;
       for (int i = j + 1 + lane(); i < rows; i += 32) s = fma(v[i], w[i], s);
@@ -391,7 +417,7 @@ __device__ void apply_q(const double* A, int lda, int rows, int k, const double*
     const double tj = tau[j];
     if (tj == 0.0) continue;
     const double* v = A + j * lda;
-    for (int kk = warp(); kk < ncols; kk += kWarps) {
+    for (int kk = warp(); kk < ncols; kk += nwarps()) {
       double* w = Y + kk * ldy;
       double s = 0.0;
       for (int i = j + 1 + lane(); i < rows; i += 32) s = fma(v[i], w[i], s);
@@ -419,14 +445,14 @@ __device__ void apply_q_wy(double* A, int lda, int rows, int k, const double* ta
   // first (A's upper triangle is still being read as structural zeros)
   gemm_tc<true, false, 0, 3>(Zw, k, A, lda, A, lda, k, k, rows);
   __syncthreads();
-  for (int e = threadIdx.x; e < k * k; e += kThreads) {
+  for (int e = threadIdx.x; e < k * k; e += nthreads()) {
     const int j = e / k, i = e - j * k;
     if (i < j) A[i + j * lda] = Zw[i + j * k];
   }
   __syncthreads();
   // Z = V(0:k, :)^T Y0  (Y0 = I: Z = V(0:k, :)^T, unit upper triangular)
   if (y0_identity) {
-    for (int e = threadIdx.x; e < k * ncols; e += kThreads) {
+    for (int e = threadIdx.x; e < k * ncols; e += nthreads()) {
       const int j = e / k, i = e - j * k;
       Zw[i + j * k] = j > i ? A[j + i * lda] : (i == j ? 1.0 : 0.0);
     }
@@ -438,7 +464,7 @@ __device__ void apply_q_wy(double* A, int lda, int rows, int k, const double* ta
   // i = t (mod 4) and keeps their running sums s_i = sum_{j > i} G_ij W_j
   {
     const int q4 = threadIdx.x & 3;
-    for (int col = threadIdx.x >> 2; col < ncols; col += kThreads / 4) {
+    for (int col = threadIdx.x >> 2; col < ncols; col += nthreads() / 4) {
       double* z = Zw + col * k;
       double sacc[16];
 #pragma unroll
@@ -473,7 +499,7 @@ __device__ void apply_q_wy(double* A, int lda, int rows, int k, const double* ta
 // Thin Q (rows x cols) from the factored form (linalg.hpp:77-98).
 __device__ void form_q(const double* A, int lda, int rows, int cols, const double* tau,
                        double* Q, int ldq) {
-  for (int e = threadIdx.x; e < rows * cols; e += kThreads) {
+  for (int e = threadIdx.x; e < rows * cols; e += nthreads()) {
     const int j = e / rows, i = e - j * rows;
     Q[i + j * ldq] = i == j ? 1.0 : 0.0;
   }
@@ -482,7 +508,7 @@ __device__ void form_q(const double* A, int lda, int rows, int cols, const doubl
     const double tj = tau[j];
     if (tj == 0.0) continue;
     const double* v = A + j * lda;
-    for (int kk = j + warp(); kk < cols; kk += kWarps) {
+    for (int kk = j + warp(); kk < cols; kk += nwarps()) {
       double* w = Q + kk * ldq;
       double s = 0.0;
       for (int i = j + 1 + lane(); i < rows; i += 32) s += v[i] * w[i];
@@ -499,9 +525,9 @@ __device__ void form_q(const double* A, int lda, int rows, int cols, const doubl
 // R (cols x cols, non-negative diagonal) to R_out; flip[j] (smem ints) marks
 // negated rows (linalg.hpp:100-113).
 __device__ void extract_r(const double* A, int lda, int cols, double* R, int ldr, int* flip) {
-  for (int j = threadIdx.x; j < cols; j += kThreads) flip[j] = A[j + j * lda] < 0.0;
+  for (int j = threadIdx.x; j < cols; j += nthreads()) flip[j] = A[j + j * lda] < 0.0;
   __syncthreads();
-  for (int e = threadIdx.x; e < cols * cols; e += kThreads) {
+  for (int e = threadIdx.x; e < cols * cols; e += nthreads()) {
     const int j = e / cols, i = e - j * cols;
     const double v = i <= j ? A[i + j * lda] : 0.0;
     R[i + j * ldr] = flip[i] ? -v : v;
@@ -544,7 +570,7 @@ __device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag, int row
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int r = 0; r < n - 1; ++r) {
-      for (int s = slot0; s < n / 2; s += kWarps * 4) {
+      for (int s = slot0; s < n / 2; s += nwarps() * 4) {
         int p, q;
         rr_pair(n, r, s, p, q);
         double* gp = G + p * ldg;
@@ -619,22 +645,22 @@ __device__ inline void jacobi(double* G, int ldg, int rows, int n, int* flag, in
 // zero) columns.  nrm/ord: smem scratch of n doubles / ints.
 __device__ void jacobi_finish(const double* G, int ldg, int rows, int n, int s, double* U, int ldu,
                               double* sigma, double* nrm, int* ord) {
-  for (int j = warp(); j < n; j += kWarps) {
+  for (int j = warp(); j < n; j += nwarps()) {
     double t = 0.0;
     for (int i = lane(); i < rows; i += 32) t += G[i + j * ldg] * G[i + j * ldg];
     t = warp_sum(t);
     if (lane() == 0) nrm[j] = sqrt(t);
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < n; j += kThreads) {
+  for (int j = threadIdx.x; j < n; j += nthreads()) {
     int rank = 0;
     const double v = nrm[j];
     for (int i = 0; i < n; ++i) rank += (nrm[i] > v) || (nrm[i] == v && i < j);
     ord[rank] = j;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < s; j += kThreads) sigma[j] = nrm[ord[j]];
-  for (int e = threadIdx.x; e < rows * s; e += kThreads) {
+  for (int j = threadIdx.x; j < s; j += nthreads()) sigma[j] = nrm[ord[j]];
+  for (int e = threadIdx.x; e < rows * s; e += nthreads()) {
     const int j = e / rows, i = e - j * rows;
     const int src = ord[j];
     const double nv = nrm[src];
