@@ -267,6 +267,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   }
 }
 
+// nb blocks of bs_new doubles from stride bs_old to stride bs_new (the
+// compaction of the coupling pool after the truncation; cudaMemcpy2D moves
+// these ~10 KB rows at a fraction of the copy bandwidth).  Ranges of one
+// launch never overlap (the host chunks the pool so).  All sizes even.
+__global__ void __launch_bounds__(kThreads) k_compact(double* __restrict__ dst, const double* __restrict__ src,
+                                                      int64_t bs_new, int64_t bs_old, int64_t nb) {
+  const int64_t h = bs_new >> 1;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const double2* s = reinterpret_cast<const double2*>(src + b * bs_old);
+    double2* d = reinterpret_cast<double2*>(dst + b * bs_new);
+    for (int64_t e = threadIdx.x; e < h; e += kThreads) __stcs(d + e, __ldcs(s + e));
+  }
+}
+
 __global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restrict__ part) {
   __shared__ double red[16];
   double s = 0.0;
@@ -1085,14 +1099,17 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
         // chunks that fit in it are copied directly, the rest through temp
         const int64_t gap = (old_off + b0 * bs_old) - (new_off[l] + b0 * bs_new);
         int64_t nb = std::min(L.nb - b0, gap / bs_new);
+        auto move = [&](double* d, const double* sp, int64_t so, int64_t cnt) {
+          const unsigned grid = unsigned(std::min<int64_t>(cnt, 148 * 8));
+          k_compact<<<grid, kThreads, 0, s>>>(d, sp, bs_new, so, cnt);
+          H2B_CUDA(cudaGetLastError());
+        };
         if (nb >= 1) {
-          H2B_CUDA(cudaMemcpy2DAsync(dst, bs_new * sizeof(double), src, bs_old * sizeof(double),
-                                     bs_new * sizeof(double), nb, cudaMemcpyDeviceToDevice, s));
+          move(dst, src, bs_old, nb);
         } else {
           nb = std::min(per, L.nb - b0);
-          H2B_CUDA(cudaMemcpy2DAsync(temp, bs_new * sizeof(double), src, bs_old * sizeof(double),
-                                     bs_new * sizeof(double), nb, cudaMemcpyDeviceToDevice, s));
-          H2B_CUDA(cudaMemcpyAsync(dst, temp, nb * bs_new * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          move(temp, src, bs_old, nb);
+          move(dst, temp, bs_new, nb);
         }
         b0 += nb;
       }

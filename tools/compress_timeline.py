@@ -1,6 +1,6 @@
 """Kernel timeline (CUPTI via torch.profiler) of compress() runs: per-run
 kernel-busy time vs the phase times, and the largest idle gaps.
-    python tools/compress_timeline.py DIM N ORDER EPS REPS"""
+    python tools/compress_timeline.py DIM N ORDER EPS REPS [seq]"""
 import json
 import sys
 
@@ -36,5 +36,11 @@ for _ in range(reps):
                           gaps_over_1ms=big, gap_total_ms=round(sum(g for g, _, _ in gaps), 1),
                           top_kernels=[(round(t, 2), k) for t, k in slow],
                           per_kernel={k: round(v, 1) for k, v in sorted(agg.items(), key=lambda kv: -kv[1])})), flush=True)
+    if len(sys.argv) > 6:  # every launch in order: name, ms
+        seq = []
+        for e in ev:
+            k = e.name.replace("h2b::(anonymous namespace)::", "").replace("void ", "").split("(")[0][:24]
+            seq.append(f"{k}:{e.time_range.elapsed_us() / 1e3:.2f}")
+        print(" ".join(seq), flush=True)
     A.close()
     del A
