@@ -124,6 +124,7 @@ struct ProjTable {
   ProjLevel L[kMaxLevels + 1];
   int tri;          // T upper triangular (orthogonalization's R factors)
   double* rowsum;   // per block row: sum of squares of the projected blocks (or null)
+  int max_row;      // longest block row over the levels (smem work list)
 };
 
 // S_b <- T_row S_b T_col^T for every block of one block row (compression.hpp:160-168),
@@ -135,17 +136,15 @@ struct ProjTable {
 // With TRI (orthogonalization: T are upper-triangular R factors) the
 // structurally zero fragments of both products are skipped.
 constexpr int kPLd = 68;  // smem leading dimension (== 4 mod 16: conflict-free fragments)
+// TS strip = Tr[i0:i0+8, :] S (8 x ro) of warp w, i0 = 8w (false: idle warp).
 template <bool TRI>
-__device__ __forceinline__ void project_block(const double* Tr, const double* Sb, const double* Tc, double* out,
-                                              double* outT, int ld_new, int ro, int rn, double& sumsq) {
+__device__ __forceinline__ bool ts_strip(const double* Tr, const double* Sb, int ro, int rn, double (&acc)[8][2]) {
   const int w = cta::warp(), t = cta::lane();
   const int fr = t >> 2, fk = t & 3;
   const int i0 = 8 * w;
-  if (i0 >= rn) return;
-  // ---- TS strip = Tr[i0:i0+8, :] S (8 x ro), 8 column tiles ----
-  double acc[8][2];
 #pragma unroll
   for (int y = 0; y < 8; ++y) acc[y][0] = acc[y][1] = 0.0;
+  if (i0 >= rn) return false;
   const int kc_end = (ro + 3) >> 2;
 #pragma unroll
   for (int kc = 0; kc < 16; ++kc) {
@@ -161,7 +160,18 @@ __device__ __forceinline__ void project_block(const double* Tr, const double* Sb
       }
     }
   }
-  // ---- out strip = TS strip (8 x ro) T_col^T (ro x rn) ----
+  return true;
+}
+
+// out strip = TS strip (8 x ro) T_col^T (ro x rn); TS's A fragments come from
+// the accumulators by two quad shuffles per k-step (TS never touches smem).
+template <bool TRI>
+__device__ __forceinline__ void out_strip(const double (&acc)[8][2], const double* Tc, double* out, double* outT,
+                                          int ld_new, int ro, int rn, double& sumsq) {
+  const int w = cta::warp(), t = cta::lane();
+  const int fr = t >> 2, fk = t & 3;
+  const int i0 = 8 * w;
+  const int kc_end = (ro + 3) >> 2;
   double o[8][2];
 #pragma unroll
   for (int y = 0; y < 8; ++y) o[y][0] = o[y][1] = 0.0;
@@ -242,6 +252,17 @@ __device__ __forceinline__ void stage64(double* dst, const double* src, int lds,
   }
 }
 
+// S_b <- T_row S_b T_col^T for every block of one block row (compression.hpp:
+// 160-168), ranks <= 64.  T_row stays in smem for the row; per block, S_b and
+// T_col are staged in smem by cp.async and warp w computes the 8-row strip
+// [8w, 8w+8) of TS = T_row S_b (DMMA, accumulators in registers) and then of
+// out = TS T_col^T.  Software pipeline over the row's blocks with single
+// buffers: S_{b+1} is loaded while out_b is computed (S_b is dead by then) and
+// T_col,{b+1} while TS_{b+1} is computed.  With TRI (orthogonalization: T are
+// upper-triangular R factors) the structurally zero fragments are skipped.
+// The row's work list (symmetric levels: upper blocks only, each also writing
+// its mirror) is compacted into smem first: no dependent global index loads
+// between blocks.
 __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__ ProjTable P,
                                                          const ProjRow* __restrict__ rows) {
   extern __shared__ double sm[];
@@ -251,29 +272,74 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   double* Tr = sm;                // rn x ro
   double* Sb = Tr + 64 * kPLd;    // ro x ro
   double* Tc = Sb + 64 * kPLd;    // rn x ro
+  int* wcnt = reinterpret_cast<int*>(Tc + 64 * kPLd);  // kWarps
+  int* blist = wcnt + 32;  // blocks to project
+  int* clist = blist + P.max_row;  // their block columns
+  int* mlist = clist + P.max_row;  // their mirror block (or -1)
   stage64(Tr, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
   const int b0 = L.rp[pr.row], b1 = L.rp[pr.row + 1];
-  double ss = 0.0;
-  for (int b = b0; b < b1; ++b) {
-    // symmetric level: (col, row) is the transpose of (row, col); the upper
-    // block computes both (S_ji' = T_j S_ij^T T_i^T = (T_i S_ij T_j^T)^T)
-    const int mb = L.mirror ? L.mirror[b] : -1;
-    if (L.mirror && L.ci[b] < pr.row && mb >= 0) continue;
-    __syncthreads();  // previous block done with Sb / Tc
-    stage64(Sb, L.S + int64_t(b) * L.ld_old * ro, L.ld_old, ro, ro);
-    stage64(Tc, L.T + int64_t(L.ci[b]) * rn * ro, rn, rn, ro);
-    cp_async_commit();
-    cp_async_wait<0>();
+  // ---- ordered compaction of the row's work list ----
+  int nk = 0;
+  for (int base = b0; base < b1; base += kThreads) {
+    const int b = base + threadIdx.x;
+    bool keep = false;
+    int c = 0, mb = -1;
+    if (b < b1) {
+      c = L.ci[b];
+      mb = L.mirror ? L.mirror[b] : -1;
+      // symmetric level: (col, row) is the transpose of (row, col); the upper
+      // block computes both (S_ji' = T_j S_ij^T T_i^T = (T_i S_ij T_j^T)^T)
+      keep = !(L.mirror && c < pr.row && mb >= 0);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (cta::lane() == 0) wcnt[cta::warp()] = __popc(bal);
     __syncthreads();
-    double* out = L.out + int64_t(b) * L.ostride;
-    double* outT = (mb >= 0 && L.ci[b] > pr.row) ? L.out + int64_t(mb) * L.ostride : nullptr;
-    double s1 = 0.0;
-    if (P.tri)
-      project_block<true>(Tr, Sb, Tc, out, outT, L.ld_new, ro, rn, s1);
-    else
-      project_block<false>(Tr, Sb, Tc, out, outT, L.ld_new, ro, rn, s1);
-    ss += outT ? 2.0 * s1 : s1;
+    int off = nk;
+    for (int w = 0; w < cta::warp(); ++w) off += wcnt[w];
+    int tot = nk;
+    for (int w = 0; w < kThreads / 32; ++w) tot += wcnt[w];
+    if (keep) {
+      const int pos = off + __popc(bal & ((1u << cta::lane()) - 1u));
+      blist[pos] = b;
+      clist[pos] = c;
+      mlist[pos] = (mb >= 0 && c > pr.row) ? mb : -1;
+    }
+    nk = tot;
+    __syncthreads();
   }
+  double ss = 0.0;
+  if (nk > 0) {
+    stage64(Sb, L.S + int64_t(blist[0]) * L.ld_old * ro, L.ld_old, ro, ro);
+    cp_async_commit();  // {T_row, S_0}
+    stage64(Tc, L.T + int64_t(clist[0]) * rn * ro, rn, rn, ro);
+    cp_async_commit();  // {T_col,0}
+  }
+  for (int k = 0; k < nk; ++k) {
+    cp_async_wait<1>();  // S_k (T_col,k may still be in flight)
+    __syncthreads();
+    double acc[8][2];
+    const bool live = P.tri ? ts_strip<true>(Tr, Sb, ro, rn, acc) : ts_strip<false>(Tr, Sb, ro, rn, acc);
+    __syncthreads();  // S_k consumed
+    if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ld_old * ro, L.ld_old, ro, ro);
+    cp_async_commit();
+    cp_async_wait<1>();  // T_col,k
+    __syncthreads();
+    const int b = blist[k], mb = mlist[k];
+    double* out = L.out + int64_t(b) * L.ostride;
+    double* outT = mb >= 0 ? L.out + int64_t(mb) * L.ostride : nullptr;
+    double s1 = 0.0;
+    if (live) {
+      if (P.tri)
+        out_strip<true>(acc, Tc, out, outT, L.ld_new, ro, rn, s1);
+      else
+        out_strip<false>(acc, Tc, out, outT, L.ld_new, ro, rn, s1);
+    }
+    ss += outT ? 2.0 * s1 : s1;
+    __syncthreads();  // T_col,k consumed
+    if (k + 1 < nk) stage64(Tc, L.T + int64_t(clist[k + 1]) * rn * ro, rn, rn, ro);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
   // ||S||_F^2 of the projected row, fused (compression.hpp:487, frob_norm_sq)
   if (P.rowsum) {
     double* red = sm;  // Tr is dead
@@ -1076,7 +1142,9 @@ void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, b
       if (any) rows.push_back({l, int32_t(r)});
     }
   }
-  const size_t smax = size_t(3) * 64 * kPLd * sizeof(double);
+  P.max_row = 1;
+  for (int l = 0; l <= q; ++l) P.max_row = std::max(P.max_row, A.cpl[l].max_row);
+  const size_t smax = size_t(3) * 64 * kPLd * sizeof(double) + (32 + 3 * size_t(P.max_row)) * sizeof(int);
   check_smem(smax, "project_coupling");
   set_smem(k_project, smax);
   ar.off = 0;
