@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -1046,8 +1047,10 @@ struct Part {
 };
 
 // ---------------------------------------------------------------- phases
+// on_t(l) (optional): called once T(l) is final in stream order on s.
+using LevelHook = std::function<void(int)>;
 void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, const Part& pt,
-                   double* tree_mem) {
+                   double* tree_mem, const LevelHook& on_t = nullptr) {
   const int q = A.q, m = A.m, kq = A.rank[q];
   require(m >= kq, "orthogonalize_basis: leaf_dim must be >= leaf rank");
   T.alloc(A, A.rank, A.rank, tree_mem);
@@ -1061,13 +1064,17 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
                                                                  T.at(q) + A.own_begin(q) * int64_t(kq) * kq);
     H2B_CUDA(cudaGetLastError());
   }
+  if (on_t) on_t(q);
   flops += fl.qr(double(nl), m, kq);
   auto level = [&](int l) {
     const int kc = A.rank[l], kp = A.rank[l - 1];
     const int64_t np = A.nodes(l - 1);
     flops += fl.gemm(double(A.nodes(l)), kc, kp, kc) + fl.qr(double(np), 2 * kc, kp);
     require(2 * kc >= kp, "qr_batched: requires rows >= cols");
-    if (kp == 0) return;
+    if (kp == 0) {
+      if (on_t) on_t(l - 1);
+      return;
+    }
     const size_t sm = (2 * size_t(2 * kc) * kp + size_t(kp) * kp + 64 + kXb) * sizeof(double) + 64 * sizeof(int);
     check_smem(sm, "orthogonalize");
     set_smem(k_orth_level, sm);
@@ -1077,6 +1084,7 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
         A.transfer.p + A.tr_off[l] + (2 * p0 - A.tr_begin(l)) * A.tr_stride(l), A.ld(l), kc, kp,
         T.at(l) + 2 * p0 * int64_t(kc) * kc, T.at(l - 1) + p0 * int64_t(kp) * kp);
     H2B_CUDA(cudaGetLastError());
+    if (on_t) on_t(l - 1);
   };
   for (int l = q; l > pt.s; --l) level(l);
   // the projection tree of the partitioned levels: remote column bases for
@@ -1086,86 +1094,118 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
   for (int l = pt.s; l >= 1; --l) level(l);
 }
 
-// Project every coupling level with T (rows x cols per node): blocks become
-// T.rows[l] x T.rows[l].  Writes into `out_pool` (may alias the current pool
-// when the shapes agree).
-// Project every coupling level with T (rows x cols per node, compression.hpp:
-// 130-169): blocks become T.rows[l] x T.rows[l].  Square T (orthogonalization)
-// projects in place.  Rectangular T (truncation) shrinks every block: the new,
-// compacted pool is written over the old one in block-order chunks staged in
-// the workspace arena -- chunk k's destination ends where chunk k+1's source
-// starts or earlier (every block only shrinks), so nothing unread is clobbered
-// and no second coupling pool is ever allocated.
-// Project every coupling level with T (rows x cols per node, compression.hpp:
-// 130-169): blocks become T.rows[l] x T.rows[l].  On symmetric levels only the
-// upper blocks are multiplied; each also writes its mirror (the transpose).
-// The new blocks are written into the OLD block slots (they only shrink), then
-// -- for the truncation's rectangular T -- compacted in block order through
-// the workspace arena: chunk k's destination ends at or before chunk k+1's
-// source, so nothing unread is clobbered and no second pool is allocated.
-void project(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, bool in_place, const Part& pt,
-             Arena& ar, double* frob2 = nullptr) {
-  const int q = A.q;
+// Projection S <- T_row S T_col^T of every coupling level (project_coupling,
+// compression.hpp:130-169), split so that it can run level by level on a
+// side stream while the orthogonalization / truncation chains (which produce
+// T level by level, bottom-up) continue on the main stream:
+//   ProjRows        the block rows with work (structure only: on symmetric
+//                   levels the rows holding an upper block), uploaded once;
+//   project_level   one k_project launch for level l once T(l) is final;
+//   project_finish  after every level: relabel the layers and, for the
+//                   rectangular T of the truncation, compact the pool.
+// Square T (orthogonalization) projects in place.  Rectangular T shrinks
+// every block: each block is written at the start of its old slot (ld =
+// pad2(new rank)), then the compaction moves the blocks down in block-order
+// chunks -- chunk k's destination ends where chunk k+1's source starts or
+// earlier (every block only shrinks), so nothing unread is clobbered and no
+// second coupling pool is ever allocated.
+struct ProjRows {
+  std::vector<int64_t> off;  // level l's rows: [off[l], off[l + 1])
+  ProjRow* d = nullptr;
+  double* rsum = nullptr;    // per row: sum of squares of the projected blocks
+  std::vector<ProjRow> h;
+  int max_row = 1;
+  static size_t need(const Matrix& A) {
+    size_t r = 1;
+    for (int l = 0; l <= A.q; ++l) r += size_t(A.cpl[l].rows);
+    return Arena::need(r, sizeof(ProjRow)) + Arena::need(r, sizeof(double));
+  }
+};
+
+const int32_t* mirror_of(const Matrix& A, int l) {
+  return (A.mirror_sym[l] && l < int(A.value_sym.size()) && A.value_sym[l]) ? A.mirror.p + A.mirror_off[l]
+                                                                           : nullptr;
+}
+
+void project_rows(const Matrix& A, Arena& ar, ProjRows& R, cudaStream_t s) {
   require(A.mirror_ready, "project_coupling: mirror map missing");
-  ProjTable P{};
-  P.tri = in_place ? 1 : 0;
-  std::vector<int64_t> new_off(q + 2, 0);
+  const int q = A.q;
+  R.off.assign(q + 2, 0);
+  R.h.clear();
+  R.max_row = 1;
   for (int l = 0; l <= q; ++l) {
     const Layer& L = A.cpl[l];
-    const int rn = T.rows[l];
-    new_off[l + 1] = new_off[l] + L.nb * int64_t(pad2(rn)) * rn;
-  }
-  std::vector<ProjRow> rows;
-  for (int l = 0; l <= q; ++l) {
-    Layer& L = A.cpl[l];
-    const int rn = T.rows[l], ro = T.cols[l];
-    if (L.nb == 0) continue;
-    require(ro == L.br && ro == L.bc, "project_coupling: dim mismatch");
-    if (pt.counts(l)) flops += fl.gemm(double(L.nb), rn, ro, ro) + fl.gemm(double(L.nb), rn, rn, ro);
-    ProjLevel& d = P.L[l];
-    d.S = L.val;
-    d.rp = L.rp;
-    d.ci = L.ci;
-    d.mirror = (A.mirror_sym[l] && l < int(A.value_sym.size()) && A.value_sym[l]) ? A.mirror.p + A.mirror_off[l]
-                                                                                    : nullptr;
-    d.T = T.at(l);
-    d.ro = ro;
-    d.rn = rn;
-    d.ld_old = L.ld;
-    d.ld_new = pad2(rn);
-    d.out = L.val;  // in the old slots
-    d.ostride = L.block_stride();
-    if (rn == 0) continue;
-    for (int64_t r = 0; r < L.rows; ++r) {
+    R.off[l] = int64_t(R.h.size());
+    R.max_row = std::max(R.max_row, L.max_row);
+    const bool mir = mirror_of(A, l) != nullptr;
+    for (int64_t r = 0; r < L.rows && L.nb > 0; ++r) {
       bool any = false;
-      for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1] && !any; ++b) any = !d.mirror || L.h_ci[b] > r;
-      if (any) rows.push_back({l, int32_t(r)});
+      for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1] && !any; ++b) any = !mir || L.h_ci[b] > r;
+      if (any) R.h.push_back({l, int32_t(r)});
     }
   }
-  P.max_row = 1;
-  for (int l = 0; l <= q; ++l) P.max_row = std::max(P.max_row, A.cpl[l].max_row);
+  R.off[q + 1] = int64_t(R.h.size());
+  ar.off = 0;
+  R.d = ar.take<ProjRow>(std::max<size_t>(1, R.h.size()));
+  R.rsum = ar.take<double>(std::max<size_t>(1, R.h.size()));
+  if (!R.h.empty())
+    H2B_CUDA(cudaMemcpyAsync(R.d, R.h.data(), R.h.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
+  H2B_CUDA(cudaStreamSynchronize(s));  // (pageable source)
+}
+
+// Level l with T(l) (T.rows[l] x T.cols[l] per node) on stream st.
+void project_level(const Matrix& A, const TreePool& T, const ProjRows& R, int l, bool tri, bool want_sum,
+                   Flops& fl, double& flops, const Part& pt, cudaStream_t st) {
+  const Layer& L = A.cpl[l];
+  const int rn = T.rows[l], ro = T.cols[l];
+  if (L.nb == 0) return;
+  require(ro == L.br && ro == L.bc, "project_coupling: dim mismatch");
+  if (pt.counts(l)) flops += fl.gemm(double(L.nb), rn, ro, ro) + fl.gemm(double(L.nb), rn, rn, ro);
+  const int64_t n = R.off[l + 1] - R.off[l];
+  if (rn == 0 || n == 0) return;
+  ProjTable P{};
+  P.tri = tri ? 1 : 0;
+  P.max_row = R.max_row;
+  P.rowsum = want_sum ? R.rsum + R.off[l] : nullptr;
+  ProjLevel& d = P.L[l];
+  d.S = L.val;
+  d.rp = L.rp;
+  d.ci = L.ci;
+  d.mirror = mirror_of(A, l);
+  d.T = const_cast<TreePool&>(T).at(l);
+  d.ro = ro;
+  d.rn = rn;
+  d.ld_old = L.ld;
+  d.ld_new = pad2(rn);
+  d.out = L.val;  // in the old slots
+  d.ostride = L.block_stride();
   const size_t smax = size_t(3) * 64 * kPLd * sizeof(double) + (32 + 3 * size_t(P.max_row)) * sizeof(int);
   check_smem(smax, "project_coupling");
   set_smem(k_project, smax);
-  ar.off = 0;
-  ProjRow* drows = ar.take<ProjRow>(std::max<size_t>(1, rows.size()));
-  double* rsum = ar.take<double>(std::max<size_t>(1, rows.size()));
-  P.rowsum = frob2 ? rsum : nullptr;
-  if (!rows.empty()) {
-    H2B_CUDA(cudaMemcpyAsync(drows, rows.data(), rows.size() * sizeof(ProjRow), cudaMemcpyHostToDevice, s));
-    k_project<<<unsigned(rows.size()), kThreads, smax, s>>>(P, drows);
-    H2B_CUDA(cudaGetLastError());
-  }
-  if (frob2) {  // sum of the counted rows (replicated top levels: rank 0 only)
-    std::vector<double> h(rows.size());
-    if (!rows.empty())
-      H2B_CUDA(cudaMemcpyAsync(h.data(), rsum, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    H2B_CUDA(cudaStreamSynchronize(s));
-    double acc = 0.0;
-    for (size_t i = 0; i < rows.size(); ++i)
-      if (pt.counts(rows[i].level)) acc += h[i];
-    *frob2 = acc;
-  }
+  k_project<<<unsigned(n), kThreads, smax, st>>>(P, R.d + R.off[l]);
+  H2B_CUDA(cudaGetLastError());
+}
+
+// ||S||_F^2 of the projected coupling (replicated top levels: rank 0 only);
+// the projection launches must be complete.
+double project_rowsum(const ProjRows& R, const Part& pt, cudaStream_t s) {
+  std::vector<double> h(R.h.size());
+  if (!R.h.empty())
+    H2B_CUDA(cudaMemcpyAsync(h.data(), R.rsum, R.h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+  double acc = 0.0;
+  for (size_t i = 0; i < R.h.size(); ++i)
+    if (pt.counts(R.h[i].level)) acc += h[i];
+  return acc;
+}
+
+// After every level's launch completed (stream order on s): compaction of the
+// shrunken blocks (not in_place) and the new layer shapes.
+void project_finish(Matrix& A, const TreePool& T, bool in_place, Arena& ar, cudaStream_t s) {
+  const int q = A.q;
+  std::vector<int64_t> new_off(q + 2, 0);
+  for (int l = 0; l <= q; ++l)
+    new_off[l + 1] = new_off[l] + A.cpl[l].nb * int64_t(pad2(T.rows[l])) * T.rows[l];
   if (!in_place) {
     // compaction: level by level, block order, chunks staged in the arena
     double* temp = ar.base + ar.off;
@@ -1334,13 +1374,6 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, c
   }
 }
 
-int read_kmax(int* d, cudaStream_t s) {
-  int h = 0;
-  H2B_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
-  H2B_CUDA(cudaStreamSynchronize(s));
-  return h;
-}
-
 double sum_host(const double* d, int64_t n, cudaStream_t s) {
   std::vector<double> h(n);
   if (n) H2B_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1411,8 +1444,10 @@ TruncSizes truncate_sizes(const Matrix& A) {
   return z;
 }
 
+// on_t(l) (optional): called once Tt(l) (new x old per node) is final in
+// stream order on s; Tt.rows[l] holds the new rank by then.
 double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s, Flops& fl,
-                double& flops, const Part& pt, double* tree_mem, Arena& ar) {
+                double& flops, const Part& pt, double* tree_mem, Arena& ar, const LevelHook& on_t = nullptr) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   Trace tr;
   const int q = A.q, m = A.m;
@@ -1470,6 +1505,8 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
                                                            Tt.at(q) + l0 * int64_t(kt) * kq, newleaf, ldn, en);
       H2B_CUDA(cudaGetLastError());
     }
+    Tt.rows[q] = kt;
+    if (on_t) on_t(q);
     lev_e[q] = sum_host(en, no, s);
     tr.at(s, "leaf apply", q);
   }
@@ -1519,6 +1556,8 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
           newtr + ntoff[l] + (2 * p0 - A.tr_begin(l)) * int64_t(ldn) * ktp, ldn, en);
       H2B_CUDA(cudaGetLastError());
     }
+    Tt.rows[l - 1] = ktp;
+    if (on_t) on_t(l - 1);
     const double el = sum_host(en, npo, s);
     lev_e[l - 1] = pt.counts(l - 1) ? el : 0.0;
     tr.at(s, "level apply", l);
@@ -1551,6 +1590,64 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   for (double e : lev_e) energy += e;
   return energy;
 }
+
+// Highest-priority stream ordered after `user` on construction; `user` is
+// ordered after it on destruction.
+struct ChainStream {
+  cudaStream_t user, s = nullptr;
+  cudaEvent_t e = nullptr;
+  explicit ChainStream(cudaStream_t u) : user(u) {
+    int lo = 0, hi = 0;
+    H2B_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    H2B_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+    H2B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    H2B_CUDA(cudaEventRecord(e, user));
+    H2B_CUDA(cudaStreamWaitEvent(s, e, 0));
+  }
+  ~ChainStream() {
+    cudaEventRecord(e, s);
+    cudaStreamWaitEvent(user, e, 0);
+    cudaStreamSynchronize(s);
+    cudaEventDestroy(e);
+    cudaStreamDestroy(s);
+  }
+};
+
+// Side stream of compress(): fork(l) makes it wait for the main stream's
+// work issued so far (T(l) final), join() makes the main stream wait for it.
+// Disabled: b is the main stream itself and both are no-ops.
+struct SideStream {
+  cudaStream_t s, b;
+  bool on;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t done = nullptr;
+  SideStream(bool enable, cudaStream_t main) : s(main), b(main), on(enable) {
+    if (!on) return;
+    int lo = 0, hi = 0;
+    H2B_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    H2B_CUDA(cudaStreamCreateWithPriority(&b, cudaStreamNonBlocking, lo));  // lowest: fills the gaps
+    ev.resize(kMaxLevels + 1, nullptr);
+    for (auto& e : ev) H2B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    H2B_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  }
+  ~SideStream() {
+    if (!on) return;
+    cudaStreamSynchronize(b);
+    for (auto e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(done);
+    cudaStreamDestroy(b);
+  }
+  void fork(int l) {
+    if (!on) return;
+    H2B_CUDA(cudaEventRecord(ev[l], s));
+    H2B_CUDA(cudaStreamWaitEvent(b, ev[l], 0));
+  }
+  void join() {
+    if (!on) return;
+    H2B_CUDA(cudaEventRecord(done, b));
+    H2B_CUDA(cudaStreamWaitEvent(s, done, 0));
+  }
+};
 
 // Resize the workspace and rebuild the BSR work list after ranks changed.
 void relayout(Matrix& A) {
@@ -1598,21 +1695,28 @@ uint64_t counted_footprint(const Matrix& A, const Part& pt) {
 void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_comm* comm) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   DeviceGuard g(A.device);
-  cudaStream_t s = A.stream;
+  // The dependency chain (orthogonalization, weights, truncation) runs on a
+  // highest-priority stream ordered after the handle's stream; the
+  // projections on a lowest-priority side stream soak up the SMs it leaves
+  // idle (SideStream).
+  ChainStream chain(A.stream);
+  cudaStream_t s = chain.s;
   // One workspace for the whole call (cached per device, see WsCache):
   // region A holds the projection trees (To, then Tt), region B the weight
   // tree R, region C the phase scratch (weights, truncation, the chunked
   // compaction of the coupling pool).
   const size_t tree_need = TreePool::need(A, A.rank, A.rank);
   const size_t arena_need = std::max({weights_arena_need(A), truncate_sizes(A).total, size_t(1) << 25});
+  const size_t proj_need = ProjRows::need(A);
   Workspace ws{A.device};
-  ws.buf = ws_checkout(A.device, 2 * tree_need + arena_need);
+  ws.buf = ws_checkout(A.device, 2 * tree_need + arena_need + proj_need);
   ws.trees = ws.buf.p;
   ws.rtree = ws.buf.p + tree_need;
   ws.arena = ws.buf.p + 2 * tree_need;
-  ws.arena_cap = ws.buf.n - 2 * tree_need;  // all the rest (projection chunks)
-  Arena ar;
+  ws.arena_cap = ws.buf.n - 2 * tree_need - proj_need;  // all the rest (projection chunks)
+  Arena ar, par;  // phase scratch; the projection work lists (at the end: live across phases)
   ar.reserve(ws.arena, ws.arena_cap);
+  par.reserve(ws.arena + ws.arena_cap, proj_need);
   if (std::getenv("H2B_TRACE"))
     fprintf(stderr, "  [trace] compress workspace %.2f GB (arena %.2f GB)\n", ws.buf.n * 8e-9,
             ws.arena_cap * 8e-9);
@@ -1634,16 +1738,41 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   }
   double sums[3] = {double(counted_footprint(A, pt)), 0.0, 0.0};
 
+  // The projections run level by level on a side stream as soon as T(l) is
+  // final, overlapping the (bottom-up, increasingly latency-bound) chains of
+  // the orthogonalization and of the truncation on the main stream.  Phase
+  // times are therefore boundary to boundary on the main stream: a
+  // projection phase is what remains of it after its producer phase.
+  // Partitioned compression (communicator callbacks between levels) runs
+  // the projections after their producers, on the main stream.
+  const bool overlap = !pt.dist();
+  SideStream side(overlap, s);
+  ProjRows PR;
+  project_rows(A, par, PR, s);
   TreePool To, R, Tt;
   double n2 = 0.0;  // ||A||_F^2 after the orthogonal projection (compression.hpp:487)
+  Matrix* Ap = &A;
+  auto hook = [Ap, &PR, &fl, &pt, &side](TreePool& T, bool tri, bool want_sum, double& fl_acc) -> LevelHook {
+    TreePool* Tp = &T;
+    double* fa = &fl_acc;
+    return [Ap, Tp, fa, tri, want_sum, &PR, &fl, &pt, &side](int l) {
+      side.fork(l);
+      project_level(*Ap, *Tp, PR, l, tri, want_sum, fl, *fa, pt, side.b);
+    };
+  };
   {
     Timer t(s);
-    orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt, ws.trees);
+    orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt, ws.trees,
+                  overlap ? hook(To, true, true, r.flops_project_orth) : nullptr);
     r.time_orthogonalize_ms = t.stop();
   }
   {
     Timer t(s);
-    project(A, To, s, fl, r.flops_project_orth, /*in_place=*/true, pt, ar, &n2);
+    if (!overlap)
+      for (int l = A.q; l >= 0; --l) project_level(A, To, PR, l, true, true, fl, r.flops_project_orth, pt, s);
+    side.join();
+    n2 = project_rowsum(PR, pt, s);
+    project_finish(A, To, /*in_place=*/true, ar, s);
     r.time_project_orth_ms = t.stop();
   }
   n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s, ws.arena);
@@ -1658,12 +1787,16 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   double energy = 0.0;
   {
     Timer t(s);
-    energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate, pt, ws.trees, ar);
+    energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate, pt, ws.trees, ar,
+                      overlap ? hook(Tt, false, false, r.flops_project_trunc) : nullptr);
     r.time_truncate_ms = t.stop();
   }
   {
     Timer t(s);
-    project(A, Tt, s, fl, r.flops_project_trunc, /*in_place=*/false, pt, ar);
+    if (!overlap)
+      for (int l = A.q; l >= 0; --l) project_level(A, Tt, PR, l, false, false, fl, r.flops_project_trunc, pt, s);
+    side.join();
+    project_finish(A, Tt, /*in_place=*/false, ar, s);
     r.time_project_trunc_ms = t.stop();
   }
   relayout(A);
