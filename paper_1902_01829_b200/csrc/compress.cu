@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(64) k_jacobi64(const double* __restrict__ Jall
   __shared__ __align__(16) double cols[64 * LD];
   __shared__ double nrm2[64];
   __shared__ double nrm[64];
-  __shared__ int flag;
+  __shared__ int flag, big;
   const int c = threadIdx.x;
   const int n = r + (r & 1);  // zero pad column when odd
   const double* J = Jall + blockIdx.x * int64_t(r) * r;
@@ -743,8 +743,12 @@ __global__ void __launch_bounds__(64) k_jacobi64(const double* __restrict__ Jall
   };
   double a = norm2();
   if (c < n) publish(a);
-  if (c == 0) flag = 0;
+  if (c == 0) flag = big = 0;
   const double tol = 2.220446049250313e-16 * 16.0;
+  // A sweep whose rotations all had |a_pq| <= tol_q sqrt(a_pp a_qq) is the
+  // last one that rotates: the next would find |a_pq| ~ (that)^2 <= tol/16 on
+  // every pair (quadratic convergence) and only confirm it, so it is skipped.
+  const double tol_q = 0.25 * sqrt(tol);
   const int m1 = n - 1;
   for (int sweep = 0; sweep < 60 && r > 1; ++sweep) {
     for (int rd = 0; rd < m1; ++rd) {
@@ -767,9 +771,11 @@ __global__ void __launch_bounds__(64) k_jacobi64(const double* __restrict__ Jall
         const bool is_p = c < pt;
         const double ap = is_p ? a : b, aq = is_p ? b : a;
         // skip rule of linalg.hpp:155-160 (sqrt(a) sqrt(b): no underflow)
-        if (!(fabs(d) <= tol * (sqrt(ap) * sqrt(aq)) || d == 0.0)) {
+        const double sab = sqrt(ap) * sqrt(aq);
+        if (!(fabs(d) <= tol * sab || d == 0.0)) {
           rot = true;
           flag = 1;
+          if (fabs(d) > tol_q * sab) big = 1;
           const double z = (aq - ap) / (2.0 * d);
           const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + hypot(1.0, z));
           const double cs = 1.0 / sqrt(1.0 + t * t);
@@ -789,13 +795,13 @@ __global__ void __launch_bounds__(64) k_jacobi64(const double* __restrict__ Jall
       if (rot) publish(a);
     }
     __syncthreads();
-    const int f = flag;
+    const int f = flag, fb = big;
     __syncthreads();
-    if (c == 0) flag = 0;
+    if (c == 0) flag = big = 0;
 #ifdef H2B_SWEEP_HIST
-    if (c == 0 && (!f || sweep == 59)) atomicAdd(&cta::g_sweep_hist[f ? 60 : sweep], 1);
+    if (c == 0 && (!f || !fb || sweep == 59)) atomicAdd(&cta::g_sweep_hist[(f && fb) ? 60 : sweep], 1);
 #endif
-    if (!f) break;
+    if (!f || !fb) break;
   }
   // sigma = column norms, stable descending order
   const double sg = sqrt(norm2());
