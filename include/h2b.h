@@ -74,12 +74,16 @@ typedef enum {
 
 typedef struct h2b_matrix h2b_matrix;
 
-/* Host description of a symmetric H^2 matrix in the export layout. */
+/* Host description of an H^2 matrix in the export layout.  symmetric = 1:
+ * one basis (row == column, what construct() produces).  symmetric = 0: the
+ * column basis V / F (H2Matrix::col_basis_store, h2_matrix.hpp:69,75-78) is
+ * given by col_ranks / col_leaf / col_transfer and coupling block (i, j) of
+ * level l is ranks[l] x col_ranks[l]. */
 typedef struct {
   int32_t n;          /* points; n == m * 2^depth */
   int32_t m;          /* leaf size (BasisTree::leaf_dim) */
   int32_t depth;      /* q */
-  int32_t symmetric;  /* must be 1 (construct() always produces symmetric matrices) */
+  int32_t symmetric;  /* 1: column basis == row basis; 0: col_* below */
   const int32_t* perm;
   const int32_t* ranks;
   const double* leaf;
@@ -90,6 +94,9 @@ typedef struct {
   const int32_t* dense_row_ptr;
   const int32_t* dense_col_idx;
   const double* dense_values;
+  const int32_t* col_ranks;     /* symmetric == 0 only (else ignored) */
+  const double* col_leaf;
+  const double* col_transfer;
 } h2b_matrix_desc;
 
 /* Parameters of the reference's ab-initio construction (ConstructionConfig +
@@ -128,6 +135,7 @@ typedef struct {
   uint64_t global_footprint_bytes; /* whole matrix (== footprint_bytes unless partitioned) */
   int32_t part_log2;          /* 2^part_log2 subtree partitions (0: whole matrix) */
   int32_t part_index;         /* partition owned by this handle */
+  int32_t col_ranks[32];      /* column basis ranks (== ranks when symmetric) */
 } h2b_matrix_info;
 
 /* Workspace buffers of a handle (device pointers, see h2b_workspace). */
@@ -162,13 +170,17 @@ H2B_API h2b_status h2b_matrix_info_get(const h2b_matrix* A, h2b_matrix_info* inf
 H2B_API h2b_status h2b_matrix_export(const h2b_matrix* A, int32_t* perm, double* leaf, double* transfer,
                              int32_t* cpl_row_ptr, int32_t* cpl_col_idx, double* cpl_values,
                              int32_t* dense_row_ptr, int32_t* dense_col_idx, double* dense_values);
+/* Column basis of a non-symmetric matrix (V leaves, F transfers; export
+ * layout, sizes from col_ranks).  Symmetric matrices: H2B_INVALID_ARGUMENT. */
+H2B_API h2b_status h2b_matrix_export_col(const h2b_matrix* A, double* col_leaf, double* col_transfer);
 H2B_API uint64_t h2b_matrix_footprint(const h2b_matrix* A);
 /* h2kit::save / h2kit::load (io.hpp:183-282): the reference's ".h2" container
  * ("H2KT" v1, FP64, CRC-32 per section), byte-compatible in both directions;
  * the pools stream straight from / into HBM.  info: BuildInfo to store (NULL:
  * the matrix's own -- set by h2b_matrix_build / h2b_matrix_load, zeros for
  * h2b_matrix_create); info_out may be NULL.  Errors: H2B_IO_ERROR with the
- * reference's messages; non-symmetric containers: H2B_UNSUPPORTED. */
+ * reference's messages.  Non-symmetric matrices: the column basis follows the
+ * row basis in the bases section (io.hpp:194-197). */
 H2B_API h2b_status h2b_matrix_save(const h2b_matrix* A, const char* path, const h2b_build_info* info);
 H2B_API h2b_status h2b_matrix_load(const char* path, int device, h2b_matrix** out, h2b_build_info* info_out);
 /* h2kit::crc32 (crc32.cpp:6-20, seed 0): the containers' section checksum
@@ -194,6 +206,8 @@ H2B_API h2b_status h2b_dense_mv(h2b_matrix* A, const double* xc, double* yc, dou
 
 /* Algebraic recompression in place (orthogonalize, project, weights,
  * truncate at relative eps, project).  Exclusive access required. */
+/* Non-symmetric matrices (h2b_compress, h2b_orthogonalize, h2b_hmv_multi):
+ * H2B_UNSUPPORTED in this version; hmv and the phase entry points support them. */
 H2B_API h2b_status h2b_compress(h2b_matrix* A, double eps, h2b_compress_report* report);
 /* Orthogonalize only (in place); projection tree written to t_out (host,
  * level-concatenated ranks[l]^2 per node) when non-NULL. */

@@ -61,13 +61,12 @@ inline void check(h2b_status st) {
 
 // Flattened export-layout copy of a reference H2Matrix<double>.
 struct Flat {
-  std::vector<int32_t> ranks, rp, ci, drp, dci;
-  std::vector<double> transfer, values;
+  std::vector<int32_t> ranks, rp, ci, drp, dci, cranks;
+  std::vector<double> transfer, values, ctransfer;
   h2b_matrix_desc desc{};
 };
 
 inline std::unique_ptr<Flat> flatten(const H2Matrix<double>& A) {
-  if (!A.symmetric) throw std::invalid_argument("h2kit_b200: only symmetric H2 matrices are supported");
   auto f = std::make_unique<Flat>();
   const int q = A.depth();
   f->ranks.assign(A.row_basis.ranks.begin(), A.row_basis.ranks.end());
@@ -97,6 +96,15 @@ inline std::unique_ptr<Flat> flatten(const H2Matrix<double>& A) {
   d.dense_row_ptr = A.dense.row_ptr.data();
   d.dense_col_idx = A.dense.col_idx.data();
   d.dense_values = A.dense.values.data();
+  if (!A.symmetric) {  // column basis V / F (h2_matrix.hpp:69,75-78)
+    const BasisTree<double>& V = A.col_basis();
+    f->cranks.assign(V.ranks.begin(), V.ranks.end());
+    for (int l = 1; l <= q; ++l) f->ctransfer.insert(f->ctransfer.end(), V.transfer[l].begin(), V.transfer[l].end());
+    d.symmetric = 0;
+    d.col_ranks = f->cranks.data();
+    d.col_leaf = V.leaf_pool.data();
+    d.col_transfer = f->ctransfer.data();
+  }
   return f;
 }
 
@@ -146,6 +154,12 @@ inline uint64_t fingerprint(const H2Matrix<double>& A) {
   for (const auto& t : A.row_basis.transfer) sample(t);
   for (const auto& L : A.coupling.levels) sample(L.values);
   sample(A.dense.values);
+  mix(uint64_t(A.symmetric));
+  if (!A.symmetric) {
+    for (int r : A.col_basis().ranks) mix(uint64_t(r));
+    sample(A.col_basis().leaf_pool);
+    for (const auto& t : A.col_basis().transfer) sample(t);
+  }
   return h;
 }
 

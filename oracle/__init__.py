@@ -124,6 +124,18 @@ class Backend:
 
     def from_host(self, hm: HostMatrix) -> "OracleMatrix":
         h = _P()
+        if not hm.symmetric:  # column basis: the reference backend only
+            if self.prefix != "ref_":
+                raise OracleError("non-symmetric matrices need the reference backend")
+            arrs = [np.ascontiguousarray(a) for a in (
+                hm.ranks.astype(np.int32), hm.col_ranks.astype(np.int32), hm.perm, hm.leaf,
+                hm.transfer, hm.col_leaf, hm.col_transfer, hm.cpl_row_ptr, hm.cpl_col_idx,
+                hm.cpl_values, hm.dense_row_ptr, hm.dense_col_idx, hm.dense_values)]
+            f = self.lib.ref_import_ns
+            f.argtypes = [C.c_int] * 3 + [C.c_void_p] * 13 + [C.POINTER(_P)]
+            f.restype = C.c_int
+            self.check(f(hm.n, hm.m, hm.depth, *[a.ctypes.data for a in arrs], C.byref(h)))
+            return OracleMatrix(self, h.value)
         arrs = [np.ascontiguousarray(a) for a in (hm.ranks.astype(np.int32), hm.perm, hm.leaf,
                                                     hm.transfer, hm.cpl_row_ptr, hm.cpl_col_idx,
                                                     hm.cpl_values, hm.dense_row_ptr,
@@ -188,10 +200,18 @@ class OracleMatrix:
         return ranks, nb, int(nd[0])
 
     def to_host(self) -> HostMatrix:
-        n, m, q, _ = self.shape()
+        n, m, q, sym = self.shape()
         ranks, nb, nd = self.layout()
-        hm = HostMatrix.empty(n, m, q, ranks, nb, nd)
+        cr = None
+        if not sym:
+            cr = np.zeros(q + 1, np.int32)
+            self.be.lib.ref_col_ranks.argtypes = [_P, C.c_void_p]
+            self.be.lib.ref_col_ranks(self.h, cr.ctypes.data)
+        hm = HostMatrix.empty(n, m, q, ranks, nb, nd, cr)
         self.be.fn("export")(self.h, *[a.ctypes.data for a in hm.arrays()])
+        if not sym:
+            self.be.lib.ref_export_col.argtypes = [_P, C.c_void_p, C.c_void_p]
+            self.be.lib.ref_export_col(self.h, hm.col_leaf.ctypes.data, hm.col_transfer.ctypes.data)
         return hm
 
     @property
@@ -204,6 +224,15 @@ class OracleMatrix:
     def vec_size(self):
         ranks, _, _ = self.layout()
         return int(sum((1 << l) * int(r) for l, r in enumerate(ranks)))
+
+    def col_vec_size(self):
+        n, m, q, sym = self.shape()
+        if sym:
+            return self.vec_size()
+        cr = np.zeros(q + 1, np.int32)
+        self.be.lib.ref_col_ranks.argtypes = [_P, C.c_void_p]
+        self.be.lib.ref_col_ranks(self.h, cr.ctypes.data)
+        return int(sum((1 << l) * int(r) for l, r in enumerate(cr)))
 
     def hmv(self, x, y=None, alpha=1.0, beta=0.0):
         x = np.ascontiguousarray(x, dtype=np.float64)
@@ -220,13 +249,13 @@ class OracleMatrix:
 
     def upsweep(self, xc):
         xc = np.ascontiguousarray(xc, dtype=np.float64)
-        out = np.zeros(self.vec_size(), np.float64)
+        out = np.zeros(self.col_vec_size(), np.float64)
         self.be.check(self.be.fn("upsweep")(self.h, xc.ctypes.data, out.ctypes.data))
         return out
 
     def tree_multiply(self, xh):
         xh = np.ascontiguousarray(xh, dtype=np.float64)
-        out = np.zeros_like(xh)
+        out = np.zeros(self.vec_size(), np.float64)
         self.be.check(self.be.fn("tree_multiply")(self.h, xh.ctypes.data, out.ctypes.data))
         return out
 

@@ -208,6 +208,76 @@ int ref_import(int n, int m, int depth, const int32_t* ranks, const int32_t* per
   });
 }
 
+// Non-symmetric variant: the column basis V / F (col_basis_store,
+// h2_matrix.hpp:69) and coupling blocks of ranks[l] x col_ranks[l].
+int ref_import_ns(int n, int m, int depth, const int32_t* ranks, const int32_t* col_ranks,
+                  const int32_t* perm, const double* leaf, const double* transfer,
+                  const double* col_leaf, const double* col_transfer, const int32_t* cpl_row_ptr,
+                  const int32_t* cpl_col_idx, const double* cpl_values, const int32_t* dense_row_ptr,
+                  const int32_t* dense_col_idx, const double* dense_values, void** out) {
+  return guarded([&] {
+    Mat* A = new Mat;
+    A->n = n;
+    A->m = m;
+    A->symmetric = false;
+    A->perm.assign(perm, perm + n);
+    const size_t nleaves = size_t(1) << depth;
+    auto basis = [&](BasisTree<double>& B, const int32_t* rk, const double* lf, const double* tr) {
+      B.flat = make_complete_binary_tree(depth);
+      B.leaf_dim = m;
+      B.ranks.assign(rk, rk + depth + 1);
+      B.leaf_pool.assign(lf, lf + nleaves * m * rk[depth]);
+      B.transfer.assign(depth + 1, {});
+      for (int l = 1; l <= depth; ++l) {
+        const size_t sz = (size_t(1) << l) * rk[l] * rk[l - 1];
+        B.transfer[l].assign(tr, tr + sz);
+        tr += sz;
+      }
+    };
+    basis(A->row_basis, ranks, leaf, transfer);
+    A->col_basis_store.emplace();
+    basis(*A->col_basis_store, col_ranks, col_leaf, col_transfer);
+    A->coupling.levels.assign(depth + 1, {});
+    for (int l = 0; l <= depth; ++l) {
+      BSRLayer<double>& L = A->coupling.levels[l];
+      L.block_rows = L.block_cols = index_t(1) << l;
+      L.brows = ranks[l];
+      L.bcols = col_ranks[l];
+      L.row_ptr.assign(cpl_row_ptr, cpl_row_ptr + L.block_rows + 1);
+      cpl_row_ptr += L.block_rows + 1;
+      const size_t nb = L.row_ptr.back();
+      L.col_idx.assign(cpl_col_idx, cpl_col_idx + nb);
+      cpl_col_idx += nb;
+      const size_t nv = nb * ranks[l] * col_ranks[l];
+      L.values.assign(cpl_values, cpl_values + nv);
+      cpl_values += nv;
+    }
+    BSRLayer<double>& D = A->dense;
+    D.block_rows = D.block_cols = index_t(nleaves);
+    D.brows = D.bcols = m;
+    D.row_ptr.assign(dense_row_ptr, dense_row_ptr + nleaves + 1);
+    const size_t nbd = D.row_ptr.back();
+    D.col_idx.assign(dense_col_idx, dense_col_idx + nbd);
+    D.values.assign(dense_values, dense_values + nbd * m * m);
+    *out = A;
+  });
+}
+
+// Column basis ranks (== row ranks when symmetric) and pools (non-symmetric).
+void ref_col_ranks(void* h, int* out) {
+  const Mat& A = *static_cast<Mat*>(h);
+  for (int l = 0; l <= A.depth(); ++l) out[l] = A.col_basis().ranks[l];
+}
+void ref_export_col(void* h, double* col_leaf, double* col_transfer) {
+  const Mat& A = *static_cast<Mat*>(h);
+  const auto& B = A.col_basis();
+  std::memcpy(col_leaf, B.leaf_pool.data(), B.leaf_pool.size() * sizeof(double));
+  for (int l = 1; l <= A.depth(); ++l) {
+    std::memcpy(col_transfer, B.transfer[l].data(), B.transfer[l].size() * sizeof(double));
+    col_transfer += B.transfer[l].size();
+  }
+}
+
 uint64_t ref_footprint(void* h) { return memory_footprint(*static_cast<Mat*>(h)).total(); }
 
 void ref_flops_reset() { flops::reset(); }

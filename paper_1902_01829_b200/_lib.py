@@ -48,7 +48,8 @@ class MatrixDesc(C.Structure):
                 ("perm", C.c_void_p), ("ranks", C.c_void_p), ("leaf", C.c_void_p),
                 ("transfer", C.c_void_p), ("cpl_row_ptr", C.c_void_p), ("cpl_col_idx", C.c_void_p),
                 ("cpl_values", C.c_void_p), ("dense_row_ptr", C.c_void_p),
-                ("dense_col_idx", C.c_void_p), ("dense_values", C.c_void_p)]
+                ("dense_col_idx", C.c_void_p), ("dense_values", C.c_void_p),
+                ("col_ranks", C.c_void_p), ("col_leaf", C.c_void_p), ("col_transfer", C.c_void_p)]
 
 
 class BuildInfo(C.Structure):
@@ -69,7 +70,7 @@ class MatrixInfo(C.Structure):
                 ("dense_max_row", C.c_int32), ("footprint_bytes", C.c_uint64),
                 ("device_bytes", C.c_uint64), ("hmv_flops", C.c_double),
                 ("global_footprint_bytes", C.c_uint64), ("part_log2", C.c_int32),
-                ("part_index", C.c_int32)]
+                ("part_index", C.c_int32), ("col_ranks", C.c_int32 * 32)]
 
 
 class CompressReport(C.Structure):
@@ -105,6 +106,7 @@ _SIGS = {
     "h2b_matrix_destroy": (C.c_int, [C.c_void_p]),
     "h2b_matrix_info_get": (C.c_int, [C.c_void_p, C.POINTER(MatrixInfo)]),
     "h2b_matrix_export": (C.c_int, [C.c_void_p] + [C.c_void_p] * 9),
+    "h2b_matrix_export_col": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "h2b_matrix_footprint": (C.c_uint64, [C.c_void_p]),
     "h2b_matrix_save": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p]),
     "h2b_matrix_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p), C.c_void_p]),

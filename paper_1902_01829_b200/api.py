@@ -45,11 +45,14 @@ class MatrixInfo:
     footprint_bytes: int
     device_bytes: int
     hmv_flops: float
+    symmetric: int = 1
+    col_ranks: list = None  # column basis ranks (== ranks when symmetric)
 
 
 class H2Matrix:
-    """Device-resident symmetric H^2 matrix (the reference's H2Matrix<double>,
-    h2_matrix.hpp:62-80, plus its HmvContext workspace, hmv.hpp:161-172)."""
+    """Device-resident H^2 matrix (the reference's H2Matrix<double>,
+    h2_matrix.hpp:62-80, plus its HmvContext workspace, hmv.hpp:161-172);
+    symmetric, or with a separate column basis (from_host / load)."""
 
     def __init__(self, handle: int, device: int):
         self._h = C.c_void_p(handle)
@@ -59,11 +62,17 @@ class H2Matrix:
     @classmethod
     def from_host(cls, hm: HostMatrix, device: int = 0) -> "H2Matrix":
         lib = _lib.load()
-        keep = [np.ascontiguousarray(a) for a in (hm.perm, hm.ranks, hm.leaf, hm.transfer,
-                                                    hm.cpl_row_ptr, hm.cpl_col_idx, hm.cpl_values,
-                                                    hm.dense_row_ptr, hm.dense_col_idx,
-                                                    hm.dense_values)]
-        d = _lib.MatrixDesc(hm.n, hm.m, hm.depth, 1, *[a.ctypes.data for a in keep])
+        keep = [np.ascontiguousarray(a) for a in (hm.perm, hm.ranks.astype(np.int32), hm.leaf,
+                                                    hm.transfer, hm.cpl_row_ptr, hm.cpl_col_idx,
+                                                    hm.cpl_values, hm.dense_row_ptr,
+                                                    hm.dense_col_idx, hm.dense_values)]
+        col = [None, None, None]
+        if not hm.symmetric:  # column basis V / F (h2_matrix.hpp:69)
+            keep += [np.ascontiguousarray(hm.col_ranks.astype(np.int32)),
+                     np.ascontiguousarray(hm.col_leaf), np.ascontiguousarray(hm.col_transfer)]
+            col = [a.ctypes.data for a in keep[-3:]]
+        d = _lib.MatrixDesc(hm.n, hm.m, hm.depth, 1 if hm.symmetric else 0,
+                            *[a.ctypes.data for a in keep[:10]], *col)
         out = C.c_void_p()
         _lib.check(lib.h2b_matrix_create(C.byref(d), device, C.byref(out)))
         return cls(out.value, device)
@@ -134,7 +143,8 @@ class H2Matrix:
         q = inf.depth
         return MatrixInfo(inf.n, inf.m, q, list(inf.ranks[:q + 1]), list(inf.cpl_blocks[:q + 1]),
                           list(inf.cpl_max_row[:q + 1]), inf.dense_blocks, inf.dense_max_row,
-                          inf.footprint_bytes, inf.device_bytes, inf.hmv_flops)
+                          inf.footprint_bytes, inf.device_bytes, inf.hmv_flops, inf.symmetric,
+                          list(inf.col_ranks[:q + 1]))
 
     @property
     def n(self) -> int:
@@ -146,14 +156,25 @@ class H2Matrix:
 
     def to_host(self) -> HostMatrix:
         inf = self.info()
-        hm = HostMatrix.empty(inf.n, inf.m, inf.depth, inf.ranks, inf.cpl_blocks,
-                              inf.dense_blocks)
+        q = inf.depth
+        sym = bool(inf.symmetric)
+        hm = HostMatrix.empty(inf.n, inf.m, q, list(inf.ranks)[:q + 1], list(inf.cpl_blocks)[:q + 1],
+                              inf.dense_blocks, None if sym else list(inf.col_ranks)[:q + 1])
         _lib.check(_lib.load().h2b_matrix_export(self._h, *[a.ctypes.data for a in hm.arrays()]))
+        if not sym:
+            _lib.check(_lib.load().h2b_matrix_export_col(self._h, hm.col_leaf.ctypes.data,
+                                                         hm.col_transfer.ctypes.data))
         return hm
 
     def vec_size(self) -> int:
+        """Length of y^ (row basis, LevelVectors::resize(A.row_basis))."""
         inf = self.info()
         return sum((1 << l) * r for l, r in enumerate(inf.ranks))
+
+    def col_vec_size(self) -> int:
+        """Length of x^ (LevelVectors::resize(A.col_basis()), hmv.hpp:166)."""
+        inf = self.info()
+        return sum((1 << l) * r for l, r in enumerate(inf.col_ranks))
 
     # -- hot path -------------------------------------------------------
     def set_phase_timing(self, on: bool = True):
@@ -202,7 +223,7 @@ def hmv_multi(A: H2Matrix, X: np.ndarray, alpha: float = 1.0, beta: float = 0.0,
 def upsweep(A: H2Matrix, xc: np.ndarray) -> np.ndarray:
     """upsweep(V, xc, n, xhat) (hmv.hpp:79-111); xc in cluster order."""
     xc = np.ascontiguousarray(xc, dtype=np.float64)
-    out = np.zeros(A.vec_size(), np.float64)
+    out = np.zeros(A.col_vec_size(), np.float64)
     _lib.check(_lib.load().h2b_upsweep(A._h, xc.ctypes.data, out.ctypes.data, _lib.PTR_HOST))
     return out
 
@@ -210,7 +231,7 @@ def upsweep(A: H2Matrix, xc: np.ndarray) -> np.ndarray:
 def tree_multiply(A: H2Matrix, xhat: np.ndarray) -> np.ndarray:
     """tree_multiply(S, xhat, yhat) (hmv.hpp:114-125)."""
     xhat = np.ascontiguousarray(xhat, dtype=np.float64)
-    out = np.zeros_like(xhat)
+    out = np.zeros(A.vec_size(), np.float64)
     _lib.check(_lib.load().h2b_tree_multiply(A._h, xhat.ctypes.data, out.ctypes.data,
                                              _lib.PTR_HOST))
     return out

@@ -135,20 +135,28 @@ uint64_t Matrix::footprint() const {
   uint64_t e = uint64_t(dense.nb) * dense.br * dense.bc + uint64_t(own_count(q)) * m * rank[q];
   for (int l = 0; l <= q; ++l) e += uint64_t(cpl[l].nb) * cpl[l].br * cpl[l].bc;
   for (int l = 1; l <= q; ++l) e += uint64_t(tr_count(l)) * rank[l] * rank[l - 1];
+  if (!symmetric) {  // the column basis counts too (h2_matrix.hpp:97-100)
+    const Matrix& C = *colb;
+    e += uint64_t(own_count(q)) * m * C.rank[q];
+    for (int l = 1; l <= q; ++l) e += uint64_t(tr_count(l)) * C.rank[l] * C.rank[l - 1];
+  }
   return e * sizeof(double);
 }
 
 uint64_t Matrix::device_bytes() const {
   return perm.bytes() + leaf.bytes() + transfer.bytes() + cpl_val.bytes() + dense_val.bytes() +
          cpl_rp.bytes() + cpl_ci.bytes() + dense_rp.bytes() + dense_ci.bytes() + work.bytes() +
-         xc.bytes() + yc.bytes() + xhat.bytes() + yhat.bytes() + xs.bytes() + ys.bytes();
+         xc.bytes() + yc.bytes() + xhat.bytes() + yhat.bytes() + xs.bytes() + ys.bytes() +
+         (colb ? colb->device_bytes() : 0);
 }
 
 double Matrix::hmv_flops() const {
   // flops.hpp:29-47 over the call sequence of hmv.hpp:175-188.
   double f = 2.0 * dense.br * dense.bc * double(dense.nb);
-  f += 2.0 * m * rank[q] * double(nodes(q)) * 2;  // leaf gemv up + down
-  for (int l = 1; l <= q; ++l) f += 2.0 * rank[l] * rank[l - 1] * double(nodes(l)) * 2;
+  const Matrix& C = col_basis();
+  f += 2.0 * m * (rank[q] + C.rank[q]) * double(nodes(q));  // leaf gemv down (U) + up (V)
+  for (int l = 1; l <= q; ++l)
+    f += 2.0 * (rank[l] * rank[l - 1] + C.rank[l] * C.rank[l - 1]) * double(nodes(l));
   for (int l = 0; l <= q; ++l)
     if (cpl[l].nb) f += 2.0 * cpl[l].br * cpl[l].bc * double(cpl[l].nb);
   return f;
@@ -209,6 +217,36 @@ void allocate(Matrix& A) {
   A.ys.alloc(A.n);
 }
 
+// Column basis of a non-symmetric matrix: leaf / transfer pools for the
+// column ranks plus the x^ side of the workspace (the upsweep runs on it).
+void allocate_col(Matrix& A, const int32_t* cranks) {
+  const int q = A.q;
+  A.symmetric = false;
+  A.colb.reset(new Matrix);
+  Matrix& C = *A.colb;
+  C.device = A.device;
+  C.stream = nullptr;  // borrowed: A's stream is passed explicitly
+  C.n = A.n;
+  C.m = A.m;
+  C.q = q;
+  C.ldm = A.ldm;
+  C.rank.assign(cranks, cranks + q + 1);
+  C.perm.alloc(A.n);
+  C.leaf.alloc(size_t(C.own_count(q)) * C.leaf_stride());
+  C.tr_off.assign(q + 2, 0);
+  int64_t t = 0;
+  for (int l = 1; l <= q; ++l) {
+    C.tr_off[l] = t;
+    t += C.tr_count(l) * C.tr_stride(l);
+  }
+  C.tr_off[q + 1] = t;
+  C.transfer.alloc(t);
+  C.vec_off.assign(q + 2, 0);
+  for (int l = 0; l <= q; ++l) C.vec_off[l + 1] = C.vec_off[l] + C.nodes(l) * C.rank[l];
+  C.xc.alloc(A.n);
+  C.xhat.alloc(std::max<int64_t>(1, C.vec_off[q + 1]));
+}
+
 // Upload the CSR structure of every layer and build the fused work list.
 // Mirror map of the coupling levels (used by the symmetric projection of
 // compress()): mirror[b] = index of block (col, row) for block b = (row, col)
@@ -223,7 +261,7 @@ void build_mirror(Matrix& A) {
   for (int l = 0; l <= q; ++l) {
     const Layer& L = A.cpl[l];
     std::vector<int32_t> mir(L.nb, -1);
-    bool ok = A.part_s == 0 && L.nb > 0;  // a partition handle does not hold the mirror rows
+    bool ok = A.part_s == 0 && L.nb > 0 && A.symmetric;  // a partition handle does not hold the mirror rows
     if (ok) {
       // transposed pattern: for row c, the blocks (r, c) in increasing r
       std::vector<int64_t> tp(L.rows + 1, 0);
@@ -364,9 +402,15 @@ void set_layer_structure(Layer& L, int64_t rows, int br, int bc, const int32_t* 
 }
 
 h2b_matrix* create_from_desc(const h2b_matrix_desc& d, int device) {
-  require(d.symmetric == 1, "only symmetric H2 matrices are supported (construct() is always symmetric)");
+  require(d.symmetric == 0 || d.symmetric == 1, "symmetric must be 0 or 1");
   require(d.perm && d.ranks && d.leaf && d.cpl_row_ptr && d.dense_row_ptr, "null pointer in descriptor");
   check_shape(d.n, d.m, d.depth, d.ranks);
+  const bool sym = d.symmetric == 1;
+  if (!sym) {
+    require(d.col_ranks && d.col_leaf, "non-symmetric descriptor: null column basis");
+    check_shape(d.n, d.m, d.depth, d.col_ranks);
+    require(d.m >= 1, "leaf size must be positive");
+  }
   need_device(device);
   std::unique_ptr<h2b_matrix> A(new h2b_matrix);
   A->device = device;
@@ -380,14 +424,25 @@ h2b_matrix* create_from_desc(const h2b_matrix_desc& d, int device) {
   const int32_t* rp = d.cpl_row_ptr;
   const int32_t* ci = d.cpl_col_idx;
   for (int l = 0; l <= q; ++l) {
-    set_layer_structure(A->cpl[l], A->nodes(l), A->rank[l], A->rank[l], rp, ci);
+    set_layer_structure(A->cpl[l], A->nodes(l), A->rank[l], sym ? A->rank[l] : d.col_ranks[l], rp, ci);
     rp += A->nodes(l) + 1;
     ci += A->cpl[l].nb;
   }
   set_layer_structure(A->dense, A->nodes(q), A->m, A->m, d.dense_row_ptr, d.dense_col_idx);
   for (int t = 0; t < d.n; ++t) require(d.perm[t] >= 0 && d.perm[t] < d.n, "perm out of range");
   allocate(*A);
+  if (!sym) allocate_col(*A, d.col_ranks);
   cudaStream_t s = A->stream;
+  if (!sym) {
+    Matrix& C = *A->colb;
+    H2B_CUDA(cudaMemcpyAsync(C.perm.p, d.perm, size_t(d.n) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    upload_blocks(d.col_leaf, C.leaf.p, C.m, C.rank[q], C.nodes(q), s);
+    const double* ct = d.col_transfer;
+    for (int l = 1; l <= q; ++l) {
+      upload_blocks(ct, C.transfer.p + C.tr_off[l], C.rank[l], C.rank[l - 1], C.nodes(l), s);
+      ct += C.nodes(l) * C.rank[l] * C.rank[l - 1];
+    }
+  }
   H2B_CUDA(cudaMemcpyAsync(A->perm.p, d.perm, size_t(d.n) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   upload_blocks(d.leaf, A->leaf.p, A->m, A->rank[q], A->nodes(q), s);
   const double* tr = d.transfer;
@@ -424,10 +479,11 @@ void hmv_device(Matrix& A, const double* x, double* y, double alpha, double beta
   const int q = A.q;
   cudaEvent_t* ev = timing_slots(A);
   if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
-  launch_up_leaf(A, x, s);
-  for (int l = q; l >= 1; --l) launch_up_level(A, l, s);
+  Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
+  launch_up_leaf(C, x, s);
+  for (int l = q; l >= 1; --l) launch_up_level(C, l, s);
   if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
-  launch_bsr(A, A.work.p, A.nwork, A.xc.p, A.yc.p, A.xhat.p, A.yhat.p, s);
+  launch_bsr(A, A.work.p, A.nwork, C.xc.p, A.yc.p, C.xhat.p, A.yhat.p, s, &C);
   if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
   for (int l = 1; l <= q; ++l) launch_down_level(A, l, s);
   launch_down_leaf(A, y, alpha, beta, true, s);
@@ -491,6 +547,11 @@ void hmv(Matrix& A, const double* x, double* y, double alpha, double beta, h2b_p
 
 void whole(const Matrix& A, const char* what) {
   require(A.part_s == 0, std::string(what) + ": not supported on a partition handle");
+}
+
+void symmetric_only(const Matrix& A, const char* what) {
+  if (!A.symmetric)
+    throw Error(H2B_UNSUPPORTED, std::string(what) + ": non-symmetric matrices are not implemented on this path");
 }
 
 // Phase helpers take host or device pointers; host data goes through
@@ -591,9 +652,10 @@ h2b_status h2b_matrix_info_get(const h2b_matrix* Ah, h2b_matrix_info* info) {
     info->n = A.n;
     info->m = A.m;
     info->depth = A.q;
-    info->symmetric = 1;
+    info->symmetric = A.symmetric ? 1 : 0;
     for (int l = 0; l <= A.q; ++l) {
       info->ranks[l] = A.rank[l];
+      info->col_ranks[l] = A.col_basis().rank[l];
       info->cpl_blocks[l] = A.cpl[l].nb;
       info->cpl_max_row[l] = A.cpl[l].max_row;
     }
@@ -648,6 +710,24 @@ h2b_status h2b_matrix_export(const h2b_matrix* Ah, int32_t* perm, double* leaf, 
   });
 }
 
+h2b_status h2b_matrix_export_col(const h2b_matrix* Ah, double* col_leaf, double* col_transfer) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    const Matrix& A = *Ah;
+    require(!A.symmetric, "h2b_matrix_export_col: the matrix is symmetric (column basis == row basis)");
+    DeviceGuard g(A.device);
+    cudaStream_t s = A.stream;
+    const Matrix& C = *A.colb;
+    const int q = A.q;
+    if (col_leaf) download_blocks(C.leaf.p, col_leaf, C.m, C.rank[q], C.nodes(q), s);
+    if (col_transfer)
+      for (int l = 1; l <= q; ++l) {
+        download_blocks(C.transfer.p + C.tr_off[l], col_transfer, C.rank[l], C.rank[l - 1], C.nodes(l), s);
+        col_transfer += C.nodes(l) * C.rank[l] * C.rank[l - 1];
+      }
+  });
+}
+
 h2b_status h2b_hmv(h2b_matrix* Ah, const double* x, double* y, double alpha, double beta,
                    h2b_ptr_kind kind, void* stream) {
   return guarded([&] {
@@ -660,6 +740,7 @@ h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx,
                          int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream) {
   return guarded([&] {
     require(Ah, "null matrix");
+    symmetric_only(*Ah, "h2b_hmv_multi");
     Matrix& A = *Ah;
     whole(A, "h2b_hmv_multi");
     require(nvec >= 0 && ldx >= A.n && ldy >= A.n, "hmv_multi: bad leading dimension");
@@ -706,11 +787,12 @@ h2b_status h2b_upsweep(h2b_matrix* Ah, const double* xc, double* xhat, h2b_ptr_k
     const bool dev = resolve_device(kind, xc);
     Staged si, so;
     const double* xin = stage_in(si, xc, A.n, dev, s);
-    launch_up_leaf(A, xin, s, /*cluster_order=*/true);
-    for (int l = A.q; l >= 1; --l) launch_up_level(A, l, s);
-    double* out = stage_out(so, xhat, A.vec_off[A.q + 1], resolve_device(kind, xhat), false, s);
-    if (A.vec_off[A.q + 1])
-      H2B_CUDA(cudaMemcpyAsync(out, A.xhat.p, A.vec_off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    Matrix& C = A.col_basis();  // upsweep(A.col_basis(), ...) (hmv.hpp:182)
+    launch_up_leaf(C, xin, s, /*cluster_order=*/true);
+    for (int l = A.q; l >= 1; --l) launch_up_level(C, l, s);
+    double* out = stage_out(so, xhat, C.vec_off[A.q + 1], resolve_device(kind, xhat), false, s);
+    if (C.vec_off[A.q + 1])
+      H2B_CUDA(cudaMemcpyAsync(out, C.xhat.p, C.vec_off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToDevice, s));
     finish_out(so, s);
   });
 }
@@ -722,9 +804,10 @@ h2b_status h2b_tree_multiply(h2b_matrix* Ah, const double* xhat, double* yhat, h
     whole(A, "h2b_tree_multiply");
     DeviceGuard g(A.device);
     cudaStream_t s = A.stream;
-    const size_t nv = A.vec_off[A.q + 1];
+    const Matrix& C = A.col_basis();
+    const size_t nv = A.vec_off[A.q + 1], nx = C.vec_off[A.q + 1];
     Staged si, so;
-    const double* xin = stage_in(si, xhat, nv, resolve_device(kind, xhat), s);
+    const double* xin = stage_in(si, xhat, nx, resolve_device(kind, xhat), s);
     double* out = stage_out(so, yhat, nv, resolve_device(kind, yhat), false, s);
     // coupling layers only: work items with layer index <= q
     std::vector<const Layer*> layers;
@@ -734,7 +817,7 @@ h2b_status h2b_tree_multiply(h2b_matrix* Ah, const double* xhat, double* yhat, h
     dw.alloc(w.size());
     if (!w.empty())
       H2B_CUDA(cudaMemcpyAsync(dw.p, w.data(), w.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    launch_bsr(A, dw.p, int64_t(w.size()), nullptr, nullptr, xin, out, s);
+    launch_bsr(A, dw.p, int64_t(w.size()), nullptr, nullptr, xin, out, s, &C);
     finish_out(so, s);
   });
 }
@@ -786,6 +869,7 @@ h2b_status h2b_compress(h2b_matrix* Ah, double eps, h2b_compress_report* report)
   return guarded([&] {
     require(Ah, "null matrix");
     whole(*Ah, "h2b_compress");
+    symmetric_only(*Ah, "h2b_compress");
     compress_matrix(*Ah, eps, report);
   });
 }
@@ -821,6 +905,7 @@ h2b_status h2b_orthogonalize(h2b_matrix* Ah, double* t_out) {
   return guarded([&] {
     require(Ah, "null matrix");
     whole(*Ah, "h2b_orthogonalize");
+    symmetric_only(*Ah, "h2b_orthogonalize");
     orthogonalize_matrix(*Ah, t_out);
   });
 }
@@ -838,7 +923,7 @@ h2b_status h2b_workspace(h2b_matrix* Ah, int which, void** ptr, int64_t* count) 
     require(Ah && ptr && count, "null argument");
     Matrix& A = *Ah;
     switch (which) {
-      case H2B_WS_XHAT: *ptr = A.xhat.p; *count = A.vec_off[A.q + 1]; break;
+      case H2B_WS_XHAT: *ptr = A.col_basis().xhat.p; *count = A.col_basis().vec_off[A.q + 1]; break;
       case H2B_WS_YHAT: *ptr = A.yhat.p; *count = A.vec_off[A.q + 1]; break;
       case H2B_WS_XC: *ptr = A.xc.p; *count = A.n; break;
       case H2B_WS_PERM: *ptr = A.perm.p; *count = A.n; break;

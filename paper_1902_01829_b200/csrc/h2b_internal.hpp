@@ -161,6 +161,15 @@ struct Matrix {
   int part_s = 0, part_g = 0;
   uint64_t global_footprint = 0;    // memory_footprint of the whole matrix
 
+  // Non-symmetric matrices (U != V, h2_matrix.hpp:69,75-78): the column basis
+  // V / F lives in colb, a basis-only Matrix (n, m, q, ldm, rank, perm, leaf,
+  // transfer, tr_off, and its own x^ workspace: xc, xhat, vec_off); coupling
+  // blocks of level l are rank[l] x colb->rank[l].  Symmetric: colb is null.
+  bool symmetric = true;
+  std::unique_ptr<Matrix> colb;
+  const Matrix& col_basis() const { return symmetric ? *this : *colb; }
+  Matrix& col_basis() { return symmetric ? *this : *colb; }
+
   ~Matrix();
   int64_t nodes(int l) const { return int64_t(1) << l; }
   int64_t own_begin(int l) const { return l < part_s ? 0 : int64_t(part_g) << (l - part_s); }
@@ -180,8 +189,9 @@ struct Matrix {
 void launch_up_leaf(const Matrix& A, const double* x, cudaStream_t s, bool cluster_order = false);
 // parents at level l-1 in [p0, p1) (children in the transfer pool)
 void launch_up_level(const Matrix& A, int l, cudaStream_t s, int64_t p0 = 0, int64_t p1 = -1);
+// x^ level offsets from xb (the column basis' vec_off), y^ from A.
 void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
-                double* ydense, const double* xh, double* yh, cudaStream_t s);
+                double* ydense, const double* xh, double* yh, cudaStream_t s, const Matrix* xb = nullptr);
 // children at level l in [c0, c1)
 void launch_down_level(const Matrix& A, int l, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1);
 // to_user: y[perm[t]] = alpha v + beta y[perm[t]] (original order); else y[t] = v

@@ -285,7 +285,7 @@ void save_matrix(const Matrix& A, const std::string& path, const h2b_build_info*
     SectionWriter w(os);  // meta
     w.put(int64_t(A.n));
     w.put(int32_t(A.m));
-    w.put(uint8_t(1));
+    w.put(uint8_t(A.symmetric ? 1 : 0));
     w.put(int32_t(bi.dim));
     w.put(uint64_t(bi.seed));
     w.put(bi.perturbation);
@@ -295,21 +295,25 @@ void save_matrix(const Matrix& A, const std::string& path, const h2b_build_info*
     w.finish();
   }
   {
-    SectionWriter w(os);  // trees + ranks + bases
+    SectionWriter w(os);  // trees + ranks + bases (row basis, then the column basis if any)
     std::vector<int32_t> parent, head, next, lp;
     flat_tree(q, parent, head, next, lp);
-    w.put_vec(parent.data(), parent.size());
-    w.put_vec(head.data(), head.size());
-    w.put_vec(next.data(), next.size());
-    w.put_vec(lp.data(), lp.size());
-    std::vector<int32_t> ranks(A.rank.begin(), A.rank.end());
-    w.put_vec(ranks.data(), ranks.size());
-    w.put(int32_t(A.m));
-    put_device_blocks(w, A.leaf.p, A.m, A.rank[q], A.nodes(q), s, host);
-    w.put(uint64_t(q + 1));
-    w.put(uint64_t(0));  // transfer[0] unused
-    for (int l = 1; l <= q; ++l)
-      put_device_blocks(w, A.transfer.p + A.tr_off[l], A.rank[l], A.rank[l - 1], A.nodes(l), s, host);
+    auto put_basis = [&](const Matrix& B) {  // io_detail::put_basis
+      w.put_vec(parent.data(), parent.size());
+      w.put_vec(head.data(), head.size());
+      w.put_vec(next.data(), next.size());
+      w.put_vec(lp.data(), lp.size());
+      std::vector<int32_t> ranks(B.rank.begin(), B.rank.end());
+      w.put_vec(ranks.data(), ranks.size());
+      w.put(int32_t(B.m));
+      put_device_blocks(w, B.leaf.p, B.m, B.rank[q], B.nodes(q), s, host);
+      w.put(uint64_t(q + 1));
+      w.put(uint64_t(0));  // transfer[0] unused
+      for (int l = 1; l <= q; ++l)
+        put_device_blocks(w, B.transfer.p + B.tr_off[l], B.rank[l], B.rank[l - 1], B.nodes(l), s, host);
+    };
+    put_basis(A);
+    if (!A.symmetric) put_basis(*A.colb);
     w.finish();
   }
   {
@@ -382,26 +386,34 @@ h2b_matrix* load_matrix(const std::string& path, int device, h2b_build_info* inf
     bi.eta = r.get<double>();
     bi.grid_order = r.get<int32_t>();
   }
-  if (!symmetric) throw Error(H2B_UNSUPPORTED, "non-symmetric H2 matrices are not supported (construct() is always symmetric)");
-  std::vector<int32_t> ranks;
-  std::vector<double> leaf, transfer;
+  std::vector<int32_t> ranks, cranks;
+  std::vector<double> leaf, transfer, cleaf, ctransfer;
   int depth;
   {
     auto buf = read_section(is);
     Reader r{buf.data(), buf.data() + buf.size()};
-    for (int k = 0; k < 4; ++k) r.get_vec<int32_t>();  // the complete binary tree is implied
-    ranks = r.get_vec<int32_t>();
-    depth = int(ranks.size()) - 1;
-    require(depth >= 0 && depth < 31, "load: bad depth");
-    require(r.get<int32_t>() == m, "load: leaf_dim != m");
-    leaf = r.get_vec<double>();
-    const uint64_t nt = r.get<uint64_t>();
-    require(nt == uint64_t(depth + 1), "load: transfer levels != depth + 1");
-    for (uint64_t l = 0; l < nt; ++l) {
-      const auto t = r.get_vec<double>();
-      transfer.insert(transfer.end(), t.begin(), t.end());
+    auto get_basis = [&](std::vector<int32_t>& rk, std::vector<double>& lf, std::vector<double>& tr) {
+      for (int k = 0; k < 4; ++k) r.get_vec<int32_t>();  // the complete binary tree is implied
+      rk = r.get_vec<int32_t>();
+      depth = int(rk.size()) - 1;
+      require(depth >= 0 && depth < 31, "load: bad depth");
+      require(r.get<int32_t>() == m, "load: leaf_dim != m");
+      lf = r.get_vec<double>();
+      const uint64_t nt = r.get<uint64_t>();
+      require(nt == uint64_t(depth + 1), "load: transfer levels != depth + 1");
+      for (uint64_t l = 0; l < nt; ++l) {
+        const auto t = r.get_vec<double>();
+        tr.insert(tr.end(), t.begin(), t.end());
+      }
+    };
+    get_basis(ranks, leaf, transfer);
+    if (!symmetric) {
+      const int rd = depth;
+      get_basis(cranks, cleaf, ctransfer);
+      require(depth == rd, "load: column basis depth != row basis depth");
     }
   }
+  const std::vector<int32_t>& colr = symmetric ? ranks : cranks;
   std::vector<int32_t> rp, ci;
   std::vector<double> vals;
   {
@@ -411,7 +423,7 @@ h2b_matrix* load_matrix(const std::string& path, int device, h2b_build_info* inf
     require(nl == uint64_t(depth + 1), "load: coupling levels != depth + 1");
     for (uint64_t l = 0; l < nl; ++l) {
       LayerIn L = get_layer(r);
-      require(L.brows == ranks[l] && L.bcols == ranks[l], "load: coupling block dims != ranks");
+      require(L.brows == ranks[l] && L.bcols == colr[l], "load: coupling block dims != ranks");
       require(L.row_ptr.size() == (size_t(1) << l) + 1, "load: coupling row_ptr size");
       rp.insert(rp.end(), L.row_ptr.begin(), L.row_ptr.end());
       ci.insert(ci.end(), L.col_idx.begin(), L.col_idx.end());
@@ -436,7 +448,10 @@ h2b_matrix* load_matrix(const std::string& path, int device, h2b_build_info* inf
   d.n = int32_t(n);
   d.m = m;
   d.depth = depth;
-  d.symmetric = 1;
+  d.symmetric = symmetric ? 1 : 0;
+  d.col_ranks = symmetric ? nullptr : cranks.data();
+  d.col_leaf = symmetric ? nullptr : cleaf.data();
+  d.col_transfer = symmetric ? nullptr : ctransfer.data();
   d.perm = perm.data();
   d.ranks = ranks.data();
   d.leaf = leaf.data();

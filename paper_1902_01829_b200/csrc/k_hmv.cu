@@ -414,8 +414,9 @@ void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, boo
 }
 
 void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
-                double* ydense, const double* xh, double* yh, cudaStream_t s) {
+                double* ydense, const double* xh, double* yh, cudaStream_t s, const Matrix* xb) {
   if (nwork == 0) return;
+  const std::vector<int64_t>& xoff = xb ? xb->vec_off : A.vec_off;
   LayerTable T{};
   for (int l = 0; l <= A.q; ++l) {
     const Layer& L = A.cpl[l];
@@ -423,7 +424,7 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
     d.val = L.val;
     d.rp = L.rp;
     d.ci = L.ci;
-    d.x = xh + A.vec_off[l];
+    d.x = xh + xoff[l];
     d.y = yh + A.vec_off[l];
     d.stride = L.block_stride();
     d.br = L.br;

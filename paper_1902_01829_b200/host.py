@@ -10,6 +10,10 @@ with every per-level ``std::vector`` pool concatenated over levels:
                                           ranks[l] x ranks[l-1]
 * ``cpl_row_ptr / cpl_col_idx / cpl_values`` -- MatrixTree::levels[l] (BSRLayer, bsr.hpp:13-31)
 * ``dense_row_ptr / dense_col_idx / dense_values`` -- H2Matrix::dense
+* ``col_ranks / col_leaf / col_transfer`` -- the column basis V / F of a
+  non-symmetric matrix (H2Matrix::col_basis_store, h2_matrix.hpp:69,75-78);
+  None when symmetric.  Coupling blocks of level l are then
+  ranks[l] x col_ranks[l].
 
 All blocks are column-major; values are float64, indices int32 (index_t,
 include/h2kit/defs.hpp:15).
@@ -37,6 +41,16 @@ class HostMatrix:
     dense_col_idx: np.ndarray
     dense_values: np.ndarray
     meta: dict = field(default_factory=dict)
+    col_ranks: np.ndarray | None = None
+    col_leaf: np.ndarray | None = None
+    col_transfer: np.ndarray | None = None
+
+    @property
+    def symmetric(self) -> bool:
+        return self.col_ranks is None
+
+    def cranks(self) -> np.ndarray:
+        return self.ranks if self.col_ranks is None else self.col_ranks
 
     # -- layout helpers -------------------------------------------------
     def nodes(self, l: int) -> int:
@@ -63,10 +77,11 @@ class HostMatrix:
         """Coupling blocks of level l as an array (nb, k, k) in column-major blocks
         (block[b][:, j] is column j)."""
         nb = self.cpl_blocks()
-        k = int(self.ranks[l])
-        o = sum(nb[j] * int(self.ranks[j]) ** 2 for j in range(l))
-        v = self.cpl_values[o:o + nb[l] * k * k]
-        return v.reshape(nb[l], k, k).transpose(0, 2, 1)
+        c = self.cranks()
+        k, kc = int(self.ranks[l]), int(c[l])
+        o = sum(nb[j] * int(self.ranks[j]) * int(c[j]) for j in range(l))
+        v = self.cpl_values[o:o + nb[l] * k * kc]
+        return v.reshape(nb[l], kc, k).transpose(0, 2, 1)
 
     def transfer_level(self, l: int) -> np.ndarray:
         """Transfers of level l as (2^l, k_l, k_{l-1})."""
@@ -87,36 +102,47 @@ class HostMatrix:
 
     def footprint(self) -> int:
         """memory_footprint(A).total() (h2_matrix.hpp:90-102)."""
-        return 8 * int(self.dense_values.size + self.cpl_values.size + self.leaf.size
-                       + self.transfer.size)
+        f = self.dense_values.size + self.cpl_values.size + self.leaf.size + self.transfer.size
+        if not self.symmetric:
+            f += self.col_leaf.size + self.col_transfer.size
+        return 8 * int(f)
 
     def hmv_flops(self) -> float:
         """Reference analytic flop model of one hmv (flops.hpp:29-47)."""
         q, m = self.depth, self.m
         r = [int(v) for v in self.ranks]
+        c = [int(v) for v in self.cranks()]
         nbd = int(self.dense_row_ptr[-1])
-        f = 2.0 * m * m * nbd + 2 * (2.0 * m * r[q] * self.nodes(q))
+        f = 2.0 * m * m * nbd + 2.0 * m * (r[q] + c[q]) * self.nodes(q)
         for l in range(1, q + 1):
-            f += 2 * (2.0 * r[l] * r[l - 1] * self.nodes(l))
+            f += 2.0 * (r[l] * r[l - 1] + c[l] * c[l - 1]) * self.nodes(l)
         for l, nb in enumerate(self.cpl_blocks()):
             if nb:
-                f += 2.0 * r[l] * r[l] * nb
+                f += 2.0 * r[l] * c[l] * nb
         return f
 
     def copy(self) -> "HostMatrix":
+        cp = lambda a: None if a is None else np.array(a, copy=True)  # noqa: E731
         return HostMatrix(self.n, self.m, self.depth, *(np.array(a, copy=True) for a in (
             self.ranks, self.perm, self.leaf, self.transfer, self.cpl_row_ptr, self.cpl_col_idx,
             self.cpl_values, self.dense_row_ptr, self.dense_col_idx, self.dense_values)),
-            meta=dict(self.meta))
+            meta=dict(self.meta), col_ranks=cp(self.col_ranks), col_leaf=cp(self.col_leaf),
+            col_transfer=cp(self.col_transfer))
 
     @staticmethod
-    def empty(n, m, depth, ranks, cpl_blocks, dense_blocks) -> "HostMatrix":
+    def empty(n, m, depth, ranks, cpl_blocks, dense_blocks, col_ranks=None) -> "HostMatrix":
         ranks = np.asarray(ranks, dtype=np.int32)
+        c = ranks if col_ranks is None else np.asarray(col_ranks, dtype=np.int32)
         nl = 1 << depth
         ntr = sum((1 << l) * int(ranks[l]) * int(ranks[l - 1]) for l in range(1, depth + 1))
         nrp = sum((1 << l) + 1 for l in range(depth + 1))
         nci = int(sum(cpl_blocks))
-        nsv = int(sum(int(b) * int(ranks[l]) ** 2 for l, b in enumerate(cpl_blocks)))
+        nsv = int(sum(int(b) * int(ranks[l]) * int(c[l]) for l, b in enumerate(cpl_blocks)))
+        col = {}
+        if col_ranks is not None:
+            ctr = sum((1 << l) * int(c[l]) * int(c[l - 1]) for l in range(1, depth + 1))
+            col = dict(col_ranks=c, col_leaf=np.zeros(nl * m * int(c[depth]), np.float64),
+                       col_transfer=np.zeros(ctr, np.float64))
         return HostMatrix(
             n=n, m=m, depth=depth, ranks=ranks,
             perm=np.zeros(n, np.int32),
@@ -128,6 +154,7 @@ class HostMatrix:
             dense_row_ptr=np.zeros(nl + 1, np.int32),
             dense_col_idx=np.zeros(int(dense_blocks), np.int32),
             dense_values=np.zeros(int(dense_blocks) * m * m, np.float64),
+            **col,
         )
 
     def arrays(self):

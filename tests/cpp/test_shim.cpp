@@ -140,6 +140,43 @@ void orthogonalize_orthonormal() {  // acceptance c3 (leaf V^T V = I)
   CHECK(worst <= 1e-12);
 }
 
+// A non-symmetric matrix (col_basis_store, h2_matrix.hpp:69): V = U D with a
+// positive diagonal D_l per level, F_c = D_l^-1 E_c D_{l-1}, S' = S D_l^-1 --
+// the same operator, evaluated by the reference and through the shim.
+void nonsymmetric_hmv() {
+  H2Matrix<double> A = kernel_matrix(2, 4096, 4);
+  H2Matrix<double> B = A;
+  B.symmetric = false;
+  B.col_basis_store = A.row_basis;
+  BasisTree<double>& V = *B.col_basis_store;
+  const int q = A.depth();
+  std::vector<std::vector<double>> d(q + 1);
+  for (int l = 0; l <= q; ++l)
+    for (int j = 0; j < A.row_basis.ranks[l]; ++j) d[l].push_back(0.5 + 0.01 * ((7 * j + 3 * l) % 50));
+  const int m = A.m, kq = A.row_basis.ranks[q];
+  for (size_t i = 0; i < V.leaf_pool.size(); ++i) V.leaf_pool[i] *= d[q][(i / m) % kq];
+  for (int l = 1; l <= q; ++l) {
+    const int kc = A.row_basis.ranks[l], kp = A.row_basis.ranks[l - 1];
+    for (size_t e = 0; e < V.transfer[l].size(); ++e) {
+      const size_t i = e % kc, j = (e / kc) % kp;
+      V.transfer[l][e] *= d[l - 1][j] / d[l][i];
+    }
+  }
+  for (int l = 0; l <= q; ++l) {
+    auto& L = B.coupling.levels[l];
+    const int k = L.brows;
+    for (size_t e = 0; e < L.values.size(); ++e) L.values[e] /= d[l][(e / k) % k];
+  }
+  const index_t n = A.n;
+  std::vector<double> x(n), yr(n), yb(n), yg(n);
+  for (index_t i = 0; i < n; ++i) x[i] = std::sin(0.37 * i) + 1.0;
+  h2kit::hmv(A, x.data(), yr.data());
+  h2kit::hmv(B, x.data(), yb.data());
+  h2kit_b200::hmv(B, x.data(), yg.data());
+  CHECK(rel(yb, yr) <= 1e-13);
+  CHECK(rel(yg, yb) <= 1e-12);
+}
+
 void errors_are_invalid_argument() {
   H2Matrix<double> A = kernel_matrix(2, 1024, 8);
   bool threw = false;
@@ -162,6 +199,7 @@ int main() {
   run("phases match the reference", phases_match_reference);
   run("compress matches the reference", compress_matches_reference);
   run("orthogonalize gives orthonormal leaves", orthogonalize_orthonormal);
+  run("non-symmetric hmv matches the reference", nonsymmetric_hmv);
   run("invalid arguments throw std::invalid_argument", errors_are_invalid_argument);
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;

@@ -1,0 +1,100 @@
+"""GPU: non-symmetric matrices (U != V; h2_matrix.hpp:69,75-78, hmv.hpp:175-188:
+the upsweep runs on A.col_basis(), the downsweep on A.row_basis).
+
+* an operator-preserving column basis V = U D gives the symmetric matrix's
+  hmv (no oracle involved);
+* random column bases of other ranks: hmv and the phase entry points equal
+  the reference's on the imported matrix; footprint and flop model too;
+* containers: byte-identical to the reference's save, both directions;
+* compress / 16-vector hmv report H2B_UNSUPPORTED (this version)."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from nonsym import random_cols, scaled
+
+import paper_1902_01829_b200 as h2
+from paper_1902_01829_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(2, 1 << 12, 4), (3, 1 << 12, 3), (2, 1 << 13, 8)]
+
+
+@pytest.mark.parametrize("dim,n,order", CASES)
+def test_scaled_column_basis_is_the_same_operator(gpu, ref, dim, n, order):
+    R = ref.construct(dim, n, grid_order=order)
+    hm = R.to_host()
+    S = h2.H2Matrix.from_host(hm)
+    N = h2.H2Matrix.from_host(scaled(hm))
+    assert N.info().symmetric == 0 and S.info().symmetric == 1
+    x = np.random.default_rng(1).random(n)
+    ys, yn = h2.hmv(S, x), h2.hmv(N, x)
+    assert rel_err(yn, ys) <= 1e-13
+    assert rel_err(yn, R.hmv(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("dim,n,order", CASES)
+def test_random_column_basis_matches_reference(gpu, ref, dim, n, order):
+    hm = random_cols(ref.construct(dim, n, grid_order=order).to_host())
+    R = ref.from_host(hm)
+    A = h2.H2Matrix.from_host(hm)
+    inf = A.info()
+    assert list(inf.col_ranks)[:hm.depth + 1] == hm.col_ranks.tolist()
+    assert A.memory_footprint() == R.footprint() == hm.footprint()
+    assert inf.hmv_flops == pytest.approx(R.hmv_flops(), rel=1e-12)
+    rng = np.random.default_rng(5)
+    x = rng.random(n)
+    assert rel_err(h2.hmv(A, x), R.hmv(x)) <= 1e-12
+    y0 = rng.random(n)
+    assert rel_err(h2.hmv(A, x, y0.copy(), 2.0, -0.5), R.hmv(x, y0.copy(), 2.0, -0.5)) <= 1e-12
+
+
+def test_phase_entry_points_use_the_column_basis(gpu, ref):
+    n = 1 << 12
+    hm = random_cols(ref.construct(2, n, grid_order=4).to_host())
+    R = ref.from_host(hm)
+    A = h2.H2Matrix.from_host(hm)
+    xc = np.random.default_rng(9).random(n)
+    xh_ref = R.upsweep(xc)
+    xh = h2.upsweep(A, xc)
+    assert xh.size == xh_ref.size  # column-rank sized
+    assert rel_err(xh, xh_ref) <= 1e-13
+    yh_ref = R.tree_multiply(xh_ref)
+    yh = h2.tree_multiply(A, xh)
+    assert yh.size == yh_ref.size  # row-rank sized
+    assert rel_err(yh, yh_ref) <= 1e-13
+
+
+def test_export_roundtrip(gpu, ref):
+    hm = random_cols(ref.construct(3, 1 << 12, grid_order=3).to_host())
+    back = h2.H2Matrix.from_host(hm).to_host()
+    assert not back.symmetric
+    for a in ("ranks", "col_ranks", "perm", "leaf", "transfer", "col_leaf", "col_transfer",
+              "cpl_row_ptr", "cpl_col_idx", "cpl_values", "dense_row_ptr", "dense_col_idx",
+              "dense_values"):
+        assert np.array_equal(getattr(back, a), getattr(hm, a)), a
+
+
+def test_container_byte_identical_both_ways(gpu, ref, tmp_path):
+    n = 1 << 12
+    hm = random_cols(ref.construct(2, n, grid_order=4).to_host())
+    R = ref.from_host(hm)
+    A = h2.H2Matrix.from_host(hm)
+    ours, theirs = tmp_path / "ours.h2", tmp_path / "ref.h2"
+    A.save(ours)
+    R.save(str(theirs))
+    assert ours.read_bytes() == theirs.read_bytes()
+    B = h2.H2Matrix.load(theirs)
+    R2 = ref.load(str(ours))
+    x = np.random.default_rng(4).random(n)
+    assert rel_err(h2.hmv(B, x), R2.hmv(x)) <= 1e-12
+    assert B.info().symmetric == 0
+
+
+def test_unsupported_paths_say_so(gpu, ref):
+    hm = scaled(ref.construct(2, 1 << 12, grid_order=4).to_host())
+    A = h2.H2Matrix.from_host(hm)
+    with pytest.raises(_lib.H2bError) as e:
+        h2.compress(A, 1e-6)
+    assert e.value.code == _lib.H2B_UNSUPPORTED and "non-symmetric" in str(e.value)
