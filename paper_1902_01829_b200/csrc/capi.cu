@@ -869,7 +869,6 @@ h2b_status h2b_compress(h2b_matrix* Ah, double eps, h2b_compress_report* report)
   return guarded([&] {
     require(Ah, "null matrix");
     whole(*Ah, "h2b_compress");
-    symmetric_only(*Ah, "h2b_compress");
     compress_matrix(*Ah, eps, report);
   });
 }

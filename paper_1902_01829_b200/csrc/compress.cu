@@ -117,9 +117,10 @@ struct ProjLevel {
   const int32_t* rp;
   const int32_t* ci;
   const int32_t* mirror;  // symmetric levels: block index of (col, row), or null
-  const double* T;    // rn x ro per node, ld rn
-  int ro, rn, ld_old, ld_new;
-  int64_t ostride;
+  const double* T;    // row projections: rn x ro per node, ld rn
+  const double* Tc;   // column projections: cn x co per node, ld cn (== T when symmetric)
+  int ro, rn, co, cn, ld_old, ld_new;
+  int64_t ostride;    // old block stride (blocks are read from and written to the old slots)
 };
 struct ProjTable {
   ProjLevel L[kMaxLevels + 1];
@@ -137,9 +138,10 @@ struct ProjTable {
 // With TRI (orthogonalization: T are upper-triangular R factors) the
 // structurally zero fragments of both products are skipped.
 constexpr int kPLd = 68;  // smem leading dimension (== 4 mod 16: conflict-free fragments)
-// TS strip = Tr[i0:i0+8, :] S (8 x ro) of warp w, i0 = 8w (false: idle warp).
+// TS strip = Tr[i0:i0+8, :] S (8 x co) of warp w, i0 = 8w (false: idle warp).
 template <bool TRI>
-__device__ __forceinline__ bool ts_strip(const double* Tr, const double* Sb, int ro, int rn, double (&acc)[8][2]) {
+__device__ __forceinline__ bool ts_strip(const double* Tr, const double* Sb, int ro, int co, int rn,
+                                         double (&acc)[8][2]) {
   const int w = cta::warp(), t = cta::lane();
   const int fr = t >> 2, fk = t & 3;
   const int i0 = 8 * w;
@@ -154,7 +156,7 @@ __device__ __forceinline__ bool ts_strip(const double* Tr, const double* Sb, int
       const double a = Tr[i0 + fr + p * kPLd];
 #pragma unroll
       for (int y = 0; y < 8; ++y) {
-        if (8 * y < ro) {
+        if (8 * y < co) {
           const double b = Sb[p + (8 * y + fr) * kPLd];
           cta::dmma(acc[y][0], acc[y][1], a, b);
         }
@@ -164,15 +166,15 @@ __device__ __forceinline__ bool ts_strip(const double* Tr, const double* Sb, int
   return true;
 }
 
-// out strip = TS strip (8 x ro) T_col^T (ro x rn); TS's A fragments come from
+// out strip = TS strip (8 x co) T_col^T (co x cn); TS's A fragments come from
 // the accumulators by two quad shuffles per k-step (TS never touches smem).
 template <bool TRI>
 __device__ __forceinline__ void out_strip(const double (&acc)[8][2], const double* Tc, double* out, double* outT,
-                                          int ld_new, int ro, int rn, double& sumsq) {
+                                          int ld_new, int co, int rn, int cn, double& sumsq) {
   const int w = cta::warp(), t = cta::lane();
   const int fr = t >> 2, fk = t & 3;
   const int i0 = 8 * w;
-  const int kc_end = (ro + 3) >> 2;
+  const int kc_end = (co + 3) >> 2;
   double o[8][2];
 #pragma unroll
   for (int y = 0; y < 8; ++y) o[y][0] = o[y][1] = 0.0;
@@ -189,7 +191,7 @@ __device__ __forceinline__ void out_strip(const double (&acc)[8][2], const doubl
       const int p = 4 * kc + fk;
 #pragma unroll
       for (int y = 0; y < 8; ++y) {
-        if (8 * y < rn && (!TRI || 4 * kc + 3 >= 8 * y)) {
+        if (8 * y < cn && (!TRI || 4 * kc + 3 >= 8 * y)) {
           const double b = Tc[8 * y + fr + p * kPLd];  // T_col[j, p]
           cta::dmma(o[y][0], o[y][1], a, b);
         }
@@ -203,7 +205,7 @@ __device__ __forceinline__ void out_strip(const double (&acc)[8][2], const doubl
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int j = 8 * y + 2 * fk + v;
-        if (j < rn) {
+        if (j < cn) {
           out[i + int64_t(j) * ld_new] = o[y][v];
           if (outT) outT[j + int64_t(i) * ld_new] = o[y][v];  // mirror block (col, row)
           sumsq = fma(o[y][v], o[y][v], sumsq);
@@ -211,7 +213,7 @@ __device__ __forceinline__ void out_strip(const double (&acc)[8][2], const doubl
       }
   }
   if (ld_new > rn && w == 0)
-    for (int j = t; j < rn; j += 32) {
+    for (int j = t; j < cn; j += 32) {
       out[rn + int64_t(j) * ld_new] = 0.0;
       if (outT) outT[rn + int64_t(j) * ld_new] = 0.0;
     }
@@ -269,10 +271,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   extern __shared__ double sm[];
   const ProjRow pr = rows[blockIdx.x];
   const ProjLevel& L = P.L[pr.level];
-  const int ro = L.ro, rn = L.rn;
+  const int ro = L.ro, rn = L.rn, co = L.co, cn = L.cn;
   double* Tr = sm;                // rn x ro
-  double* Sb = Tr + 64 * kPLd;    // ro x ro
-  double* Tc = Sb + 64 * kPLd;    // rn x ro
+  double* Sb = Tr + 64 * kPLd;    // ro x co
+  double* Tc = Sb + 64 * kPLd;    // cn x co
   int* wcnt = reinterpret_cast<int*>(Tc + 64 * kPLd);  // kWarps
   int* blist = wcnt + 32;  // blocks to project
   int* clist = blist + P.max_row;  // their block columns
@@ -310,18 +312,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   }
   double ss = 0.0;
   if (nk > 0) {
-    stage64(Sb, L.S + int64_t(blist[0]) * L.ld_old * ro, L.ld_old, ro, ro);
+    stage64(Sb, L.S + int64_t(blist[0]) * L.ostride, L.ld_old, ro, co);
     cp_async_commit();  // {T_row, S_0}
-    stage64(Tc, L.T + int64_t(clist[0]) * rn * ro, rn, rn, ro);
+    stage64(Tc, L.Tc + int64_t(clist[0]) * cn * co, cn, cn, co);
     cp_async_commit();  // {T_col,0}
   }
   for (int k = 0; k < nk; ++k) {
     cp_async_wait<1>();  // S_k (T_col,k may still be in flight)
     __syncthreads();
     double acc[8][2];
-    const bool live = P.tri ? ts_strip<true>(Tr, Sb, ro, rn, acc) : ts_strip<false>(Tr, Sb, ro, rn, acc);
+    const bool live = P.tri ? ts_strip<true>(Tr, Sb, ro, co, rn, acc) : ts_strip<false>(Tr, Sb, ro, co, rn, acc);
     __syncthreads();  // S_k consumed
-    if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ld_old * ro, L.ld_old, ro, ro);
+    if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ostride, L.ld_old, ro, co);
     cp_async_commit();
     cp_async_wait<1>();  // T_col,k
     __syncthreads();
@@ -331,13 +333,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
     double s1 = 0.0;
     if (live) {
       if (P.tri)
-        out_strip<true>(acc, Tc, out, outT, L.ld_new, ro, rn, s1);
+        out_strip<true>(acc, Tc, out, outT, L.ld_new, co, rn, cn, s1);
       else
-        out_strip<false>(acc, Tc, out, outT, L.ld_new, ro, rn, s1);
+        out_strip<false>(acc, Tc, out, outT, L.ld_new, co, rn, cn, s1);
     }
     ss += outT ? 2.0 * s1 : s1;
     __syncthreads();  // T_col,k consumed
-    if (k + 1 < nk) stage64(Tc, L.T + int64_t(clist[k + 1]) * rn * ro, rn, rn, ro);
+    if (k + 1 < nk) stage64(Tc, L.Tc + int64_t(clist[k + 1]) * cn * co, cn, cn, co);
     cp_async_commit();
   }
   cp_async_wait<0>();
@@ -482,10 +484,22 @@ constexpr int kWWarps = 4;  // nodes (warps) per CTA
 struct WItem {
   int32_t node, b0, b1, out, par;
 };
+// Where the blocks of the stacks come from: row stacks hold S_b^T of the
+// blocks of a block row (trans = 1); column stacks (non-symmetric matrices,
+// the transposed layers of compression.hpp:493-522) hold S_b of the blocks of
+// a block column (trans = 0), listed by bidx.  sb: stack rows per block.
+struct WSrc {
+  const double* S;
+  int lds;
+  int64_t stride;
+  int sb;
+  int trans;
+  const int32_t* bidx;  // block of stack position p (null: p itself)
+};
 
-template <int NCOL, int CR>
+template <int NCOL, int CR, bool TRANS>
 __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __restrict__ P, int kc, int kp,
-                                                          const double* __restrict__ S, int lds,
+                                                          const __grid_constant__ WSrc src_blocks,
                                                           double* __restrict__ Rout, int out_t,
                                                           const WItem* __restrict__ items, int64_t nitems,
                                                           int* __restrict__ next) {
@@ -531,19 +545,32 @@ __global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __res
       }
       prow += nr;
     } else {
-      const int nr = min(CR, kc - brow);
+      const WSrc& W = src_blocks;
+      const int nr = min(CR, W.sb - brow);
+      const int64_t bb = W.bidx ? W.bidx[b] : b;
+      const int lds = W.lds;
+      if (TRANS) {  // stack rows = columns of S_b: row c of the block, coalesced over lanes
 #pragma unroll
-      for (int t = 0; t < NCOL; ++t) {
-        const int c = lane + 32 * t;
-        const double* src = S + int64_t(b) * lds * kc + c + int64_t(brow) * lds;
+        for (int t = 0; t < NCOL; ++t) {
+          const int c = lane + 32 * t;
+          const double* src = W.S + bb * W.stride + c + int64_t(brow) * lds;
 #pragma unroll
-        for (int i = 0; i < CR; ++i) {
-          B[t][i] = (c < kc && i < nr) ? __ldcs(src) : 0.0;
-          src += lds;
+          for (int i = 0; i < CR; ++i) {
+            B[t][i] = (c < kc && i < nr) ? __ldcs(src) : 0.0;
+            src += lds;
+          }
+        }
+      } else {  // stack rows = rows of S_b: column c of the block
+#pragma unroll
+        for (int t = 0; t < NCOL; ++t) {
+          const int c = lane + 32 * t;
+          const double* src = W.S + bb * W.stride + int64_t(c) * lds + brow;
+#pragma unroll
+          for (int i = 0; i < CR; ++i) B[t][i] = (c < kc && i < nr) ? __ldcs(src + i) : 0.0;
         }
       }
       brow += nr;
-      if (brow >= kc) {
+      if (brow >= W.sb) {
         brow = 0;
         ++b;
       }
@@ -1160,15 +1187,17 @@ void project_rows(const Matrix& A, Arena& ar, ProjRows& R, cudaStream_t s) {
 }
 
 // Level l with T(l) (T.rows[l] x T.cols[l] per node) on stream st.
-void project_level(const Matrix& A, const TreePool& T, const ProjRows& R, int l, bool tri, bool want_sum,
-                   Flops& fl, double& flops, const Part& pt, cudaStream_t st) {
+// Level l with T(l) (row projections, T.rows[l] x T.cols[l] per node) and
+// Tc(l) (column projections; the same tree when symmetric) on stream st.
+void project_level(const Matrix& A, const TreePool& T, const TreePool& Tc, const ProjRows& R, int l, bool tri,
+                   bool want_sum, Flops& fl, double& flops, const Part& pt, cudaStream_t st) {
   const Layer& L = A.cpl[l];
-  const int rn = T.rows[l], ro = T.cols[l];
+  const int rn = T.rows[l], ro = T.cols[l], cn = Tc.rows[l], co = Tc.cols[l];
   if (L.nb == 0) return;
-  require(ro == L.br && ro == L.bc, "project_coupling: dim mismatch");
-  if (pt.counts(l)) flops += fl.gemm(double(L.nb), rn, ro, ro) + fl.gemm(double(L.nb), rn, rn, ro);
+  require(ro == L.br && co == L.bc, "project_coupling: dim mismatch");
+  if (pt.counts(l)) flops += fl.gemm(double(L.nb), rn, co, ro) + fl.gemm(double(L.nb), rn, cn, co);
   const int64_t n = R.off[l + 1] - R.off[l];
-  if (rn == 0 || n == 0) return;
+  if (rn == 0 || cn == 0 || n == 0) return;
   ProjTable P{};
   P.tri = tri ? 1 : 0;
   P.max_row = R.max_row;
@@ -1179,8 +1208,11 @@ void project_level(const Matrix& A, const TreePool& T, const ProjRows& R, int l,
   d.ci = L.ci;
   d.mirror = mirror_of(A, l);
   d.T = const_cast<TreePool&>(T).at(l);
+  d.Tc = const_cast<TreePool&>(Tc).at(l);
   d.ro = ro;
   d.rn = rn;
+  d.co = co;
+  d.cn = cn;
   d.ld_old = L.ld;
   d.ld_new = pad2(rn);
   d.out = L.val;  // in the old slots
@@ -1207,18 +1239,18 @@ double project_rowsum(const ProjRows& R, const Part& pt, cudaStream_t s) {
 
 // After every level's launch completed (stream order on s): compaction of the
 // shrunken blocks (not in_place) and the new layer shapes.
-void project_finish(Matrix& A, const TreePool& T, bool in_place, Arena& ar, cudaStream_t s) {
+void project_finish(Matrix& A, const TreePool& T, const TreePool& Tc, bool in_place, Arena& ar, cudaStream_t s) {
   const int q = A.q;
   std::vector<int64_t> new_off(q + 2, 0);
   for (int l = 0; l <= q; ++l)
-    new_off[l + 1] = new_off[l] + A.cpl[l].nb * int64_t(pad2(T.rows[l])) * T.rows[l];
+    new_off[l + 1] = new_off[l] + A.cpl[l].nb * int64_t(pad2(T.rows[l])) * Tc.rows[l];
   if (!in_place) {
     // compaction: level by level, block order, chunks staged in the arena
     double* temp = ar.base + ar.off;
     const int64_t cap = int64_t(ar.cap - ar.off);
     for (int l = 0; l <= q; ++l) {
       const Layer& L = A.cpl[l];
-      const int64_t bs_new = int64_t(pad2(T.rows[l])) * T.rows[l], bs_old = L.block_stride();
+      const int64_t bs_new = int64_t(pad2(T.rows[l])) * Tc.rows[l], bs_old = L.block_stride();
       if (L.nb == 0 || bs_new == 0) continue;
       const int64_t per = std::max<int64_t>(1, cap / bs_new);
       const int64_t old_off = L.val - A.cpl_val.p;
@@ -1248,7 +1280,8 @@ void project_finish(Matrix& A, const TreePool& T, bool in_place, Arena& ar, cuda
   H2B_CUDA(cudaStreamSynchronize(s));
   for (int l = 0; l <= q; ++l) {
     Layer& L = A.cpl[l];
-    L.br = L.bc = T.rows[l];
+    L.br = T.rows[l];
+    L.bc = Tc.rows[l];
     L.ld = pad2(L.br);
     L.val = A.cpl_val.p + new_off[l];
   }
@@ -1274,11 +1307,13 @@ int weights_slots(int device, int kc) {
   constexpr int CR = 32;
   const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
   if (kc > 32) {
-    set_smem(k_weights<2, CR>, sm);
-    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<2, CR>, 32 * kWWarps, sm));
+    set_smem(k_weights<2, CR, true>, sm);
+    set_smem(k_weights<2, CR, false>, sm);
+    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<2, CR, true>, 32 * kWWarps, sm));
   } else {
-    set_smem(k_weights<1, CR>, sm);
-    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<1, CR>, 32 * kWWarps, sm));
+    set_smem(k_weights<1, CR, true>, sm);
+    set_smem(k_weights<1, CR, false>, sm);
+    H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_weights<1, CR, true>, 32 * kWWarps, sm));
   }
   return sms * std::max(1, per_sm) * kWWarps;
 }
@@ -1286,13 +1321,18 @@ int weights_slots(int device, int kc) {
 size_t weights_arena_need(const Matrix& A) {
   size_t pmax = 1, items = 2;
   const int slots = weights_slots(A.device, 64);
+  const Matrix& Cb = A.col_basis();
   for (int l = 1; l <= A.q; ++l) {
-    pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
+    pmax = std::max({pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l],
+                     size_t(A.nodes(l)) * Cb.rank[l - 1] * Cb.rank[l]});
     items = std::max(items, size_t(std::max<int64_t>(A.own_count(l), slots)) + 2);
   }
-  // P, segment R's (<= slots + nodes), two item lists + counters
+  size_t nbmax = 1;
+  for (int l = 1; l <= A.q; ++l) nbmax = std::max(nbmax, size_t(A.cpl[l].nb));
+  // P, segment R's (<= slots + nodes), two item lists + counters, column-stack block list
   return Arena::need(pmax, sizeof(double)) + Arena::need(size_t(2 * items) * 64 * 64, sizeof(double)) +
-         2 * Arena::need(items * sizeof(WItem) / sizeof(int32_t) + 4, sizeof(int32_t));
+         2 * Arena::need(items * sizeof(WItem) / sizeof(int32_t) + 4, sizeof(int32_t)) +
+         Arena::need(4, 4) + Arena::need(nbmax, sizeof(int32_t));
 }
 
 // Weight tree (generate_weight_tree, compression.hpp:213-256), level by level
@@ -1301,13 +1341,34 @@ size_t weights_arena_need(const Matrix& A) {
 // warps (partial R's, stored transposed), then a merge launch re-triangularises
 // [R_0; ...; R_{nseg-1}] per node -- the same kernel, reading the partial R's
 // as blocks.  Items are issued longest first (LPT).
-void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, const Part& pt, double* tree_mem,
-             Arena& ar) {
+// Transposed structure of a coupling level (the column stacks of a
+// non-symmetric matrix, compression.hpp:497-520): for block column c, the
+// blocks (r, c) in increasing r at [cp[c], cp[c + 1]) of cb.
+void transpose_structure(const Layer& L, std::vector<int32_t>& cp, std::vector<int32_t>& cb, int& max_col) {
+  cp.assign(L.rows + 1, 0);
+  for (int64_t b = 0; b < L.nb; ++b) ++cp[L.h_ci[b] + 1];
+  for (int64_t c = 0; c < L.rows; ++c) cp[c + 1] += cp[c];
+  max_col = 0;
+  for (int64_t c = 0; c < L.rows; ++c) max_col = std::max(max_col, cp[c + 1] - cp[c]);
+  std::vector<int32_t> cur(cp.begin(), cp.end() - 1);
+  cb.assign(L.nb, 0);
+  for (int64_t r = 0; r < L.rows; ++r)
+    for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1]; ++b) cb[cur[L.h_ci[b]]++] = b;
+}
+
+// Weight tree of basis B (generate_weight_tree, compression.hpp:213-256):
+// B = A (row basis, row stacks of S^T) or, with col, A's column basis over
+// the transposed layers (column stacks of S).
+void weights(Matrix& A, Matrix& B, bool col, TreePool& R, cudaStream_t s, Flops& fl, double& flops, const Part& pt,
+             double* tree_mem, Arena& ar) {
   const int q = A.q;
-  R.alloc(A, A.rank, A.rank, tree_mem);
-  H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * A.rank[0] * A.rank[0], s));
-  size_t pmax = 1;
-  for (int l = 1; l <= q; ++l) pmax = std::max(pmax, size_t(A.nodes(l)) * A.rank[l - 1] * A.rank[l]);
+  R.alloc(B, B.rank, B.rank, tree_mem);
+  H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * B.rank[0] * B.rank[0], s));
+  size_t pmax = 1, nbmax = 1;
+  for (int l = 1; l <= q; ++l) {
+    pmax = std::max(pmax, size_t(B.nodes(l)) * B.rank[l - 1] * B.rank[l]);
+    nbmax = std::max(nbmax, size_t(A.cpl[l].nb));
+  }
   ar.off = 0;
   double* Pall = ar.take<double>(pmax);
   const int slots = weights_slots(A.device, 64);
@@ -1317,30 +1378,39 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, c
   WItem* ditems = ar.take<WItem>(maxitems);
   WItem* dmerge = ar.take<WItem>(maxitems);
   int* counters = ar.take<int>(4);
+  int32_t* dcb = col ? ar.take<int32_t>(nbmax) : nullptr;
   std::vector<WItem> items, merge;
+  std::vector<int32_t> cp, cb;
   for (int l = 1; l <= q; ++l) {
-    const int kc = A.rank[l], kp = A.rank[l - 1];
+    const int kc = B.rank[l], kp = B.rank[l - 1];
     const Layer& L = A.cpl[l];
-    const int ld_ref = kp + L.max_row * kc;  // the reference's padded stack height
-    flops += fl.gemm(double(A.nodes(l)), kp, kc, kp) + fl.qr(double(A.nodes(l)), ld_ref, kc);
+    int max_row = L.max_row;
+    if (col) transpose_structure(L, cp, cb, max_row);
+    const std::vector<int32_t>& ptr = col ? cp : L.h_rp;
+    const int ld_ref = kp + max_row * kc;  // the reference's padded stack height
+    flops += fl.gemm(double(B.nodes(l)), kp, kc, kp) + fl.qr(double(B.nodes(l)), ld_ref, kc);
     require(ld_ref >= kc, "qr_r_only_batched: requires rows >= cols");
     if (kc == 0) continue;
+    require(L.nb == 0 || (col ? L.bc : L.br) == kc, "generate_weight_tree: dim mismatch");
     const int64_t r0 = A.own_begin(l), nn = A.own_count(l);  // r0 is even unless l == s (one node)
     if (nn == 0) continue;
     if (kp > 0) {
       k_weights_parent<<<unsigned(nn), kThreads, 0, s>>>(
-          A.transfer.p + A.tr_off[l] + (r0 - A.tr_begin(l)) * A.tr_stride(l), A.ld(l), kc, kp,
+          B.transfer.p + B.tr_off[l] + (r0 - B.tr_begin(l)) * B.tr_stride(l), B.ld(l), kc, kp,
           R.at(l - 1) + (r0 >> 1) * int64_t(kp) * kp, Pall);
       H2B_CUDA(cudaGetLastError());
     }
+    if (col && L.nb)
+      H2B_CUDA(cudaMemcpyAsync(dcb, cb.data(), cb.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    const WSrc src{L.val, L.ld, L.block_stride(), col ? L.br : L.bc, col ? 0 : 1, col ? dcb : nullptr};
     const int lslots = weights_slots(A.device, kc);
     int nseg = 1;
-    if (nn < lslots) nseg = int(std::min<int64_t>((lslots + nn - 1) / nn, std::max(1, L.max_row / 4)));
+    if (nn < lslots) nseg = int(std::min<int64_t>((lslots + nn - 1) / nn, std::max(1, max_row / 4)));
     nseg = std::max(1, std::min(nseg, int(maxitems / std::max<int64_t>(1, nn))));
     items.clear();
     merge.clear();
     for (int64_t i = 0; i < nn; ++i) {
-      const int32_t b0 = L.h_rp[r0 + i], b1 = L.h_rp[r0 + i + 1];
+      const int32_t b0 = ptr[r0 + i], b1 = ptr[r0 + i + 1];
       if (nseg == 1) {
         items.push_back({int32_t(i), b0, b1, int32_t(i), 1});
       } else {
@@ -1360,20 +1430,28 @@ void weights(Matrix& A, TreePool& R, cudaStream_t s, Flops& fl, double& flops, c
     constexpr int CR = 32;
     const size_t sm = kWWarps * (size_t(((kc * (kc + 1)) / 2 + 1) & ~1) + 2 * size_t(CR + 2)) * sizeof(double);
     double* Rl = R.at(l) + r0 * int64_t(kc) * kc;
-    auto launch = [&](const double* S, int lds, double* Rout, int out_t, const WItem* it, int64_t n, int* next) {
+    auto launch = [&](const WSrc& src, double* Rout, int out_t, const WItem* it, int64_t n, int* next) {
       const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((n + kWWarps - 1) / kWWarps,
                                                                           lslots / kWWarps)));
-      if (kc > 32)
-        k_weights<2, CR><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, S, lds, Rout, out_t, it, n, next);
-      else
-        k_weights<1, CR><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, S, lds, Rout, out_t, it, n, next);
+      if (src.trans) {
+        if (kc > 32)
+          k_weights<2, CR, true><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, src, Rout, out_t, it, n, next);
+        else
+          k_weights<1, CR, true><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, src, Rout, out_t, it, n, next);
+      } else {
+        if (kc > 32)
+          k_weights<2, CR, false><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, src, Rout, out_t, it, n, next);
+        else
+          k_weights<1, CR, false><<<grid, 32 * kWWarps, sm, s>>>(Pall, kc, kp, src, Rout, out_t, it, n, next);
+      }
       H2B_CUDA(cudaGetLastError());
     };
     if (nseg == 1) {
-      launch(L.val, L.ld, Rl, 0, ditems, int64_t(items.size()), counters);
+      launch(src, Rl, 0, ditems, int64_t(items.size()), counters);
     } else {
-      launch(L.val, L.ld, segR, 1, ditems, int64_t(items.size()), counters);
-      launch(segR, kc, Rl, 0, dmerge, int64_t(merge.size()), counters + 1);
+      launch(src, segR, 1, ditems, int64_t(items.size()), counters);
+      // the partial R's, stored transposed, read as kc x kc "blocks"
+      launch(WSrc{segR, kc, int64_t(kc) * kc, kc, 1, nullptr}, Rl, 0, dmerge, int64_t(merge.size()), counters + 1);
     }
     // the next level's uploads reuse the item buffers: keep stream order
     H2B_CUDA(cudaStreamSynchronize(s));
@@ -1662,6 +1740,12 @@ void relayout(Matrix& A) {
   for (int l = 0; l <= q; ++l) A.vec_off[l + 1] = A.vec_off[l] + A.nodes(l) * A.rank[l];
   A.xhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
   A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
+  if (!A.symmetric) {  // x^ lives with the column basis
+    Matrix& C = *A.colb;
+    C.vec_off.assign(q + 2, 0);
+    for (int l = 0; l <= q; ++l) C.vec_off[l + 1] = C.vec_off[l] + C.nodes(l) * C.rank[l];
+    C.xhat.alloc(std::max<int64_t>(1, C.vec_off[q + 1]));
+  }
   A.xh16.release();
   A.yh16.release();
   upload_structure(A);
@@ -1695,6 +1779,11 @@ uint64_t counted_footprint(const Matrix& A, const Part& pt) {
     if (pt.counts(l)) e += uint64_t(A.cpl[l].nb) * A.cpl[l].br * A.cpl[l].bc;
   for (int l = 1; l <= A.q; ++l)
     if (l > pt.s || pt.counts(0)) e += uint64_t(A.tr_count(l)) * A.rank[l] * A.rank[l - 1];
+  if (!A.symmetric) {  // the column basis (h2_matrix.hpp:97-100; never partitioned)
+    const Matrix& C = *A.colb;
+    e += uint64_t(C.own_count(C.q)) * C.m * C.rank[C.q];
+    for (int l = 1; l <= C.q; ++l) e += uint64_t(C.tr_count(l)) * C.rank[l] * C.rank[l - 1];
+  }
   return e * sizeof(double);
 }
 
@@ -1711,13 +1800,20 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   // region A holds the projection trees (To, then Tt), region B the weight
   // tree R, region C the phase scratch (weights, truncation, the chunked
   // compaction of the coupling pool).
-  const size_t tree_need = TreePool::need(A, A.rank, A.rank);
-  const size_t arena_need = std::max({weights_arena_need(A), truncate_sizes(A).total, size_t(1) << 25});
+  // (non-symmetric: the column basis' trees follow the row basis' in A and B)
+  const bool sym = A.symmetric;
+  Matrix& Cb = A.col_basis();
+  const size_t tree_row = TreePool::need(A, A.rank, A.rank);
+  const size_t tree_need = tree_row + (sym ? 0 : TreePool::need(Cb, Cb.rank, Cb.rank));
+  const size_t arena_need = std::max({weights_arena_need(A), truncate_sizes(A).total,
+                                      sym ? size_t(0) : truncate_sizes(Cb).total, size_t(1) << 25});
   const size_t proj_need = ProjRows::need(A);
   Workspace ws{A.device};
   ws.buf = ws_checkout(A.device, 2 * tree_need + arena_need + proj_need);
   ws.trees = ws.buf.p;
   ws.rtree = ws.buf.p + tree_need;
+  double* trees_col = ws.trees + tree_row;
+  double* rtree_col = ws.rtree + tree_row;
   ws.arena = ws.buf.p + 2 * tree_need;
   ws.arena_cap = ws.buf.n - 2 * tree_need - proj_need;  // all the rest (projection chunks)
   Arena ar, par;  // phase scratch; the projection work lists (at the end: live across phases)
@@ -1751,11 +1847,13 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   // projection phase is what remains of it after its producer phase.
   // Partitioned compression (communicator callbacks between levels) runs
   // the projections after their producers, on the main stream.
-  const bool overlap = !pt.dist();
+  const bool overlap = !pt.dist() && sym;
   SideStream side(overlap, s);
   ProjRows PR;
   project_rows(A, par, PR, s);
-  TreePool To, R, Tt;
+  TreePool To, R, Tt, Toc, Rc, Ttc;  // row basis; column basis (non-symmetric)
+  TreePool& To_c = sym ? To : Toc;
+  TreePool& Tt_c = sym ? Tt : Ttc;
   double n2 = 0.0;  // ||A||_F^2 after the orthogonal projection (compression.hpp:487)
   Matrix* Ap = &A;
   auto hook = [Ap, &PR, &fl, &pt, &side](TreePool& T, bool tri, bool want_sum, double& fl_acc) -> LevelHook {
@@ -1763,22 +1861,24 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     double* fa = &fl_acc;
     return [Ap, Tp, fa, tri, want_sum, &PR, &fl, &pt, &side](int l) {
       side.fork(l);
-      project_level(*Ap, *Tp, PR, l, tri, want_sum, fl, *fa, pt, side.b);
+      project_level(*Ap, *Tp, *Tp, PR, l, tri, want_sum, fl, *fa, pt, side.b);
     };
   };
   {
     Timer t(s);
     orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt, ws.trees,
                   overlap ? hook(To, true, true, r.flops_project_orth) : nullptr);
+    if (!sym) orthogonalize(Cb, Toc, s, fl, r.flops_orthogonalize, pt, trees_col);
     r.time_orthogonalize_ms = t.stop();
   }
   {
     Timer t(s);
     if (!overlap)
-      for (int l = A.q; l >= 0; --l) project_level(A, To, PR, l, true, true, fl, r.flops_project_orth, pt, s);
+      for (int l = A.q; l >= 0; --l)
+        project_level(A, To, To_c, PR, l, true, true, fl, r.flops_project_orth, pt, s);
     side.join();
     n2 = project_rowsum(PR, pt, s);
-    project_finish(A, To, /*in_place=*/true, ar, s);
+    project_finish(A, To, To_c, /*in_place=*/true, ar, s);
     r.time_project_orth_ms = t.stop();
   }
   n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s, ws.arena);
@@ -1786,7 +1886,8 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   r.frobenius_norm = std::sqrt(n2);
   {
     Timer t(s);
-    weights(A, R, s, fl, r.flops_weights, pt, ws.rtree, ar);
+    weights(A, A, false, R, s, fl, r.flops_weights, pt, ws.rtree, ar);
+    if (!sym) weights(A, Cb, true, Rc, s, fl, r.flops_weights, pt, rtree_col, ar);  // transposed layers
     r.time_weights_ms = t.stop();
   }
   for (int l = 0; l <= A.q; ++l) A.cpl[l].max_row = saved_max[l];
@@ -1795,14 +1896,16 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     Timer t(s);
     energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate, pt, ws.trees, ar,
                       overlap ? hook(Tt, false, false, r.flops_project_trunc) : nullptr);
+    if (!sym) energy += truncate(Cb, Rc, eps, Ttc, s, fl, r.flops_truncate, pt, trees_col, ar);
     r.time_truncate_ms = t.stop();
   }
   {
     Timer t(s);
     if (!overlap)
-      for (int l = A.q; l >= 0; --l) project_level(A, Tt, PR, l, false, false, fl, r.flops_project_trunc, pt, s);
+      for (int l = A.q; l >= 0; --l)
+        project_level(A, Tt, Tt_c, PR, l, false, false, fl, r.flops_project_trunc, pt, s);
     side.join();
-    project_finish(A, Tt, /*in_place=*/false, ar, s);
+    project_finish(A, Tt, Tt_c, /*in_place=*/false, ar, s);
     r.time_project_trunc_ms = t.stop();
   }
   relayout(A);

@@ -6,7 +6,11 @@ the upsweep runs on A.col_basis(), the downsweep on A.row_basis).
 * random column bases of other ranks: hmv and the phase entry points equal
   the reference's on the imported matrix; footprint and flop model too;
 * containers: byte-identical to the reference's save, both directions;
-* compress / 16-vector hmv report H2B_UNSUPPORTED (this version)."""
+* compress (both bases orthogonalized, projected, weighted -- the column
+  weight tree over the transposed layers -- and truncated,
+  compression.hpp:466-551) against the reference's compress of the same
+  matrix: row and column ranks, error estimate, bytes, the operator;
+* the 16-vector hmv reports H2B_UNSUPPORTED (this version)."""
 import numpy as np
 import pytest
 
@@ -92,9 +96,48 @@ def test_container_byte_identical_both_ways(gpu, ref, tmp_path):
     assert B.info().symmetric == 0
 
 
+def _col_ranks(R):
+    import ctypes as C
+    q = R.shape()[2]
+    cr = np.zeros(q + 1, np.int32)
+    R.be.lib.ref_col_ranks.argtypes = [C.c_void_p, C.c_void_p]
+    R.be.lib.ref_col_ranks(R.h, cr.ctypes.data)
+    return cr.tolist()
+
+
+@pytest.mark.parametrize("dim,n,order,eps,make", [(2, 1 << 13, 8, 1e-7, "scaled"),
+                                                   (3, 1 << 12, 4, 1e-6, "scaled"),
+                                                   (2, 1 << 12, 6, 1e-5, "random")])
+def test_compress_matches_reference(gpu, ref, dim, n, order, eps, make):
+    base = ref.construct(dim, n, grid_order=order).to_host()
+    hm = scaled(base) if make == "scaled" else random_cols(base)
+    R = ref.from_host(hm)
+    A = h2.H2Matrix.from_host(hm)
+    x = np.random.default_rng(3).random(n)
+    y0 = R.hmv(x)
+    rr = R.compress(eps)
+    rg = h2.compress(A, eps)
+    inf = A.info()
+    assert inf.symmetric == 0
+    assert all(abs(a - b) <= 1 for a, b in zip(rg.new_ranks, rr["new_ranks"])), (rg.new_ranks, rr["new_ranks"])
+    cr = _col_ranks(R)
+    assert all(abs(a - b) <= 1 for a, b in zip(inf.col_ranks, cr)), (inf.col_ranks, cr)
+    if rg.new_ranks == rr["new_ranks"] and list(inf.col_ranks) == cr:
+        assert rg.bytes_after == int(rr["bytes_after"])
+    assert rg.bytes_before == int(rr["bytes_before"])
+    assert 0.5 * rr["frobenius_error"] <= rg.frobenius_error <= 2.0 * rr["frobenius_error"] + 1e-15
+    assert rg.frobenius_norm == pytest.approx(rr["frobenius_norm"], rel=1e-10)
+    yg, yr = h2.hmv(A, x), R.hmv(x)
+    assert rel_err(yg, y0) <= 10 * eps
+    assert rel_err(yg, yr) <= 10 * eps
+    # the compressed matrix round-trips through the reference
+    back = ref.from_host(A.to_host())
+    assert rel_err(back.hmv(x), yg) <= 1e-12
+
+
 def test_unsupported_paths_say_so(gpu, ref):
     hm = scaled(ref.construct(2, 1 << 12, grid_order=4).to_host())
     A = h2.H2Matrix.from_host(hm)
     with pytest.raises(_lib.H2bError) as e:
-        h2.compress(A, 1e-6)
+        h2.hmv_multi(A, np.ones((16, 1 << 12)))
     assert e.value.code == _lib.H2B_UNSUPPORTED and "non-symmetric" in str(e.value)
