@@ -206,8 +206,8 @@ H2B_API h2b_status h2b_dense_mv(h2b_matrix* A, const double* xc, double* yc, dou
 
 /* Algebraic recompression in place (orthogonalize, project, weights,
  * truncate at relative eps, project).  Exclusive access required. */
-/* Non-symmetric matrices: h2b_compress, h2b_hmv and the phase entry points
- * support them; h2b_orthogonalize and h2b_hmv_multi return H2B_UNSUPPORTED. */
+/* Non-symmetric matrices: h2b_compress, h2b_hmv, h2b_hmv_multi and the phase
+ * entry points support them; h2b_orthogonalize returns H2B_UNSUPPORTED. */
 H2B_API h2b_status h2b_compress(h2b_matrix* A, double eps, h2b_compress_report* report);
 /* Orthogonalize only (in place); projection tree written to t_out (host,
  * level-concatenated ranks[l]^2 per node) when non-NULL. */

@@ -740,7 +740,6 @@ h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx,
                          int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream) {
   return guarded([&] {
     require(Ah, "null matrix");
-    symmetric_only(*Ah, "h2b_hmv_multi");
     Matrix& A = *Ah;
     whole(A, "h2b_hmv_multi");
     require(nvec >= 0 && ldx >= A.n && ldy >= A.n, "hmv_multi: bad leading dimension");

@@ -232,7 +232,8 @@ void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_
                       double alpha, double beta, cudaStream_t s) {
   require(nv >= 1 && nv <= NV, "hmv_multi: 1..16 vectors per pass");
   const int q = A.q;
-  const int64_t nvec_pool = std::max<int64_t>(1, A.vec_off[q + 1]) * NV;
+  const Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
+  const int64_t nvec_pool = std::max<int64_t>({1, A.vec_off[q + 1], C.vec_off[q + 1]}) * NV;
   if (A.xc16.n < size_t(A.n) * NV) {
     A.xc16.alloc(size_t(A.n) * NV);
     A.yc16.alloc(size_t(A.n) * NV);
@@ -248,21 +249,21 @@ void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_
   const int64_t nl = A.nodes(q);
   double* xh = A.xh16.p;
   double* yh = A.yh16.p;
-  if (A.rank[q] > 0) {
-    k_up_leaf_mv<<<wgrid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[q], nl, A.xc16.p,
-                                               xh + A.vec_off[q] * NV);
+  if (C.rank[q] > 0) {
+    k_up_leaf_mv<<<wgrid(nl), kThreads, 0, s>>>(C.leaf.p, C.ldm, C.m, C.rank[q], nl, A.xc16.p,
+                                               xh + C.vec_off[q] * NV);
     H2B_CUDA(cudaGetLastError());
   }
   for (int l = q; l >= 1; --l) {
-    const int kc = A.rank[l], kp = A.rank[l - 1];
+    const int kc = C.rank[l], kp = C.rank[l - 1];
     const int64_t np = A.nodes(l - 1);
     if (kp == 0) continue;
     if (kc == 0) {
-      H2B_CUDA(cudaMemsetAsync(xh + A.vec_off[l - 1] * NV, 0, size_t(np) * kp * NV * sizeof(double), s));
+      H2B_CUDA(cudaMemsetAsync(xh + C.vec_off[l - 1] * NV, 0, size_t(np) * kp * NV * sizeof(double), s));
       continue;
     }
-    k_up_level_mv<<<wgrid(np), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, np,
-                                                 xh + A.vec_off[l] * NV, xh + A.vec_off[l - 1] * NV);
+    k_up_level_mv<<<wgrid(np), kThreads, 0, s>>>(C.transfer.p + C.tr_off[l], C.ld(l), kc, kp, np,
+                                                 xh + C.vec_off[l] * NV, xh + C.vec_off[l - 1] * NV);
     H2B_CUDA(cudaGetLastError());
   }
   LayerTableMV T{};
@@ -272,7 +273,7 @@ void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_
     d.val = L.val;
     d.rp = L.rp;
     d.ci = L.ci;
-    d.x = xh + A.vec_off[l] * NV;
+    d.x = xh + C.vec_off[l] * NV;
     d.y = yh + A.vec_off[l] * NV;
     d.stride = L.block_stride();
     d.br = L.br;

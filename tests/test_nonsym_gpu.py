@@ -10,7 +10,7 @@ the upsweep runs on A.col_basis(), the downsweep on A.row_basis).
   weight tree over the transposed layers -- and truncated,
   compression.hpp:466-551) against the reference's compress of the same
   matrix: row and column ranks, error estimate, bytes, the operator;
-* the 16-vector hmv reports H2B_UNSUPPORTED (this version)."""
+* the 16-vector pass; h2b_orthogonalize reports H2B_UNSUPPORTED (this version)."""
 import numpy as np
 import pytest
 
@@ -135,9 +135,22 @@ def test_compress_matches_reference(gpu, ref, dim, n, order, eps, make):
     assert rel_err(back.hmv(x), yg) <= 1e-12
 
 
+def test_multi_vector_pass(gpu, ref):
+    """16 right-hand sides on the FP64 tensor cores (h2b_hmv_multi): the
+    upsweep on the column basis, as in the single-vector path."""
+    n = 1 << 12
+    hm = random_cols(ref.construct(2, n, grid_order=6).to_host())
+    R = ref.from_host(hm)
+    A = h2.H2Matrix.from_host(hm)
+    X = np.random.default_rng(8).random((16, n))
+    Y = h2.hmv_multi(A, X)
+    for v in (0, 7, 15):
+        assert rel_err(Y[v], R.hmv(X[v])) <= 1e-12
+
+
 def test_unsupported_paths_say_so(gpu, ref):
     hm = scaled(ref.construct(2, 1 << 12, grid_order=4).to_host())
     A = h2.H2Matrix.from_host(hm)
     with pytest.raises(_lib.H2bError) as e:
-        h2.hmv_multi(A, np.ones((16, 1 << 12)))
+        h2.orthogonalize_basis(A)
     assert e.value.code == _lib.H2B_UNSUPPORTED and "non-symmetric" in str(e.value)
