@@ -1,6 +1,6 @@
 // CTA-cooperative FP64 small dense linear algebra in shared memory (the
 // per-entry bodies of the reference's batched engine, include/h2kit/linalg.hpp
-// and batch.hpp, re-designed for one 256-thread CTA per batch entry).
+// and batch.hpp, re-designed for one CTA per batch entry).
 //
 // Conventions follow the reference exactly where results are defined by them:
 //  * Householder QR with beta = -sign(alpha)||x||, tau = (beta-alpha)/beta,
@@ -9,8 +9,7 @@
 //  * One-sided Jacobi SVD with the skip rule |a_pq| <= 16 eps sqrt(a_pp a_qq)
 //    or a_pq == 0 and at most 60 sweeps (:142-176); sigma are the column norms,
 //    stable-sorted descending; zero columns give zero vectors (:178-232).
-//    The pair order is the parallel round-robin (tournament) ordering instead
-//    of the cyclic row order, so n/2 rotations run concurrently.
+//    (The Jacobi kernel itself is k_jacobi64 in compress.cu.)
 // All matrices are column-major with explicit leading dimensions.
 #pragma once
 
@@ -56,54 +55,6 @@ __device__ __forceinline__ void copy_block(double* dst, int ldd, const double* s
     const int j = e / rows, i = e - j * rows;
     dst[i + j * ldd] = src[i + j * lds];
   }
-}
-
-__device__ __forceinline__ void zero_block(double* dst, int ldd, int rows, int cols) {
-  for (int e = threadIdx.x; e < rows * cols; e += nthreads()) {
-    const int j = e / rows, i = e - j * rows;
-    dst[i + j * ldd] = 0.0;
-  }
-}
-
-// C (m x n) = op(A) (m x k) * op(B) (k x n); all operands in smem (or any
-// memory).  Each thread owns a 4 x 4 register tile of a 64 x 64 output tile.
-template <bool TA, bool TB>
-__device__ void gemm(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
-                     int m, int n, int k) {
-  const int tr = (threadIdx.x & 15) * 4;   // row offset in the 64x64 tile
-  const int tc = (threadIdx.x >> 4) * 4;   // col offset
-  for (int i0 = 0; i0 < m; i0 += 64)
-    for (int j0 = 0; j0 < n; j0 += 64) {
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-      for (int p = 0; p < k; ++p) {
-        double av[4], bv[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int i = i0 + tr + a;
-          av[a] = i < m ? (TA ? A[p + i * lda] : A[i + p * lda]) : 0.0;
-        }
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int j = j0 + tc + b;
-          bv[b] = j < n ? (TB ? B[j + p * ldb] : B[p + j * ldb]) : 0.0;
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int i = i0 + tr + a, j = j0 + tc + b;
-          if (i < m && j < n) C[i + j * ldc] = acc[a][b];
-        }
-    }
 }
 
 // Smallest leading dimension >= rows that is == 4 (mod 16) doubles: makes the
@@ -303,134 +254,6 @@ __device__ void householder_regs(double* A, int lda, int rows, int cols, double*
   __syncthreads();
 }
 
-__device__ inline void householder(double* A, int lda, int rows, int cols, double* tau, double* xb) {
-  if (rows <= 64)
-    householder_regs<16>(A, lda, rows, cols, tau, xb);
-  else
-    householder_regs<32>(A, lda, rows, cols, tau, xb);  // rows <= 128 (2 k_child, m <= 64)
-}
-
-// Householder QR with column pivoting (largest remaining column norm, first
-// index on ties), in place: reflectors below the diagonal, R on and above it,
-// perm[j] = original index of the column now at position j.  The remaining
-// column norms are recomputed exactly inside every trailing update (one extra
-// FMA per element), so no norm downdating.  Same reflector convention as
-// householder().  nrm: cols doubles, red: >= 16 doubles, sel: 1 int (smem).
-__device__ void qrcp(double* A, int lda, int rows, int cols, double* tau, int* perm, double* nrm,
-                     double* red, int* sel) {
-  for (int kk = warp(); kk < cols; kk += nwarps()) {
-    const double* w = A + kk * lda;
-    double t = 0.0;
-    for (int i = lane(); i < rows; i += 32) t = fma(w[i], w[i], t);
-    t = warp_sum(t);
-    if (lane() == 0) {
-      nrm[kk] = t;
-      perm[kk] = kk;
-    }
-  }
-  __syncthreads();
-  const int steps = rows < cols ? rows : cols;
-  for (int j = 0; j < steps; ++j) {
-    if (warp() == 0) {  // argmax of the remaining norms
-      double bv = -1.0;
-      int bi = cols;
-      for (int kk = j + lane(); kk < cols; kk += 32)
-        if (nrm[kk] > bv) {
-          bv = nrm[kk];
-          bi = kk;
-        }
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const double ov = __shfl_xor_sync(kFull, bv, o);
-        const int oi = __shfl_xor_sync(kFull, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      if (lane() == 0) *sel = bi;
-    }
-    __syncthreads();
-    const int pj = *sel;
-    if (pj != j) {
-      double* a = A + j * lda;
-      double* b = A + pj * lda;
-      for (int i = threadIdx.x; i < rows; i += nthreads()) {
-        const double t = a[i];
-        a[i] = b[i];
-        b[i] = t;
-      }
-      if (threadIdx.x == 0) {
-        const double tn = nrm[j];
-        nrm[j] = nrm[pj];
-        nrm[pj] = tn;
-        const int tp = perm[j];
-        perm[j] = perm[pj];
-        perm[pj] = tp;
-      }
-      __syncthreads();
-    }
-    double* v = A + j * lda;
-    const double nx = sqrt(nrm[j]);  // exact: recomputed by the previous update
-    if (nx == 0.0) {  // all remaining columns are zero
-      if (threadIdx.x == 0) tau[j] = 0.0;
-      __syncthreads();
-      continue;
-    }
-    const double al = v[j];
-    const double be = al >= 0.0 ? -nx : nx;
-    const double tj = (be - al) / be;
-    const double sc = 1.0 / (al - be);
-    __syncthreads();  // everyone has read v[j]
-    for (int i = j + 1 + threadIdx.x; i < rows; i += nthreads()) v[i] *= sc;
-    if (threadIdx.x == 0) {
-      v[j] = be;
-      tau[j] = tj;
-    }
-    __syncthreads();
-    for (int kk = j + 1 + warp(); kk < cols; kk += nwarps()) {
-      double* w = A + kk * lda;
-      double s = 0.0;
-      for (int i = j + 1 + lane(); i < rows; i += 32) s = fma(v[i], w[i], s);
-      s = warp_sum(s);
-      const double d = (w[j] + s) * tj;
-      __syncwarp();
-      if (lane() == 0) w[j] -= d;
-      double t = 0.0;
-      for (int i = j + 1 + lane(); i < rows; i += 32) {
-        const double nv = fma(-v[i], d, w[i]);
-        w[i] = nv;
-        t = fma(nv, nv, t);
-      }
-      t = warp_sum(t);
-      if (lane() == 0) nrm[kk] = t;
-    }
-    __syncthreads();
-  }
-}
-
-// Y (rows x ncols, ld ldy) <- H_0 H_1 ... H_{k-1} Y for the k reflectors
-// stored below the diagonal of A (unit leading entry, tau[j]).
-__device__ void apply_q(const double* A, int lda, int rows, int k, const double* tau, double* Y,
-                        int ldy, int ncols) {
-  for (int j = k - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* v = A + j * lda;
-    for (int kk = warp(); kk < ncols; kk += nwarps()) {
-      double* w = Y + kk * ldy;
-      double s = 0.0;
-      for (int i = j + 1 + lane(); i < rows; i += 32) s = fma(v[i], w[i], s);
-      s = warp_sum(s);
-      const double d = (w[j] + s) * tj;
-      __syncwarp();
-      if (lane() == 0) w[j] -= d;
-      for (int i = j + 1 + lane(); i < rows; i += 32) w[i] = fma(-v[i], d, w[i]);
-    }
-    __syncthreads();
-  }
-}
-
 // Y <- H_0 H_1 ... H_{k-1} [Y0; 0] for the k reflectors below the diagonal
 // of A (rows x k, unit leading entries, tau[j]; tau = 0 marks an identity),
 // Y0 = the top k x ncols of Y (global or smem, ld ldy; rows k.. of Y are
@@ -496,32 +319,6 @@ __device__ void apply_q_wy(double* A, int lda, int rows, int k, const double* ta
   __syncthreads();
 }
 
-// Thin Q (rows x cols) from the factored form (linalg.hpp:77-98).
-__device__ void form_q(const double* A, int lda, int rows, int cols, const double* tau,
-                       double* Q, int ldq) {
-  for (int e = threadIdx.x; e < rows * cols; e += nthreads()) {
-    const int j = e / rows, i = e - j * rows;
-    Q[i + j * ldq] = i == j ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int j = cols - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* v = A + j * lda;
-    for (int kk = j + warp(); kk < cols; kk += nwarps()) {
-      double* w = Q + kk * ldq;
-      double s = 0.0;
-      for (int i = j + 1 + lane(); i < rows; i += 32) s += v[i] * w[i];
-      s = warp_sum(s);
-      const double d = (w[j] + s) * tj;
-      __syncwarp();
-      if (lane() == 0) w[j] -= d;
-      for (int i = j + 1 + lane(); i < rows; i += 32) w[i] -= v[i] * d;
-    }
-    __syncthreads();
-  }
-}
-
 // R (cols x cols, non-negative diagonal) to R_out; flip[j] (smem ints) marks
 // negated rows (linalg.hpp:100-113).
 __device__ void extract_r(const double* A, int lda, int cols, double* R, int ldr, int* flip) {
@@ -534,140 +331,10 @@ __device__ void extract_r(const double* A, int lda, int cols, double* R, int ldr
   }
 }
 
-// Round-robin (circle method) pairing of n (even) columns: round r in
-// [0, n-1), slot s in [0, n/2).
-__device__ __forceinline__ void rr_pair(int n, int r, int s, int& p, int& q) {
-  const int m = n - 1;
-  if (s == 0) {
-    p = r;
-    q = m;
-  } else {
-    p = (r + s) % m;
-    q = (r - s + m) % m;
-  }
-  if (p > q) {
-    const int t = p;
-    p = q;
-    q = t;
-  }
-}
-
-// One-sided Jacobi on the columns of G (rows x n, n even; pad with a zero
-// column for odd counts).  flag: one int of smem.  Eight lanes own one
-// column pair (four pairs per warp, 32 pairs per CTA step) and keep it in
-// registers (RPT rows per lane) between the three dot products (reduced with
-// width-8 shuffles) and the rotation.
+// Sweep histogram of the truncation Jacobi (compile with -DH2B_SWEEP_HIST).
 #ifdef H2B_SWEEP_HIST
 __device__ int g_sweep_hist[64];
 #endif
-template <int RPT>
-__device__ void jacobi_t(double* G, int ldg, int rows, int n, int* flag, int rows_dot) {
-  const double tol = 2.220446049250313e-16 * 16.0;
-  const int sub = lane() & 7;
-  const int slot0 = warp() * 4 + (lane() >> 3);
-  const unsigned gmask = 0xffu << (lane() & 24);
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    if (threadIdx.x == 0) *flag = 0;
-    __syncthreads();
-    for (int r = 0; r < n - 1; ++r) {
-      for (int s = slot0; s < n / 2; s += nwarps() * 4) {
-        int p, q;
-        rr_pair(n, r, s, p, q);
-        double* gp = G + p * ldg;
-        double* gq = G + q * ldg;
-        double u[RPT], w[RPT];
-        double a = 0.0, b = 0.0, d = 0.0;
-#pragma unroll
-        for (int t = 0; t < RPT; ++t) {
-          const int i = sub + 8 * t;
-          u[t] = i < rows ? gp[i] : 0.0;
-          w[t] = i < rows ? gq[i] : 0.0;
-          if (i < rows_dot) {  // rows beyond rows_dot only accumulate rotations
-            a += u[t] * u[t];
-            b += w[t] * w[t];
-            d += u[t] * w[t];
-          }
-        }
-#pragma unroll
-        for (int m = 1; m < 8; m <<= 1) {
-          a += __shfl_xor_sync(gmask, a, m, 8);
-          b += __shfl_xor_sync(gmask, b, m, 8);
-          d += __shfl_xor_sync(gmask, d, m, 8);
-        }
-        // sqrt(a) sqrt(b) and hypot(1, z): the reference's rule and rotation
-        // (linalg.hpp:155-170) without the under/overflow of a*b and z*z,
-        // which turn tiny-column pairs into no-op rotations that never
-        // satisfy the convergence test
-        if (fabs(d) <= tol * (sqrt(a) * sqrt(b)) || d == 0.0) continue;
-        if (sub == 0) *flag = 1;
-        const double z = (b - a) / (2.0 * d);
-        const double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + hypot(1.0, z));
-        const double cs = 1.0 / sqrt(1.0 + t * t);
-        const double sn = cs * t;
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-          const int i = sub + 8 * k;
-          if (i < rows) {
-            gp[i] = cs * u[k] - sn * w[k];
-            gq[i] = sn * u[k] + cs * w[k];
-          }
-        }
-      }
-      __syncthreads();
-    }
-    if (*flag == 0) {
-#ifdef H2B_SWEEP_HIST
-      if (threadIdx.x == 0) atomicAdd(&g_sweep_hist[sweep], 1);
-#endif
-      break;
-    }
-    __syncthreads();
-#ifdef H2B_SWEEP_HIST
-    if (sweep == 59 && threadIdx.x == 0) atomicAdd(&g_sweep_hist[60], 1);
-#endif
-  }
-  __syncthreads();
-}
-
-// rows_dot < rows: the dot products (and hence the rotations) are defined by
-// the first rows_dot rows; the remaining rows (e.g. an appended identity)
-// only accumulate the rotations.
-__device__ inline void jacobi(double* G, int ldg, int rows, int n, int* flag, int rows_dot = -1) {
-  if (rows_dot < 0) rows_dot = rows;
-  // rows <= 64: the preconditioned SVD only rotates square triangular factors
-  if (rows <= 32)
-    jacobi_t<4>(G, ldg, rows, n, flag, rows_dot);
-  else
-    jacobi_t<8>(G, ldg, rows, n, flag, rows_dot);
-}
-
-// After jacobi(): sigma[j] (descending, stable) and U (rows x s) with unit (or
-// zero) columns.  nrm/ord: smem scratch of n doubles / ints.
-__device__ void jacobi_finish(const double* G, int ldg, int rows, int n, int s, double* U, int ldu,
-                              double* sigma, double* nrm, int* ord) {
-  for (int j = warp(); j < n; j += nwarps()) {
-    double t = 0.0;
-    for (int i = lane(); i < rows; i += 32) t += G[i + j * ldg] * G[i + j * ldg];
-    t = warp_sum(t);
-    if (lane() == 0) nrm[j] = sqrt(t);
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < n; j += nthreads()) {
-    int rank = 0;
-    const double v = nrm[j];
-    for (int i = 0; i < n; ++i) rank += (nrm[i] > v) || (nrm[i] == v && i < j);
-    ord[rank] = j;
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < s; j += nthreads()) sigma[j] = nrm[ord[j]];
-  for (int e = threadIdx.x; e < rows * s; e += nthreads()) {
-    const int j = e / rows, i = e - j * rows;
-    const int src = ord[j];
-    const double nv = nrm[src];
-    U[i + j * ldu] = nv > 0.0 ? G[i + src * ldg] * (1.0 / nv) : 0.0;
-  }
-  __syncthreads();
-}
 
 }  // namespace cta
 }  // namespace h2b
