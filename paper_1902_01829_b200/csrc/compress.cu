@@ -219,6 +219,97 @@ __device__ __forceinline__ void out_strip(const double (&acc)[8][2], const doubl
     }
 }
 
+// Column-strip form of TS = Tr S for warp w: columns [8w, 8w+8) of TS, all
+// row tiles below rn (acc[x] = row tile x).  With a triangular Tr every warp
+// skips the same fragments (row tile x needs k >= 8x), so the 8 warps carry
+// equal work -- the row-strip form gives warp w 16 - 2w k-steps.  Returns
+// false for an idle warp (8w >= co).
+template <bool TRI>
+__device__ __forceinline__ bool ts_cols(const double* Tr, const double* Sb, int ro, int co, int rn,
+                                        double (&acc)[8][2]) {
+  const int w = cta::warp(), t = cta::lane();
+  const int fr = t >> 2, fk = t & 3;
+  const int j0 = 8 * w;
+#pragma unroll
+  for (int x = 0; x < 8; ++x) acc[x][0] = acc[x][1] = 0.0;
+  if (j0 >= co) return false;
+  const int kc_end = (ro + 3) >> 2;
+#pragma unroll
+  for (int kc = 0; kc < 16; ++kc) {
+    if (kc < kc_end) {
+      const int p = 4 * kc + fk;
+      const double b = Sb[p + (j0 + fr) * kPLd];  // S[p, j0 + fr]
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        if (8 * x < rn && (!TRI || 4 * kc + 3 >= 8 * x)) {
+          const double a = Tr[8 * x + fr + p * kPLd];
+          cta::dmma(acc[x][0], acc[x][1], a, b);
+        }
+      }
+    }
+  }
+  return true;
+}
+
+// TS column strip of warp w into smem (ld kPLd): acc[x][v] = TS[8x + fr, 8w + 2fk + v].
+__device__ __forceinline__ void ts_store(const double (&acc)[8][2], double* TSb, int rn) {
+  const int w = cta::warp(), t = cta::lane();
+  const int fr = t >> 2, fk = t & 3;
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+    if (8 * x < rn) {
+      TSb[8 * x + fr + (8 * w + 2 * fk) * kPLd] = acc[x][0];
+      TSb[8 * x + fr + (8 * w + 2 * fk + 1) * kPLd] = acc[x][1];
+    }
+}
+
+// out strip of warp w = TS[8w:8w+8, :] T_col^T with TS's A fragments from smem.
+template <bool TRI>
+__device__ __forceinline__ void out_rows(const double* TSb, const double* Tc, double* out, double* outT,
+                                         int ld_new, int co, int rn, int cn, double& sumsq) {
+  const int w = cta::warp(), t = cta::lane();
+  const int fr = t >> 2, fk = t & 3;
+  const int i0 = 8 * w;
+  if (i0 >= rn) return;
+  const int kc_end = (co + 3) >> 2;
+  double o[8][2];
+#pragma unroll
+  for (int y = 0; y < 8; ++y) o[y][0] = o[y][1] = 0.0;
+#pragma unroll
+  for (int kc = 0; kc < 16; ++kc) {
+    if (kc < kc_end) {
+      const int p = 4 * kc + fk;
+      const double a = TSb[i0 + fr + p * kPLd];
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        if (8 * y < cn && (!TRI || 4 * kc + 3 >= 8 * y)) {
+          const double b = Tc[8 * y + fr + p * kPLd];  // T_col[j, p]
+          cta::dmma(o[y][0], o[y][1], a, b);
+        }
+      }
+    }
+  }
+  const int i = i0 + fr;
+  if (i < rn) {
+#pragma unroll
+    for (int y = 0; y < 8; ++y)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = 8 * y + 2 * fk + v;
+        if (j < cn) {
+          out[i + int64_t(j) * ld_new] = o[y][v];
+          if (outT) outT[j + int64_t(i) * ld_new] = o[y][v];  // mirror block (col, row)
+          sumsq = fma(o[y][v], o[y][v], sumsq);
+        }
+      }
+  }
+  if (ld_new > rn && w == 0)
+    for (int j = t; j < cn; j += 32) {
+      out[rn + int64_t(j) * ld_new] = 0.0;
+      if (outT) outT[rn + int64_t(j) * ld_new] = 0.0;
+    }
+}
+
 // 8-byte asynchronous global -> shared copies (cp.async.ca), grouped.
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -320,27 +411,43 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   for (int k = 0; k < nk; ++k) {
     cp_async_wait<1>();  // S_k (T_col,k may still be in flight)
     __syncthreads();
-    double acc[8][2];
-    const bool live = P.tri ? ts_strip<true>(Tr, Sb, ro, co, rn, acc) : ts_strip<false>(Tr, Sb, ro, co, rn, acc);
-    __syncthreads();  // S_k consumed
-    if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ostride, L.ld_old, ro, co);
-    cp_async_commit();
-    cp_async_wait<1>();  // T_col,k
-    __syncthreads();
     const int b = blist[k], mb = mlist[k];
     double* out = L.out + int64_t(b) * L.ostride;
     double* outT = mb >= 0 ? L.out + int64_t(mb) * L.ostride : nullptr;
     double s1 = 0.0;
-    if (live) {
-      if (P.tri)
-        out_strip<true>(acc, Tc, out, outT, L.ld_new, co, rn, cn, s1);
-      else
-        out_strip<false>(acc, Tc, out, outT, L.ld_new, co, rn, cn, s1);
+    double acc[8][2];
+    if (P.tri) {
+      // triangular T_row: TS by column strips (balanced over the warps; the
+      // row strips give warp w 16 - 2w k-steps), through smem over S_k, into
+      // the row strips of out.  S_{k+1} then loads after out_k.
+      const bool live = ts_cols<true>(Tr, Sb, ro, co, rn, acc);
+      __syncthreads();  // S_k consumed
+      if (live) ts_store(acc, Sb, rn);
+      cp_async_wait<0>();  // T_col,k
+      __syncthreads();
+      out_rows<true>(Sb, Tc, out, outT, L.ld_new, co, rn, cn, s1);
+      __syncthreads();  // TS, T_col,k consumed
+      if (k + 1 < nk) {
+        stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ostride, L.ld_old, ro, co);
+        cp_async_commit();
+        stage64(Tc, L.Tc + int64_t(clist[k + 1]) * cn * co, cn, cn, co);
+        cp_async_commit();
+      }
+    } else {
+      // row strips, TS in registers: S_{k+1} loads under out_k and T_col,{k+1}
+      // under TS_{k+1}
+      const bool live = ts_strip<false>(Tr, Sb, ro, co, rn, acc);
+      __syncthreads();  // S_k consumed
+      if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ostride, L.ld_old, ro, co);
+      cp_async_commit();
+      cp_async_wait<1>();  // T_col,k
+      __syncthreads();
+      if (live) out_strip<false>(acc, Tc, out, outT, L.ld_new, co, rn, cn, s1);
+      __syncthreads();  // T_col,k consumed
+      if (k + 1 < nk) stage64(Tc, L.Tc + int64_t(clist[k + 1]) * cn * co, cn, cn, co);
+      cp_async_commit();
     }
     ss += outT ? 2.0 * s1 : s1;
-    __syncthreads();  // T_col,k consumed
-    if (k + 1 < nk) stage64(Tc, L.Tc + int64_t(clist[k + 1]) * cn * co, cn, cn, co);
-    cp_async_commit();
   }
   cp_async_wait<0>();
   // ||S||_F^2 of the projected row, fused (compression.hpp:487, frob_norm_sq)
