@@ -130,11 +130,27 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+_JSON_OUT = None  # the bench line's stream once stdout is handed to the libraries
+
+
+def emit(line: dict):
+    """Print THE bench line: on the saved stdout when dist_setup redirected
+    file descriptor 1 (NCCL and the CUDA libraries write banners such as
+    "NCCL version ..." to fd 1, which must not precede the JSON line)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def dist_setup(force: bool = False):
+    global _JSON_OUT
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 or force:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)  # library output on fd 1 goes to stderr
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
@@ -317,7 +333,7 @@ def run_reference(args):
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": round(cb["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_distributed(args, cfg, world, rank, local):
@@ -435,7 +451,7 @@ def run_distributed(args, cfg, world, rank, local):
         "clocks": clocks,
         "compression": comp,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     dist.destroy_process_group()
 
 
@@ -601,7 +617,7 @@ def main():
         "accuracy": acc,
         "compression": comp,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 if __name__ == "__main__":
