@@ -481,11 +481,11 @@ void hmv_device(Matrix& A, const double* x, double* y, double alpha, double beta
   if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
   Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
   launch_up_leaf(C, x, s);
-  for (int l = q; l >= 1; --l) launch_up_level(C, l, s);
+  if (q >= 1) launch_up_fused(A, C, s);  // levels q..1 in one dataflow launch
   if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
   launch_bsr(A, A.work.p, A.nwork, C.xc.p, A.yc.p, C.xhat.p, A.yhat.p, s, &C);
   if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
-  for (int l = 1; l <= q; ++l) launch_down_level(A, l, s);
+  if (q >= 1) launch_down_fused(A, s);
   launch_down_leaf(A, y, alpha, beta, true, s);
   if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
 }

@@ -128,6 +128,11 @@ struct Matrix {
   std::vector<int64_t> vec_off;     // node-vector level offsets, size q + 2
   DevBuf<uint32_t> work;            // BSR work list (dense + coupling rows)
   int64_t nwork = 0;
+  // Fused dataflow sweeps (launch_up_fused / launch_down_fused): per-node
+  // completion flags (epoch-valued, never reset) and the work tickets.
+  DevBuf<uint32_t> sweep_flag;
+  DevBuf<unsigned long long> sweep_ticket;  // [0] up, [1] down
+  uint32_t sweep_epoch = 0;
 
   // HmvContext analogue (hmv.hpp:161-172): one workspace per handle.
   DevBuf<double> xc, yc, xhat, yhat, xs, ys;
@@ -198,6 +203,12 @@ void launch_down_level(const Matrix& A, int l, cudaStream_t s, int64_t c0 = 0, i
 // with t relative to the first owned leaf (cluster-order slice).
 void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
                       cudaStream_t s);
+// Whole-matrix upsweep above the leaves (levels q..1 of basis B, x^ of B) and
+// downsweep (levels 1..q of A) as ONE persistent launch each: warps claim
+// nodes deepest-first (up) / top-down (down) and wait for their children /
+// parent through per-node flags (A holds the flags and tickets).
+void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s);
+void launch_down_fused(Matrix& A, cudaStream_t s);
 void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s);
 
 // 16-vector FP64-MMA mat-vec, device pointers (k_hmv_mv.cu).

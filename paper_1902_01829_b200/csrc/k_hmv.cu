@@ -243,6 +243,120 @@ __global__ void __launch_bounds__(kThreads) k_down_leaf(
   }
 }
 
+// ---- fused dataflow sweeps ------------------------------------------------
+// Items are the nodes of all levels in dependency order; a warp claims the
+// next item with an atomic ticket (reset before each launch), waits on
+// the flags of the nodes it reads, computes exactly like k_up_level /
+// k_down_level, and publishes its node's flag.  Claimed items only ever wait
+// for items claimed earlier, whose warps are running: deadlock-free at any
+// residency.  Flags hold an epoch (2e: up done, 2e + 1: down done) so they are
+// never cleared.  Node vectors written by other SMs are read with ld.cg.
+struct SweepLevel {
+  const double* T;   // transfers of the child level (block (c - cbegin) * stride)
+  int64_t stride;
+  int ldc, kc, kp, l;  // child level l, parent level l - 1
+  const double* in;  // up: x^ of level l;   down: y^ of level l - 1
+  double* out;       // up: x^ of level l-1; down: y^ of level l
+  int64_t n;         // items (up: parents, down: children)
+};
+struct SweepTable {
+  SweepLevel L[kMaxLevels];
+  int64_t start[kMaxLevels + 1];
+  int nl;
+  int q;
+};
+
+__device__ __forceinline__ int64_t node_id(int level, int64_t i) { return (int64_t(1) << level) - 1 + i; }
+
+__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t want) {
+  if (lane_id() == 0) {
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v >= want) break;
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void set_flag(uint32_t* f, uint32_t v) {
+  __syncwarp();
+  if (lane_id() == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+  }
+}
+
+__device__ __forceinline__ int claim(unsigned long long* ticket, unsigned long long base) {
+  unsigned long long t = 0;
+  if (lane_id() == 0) t = atomicAdd(ticket, 1ull);
+  t = __shfl_sync(kFull, t, 0);
+  return int(t - base);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant__ SweepTable S,
+                                                       uint32_t* __restrict__ flag, uint32_t epoch,
+                                                       unsigned long long* __restrict__ ticket,
+                                                       unsigned long long base) {
+  const int r = 2 * lane_id();
+  const int64_t total = S.start[S.nl];
+  for (;;) {
+    const int64_t it = claim(ticket, base);
+    if (it >= total) break;
+    int e = 0;
+    while (it >= S.start[e + 1]) ++e;
+    const SweepLevel& L = S.L[e];
+    const int64_t p = it - S.start[e];
+    if (L.l < S.q) {  // children computed by this launch (leaves: by k_up_leaf before it)
+      wait_flag(flag + node_id(L.l, 2 * p), epoch);
+      wait_flag(flag + node_id(L.l, 2 * p + 1), epoch);
+    }
+    if (L.kp > 0) {
+      double o0 = 0.0, o1 = 0.0;
+      if (L.kc > 0) {
+        const double* x0 = L.in + (2 * p) * L.kc;
+        const double* x1 = x0 + L.kc;
+        const double v0 = r < L.kc ? __ldcg(x0 + r) : 0.0, v1 = r + 1 < L.kc ? __ldcg(x0 + r + 1) : 0.0;
+        const double w0 = r < L.kc ? __ldcg(x1 + r) : 0.0, w1 = r + 1 < L.kc ? __ldcg(x1 + r + 1) : 0.0;
+        const double* A = L.T + (2 * p) * L.stride;
+        o0 = gemvT_group<true>(A, A + L.stride, L.ldc, L.kp, 0, v0, v1, w0, w1, r < L.ldc);
+        o1 = gemvT_group<true>(A, A + L.stride, L.ldc, L.kp, 1, v0, v1, w0, w1, r < L.ldc);
+      }
+      if (r < L.kp) L.out[p * L.kp + r] = o0;
+      if (r + 1 < L.kp) L.out[p * L.kp + r + 1] = o1;
+    }
+    set_flag(flag + node_id(L.l - 1, p), epoch);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_down_fused(const __grid_constant__ SweepTable S,
+                                                         uint32_t* __restrict__ flag, uint32_t epoch,
+                                                         unsigned long long* __restrict__ ticket,
+                                                         unsigned long long base) {
+  const int r = 2 * lane_id();
+  const int64_t total = S.start[S.nl];
+  for (;;) {
+    const int64_t it = claim(ticket, base);
+    if (it >= total) break;
+    int e = 0;
+    while (it >= S.start[e + 1]) ++e;
+    const SweepLevel& L = S.L[e];
+    const int64_t c = it - S.start[e];
+    if (L.l > 1) wait_flag(flag + node_id(L.l - 1, c >> 1), epoch);  // the root's y^ is final
+    if (L.kc > 0 && L.kp > 0) {
+      const double* yp = L.in + (c >> 1) * L.kp;
+      const double a0 = r < L.kp ? __ldcg(yp + r) : 0.0, a1 = r + 1 < L.kp ? __ldcg(yp + r + 1) : 0.0;
+      double acc0, acc1;
+      gemvN_pair(L.T + c * L.stride, L.ldc, L.kp, a0, a1, r < L.ldc, acc0, acc1);
+      double* y = L.out + c * L.kc;
+      if (r < L.kc) y[r] = acc0 + __ldcg(y + r);
+      if (r + 1 < L.kc) y[r + 1] = acc1 + __ldcg(y + r + 1);
+    }
+    set_flag(flag + node_id(L.l, c), epoch);
+  }
+}
+
 struct LayerDesc {
   const double* val;
   const int32_t* rp;
@@ -390,6 +504,87 @@ void launch_up_level(const Matrix& A, int l, cudaStream_t s, int64_t p0, int64_t
   }
   k_up_level<<<warp_grid(np), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, p0, p1,
                                                 A.tr_begin(l), A.xhat.p + A.vec_off[l], xp);
+  H2B_CUDA(cudaGetLastError());
+}
+
+namespace {
+unsigned persistent_grid(const void* kernel) {
+  int per_sm = 0;
+  H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+  return unsigned(std::max(1, per_sm) * sm_count());
+}
+
+void sweep_state(Matrix& A) {
+  const int64_t nodes = int64_t(2) << A.q;
+  if (A.sweep_flag.n < size_t(nodes)) {
+    A.sweep_flag.alloc(nodes);
+    H2B_CUDA(cudaMemset(A.sweep_flag.p, 0, nodes * sizeof(uint32_t)));
+    A.sweep_ticket.alloc(2);
+    H2B_CUDA(cudaMemset(A.sweep_ticket.p, 0, 2 * sizeof(unsigned long long)));
+    A.sweep_epoch = 0;
+  }
+}
+}  // namespace
+
+void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s) {
+  require(A.part_s == 0, "launch_up_fused: whole matrices only");
+  sweep_state(A);
+  ++A.sweep_epoch;  // this hmv's epoch: up flags 2e, down flags 2e + 1
+  const int q = B.q;
+  SweepTable T{};
+  T.q = q;
+  int64_t tot = 0;
+  for (int l = q; l >= 1; --l) {
+    SweepLevel& L = T.L[T.nl];
+    L.T = B.transfer.p + B.tr_off[l];
+    L.stride = B.tr_stride(l);
+    L.ldc = B.ld(l);
+    L.kc = B.rank[l];
+    L.kp = B.rank[l - 1];
+    L.l = l;
+    L.in = B.xhat.p + B.vec_off[l];
+    L.out = B.xhat.p + B.vec_off[l - 1];
+    L.n = B.nodes(l - 1);
+    T.start[T.nl] = tot;
+    tot += L.n;
+    ++T.nl;
+  }
+  T.start[T.nl] = tot;
+  if (tot == 0) return;
+  H2B_CUDA(cudaMemsetAsync(A.sweep_ticket.p, 0, sizeof(unsigned long long), s));
+  k_up_fused<<<persistent_grid((const void*)k_up_fused), kThreads, 0, s>>>(T, A.sweep_flag.p, 2 * A.sweep_epoch,
+                                                                          A.sweep_ticket.p, 0ull);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_down_fused(Matrix& A, cudaStream_t s) {
+  require(A.part_s == 0, "launch_down_fused: whole matrices only");
+  sweep_state(A);
+  const int q = A.q;
+  SweepTable T{};
+  T.q = q;
+  int64_t tot = 0;
+  for (int l = 1; l <= q; ++l) {
+    SweepLevel& L = T.L[T.nl];
+    L.T = A.transfer.p + A.tr_off[l];
+    L.stride = A.tr_stride(l);
+    L.ldc = A.ld(l);
+    L.kc = A.rank[l];
+    L.kp = A.rank[l - 1];
+    L.l = l;
+    L.in = A.yhat.p + A.vec_off[l - 1];
+    L.out = A.yhat.p + A.vec_off[l];
+    L.n = A.nodes(l);
+    T.start[T.nl] = tot;
+    tot += L.n;
+    ++T.nl;
+  }
+  T.start[T.nl] = tot;
+  if (tot == 0) return;
+  H2B_CUDA(cudaMemsetAsync(A.sweep_ticket.p + 1, 0, sizeof(unsigned long long), s));
+  k_down_fused<<<persistent_grid((const void*)k_down_fused), kThreads, 0, s>>>(T, A.sweep_flag.p,
+                                                                              2 * A.sweep_epoch + 1,
+                                                                              A.sweep_ticket.p + 1, 0ull);
   H2B_CUDA(cudaGetLastError());
 }
 
