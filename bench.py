@@ -501,6 +501,7 @@ def main():
     # our kernels per step: k_up_leaf, k_up_fused (levels q..1), k_bsr,
     # k_down_fused (levels 1..q), k_down_leaf (plus two 16-byte ticket memsets)
     launches = 5 if info.depth >= 1 else 3
+    r = info.ranks
 
     for _ in range(args.warmup):
         h2.hmv(A, xt, yt, stream=sp)
