@@ -35,23 +35,6 @@ __device__ __forceinline__ int64_t warp_count() {
   return (int64_t(gridDim.x) * blockDim.x) >> 5;
 }
 
-// Butterfly reduce-scatter: lane L returns sum over all lanes of p[L].
-// 31 double shuffles for 32 independent dot products.
-__device__ __forceinline__ double reduce_scatter32(double (&p)[32]) {
-  const int lane = lane_id();
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const double send = up ? p[i] : p[i + s];
-      const double keep = up ? p[i + s] : p[i];
-      p[i] = keep + __shfl_xor_sync(kFull, send, s);
-    }
-  }
-  return p[0];
-}
-
 // Transposed product for the column group g in {0,1}:
 //   returns out[2*lane + g] = sum_r A[r, 2*lane+g] * v[r]  (+ B^T w when TWO)
 // A, B: column-major, leading dim ld (even), `cols` columns; the lane's row
