@@ -476,6 +476,7 @@ cudaEvent_t* timing_slots(Matrix& A) {
 }
 
 void hmv_device(Matrix& A, const double* x, double* y, double alpha, double beta, cudaStream_t s) {
+  NvtxRange nv("h2b hmv");
   const int q = A.q;
   cudaEvent_t* ev = timing_slots(A);
   if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));

@@ -1972,6 +1972,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     };
   };
   {
+    NvtxRange nv("h2b compress: orthogonalize");
     Timer t(s);
     orthogonalize(A, To, s, fl, r.flops_orthogonalize, pt, ws.trees,
                   overlap ? hook(To, true, true, r.flops_project_orth) : nullptr);
@@ -1979,6 +1980,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     r.time_orthogonalize_ms = t.stop();
   }
   {
+    NvtxRange nv("h2b compress: project (orthogonal)");
     Timer t(s);
     if (!overlap)
       for (int l = A.q; l >= 0; --l)
@@ -1992,6 +1994,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   pt.sum_f64(&n2, 1);
   r.frobenius_norm = std::sqrt(n2);
   {
+    NvtxRange nv("h2b compress: weight tree");
     Timer t(s);
     weights(A, A, false, R, s, fl, r.flops_weights, pt, ws.rtree, ar);
     if (!sym) weights(A, Cb, true, Rc, s, fl, r.flops_weights, pt, rtree_col, ar);  // transposed layers
@@ -2000,6 +2003,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   for (int l = 0; l <= A.q; ++l) A.cpl[l].max_row = saved_max[l];
   double energy = 0.0;
   {
+    NvtxRange nv("h2b compress: truncate");
     Timer t(s);
     energy = truncate(A, R, eps, Tt, s, fl, r.flops_truncate, pt, ws.trees, ar,
                       overlap ? hook(Tt, false, false, r.flops_project_trunc) : nullptr);
@@ -2007,6 +2011,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     r.time_truncate_ms = t.stop();
   }
   {
+    NvtxRange nv("h2b compress: project (truncated)");
     Timer t(s);
     if (!overlap)
       for (int l = A.q; l >= 0; --l)

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "h2b.h"
+#include "nvtx3/nvToolsExt.h"
 
 namespace h2b {
 
@@ -46,6 +47,14 @@ inline void require(bool ok, const std::string& msg) {
   } while (0)
 
 inline int pad2(int r) { return r + (r & 1); }
+
+// NVTX range for the profilers (nsys / ncu --nvtx); no cost without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Largest block dimension the compiled warp kernels cover (rows owned by a
 // lane pair: 2 * 32 lanes).
