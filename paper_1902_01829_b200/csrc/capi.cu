@@ -481,12 +481,13 @@ void hmv_device(Matrix& A, const double* x, double* y, double alpha, double beta
   cudaEvent_t* ev = timing_slots(A);
   if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
   Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
+  sweep_begin(A);
   launch_up_leaf(C, x, s);
-  if (q >= 1) launch_up_fused(A, C, s);  // levels q..1 in one dataflow launch
+  if (q >= 1) launch_up_fused(A, C, s, q, 1, false);  // levels q..1 in one dataflow launch
   if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
   launch_bsr(A, A.work.p, A.nwork, C.xc.p, A.yc.p, C.xhat.p, A.yhat.p, s, &C);
   if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
-  if (q >= 1) launch_down_fused(A, s);
+  if (q >= 1) launch_down_fused(A, s, false);
   launch_down_leaf(A, y, alpha, beta, true, s);
   if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
 }
@@ -937,9 +938,11 @@ h2b_status h2b_part_upsweep(h2b_matrix* Ah, const double* x, void* stream) {
     Matrix& A = *Ah;
     DeviceGuard g(A.device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    sweep_begin(A);
     launch_up_leaf(A, x, s);
     launch_gather(A.perm.p, x, A.xc.p, A.n, s);  // dense blocks read remote columns
-    for (int l = A.q; l > A.part_s; --l) launch_up_level(A, l, s, A.own_begin(l - 1), A.own_end(l - 1));
+    // this partition's levels q..s+1: one dataflow launch over its nodes
+    if (A.q > A.part_s) launch_up_fused(A, A, s, A.q, A.part_s + 1, true);
   });
 }
 
@@ -951,11 +954,12 @@ h2b_status h2b_part_finish(h2b_matrix* Ah, double* y_slice, void* stream) {
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
     cudaEvent_t* ev = timing_slots(A);
     if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
-    for (int l = A.part_s; l >= 1; --l) launch_up_level(A, l, s);  // replicated top
+    // replicated top (level s's x^ gathered from every partition)
+    if (A.part_s >= 1) launch_up_fused(A, A, s, A.part_s, 1, false);
     if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
     launch_bsr(A, A.work.p, A.nwork, A.xc.p, A.yc.p, A.xhat.p, A.yhat.p, s);
     if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
-    for (int l = 1; l <= A.q; ++l) launch_down_level(A, l, s, A.own_begin(l), A.own_end(l));
+    if (A.q >= 1) launch_down_fused(A, s, true);  // replicated top + own subtree
     launch_down_leaf(A, y_slice, 1.0, 0.0, false, s);
     if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
   });

@@ -216,8 +216,12 @@ void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, boo
 // downsweep (levels 1..q of A) as ONE persistent launch each: warps claim
 // nodes deepest-first (up) / top-down (down) and wait for their children /
 // parent through per-node flags (A holds the flags and tickets).
-void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s);
-void launch_down_fused(Matrix& A, cudaStream_t s);
+// sweep_begin: a new epoch for the flags (once per mat-vec).  Up: child
+// levels l_hi..l_lo (l_hi's x^ is input); down: levels 1..q (the root's y^ is
+// input); own: this handle's node ranges (partition), else all nodes.
+void sweep_begin(Matrix& A);
+void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s, int l_hi, int l_lo, bool own);
+void launch_down_fused(Matrix& A, cudaStream_t s, bool own);
 void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s);
 
 // 16-vector FP64-MMA mat-vec, device pointers (k_hmv_mv.cu).

@@ -236,17 +236,17 @@ __global__ void __launch_bounds__(kThreads) k_down_leaf(
 // never cleared.  Node vectors written by other SMs are read with ld.cg.
 struct SweepLevel {
   const double* T;   // transfers of the child level (block (c - cbegin) * stride)
-  int64_t stride;
+  int64_t stride, cbegin;
   int ldc, kc, kp, l;  // child level l, parent level l - 1
   const double* in;  // up: x^ of level l;   down: y^ of level l - 1
   double* out;       // up: x^ of level l-1; down: y^ of level l
-  int64_t n;         // items (up: parents, down: children)
+  int64_t n, i0;     // items (up: parents i0.., down: children i0..)
 };
 struct SweepTable {
   SweepLevel L[kMaxLevels];
   int64_t start[kMaxLevels + 1];
   int nl;
-  int q;
+  int q;  // up: the deepest child level (its x^ is input); down: the top parent level (its y^ is input)
 };
 
 __device__ __forceinline__ int64_t node_id(int level, int64_t i) { return (int64_t(1) << level) - 1 + i; }
@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant_
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevel& L = S.L[e];
-    const int64_t p = it - S.start[e];
-    if (L.l < S.q) {  // children computed by this launch (leaves: by k_up_leaf before it)
+    const int64_t p = L.i0 + (it - S.start[e]);
+    if (L.l < S.q) {  // children computed by this launch (level q: input, e.g. by k_up_leaf)
       wait_flag(flag + node_id(L.l, 2 * p), epoch);
       wait_flag(flag + node_id(L.l, 2 * p + 1), epoch);
     }
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant_
         const double* x1 = x0 + L.kc;
         const double v0 = r < L.kc ? __ldcg(x0 + r) : 0.0, v1 = r + 1 < L.kc ? __ldcg(x0 + r + 1) : 0.0;
         const double w0 = r < L.kc ? __ldcg(x1 + r) : 0.0, w1 = r + 1 < L.kc ? __ldcg(x1 + r + 1) : 0.0;
-        const double* A = L.T + (2 * p) * L.stride;
+        const double* A = L.T + (2 * p - L.cbegin) * L.stride;
         o0 = gemvT_group<true>(A, A + L.stride, L.ldc, L.kp, 0, v0, v1, w0, w1, r < L.ldc);
         o1 = gemvT_group<true>(A, A + L.stride, L.ldc, L.kp, 1, v0, v1, w0, w1, r < L.ldc);
       }
@@ -325,13 +325,13 @@ __global__ void __launch_bounds__(kThreads) k_down_fused(const __grid_constant__
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevel& L = S.L[e];
-    const int64_t c = it - S.start[e];
-    if (L.l > 1) wait_flag(flag + node_id(L.l - 1, c >> 1), epoch);  // the root's y^ is final
+    const int64_t c = L.i0 + (it - S.start[e]);
+    if (L.l - 1 > S.q) wait_flag(flag + node_id(L.l - 1, c >> 1), epoch);  // (top parent level: input)
     if (L.kc > 0 && L.kp > 0) {
       const double* yp = L.in + (c >> 1) * L.kp;
       const double a0 = r < L.kp ? __ldcg(yp + r) : 0.0, a1 = r + 1 < L.kp ? __ldcg(yp + r + 1) : 0.0;
       double acc0, acc1;
-      gemvN_pair(L.T + c * L.stride, L.ldc, L.kp, a0, a1, r < L.ldc, acc0, acc1);
+      gemvN_pair(L.T + (c - L.cbegin) * L.stride, L.ldc, L.kp, a0, a1, r < L.ldc, acc0, acc1);
       double* y = L.out + c * L.kc;
       if (r < L.kc) y[r] = acc0 + __ldcg(y + r);
       if (r + 1 < L.kc) y[r + 1] = acc1 + __ldcg(y + r + 1);
@@ -509,25 +509,29 @@ void sweep_state(Matrix& A) {
 }
 }  // namespace
 
-void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s) {
-  require(A.part_s == 0, "launch_up_fused: whole matrices only");
+void sweep_begin(Matrix& A) {
   sweep_state(A);
   ++A.sweep_epoch;  // this hmv's epoch: up flags 2e, down flags 2e + 1
-  const int q = B.q;
+}
+
+void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s, int l_hi, int l_lo, bool own) {
+  sweep_state(A);
   SweepTable T{};
-  T.q = q;
+  T.q = l_hi;
   int64_t tot = 0;
-  for (int l = q; l >= 1; --l) {
+  for (int l = l_hi; l >= l_lo; --l) {
     SweepLevel& L = T.L[T.nl];
     L.T = B.transfer.p + B.tr_off[l];
     L.stride = B.tr_stride(l);
+    L.cbegin = B.tr_begin(l);
     L.ldc = B.ld(l);
     L.kc = B.rank[l];
     L.kp = B.rank[l - 1];
     L.l = l;
     L.in = B.xhat.p + B.vec_off[l];
     L.out = B.xhat.p + B.vec_off[l - 1];
-    L.n = B.nodes(l - 1);
+    L.i0 = own ? B.own_begin(l - 1) : 0;
+    L.n = own ? B.own_count(l - 1) : B.nodes(l - 1);
     T.start[T.nl] = tot;
     tot += L.n;
     ++T.nl;
@@ -540,24 +544,25 @@ void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s) {
   H2B_CUDA(cudaGetLastError());
 }
 
-void launch_down_fused(Matrix& A, cudaStream_t s) {
-  require(A.part_s == 0, "launch_down_fused: whole matrices only");
+void launch_down_fused(Matrix& A, cudaStream_t s, bool own) {
   sweep_state(A);
   const int q = A.q;
   SweepTable T{};
-  T.q = q;
+  T.q = 0;  // the root's y^ is final (after the coupling multiply)
   int64_t tot = 0;
   for (int l = 1; l <= q; ++l) {
     SweepLevel& L = T.L[T.nl];
     L.T = A.transfer.p + A.tr_off[l];
     L.stride = A.tr_stride(l);
+    L.cbegin = A.tr_begin(l);
     L.ldc = A.ld(l);
     L.kc = A.rank[l];
     L.kp = A.rank[l - 1];
     L.l = l;
     L.in = A.yhat.p + A.vec_off[l - 1];
     L.out = A.yhat.p + A.vec_off[l];
-    L.n = A.nodes(l);
+    L.i0 = own ? A.own_begin(l) : 0;
+    L.n = own ? A.own_count(l) : A.nodes(l);
     T.start[T.nl] = tot;
     tot += L.n;
     ++T.nl;
