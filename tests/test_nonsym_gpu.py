@@ -9,7 +9,13 @@ the upsweep runs on A.col_basis(), the downsweep on A.row_basis).
 * compress (both bases orthogonalized, projected, weighted -- the column
   weight tree over the transposed layers -- and truncated,
   compression.hpp:466-551) against the reference's compress of the same
-  matrix: row and column ranks, error estimate, bytes, the operator;
+  matrix: row and column ranks, error estimate, bytes, the operator.  The
+  reference's weight-tree marshaling (compression.hpp:194-205, 236-243)
+  assumes square coupling blocks (ranks[l] x ranks[l]): with row rank !=
+  column rank on a level that has blocks it reads past them (undefined
+  behaviour: run-to-run different results, NaNs), so reference parity uses
+  equal ranks on the levels with blocks; unequal ranks are checked by the
+  operator they preserve;
 * the 16-vector pass; h2b_orthogonalize reports H2B_UNSUPPORTED (this version)."""
 import numpy as np
 import pytest
@@ -110,7 +116,7 @@ def _col_ranks(R):
                                                    (2, 1 << 12, 6, 1e-5, "random")])
 def test_compress_matches_reference(gpu, ref, dim, n, order, eps, make):
     base = ref.construct(dim, n, grid_order=order).to_host()
-    hm = scaled(base) if make == "scaled" else random_cols(base)
+    hm = scaled(base) if make == "scaled" else random_cols(base, drop=0)  # (see module doc)
     R = ref.from_host(hm)
     A = h2.H2Matrix.from_host(hm)
     x = np.random.default_rng(3).random(n)
@@ -154,3 +160,65 @@ def test_unsupported_paths_say_so(gpu, ref):
     with pytest.raises(_lib.H2bError) as e:
         h2.orthogonalize_basis(A)
     assert e.value.code == _lib.H2B_UNSUPPORTED and "non-symmetric" in str(e.value)
+
+
+def _with_col_ranks(base, col_ranks, seed):
+    """The structure of `base` with a fresh random column basis of the given ranks."""
+    from paper_1902_01829_b200.host import HostMatrix
+    q, m, n = base.depth, base.m, base.n
+    hm = HostMatrix.empty(n, m, q, base.ranks, base.cpl_blocks(), int(base.dense_row_ptr[-1]),
+                          np.asarray(col_ranks, np.int32))
+    rng = np.random.default_rng(seed)
+    for a in ("perm", "leaf", "transfer", "cpl_row_ptr", "cpl_col_idx", "dense_row_ptr", "dense_col_idx",
+              "dense_values"):
+        getattr(hm, a)[:] = getattr(base, a)
+    hm.col_leaf[:] = rng.standard_normal(hm.col_leaf.size) / 8
+    hm.col_transfer[:] = rng.standard_normal(hm.col_transfer.size) / 2
+    hm.cpl_values[:] = rng.standard_normal(hm.cpl_values.size) * 1e-2
+    return hm
+
+
+@pytest.mark.parametrize("drop", [0, 1, 5])
+def test_odd_and_empty_column_ranks(gpu, ref, drop):
+    """Odd column ranks, zero on the top levels (no coupling there, as after a
+    compress): padded leading dimensions and empty levels on the x^ side.
+    hmv / 16 vectors against the reference; compress against the reference
+    where its marshaling is defined (drop 0: equal ranks on the levels with
+    blocks), otherwise by the operator it preserves."""
+    n = 1 << 12
+    base = ref.construct(2, n, grid_order=5).to_host()  # rank 25
+    cr = [0, 0, 0] + [25 - drop] * (base.depth - 2)
+    hm = _with_col_ranks(base, cr, drop)
+    R = ref.from_host(hm)
+    A = h2.H2Matrix.from_host(hm)
+    rng = np.random.default_rng(drop)
+    x = rng.random(n)
+    y0 = R.hmv(x)
+    assert rel_err(h2.hmv(A, x), y0) <= 1e-12
+    X = rng.random((16, n))
+    assert rel_err(h2.hmv_multi(A, X)[3], R.hmv(X[3])) <= 1e-12
+    eps = 1e-6
+    rg = h2.compress(A, eps)
+    assert all(a <= b for a, b in zip(rg.new_ranks, rg.old_ranks))
+    assert rel_err(h2.hmv(A, x), y0) <= 10 * eps
+    if drop == 0:
+        rr = R.compress(eps)
+        assert all(abs(a - b) <= 1 for a, b in zip(rg.new_ranks, rr["new_ranks"]))
+        assert rel_err(h2.hmv(A, x), R.hmv(x)) <= 10 * eps
+
+
+def test_invalid_weight_stack_rejected_like_reference(gpu, ref):
+    """A column rank above an empty level whose stacks would be shorter than
+    wide: the reference's qr_r_only_batched rejects it; so does compress()."""
+    import oracle
+    n = 1 << 12
+    base = ref.construct(2, n, grid_order=5).to_host()
+    hm = _with_col_ranks(base, [0, 0] + [24] * (base.depth - 1), 1)
+    R = ref.from_host(hm)
+    A = h2.H2Matrix.from_host(hm)
+    with pytest.raises(oracle.OracleInvalidArgument) as er:
+        R.compress(1e-6)
+    with pytest.raises(_lib.H2bInvalidArgument) as eg:
+        h2.compress(A, 1e-6)
+    assert "qr_r_only_batched: requires rows >= cols" in str(er.value)
+    assert "qr_r_only_batched: requires rows >= cols" in str(eg.value)

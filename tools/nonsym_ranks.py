@@ -4,7 +4,7 @@ from nonsym import scaled, random_cols
 ref = oracle.reference()
 for dim, n, order, eps, make in [(2, 1 << 13, 8, 1e-7, "scaled"), (3, 1 << 12, 4, 1e-6, "scaled"), (2, 1 << 12, 6, 1e-5, "random"), (2, 1 << 14, 8, 1e-7, "scaled")]:
     base = ref.construct(dim, n, grid_order=order).to_host()
-    hm = scaled(base) if make == "scaled" else random_cols(base)
+    hm = scaled(base) if make == "scaled" else random_cols(base, drop=0)
     R = ref.from_host(hm); A = h2.H2Matrix.from_host(hm)
     rr = R.compress(eps); rg = h2.compress(A, eps)
     import ctypes as C
