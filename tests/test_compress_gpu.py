@@ -173,3 +173,25 @@ def test_compress_errors(gpu):
     A = h2.H2Matrix.construct(2, 1 << 10)
     with pytest.raises(h2.H2bInvalidArgument, match="eps must be non-negative"):
         h2.compress(A, -1.0)
+
+
+@pytest.mark.parametrize("dim,n,order", [(2, 1 << 13, 8), (3, 1 << 12, 4)])
+@pytest.mark.parametrize("eps", [1e-3, 1e-5, 1e-8, 1e-10, 1e-12])
+def test_compress_eps_sweep_matches_reference(gpu, ref, dim, n, order, eps):
+    """Ranks, bytes, error estimate and the compressed operator against the
+    reference over a wide tolerance range (rank decisions at eps * sigma_1
+    from 1e-3 down to 1e-12 of the graded spectra)."""
+    R = ref.construct(dim, n, grid_order=order)
+    A = h2.H2Matrix.from_host(R.to_host())
+    x = np.random.default_rng(17).random(n)
+    y0 = R.hmv(x)
+    rr = R.compress(eps)
+    rg = h2.compress(A, eps)
+    assert _ranks_close(rg.new_ranks, rr["new_ranks"]), (rg.new_ranks, rr["new_ranks"])
+    if rg.new_ranks == rr["new_ranks"]:
+        assert rg.bytes_after == int(rr["bytes_after"])
+    if rr["frobenius_error"] > 1e-14:
+        assert 0.5 <= rg.frobenius_error / rr["frobenius_error"] <= 2.0
+    tol = max(10 * eps, 1e-12)
+    assert rel_err(h2.hmv(A, x), y0) <= tol
+    assert rel_err(h2.hmv(A, x), R.hmv(x)) <= tol
