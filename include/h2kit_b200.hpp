@@ -200,7 +200,7 @@ inline void pull(h2b_matrix* h, H2Matrix<double>& A) {
   std::vector<double> tr;
   size_t ntr = 0, nsv = 0;
   for (int l = 1; l <= q; ++l) ntr += (size_t(1) << l) * inf.ranks[l] * inf.ranks[l - 1];
-  for (int l = 0; l <= q; ++l) nsv += size_t(inf.cpl_blocks[l]) * inf.ranks[l] * inf.ranks[l];
+  for (int l = 0; l <= q; ++l) nsv += size_t(inf.cpl_blocks[l]) * inf.ranks[l] * inf.col_ranks[l];
   B.leaf_pool.assign((size_t(1) << q) * inf.m * inf.ranks[q], 0.0);
   tr.resize(ntr);
   std::vector<double> sv(nsv);
@@ -215,10 +215,26 @@ inline void pull(h2b_matrix* h, H2Matrix<double>& A) {
   o = 0;
   for (int l = 0; l <= q; ++l) {
     auto& L = A.coupling.levels[l];
-    const size_t sz = size_t(inf.cpl_blocks[l]) * inf.ranks[l] * inf.ranks[l];
+    const size_t sz = size_t(inf.cpl_blocks[l]) * inf.ranks[l] * inf.col_ranks[l];
     L.values.assign(sv.begin() + o, sv.begin() + o + sz);
-    L.brows = L.bcols = inf.ranks[l];
+    L.brows = inf.ranks[l];
+    L.bcols = inf.col_ranks[l];
     o += sz;
+  }
+  if (!inf.symmetric) {  // the column basis V / F (h2_matrix.hpp:69)
+    BasisTree<double>& V = *A.col_basis_store;
+    V.ranks.assign(inf.col_ranks, inf.col_ranks + q + 1);
+    size_t nct = 0;
+    for (int l = 1; l <= q; ++l) nct += (size_t(1) << l) * inf.col_ranks[l] * inf.col_ranks[l - 1];
+    std::vector<double> ct(nct);
+    V.leaf_pool.assign((size_t(1) << q) * inf.m * inf.col_ranks[q], 0.0);
+    check(h2b_matrix_export_col(h, V.leaf_pool.data(), ct.data()));
+    o = 0;
+    for (int l = 1; l <= q; ++l) {
+      const size_t sz = (size_t(1) << l) * inf.col_ranks[l] * inf.col_ranks[l - 1];
+      V.transfer[l].assign(ct.begin() + o, ct.begin() + o + sz);
+      o += sz;
+    }
   }
 }
 

@@ -175,6 +175,20 @@ void nonsymmetric_hmv() {
   h2kit_b200::hmv(B, x.data(), yg.data());
   CHECK(rel(yb, yr) <= 1e-13);
   CHECK(rel(yg, yb) <= 1e-12);
+  // compress through the shim: the host object (both bases) is refreshed and
+  // matches the reference's own compress of the same matrix
+  H2Matrix<double> Bref = B;
+  const auto rr = h2kit::compress(Bref, 1e-7);
+  const auto rg = h2kit_b200::compress(B, 1e-7);
+  for (size_t l = 0; l < rr.new_ranks.size(); ++l) CHECK(rg.new_ranks[l] == rr.new_ranks[l]);
+  for (size_t l = 0; l < rr.new_ranks.size(); ++l)
+    CHECK(B.col_basis_store->ranks[l] == Bref.col_basis_store->ranks[l]);
+  CHECK(rg.bytes_after == memory_footprint(B).total());
+  std::vector<double> y1(n), y2(n);
+  h2kit::hmv(B, x.data(), y1.data());      // the refreshed host object, on the CPU
+  h2kit::hmv(Bref, x.data(), y2.data());
+  CHECK(rel(y1, yr) <= 1e-6);
+  CHECK(rel(y1, y2) <= 1e-6);
 }
 
 void errors_are_invalid_argument() {
@@ -199,7 +213,7 @@ int main() {
   run("phases match the reference", phases_match_reference);
   run("compress matches the reference", compress_matches_reference);
   run("orthogonalize gives orthonormal leaves", orthogonalize_orthonormal);
-  run("non-symmetric hmv matches the reference", nonsymmetric_hmv);
+  run("non-symmetric hmv and compress match the reference", nonsymmetric_hmv);
   run("invalid arguments throw std::invalid_argument", errors_are_invalid_argument);
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
