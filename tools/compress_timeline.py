@@ -27,6 +27,16 @@ for _ in range(reps):
         gaps.append((g, a.name[:40], b.name[:40]))
     big = [(round(g, 2), a, b) for g, a, b in gaps if g > 1.0]
     gaps.sort(reverse=True)
+    # device idle time: the span minus the union of kernel intervals
+    idle, cur_end, holes = 0.0, None, []
+    for e in ev:
+        st, en = e.time_range.start, e.time_range.end
+        if cur_end is not None and st > cur_end:
+            idle += (st - cur_end) / 1e3
+            holes.append((round((st - cur_end) / 1e3, 3), e.name.replace("h2b::(anonymous namespace)::", "")[:28]))
+        cur_end = en if cur_end is None else max(cur_end, en)
+    holes.sort(reverse=True)
+    print(json.dumps(dict(idle_ms=round(idle, 2), n_holes=len(holes), top_holes=holes[:12])), flush=True)
     slow = sorted(((e.time_range.elapsed_us() / 1e3, e.name[:50]) for e in ev), reverse=True)[:6]
     agg = {}
     for e in ev:
