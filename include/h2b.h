@@ -16,7 +16,8 @@
  *   h2b_downsweep        <- h2kit::downsweep(U, yhat, yc, n)          hmv.hpp:129-157
  *   h2b_dense_mv         <- h2kit::block_sparse_mv(A.dense, xc, yc, alpha, beta)  bsr.hpp:79-82
  *   h2b_compress         <- h2kit::compress(A, eps)                   include/h2kit/compression.hpp:466-551
- *   h2b_orthogonalize    <- h2kit::orthogonalize_basis(B)             compression.hpp:69-126
+ *   h2b_orthogonalize    <- h2kit::orthogonalize_basis(A.row_basis)   compression.hpp:69-126
+ *   h2b_orthogonalize_col <- h2kit::orthogonalize_basis(A.col_basis())
  *   h2b_matrix_build     <- h2kit::construct<double>(points, spec, cfg)  include/h2kit/construction.hpp:179-200
  *   h2b_matrix_create    <- (host H2Matrix<double> -> device mirror; the HmvContext analogue hmv.hpp:161-172)
  *   h2b_matrix_export    <- (device -> host H2Matrix<double> arrays, e.g. after compress)
@@ -206,12 +207,17 @@ H2B_API h2b_status h2b_dense_mv(h2b_matrix* A, const double* xc, double* yc, dou
 
 /* Algebraic recompression in place (orthogonalize, project, weights,
  * truncate at relative eps, project).  Exclusive access required. */
-/* Non-symmetric matrices: h2b_compress, h2b_hmv, h2b_hmv_multi and the phase
- * entry points support them; h2b_orthogonalize returns H2B_UNSUPPORTED. */
+/* Non-symmetric matrices (a separate column basis) are supported by every
+ * entry point; h2b_orthogonalize works on the row basis, h2b_orthogonalize_col
+ * on the column basis. */
 H2B_API h2b_status h2b_compress(h2b_matrix* A, double eps, h2b_compress_report* report);
 /* Orthogonalize only (in place); projection tree written to t_out (host,
  * level-concatenated ranks[l]^2 per node) when non-NULL. */
 H2B_API h2b_status h2b_orthogonalize(h2b_matrix* A, double* t_out);
+/* orthogonalize_basis(A.col_basis()) (compression.hpp:69-126, h2_matrix.hpp:75-78):
+ * the column basis of a non-symmetric matrix (t_out: col_ranks[l]^2 per node);
+ * on a symmetric matrix the same as h2b_orthogonalize. */
+H2B_API h2b_status h2b_orthogonalize_col(h2b_matrix* A, double* t_out);
 /* compress() keeps its device workspace (projection / weight trees and
  * scratch, a few GB) cached per device for the next call; this frees it. */
 H2B_API h2b_status h2b_release_cached_memory(int device);

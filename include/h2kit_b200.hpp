@@ -12,6 +12,7 @@
 //   h2kit::compress(A, eps)                 ->  h2kit_b200::compress(A, eps)
 //        (include/h2kit/compression.hpp:466-551)
 //   h2kit::orthogonalize_basis(B)           ->  h2kit_b200::orthogonalize_basis(A)   (:69-126)
+//     (B = A.col_basis() of a non-symmetric A -> h2kit_b200::orthogonalize_col_basis(A))
 //
 // Semantics match the reference: alpha/beta (beta == 0 never reads y), x/y
 // in original point order, compress() mutates A in place and returns a
@@ -336,6 +337,20 @@ inline std::vector<double> orthogonalize_basis(H2Matrix<double>& A) {
     nt += (size_t(1) << l) * A.row_basis.ranks[l] * A.row_basis.ranks[l];
   std::vector<double> T(nt);
   detail::check(h2b_orthogonalize(m->get(), T.data()));
+  detail::pull(m->get(), A);
+  detail::rekey(A, m);
+  return T;
+}
+
+// orthogonalize_basis(A.col_basis()) (h2_matrix.hpp:75-78): the column basis of
+// a non-symmetric matrix, in place (the row basis itself when symmetric).
+inline std::vector<double> orthogonalize_col_basis(H2Matrix<double>& A) {
+  auto m = detail::mirror_of(A);
+  size_t nt = 0;
+  for (int l = 0; l <= A.depth(); ++l)
+    nt += (size_t(1) << l) * A.col_basis().ranks[l] * A.col_basis().ranks[l];
+  std::vector<double> T(nt);
+  detail::check(h2b_orthogonalize_col(m->get(), T.data()));
   detail::pull(m->get(), A);
   detail::rekey(A, m);
   return T;

@@ -293,6 +293,18 @@ class OracleMatrix:
         self.be.check(self.be.fn("orthogonalize")(self.h, out.ctypes.data))
         return out
 
+    def orthogonalize_col(self):
+        """orthogonalize_basis(A.col_basis()) (reference backend only)."""
+        n, m, q, sym = self.shape()
+        cr = np.zeros(q + 1, np.int32)
+        self.be.lib.ref_col_ranks.argtypes = [_P, C.c_void_p]
+        self.be.lib.ref_col_ranks(self.h, cr.ctypes.data)
+        out = np.zeros(int(sum((1 << l) * int(r) ** 2 for l, r in enumerate(cr))), np.float64)
+        f = self.be.lib.ref_orthogonalize_col
+        f.argtypes, f.restype = [_P, _P], _I
+        self.be.check(f(self.h, out.ctypes.data))
+        return out
+
     def orth_project_weights(self):
         ranks, _, _ = self.layout()
         out = np.zeros(int(sum((1 << l) * int(r) ** 2 for l, r in enumerate(ranks))), np.float64)

@@ -378,6 +378,19 @@ int ref_orthogonalize(void* h, double* t_out) {
   });
 }
 
+// The same on the column basis (h2_matrix.hpp:75-78; the row basis itself
+// when symmetric); T: col_ranks[l]^2 per node.
+int ref_orthogonalize_col(void* h, double* t_out) {
+  return guarded([&] {
+    Mat& A = *static_cast<Mat*>(h);
+    const ProjectionTree<double> T = orthogonalize_basis(A.col_basis());
+    for (auto& p : T.pool) {
+      std::memcpy(t_out, p.data(), p.size() * sizeof(double));
+      t_out += p.size();
+    }
+  });
+}
+
 // Orthogonalize + project (in place), then the weight tree R (level-
 // concatenated, k_l x k_l per node).
 int ref_orth_project_weights(void* h, double* r_out) {

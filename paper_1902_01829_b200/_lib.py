@@ -122,6 +122,7 @@ _SIGS = {
     "h2b_compress": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(CompressReport)]),
     "h2b_part_compress": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(Comm), C.POINTER(CompressReport)]),
     "h2b_orthogonalize": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "h2b_orthogonalize_col": (C.c_int, [C.c_void_p, C.c_void_p]),
     "h2b_last_hmv_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "h2b_matrix_build_part": (C.c_int, [C.POINTER(BuildConfig), C.c_int, C.c_int, C.c_int,
                                         C.POINTER(C.c_void_p)]),

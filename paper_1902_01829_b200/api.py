@@ -300,12 +300,20 @@ def compress(A: H2Matrix, eps: float) -> CompressionReport:
     return report_from_c(rep, depth)
 
 
-def orthogonalize_basis(A: H2Matrix) -> np.ndarray:
-    """orthogonalize_basis(B) (compression.hpp:69-126): returns the projection tree
-    (level-concatenated k_l x k_l blocks)."""
+def orthogonalize_basis(A: H2Matrix, basis: str = "row") -> np.ndarray:
+    """orthogonalize_basis(B) (compression.hpp:69-126) on B = A.row_basis
+    (basis="row") or A.col_basis() (basis="col"; the same tree when A is
+    symmetric): the basis is orthogonalized in place, the coupling is not
+    projected.  Returns the projection tree (level-concatenated k_l x k_l
+    blocks, k = that basis' ranks)."""
+    if basis not in ("row", "col"):
+        raise ValueError("basis must be 'row' or 'col'")
     inf = A.info()
-    out = np.zeros(sum((1 << l) * r * r for l, r in enumerate(inf.ranks)), np.float64)
-    _lib.check(_lib.load().h2b_orthogonalize(A._h, out.ctypes.data))
+    ranks = inf.ranks if basis == "row" else inf.col_ranks
+    out = np.zeros(sum((1 << l) * int(ranks[l]) ** 2 for l in range(inf.depth + 1)), np.float64)
+    lib = _lib.load()
+    f = lib.h2b_orthogonalize if basis == "row" else lib.h2b_orthogonalize_col
+    _lib.check(f(A._h, out.ctypes.data))
     return out
 
 

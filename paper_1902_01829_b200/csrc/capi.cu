@@ -551,11 +551,6 @@ void whole(const Matrix& A, const char* what) {
   require(A.part_s == 0, std::string(what) + ": not supported on a partition handle");
 }
 
-void symmetric_only(const Matrix& A, const char* what) {
-  if (!A.symmetric)
-    throw Error(H2B_UNSUPPORTED, std::string(what) + ": non-symmetric matrices are not implemented on this path");
-}
-
 // Phase helpers take host or device pointers; host data goes through
 // temporary device buffers.
 struct Staged {
@@ -600,7 +595,7 @@ h2b_matrix* load_matrix(const std::string& path, int device, h2b_build_info* inf
 uint32_t crc32_bytes(const void* p, size_t n);
 void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_comm* comm = nullptr);
 void release_workspaces(int device);
-void orthogonalize_matrix(Matrix& A, double* t_out);
+void orthogonalize_matrix(Matrix& A, double* t_out, bool col);
 }  // namespace h2b
 
 extern "C" {
@@ -901,12 +896,21 @@ h2b_status h2b_part_compress(h2b_matrix* Ah, double eps, const h2b_comm* comm, h
   });
 }
 
+// orthogonalize_basis(A.row_basis) / orthogonalize_basis(A.col_basis())
+// (compression.hpp:69-126, h2_matrix.hpp:69-78); symmetric: the same tree.
 h2b_status h2b_orthogonalize(h2b_matrix* Ah, double* t_out) {
   return guarded([&] {
     require(Ah, "null matrix");
     whole(*Ah, "h2b_orthogonalize");
-    symmetric_only(*Ah, "h2b_orthogonalize");
-    orthogonalize_matrix(*Ah, t_out);
+    orthogonalize_matrix(*Ah, t_out, false);
+  });
+}
+
+h2b_status h2b_orthogonalize_col(h2b_matrix* Ah, double* t_out) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    whole(*Ah, "h2b_orthogonalize_col");
+    orthogonalize_matrix(*Ah, t_out, true);
   });
 }
 

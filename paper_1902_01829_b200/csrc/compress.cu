@@ -2046,15 +2046,18 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
 #endif
 }
 
-void orthogonalize_matrix(Matrix& A, double* t_out) {
+// col: the column basis (non-symmetric matrices; the row basis itself when
+// symmetric).  The coupling is not projected (the reference's contract).
+void orthogonalize_matrix(Matrix& A, double* t_out, bool col) {
   DeviceGuard g(A.device);
   cudaStream_t s = A.stream;
+  Matrix& B = col ? A.col_basis() : A;
   Flops fl;
   double f = 0;
   TreePool T;
   Workspace ws{A.device};
-  ws.buf = ws_checkout(A.device, TreePool::need(A, A.rank, A.rank));
-  orthogonalize(A, T, s, fl, f, Part{}, ws.buf.p);
+  ws.buf = ws_checkout(A.device, TreePool::need(B, B.rank, B.rank));
+  orthogonalize(B, T, s, fl, f, Part{}, ws.buf.p);
   if (t_out && T.off[A.q + 1])
     H2B_CUDA(cudaMemcpyAsync(t_out, T.p, T.off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToHost, s));
   H2B_CUDA(cudaStreamSynchronize(s));

@@ -143,8 +143,7 @@ void orthogonalize_orthonormal() {  // acceptance c3 (leaf V^T V = I)
 // A non-symmetric matrix (col_basis_store, h2_matrix.hpp:69): V = U D with a
 // positive diagonal D_l per level, F_c = D_l^-1 E_c D_{l-1}, S' = S D_l^-1 --
 // the same operator, evaluated by the reference and through the shim.
-void nonsymmetric_hmv() {
-  H2Matrix<double> A = kernel_matrix(2, 4096, 4);
+H2Matrix<double> scaled_nonsym(const H2Matrix<double>& A) {
   H2Matrix<double> B = A;
   B.symmetric = false;
   B.col_basis_store = A.row_basis;
@@ -167,6 +166,12 @@ void nonsymmetric_hmv() {
     const int k = L.brows;
     for (size_t e = 0; e < L.values.size(); ++e) L.values[e] /= d[l][(e / k) % k];
   }
+  return B;
+}
+
+void nonsymmetric_hmv() {
+  H2Matrix<double> A = kernel_matrix(2, 4096, 4);
+  H2Matrix<double> B = scaled_nonsym(A);
   const index_t n = A.n;
   std::vector<double> x(n), yr(n), yb(n), yg(n);
   for (index_t i = 0; i < n; ++i) x[i] = std::sin(0.37 * i) + 1.0;
@@ -189,6 +194,30 @@ void nonsymmetric_hmv() {
   h2kit::hmv(Bref, x.data(), y2.data());
   CHECK(rel(y1, yr) <= 1e-6);
   CHECK(rel(y1, y2) <= 1e-6);
+}
+
+// orthogonalize_basis on each basis of a non-symmetric matrix (compression.hpp:
+// 69-126): the shim's row / column entry points against the reference's.
+std::vector<double> flat(const ProjectionTree<double>& T) {
+  std::vector<double> v;
+  for (const auto& p : T.pool) v.insert(v.end(), p.begin(), p.end());
+  return v;
+}
+void nonsymmetric_orthogonalize() {
+  H2Matrix<double> B = scaled_nonsym(kernel_matrix(2, 4096, 4));
+  H2Matrix<double> R = B;
+  const auto tr_row = flat(h2kit::orthogonalize_basis(R.row_basis));
+  const auto tr_col = flat(h2kit::orthogonalize_basis(R.col_basis()));
+  const auto tg_row = h2kit_b200::orthogonalize_basis(B);
+  const auto tg_col = h2kit_b200::orthogonalize_col_basis(B);
+  CHECK(rel(tg_row, tr_row) <= 1e-11);
+  CHECK(rel(tg_col, tr_col) <= 1e-11);
+  CHECK(rel(B.row_basis.leaf_pool, R.row_basis.leaf_pool) <= 1e-11);
+  CHECK(rel(B.col_basis().leaf_pool, R.col_basis().leaf_pool) <= 1e-11);
+  for (int l = 1; l <= B.depth(); ++l) {
+    CHECK(rel(B.row_basis.transfer[l], R.row_basis.transfer[l]) <= 1e-11);
+    CHECK(rel(B.col_basis().transfer[l], R.col_basis().transfer[l]) <= 1e-11);
+  }
 }
 
 void errors_are_invalid_argument() {
@@ -214,6 +243,7 @@ int main() {
   run("compress matches the reference", compress_matches_reference);
   run("orthogonalize gives orthonormal leaves", orthogonalize_orthonormal);
   run("non-symmetric hmv and compress match the reference", nonsymmetric_hmv);
+  run("non-symmetric orthogonalize (row and column bases) matches the reference", nonsymmetric_orthogonalize);
   run("invalid arguments throw std::invalid_argument", errors_are_invalid_argument);
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;

@@ -16,7 +16,10 @@ the upsweep runs on A.col_basis(), the downsweep on A.row_basis).
   behaviour: run-to-run different results, NaNs), so reference parity uses
   equal ranks on the levels with blocks; unequal ranks are checked by the
   operator they preserve;
-* the 16-vector pass; h2b_orthogonalize reports H2B_UNSUPPORTED (this version)."""
+* the 16-vector pass;
+* orthogonalize_basis on the row basis and on the column basis (the two
+  entry points h2b_orthogonalize / h2b_orthogonalize_col) against the
+  reference's orthogonalize_basis(A.row_basis / A.col_basis())."""
 import numpy as np
 import pytest
 
@@ -154,12 +157,33 @@ def test_multi_vector_pass(gpu, ref):
         assert rel_err(Y[v], R.hmv(X[v])) <= 1e-12
 
 
-def test_unsupported_paths_say_so(gpu, ref):
-    hm = scaled(ref.construct(2, 1 << 12, grid_order=4).to_host())
+@pytest.mark.parametrize("make", ["scaled", "random"])
+def test_orthogonalize_each_basis_matches_reference(gpu, ref, make):
+    """compression.hpp:69-126 on A.row_basis, then on A.col_basis(): projection
+    trees and the orthogonalized pools against the reference's; the other
+    basis and the coupling are untouched."""
+    base = ref.construct(2, 1 << 12, grid_order=6).to_host()
+    hm = scaled(base) if make == "scaled" else random_cols(base)
+    R = ref.from_host(hm)
     A = h2.H2Matrix.from_host(hm)
-    with pytest.raises(_lib.H2bError) as e:
-        h2.orthogonalize_basis(A)
-    assert e.value.code == _lib.H2B_UNSUPPORTED and "non-symmetric" in str(e.value)
+    t_row = h2.orthogonalize_basis(A, "row")
+    assert rel_err(t_row, R.orthogonalize()) <= 1e-11
+    mid = A.to_host()
+    assert np.array_equal(mid.col_leaf, hm.col_leaf) and np.array_equal(mid.col_transfer, hm.col_transfer)
+    assert np.array_equal(mid.cpl_values, hm.cpl_values)
+    t_col = h2.orthogonalize_basis(A, "col")
+    assert rel_err(t_col, R.orthogonalize_col()) <= 1e-11
+    got, want = A.to_host(), R.to_host()
+    for a in ("leaf", "transfer", "col_leaf", "col_transfer"):
+        assert rel_err(getattr(got, a), getattr(want, a)) <= 1e-11, a
+    assert np.array_equal(got.leaf, mid.leaf)  # the row basis untouched by the column call
+    # orthonormal column leaves (acceptance c3 on V)
+    m, kq = hm.m, int(hm.col_ranks[-1])
+    V = got.col_leaf.reshape(-1, kq, m).transpose(0, 2, 1)
+    G = np.einsum("bij,bik->bjk", V, V)
+    assert np.max(np.abs(G - np.eye(kq))) <= 1e-12
+    with pytest.raises(ValueError):
+        h2.orthogonalize_basis(A, "diagonal")
 
 
 def _with_col_ranks(base, col_ranks, seed):
