@@ -584,7 +584,11 @@ __device__ __forceinline__ void weights_step(double (&B)[NCOL][CR], const double
   }
 }
 
-constexpr int kWWarps = 4;  // nodes (warps) per CTA
+// nodes (warps) per CTA.  One-warp CTAs, 12 per SM (the register and shared
+// memory limit), measured at C3: weight tree 108.2 ms against 112.8 ms for
+// 4-warp CTAs x 3 (2 x 6: 112.7, 6 x 2: 113.3).
+constexpr int kWWarps = 1;
+constexpr int kWCtas = 12;  // resident CTAs per SM (launch bound)
 // A work item of k_weights: the stack rows [parent rows if par][blocks b0..b1)
 // of node `node`, R written to slot `out` (transposed when the launch's out_t
 // is set, so a merge launch can read the partial R's as "blocks").
@@ -605,7 +609,7 @@ struct WSrc {
 };
 
 template <int NCOL, int CR, bool TRANS>
-__global__ void __launch_bounds__(32 * kWWarps, 3) k_weights(const double* __restrict__ P, int kc, int kp,
+__global__ void __launch_bounds__(32 * kWWarps, kWCtas) k_weights(const double* __restrict__ P, int kc, int kp,
                                                           const __grid_constant__ WSrc src_blocks,
                                                           double* __restrict__ Rout, int out_t,
                                                           const WItem* __restrict__ items, int64_t nitems,
