@@ -246,3 +246,16 @@ def test_invalid_weight_stack_rejected_like_reference(gpu, ref):
         h2.compress(A, 1e-6)
     assert "qr_r_only_batched: requires rows >= cols" in str(er.value)
     assert "qr_r_only_batched: requires rows >= cols" in str(eg.value)
+
+
+def test_orthogonalize_col_on_symmetric_is_the_row_basis(gpu, ref):
+    """A.col_basis() is A.row_basis when symmetric (h2_matrix.hpp:75-78): both
+    entry points orthogonalize the one basis, bitwise alike."""
+    hm = ref.construct(2, 1 << 12, grid_order=6).to_host()
+    A, B = h2.H2Matrix.from_host(hm), h2.H2Matrix.from_host(hm)
+    t_row = h2.orthogonalize_basis(A, "row")
+    t_col = h2.orthogonalize_basis(B, "col")
+    assert np.array_equal(t_row, t_col)
+    a, b = A.to_host(), B.to_host()
+    assert np.array_equal(a.leaf, b.leaf) and np.array_equal(a.transfer, b.transfer)
+    assert rel_err(t_row, ref.from_host(hm).orthogonalize()) <= 1e-11
