@@ -29,3 +29,21 @@ def test_scaled_basis_is_the_same_operator_in_the_reference(ref):
     N = ref.from_host(scaled(R.to_host()))
     x = np.random.default_rng(2).random(n)
     assert rel_err(N.hmv(x), R.hmv(x)) <= 1e-13
+
+
+def test_reference_column_orthogonalize_binding(ref):
+    """oracle binding of orthogonalize_basis(A.col_basis()) (the checker of
+    h2b_orthogonalize_col): orthonormal column leaves, the row basis untouched,
+    and on a symmetric matrix the row-basis result."""
+    base = ref.construct(2, 1 << 11, grid_order=4).to_host()
+    R = ref.from_host(random_cols(base))
+    before = R.to_host()
+    t = R.orthogonalize_col()
+    after = R.to_host()
+    assert t.size == sum((1 << l) * int(k) ** 2 for l, k in enumerate(before.col_ranks))
+    assert np.array_equal(after.leaf, before.leaf) and np.array_equal(after.transfer, before.transfer)
+    k, m = int(after.col_ranks[-1]), after.m
+    V = after.col_leaf.reshape(-1, k, m).transpose(0, 2, 1)
+    assert np.max(np.abs(np.einsum("bij,bik->bjk", V, V) - np.eye(k))) <= 1e-12
+    S1, S2 = ref.from_host(base), ref.from_host(base)
+    assert np.array_equal(S1.orthogonalize_col(), S2.orthogonalize())
