@@ -193,6 +193,19 @@ H2B_API uint32_t h2b_crc32(const void* data, uint64_t len);
  * the matrix's own stream). Host pointers: the call is synchronous. */
 H2B_API h2b_status h2b_hmv(h2b_matrix* A, const double* x, double* y, double alpha, double beta,
                    h2b_ptr_kind kind, void* stream);
+/* Per-caller workspaces: the HmvContext analogue (hmv.hpp:159-172).  The
+ * reference allows concurrent hmv calls on one immutable matrix with one
+ * context each; so does this library.  A context is sized lazily for the
+ * matrix it is used with (and re-sized after compress changed the ranks).
+ * Calls that share a context (or use none: the handle's own workspace) are
+ * serialised in device order across streams, never raced. */
+typedef struct h2b_context h2b_context;
+H2B_API h2b_status h2b_context_create(h2b_matrix* A, h2b_context** out);
+H2B_API h2b_status h2b_context_destroy(h2b_context* ctx);
+/* hmv(A, x, y, alpha, beta, ctx) (hmv.hpp:175-188); ctx may be NULL. */
+H2B_API h2b_status h2b_hmv_ctx(h2b_matrix* A, h2b_context* ctx, const double* x, double* y, double alpha,
+                               double beta, h2b_ptr_kind kind, void* stream);
+
 /* nvec columns, leading dimensions ldx/ldy (>= n). */
 H2B_API h2b_status h2b_hmv_multi(h2b_matrix* A, int nvec, const double* X, int64_t ldx, double* Y,
                          int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream);
@@ -201,7 +214,8 @@ H2B_API h2b_status h2b_hmv_multi(h2b_matrix* A, int nvec, const double* X, int64
  * are level-concatenated: level l holds 2^l * ranks[l] doubles). */
 H2B_API h2b_status h2b_upsweep(h2b_matrix* A, const double* xc, double* xhat, h2b_ptr_kind kind);
 H2B_API h2b_status h2b_tree_multiply(h2b_matrix* A, const double* xhat, double* yhat, h2b_ptr_kind kind);
-H2B_API h2b_status h2b_downsweep(h2b_matrix* A, const double* yhat, double* yc, h2b_ptr_kind kind);
+/* yhat is in/out like the reference's LevelVectors (y^l += E y^{l-1}); yc += U y^q. */
+H2B_API h2b_status h2b_downsweep(h2b_matrix* A, double* yhat, double* yc, h2b_ptr_kind kind);
 H2B_API h2b_status h2b_dense_mv(h2b_matrix* A, const double* xc, double* yc, double alpha, double beta,
                         h2b_ptr_kind kind);
 

@@ -115,15 +115,28 @@ class Mirror {
     auto f = flatten(A);
     check(h2b_matrix_create(&f->desc, device, &h_));
   }
-  ~Mirror() {
-    if (h_) h2b_matrix_destroy(h_);
-  }
   Mirror(const Mirror&) = delete;
   Mirror& operator=(const Mirror&) = delete;
   h2b_matrix* get() const { return h_; }
+  // The device workspace of a caller's HmvContext (created on first use).
+  h2b_context* context(const void* key) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = ctx_.find(key);
+    if (it != ctx_.end()) return it->second;
+    h2b_context* c = nullptr;
+    check(h2b_context_create(h_, &c));
+    ctx_[key] = c;
+    return c;
+  }
+  ~Mirror() {
+    for (auto& kv : ctx_) h2b_context_destroy(kv.second);
+    if (h_) h2b_matrix_destroy(h_);
+  }
 
  private:
   h2b_matrix* h_ = nullptr;
+  std::mutex mu_;
+  std::map<const void*, h2b_context*> ctx_;
 };
 
 inline std::mutex& cache_mutex() {
@@ -247,13 +260,13 @@ inline void invalidate(const H2Matrix<double>& A) {
   detail::cache().erase(&A);
 }
 
-// y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-188).  ctx is accepted for
-// signature compatibility; the device workspace lives in the mirror.
+// y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-188).  Each HmvContext gets
+// its own device workspace (h2b_context), so concurrent calls with one
+// context each run concurrently, like the reference's (hmv.hpp:159-160).
 inline void hmv(const H2Matrix<double>& A, const double* x, double* y, double alpha, double beta,
                 HmvContext<double>& ctx) {
-  (void)ctx;
   auto m = detail::mirror_of(A);
-  detail::check(h2b_hmv(m->get(), x, y, alpha, beta, H2B_PTR_AUTO, nullptr));
+  detail::check(h2b_hmv_ctx(m->get(), m->context(&ctx), x, y, alpha, beta, H2B_PTR_AUTO, nullptr));
 }
 
 inline void hmv(const H2Matrix<double>& A, const double* x, double* y, double alpha = 1.0,
@@ -280,11 +293,21 @@ inline void upsweep(const H2Matrix<double>& A, const double* xc, LevelVectors<do
 inline void tree_multiply(const H2Matrix<double>& A, const LevelVectors<double>& xhat,
                           LevelVectors<double>& yhat) {
   auto m = detail::mirror_of(A);
-  std::vector<double> xf, yf;
-  for (auto& p : xhat.pool) xf.insert(xf.end(), p.begin(), p.end());
-  yf.assign(xf.size(), 0.0);
-  detail::check(h2b_tree_multiply(m->get(), xf.data(), yf.data(), H2B_PTR_HOST));
+  // x^ follows the column basis, y^ the row basis (hmv.hpp:166-167): size
+  // each side from its own basis, never one from the other.
+  LevelVectors<double> xs;
+  xs.resize(A.col_basis());
+  std::vector<double> xf;
+  for (size_t l = 0; l < xs.pool.size(); ++l) {
+    if (l >= xhat.pool.size() || xhat.pool[l].size() != xs.pool[l].size())
+      throw std::invalid_argument("tree_multiply: dim mismatch");
+    xf.insert(xf.end(), xhat.pool[l].begin(), xhat.pool[l].end());
+  }
   yhat.resize(A.row_basis);
+  size_t ny = 0;
+  for (auto& p : yhat.pool) ny += p.size();
+  std::vector<double> yf(std::max<size_t>(ny, 1), 0.0);
+  detail::check(h2b_tree_multiply(m->get(), xf.data(), yf.data(), H2B_PTR_HOST));
   size_t o = 0;
   for (auto& p : yhat.pool) {
     std::copy(yf.begin() + o, yf.begin() + o + p.size(), p.begin());
@@ -292,11 +315,25 @@ inline void tree_multiply(const H2Matrix<double>& A, const LevelVectors<double>&
   }
 }
 
+// downsweep (hmv.hpp:129-157): y^ is updated in place like the reference's
+// LevelVectors (y^l += E y^{l-1}), yc += U y^q.
 inline void downsweep(const H2Matrix<double>& A, LevelVectors<double>& yhat, double* yc) {
   auto m = detail::mirror_of(A);
+  LevelVectors<double> ys;
+  ys.resize(A.row_basis);
   std::vector<double> yf;
-  for (auto& p : yhat.pool) yf.insert(yf.end(), p.begin(), p.end());
+  for (size_t l = 0; l < ys.pool.size(); ++l) {
+    if (l >= yhat.pool.size() || yhat.pool[l].size() != ys.pool[l].size())
+      throw std::invalid_argument("downsweep: dim mismatch");
+    yf.insert(yf.end(), yhat.pool[l].begin(), yhat.pool[l].end());
+  }
+  yf.resize(std::max<size_t>(yf.size(), 1));
   detail::check(h2b_downsweep(m->get(), yf.data(), yc, H2B_PTR_HOST));
+  size_t o = 0;
+  for (auto& p : yhat.pool) {
+    std::copy(yf.begin() + o, yf.begin() + o + p.size(), p.begin());
+    o += p.size();
+  }
 }
 
 // compress(A, eps) (compression.hpp:466-551): runs on the device mirror and

@@ -132,6 +132,10 @@ _SIGS = {
     "h2b_validate_sampled": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double,
                                        C.c_uint64, C.POINTER(C.c_double)]),
     "h2b_set_phase_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "h2b_context_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "h2b_context_destroy": (C.c_int, [C.c_void_p]),
+    "h2b_hmv_ctx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                              C.c_int, C.c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -32,6 +32,43 @@ def _ptr(a):
     raise TypeError(f"unsupported array type {type(a)}")
 
 
+def _bad(msg: str) -> Exception:
+    """The Python face of the reference's std::invalid_argument."""
+    return _lib.H2bInvalidArgument(_lib.H2B_INVALID_ARGUMENT, msg)
+
+
+def _vec(a, n: int, name: str, writable: bool = False):
+    """(pointer, kind) of a float64 vector of exactly n entries: a C-contiguous
+    numpy array (host) or a contiguous torch tensor (host or CUDA).  The C side
+    copies exactly n doubles from / to the pointer, so anything else is a
+    ValueError here (the reference's std::invalid_argument), never an
+    out-of-bounds access."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise _bad(f"{name}: must be a C-contiguous float64 array")
+        if writable and not a.flags.writeable:
+            raise _bad(f"{name}: must be writable")
+        if a.size != n:
+            raise _bad(f"{name}: has {a.size} entries, expected {n}")
+        return a.ctypes.data, _lib.PTR_HOST
+    if hasattr(a, "data_ptr"):
+        import torch
+        if a.dtype != torch.float64 or not a.is_contiguous():
+            raise _bad(f"{name}: must be a contiguous float64 tensor")
+        if a.numel() != n:
+            raise _bad(f"{name}: has {a.numel()} entries, expected {n}")
+        return a.data_ptr(), (_lib.PTR_DEVICE if a.is_cuda else _lib.PTR_HOST)
+    raise TypeError(f"{name}: unsupported array type {type(a)}")
+
+
+def _host_vec(a, n: int, name: str) -> np.ndarray:
+    """A float64 host copy-or-view of exactly n entries (input vectors)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.size != n:
+        raise _bad(f"{name}: has {a.size} entries, expected {n}")
+    return a
+
+
 @dataclass
 class MatrixInfo:
     n: int
@@ -62,6 +99,7 @@ class H2Matrix:
     @classmethod
     def from_host(cls, hm: HostMatrix, device: int = 0) -> "H2Matrix":
         lib = _lib.load()
+        hm.validate()
         keep = [np.ascontiguousarray(a) for a in (hm.perm, hm.ranks.astype(np.int32), hm.leaf,
                                                     hm.transfer, hm.cpl_row_ptr, hm.cpl_col_idx,
                                                     hm.cpl_values, hm.dense_row_ptr,
@@ -148,7 +186,9 @@ class H2Matrix:
 
     @property
     def n(self) -> int:
-        return self.info().n
+        if getattr(self, "_n", None) is None:
+            self._n = self.info().n  # fixed for the handle's lifetime
+        return self._n
 
     def memory_footprint(self) -> int:
         """memory_footprint(A).total() (h2_matrix.hpp:90-102)."""
@@ -186,7 +226,30 @@ class H2Matrix:
         return list(buf)
 
 
-def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=None):
+class HmvContext:
+    """HmvContext<double> (hmv.hpp:159-172): a per-caller device workspace.
+    Concurrent hmv calls on one matrix are safe with one context each (calls
+    sharing a context are serialised in device order)."""
+
+    def __init__(self, A: H2Matrix):
+        out = C.c_void_p()
+        _lib.check(_lib.load().h2b_context_create(A._h, C.byref(out)))
+        self._c = out
+
+    def close(self):
+        if self._c and self._c.value:
+            _lib.check(_lib.load().h2b_context_destroy(self._c))
+            self._c = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=None,
+        ctx: HmvContext | None = None):
     """y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-194). Returns y."""
     if y is None:
         if isinstance(x, np.ndarray):
@@ -194,8 +257,9 @@ def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=No
         else:
             import torch
             y = torch.zeros_like(x)
-    px, kx = _ptr(x)
-    py, ky = _ptr(y)
+    n = A.n
+    px, kx = _vec(x, n, "hmv: x")
+    py, ky = _vec(y, n, "hmv: y", writable=True)
     kind = _lib.PTR_DEVICE if (kx == ky == _lib.PTR_DEVICE) else (
         _lib.PTR_HOST if (kx == ky == _lib.PTR_HOST) else _lib.PTR_AUTO)
     if stream is None and _lib.PTR_DEVICE in (kx, ky):
@@ -203,8 +267,11 @@ def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=No
         # matrix's own non-blocking stream, unordered with torch's work)
         from .dist import torch_stream_handle
         stream = torch_stream_handle()
-    _lib.check(_lib.load().h2b_hmv(A._h, px, py, float(alpha), float(beta), kind,
-                                   None if stream is None else C.c_void_p(stream)))
+    st = None if stream is None else C.c_void_p(stream)
+    if ctx is None:
+        _lib.check(_lib.load().h2b_hmv(A._h, px, py, float(alpha), float(beta), kind, st))
+    else:
+        _lib.check(_lib.load().h2b_hmv_ctx(A._h, ctx._c, px, py, float(alpha), float(beta), kind, st))
     return y
 
 
@@ -212,9 +279,14 @@ def hmv_multi(A: H2Matrix, X: np.ndarray, alpha: float = 1.0, beta: float = 0.0,
     """Column-wise hmv of X (n x nvec, column-major i.e. X[:, v] contiguous when
     passed as a (nvec, n) C array)."""
     X = np.ascontiguousarray(X, dtype=np.float64)
+    if X.ndim != 2 or X.shape[1] != A.n:
+        raise _bad(f"hmv_multi: bad leading dimension (X must be (nvec, {A.n}))")
     nvec, n = X.shape
     if Y is None:
         Y = np.zeros_like(X)
+    elif (not isinstance(Y, np.ndarray) or Y.dtype != np.float64 or Y.shape != X.shape
+          or not Y.flags.c_contiguous or not Y.flags.writeable):
+        raise _bad(f"hmv_multi: Y must be a writable C-contiguous float64 {X.shape} array")
     _lib.check(_lib.load().h2b_hmv_multi(A._h, nvec, X.ctypes.data, n, Y.ctypes.data, n,
                                          float(alpha), float(beta), _lib.PTR_HOST, None))
     return Y
@@ -222,7 +294,7 @@ def hmv_multi(A: H2Matrix, X: np.ndarray, alpha: float = 1.0, beta: float = 0.0,
 
 def upsweep(A: H2Matrix, xc: np.ndarray) -> np.ndarray:
     """upsweep(V, xc, n, xhat) (hmv.hpp:79-111); xc in cluster order."""
-    xc = np.ascontiguousarray(xc, dtype=np.float64)
+    xc = _host_vec(xc, A.n, "upsweep: xc")
     out = np.zeros(A.col_vec_size(), np.float64)
     _lib.check(_lib.load().h2b_upsweep(A._h, xc.ctypes.data, out.ctypes.data, _lib.PTR_HOST))
     return out
@@ -230,7 +302,7 @@ def upsweep(A: H2Matrix, xc: np.ndarray) -> np.ndarray:
 
 def tree_multiply(A: H2Matrix, xhat: np.ndarray) -> np.ndarray:
     """tree_multiply(S, xhat, yhat) (hmv.hpp:114-125)."""
-    xhat = np.ascontiguousarray(xhat, dtype=np.float64)
+    xhat = _host_vec(xhat, A.col_vec_size(), "tree_multiply: xhat")
     out = np.zeros(A.vec_size(), np.float64)
     _lib.check(_lib.load().h2b_tree_multiply(A._h, xhat.ctypes.data, out.ctypes.data,
                                              _lib.PTR_HOST))
@@ -238,16 +310,23 @@ def tree_multiply(A: H2Matrix, xhat: np.ndarray) -> np.ndarray:
 
 
 def downsweep(A: H2Matrix, yhat: np.ndarray, yc: np.ndarray) -> np.ndarray:
-    """downsweep(U, yhat, yc, n) (hmv.hpp:129-157): returns yc + U-expansion."""
-    yhat = np.ascontiguousarray(yhat, dtype=np.float64)
-    yc = np.array(yc, dtype=np.float64, copy=True)
-    _lib.check(_lib.load().h2b_downsweep(A._h, yhat.ctypes.data, yc.ctypes.data, _lib.PTR_HOST))
+    """downsweep(U, yhat, yc, n) (hmv.hpp:129-157): returns yc + the U-expansion.
+    Like the reference's LevelVectors, yhat is updated in place
+    (y^l += E y^{l-1}) when it is a writable float64 array of the right size."""
+    nv = A.vec_size()
+    inplace = (isinstance(yhat, np.ndarray) and yhat.dtype == np.float64 and yhat.flags.c_contiguous
+               and yhat.flags.writeable)
+    yh = yhat if inplace else np.array(_host_vec(yhat, nv, "downsweep: yhat"), copy=True)
+    if yh.size != nv:
+        raise _bad(f"downsweep: yhat has {yh.size} entries, expected {nv}")
+    yc = np.array(_host_vec(yc, A.n, "downsweep: yc"), copy=True)
+    _lib.check(_lib.load().h2b_downsweep(A._h, yh.ctypes.data, yc.ctypes.data, _lib.PTR_HOST))
     return yc
 
 
 def dense_mv(A: H2Matrix, xc: np.ndarray) -> np.ndarray:
     """block_sparse_mv(A.dense, xc, yc, 1, 0) (bsr.hpp:79-82)."""
-    xc = np.ascontiguousarray(xc, dtype=np.float64)
+    xc = _host_vec(xc, A.n, "dense_mv: xc")
     out = np.zeros_like(xc)
     _lib.check(_lib.load().h2b_dense_mv(A._h, xc.ctypes.data, out.ctypes.data, 1.0, 0.0,
                                         _lib.PTR_HOST))
@@ -324,6 +403,8 @@ def validate_sampled(A: H2Matrix, fraction: float, seed: int = 1, points=None, d
     pp = None
     if points is not None:
         points = np.ascontiguousarray(points, dtype=np.float64)
+        if points.ndim != 2 or points.shape[0] != A.n or points.shape[1] not in (2, 3):
+            raise _bad(f"validate_sampled: points must be ({A.n}, 2|3)")
         dim = points.shape[1]
         pp = points.ctypes.data
     err = C.c_double()

@@ -144,10 +144,54 @@ uint64_t Matrix::footprint() const {
 }
 
 uint64_t Matrix::device_bytes() const {
-  return perm.bytes() + leaf.bytes() + transfer.bytes() + cpl_val.bytes() + dense_val.bytes() +
-         cpl_rp.bytes() + cpl_ci.bytes() + dense_rp.bytes() + dense_ci.bytes() + work.bytes() +
-         xc.bytes() + yc.bytes() + xhat.bytes() + yhat.bytes() + xs.bytes() + ys.bytes() +
-         (colb ? colb->device_bytes() : 0);
+  uint64_t b = perm.bytes() + leaf.bytes() + transfer.bytes() + cpl_val.bytes() + dense_val.bytes() +
+               cpl_rp.bytes() + cpl_ci.bytes() + dense_rp.bytes() + dense_ci.bytes() + work.bytes() +
+               (colb ? colb->device_bytes() : 0);
+  if (work0)
+    b += work0->xc.bytes() + work0->yc.bytes() + work0->xhat.bytes() + work0->yhat.bytes() + work0->xs.bytes() +
+         work0->ys.bytes() + work0->xc16.bytes() + work0->yc16.bytes() + work0->xh16.bytes() +
+         work0->yh16.bytes() + work0->flag.bytes();
+  return b;
+}
+
+// ---------------------------------------------------------------- workspaces
+void ensure_work(Matrix& A, Work& w) {
+  if (w.owner == &A && w.layout == A.layout_version) return;
+  const Matrix& C = A.col_basis();
+  const int q = A.q;
+  w.device = A.device;
+  w.xc.alloc(A.n);
+  w.yc.alloc(A.n);
+  w.xhat.alloc(std::max<int64_t>(1, C.vec_off[q + 1]));
+  w.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
+  w.xs.release();
+  w.ys.release();
+  w.xh16.release();
+  w.yh16.release();
+  if (!w.done) H2B_CUDA(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
+  w.owner = &A;
+  w.layout = A.layout_version;
+}
+
+Work& default_work(Matrix& A) {
+  if (!A.work0) A.work0.reset(new Work);
+  return *A.work0;
+}
+
+WorkUse::WorkUse(Work& work, cudaStream_t st) : w(work), s(st) {
+  w.mu.lock();
+  if (w.done) {
+    const cudaError_t e = cudaStreamWaitEvent(s, w.done, 0);
+    if (e != cudaSuccess) {
+      w.mu.unlock();
+      H2B_CUDA(e);
+    }
+  }
+}
+
+WorkUse::~WorkUse() {
+  if (w.done) cudaEventRecord(w.done, s);
+  w.mu.unlock();
 }
 
 double Matrix::hmv_flops() const {
@@ -209,12 +253,7 @@ void allocate(Matrix& A) {
 
   A.vec_off.assign(q + 2, 0);
   for (int l = 0; l <= q; ++l) A.vec_off[l + 1] = A.vec_off[l] + A.nodes(l) * A.rank[l];
-  A.xc.alloc(A.n);
-  A.yc.alloc(A.n);
-  A.xhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
-  A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
-  A.xs.alloc(A.n);
-  A.ys.alloc(A.n);
+  ++A.layout_version;
 }
 
 // Column basis of a non-symmetric matrix: leaf / transfer pools for the
@@ -243,8 +282,7 @@ void allocate_col(Matrix& A, const int32_t* cranks) {
   C.transfer.alloc(t);
   C.vec_off.assign(q + 2, 0);
   for (int l = 0; l <= q; ++l) C.vec_off[l + 1] = C.vec_off[l] + C.nodes(l) * C.rank[l];
-  C.xc.alloc(A.n);
-  C.xhat.alloc(std::max<int64_t>(1, C.vec_off[q + 1]));
+  ++A.layout_version;
 }
 
 // Upload the CSR structure of every layer and build the fused work list.
@@ -475,25 +513,29 @@ cudaEvent_t* timing_slots(Matrix& A) {
   return e;
 }
 
-void hmv_device(Matrix& A, const double* x, double* y, double alpha, double beta, cudaStream_t s) {
+// One mat-vec on device pointers with workspace w (held by the caller).
+void hmv_device(Matrix& A, Work& w, const double* x, double* y, double alpha, double beta, cudaStream_t s) {
   NvtxRange nv("h2b hmv");
   const int q = A.q;
   cudaEvent_t* ev = timing_slots(A);
   if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
   Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
-  sweep_begin(A);
-  launch_up_leaf(C, x, s);
-  if (q >= 1) launch_up_fused(A, C, s, q, 1, false);  // levels q..1 in one dataflow launch
+  sweep_begin(w, A, s);
+  launch_up_leaf(C, x, w.xc.p, w.xhat.p, s);
+  if (q >= 1) launch_up_fused(w, C, w.xhat.p, s, q, 1, false);  // levels q..1 in one dataflow launch
   if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
-  launch_bsr(A, A.work.p, A.nwork, C.xc.p, A.yc.p, C.xhat.p, A.yhat.p, s, &C);
+  launch_bsr(A, A.work.p, A.nwork, w.xc.p, w.yc.p, w.xhat.p, w.yhat.p, s, &C);
   if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
-  if (q >= 1) launch_down_fused(A, s, false);
-  launch_down_leaf(A, y, alpha, beta, true, s);
+  if (q >= 1) launch_down_fused(w, A, w.yhat.p, s, false);
+  launch_down_leaf(A, w.yhat.p, w.yc.p, y, alpha, beta, true, s);
   if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
 }
 
 void hmv_for_validation(Matrix& A, const double* x, double* y, cudaStream_t s) {
-  hmv_device(A, x, y, 1.0, 0.0, s);
+  Work& w = default_work(A);
+  WorkUse u(w, s);
+  ensure_work(A, w);
+  hmv_device(A, w, x, y, 1.0, 0.0, s);
 }
 
 double validate_sampled_device(Matrix& A, const double* points_host, int dim, double ell,
@@ -517,34 +559,46 @@ bool is_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
-void copy_in(Matrix& A, double* dst, const double* src, size_t n, cudaStream_t s) {
+void copy_in(double* dst, const double* src, size_t n, cudaStream_t s) {
   H2B_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, s));
 }
 
-void copy_out(Matrix& A, double* dst, const double* src, size_t n, cudaStream_t s) {
+void copy_out(double* dst, const double* src, size_t n, cudaStream_t s) {
   H2B_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, s));
 }
 
-void hmv(Matrix& A, const double* x, double* y, double alpha, double beta, h2b_ptr_kind kind,
+// hmv(A, x, y, alpha, beta, ctx) (hmv.hpp:175-188); w = nullptr: the handle's
+// own workspace.
+void hmv(Matrix& A, Work* wp, const double* x, double* y, double alpha, double beta, h2b_ptr_kind kind,
          cudaStream_t s) {
   require(x && y, "hmv: null vector");
   require(A.part_s == 0, "hmv: partition handles use h2b_part_upsweep / h2b_part_finish");
   DeviceGuard g(A.device);
   if (!s) s = A.stream;
+  Work& w = wp ? *wp : default_work(A);
+  require(w.device == A.device || w.owner == nullptr, "hmv: context belongs to another device");
   const bool dx = resolve_device(kind, x), dy = resolve_device(kind, y);
-  const double* xd = x;
-  double* yd = y;
-  if (!dx) {
-    copy_in(A, A.xs.p, x, A.n, s);
-    xd = A.xs.p;
+  bool sync = false;
+  {
+    WorkUse u(w, s);
+    ensure_work(A, w);
+    const double* xd = x;
+    double* yd = y;
+    if (!dx) {
+      if (!w.xs.p) w.xs.alloc(A.n);
+      copy_in(w.xs.p, x, A.n, s);
+      xd = w.xs.p;
+    }
+    if (!dy) {
+      if (!w.ys.p) w.ys.alloc(A.n);
+      if (beta != 0.0) copy_in(w.ys.p, y, A.n, s);
+      yd = w.ys.p;
+    }
+    hmv_device(A, w, xd, yd, alpha, beta, s);
+    if (!dy) copy_out(y, w.ys.p, A.n, s);
+    sync = !dx || !dy;
   }
-  if (!dy) {
-    if (beta != 0.0) copy_in(A, A.ys.p, y, A.n, s);
-    yd = A.ys.p;
-  }
-  hmv_device(A, xd, yd, alpha, beta, s);
-  if (!dy) copy_out(A, y, A.ys.p, A.n, s);
-  if (!dx || !dy) H2B_CUDA(cudaStreamSynchronize(s));
+  if (sync) H2B_CUDA(cudaStreamSynchronize(s));
 }
 
 void whole(const Matrix& A, const char* what) {
@@ -729,7 +783,42 @@ h2b_status h2b_hmv(h2b_matrix* Ah, const double* x, double* y, double alpha, dou
                    h2b_ptr_kind kind, void* stream) {
   return guarded([&] {
     require(Ah, "null matrix");
-    hmv(*Ah, x, y, alpha, beta, kind, static_cast<cudaStream_t>(stream));
+    hmv(*Ah, nullptr, x, y, alpha, beta, kind, static_cast<cudaStream_t>(stream));
+  });
+}
+
+h2b_status h2b_context_create(h2b_matrix* Ah, h2b_context** out) {
+  return guarded([&] {
+    require(Ah && out, "null argument");
+    Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    std::unique_ptr<h2b_context> c(new h2b_context);
+    c->device = A.device;
+    ensure_work(A, *c);
+    *out = c.release();
+  });
+}
+
+h2b_status h2b_context_destroy(h2b_context* c) {
+  return guarded([&] {
+    if (!c) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    {
+      std::lock_guard<std::mutex> lk(c->mu);
+      if (c->done) cudaEventSynchronize(c->done);  // no kernel may still use the buffers
+    }
+    delete c;
+    cudaSetDevice(prev);
+  });
+}
+
+h2b_status h2b_hmv_ctx(h2b_matrix* Ah, h2b_context* ctx, const double* x, double* y, double alpha, double beta,
+                       h2b_ptr_kind kind, void* stream) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    hmv(*Ah, ctx, x, y, alpha, beta, kind, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -764,8 +853,13 @@ h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx,
       yd = ys.p;
       ly = A.n;
     }
-    for (int v0 = 0; v0 < nvec; v0 += 16)
-      hmv_multi_device(A, xd + v0 * lx, lx, yd + v0 * ly, ly, std::min(16, nvec - v0), alpha, beta, s);
+    {
+      Work& w = default_work(A);
+      WorkUse u(w, s);
+      ensure_work(A, w);
+      for (int v0 = 0; v0 < nvec; v0 += 16)
+        hmv_multi_device(A, w, xd + v0 * lx, lx, yd + v0 * ly, ly, std::min(16, nvec - v0), alpha, beta, s);
+    }
     if (!dy)
       H2B_CUDA(cudaMemcpy2DAsync(Y, ldy * sizeof(double), ys.p, A.n * sizeof(double), A.n * sizeof(double),
                                  nvec, cudaMemcpyDeviceToHost, s));
@@ -784,11 +878,16 @@ h2b_status h2b_upsweep(h2b_matrix* Ah, const double* xc, double* xhat, h2b_ptr_k
     Staged si, so;
     const double* xin = stage_in(si, xc, A.n, dev, s);
     Matrix& C = A.col_basis();  // upsweep(A.col_basis(), ...) (hmv.hpp:182)
-    launch_up_leaf(C, xin, s, /*cluster_order=*/true);
-    for (int l = A.q; l >= 1; --l) launch_up_level(C, l, s);
     double* out = stage_out(so, xhat, C.vec_off[A.q + 1], resolve_device(kind, xhat), false, s);
-    if (C.vec_off[A.q + 1])
-      H2B_CUDA(cudaMemcpyAsync(out, C.xhat.p, C.vec_off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    {
+      Work& w = default_work(A);
+      WorkUse u(w, s);
+      ensure_work(A, w);
+      launch_up_leaf(C, xin, w.xc.p, w.xhat.p, s, /*cluster_order=*/true);
+      for (int l = A.q; l >= 1; --l) launch_up_level(C, l, w.xhat.p, s);
+      if (C.vec_off[A.q + 1])
+        H2B_CUDA(cudaMemcpyAsync(out, w.xhat.p, C.vec_off[A.q + 1] * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
     finish_out(so, s);
   });
 }
@@ -818,7 +917,9 @@ h2b_status h2b_tree_multiply(h2b_matrix* Ah, const double* xhat, double* yhat, h
   });
 }
 
-h2b_status h2b_downsweep(h2b_matrix* Ah, const double* yhat, double* yc, h2b_ptr_kind kind) {
+// downsweep(U, yhat, y, n) (hmv.hpp:129-157): yhat is updated in place
+// (y^l += E y^{l-1}), y += U y^q.
+h2b_status h2b_downsweep(h2b_matrix* Ah, double* yhat, double* yc, h2b_ptr_kind kind) {
   return guarded([&] {
     require(Ah && yhat && yc, "null argument");
     Matrix& A = *Ah;
@@ -826,13 +927,18 @@ h2b_status h2b_downsweep(h2b_matrix* Ah, const double* yhat, double* yc, h2b_ptr
     DeviceGuard g(A.device);
     cudaStream_t s = A.stream;
     const size_t nv = A.vec_off[A.q + 1];
-    Staged si, so;
-    const double* yin = stage_in(si, yhat, nv, resolve_device(kind, yhat), s);
-    if (nv) H2B_CUDA(cudaMemcpyAsync(A.yhat.p, yin, nv * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    Staged sh, so;
+    double* yh = stage_out(sh, yhat, nv, resolve_device(kind, yhat), true, s);
     double* out = stage_out(so, yc, A.n, resolve_device(kind, yc), true, s);
-    H2B_CUDA(cudaMemcpyAsync(A.yc.p, out, A.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    for (int l = 1; l <= A.q; ++l) launch_down_level(A, l, s);
-    launch_down_leaf(A, out, 1.0, 0.0, false, s);
+    {
+      Work& w = default_work(A);
+      WorkUse u(w, s);
+      ensure_work(A, w);
+      H2B_CUDA(cudaMemcpyAsync(w.yc.p, out, A.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      for (int l = 1; l <= A.q; ++l) launch_down_level(A, l, yh, s);
+      launch_down_leaf(A, yh, w.yc.p, out, 1.0, 0.0, false, s);
+    }
+    finish_out(sh, s);
     finish_out(so, s);
   });
 }
@@ -856,7 +962,7 @@ h2b_status h2b_dense_mv(h2b_matrix* Ah, const double* xc, double* yc, double alp
     dw.alloc(w.size());
     if (!w.empty())
       H2B_CUDA(cudaMemcpyAsync(dw.p, w.data(), w.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    launch_bsr(A, dw.p, int64_t(w.size()), xin, out, A.xhat.p, A.yhat.p, s);
+    launch_bsr(A, dw.p, int64_t(w.size()), xin, out, nullptr, nullptr, s);
     finish_out(so, s);
   });
 }
@@ -926,10 +1032,16 @@ h2b_status h2b_workspace(h2b_matrix* Ah, int which, void** ptr, int64_t* count) 
   return guarded([&] {
     require(Ah && ptr && count, "null argument");
     Matrix& A = *Ah;
+    DeviceGuard g(A.device);
+    Work& w = default_work(A);
+    {
+      WorkUse u(w, A.stream);
+      ensure_work(A, w);
+    }
     switch (which) {
-      case H2B_WS_XHAT: *ptr = A.col_basis().xhat.p; *count = A.col_basis().vec_off[A.q + 1]; break;
-      case H2B_WS_YHAT: *ptr = A.yhat.p; *count = A.vec_off[A.q + 1]; break;
-      case H2B_WS_XC: *ptr = A.xc.p; *count = A.n; break;
+      case H2B_WS_XHAT: *ptr = w.xhat.p; *count = A.col_basis().vec_off[A.q + 1]; break;
+      case H2B_WS_YHAT: *ptr = w.yhat.p; *count = A.vec_off[A.q + 1]; break;
+      case H2B_WS_XC: *ptr = w.xc.p; *count = A.n; break;
       case H2B_WS_PERM: *ptr = A.perm.p; *count = A.n; break;
       default: require(false, "h2b_workspace: unknown buffer");
     }
@@ -942,11 +1054,14 @@ h2b_status h2b_part_upsweep(h2b_matrix* Ah, const double* x, void* stream) {
     Matrix& A = *Ah;
     DeviceGuard g(A.device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
-    sweep_begin(A);
-    launch_up_leaf(A, x, s);
-    launch_gather(A.perm.p, x, A.xc.p, A.n, s);  // dense blocks read remote columns
+    Work& w = default_work(A);
+    WorkUse u(w, s);
+    ensure_work(A, w);
+    sweep_begin(w, A, s);
+    launch_up_leaf(A, x, w.xc.p, w.xhat.p, s);
+    launch_gather(A.perm.p, x, w.xc.p, A.n, s);  // dense blocks read remote columns
     // this partition's levels q..s+1: one dataflow launch over its nodes
-    if (A.q > A.part_s) launch_up_fused(A, A, s, A.q, A.part_s + 1, true);
+    if (A.q > A.part_s) launch_up_fused(w, A, w.xhat.p, s, A.q, A.part_s + 1, true);
   });
 }
 
@@ -956,15 +1071,18 @@ h2b_status h2b_part_finish(h2b_matrix* Ah, double* y_slice, void* stream) {
     Matrix& A = *Ah;
     DeviceGuard g(A.device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    Work& w = default_work(A);
+    WorkUse u(w, s);
+    ensure_work(A, w);
     cudaEvent_t* ev = timing_slots(A);
     if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
     // replicated top (level s's x^ gathered from every partition)
-    if (A.part_s >= 1) launch_up_fused(A, A, s, A.part_s, 1, false);
+    if (A.part_s >= 1) launch_up_fused(w, A, w.xhat.p, s, A.part_s, 1, false);
     if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
-    launch_bsr(A, A.work.p, A.nwork, A.xc.p, A.yc.p, A.xhat.p, A.yhat.p, s);
+    launch_bsr(A, A.work.p, A.nwork, w.xc.p, w.yc.p, w.xhat.p, w.yhat.p, s);
     if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
-    if (A.q >= 1) launch_down_fused(A, s, true);  // replicated top + own subtree
-    launch_down_leaf(A, y_slice, 1.0, 0.0, false, s);
+    if (A.q >= 1) launch_down_fused(w, A, w.yhat.p, s, true);  // replicated top + own subtree
+    launch_down_leaf(A, w.yhat.p, w.yc.p, y_slice, 1.0, 0.0, false, s);
     if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
   });
 }

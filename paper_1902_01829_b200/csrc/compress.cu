@@ -120,7 +120,8 @@ struct ProjLevel {
   const double* T;    // row projections: rn x ro per node, ld rn
   const double* Tc;   // column projections: cn x co per node, ld cn (== T when symmetric)
   int ro, rn, co, cn, ld_old, ld_new;
-  int64_t ostride;    // old block stride (blocks are read from and written to the old slots)
+  int64_t istride;    // block stride of S
+  int64_t ostride;    // block stride of out (compress(): the old slots, == istride)
 };
 struct ProjTable {
   ProjLevel L[kMaxLevels + 1];
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   }
   double ss = 0.0;
   if (nk > 0) {
-    stage64(Sb, L.S + int64_t(blist[0]) * L.ostride, L.ld_old, ro, co);
+    stage64(Sb, L.S + int64_t(blist[0]) * L.istride, L.ld_old, ro, co);
     cp_async_commit();  // {T_row, S_0}
     stage64(Tc, L.Tc + int64_t(clist[0]) * cn * co, cn, cn, co);
     cp_async_commit();  // {T_col,0}
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
       out_rows<true>(Sb, Tc, out, outT, L.ld_new, co, rn, cn, s1);
       __syncthreads();  // TS, T_col,k consumed
       if (k + 1 < nk) {
-        stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ostride, L.ld_old, ro, co);
+        stage64(Sb, L.S + int64_t(blist[k + 1]) * L.istride, L.ld_old, ro, co);
         cp_async_commit();
         stage64(Tc, L.Tc + int64_t(clist[k + 1]) * cn * co, cn, cn, co);
         cp_async_commit();
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
       // under TS_{k+1}
       const bool live = ts_strip<false>(Tr, Sb, ro, co, rn, acc);
       __syncthreads();  // S_k consumed
-      if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.ostride, L.ld_old, ro, co);
+      if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.istride, L.ld_old, ro, co);
       cp_async_commit();
       cp_async_wait<1>();  // T_col,k
       __syncthreads();
@@ -1271,7 +1272,9 @@ const int32_t* mirror_of(const Matrix& A, int l) {
                                                                            : nullptr;
 }
 
-void project_rows(const Matrix& A, Arena& ar, ProjRows& R, cudaStream_t s) {
+// sym_T: the row and column projection trees are the same tree, so a
+// symmetric level's lower blocks are the upper ones' transposes.
+void project_rows(const Matrix& A, Arena& ar, ProjRows& R, cudaStream_t s, bool sym_T = true) {
   require(A.mirror_ready, "project_coupling: mirror map missing");
   const int q = A.q;
   R.off.assign(q + 2, 0);
@@ -1281,7 +1284,7 @@ void project_rows(const Matrix& A, Arena& ar, ProjRows& R, cudaStream_t s) {
     const Layer& L = A.cpl[l];
     R.off[l] = int64_t(R.h.size());
     R.max_row = std::max(R.max_row, L.max_row);
-    const bool mir = mirror_of(A, l) != nullptr;
+    const bool mir = sym_T && mirror_of(A, l) != nullptr;
     for (int64_t r = 0; r < L.rows && L.nb > 0; ++r) {
       bool any = false;
       for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1] && !any; ++b) any = !mir || L.h_ci[b] > r;
@@ -1300,8 +1303,10 @@ void project_rows(const Matrix& A, Arena& ar, ProjRows& R, cudaStream_t s) {
 // Level l with T(l) (T.rows[l] x T.cols[l] per node) on stream st.
 // Level l with T(l) (row projections, T.rows[l] x T.cols[l] per node) and
 // Tc(l) (column projections; the same tree when symmetric) on stream st.
+// out / ostride: where the projected blocks go (default: the old slots).
 void project_level(const Matrix& A, const TreePool& T, const TreePool& Tc, const ProjRows& R, int l, bool tri,
-                   bool want_sum, Flops& fl, double& flops, const Part& pt, cudaStream_t st) {
+                   bool want_sum, Flops& fl, double& flops, const Part& pt, cudaStream_t st, bool sym_T = true,
+                   double* out = nullptr, int64_t ostride = 0) {
   const Layer& L = A.cpl[l];
   const int rn = T.rows[l], ro = T.cols[l], cn = Tc.rows[l], co = Tc.cols[l];
   if (L.nb == 0) return;
@@ -1317,7 +1322,7 @@ void project_level(const Matrix& A, const TreePool& T, const TreePool& Tc, const
   d.S = L.val;
   d.rp = L.rp;
   d.ci = L.ci;
-  d.mirror = mirror_of(A, l);
+  d.mirror = sym_T ? mirror_of(A, l) : nullptr;
   d.T = const_cast<TreePool&>(T).at(l);
   d.Tc = const_cast<TreePool&>(Tc).at(l);
   d.ro = ro;
@@ -1326,8 +1331,9 @@ void project_level(const Matrix& A, const TreePool& T, const TreePool& Tc, const
   d.cn = cn;
   d.ld_old = L.ld;
   d.ld_new = pad2(rn);
-  d.out = L.val;  // in the old slots
-  d.ostride = L.block_stride();
+  d.istride = L.block_stride();
+  d.out = out ? out : L.val;  // default: in the old slots
+  d.ostride = out ? ostride : L.block_stride();
   const size_t smax = size_t(3) * 64 * kPLd * sizeof(double) + (32 + 3 * size_t(P.max_row)) * sizeof(int);
   check_smem(smax, "project_coupling");
   set_smem(k_project, smax);
@@ -1642,7 +1648,8 @@ TruncSizes truncate_sizes(const Matrix& A) {
 // on_t(l) (optional): called once Tt(l) (new x old per node) is final in
 // stream order on s; Tt.rows[l] holds the new rank by then.
 double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s, Flops& fl,
-                double& flops, const Part& pt, double* tree_mem, Arena& ar, const LevelHook& on_t = nullptr) {
+                double& flops, const Part& pt, double* tree_mem, Arena& ar, const LevelHook& on_t = nullptr,
+                std::vector<double>* level_energy = nullptr) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   Trace tr;
   const int q = A.q, m = A.m;
@@ -1781,6 +1788,7 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   if (nleaf) H2B_CUDA(cudaMemcpyAsync(A.leaf.p, newleaf, nleaf * sizeof(double), cudaMemcpyDeviceToDevice, s));
   H2B_CUDA(cudaStreamSynchronize(s));
   A.tr_off = toff;
+  if (level_energy) *level_energy = lev_e;
   double energy = 0.0;
   for (double e : lev_e) energy += e;
   return energy;
@@ -1849,16 +1857,13 @@ void relayout(Matrix& A) {
   const int q = A.q;
   A.vec_off.assign(q + 2, 0);
   for (int l = 0; l <= q; ++l) A.vec_off[l + 1] = A.vec_off[l] + A.nodes(l) * A.rank[l];
-  A.xhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
-  A.yhat.alloc(std::max<int64_t>(1, A.vec_off[q + 1]));
-  if (!A.symmetric) {  // x^ lives with the column basis
+  if (!A.symmetric) {  // x^ follows the column basis
     Matrix& C = *A.colb;
     C.vec_off.assign(q + 2, 0);
     for (int l = 0; l <= q; ++l) C.vec_off[l + 1] = C.vec_off[l] + C.nodes(l) * C.rank[l];
-    C.xhat.alloc(std::max<int64_t>(1, C.vec_off[q + 1]));
   }
-  A.xh16.release();
-  A.yh16.release();
+  // every workspace (the handle's and any h2b_context) re-sizes on next use
+  ++A.layout_version;
   upload_structure(A);
 }
 

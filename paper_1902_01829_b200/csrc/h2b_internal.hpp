@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -118,6 +119,35 @@ struct Layer {
 // Work item of the fused BSR kernel: (layer << 26) | block_row.
 constexpr int kLayerShift = 26;
 
+// Per-caller mat-vec workspace: the HmvContext analogue (hmv.hpp:159-172,
+// "a context is not thread-safe, concurrent hmv calls need one context
+// each").  Every user of a Work holds its mutex while enqueueing and orders
+// its stream after the previous user's work on the device (event `done`), so
+// two streams sharing one Work serialise on the device instead of racing;
+// two Works on one matrix run concurrently.
+struct Work {
+  int device = 0;
+  const void* owner = nullptr;      // matrix the buffers were sized for
+  uint64_t layout = 0;              // ... and its layout_version
+  DevBuf<double> xc, yc;            // x, y in cluster order (n)
+  DevBuf<double> xhat, yhat;        // x^ (column-basis ranks), y^ (row-basis ranks), level-concatenated
+  DevBuf<double> xs, ys;            // device staging of host x / y
+  DevBuf<double> xc16, yc16, xh16, yh16;  // 16-vector panels (k_hmv_mv.cu), lazily allocated
+  // Fused dataflow sweeps (launch_up_fused / launch_down_fused): per-node
+  // completion flags (epoch-valued, never reset) and the work tickets.
+  DevBuf<uint32_t> flag;
+  DevBuf<unsigned long long> ticket;  // [0] up, [1] down
+  uint32_t epoch = 0;
+  std::mutex mu;
+  cudaEvent_t done = nullptr;
+  Work() = default;
+  Work(const Work&) = delete;
+  Work& operator=(const Work&) = delete;
+  ~Work() {
+    if (done) cudaEventDestroy(done);
+  }
+};
+
 struct Matrix {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -137,15 +167,12 @@ struct Matrix {
   std::vector<int64_t> vec_off;     // node-vector level offsets, size q + 2
   DevBuf<uint32_t> work;            // BSR work list (dense + coupling rows)
   int64_t nwork = 0;
-  // Fused dataflow sweeps (launch_up_fused / launch_down_fused): per-node
-  // completion flags (epoch-valued, never reset) and the work tickets.
-  DevBuf<uint32_t> sweep_flag;
-  DevBuf<unsigned long long> sweep_ticket;  // [0] up, [1] down
-  uint32_t sweep_epoch = 0;
 
-  // HmvContext analogue (hmv.hpp:161-172): one workspace per handle.
-  DevBuf<double> xc, yc, xhat, yhat, xs, ys;
-  DevBuf<double> xc16, yc16, xh16, yh16;  // 16-vector panels (k_hmv_mv.cu), lazily allocated
+  // The handle's own mat-vec workspace (the default HmvContext; h2b_context
+  // handles are further ones).  layout_version changes whenever the ranks
+  // (hence the x^ / y^ sizes) change, e.g. after compress().
+  std::unique_ptr<Work> work0;
+  uint64_t layout_version = 1;
   // Points (original order) + kernel of a device-built matrix, for
   // h2b_validate_sampled (validate.cu).
   DevBuf<double> pts_orig;
@@ -200,32 +227,54 @@ struct Matrix {
 };
 
 // ---- launchers (k_hmv.cu) ----
-void launch_up_leaf(const Matrix& A, const double* x, cudaStream_t s, bool cluster_order = false);
+// Node vectors (xhat / yhat) are whole level-concatenated buffers laid out by
+// the basis' vec_off.  x in original order (perm gather fused) unless
+// cluster_order; xc receives x in cluster order.
+void launch_up_leaf(const Matrix& B, const double* x, double* xc, double* xhat, cudaStream_t s,
+                    bool cluster_order = false);
 // parents at level l-1 in [p0, p1) (children in the transfer pool)
-void launch_up_level(const Matrix& A, int l, cudaStream_t s, int64_t p0 = 0, int64_t p1 = -1);
+void launch_up_level(const Matrix& B, int l, double* xhat, cudaStream_t s, int64_t p0 = 0, int64_t p1 = -1);
 // x^ level offsets from xb (the column basis' vec_off), y^ from A.
 void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
                 double* ydense, const double* xh, double* yh, cudaStream_t s, const Matrix* xb = nullptr);
 // children at level l in [c0, c1)
-void launch_down_level(const Matrix& A, int l, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1);
-// to_user: y[perm[t]] = alpha v + beta y[perm[t]] (original order); else y[t] = v
-// with t relative to the first owned leaf (cluster-order slice).
-void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
-                      cudaStream_t s);
-// Whole-matrix upsweep above the leaves (levels q..1 of basis B, x^ of B) and
+void launch_down_level(const Matrix& A, int l, double* yhat, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1);
+// yc += U y^q; to_user: y[perm[t]] = alpha v + beta y[perm[t]] (original
+// order); else y[t] = v with t relative to the first owned leaf (cluster-order slice).
+void launch_down_leaf(const Matrix& A, const double* yhat, const double* yc, double* y, double alpha,
+                      double beta, bool to_user, cudaStream_t s);
+// Whole-matrix upsweep above the leaves (levels l_hi..l_lo of basis B) and
 // downsweep (levels 1..q of A) as ONE persistent launch each: warps claim
 // nodes deepest-first (up) / top-down (down) and wait for their children /
-// parent through per-node flags (A holds the flags and tickets).
-// sweep_begin: a new epoch for the flags (once per mat-vec).  Up: child
-// levels l_hi..l_lo (l_hi's x^ is input); down: levels 1..q (the root's y^ is
-// input); own: this handle's node ranges (partition), else all nodes.
-void sweep_begin(Matrix& A);
-void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s, int l_hi, int l_lo, bool own);
-void launch_down_fused(Matrix& A, cudaStream_t s, bool own);
+// parent through per-node flags (held by the Work w).
+// sweep_begin: a new epoch for the flags (once per mat-vec, stream-ordered
+// on s).  Up: child levels l_hi..l_lo (l_hi's x^ is input); down: levels
+// 1..q (the root's y^ is input); own: this handle's node ranges (partition).
+void sweep_begin(Work& w, const Matrix& A, cudaStream_t s);
+void launch_up_fused(Work& w, const Matrix& B, double* xhat, cudaStream_t s, int l_hi, int l_lo, bool own);
+void launch_down_fused(Work& w, const Matrix& A, double* yhat, cudaStream_t s, bool own);
 void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s);
+// y[perm[t]] = alpha ys[t] + beta y[perm[t]] (t < n): the owner-row scatter of
+// a cluster-order y (partitioned mat-vec).
+void launch_scatter(const int32_t* perm, const double* ys, double* y, int64_t n, double alpha, double beta,
+                    cudaStream_t s);
+
+// ---- workspaces (capi.cu) ----
+// (Re)size w for A's current layout; the default workspace of A.
+void ensure_work(Matrix& A, Work& w);
+Work& default_work(Matrix& A);
+// Holds w for one call on stream s (mutex + device-order after the previous user).
+struct WorkUse {
+  Work& w;
+  cudaStream_t s;
+  WorkUse(Work& work, cudaStream_t st);
+  ~WorkUse();
+  WorkUse(const WorkUse&) = delete;
+  WorkUse& operator=(const WorkUse&) = delete;
+};
 
 // 16-vector FP64-MMA mat-vec, device pointers (k_hmv_mv.cu).
-void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
+void hmv_multi_device(Matrix& A, Work& w, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
                       double alpha, double beta, cudaStream_t s);
 
 // Build the fused BSR work list for the given layers (rows sorted by
@@ -239,5 +288,6 @@ void launch_repack(const double* src, int64_t ss, int ld_src, double* dst, int64
 
 }  // namespace h2b
 
-// The opaque handle of include/h2b.h is the device matrix itself.
+// The opaque handles of include/h2b.h: the device matrix itself, and a Work.
 struct h2b_matrix : h2b::Matrix {};
+struct h2b_context : h2b::Work {};

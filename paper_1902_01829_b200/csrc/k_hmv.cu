@@ -426,6 +426,15 @@ __global__ void k_gather(const int32_t* __restrict__ perm, const double* __restr
     xc[t] = x[perm[t]];
 }
 
+__global__ void k_scatter(const int32_t* __restrict__ perm, const double* __restrict__ ys,
+                          double* __restrict__ y, int64_t n, double alpha, double beta) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    double* o = y + perm[t];
+    *o = alpha * ys[t] + (beta == 0.0 ? 0.0 : beta * *o);
+  }
+}
+
 __global__ void k_repack(const double* __restrict__ src, int64_t ss, int ld_src,
                          double* __restrict__ dst, int64_t sd, int ld_dst, int rows, int cols,
                          int64_t count) {
@@ -467,26 +476,26 @@ unsigned flat_grid(int64_t n) {
 
 }  // namespace
 
-void launch_up_leaf(const Matrix& A, const double* x, cudaStream_t s, bool cluster_order) {
-  const int64_t nl = A.own_count(A.q);
-  k_up_leaf<<<warp_grid(nl), kThreads, 0, s>>>(x, cluster_order ? nullptr : A.perm.p, A.leaf.p, A.m, A.ldm,
-                                               A.rank[A.q], nl, A.own_begin(A.q), A.xc.p,
-                                               A.xhat.p + A.vec_off[A.q]);
+void launch_up_leaf(const Matrix& B, const double* x, double* xc, double* xhat, cudaStream_t s,
+                    bool cluster_order) {
+  const int64_t nl = B.own_count(B.q);
+  k_up_leaf<<<warp_grid(nl), kThreads, 0, s>>>(x, cluster_order ? nullptr : B.perm.p, B.leaf.p, B.m, B.ldm,
+                                               B.rank[B.q], nl, B.own_begin(B.q), xc, xhat + B.vec_off[B.q]);
   H2B_CUDA(cudaGetLastError());
 }
 
-void launch_up_level(const Matrix& A, int l, cudaStream_t s, int64_t p0, int64_t p1) {
-  const int kc = A.rank[l], kp = A.rank[l - 1];
-  if (p1 < 0) p1 = A.nodes(l - 1);
-  double* xp = A.xhat.p + A.vec_off[l - 1];
+void launch_up_level(const Matrix& B, int l, double* xhat, cudaStream_t s, int64_t p0, int64_t p1) {
+  const int kc = B.rank[l], kp = B.rank[l - 1];
+  if (p1 < 0) p1 = B.nodes(l - 1);
+  double* xp = xhat + B.vec_off[l - 1];
   const int64_t np = p1 - p0;
   if (kp == 0 || np <= 0) return;
   if (kc == 0) {
     H2B_CUDA(cudaMemsetAsync(xp + p0 * kp, 0, size_t(np) * kp * sizeof(double), s));
     return;
   }
-  k_up_level<<<warp_grid(np), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, p0, p1,
-                                                A.tr_begin(l), A.xhat.p + A.vec_off[l], xp);
+  k_up_level<<<warp_grid(np), kThreads, 0, s>>>(B.transfer.p + B.tr_off[l], B.ld(l), kc, kp, p0, p1,
+                                                B.tr_begin(l), xhat + B.vec_off[l], xp);
   H2B_CUDA(cudaGetLastError());
 }
 
@@ -496,26 +505,22 @@ unsigned persistent_grid(const void* kernel) {
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
   return unsigned(std::max(1, per_sm) * sm_count());
 }
-
-void sweep_state(Matrix& A) {
-  const int64_t nodes = int64_t(2) << A.q;
-  if (A.sweep_flag.n < size_t(nodes)) {
-    A.sweep_flag.alloc(nodes);
-    H2B_CUDA(cudaMemset(A.sweep_flag.p, 0, nodes * sizeof(uint32_t)));
-    A.sweep_ticket.alloc(2);
-    H2B_CUDA(cudaMemset(A.sweep_ticket.p, 0, 2 * sizeof(unsigned long long)));
-    A.sweep_epoch = 0;
-  }
-}
 }  // namespace
 
-void sweep_begin(Matrix& A) {
-  sweep_state(A);
-  ++A.sweep_epoch;  // this hmv's epoch: up flags 2e, down flags 2e + 1
+void sweep_begin(Work& w, const Matrix& A, cudaStream_t s) {
+  const int64_t nodes = int64_t(2) << A.q;
+  if (w.flag.n < size_t(nodes) || !w.ticket.p) {
+    // stream-ordered zeroing: the kernels of this mat-vec run after it
+    w.flag.alloc(nodes);
+    H2B_CUDA(cudaMemsetAsync(w.flag.p, 0, nodes * sizeof(uint32_t), s));
+    w.ticket.alloc(2);
+    H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, 2 * sizeof(unsigned long long), s));
+    w.epoch = 0;
+  }
+  ++w.epoch;  // this hmv's epoch: up flags 2e, down flags 2e + 1
 }
 
-void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s, int l_hi, int l_lo, bool own) {
-  sweep_state(A);
+void launch_up_fused(Work& w, const Matrix& B, double* xhat, cudaStream_t s, int l_hi, int l_lo, bool own) {
   SweepTable T{};
   T.q = l_hi;
   int64_t tot = 0;
@@ -528,8 +533,8 @@ void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s, int l_hi, int l
     L.kc = B.rank[l];
     L.kp = B.rank[l - 1];
     L.l = l;
-    L.in = B.xhat.p + B.vec_off[l];
-    L.out = B.xhat.p + B.vec_off[l - 1];
+    L.in = xhat + B.vec_off[l];
+    L.out = xhat + B.vec_off[l - 1];
     L.i0 = own ? B.own_begin(l - 1) : 0;
     L.n = own ? B.own_count(l - 1) : B.nodes(l - 1);
     T.start[T.nl] = tot;
@@ -538,14 +543,14 @@ void launch_up_fused(Matrix& A, const Matrix& B, cudaStream_t s, int l_hi, int l
   }
   T.start[T.nl] = tot;
   if (tot == 0) return;
-  H2B_CUDA(cudaMemsetAsync(A.sweep_ticket.p, 0, sizeof(unsigned long long), s));
-  k_up_fused<<<persistent_grid((const void*)k_up_fused), kThreads, 0, s>>>(T, A.sweep_flag.p, 2 * A.sweep_epoch,
-                                                                          A.sweep_ticket.p, 0ull);
+  require(w.flag.n >= (size_t(2) << B.q), "launch_up_fused: sweep_begin missing");
+  H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
+  k_up_fused<<<persistent_grid((const void*)k_up_fused), kThreads, 0, s>>>(T, w.flag.p, 2 * w.epoch, w.ticket.p,
+                                                                          0ull);
   H2B_CUDA(cudaGetLastError());
 }
 
-void launch_down_fused(Matrix& A, cudaStream_t s, bool own) {
-  sweep_state(A);
+void launch_down_fused(Work& w, const Matrix& A, double* yhat, cudaStream_t s, bool own) {
   const int q = A.q;
   SweepTable T{};
   T.q = 0;  // the root's y^ is final (after the coupling multiply)
@@ -559,8 +564,8 @@ void launch_down_fused(Matrix& A, cudaStream_t s, bool own) {
     L.kc = A.rank[l];
     L.kp = A.rank[l - 1];
     L.l = l;
-    L.in = A.yhat.p + A.vec_off[l - 1];
-    L.out = A.yhat.p + A.vec_off[l];
+    L.in = yhat + A.vec_off[l - 1];
+    L.out = yhat + A.vec_off[l];
     L.i0 = own ? A.own_begin(l) : 0;
     L.n = own ? A.own_count(l) : A.nodes(l);
     T.start[T.nl] = tot;
@@ -569,30 +574,29 @@ void launch_down_fused(Matrix& A, cudaStream_t s, bool own) {
   }
   T.start[T.nl] = tot;
   if (tot == 0) return;
-  H2B_CUDA(cudaMemsetAsync(A.sweep_ticket.p + 1, 0, sizeof(unsigned long long), s));
-  k_down_fused<<<persistent_grid((const void*)k_down_fused), kThreads, 0, s>>>(T, A.sweep_flag.p,
-                                                                              2 * A.sweep_epoch + 1,
-                                                                              A.sweep_ticket.p + 1, 0ull);
+  require(w.flag.n >= (size_t(2) << A.q), "launch_down_fused: sweep_begin missing");
+  H2B_CUDA(cudaMemsetAsync(w.ticket.p + 1, 0, sizeof(unsigned long long), s));
+  k_down_fused<<<persistent_grid((const void*)k_down_fused), kThreads, 0, s>>>(T, w.flag.p, 2 * w.epoch + 1,
+                                                                              w.ticket.p + 1, 0ull);
   H2B_CUDA(cudaGetLastError());
 }
 
-void launch_down_level(const Matrix& A, int l, cudaStream_t s, int64_t c0, int64_t c1) {
+void launch_down_level(const Matrix& A, int l, double* yhat, cudaStream_t s, int64_t c0, int64_t c1) {
   const int kc = A.rank[l], kp = A.rank[l - 1];
   if (c1 < 0) c1 = A.nodes(l);
   const int64_t nc = c1 - c0;
   if (kc == 0 || kp == 0 || nc <= 0) return;
-  k_down_level<<<warp_grid(nc), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp,
-                                                  c0, c1, A.tr_begin(l), A.yhat.p + A.vec_off[l - 1],
-                                                  A.yhat.p + A.vec_off[l]);
+  k_down_level<<<warp_grid(nc), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, c0, c1,
+                                                  A.tr_begin(l), yhat + A.vec_off[l - 1], yhat + A.vec_off[l]);
   H2B_CUDA(cudaGetLastError());
 }
 
-void launch_down_leaf(const Matrix& A, double* y, double alpha, double beta, bool to_user,
-                      cudaStream_t s) {
+void launch_down_leaf(const Matrix& A, const double* yhat, const double* yc, double* y, double alpha,
+                      double beta, bool to_user, cudaStream_t s) {
   const int64_t nl = A.own_count(A.q);
-  k_down_leaf<<<warp_grid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[A.q], nl,
-                                                 A.own_begin(A.q), A.yhat.p + A.vec_off[A.q], A.yc.p, A.perm.p, y,
-                                                 alpha, beta, to_user ? 1 : 0);
+  k_down_leaf<<<warp_grid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[A.q], nl, A.own_begin(A.q),
+                                                 yhat + A.vec_off[A.q], yc, A.perm.p, y, alpha, beta,
+                                                 to_user ? 1 : 0);
   H2B_CUDA(cudaGetLastError());
 }
 
@@ -630,6 +634,13 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
 
 void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, cudaStream_t s) {
   k_gather<<<flat_grid(n), kThreads, 0, s>>>(perm, x, xc, n);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_scatter(const int32_t* perm, const double* ys, double* y, int64_t n, double alpha, double beta,
+                    cudaStream_t s) {
+  if (n == 0) return;
+  k_scatter<<<flat_grid(n), kThreads, 0, s>>>(perm, ys, y, n, alpha, beta);
   H2B_CUDA(cudaGetLastError());
 }
 

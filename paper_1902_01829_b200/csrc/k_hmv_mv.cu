@@ -229,29 +229,29 @@ unsigned wgrid(int64_t items) {
 }  // namespace
 
 // Y (n x nv, ld ldy) <- alpha A X + beta Y for nv <= 16 vectors, device pointers.
-void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
+void hmv_multi_device(Matrix& A, Work& w, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
                       double alpha, double beta, cudaStream_t s) {
   require(nv >= 1 && nv <= NV, "hmv_multi: 1..16 vectors per pass");
   const int q = A.q;
   const Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
   const int64_t nvec_pool = std::max<int64_t>({1, A.vec_off[q + 1], C.vec_off[q + 1]}) * NV;
-  if (A.xc16.n < size_t(A.n) * NV) {
-    A.xc16.alloc(size_t(A.n) * NV);
-    A.yc16.alloc(size_t(A.n) * NV);
+  if (w.xc16.n < size_t(A.n) * NV) {
+    w.xc16.alloc(size_t(A.n) * NV);
+    w.yc16.alloc(size_t(A.n) * NV);
   }
-  if (A.xh16.n < size_t(nvec_pool)) {
-    A.xh16.alloc(nvec_pool);
-    A.yh16.alloc(nvec_pool);
+  if (w.xh16.n < size_t(nvec_pool)) {
+    w.xh16.alloc(nvec_pool);
+    w.yh16.alloc(nvec_pool);
   }
   const int64_t n = A.n;
   k_gather_mv<<<unsigned(std::min<int64_t>((n * NV + 255) / 256, int64_t(sms()) * 16)), 256, 0, s>>>(
-      A.perm.p, X, ldx, nv, n, A.xc16.p);
+      A.perm.p, X, ldx, nv, n, w.xc16.p);
   H2B_CUDA(cudaGetLastError());
   const int64_t nl = A.nodes(q);
-  double* xh = A.xh16.p;
-  double* yh = A.yh16.p;
+  double* xh = w.xh16.p;
+  double* yh = w.yh16.p;
   if (C.rank[q] > 0) {
-    k_up_leaf_mv<<<wgrid(nl), kThreads, 0, s>>>(C.leaf.p, C.ldm, C.m, C.rank[q], nl, A.xc16.p,
+    k_up_leaf_mv<<<wgrid(nl), kThreads, 0, s>>>(C.leaf.p, C.ldm, C.m, C.rank[q], nl, w.xc16.p,
                                                xh + C.vec_off[q] * NV);
     H2B_CUDA(cudaGetLastError());
   }
@@ -285,8 +285,8 @@ void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_
   d.val = A.dense.val;
   d.rp = A.dense.rp;
   d.ci = A.dense.ci;
-  d.x = A.xc16.p;
-  d.y = A.yc16.p;
+  d.x = w.xc16.p;
+  d.y = w.yc16.p;
   d.stride = A.dense.block_stride();
   d.br = A.dense.br;
   d.bc = A.dense.bc;
@@ -304,7 +304,7 @@ void hmv_multi_device(Matrix& A, const double* X, int64_t ldx, double* Y, int64_
     H2B_CUDA(cudaGetLastError());
   }
   k_down_leaf_mv<<<wgrid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[q], nl,
-                                                yh + A.vec_off[q] * NV, A.yc16.p, A.perm.p, Y, ldy, nv,
+                                                yh + A.vec_off[q] * NV, w.yc16.p, A.perm.p, Y, ldy, nv,
                                                 alpha, beta);
   H2B_CUDA(cudaGetLastError());
 }

@@ -121,6 +121,44 @@ class HostMatrix:
                 f += 2.0 * r[l] * c[l] * nb
         return f
 
+    def validate(self) -> None:
+        """Array dtypes and sizes against n, m, depth, ranks and the block
+        counts of the row pointers (ValueError otherwise): the C side reads
+        exactly that many entries from every pointer."""
+        q, m, n = int(self.depth), int(self.m), int(self.n)
+        if q < 0 or q > 30 or m < 1 or (m << q) != n:
+            raise ValueError("HostMatrix: n must equal m * 2^depth")
+
+        def arr(a, dt, size, name):
+            if not isinstance(a, np.ndarray) or a.dtype != dt:
+                raise ValueError(f"HostMatrix.{name}: must be a {np.dtype(dt).name} array")
+            if a.size != size:
+                raise ValueError(f"HostMatrix.{name}: has {a.size} entries, expected {size}")
+
+        if len(self.ranks) != q + 1:
+            raise ValueError(f"HostMatrix.ranks: expected {q + 1} levels")
+        r = [int(v) for v in self.ranks]
+        c = [int(v) for v in self.cranks()]
+        if len(c) != q + 1:
+            raise ValueError(f"HostMatrix.col_ranks: expected {q + 1} levels")
+        arr(self.perm, np.int32, n, "perm")
+        arr(self.leaf, np.float64, (1 << q) * m * r[q], "leaf")
+        arr(self.transfer, np.float64, sum((1 << l) * r[l] * r[l - 1] for l in range(1, q + 1)), "transfer")
+        arr(self.cpl_row_ptr, np.int32, sum((1 << l) + 1 for l in range(q + 1)), "cpl_row_ptr")
+        nb = self.cpl_blocks()
+        if any(b < 0 for b in nb):
+            raise ValueError("HostMatrix.cpl_row_ptr: negative block count")
+        arr(self.cpl_col_idx, np.int32, sum(nb), "cpl_col_idx")
+        arr(self.cpl_values, np.float64, sum(b * r[l] * c[l] for l, b in enumerate(nb)), "cpl_values")
+        arr(self.dense_row_ptr, np.int32, (1 << q) + 1, "dense_row_ptr")
+        nd = int(self.dense_row_ptr[-1])
+        arr(self.dense_col_idx, np.int32, nd, "dense_col_idx")
+        arr(self.dense_values, np.float64, nd * m * m, "dense_values")
+        if not self.symmetric:
+            arr(self.col_leaf, np.float64, (1 << q) * m * c[q], "col_leaf")
+            arr(self.col_transfer, np.float64, sum((1 << l) * c[l] * c[l - 1] for l in range(1, q + 1)),
+                "col_transfer")
+
     def copy(self) -> "HostMatrix":
         cp = lambda a: None if a is None else np.array(a, copy=True)  # noqa: E731
         return HostMatrix(self.n, self.m, self.depth, *(np.array(a, copy=True) for a in (

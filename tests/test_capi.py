@@ -70,3 +70,24 @@ def test_invalid_arguments_before_device():
         H2Matrix.construct(2, 1024, eta=0.0)
     with pytest.raises(ValueError):
         H2Matrix.construct(2, 900)
+
+
+def test_hostmatrix_validate_rejects_bad_sizes(orc):
+    """api.H2Matrix.from_host validates every pool size before the C call
+    (the C side copies exactly the sizes implied by n, ranks and row_ptr)."""
+    import numpy as np
+    import pytest
+    hm = orc.construct(2, 1024).to_host()
+    hm.validate()
+    bad = hm.copy()
+    bad.leaf = bad.leaf[:-1]
+    with pytest.raises(ValueError):
+        bad.validate()
+    bad = hm.copy()
+    bad.perm = bad.perm.astype(np.int64)
+    with pytest.raises(ValueError):
+        bad.validate()
+    bad = hm.copy()
+    bad.cpl_values = np.zeros(3)
+    with pytest.raises(ValueError):
+        bad.validate()

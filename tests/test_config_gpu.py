@@ -1,0 +1,119 @@
+"""Parity at the BASELINE.json configurations themselves,
+against goldens the REAL reference produced on the GPU host
+(tests/golden/make_config_golden.py -> tests/golden/config/).
+
+* hmv (hmv.hpp:175-188), x = random_vector(n, 1): relative 2-norm error of y at
+  65 536 fixed indices (all of y for n <= 2^16) <= 1e-12 (north_star bar), and
+  ||y||_2 to 1e-12.
+* compress (compression.hpp:466-551): per-level ranks identical, bytes after
+  identical, reference-model flops to 1e-12, frobenius_error within [0.5, 2]x
+  (and in fact to 1e-6), and the compressed operator's y at the same indices
+  within 10 eps of the reference's compressed operator.
+
+C4 (2D n = 2^22, 76.98 GB) and C3 (3D n = 2^20, 60.4 GB) hold coupling pools of
+6.4e9 / 5.7e9 elements: the int64 offset paths beyond 2^31 elements are
+compared with the reference here.  The device builds the matrices itself
+(h2b_matrix_build, bit-identical structure to the reference's construct())."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR, rel_err
+
+import paper_1902_01829_b200 as h2
+
+pytestmark = pytest.mark.gpu
+
+CONFIG_DIR = os.path.join(GOLDEN_DIR, "config")
+
+
+def load_case(name):
+    with open(os.path.join(CONFIG_DIR, name + ".json")) as f:
+        meta = json.load(f)
+    arr = np.load(os.path.join(CONFIG_DIR, name + ".npz"))
+    return meta, {k: arr[k] for k in arr.files}
+
+
+def build(meta):
+    return h2.H2Matrix.construct(meta["dim"], meta["n"], leaf_size=meta["leaf_size"],
+                                 grid_order=meta["grid_order"], eta=meta["eta"], ell=meta["ell"],
+                                 perturbation=meta["perturbation"], seed=meta["seed"])
+
+
+def check_structure(A, meta):
+    inf = A.info()
+    assert inf.ranks == meta["ranks"]
+    assert inf.cpl_blocks == meta["cpl_blocks"]
+    assert inf.dense_blocks == meta["dense_blocks"]
+    assert A.memory_footprint() == meta["footprint"]
+    assert inf.hmv_flops == pytest.approx(meta["hmv_flops"], rel=1e-12)
+
+
+def check_hmv(A, meta, arr, orc, key="y", norm_key="y_norm2", tol=1e-12):
+    import torch
+    n = meta["n"]
+    x = torch.from_numpy(orc.random_vector(n, 1)).cuda()
+    y = torch.zeros_like(x)
+    h2.hmv(A, x, y)
+    torch.cuda.synchronize()
+    yh = y.cpu().numpy()
+    idx = arr["idx"]
+    err = rel_err(yh[idx], arr[key])
+    assert err <= tol, (meta["case"], key, err)
+    assert float(np.linalg.norm(yh)) == pytest.approx(meta[norm_key], rel=max(tol, 1e-12))
+    return err
+
+
+def check_compress(A, meta, arr, orc):
+    g = meta["compress"]
+    rep = h2.compress(A, meta["eps"])
+    assert rep.new_ranks == g["new_ranks"], (meta["case"], rep.new_ranks, g["new_ranks"])
+    assert rep.bytes_before == int(g["bytes_before"])
+    assert rep.bytes_after == int(g["bytes_after"])
+    assert A.memory_footprint() == int(g["bytes_after"])
+    assert rep.frobenius_norm == pytest.approx(g["frobenius_norm"], rel=1e-10)
+    assert 0.5 <= rep.frobenius_error / g["frobenius_error"] <= 2.0
+    assert rep.frobenius_error == pytest.approx(g["frobenius_error"], rel=1e-6)
+    assert rep.total_flops() == pytest.approx(g["total_flops"], rel=1e-12)
+    check_hmv(A, meta, arr, orc, key="yc", norm_key="yc_norm2", tol=10 * meta["eps"])
+    return rep
+
+
+@pytest.mark.parametrize("case", ["C1", "C1k64", "C2", "C2alt"])
+def test_config_hmv_and_compress(gpu, orc, case):
+    meta, arr = load_case(case)
+    A = build(meta)
+    try:
+        check_structure(A, meta)
+        check_hmv(A, meta, arr, orc)
+        check_compress(A, meta, arr, orc)
+    finally:
+        A.close()
+        h2.release_cached_memory(0)
+
+
+def test_config_C4_hmv_n2_22(gpu, orc):
+    """C4: 2D n = 2^22, k = 64, 76.98 GB (coupling pool 6.4e9 elements)."""
+    meta, arr = load_case("C4")
+    A = build(meta)
+    try:
+        check_structure(A, meta)
+        assert sum(b * 64 * 64 for b in meta["cpl_blocks"]) > 2 ** 31
+        check_hmv(A, meta, arr, orc)
+    finally:
+        A.close()
+
+
+def test_config_C3_compress_3d_n2_20(gpu, orc):
+    """C3: 3D n = 2^20, k = 64, eps = 1e-6 (60.4 GB; coupling pool 5.7e9 elements)."""
+    meta, arr = load_case("C3")
+    A = build(meta)
+    try:
+        check_structure(A, meta)
+        check_hmv(A, meta, arr, orc)
+        check_compress(A, meta, arr, orc)
+    finally:
+        A.close()
+        h2.release_cached_memory(0)

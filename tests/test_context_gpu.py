@@ -1,0 +1,132 @@
+"""Per-caller workspaces (HmvContext, hmv.hpp:159-172): the reference allows
+concurrent hmv on one immutable matrix with one context each.
+Two threads x two contexts x two CUDA streams on one device matrix must give
+results bitwise equal to a sequential mat-vec; calls sharing a context (or the
+handle's own workspace) from several streams are serialised, not raced."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1902_01829_b200 as h2
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_threads(fns):
+    errs = []
+
+    def wrap(f):
+        try:
+            f()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=wrap, args=(f,)) for f in fns]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+def test_two_threads_two_contexts_two_streams_bitwise(gpu):
+    import torch
+    A = h2.H2Matrix.construct(2, 1 << 16)
+    n = A.n
+    xs = [torch.rand(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(s))
+          for s in (1, 2)]
+    ref = [h2.hmv(A, x) for x in xs]
+    torch.cuda.synchronize()
+    ctxs = [h2.HmvContext(A), h2.HmvContext(A)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    reps = 20
+    outs = [[torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(reps)] for _ in range(2)]
+
+    def worker(i):
+        def f():
+            with torch.cuda.stream(streams[i]):
+                for r in range(reps):
+                    h2.hmv(A, xs[i], outs[i][r], ctx=ctxs[i], stream=streams[i].cuda_stream)
+        return f
+
+    _run_threads([worker(0), worker(1)])
+    torch.cuda.synchronize()
+    for i in range(2):
+        for r in range(reps):
+            assert torch.equal(outs[i][r], ref[i]), (i, r)
+    for c in ctxs:
+        c.close()
+    A.close()
+
+
+def test_shared_workspace_across_streams_is_serialised(gpu):
+    """No context: both threads use the handle's workspace from their own
+    streams; the device-order hand-off keeps every result exact."""
+    import torch
+    A = h2.H2Matrix.construct(2, 1 << 15)
+    n = A.n
+    xs = [torch.rand(n, dtype=torch.float64, device="cuda") for _ in range(2)]
+    ref = [h2.hmv(A, x) for x in xs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    reps = 15
+    outs = [[torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(reps)] for _ in range(2)]
+
+    def worker(i):
+        def f():
+            for r in range(reps):
+                h2.hmv(A, xs[i], outs[i][r], stream=streams[i].cuda_stream)
+        return f
+
+    _run_threads([worker(0), worker(1)])
+    torch.cuda.synchronize()
+    for i in range(2):
+        for r in range(reps):
+            assert torch.equal(outs[i][r], ref[i]), (i, r)
+    A.close()
+
+
+def test_context_follows_compress(gpu, orc):
+    """A context created before compress() re-sizes itself for the new ranks
+    (the reference's context would be invalid, App. C of SURVEY.md)."""
+    A = h2.H2Matrix.construct(2, 4096)
+    ctx = h2.HmvContext(A)
+    x = orc.random_vector(4096, 1)
+    y0 = h2.hmv(A, x, ctx=ctx)
+    h2.compress(A, 1e-7)
+    y1 = h2.hmv(A, x, ctx=ctx)
+    y2 = h2.hmv(A, x)
+    assert np.array_equal(y1, y2)
+    assert np.linalg.norm(y1 - y0) / np.linalg.norm(y0) <= 1e-6
+    ctx.close()
+
+
+def test_host_pointer_hmv_with_context(gpu, orc):
+    O = orc.construct(2, 2048)
+    A = h2.H2Matrix.from_host(O.to_host())
+    ctx = h2.HmvContext(A)
+    x = orc.random_vector(2048, 3)
+    y0 = orc.random_vector(2048, 4)
+    y = h2.hmv(A, x, y0.copy(), 2.0, 3.0, ctx=ctx)
+    yr = O.hmv(x, y0, 2.0, 3.0)
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) <= 1e-12
+
+
+def test_python_argument_checks(gpu):
+    A = h2.H2Matrix.construct(2, 1024)
+    with pytest.raises(ValueError):
+        h2.hmv(A, np.zeros(1000))
+    with pytest.raises(ValueError):
+        h2.hmv(A, np.zeros(1024, np.float32))
+    with pytest.raises(ValueError):
+        h2.hmv(A, np.zeros(1024), np.zeros(1023))
+    with pytest.raises(ValueError):
+        h2.upsweep(A, np.zeros(10))
+    with pytest.raises(ValueError):
+        h2.tree_multiply(A, np.zeros(3))
+    with pytest.raises(ValueError):
+        h2.downsweep(A, np.zeros(A.vec_size() + 1), np.zeros(1024))
+    with pytest.raises(ValueError):
+        h2.validate_sampled(A, 0.1, points=np.zeros((1000, 2)))

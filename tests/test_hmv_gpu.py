@@ -104,8 +104,21 @@ def test_phases_match_oracle(gpu, orc):
         assert rel_err(yh, O.tree_multiply(xh)) <= TOL
         yd = h2.dense_mv(A, xc)
         assert rel_err(yd, O.dense_mv(xc)) <= TOL
+        yh_in = yh.copy()
         yc = h2.downsweep(A, yh, yd)
-        assert rel_err(yc, O.downsweep(yh, yd)) <= TOL
+        assert rel_err(yc, O.downsweep(yh_in, yd)) <= TOL
+        # the reference's downsweep leaves y^l += E y^{l-1} in its LevelVectors
+        # (hmv.hpp:136-146); so does h2b_downsweep
+        exp = yh_in.copy()
+        off = hm.vec_offsets()
+        for l in range(1, hm.depth + 1):
+            kc, kp = int(hm.ranks[l]), int(hm.ranks[l - 1])
+            E = hm.transfer_level(l)
+            par = exp[off[l - 1]:off[l]].reshape(1 << (l - 1), kp)
+            ch = exp[off[l]:off[l + 1]].reshape(1 << l, kc)
+            if kc and kp:
+                ch += np.einsum("cij,cj->ci", E, par[np.arange(1 << l) >> 1])
+        assert rel_err(yh, exp) <= TOL
 
 
 def test_linearity_and_self_adjoint(gpu):
