@@ -283,6 +283,77 @@ typedef struct h2b_comm {
 H2B_API h2b_status h2b_part_compress(h2b_matrix* A, double eps, const h2b_comm* comm,
                                      h2b_compress_report* report);
 
+/* ---- the reference's component objects and the phase API ----
+ * BasisTree<double> (h2_matrix.hpp:17-41), MatrixTree<double> (:46-51) and
+ * BSRLayer<double> (bsr.hpp:13-31) as device handles, and the reference
+ * functions that take them:
+ *   h2b_basis_upsweep         <- upsweep(V, x, n, xhat)              hmv.hpp:79-111
+ *   h2b_basis_downsweep       <- downsweep(U, yhat, y, n)            hmv.hpp:129-157
+ *   h2b_mtree_multiply        <- tree_multiply(S, xhat, yhat)        hmv.hpp:114-125
+ *   h2b_block_sparse_mv       <- block_sparse_mv(L, x, y, alpha, beta)  bsr.hpp:79-82
+ *   h2b_orthogonalize_basis   <- orthogonalize_basis(B) -> ProjectionTree  compression.hpp:69-126
+ *   h2b_project_coupling      <- project_coupling(Trow, Tcol, S)     compression.hpp:130-169
+ *   h2b_generate_weight_tree  <- generate_weight_tree(B, S) -> WeightTree  compression.hpp:213-256
+ *   h2b_truncate_basis        <- truncate_basis(B, R, eps, Tout) -> TruncationResult  compression.hpp:267-420
+ * Trees (ProjectionTree / WeightTree) cross as the reference's per-level pools
+ * concatenated over levels: rows[l] x cols[l] per node, column-major, node i
+ * of level l at offset i rows[l] cols[l] within the level.  Node vectors
+ * (LevelVectors) likewise.  Vectors and trees may be host or device memory. */
+typedef struct h2b_basis h2b_basis;
+typedef struct h2b_mtree h2b_mtree;
+typedef struct h2b_layer h2b_layer;
+
+typedef struct {
+  int32_t m;                /* BasisTree::leaf_dim */
+  int32_t depth;            /* q */
+  const int32_t* ranks;     /* depth + 1 */
+  const double* leaf;       /* 2^depth blocks of m x ranks[depth] */
+  const double* transfer;   /* l = 1..depth: 2^l blocks of ranks[l] x ranks[l-1] */
+} h2b_basis_desc;
+
+typedef struct {
+  int32_t block_rows, block_cols;  /* BSRLayer::block_rows / block_cols */
+  int32_t brows, bcols;            /* block shape */
+  const int32_t* row_ptr;          /* block_rows + 1 */
+  const int32_t* col_idx;          /* row_ptr[block_rows] */
+  const double* values;            /* blocks in col_idx order, column-major */
+} h2b_layer_desc;
+
+H2B_API h2b_status h2b_basis_create(const h2b_basis_desc* desc, int device, h2b_basis** out);
+H2B_API h2b_status h2b_basis_destroy(h2b_basis* B);
+/* leaf size, depth, ranks (depth + 1 entries); any pointer may be NULL */
+H2B_API h2b_status h2b_basis_shape(const h2b_basis* B, int32_t* m, int32_t* depth, int32_t* ranks);
+H2B_API h2b_status h2b_basis_export(const h2b_basis* B, double* leaf, double* transfer);
+H2B_API h2b_status h2b_basis_upsweep(h2b_basis* V, const double* x, int64_t n, double* xhat, h2b_ptr_kind kind);
+H2B_API h2b_status h2b_basis_downsweep(h2b_basis* U, double* yhat, double* y, int64_t n, h2b_ptr_kind kind);
+/* B orthogonalized in place; t_out (may be NULL): T, ranks[l]^2 per node. */
+H2B_API h2b_status h2b_orthogonalize_basis(h2b_basis* B, double* t_out);
+/* B truncated in place.  r_tree: R (ranks[l]^2 per node); t_out: Tout,
+ * new_ranks[l] x old ranks[l] per node (capacity old ranks[l]^2 per node);
+ * new_ranks / discarded_energy: TruncationResult, depth + 1 each.  NULLs skip. */
+H2B_API h2b_status h2b_truncate_basis(h2b_basis* B, const double* r_tree, double eps, double* t_out,
+                                      int32_t* new_ranks, double* discarded_energy);
+
+H2B_API h2b_status h2b_layer_create(const h2b_layer_desc* desc, int device, h2b_layer** out);
+H2B_API h2b_status h2b_layer_destroy(h2b_layer* L);
+/* y <- alpha L x + beta y in the reference's exact arithmetic (bitwise equal). */
+H2B_API h2b_status h2b_block_sparse_mv(h2b_layer* L, const double* x, double* y, double alpha, double beta,
+                                       h2b_ptr_kind kind);
+
+/* MatrixTree: nlevels layers, level l with block_rows = block_cols = 2^l. */
+H2B_API h2b_status h2b_mtree_create(int32_t nlevels, const h2b_layer_desc* levels, int device, h2b_mtree** out);
+H2B_API h2b_status h2b_mtree_destroy(h2b_mtree* S);
+H2B_API h2b_status h2b_mtree_shape(const h2b_mtree* S, int32_t* brows, int32_t* bcols, int64_t* nblocks);
+H2B_API h2b_status h2b_mtree_export(const h2b_mtree* S, double* values);
+/* xhat: 2^l bcols[l] per level; yhat: 2^l brows[l] per level. */
+H2B_API h2b_status h2b_mtree_multiply(h2b_mtree* S, const double* xhat, double* yhat, h2b_ptr_kind kind);
+/* tcol == NULL: the column tree is trow (project_coupling(T, T, S)). */
+H2B_API h2b_status h2b_project_coupling(const double* trow, const int32_t* trow_rows, const int32_t* trow_cols,
+                                        const double* tcol, const int32_t* tcol_rows, const int32_t* tcol_cols,
+                                        h2b_mtree* S);
+/* r_out: R, ranks[l]^2 per node (R^0 = 0). */
+H2B_API h2b_status h2b_generate_weight_tree(h2b_basis* B, h2b_mtree* S, double* r_out);
+
 /* Per-phase device time of the h2b_hmv calls made since phase timing was
  * enabled or last read, averaged per call (ms; CUDA events recorded on the
  * launching stream, no host syncs inside h2b_hmv):

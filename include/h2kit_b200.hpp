@@ -11,8 +11,16 @@
 //   h2kit::upsweep / tree_multiply / downsweep  (:79-157)
 //   h2kit::compress(A, eps)                 ->  h2kit_b200::compress(A, eps)
 //        (include/h2kit/compression.hpp:466-551)
-//   h2kit::orthogonalize_basis(B)           ->  h2kit_b200::orthogonalize_basis(A)   (:69-126)
-//     (B = A.col_basis() of a non-symmetric A -> h2kit_b200::orthogonalize_col_basis(A))
+//   h2kit::orthogonalize_basis(B)           ->  h2kit_b200::orthogonalize_basis(B)   (:69-126)
+//   h2kit::project_coupling(Tr, Tc, S)      ->  h2kit_b200::project_coupling(Tr, Tc, S)  (:130-169)
+//   h2kit::generate_weight_tree(B, S)       ->  h2kit_b200::generate_weight_tree(B, S)   (:213-256)
+//   h2kit::truncate_basis(B, R, eps, T)     ->  h2kit_b200::truncate_basis(B, R, eps, T) (:267-420)
+//   h2kit::upsweep(V, x, n, xhat) / downsweep(U, yhat, y, n) / tree_multiply(S, xhat, yhat)
+//   h2kit::block_sparse_mv(L, x, y, alpha, beta)                                (bsr.hpp:79-82)
+// on the reference's own component types (BasisTree / MatrixTree / BSRLayer /
+// ProjectionTree / WeightTree / LevelVectors).  include/h2kit_b200_bind.hpp
+// turns all of them into explicit specializations of the h2kit templates, so
+// unmodified reference code (and its tests) runs on the B200.
 //
 // Semantics match the reference: alpha/beta (beta == 0 never reads y), x/y
 // in original point order, compress() mutates A in place and returns a
@@ -50,6 +58,9 @@ using h2kit::HmvContext;
 using h2kit::index_t;
 using h2kit::LevelVectors;
 using h2kit::MatrixTree;
+using h2kit::ProjectionTree;
+using h2kit::TruncationResult;
+using h2kit::WeightTree;
 
 namespace detail {
 
@@ -252,6 +263,213 @@ inline void pull(h2b_matrix* h, H2Matrix<double>& A) {
   }
 }
 
+// ---- component objects (BasisTree / MatrixTree / BSRLayer) ----------------
+inline void mix_sample(uint64_t& h, const std::vector<double>& v) {
+  auto mix = [&](uint64_t x) { h = (h ^ x) * 1099511628211ull; };
+  mix(v.size());
+  mix(reinterpret_cast<uintptr_t>(v.data()));
+  const size_t step = v.size() / 61 + 1;
+  for (size_t i = 0; i < v.size(); i += step) {
+    uint64_t b;
+    std::memcpy(&b, &v[i], sizeof(b));
+    mix(b);
+  }
+}
+
+inline void require_complete(const BasisTree<double>& B) {
+  for (int l = 0; l <= B.depth(); ++l)
+    if (B.flat.level_size(l) != (index_t(1) << l))
+      throw std::invalid_argument("h2kit_b200: the basis tree must be the complete binary tree");
+}
+
+inline uint64_t fingerprint(const BasisTree<double>& B) {
+  uint64_t h = 1469598103934665603ull;
+  h = (h ^ uint64_t(B.depth())) * 1099511628211ull;
+  h = (h ^ uint64_t(B.leaf_dim)) * 1099511628211ull;
+  for (int r : B.ranks) h = (h ^ uint64_t(r)) * 1099511628211ull;
+  mix_sample(h, B.leaf_pool);
+  for (const auto& t : B.transfer) mix_sample(h, t);
+  return h;
+}
+
+inline uint64_t fingerprint(const MatrixTree<double>& S) {
+  uint64_t h = 1469598103934665603ull;
+  for (const auto& L : S.levels) {
+    h = (h ^ uint64_t(L.brows) ^ (uint64_t(L.bcols) << 20) ^ (uint64_t(L.block_rows) << 40)) * 1099511628211ull;
+    h = (h ^ uint64_t(L.num_blocks())) * 1099511628211ull;
+    mix_sample(h, L.values);
+  }
+  return h;
+}
+
+inline uint64_t fingerprint(const BSRLayer<double>& L) {
+  uint64_t h = 1469598103934665603ull;
+  h = (h ^ uint64_t(L.brows) ^ (uint64_t(L.bcols) << 20)) * 1099511628211ull;
+  h = (h ^ uint64_t(L.block_rows) ^ (uint64_t(L.block_cols) << 32)) * 1099511628211ull;
+  h = (h ^ uint64_t(L.num_blocks())) * 1099511628211ull;
+  for (index_t c : L.col_idx) h = (h ^ uint64_t(c)) * 1099511628211ull;
+  mix_sample(h, L.values);
+  return h;
+}
+
+template <class H, h2b_status (*Destroy)(H*)>
+struct Handle {
+  H* h = nullptr;
+  ~Handle() {
+    if (h) Destroy(h);
+  }
+};
+using BasisHandle = Handle<h2b_basis, h2b_basis_destroy>;
+using TreeHandle = Handle<h2b_mtree, h2b_mtree_destroy>;
+using LayerHandle = Handle<h2b_layer, h2b_layer_destroy>;
+
+template <class M>
+struct CompEntry {
+  uint64_t fp;
+  std::shared_ptr<M> m;
+};
+template <class M>
+inline std::map<const void*, CompEntry<M>>& comp_cache() {
+  static std::map<const void*, CompEntry<M>> c;
+  return c;
+}
+
+// Cached device mirror of a component object keyed by address + fingerprint.
+template <class M, class Obj, class Make>
+inline std::shared_ptr<M> comp_of(const Obj& o, Make make) {
+  const uint64_t fp = fingerprint(o);
+  std::lock_guard<std::mutex> g(cache_mutex());
+  auto& c = comp_cache<M>();
+  auto it = c.find(&o);
+  if (it != c.end() && it->second.fp == fp) return it->second.m;
+  auto m = std::make_shared<M>();
+  make(*m);
+  c[&o] = CompEntry<M>{fp, m};
+  return m;
+}
+template <class M, class Obj>
+inline void comp_rekey(const Obj& o, const std::shared_ptr<M>& m) {
+  const uint64_t fp = fingerprint(o);
+  std::lock_guard<std::mutex> g(cache_mutex());
+  comp_cache<M>()[&o] = CompEntry<M>{fp, m};
+}
+
+inline std::shared_ptr<BasisHandle> basis_of(const BasisTree<double>& B) {
+  return comp_of<BasisHandle>(B, [&](BasisHandle& m) {
+    require_complete(B);
+    const int q = B.depth();
+    std::vector<double> tr;
+    for (int l = 1; l <= q; ++l) tr.insert(tr.end(), B.transfer[l].begin(), B.transfer[l].end());
+    std::vector<int32_t> ranks(B.ranks.begin(), B.ranks.end());
+    h2b_basis_desc d{B.leaf_dim, q, ranks.data(), B.leaf_pool.data(), tr.data()};
+    check(h2b_basis_create(&d, 0, &m.h));
+  });
+}
+
+inline std::vector<h2b_layer_desc> layer_descs(const MatrixTree<double>& S,
+                                                std::vector<std::vector<index_t>>& rps) {
+  std::vector<h2b_layer_desc> d(S.levels.size());
+  rps.resize(S.levels.size());
+  for (size_t l = 0; l < S.levels.size(); ++l) {
+    const BSRLayer<double>& L = S.levels[l];
+    const index_t rows = index_t(1) << l;
+    if (L.row_ptr.empty()) rps[l].assign(size_t(rows) + 1, 0);  // an empty level: no structure stored
+    const index_t* rp = L.row_ptr.empty() ? rps[l].data() : L.row_ptr.data();
+    d[l] = h2b_layer_desc{L.row_ptr.empty() ? rows : L.block_rows, L.row_ptr.empty() ? rows : L.block_cols,
+                          L.brows, L.bcols, rp, L.col_idx.data(), L.values.data()};
+  }
+  return d;
+}
+
+inline std::shared_ptr<TreeHandle> tree_of(const MatrixTree<double>& S) {
+  return comp_of<TreeHandle>(S, [&](TreeHandle& m) {
+    std::vector<std::vector<index_t>> rps;
+    const auto d = layer_descs(S, rps);
+    check(h2b_mtree_create(int32_t(d.size()), d.data(), 0, &m.h));
+  });
+}
+
+inline std::shared_ptr<LayerHandle> layer_of(const BSRLayer<double>& L) {
+  return comp_of<LayerHandle>(L, [&](LayerHandle& m) {
+    std::vector<index_t> rp = L.row_ptr;
+    if (rp.empty()) rp.assign(size_t(L.block_rows) + 1, 0);
+    h2b_layer_desc d{L.block_rows, L.block_cols, L.brows, L.bcols, rp.data(), L.col_idx.data(), L.values.data()};
+    check(h2b_layer_create(&d, 0, &m.h));
+  });
+}
+
+// Device basis -> the reference object (ranks, leaves, transfers).
+inline void pull_basis(h2b_basis* h, BasisTree<double>& B) {
+  const int q = B.depth();
+  std::vector<int32_t> r(q + 1);
+  check(h2b_basis_shape(h, nullptr, nullptr, r.data()));
+  B.ranks.assign(r.begin(), r.end());
+  size_t ntr = 0;
+  for (int l = 1; l <= q; ++l) ntr += (size_t(1) << l) * r[l] * r[l - 1];
+  std::vector<double> tr(std::max<size_t>(ntr, 1));
+  B.leaf_pool.assign((size_t(1) << q) * B.leaf_dim * r[q], 0.0);
+  check(h2b_basis_export(h, B.leaf_pool.data(), tr.data()));
+  B.transfer.resize(q + 1);
+  size_t o = 0;
+  for (int l = 1; l <= q; ++l) {
+    const size_t sz = (size_t(1) << l) * r[l] * r[l - 1];
+    B.transfer[l].assign(tr.begin() + o, tr.begin() + o + sz);
+    o += sz;
+  }
+}
+
+// Device matrix tree -> the reference object (block shapes and values).
+inline void pull_tree(h2b_mtree* h, MatrixTree<double>& S) {
+  const size_t nl = S.levels.size();
+  std::vector<int32_t> br(nl), bc(nl);
+  std::vector<int64_t> nb(nl);
+  check(h2b_mtree_shape(h, br.data(), bc.data(), nb.data()));
+  size_t nv = 0;
+  for (size_t l = 0; l < nl; ++l) nv += size_t(nb[l]) * br[l] * bc[l];
+  std::vector<double> v(std::max<size_t>(nv, 1));
+  check(h2b_mtree_export(h, v.data()));
+  size_t o = 0;
+  for (size_t l = 0; l < nl; ++l) {
+    auto& L = S.levels[l];
+    const size_t sz = size_t(nb[l]) * br[l] * bc[l];
+    L.brows = br[l];
+    L.bcols = bc[l];
+    if (nb[l]) L.values.assign(v.begin() + o, v.begin() + o + sz);
+    o += sz;
+  }
+}
+
+template <class Pools>
+inline std::vector<double> flat_pools(const Pools& pools) {
+  std::vector<double> f;
+  for (const auto& p : pools) f.insert(f.end(), p.begin(), p.end());
+  if (f.empty()) f.push_back(0.0);
+  return f;
+}
+
+// The reference's flop model of one hmv (flops.hpp add_* over the call
+// sequence of hmv.hpp:175-188), so h2kit::flops counters keep reporting.
+inline void count_upsweep(const BasisTree<double>& V) {
+  const int q = V.depth();
+  h2kit::flops::add_gemv(size_t(1) << q, V.leaf_dim, V.ranks[q]);
+  for (int l = q; l >= 1; --l) h2kit::flops::add_gemv(size_t(1) << l, V.ranks[l], V.ranks[l - 1]);
+}
+inline void count_downsweep(const BasisTree<double>& U) {
+  const int q = U.depth();
+  for (int l = 1; l <= q; ++l) h2kit::flops::add_gemv(size_t(1) << l, U.ranks[l], U.ranks[l - 1]);
+  h2kit::flops::add_gemv(size_t(1) << q, U.leaf_dim, U.ranks[q]);
+}
+inline void count_tree(const MatrixTree<double>& S) {
+  for (const auto& L : S.levels)
+    if (!L.empty()) h2kit::flops::add_spmv(L.num_blocks(), L.brows, L.bcols);
+}
+inline void count_hmv(const H2Matrix<double>& A) {
+  h2kit::flops::add_spmv(A.dense.num_blocks(), A.dense.brows, A.dense.bcols);
+  count_upsweep(A.col_basis());
+  count_tree(A.coupling);
+  count_downsweep(A.row_basis);
+}
+
 }  // namespace detail
 
 // Drop the cached device mirror of A (call after mutating A on the host).
@@ -267,12 +485,207 @@ inline void hmv(const H2Matrix<double>& A, const double* x, double* y, double al
                 HmvContext<double>& ctx) {
   auto m = detail::mirror_of(A);
   detail::check(h2b_hmv_ctx(m->get(), m->context(&ctx), x, y, alpha, beta, H2B_PTR_AUTO, nullptr));
+  detail::count_hmv(A);
 }
 
 inline void hmv(const H2Matrix<double>& A, const double* x, double* y, double alpha = 1.0,
                 double beta = 0.0) {
   auto m = detail::mirror_of(A);
   detail::check(h2b_hmv(m->get(), x, y, alpha, beta, H2B_PTR_AUTO, nullptr));
+  detail::count_hmv(A);
+}
+
+// ---- the reference's phase API on its own component types ----------------
+
+// upsweep(V, x, n, xhat) (hmv.hpp:79-111): x in cluster order.
+inline void upsweep(const BasisTree<double>& V, const double* x, index_t n, LevelVectors<double>& xhat) {
+  auto m = detail::basis_of(V);
+  LevelVectors<double> shape;
+  shape.resize(V);
+  bool sized = xhat.pool.size() == shape.pool.size();
+  for (size_t l = 0; sized && l < shape.pool.size(); ++l) sized = xhat.pool[l].size() == shape.pool[l].size();
+  if (!sized) xhat.resize(V);
+  std::vector<double> flat = detail::flat_pools(shape.pool);
+  detail::check(h2b_basis_upsweep(m->h, x, n, flat.data(), H2B_PTR_HOST));
+  size_t o = 0;
+  for (auto& p : xhat.pool) {
+    std::copy(flat.begin() + o, flat.begin() + o + p.size(), p.begin());
+    o += p.size();
+  }
+  detail::count_upsweep(V);
+}
+
+// downsweep(U, yhat, y, n) (hmv.hpp:129-157): yhat updated in place, y += U y^q.
+inline void downsweep(const BasisTree<double>& U, LevelVectors<double>& yhat, double* y, index_t n) {
+  auto m = detail::basis_of(U);
+  LevelVectors<double> shape;
+  shape.resize(U);
+  if (yhat.pool.size() != shape.pool.size()) throw std::invalid_argument("downsweep: dim mismatch");
+  for (size_t l = 0; l < shape.pool.size(); ++l)
+    if (yhat.pool[l].size() != shape.pool[l].size()) throw std::invalid_argument("downsweep: dim mismatch");
+  std::vector<double> flat = detail::flat_pools(yhat.pool);
+  detail::check(h2b_basis_downsweep(m->h, flat.data(), y, n, H2B_PTR_HOST));
+  size_t o = 0;
+  for (auto& p : yhat.pool) {
+    std::copy(flat.begin() + o, flat.begin() + o + p.size(), p.begin());
+    o += p.size();
+  }
+  detail::count_downsweep(U);
+}
+
+// tree_multiply(S, xhat, yhat) (hmv.hpp:114-125).
+inline void tree_multiply(const MatrixTree<double>& S, const LevelVectors<double>& xhat,
+                          LevelVectors<double>& yhat) {
+  const size_t nl = S.levels.size();
+  if (xhat.pool.size() < nl || yhat.pool.size() < nl) throw std::invalid_argument("tree_multiply: dim mismatch");
+  for (size_t l = 0; l < nl; ++l) {
+    const auto& L = S.levels[l];
+    const size_t nodes = size_t(1) << l;
+    if (!L.empty() && (xhat.pool[l].size() != nodes * L.bcols || yhat.pool[l].size() != nodes * L.brows))
+      throw std::invalid_argument("tree_multiply: dim mismatch");
+  }
+  auto m = detail::tree_of(S);
+  std::vector<int32_t> br(nl), bc(nl);
+  detail::check(h2b_mtree_shape(m->h, br.data(), bc.data(), nullptr));
+  std::vector<double> xf, yf;
+  for (size_t l = 0; l < nl; ++l) {
+    const size_t nodes = size_t(1) << l;
+    if (xhat.pool[l].size() == nodes * bc[l])
+      xf.insert(xf.end(), xhat.pool[l].begin(), xhat.pool[l].end());
+    else
+      xf.insert(xf.end(), nodes * bc[l], 0.0);  // an empty level of another shape: unread
+  }
+  size_t ny = 0;
+  for (size_t l = 0; l < nl; ++l) ny += (size_t(1) << l) * br[l];
+  yf.assign(std::max<size_t>(ny, 1), 0.0);
+  if (xf.empty()) xf.push_back(0.0);
+  detail::check(h2b_mtree_multiply(m->h, xf.data(), yf.data(), H2B_PTR_HOST));
+  size_t o = 0;
+  for (size_t l = 0; l < nl; ++l) {
+    const size_t sz = (size_t(1) << l) * br[l];
+    auto& p = yhat.pool[l];
+    if (p.size() == sz)
+      std::copy(yf.begin() + o, yf.begin() + o + sz, p.begin());
+    else
+      std::fill(p.begin(), p.end(), 0.0);  // empty level (hmv.hpp:119-122)
+    o += sz;
+  }
+  detail::count_tree(S);
+}
+
+// block_sparse_mv(L, x, y, alpha, beta) (bsr.hpp:79-82): bitwise the reference's result.
+inline void block_sparse_mv(const BSRLayer<double>& L, const double* x, double* y, double alpha, double beta) {
+  auto m = detail::layer_of(L);
+  detail::check(h2b_block_sparse_mv(m->h, x, y, alpha, beta, H2B_PTR_HOST));
+  h2kit::flops::add_spmv(L.num_blocks(), L.brows, L.bcols);
+}
+
+// orthogonalize_basis(B) (compression.hpp:69-126): B in place, returns T.
+inline ProjectionTree<double> orthogonalize_basis(BasisTree<double>& B) {
+  auto m = detail::basis_of(B);
+  const int q = B.depth();
+  ProjectionTree<double> Tp;
+  Tp.rows = B.ranks;
+  Tp.cols = B.ranks;
+  Tp.pool.resize(q + 1);
+  size_t nt = 0;
+  for (int l = 0; l <= q; ++l) nt += (size_t(1) << l) * B.ranks[l] * B.ranks[l];
+  std::vector<double> flat(std::max<size_t>(nt, 1));
+  detail::check(h2b_orthogonalize_basis(m->h, flat.data()));
+  size_t o = 0;
+  for (int l = 0; l <= q; ++l) {
+    const size_t sz = (size_t(1) << l) * B.ranks[l] * B.ranks[l];
+    Tp.pool[l].assign(flat.begin() + o, flat.begin() + o + sz);
+    o += sz;
+  }
+  detail::pull_basis(m->h, B);
+  detail::comp_rekey(B, m);
+  return Tp;
+}
+
+// project_coupling(Trow, Tcol, S) (compression.hpp:130-169).
+inline void project_coupling(const ProjectionTree<double>& Trow, const ProjectionTree<double>& Tcol,
+                             MatrixTree<double>& S) {
+  const size_t nl = S.levels.size();
+  if (Trow.rows.size() < nl || Trow.cols.size() < nl || Tcol.rows.size() < nl || Tcol.cols.size() < nl)
+    throw std::invalid_argument("project_coupling: dim mismatch");
+  for (size_t l = 0; l < nl; ++l) {
+    const auto& L = S.levels[l];
+    if (!L.empty() && (Trow.cols[l] != L.brows || Tcol.cols[l] != L.bcols))
+      throw std::invalid_argument("project_coupling: dim mismatch");
+  }
+  auto m = detail::tree_of(S);
+  std::vector<int32_t> rr(Trow.rows.begin(), Trow.rows.begin() + nl), rc(Trow.cols.begin(), Trow.cols.begin() + nl);
+  std::vector<int32_t> cr(Tcol.rows.begin(), Tcol.rows.begin() + nl), cc(Tcol.cols.begin(), Tcol.cols.begin() + nl);
+  std::vector<double> tr, tc;
+  for (size_t l = 0; l < nl; ++l) tr.insert(tr.end(), Trow.pool[l].begin(), Trow.pool[l].end());
+  const bool same = &Trow == &Tcol;
+  if (!same)
+    for (size_t l = 0; l < nl; ++l) tc.insert(tc.end(), Tcol.pool[l].begin(), Tcol.pool[l].end());
+  if (tr.empty()) tr.push_back(0.0);
+  if (!same && tc.empty()) tc.push_back(0.0);
+  detail::check(h2b_project_coupling(tr.data(), rr.data(), rc.data(), same ? nullptr : tc.data(), cr.data(),
+                                     cc.data(), m->h));
+  for (size_t l = 0; l < nl; ++l) {
+    const auto& L = S.levels[l];
+    if (!L.empty()) {
+      h2kit::flops::add_gemm(L.num_blocks(), Trow.rows[l], L.bcols, L.brows);
+      h2kit::flops::add_gemm(L.num_blocks(), Trow.rows[l], Tcol.rows[l], L.bcols);
+    }
+  }
+  detail::pull_tree(m->h, S);
+  detail::comp_rekey(S, m);
+}
+
+// generate_weight_tree(B, S) (compression.hpp:213-256); B must be orthogonal.
+inline WeightTree<double> generate_weight_tree(const BasisTree<double>& B, const MatrixTree<double>& S) {
+  auto mb = detail::basis_of(B);
+  auto ms = detail::tree_of(S);
+  const int q = B.depth();
+  WeightTree<double> R;
+  R.dim = B.ranks;
+  R.pool.resize(q + 1);
+  size_t nr = 0;
+  for (int l = 0; l <= q; ++l) nr += (size_t(1) << l) * B.ranks[l] * B.ranks[l];
+  std::vector<double> flat(std::max<size_t>(nr, 1));
+  detail::check(h2b_generate_weight_tree(mb->h, ms->h, flat.data()));
+  size_t o = 0;
+  for (int l = 0; l <= q; ++l) {
+    const size_t sz = (size_t(1) << l) * B.ranks[l] * B.ranks[l];
+    R.pool[l].assign(flat.begin() + o, flat.begin() + o + sz);
+    o += sz;
+  }
+  return R;
+}
+
+// truncate_basis(B, R, eps, Tout) (compression.hpp:267-420): B in place.
+inline TruncationResult truncate_basis(BasisTree<double>& B, const WeightTree<double>& R, double eps,
+                                       ProjectionTree<double>& Tout) {
+  if (eps < 0) throw std::invalid_argument("truncate_basis: eps must be non-negative");
+  auto m = detail::basis_of(B);
+  const int q = B.depth();
+  const std::vector<int> old = B.ranks;
+  std::vector<double> rf = detail::flat_pools(R.pool);
+  size_t nt = 0;
+  for (int l = 0; l <= q; ++l) nt += (size_t(1) << l) * old[l] * old[l];
+  std::vector<double> tf(std::max<size_t>(nt, 1));
+  std::vector<int32_t> nr(q + 1);
+  TruncationResult res;
+  res.discarded_energy.assign(q + 1, 0.0);
+  detail::check(h2b_truncate_basis(m->h, rf.data(), eps, tf.data(), nr.data(), res.discarded_energy.data()));
+  res.new_ranks.assign(nr.begin(), nr.end());
+  Tout.rows = res.new_ranks;
+  Tout.cols = old;
+  Tout.pool.assign(q + 1, {});
+  size_t o = 0;
+  for (int l = 0; l <= q; ++l) {
+    const size_t sz = (size_t(1) << l) * nr[l] * old[l];
+    Tout.pool[l].assign(tf.begin() + o, tf.begin() + o + sz);
+    o += sz;
+  }
+  detail::pull_basis(m->h, B);
+  detail::comp_rekey(B, m);
+  return res;
 }
 
 // Phase entry points (hmv.hpp:79-157) on the mirror of A; node vectors use

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -101,6 +102,16 @@ void upload_blocks(const double* h, double* d, int rows, int cols, int64_t count
 }
 
 }  // namespace
+
+// for phases.cu
+h2b_status guarded_call(const std::function<void()>& f) { return guarded(f); }
+void need_device_public(int device) { need_device(device); }
+bool resolve_device_public(h2b_ptr_kind kind, const void* p) { return resolve_device(kind, p); }
+// host -> padded device blocks, synchronous (phases.cu)
+void upload_blocks_sync(const double* h, double* d, int rows, int cols, int64_t count, cudaStream_t s) {
+  upload_blocks(h, d, rows, cols, count, s);
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
 
 // padded device blocks -> unpadded host blocks (also used by io.cu)
 void download_blocks(const double* d, double* h, int rows, int cols, int64_t count,
@@ -424,8 +435,10 @@ void check_shape(int n, int m, int depth, const int32_t* ranks) {
   require(int64_t(1) << (depth + 1) < (int64_t(1) << kLayerShift), "tree too deep for the work-list encoding");
 }
 
+// cols: block columns (BSRLayer::block_cols; -1: == rows, a coupling level).
 void set_layer_structure(Layer& L, int64_t rows, int br, int bc, const int32_t* rp,
-                         const int32_t* ci) {
+                         const int32_t* ci, int64_t cols = -1) {
+  if (cols < 0) cols = rows;
   L.rows = rows;
   L.br = br;
   L.bc = bc;
@@ -436,7 +449,7 @@ void set_layer_structure(Layer& L, int64_t rows, int br, int bc, const int32_t* 
   L.h_ci.assign(ci, ci + L.nb);
   for (int64_t r = 0; r < rows; ++r)
     for (int32_t b = L.h_rp[r]; b < L.h_rp[r + 1]; ++b)
-      require(L.h_ci[b] >= 0 && L.h_ci[b] < rows, "col_idx out of range");
+      require(L.h_ci[b] >= 0 && L.h_ci[b] < cols, "col_idx out of range");
 }
 
 h2b_matrix* create_from_desc(const h2b_matrix_desc& d, int device) {

@@ -2055,6 +2055,111 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
 #endif
 }
 
+// ---------------------------------------------------------------- phase API
+// The reference's compression phases on component objects (phases.cu):
+// B a basis-only Matrix (BasisTree), S a coupling-only Matrix (MatrixTree).
+// Trees (ProjectionTree / WeightTree pools) are level-concatenated device
+// arrays, rows[l] x cols[l] per node, column-major, like the reference's pools.
+
+// orthogonalize_basis(B) (compression.hpp:69-126): t_dev gets T (k_l x k_l per node).
+void phase_orthogonalize(Matrix& B, double* t_dev, cudaStream_t s) {
+  Flops fl;
+  double f = 0;
+  TreePool T;
+  orthogonalize(B, T, s, fl, f, Part{}, t_dev);
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+// project_coupling(Trow, Tcol, S) (compression.hpp:130-169) into a fresh pool
+// (the new block shapes may be larger than the old ones); same: Tcol is Trow.
+void phase_project(Matrix& S, const double* tr, const std::vector<int>& tr_rows, const std::vector<int>& tr_cols,
+                   const double* tc, const std::vector<int>& tc_rows, const std::vector<int>& tc_cols, bool same,
+                   cudaStream_t s) {
+  const int q = S.q;
+  TreePool Tr, Tc;
+  Tr.alloc(S, tr_rows, tr_cols, const_cast<double*>(tr));
+  Tc.alloc(S, tc_rows, tc_cols, const_cast<double*>(tc));
+  for (int l = 0; l <= q; ++l) {
+    const Layer& L = S.cpl[l];
+    if (L.nb == 0) continue;
+    require(tr_cols[l] == L.br && tc_cols[l] == L.bc, "project_coupling: dim mismatch");
+    if (tr_rows[l] > kMaxDim || tc_rows[l] > kMaxDim)
+      throw Error(H2B_UNSUPPORTED, "project_coupling: rank > 64 not supported by the compiled kernels");
+  }
+  std::vector<int64_t> noff(q + 2, 0);
+  for (int l = 0; l <= q; ++l) noff[l + 1] = noff[l] + S.cpl[l].nb * int64_t(pad2(tr_rows[l])) * tc_rows[l];
+  DevBuf<double> out;
+  out.alloc(std::max<int64_t>(1, noff[q + 1]));
+  Workspace ws{S.device};
+  ws.buf = ws_checkout(S.device, ProjRows::need(S) + 64);
+  Arena par;
+  par.reserve(ws.buf.p, ws.buf.n);
+  ProjRows PR;
+  project_rows(S, par, PR, s, same);
+  Flops fl;
+  double f = 0;
+  for (int l = 0; l <= q; ++l)
+    project_level(S, Tr, Tc, PR, l, /*tri=*/false, /*want_sum=*/false, fl, f, Part{}, s, same, out.p + noff[l],
+                  int64_t(pad2(tr_rows[l])) * tc_rows[l]);
+  H2B_CUDA(cudaStreamSynchronize(s));
+  S.cpl_val = std::move(out);
+  for (int l = 0; l <= q; ++l) {
+    Layer& L = S.cpl[l];
+    L.br = tr_rows[l];
+    L.bc = tc_rows[l];
+    L.ld = pad2(L.br);
+    L.val = S.cpl_val.p + noff[l];
+  }
+}
+
+// generate_weight_tree(B, S) (compression.hpp:213-256): r_dev gets R (k_l x k_l
+// per node, upper triangular; R^0 = 0).
+void phase_weights(Matrix& S, Matrix& B, double* r_dev, cudaStream_t s) {
+  require(S.q == B.q, "generate_weight_tree: depth mismatch");
+  for (int l = 1; l <= S.q; ++l)
+    require(S.cpl[l].nb == 0 || S.cpl[l].br == B.rank[l], "generate_weight_tree: dim mismatch");
+  Flops fl;
+  double f = 0;
+  TreePool R;
+  Workspace ws{S.device};
+  const size_t need = weights_arena_need(S) + 64;
+  ws.buf = ws_checkout(S.device, need);
+  Arena ar;
+  ar.reserve(ws.buf.p, ws.buf.n);
+  weights(S, B, false, R, s, fl, f, Part{}, r_dev, ar);
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
+
+// truncate_basis(B, R, eps, Tout) (compression.hpp:267-420): B is truncated in
+// place; t_dev gets Tout level-concatenated, new_rank[l] x old_rank[l] per node;
+// energy[l] the discarded energy of level l.
+void phase_truncate(Matrix& B, const double* r_dev, double eps, double* t_dev, std::vector<double>& energy,
+                    cudaStream_t s) {
+  require(eps >= 0.0, "truncate_basis: eps must be non-negative");
+  const std::vector<int> old = B.rank;
+  Flops fl;
+  double f = 0;
+  TreePool R, Tt;
+  R.alloc(B, B.rank, B.rank, const_cast<double*>(r_dev));
+  const size_t tree = TreePool::need(B, old, old);
+  Workspace ws{B.device};
+  const size_t arena = truncate_sizes(B).total + 64;
+  ws.buf = ws_checkout(B.device, tree + arena);
+  Arena ar;
+  ar.reserve(ws.buf.p + tree, ws.buf.n - tree);
+  truncate(B, R, eps, Tt, s, fl, f, Part{}, ws.buf.p, ar, nullptr, &energy);
+  int64_t o = 0;
+  for (int l = 0; l <= B.q; ++l) {
+    const int64_t c = B.nodes(l) * int64_t(Tt.rows[l]) * old[l];
+    if (c) H2B_CUDA(cudaMemcpyAsync(t_dev + o, Tt.at(l), c * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    o += c;
+  }
+  H2B_CUDA(cudaStreamSynchronize(s));
+  B.vec_off.assign(B.q + 2, 0);
+  for (int l = 0; l <= B.q; ++l) B.vec_off[l + 1] = B.vec_off[l] + B.nodes(l) * B.rank[l];
+  ++B.layout_version;
+}
+
 // col: the column basis (non-symmetric matrices; the row basis itself when
 // symmetric).  The coupling is not projected (the reference's contract).
 void orthogonalize_matrix(Matrix& A, double* t_out, bool col) {

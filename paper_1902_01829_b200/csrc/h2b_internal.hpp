@@ -237,6 +237,9 @@ void launch_up_level(const Matrix& B, int l, double* xhat, cudaStream_t s, int64
 // x^ level offsets from xb (the column basis' vec_off), y^ from A.
 void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
                 double* ydense, const double* xh, double* yh, cudaStream_t s, const Matrix* xb = nullptr);
+// One generic BSR layer, y <- alpha L x + beta y (block_sparse_mv, bsr.hpp:50-82),
+// bitwise the reference's arithmetic (phase API).
+void launch_bsr_exact(const Layer& L, const double* x, double* y, double alpha, double beta, cudaStream_t s);
 // children at level l in [c0, c1)
 void launch_down_level(const Matrix& A, int l, double* yhat, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1);
 // yc += U y^q; to_user: y[perm[t]] = alpha v + beta y[perm[t]] (original

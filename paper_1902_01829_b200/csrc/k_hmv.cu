@@ -419,6 +419,44 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
   }
 }
 
+// block_sparse_mv(L, x, y, alpha, beta) for one generic layer (any block_rows x
+// block_cols, brows / bcols <= 64), in the reference's exact arithmetic
+// (bsr.hpp:50-73): y_r = (beta == 0 ? 0 : beta y_r), then for every block in
+// col_idx order and every column j, y_r += col_j * (alpha x_j) -- unfused
+// multiply and add, so the result is bitwise the reference's.  Warp per block
+// row, lane per row pair; the phase API's instance, not the mat-vec's.
+__global__ void __launch_bounds__(kThreads) k_bsr_exact(const double* __restrict__ val, int64_t stride, int ld,
+                                                        int br, int bc, const int32_t* __restrict__ rp,
+                                                        const int32_t* __restrict__ ci, int64_t rows,
+                                                        const double* __restrict__ x, double* __restrict__ y,
+                                                        double alpha, double beta) {
+  const int lane = lane_id();
+  for (int64_t r = warp_global(); r < rows; r += warp_count()) {
+    double* yr = y + r * br;
+    double acc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      acc[h] = (i < br && beta != 0.0) ? __dmul_rn(beta, yr[i]) : 0.0;
+    }
+    for (int b = rp[r]; b < rp[r + 1]; ++b) {
+      const double* blk = val + int64_t(b) * stride;
+      const double* xs = x + int64_t(ci[b]) * bc;
+      for (int j = 0; j < bc; ++j) {
+        const double xv = __dmul_rn(alpha, __ldg(xs + j));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h;
+          if (i < br) acc[h] = __dadd_rn(acc[h], __dmul_rn(blk[i + int64_t(j) * ld], xv));
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (lane + 32 * h < br) yr[lane + 32 * h] = acc[h];
+  }
+}
+
 __global__ void k_gather(const int32_t* __restrict__ perm, const double* __restrict__ x,
                          double* __restrict__ xc, int64_t n) {
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n;
@@ -629,6 +667,13 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
   d.bc = A.dense.bc;
   d.ld = std::max(2, A.dense.ld);
   k_bsr<<<warp_grid(nwork), kThreads, 0, s>>>(T, work, nwork);
+  H2B_CUDA(cudaGetLastError());
+}
+
+void launch_bsr_exact(const Layer& L, const double* x, double* y, double alpha, double beta, cudaStream_t s) {
+  if (L.rows == 0 || L.br == 0) return;
+  k_bsr_exact<<<warp_grid(L.rows), kThreads, 0, s>>>(L.val, L.block_stride(), std::max(1, L.ld), L.br, L.bc, L.rp,
+                                                     L.ci, L.rows, x, y, alpha, beta);
   H2B_CUDA(cudaGetLastError());
 }
 

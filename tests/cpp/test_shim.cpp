@@ -37,12 +37,13 @@ H2Matrix<double> kernel_matrix(int dim, index_t n, int order) {
 }
 
 double rel(const std::vector<double>& a, const std::vector<double>& b) {
+  if (a.size() != b.size()) return 1e300;
   double num = 0, den = 0;
   for (size_t i = 0; i < a.size(); ++i) {
     num += (a[i] - b[i]) * (a[i] - b[i]);
     den += b[i] * b[i];
   }
-  return std::sqrt(num / den);
+  return den > 0 ? std::sqrt(num / den) : std::sqrt(num);  // (zero reference: absolute)
 }
 
 std::vector<double> rnd(index_t n, unsigned seed) {
@@ -220,6 +221,144 @@ void nonsymmetric_orthogonalize() {
   }
 }
 
+// The reference's phase API on its own component types, shim
+// against reference, phase by phase on the same inputs.
+std::vector<double> flatv(const LevelVectors<double>& v) {
+  std::vector<double> f;
+  for (const auto& p : v.pool) f.insert(f.end(), p.begin(), p.end());
+  return f;
+}
+// per-node R^T R (level l, k x k blocks), concatenated
+std::vector<double> gram(const std::vector<double>& pool, index_t nodes, int rows, int cols) {
+  std::vector<double> g(size_t(nodes) * cols * cols, 0.0);
+  for (index_t b = 0; b < nodes; ++b) {
+    const double* R = pool.data() + size_t(b) * rows * cols;
+    for (int j = 0; j < cols; ++j)
+      for (int i = 0; i < cols; ++i) {
+        double acc = 0;
+        for (int s = 0; s < rows; ++s) acc += R[s + size_t(i) * rows] * R[s + size_t(j) * rows];
+        g[size_t(b) * cols * cols + i + size_t(j) * cols] = acc;
+      }
+  }
+  return g;
+}
+
+void component_phases_match_reference() {
+  for (auto [dim, n, order, eps] : {std::tuple{2, 4096, 8, 1e-7}, std::tuple{3, 4096, 4, 1e-6}}) {
+    H2Matrix<double> G = kernel_matrix(dim, n, order);
+    H2Matrix<double> R = G;
+    const int q = G.depth();
+    const auto xc = rnd(n, 5);
+    // upsweep / tree_multiply / downsweep (hmv.hpp:79-157)
+    LevelVectors<double> xg, xr, yg, yr;
+    xg.resize(G.row_basis);
+    xr.resize(R.row_basis);
+    h2kit_b200::upsweep(G.row_basis, xc.data(), n, xg);
+    h2kit::upsweep(R.row_basis, xc.data(), n, xr);
+    CHECK(rel(flatv(xg), flatv(xr)) <= 1e-13);
+    yg.resize(G.row_basis);
+    yr.resize(R.row_basis);
+    h2kit_b200::tree_multiply(G.coupling, xr, yg);
+    h2kit::tree_multiply(R.coupling, xr, yr);
+    CHECK(flatv(yg) == flatv(yr));  // block_sparse_mv in the reference's exact arithmetic
+    std::vector<double> ycg = rnd(n, 6), ycr = ycg;
+    h2kit_b200::downsweep(G.row_basis, yg, ycg.data(), n);
+    h2kit::downsweep(R.row_basis, yr, ycr.data(), n);
+    CHECK(rel(ycg, ycr) <= 1e-13);
+    CHECK(rel(flatv(yg), flatv(yr)) <= 1e-13);  // y^ updated in place like the reference
+    // block_sparse_mv (bsr.hpp:79-82) with alpha / beta: bitwise
+    std::vector<double> dg = rnd(n, 7), dr = dg;
+    h2kit_b200::block_sparse_mv(G.dense, xc.data(), dg.data(), 2.0, 0.5);
+    h2kit::block_sparse_mv(R.dense, xc.data(), dr.data(), 2.0, 0.5);
+    CHECK(dg == dr);
+    // orthogonalize_basis (compression.hpp:69-126)
+    const ProjectionTree<double> Tg = h2kit_b200::orthogonalize_basis(G.row_basis);
+    const ProjectionTree<double> Tr = h2kit::orthogonalize_basis(R.row_basis);
+    CHECK(rel(flat(Tg), flat(Tr)) <= 1e-11);
+    CHECK(Tg.rows == Tr.rows && Tg.cols == Tr.cols);
+    CHECK(rel(G.row_basis.leaf_pool, R.row_basis.leaf_pool) <= 1e-11);
+    // project_coupling (:130-169), square T
+    h2kit_b200::project_coupling(Tg, Tg, G.coupling);
+    h2kit::project_coupling(Tr, Tr, R.coupling);
+    for (int l = 0; l <= q; ++l)
+      if (!R.coupling.levels[l].empty()) CHECK(rel(G.coupling.levels[l].values, R.coupling.levels[l].values) <= 1e-11);
+    // generate_weight_tree (:213-256): R^T R per node (the c6 Gram identity),
+    // and R itself (both take diag(R) >= 0, linalg.hpp:100-113)
+    const WeightTree<double> Wg = h2kit_b200::generate_weight_tree(G.row_basis, G.coupling);
+    const WeightTree<double> Wr = h2kit::generate_weight_tree(R.row_basis, R.coupling);
+    CHECK(Wg.dim == Wr.dim);
+    for (int l = 1; l <= q; ++l) {
+      const int k = Wr.dim[l];
+      if (k == 0) continue;
+      CHECK(rel(gram(Wg.pool[l], index_t(1) << l, k, k), gram(Wr.pool[l], index_t(1) << l, k, k)) <= 1e-11);
+      CHECK(rel(Wg.pool[l], Wr.pool[l]) <= 1e-9);
+    }
+    // truncate_basis (:267-420): ranks identical, energies, and Tout up to the
+    // singular vectors' signs (T^T T per node)
+    ProjectionTree<double> Ug, Ur;
+    const TruncationResult tg = h2kit_b200::truncate_basis(G.row_basis, Wg, eps, Ug);
+    const TruncationResult tr = h2kit::truncate_basis(R.row_basis, Wr, eps, Ur);
+    CHECK(tg.new_ranks == tr.new_ranks);
+    CHECK(G.row_basis.ranks == R.row_basis.ranks);
+    double eg = 0, er = 0;
+    for (int l = 0; l <= q; ++l) {
+      eg += tg.discarded_energy[l];
+      er += tr.discarded_energy[l];
+      CHECK(std::abs(tg.discarded_energy[l] - tr.discarded_energy[l]) <= 1e-9 * er + 1e-30);
+    }
+    CHECK(std::abs(eg - er) <= 1e-9 * er);
+    CHECK(Ug.rows == Ur.rows && Ug.cols == Ur.cols);
+    for (int l = 0; l <= q; ++l) {
+      if (Ur.rows[l] == 0) continue;
+      CHECK(rel(gram(Ug.pool[l], index_t(1) << l, Ur.rows[l], Ur.cols[l]),
+                gram(Ur.pool[l], index_t(1) << l, Ur.rows[l], Ur.cols[l])) <= 1e-8);
+    }
+    // project with the rectangular T, then the compressed operators agree
+    h2kit_b200::project_coupling(Ug, Ug, G.coupling);
+    h2kit::project_coupling(Ur, Ur, R.coupling);
+    for (int l = 0; l <= q; ++l) {
+      CHECK(G.coupling.levels[l].brows == R.coupling.levels[l].brows);
+      CHECK(G.coupling.levels[l].bcols == R.coupling.levels[l].bcols);
+    }
+    const auto x = rnd(n, 8);
+    std::vector<double> y1(n), y2(n);
+    h2kit::hmv(G, x.data(), y1.data());  // the refreshed host objects, on the CPU
+    h2kit::hmv(R, x.data(), y2.data());
+    CHECK(rel(y1, y2) <= 10 * eps);
+  }
+}
+
+// A 1-level, 1x1-block tree (test_compression.cpp:126-147): T_row = 2,
+// T_col = 3 turn S = 5 into 30; a rectangular projection grows the blocks.
+void scalar_and_growing_projection() {
+  BSRLayer<double> L;
+  L.block_rows = L.block_cols = 1;
+  L.brows = L.bcols = 1;
+  L.row_ptr = {0, 1};
+  L.col_idx = {0};
+  L.values = {5.0};
+  MatrixTree<double> S;
+  S.levels.push_back(L);
+  ProjectionTree<double> Tr, Tc;
+  Tr.pool = {{2.0}};
+  Tr.rows = {1};
+  Tr.cols = {1};
+  Tc.pool = {{3.0}};
+  Tc.rows = {1};
+  Tc.cols = {1};
+  h2kit_b200::project_coupling(Tr, Tc, S);
+  CHECK(S.levels[0].values.size() == 1 && std::abs(S.levels[0].values[0] - 30.0) <= 1e-15);
+  ProjectionTree<double> G2;  // 2 x 1: the block grows to 2 x 2
+  G2.pool = {{1.0, -1.0}};
+  G2.rows = {2};
+  G2.cols = {1};
+  MatrixTree<double> S2 = S, S3 = S;
+  h2kit_b200::project_coupling(G2, G2, S2);
+  h2kit::project_coupling(G2, G2, S3);
+  CHECK(S2.levels[0].brows == 2 && S2.levels[0].bcols == 2);
+  CHECK(S2.levels[0].values == S3.levels[0].values);
+}
+
 void errors_are_invalid_argument() {
   H2Matrix<double> A = kernel_matrix(2, 1024, 8);
   bool threw = false;
@@ -244,6 +383,8 @@ int main() {
   run("orthogonalize gives orthonormal leaves", orthogonalize_orthonormal);
   run("non-symmetric hmv and compress match the reference", nonsymmetric_hmv);
   run("non-symmetric orthogonalize (row and column bases) matches the reference", nonsymmetric_orthogonalize);
+  run("component phase API (BasisTree / MatrixTree / BSRLayer) matches the reference", component_phases_match_reference);
+  run("scalar and growing projections", scalar_and_growing_projection);
   run("invalid arguments throw std::invalid_argument", errors_are_invalid_argument);
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
