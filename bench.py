@@ -14,8 +14,13 @@ e2e    = the same metric through the public API with pinned HOST x/y: each step
          copies x H2D and y D2H inside h2b_hmv (counted in the timed region).
 roofline = the dominant kernel (k_bsr: coupling + dense blocks) from per-phase
          CUDA events recorded on the launching stream during the timed region.
-cpu_baseline = the unmodified reference (oracle/_ref, OpenMP, all host cores)
-         on a bounded sample (2D n=2^18, same structure family).
+cpu_baseline = the unmodified reference (oracle/_ref, OpenMP pinned
+         close/cores, all host threads) on the SAME workload: its own
+         construct() of the n=2^22 matrix (~32 s, 77 GB host RAM) and >= 5
+         hmv steps with one HmvContext (the CLI matvec loop, h2kit.cpp:104-141),
+         in a child process so its OpenMP pinning and memory stay out of ours.
+--impl reference = the same, K timed steps after W warm-ups, plus one
+         1-thread step; same config, metric and unit as our arm.
 
 N > 1 (torchrun): the same n=2^22 matrix is partitioned by top-level subtrees
 across the ranks (1/N of the matrix per GPU) and one mat-vec exchanges x^ and
@@ -39,7 +44,7 @@ METRIC = "H2 mat-vec GB/s (% of HBM peak) & ms at n=2^22; compression GFLOP/s"
 WORKLOAD = dict(workload="H2 single-vector mat-vec, 2D exponential covariance", dim=2,
                 n=1 << 22, leaf_size=64, grid_order=8, rank=64, eta=2.0, ell=0.1,
                 perturbation=0.25, seed=1)
-CPU_SAMPLE_N = 1 << 18
+CONFIG_GOLDEN = os.path.join(ROOT, "tests", "golden", "config")
 
 
 def load_peaks():
@@ -178,8 +183,37 @@ def barrier(world: int):
         dist.barrier()
 
 
-def cpu_reference_sample(steps: int | None = None, budget_s: float = 20.0):
-    """The unmodified reference hmv on the host cores (bounded sample)."""
+def host_cpu_info():
+    """CPU model / family / cores / RAM of this host (the CPU baseline's machine)."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                k, _, v = ln.partition(":")
+                k = k.strip()
+                if k in ("model name", "cpu family", "model", "stepping") and k not in info:
+                    info[k] = v.strip()
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    info["mem_total_gb"] = round(int(ln.split()[1]) / 2 ** 20, 1)
+                    break
+    except OSError:
+        pass
+    return info
+
+
+def pin_openmp():
+    """OMP_PROC_BIND=close OMP_PLACES=cores (unpinned reference runs
+    vary 10-100x); must be set before libgomp is loaded."""
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+
+
+def cpu_reference_sample(cfg, steps: int = 5, warmup: int = 1, one_thread: bool = False):
+    """The unmodified reference on the full workload: construct() of the same
+    matrix, then `steps` timed hmv calls with one HmvContext (ref_hmv_reps:
+    the CLI matvec loop) after `warmup`, all host threads, OpenMP pinned."""
     import numpy as np
 
     import oracle
@@ -187,28 +221,73 @@ def cpu_reference_sample(steps: int | None = None, budget_s: float = 20.0):
     be = oracle.best()
     cores = os.cpu_count() or 1
     be.set_threads(cores)
+    n = cfg["n"]
     t0 = time.time()
-    A = be.construct(2, CPU_SAMPLE_N, grid_order=8)
+    A = be.construct(cfg["dim"], n, leaf_size=cfg["leaf_size"], grid_order=cfg["grid_order"], eta=cfg["eta"],
+                     ell=cfg["ell"], perturbation=cfg["perturbation"], seed=cfg["seed"])
     build_s = time.time() - t0
-    x = be.random_vector(CPU_SAMPLE_N, 1)
-    A.hmv(x)  # warm-up
+    x = be.random_vector(n, 1)
+    y = np.zeros_like(x)
     fp = A.footprint()
+
+    def step():
+        if kind == "reference":
+            be.check(be.lib.ref_hmv_reps(A.h, x.ctypes.data, y.ctypes.data, 1))
+        else:
+            A.hmv(x)
+
+    for _ in range(max(0, warmup)):
+        step()
     times = []
-    t_all = time.time()
-    while True:
+    for _ in range(max(1, steps)):
         t = time.perf_counter()
-        A.hmv(x)
+        step()
         times.append(time.perf_counter() - t)
-        if steps is not None and len(times) >= steps:
-            break
-        if steps is None and (time.time() - t_all > budget_s or len(times) >= 200):
-            break
     mean = sum(times) / len(times)
-    return {"value": fp / mean / 1e9, "unit": "GB/s", "cores": be.max_threads(), "kind": kind,
-            "ms_per_step": mean * 1e3,
-            "sample": f"reference hmv (OpenMP, {be.max_threads()} threads) on 2D n=2^18 k=64 "
-                      f"({fp / 1e9:.3f} GB footprint), {len(times)} reps after 1 warm-up; "
-                      f"host construct {build_s:.1f} s"}
+    out = {"value": fp / mean / 1e9, "unit": "GB/s", "cores": be.max_threads(), "kind": kind,
+           "ms_per_step": mean * 1e3, "ms_min": min(times) * 1e3, "reps": len(times),
+           "footprint_bytes": fp, "construct_s": round(build_s, 1), "host": host_cpu_info(),
+           "omp": {k: os.environ.get(k) for k in ("OMP_PROC_BIND", "OMP_PLACES")},
+           "sample": f"the full workload: reference construct() of the 2D n=2^{n.bit_length() - 1} k=64 matrix "
+                     f"({fp / 1e9:.2f} GB) + {len(times)} timed hmv steps (one HmvContext) after {warmup} "
+                     f"warm-up, OpenMP {be.max_threads()} threads pinned close/cores"}
+    if one_thread and kind == "reference":
+        be.set_threads(1)
+        t = time.perf_counter()
+        step()
+        dt = time.perf_counter() - t
+        be.set_threads(cores)
+        out["one_thread"] = {"ms_per_step": round(dt * 1e3, 1), "value": round(fp / dt / 1e9, 3), "reps": 1}
+    return out
+
+
+def cpu_baseline_subprocess(cfg, timeout_s: float = 900.0):
+    """cpu_reference_sample in a child process (its OpenMP pinning and the
+    77 GB host matrix stay out of the GPU process)."""
+    env = dict(os.environ)
+    env.setdefault("OMP_PROC_BIND", "close")
+    env.setdefault("OMP_PLACES", "cores")
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-json", "--n", str(cfg["n"])],
+                       capture_output=True, text=True, timeout=timeout_s, env=env)
+    if r.returncode != 0:
+        raise RuntimeError((r.stderr or r.stdout).strip().splitlines()[-1] if (r.stderr or r.stdout) else "failed")
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def recorded_reference_compress():
+    """The reference's compress() of C3 on this pool's GPU host (16 threads,
+    pinned), recorded by tests/golden/make_config_golden.py (136.98 s; the
+    parity goldens come from the same run)."""
+    try:
+        with open(os.path.join(CONFIG_GOLDEN, "C3.json")) as f:
+            d = json.load(f)
+        c = d["compress"]
+        return {"wall_ms": round(1e3 * c["wall_s"], 0), "model_flops": c["total_flops"],
+                "model_gflops": round(c["model_GFLOPs"], 2), "threads": d["threads"], "kind": "reference",
+                "host": d["host"], "source": "tests/golden/config/C3.json (recorded by "
+                "tests/golden/make_config_golden.py on the GPU host; not re-run by bench.py)"}
+    except Exception:  # noqa: BLE001
+        return None
 
 
 FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 measured on this pool's B200 (tools/fp64_peak.cu: 37.07); DFMA 36.4
@@ -319,20 +398,25 @@ def multi16_run(A, torch, steps):
 
 
 def run_reference(args):
-    world, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    """--impl reference: the unmodified reference (oracle/_ref) on the host
+    cores, same workload / metric / unit as our arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cb = cpu_reference_sample(steps=max(1, args.steps))
+    pin_openmp()
+    cfg = dict(WORKLOAD, n=args.n)
+    cb = cpu_reference_sample(cfg, steps=max(1, args.steps), warmup=args.warmup, one_thread=True)
     line = {"metric": METRIC, "value": round(cb["value"], 3), "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cb["ms_per_step"], 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": dict(WORKLOAD, n=CPU_SAMPLE_N,
-                           note="CPU sample of the n=2^22 workload (77 GB does not fit a bounded "
-                                "CPU run); same structure family, same metric"),
+            "config": dict(cfg, parallelism=f"OpenMP {cb['cores']} threads (host)", same_config=True,
+                           construct_s=cb["construct_s"]),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "host": cb["host"], "omp": cb["omp"], "one_thread": cb.get("one_thread"),
             "e2e": {"value": round(cb["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "compression_recorded": recorded_reference_compress()}
     emit(line)
 
 
@@ -467,7 +551,12 @@ def main():
     ap.add_argument("--compress-reps", type=int, default=3)
     ap.add_argument("--dist", action="store_true",
                     help="use the subtree-partitioned path even at N=1 (testing)")
+    ap.add_argument("--cpu-baseline-json", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_baseline_json:  # child process of cpu_baseline_subprocess
+        pin_openmp()
+        print(json.dumps(cpu_reference_sample(dict(WORKLOAD, n=args.n))))
+        return
     if args.impl == "reference":
         return run_reference(args)
     args.warmup = max(3, args.warmup)
@@ -579,11 +668,15 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_sample(budget_s=15.0)
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cb = cpu_baseline_subprocess(cfg)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu.update(ms_per_step=round(cb["ms_per_step"], 1), host=cb["host"], omp=cb["omp"],
+                       same_config=True)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
+    if comp is not None:
+        comp["cpu_baseline"] = recorded_reference_compress()
     line = {
         "metric": METRIC,
         "value": round(value, 2),
