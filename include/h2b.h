@@ -261,6 +261,33 @@ H2B_API h2b_status h2b_workspace(h2b_matrix* A, int which, void** ptr, int64_t* 
 H2B_API h2b_status h2b_part_upsweep(h2b_matrix* A, const double* x, void* stream);
 H2B_API h2b_status h2b_part_finish(h2b_matrix* A, double* y_slice, void* stream);
 
+/* ---- one-call partitioned mat-vec, driven from the host through a
+ * stream-ordered device communicator (NCCL) ----
+ * allgather: enqueue on `stream` the in-place all-gather of buf, which holds
+ * nparts slices of `count` doubles, slice `part` this rank's; with NCCL:
+ *   ncclAllGather(buf + part * count, buf, count, ncclDouble, comm, (cudaStream_t)stream)
+ * Return 0 once enqueued (no host synchronisation is needed). */
+typedef struct h2b_dcomm {
+  void* ctx;
+  int (*allgather)(void* ctx, double* buf, int64_t count, void* stream);
+} h2b_dcomm;
+typedef enum {
+  H2B_Y_REPLICATED = 0, /* y complete on every rank (cluster-order slices all-gathered, then scattered) */
+  H2B_Y_OWNED = 1       /* each rank writes only its own rows y[perm[t]], t in its cluster-order range */
+} h2b_y_mode;
+/* y <- alpha A x + beta y on every rank of a partitioned matrix (x: full,
+ * original order, device; y device).  Per call: one x^ all-gather (every level
+ * >= s packed into one buffer) and, for H2B_Y_REPLICATED, one y all-gather;
+ * comm may be NULL for a single partition.  Every kernel is in libh2b.so
+ * (pack / unpack, the owner-row scatter); nothing is computed on the host. */
+H2B_API h2b_status h2b_part_hmv(h2b_matrix* A, const double* x, double* y, double alpha, double beta, int y_mode,
+                                const h2b_dcomm* comm, void* stream);
+/* nvec right-hand sides (X, Y: n x nvec column-major, device), 16 per pass on
+ * the FP64 tensor cores; one x^ all-gather (and one y all-gather) per pass. */
+H2B_API h2b_status h2b_part_hmv_multi(h2b_matrix* A, int nvec, const double* X, int64_t ldx, double* Y,
+                                      int64_t ldy, double alpha, double beta, int y_mode, const h2b_dcomm* comm,
+                                      void* stream);
+
 /* ---- subtree-partitioned compression (compression.hpp:466-551 on 2^s GPUs) ----
  * Every rank calls h2b_part_compress on its partition handle with the same eps;
  * the library runs the phases on the rank's subtree and calls back into the

@@ -95,6 +95,17 @@ class Comm(C.Structure):
                 ("allreduce_max_i32", ALLREDUCE_I32_FN), ("allreduce_sum_f64", ALLREDUCE_F64_FN)]
 
 
+# h2b_dcomm (include/h2b.h): stream-ordered device all-gather of the
+# partitioned mat-vec (h2b_part_hmv / h2b_part_hmv_multi)
+DALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class DComm(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", DALLGATHER_FN)]
+
+
+Y_REPLICATED, Y_OWNED = 0, 1
+
 # name -> (restype, argtypes)
 _SIGS = {
     "h2b_last_error": (C.c_char_p, []),
@@ -129,6 +140,10 @@ _SIGS = {
     "h2b_workspace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "h2b_part_upsweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "h2b_part_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "h2b_part_hmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int,
+                               C.POINTER(DComm), C.c_void_p]),
+    "h2b_part_hmv_multi": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                     C.c_double, C.c_double, C.c_int, C.POINTER(DComm), C.c_void_p]),
     "h2b_validate_sampled": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double,
                                        C.c_uint64, C.POINTER(C.c_double)]),
     "h2b_set_phase_timing": (C.c_int, [C.c_void_p, C.c_int]),

@@ -161,7 +161,7 @@ uint64_t Matrix::device_bytes() const {
   if (work0)
     b += work0->xc.bytes() + work0->yc.bytes() + work0->xhat.bytes() + work0->yhat.bytes() + work0->xs.bytes() +
          work0->ys.bytes() + work0->xc16.bytes() + work0->yc16.bytes() + work0->xh16.bytes() +
-         work0->yh16.bytes() + work0->flag.bytes();
+         work0->yh16.bytes() + work0->flag.bytes() + work0->xg.bytes() + work0->yg.bytes();
   return b;
 }
 
@@ -179,6 +179,8 @@ void ensure_work(Matrix& A, Work& w) {
   w.ys.release();
   w.xh16.release();
   w.yh16.release();
+  w.xg.release();
+  w.yg.release();
   if (!w.done) H2B_CUDA(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
   w.owner = &A;
   w.layout = A.layout_version;
@@ -1097,6 +1099,106 @@ h2b_status h2b_part_finish(h2b_matrix* Ah, double* y_slice, void* stream) {
     if (A.q >= 1) launch_down_fused(w, A, w.yhat.p, s, true);  // replicated top + own subtree
     launch_down_leaf(A, w.yhat.p, w.yc.p, y_slice, 1.0, 0.0, false, s);
     if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
+  });
+}
+
+namespace {
+// comm->allgather of nparts slices of `count` doubles in buf, stream-ordered.
+void dcomm_allgather(const h2b_dcomm* comm, double* buf, int64_t count, cudaStream_t s) {
+  if (comm->allgather(comm->ctx, buf, count, s) != 0) throw Error(H2B_CUDA_ERROR, "communicator: allgather failed");
+}
+
+void require_dcomm(const Matrix& A, const h2b_dcomm* comm) {
+  require(A.symmetric, "partitioned mat-vec: symmetric matrices only");
+  require(A.part_s == 0 || (comm && comm->allgather), "partitioned mat-vec: null communicator");
+}
+}  // namespace
+
+h2b_status h2b_part_hmv(h2b_matrix* Ah, const double* x, double* y, double alpha, double beta, int y_mode,
+                        const h2b_dcomm* comm, void* stream) {
+  return guarded([&] {
+    require(Ah && x && y, "null argument");
+    require(y_mode == H2B_Y_REPLICATED || y_mode == H2B_Y_OWNED, "h2b_part_hmv: bad y_mode");
+    Matrix& A = *Ah;
+    require_dcomm(A, comm);
+    DeviceGuard g(A.device);
+    require(resolve_device(H2B_PTR_AUTO, x) && resolve_device(H2B_PTR_AUTO, y), "h2b_part_hmv: device vectors");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    const int nparts = 1 << A.part_s;
+    Work& w = default_work(A);
+    WorkUse u(w, s);
+    ensure_work(A, w);
+    cudaEvent_t* ev = timing_slots(A);  // upsweep + exchange | coupling + dense | downsweep + y
+    if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
+    sweep_begin(w, A, s);
+    launch_up_leaf(A, x, w.xc.p, w.xhat.p, s);
+    if (A.part_s > 0) launch_gather(A.perm.p, x, w.xc.p, A.n, s);  // dense blocks read remote columns
+    if (A.q > A.part_s) launch_up_fused(w, A, w.xhat.p, s, A.q, A.part_s + 1, true);
+    if (nparts > 1) {  // one all-gather of every level >= s
+      const int64_t cnt = part_exchange_count(A, 1);
+      if (w.xg.n < size_t(cnt) * nparts) w.xg.alloc(size_t(cnt) * nparts);
+      launch_pack_xhat(A, 1, w.xhat.p, w.xg.p, s);
+      dcomm_allgather(comm, w.xg.p, cnt, s);
+      launch_unpack_xhat(A, 1, w.xg.p, w.xhat.p, s);
+    }
+    if (A.part_s >= 1) launch_up_fused(w, A, w.xhat.p, s, A.part_s, 1, false);  // replicated top
+    if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
+    launch_bsr(A, A.work.p, A.nwork, w.xc.p, w.yc.p, w.xhat.p, w.yhat.p, s);
+    if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
+    if (A.q >= 1) launch_down_fused(w, A, w.yhat.p, s, true);
+    if (y_mode == H2B_Y_OWNED || nparts == 1) {
+      launch_down_leaf(A, w.yhat.p, w.yc.p, y, alpha, beta, true, s);  // owned rows, original order
+    } else {
+      const int64_t slice = A.n / nparts;
+      if (w.yg.n < size_t(A.n)) w.yg.alloc(A.n);
+      launch_down_leaf(A, w.yhat.p, w.yc.p, w.yg.p + A.part_g * slice, 1.0, 0.0, false, s);
+      dcomm_allgather(comm, w.yg.p, slice, s);
+      launch_scatter(A.perm.p, w.yg.p, y, A.n, alpha, beta, s);
+    }
+    if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
+  });
+}
+
+h2b_status h2b_part_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                              double alpha, double beta, int y_mode, const h2b_dcomm* comm, void* stream) {
+  return guarded([&] {
+    require(Ah, "null matrix");
+    require(y_mode == H2B_Y_REPLICATED || y_mode == H2B_Y_OWNED, "h2b_part_hmv_multi: bad y_mode");
+    Matrix& A = *Ah;
+    require_dcomm(A, comm);
+    require(nvec >= 0 && ldx >= A.n && ldy >= A.n, "hmv_multi: bad leading dimension");
+    require(X && Y, "hmv_multi: null vector");
+    if (nvec == 0) return;
+    DeviceGuard g(A.device);
+    require(resolve_device(H2B_PTR_AUTO, X) && resolve_device(H2B_PTR_AUTO, Y), "h2b_part_hmv_multi: device vectors");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    const int nparts = 1 << A.part_s;
+    constexpr int NV = 16;
+    Work& w = default_work(A);
+    WorkUse u(w, s);
+    ensure_work(A, w);
+    for (int v0 = 0; v0 < nvec; v0 += NV) {
+      const int nv = std::min(NV, nvec - v0);
+      const double* Xv = X + v0 * ldx;
+      double* Yv = Y + v0 * ldy;
+      part_mv_upsweep(A, w, Xv, ldx, nv, s);
+      if (nparts > 1) {
+        const int64_t cnt = part_exchange_count(A, NV);
+        if (w.xg.n < size_t(cnt) * nparts) w.xg.alloc(size_t(cnt) * nparts);
+        launch_pack_xhat(A, NV, w.xh16.p, w.xg.p, s);
+        dcomm_allgather(comm, w.xg.p, cnt, s);
+        launch_unpack_xhat(A, NV, w.xg.p, w.xh16.p, s);
+      }
+      if (y_mode == H2B_Y_OWNED || nparts == 1) {
+        part_mv_finish(A, w, Yv, ldy, nv, alpha, beta, nullptr, s);
+      } else {
+        const int64_t slice = int64_t(A.n / nparts) * NV;
+        if (w.yg.n < size_t(A.n) * NV) w.yg.alloc(size_t(A.n) * NV);
+        part_mv_finish(A, w, Yv, ldy, nv, alpha, beta, w.yg.p + A.part_g * slice, s);
+        dcomm_allgather(comm, w.yg.p, slice, s);
+        launch_scatter_mv(A.perm.p, w.yg.p, A.n, nv, Yv, ldy, alpha, beta, s);
+      }
+    }
   });
 }
 

@@ -133,6 +133,7 @@ struct Work {
   DevBuf<double> xhat, yhat;        // x^ (column-basis ranks), y^ (row-basis ranks), level-concatenated
   DevBuf<double> xs, ys;            // device staging of host x / y
   DevBuf<double> xc16, yc16, xh16, yh16;  // 16-vector panels (k_hmv_mv.cu), lazily allocated
+  DevBuf<double> xg, yg;            // partitioned mat-vec exchange buffers (x^ slices, y slices), lazily allocated
   // Fused dataflow sweeps (launch_up_fused / launch_down_fused): per-node
   // completion flags (epoch-valued, never reset) and the work tickets.
   DevBuf<uint32_t> flag;
@@ -279,6 +280,24 @@ struct WorkUse {
 // 16-vector FP64-MMA mat-vec, device pointers (k_hmv_mv.cu).
 void hmv_multi_device(Matrix& A, Work& w, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
                       double alpha, double beta, cudaStream_t s);
+// Partitioned 16-vector pass (k_hmv_mv.cu): owned leaves + levels > part_s
+// into w.xh16; then (after the x^ exchange) the replicated top, owned rows,
+// downsweep and leaf expansion into Y (yslice null: owned rows of Y, original
+// order, alpha / beta applied) or the cluster-order vector-minor slice.
+void part_mv_upsweep(Matrix& A, Work& w, const double* X, int64_t ldx, int nv, cudaStream_t s);
+void part_mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha, double beta, double* yslice,
+                    cudaStream_t s);
+// Y[perm[t] + v ldy] = alpha yc[t * 16 + v] + beta Y[...], t < n, v < nv.
+void launch_scatter_mv(const int32_t* perm, const double* yc, int64_t n, int nv, double* Y, int64_t ldy,
+                       double alpha, double beta, cudaStream_t s);
+
+// ---- x^ exchange of the partitioned mat-vec (part_hmv.cu) ----
+// Doubles per partition slice (x^ entries of width `width`: 1 or 16).
+int64_t part_exchange_count(const Matrix& A, int width);
+// slice part_g of buf <- this partition's x^ runs at levels >= part_s
+void launch_pack_xhat(const Matrix& A, int width, const double* pool, double* buf, cudaStream_t s);
+// x^ runs of every other partition <- their slices of buf
+void launch_unpack_xhat(const Matrix& A, int width, const double* buf, double* pool, cudaStream_t s);
 
 // Build the fused BSR work list for the given layers (rows sorted by
 // decreasing block count so the round-robin warp assignment is balanced).

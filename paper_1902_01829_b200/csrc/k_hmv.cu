@@ -12,6 +12,7 @@
 //                  scatter y[perm[t]] = alpha yc[t] + beta y[perm[t]] (hmv.hpp:184-187)
 // All matrix bytes are read exactly once per phase with streaming
 // (evict-first) 128-bit loads; node vectors stay L2-resident.
+#include "dataflow.cuh"
 #include "h2b_internal.hpp"
 
 #include <algorithm>
@@ -249,33 +250,12 @@ struct SweepTable {
   int q;  // up: the deepest child level (its x^ is input); down: the top parent level (its y^ is input)
 };
 
-__device__ __forceinline__ int64_t node_id(int level, int64_t i) { return (int64_t(1) << level) - 1 + i; }
-
-__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t want) {
-  if (lane_id() == 0) {
-    uint32_t v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      if (v >= want) break;
-      __nanosleep(64);
-    }
-  }
-  __syncwarp();
-}
-
-__device__ __forceinline__ void set_flag(uint32_t* f, uint32_t v) {
-  __syncwarp();
-  if (lane_id() == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
-  }
-}
+using df::node_id;
+using df::set_flag;
+using df::wait_flag;
 
 __device__ __forceinline__ int claim(unsigned long long* ticket, unsigned long long base) {
-  unsigned long long t = 0;
-  if (lane_id() == 0) t = atomicAdd(ticket, 1ull);
-  t = __shfl_sync(kFull, t, 0);
-  return int(t - base);
+  return int(df::claim(ticket) - int64_t(base));
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant__ SweepTable S,

@@ -8,7 +8,19 @@
 // Node vectors and cluster-order vectors are stored "vector-minor":
 // element (row t, vector v) at t * 16 + v, so an 8 x 4 / 4 x 8 fragment of a
 // panel is four 64-byte segments.  Matrix operands are streamed from HBM
-// straight into the A fragments with evict-first loads.
+// straight into the A fragments with evict-first 128-bit loads:
+//   * transposed products (V^T x, F^T x^) pair their k-steps: lane k-slot fk
+//     of a pair of k-steps covers the two ADJACENT contraction rows 2j, 2j+1
+//     (j = j0 + fk), so one 16-byte load feeds two DMMAs and a block column is
+//     read in 64-byte pieces (the 8-byte form fetched every sector twice);
+//   * untransposed products (E y^, U y^, S x^) pair their row tiles: tiles
+//     2z / 2z+1 hold the rows 16z + 2fr / 16z + 2fr + 1, one 16-byte load per
+//     lane and k-step feeds both.
+// Phases: k_up_leaf_mv (perm gather fused, coalesced through shared memory),
+// k_up_fused_mv (levels q..1, one dataflow launch), k_bsr_mv (dense + every
+// coupling level), k_down_fused_mv (levels 1..q, one dataflow launch),
+// k_down_leaf_mv (alpha/beta scatter fused, coalesced through shared memory).
+#include "dataflow.cuh"
 #include "h2b_internal.hpp"
 
 #include <algorithm>
@@ -17,7 +29,8 @@ namespace h2b {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int NV = 16;  // vectors per pass (2 DMMA column tiles)
+constexpr int NV = 16;        // vectors per pass (2 DMMA column tiles)
+constexpr int kLeafWarps = 4; // leaf kernels: 4 warps x 8 KB shared panel
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int64_t warp_global() {
@@ -29,6 +42,21 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+// Streaming 16-byte matrix loads.  POL: 0 evict-first, 1 non-coherent,
+// 2 non-coherent + L2::256B prefetch, 3 evict-first + L2::256B prefetch
+// (measured: see hmv_multi_device).
+template <int POL = 0>
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  if (POL == 0) return __ldcs(reinterpret_cast<const double2*>(p));
+  if (POL == 1) return __ldg(reinterpret_cast<const double2*>(p));
+  double2 v;
+  if (POL == 2)
+    asm("ld.global.nc.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  else
+    asm("ld.global.cs.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
 }
 
 struct Acc {
@@ -43,7 +71,8 @@ struct Acc {
 
 // acc (M x 16) += op(A) (M x K) * B (K x 16), B vector-minor (B[p * 16 + v]).
 // op(A)(i, p) = TA ? A[p + i * lda] : A[i + p * lda]; A streamed (evict-first).
-template <bool TA, int UNROLL = 2>
+// Natural tile layout (row tile x = rows 8x .. 8x+7).  Used by k_bsr_mv.
+template <bool TA, int UNROLL = 2, int POL = 0>
 __device__ __forceinline__ void mma_panel(Acc& acc, const double* __restrict__ A, int lda, int M,
                                           int K, const double* __restrict__ B) {
   const int lane = lane_id();
@@ -59,7 +88,17 @@ __device__ __forceinline__ void mma_panel(Acc& acc, const double* __restrict__ A
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
       const int i = 8 * x + fr;
-      a[x] = (pk && i < M) ? __ldcs(TA ? A + p + int64_t(i) * lda : A + i + int64_t(p) * lda) : 0.0;
+      const double* pa = TA ? A + p + int64_t(i) * lda : A + i + int64_t(p) * lda;
+      double av = 0.0;
+      if (pk && i < M) {
+        if (POL == 0)
+          av = __ldcs(pa);
+        else if (POL == 1)
+          av = __ldg(pa);
+        else
+          asm("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(av) : "l"(pa));
+      }
+      a[x] = av;
     }
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
@@ -71,7 +110,7 @@ __device__ __forceinline__ void mma_panel(Acc& acc, const double* __restrict__ A
   }
 }
 
-// out (M x 16, vector-minor) = acc (+ out when add).
+// out (M x 16, vector-minor) = acc (+ out when add); natural tile layout.
 __device__ __forceinline__ void store_panel(const Acc& acc, double* __restrict__ out, int M, bool add) {
   const int lane = lane_id();
   const int fr = lane >> 2, fc = 2 * (lane & 3);
@@ -84,7 +123,7 @@ __device__ __forceinline__ void store_panel(const Acc& acc, double* __restrict__
       double2* o = reinterpret_cast<double2*>(out + i * NV + 8 * y + fc);
       double2 v = make_double2(acc.c[x][y][0], acc.c[x][y][1]);
       if (add) {
-        const double2 old = *o;
+        const double2 old = __ldcg(o);
         v.x += old.x;
         v.y += old.y;
       }
@@ -93,41 +132,244 @@ __device__ __forceinline__ void store_panel(const Acc& acc, double* __restrict__
   }
 }
 
-// xc16[t][v] = X[perm[t] + v * ldx] (v < nv; zero padding above).
-__global__ void k_gather_mv(const int32_t* __restrict__ perm, const double* __restrict__ X,
-                            int64_t ldx, int nv, int64_t n, double* __restrict__ xc) {
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * NV;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = e / NV;
-    const int v = int(e - t * NV);
-    xc[e] = v < nv ? X[perm[t] + v * ldx] : 0.0;
+// ---- transposed products with paired k-steps ------------------------------
+// acc (M x 16) += A^T (M x K) * B (K x 16) with A column-major (K x M, lda
+// even, rows K..lda-1 may be padding), i.e. acc(i, :) += sum_p A[p + i lda] B(p, :).
+// Lane k-slot fk of pair-step j0 takes the contraction rows 2j, 2j+1
+// (j = j0 + fk): A by one 16-byte load per row tile, B by the callback
+// bpair(j, y) -> (B(2j, 8y + fr), B(2j + 1, 8y + fr)), which must return 0
+// for rows >= K.  UNROLL pair-steps (8 contraction rows each) in flight.
+template <int UNROLL, int POL, class BPair>
+__device__ __forceinline__ void mma_T_pairs(Acc& acc, const double* __restrict__ A, int lda, int M, int K,
+                                            BPair bpair) {
+  const int lane = lane_id();
+  const int fr = lane >> 2, fk = lane & 3;
+  const int np = (K + 1) >> 1;
+#pragma unroll UNROLL
+  for (int j0 = 0; j0 < np; j0 += 4) {
+    const int j = j0 + fk;
+    const bool ok = j < np;
+    const bool hi = 2 * j + 1 < K;
+    double2 b[2];
+#pragma unroll
+    for (int y = 0; y < 2; ++y) b[y] = bpair(j, y, ok);
+    double2 a[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const int i = 8 * x + fr;
+      a[x] = (ok && i < M) ? ld_stream2<POL>(A + 2 * j + int64_t(i) * lda) : make_double2(0.0, 0.0);
+      if (!hi) a[x].y = 0.0;  // padding row of an odd K
+    }
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      if (8 * x < M) {  // warp-uniform
+        dmma(acc.c[x][0][0], acc.c[x][0][1], a[x].x, b[0].x);
+        dmma(acc.c[x][1][0], acc.c[x][1][1], a[x].x, b[1].x);
+        dmma(acc.c[x][0][0], acc.c[x][0][1], a[x].y, b[0].y);
+        dmma(acc.c[x][1][0], acc.c[x][1][1], a[x].y, b[1].y);
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_up_leaf_mv(const double* __restrict__ leaf, int ldm,
-                                                         int m, int k, int64_t nleaves,
-                                                         const double* __restrict__ xc,
-                                                         double* __restrict__ xh) {
+// ---- untransposed products with paired row tiles -------------------------
+// acc += A (M x K, column-major, lda even >= M) * B (K x 16, vector-minor).
+// Row tile 2z holds rows 16z + 2fr, tile 2z + 1 rows 16z + 2fr + 1 (lane
+// row fr): one 16-byte load per tile pair and k-step.
+__device__ __forceinline__ int prow(int x, int fr) { return 16 * (x >> 1) + 2 * fr + (x & 1); }
+
+template <int UNROLL, int POL>
+__device__ __forceinline__ void mma_N_pairs(Acc& acc, const double* __restrict__ A, int lda, int M, int K,
+                                            const double* __restrict__ B) {
+  const int lane = lane_id();
+  const int fr = lane >> 2, fk = lane & 3;
+#pragma unroll UNROLL
+  for (int p0 = 0; p0 < K; p0 += 4) {
+    const int p = p0 + fk;
+    const bool pk = p < K;
+    double b[2];
+#pragma unroll
+    for (int y = 0; y < 2; ++y) b[y] = pk ? __ldcg(B + p * NV + 8 * y + fr) : 0.0;
+    double2 a[4];
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const int r = 16 * z + 2 * fr;
+      a[z] = (pk && r < M) ? ld_stream2<POL>(A + r + int64_t(p) * lda) : make_double2(0.0, 0.0);
+      if (r + 1 >= M) a[z].y = 0.0;  // padding row of an odd M
+    }
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      if (16 * z < M) {  // warp-uniform
+        dmma(acc.c[2 * z][0][0], acc.c[2 * z][0][1], a[z].x, b[0]);
+        dmma(acc.c[2 * z][1][0], acc.c[2 * z][1][1], a[z].x, b[1]);
+        dmma(acc.c[2 * z + 1][0][0], acc.c[2 * z + 1][0][1], a[z].y, b[0]);
+        dmma(acc.c[2 * z + 1][1][0], acc.c[2 * z + 1][1][1], a[z].y, b[1]);
+      }
+    }
+  }
+}
+
+// out (M x 16, vector-minor) = acc (+ out when add); paired-row tile layout.
+__device__ __forceinline__ void store_panel_pr(const Acc& acc, double* __restrict__ out, int M, bool add) {
+  const int lane = lane_id();
+  const int fr = lane >> 2, fc = 2 * (lane & 3);
+#pragma unroll
+  for (int x = 0; x < 8; ++x) {
+    const int i = prow(x, fr);
+    if (i >= M) continue;
+#pragma unroll
+    for (int y = 0; y < 2; ++y) {
+      double2* o = reinterpret_cast<double2*>(out + i * NV + 8 * y + fc);
+      double2 v = make_double2(acc.c[x][y][0], acc.c[x][y][1]);
+      if (add) {
+        const double2 old = __ldcg(o);
+        v.x += old.x;
+        v.y += old.y;
+      }
+      *o = v;
+    }
+  }
+}
+
+// ---- shared 64 x 16 panel of one leaf ------------------------------------
+// Pair-interleaved and swizzled: rows 2j, 2j+1 of vector v form one 16-byte
+// unit at j * 16 + (v ^ ((j & 3) << 1)).  The B fragments of mma_T_pairs read
+// 8 distinct bank slots per quarter warp; the gather below writes them so too.
+__device__ __forceinline__ int punit(int j, int v) { return j * NV + (v ^ ((j & 3) << 1)); }
+
+// Leaf i: xc16[t][v] = X[perm[t] + v ldx] (fused gather, hmv.hpp:179), then
+// x^q_i = V_i^T xc_i (hmv.hpp:86-97) for 16 vectors.
+template <int POL, int UNR>
+__global__ void __launch_bounds__(32 * kLeafWarps) k_up_leaf_mv(
+    const double* __restrict__ leaf, int ldm, int m, int k, int64_t nleaves, int64_t leaf0,
+    const int32_t* __restrict__ perm, const double* __restrict__ X, int64_t ldx, int nv, int write_xc,
+    double* __restrict__ xc, double* __restrict__ xh) {
+  __shared__ double2 panel_all[kLeafWarps][32 * NV];
+  double2* panel = panel_all[threadIdx.x >> 5];
+  const int lane = lane_id();
   const int64_t stride = int64_t(ldm) * k;
-  for (int64_t i = warp_global(); i < nleaves; i += warp_count()) {
-    Acc acc;
-    acc.zero();
-    mma_panel<true>(acc, leaf + i * stride, ldm, k, m, xc + i * m * NV);  // V^T (k x m) X (m x 16)
-    store_panel(acc, xh + i * k * NV, k, false);
+  for (int64_t il = warp_global(); il < nleaves; il += warp_count()) {
+    const int64_t i = leaf0 + il;  // global leaf; the pool holds the owned leaves only
+    const int64_t base = i * m;
+    // gather: lane L owns rows 2L, 2L + 1; the vector order is rotated by L / 4
+    // so the 16-byte smem stores of a quarter warp hit 8 distinct slots
+    const int t0 = 2 * lane, t1 = t0 + 1;
+    const int64_t o0 = t0 < m ? int64_t(__ldg(perm + base + t0)) : -1;
+    const int64_t o1 = t1 < m ? int64_t(__ldg(perm + base + t1)) : -1;
+#pragma unroll 4
+    for (int s = 0; s < NV; ++s) {
+      const int v = (s + (lane >> 2)) & (NV - 1);
+      const bool vok = v < nv;
+      const double a = (vok && o0 >= 0) ? __ldg(X + o0 + v * ldx) : 0.0;
+      const double b = (vok && o1 >= 0) ? __ldg(X + o1 + v * ldx) : 0.0;
+      panel[punit(lane, v)] = make_double2(a, b);
+    }
+    __syncwarp();
+    // xc16 rows of this leaf, coalesced 16-byte stores (unless a full gather
+    // already wrote them: partitions, whose dense blocks read remote rows)
+    const double* pd = reinterpret_cast<const double*>(panel);
+    double* xo = xc + base * NV;
+#pragma unroll 4
+    for (int s = 0; s < NV && write_xc; ++s) {
+      const int e = 2 * (s * 32 + lane);  // element (t, v) = (e / 16, e % 16), v even
+      const int t = e >> 4, v = e & (NV - 1);
+      if (t < m) {
+        const int j = t >> 1, h = t & 1;
+        *reinterpret_cast<double2*>(xo + e) =
+            make_double2(pd[2 * punit(j, v) + h], pd[2 * punit(j, v + 1) + h]);
+      }
+    }
+    if (k > 0) {
+      Acc acc;
+      acc.zero();
+      const int fr = lane >> 2;
+      mma_T_pairs<UNR, POL>(acc, leaf + il * stride, ldm, k, m, [&](int j, int y, bool ok) {
+        return ok ? panel[punit(j, 8 * y + fr)] : make_double2(0.0, 0.0);
+      });
+      store_panel(acc, xh + i * k * NV, k, false);
+    }
+    __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_up_level_mv(const double* __restrict__ F, int ldc,
-                                                          int kc, int kp, int64_t np,
-                                                          const double* __restrict__ xl,
-                                                          double* __restrict__ xp) {
-  const int64_t stride = int64_t(ldc) * kp;
-  for (int64_t p = warp_global(); p < np; p += warp_count()) {
-    Acc acc;
-    acc.zero();
-    mma_panel<true>(acc, F + (2 * p) * stride, ldc, kp, kc, xl + (2 * p) * kc * NV);
-    mma_panel<true>(acc, F + (2 * p + 1) * stride, ldc, kp, kc, xl + (2 * p + 1) * kc * NV);
-    store_panel(acc, xp + p * kp * NV, kp, false);
+// ---- fused dataflow sweeps (see dataflow.cuh) -----------------------------
+struct SweepLevelMV {
+  const double* T;  // transfers of the child level l (block (c - cbegin) * stride)
+  int64_t stride, cbegin;
+  int ldc, kc, kp, l;
+  const double* in;  // up: x^ of level l (vector-minor); down: y^ of level l - 1
+  double* out;       // up: x^ of level l - 1;             down: y^ of level l
+  int64_t n, i0;     // items (up: parents i0.., down: children i0..)
+};
+struct SweepTableMV {
+  SweepLevelMV L[kMaxLevels];
+  int64_t start[kMaxLevels + 1];
+  int nl;
+  int q;  // up: the deepest child level (input); down: the top parent level (input)
+};
+
+// x^{l-1}_p = F_2p^T x^l_2p + F_2p+1^T x^l_2p+1 (hmv.hpp:98-110), levels q..1.
+template <int POL, int UNR>
+__global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant__ SweepTableMV S,
+                                                          uint32_t* __restrict__ flag, uint32_t epoch,
+                                                          unsigned long long* __restrict__ ticket) {
+  const int fr = lane_id() >> 2;
+  const int64_t total = S.start[S.nl];
+  for (;;) {
+    const int64_t it = df::claim(ticket);
+    if (it >= total) break;
+    int e = 0;
+    while (it >= S.start[e + 1]) ++e;
+    const SweepLevelMV& L = S.L[e];
+    const int64_t p = L.i0 + (it - S.start[e]);
+    if (L.l < S.q) {
+      df::wait_flag(flag + df::node_id(L.l, 2 * p), epoch);
+      df::wait_flag(flag + df::node_id(L.l, 2 * p + 1), epoch);
+    }
+    if (L.kp > 0) {
+      Acc acc;
+      acc.zero();
+      if (L.kc > 0) {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          const double* xin = L.in + (2 * p + c) * L.kc * NV;
+          const int kc = L.kc;
+          mma_T_pairs<UNR, POL>(acc, L.T + (2 * p + c - L.cbegin) * L.stride, L.ldc, L.kp, kc,
+                                [&](int j, int y, bool ok) {
+            const int r = 2 * j;
+            const double lo = (ok && r < kc) ? __ldcg(xin + r * NV + 8 * y + fr) : 0.0;
+            const double hi = (ok && r + 1 < kc) ? __ldcg(xin + (r + 1) * NV + 8 * y + fr) : 0.0;
+            return make_double2(lo, hi);
+          });
+        }
+      }
+      store_panel(acc, L.out + p * L.kp * NV, L.kp, false);
+    }
+    df::set_flag(flag + df::node_id(L.l - 1, p), epoch);
+  }
+}
+
+// y^l_c += E_c y^{l-1}_{c/2} (hmv.hpp:136-146), levels 1..q.
+template <int POL, int UNR>
+__global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constant__ SweepTableMV S,
+                                                            uint32_t* __restrict__ flag, uint32_t epoch,
+                                                            unsigned long long* __restrict__ ticket) {
+  const int64_t total = S.start[S.nl];
+  for (;;) {
+    const int64_t it = df::claim(ticket);
+    if (it >= total) break;
+    int e = 0;
+    while (it >= S.start[e + 1]) ++e;
+    const SweepLevelMV& L = S.L[e];
+    const int64_t c = L.i0 + (it - S.start[e]);
+    if (L.l - 1 > S.q) df::wait_flag(flag + df::node_id(L.l - 1, c >> 1), epoch);
+    if (L.kc > 0 && L.kp > 0) {
+      Acc acc;
+      acc.zero();
+      mma_N_pairs<UNR, POL>(acc, L.T + (c - L.cbegin) * L.stride, L.ldc, L.kc, L.kp, L.in + (c >> 1) * L.kp * NV);
+      store_panel_pr(acc, L.out + c * L.kc * NV, L.kc, true);
+    }
+    df::set_flag(flag + df::node_id(L.l, c), epoch);
   }
 }
 
@@ -145,6 +387,7 @@ struct LayerTableMV {
 };
 
 // Y_r = sum_b B_b X_{col(b)} for every work item (row of one layer).
+template <int V>
 __global__ void __launch_bounds__(kThreads, 1) k_bsr_mv(const __grid_constant__ LayerTableMV T,
                                                      const uint32_t* __restrict__ work,
                                                      int64_t nwork) {
@@ -160,55 +403,104 @@ __global__ void __launch_bounds__(kThreads, 1) k_bsr_mv(const __grid_constant__ 
       // the whole 64-deep block unrolled: its 128 fragment loads per lane are
       // in flight together (measured at n = 2^22: 8 k-steps 19.35 ms per
       // 16 vectors, 16 k-steps 18.39 ms, 4 k-steps at 2 CTAs/SM 19.78 ms)
-      mma_panel<false, 16>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc,
-                          D.x + int64_t(col) * D.bc * NV);
+      if (V < 3)
+        mma_panel<false, 16, V>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc,
+                                D.x + int64_t(col) * D.bc * NV);
+      else
+        mma_N_pairs<16, V - 3>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc,
+                               D.x + int64_t(col) * D.bc * NV);
     }
-    store_panel(acc, D.y + int64_t(row) * D.br * NV, D.br, false);
+    if (V < 3)
+      store_panel(acc, D.y + int64_t(row) * D.br * NV, D.br, false);
+    else
+      store_panel_pr(acc, D.y + int64_t(row) * D.br * NV, D.br, false);
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_down_level_mv(const double* __restrict__ E, int ldc,
-                                                            int kc, int kp, int64_t nc,
-                                                            const double* __restrict__ yp,
-                                                            double* __restrict__ yl) {
-  const int64_t stride = int64_t(ldc) * kp;
-  for (int64_t c = warp_global(); c < nc; c += warp_count()) {
-    Acc acc;
-    acc.zero();
-    mma_panel<false>(acc, E + c * stride, ldc, kc, kp, yp + (c >> 1) * kp * NV);
-    store_panel(acc, yl + c * kc * NV, kc, true);
-  }
-}
-
-// Y[perm[t] + v ldy] = alpha (U y^ + yc)[t][v] + beta Y[...].
-__global__ void __launch_bounds__(kThreads) k_down_leaf_mv(
-    const double* __restrict__ U, int ldm, int m, int k, int64_t nleaves,
+// Leaf i: Y[perm[t] + v ldy] = alpha (U_i y^q_i + yc)[t][v] + beta Y[...]
+// (hmv.hpp:147-156, 184-187).  The result rows go through a shared [v][t]
+// panel so the scatter is coalesced along t.
+constexpr int kSLd = 68;  // shared [v][t] leading dimension (2-way store conflicts, conflict-free reads)
+template <int POL, int UNR>
+__global__ void __launch_bounds__(32 * kLeafWarps) k_down_leaf_mv(
+    const double* __restrict__ U, int ldm, int m, int k, int64_t nleaves, int64_t leaf0,
     const double* __restrict__ yh, const double* __restrict__ yc, const int32_t* __restrict__ perm,
-    double* __restrict__ Y, int64_t ldy, int nv, double alpha, double beta) {
+    double* __restrict__ Y, int64_t ldy, int nv, double alpha, double beta, double* __restrict__ yslice) {
+  __shared__ __align__(16) double panel_all[kLeafWarps][NV * kSLd];
+  double* panel = panel_all[threadIdx.x >> 5];
   const int lane = lane_id();
   const int fr = lane >> 2, fc = 2 * (lane & 3);
   const int64_t stride = int64_t(ldm) * k;
-  for (int64_t i = warp_global(); i < nleaves; i += warp_count()) {
+  for (int64_t il = warp_global(); il < nleaves; il += warp_count()) {
+    const int64_t i = leaf0 + il;  // global leaf; the pool holds the owned leaves only
     Acc acc;
     acc.zero();
-    if (k > 0) mma_panel<false>(acc, U + i * stride, ldm, m, k, yh + i * k * NV);
+    if (k > 0) mma_N_pairs<UNR, POL>(acc, U + il * stride, ldm, m, k, yh + i * k * NV);
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
-      const int r = 8 * x + fr;
+      const int r = prow(x, fr);
       if (r >= m) continue;
-      const int64_t t = i * m + r;
-      const int64_t o = perm[t];
 #pragma unroll
       for (int y = 0; y < 2; ++y)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int v = 8 * y + fc + h;
-          if (v >= nv) continue;
-          const double val = acc.c[x][y][h] + yc[t * NV + v];
-          double* dst = Y + o + v * ldy;
-          *dst = alpha * val + (beta == 0.0 ? 0.0 : beta * *dst);
-        }
+        for (int h = 0; h < 2; ++h) panel[(8 * y + fc + h) * kSLd + r] = acc.c[x][y][h];
     }
+    __syncwarp();
+    const int64_t base = i * m;
+    const double* yci = yc + base * NV;
+    if (yslice) {  // partition: the cluster-order slice (vector-minor), alpha / beta applied by the scatter
+      double* yo = yslice + il * m * NV;
+      for (int e = lane; e < m * NV; e += 32) yo[e] = panel[(e & (NV - 1)) * kSLd + (e >> 4)] + yci[e];
+      __syncwarp();
+      continue;
+    }
+    const int t0 = 2 * lane, t1 = t0 + 1;
+    const int64_t o0 = t0 < m ? int64_t(__ldg(perm + base + t0)) : -1;
+    const int64_t o1 = t1 < m ? int64_t(__ldg(perm + base + t1)) : -1;
+#pragma unroll 2
+    for (int v = 0; v < nv; ++v) {
+      const double2 u = *reinterpret_cast<const double2*>(panel + v * kSLd + t0);
+      if (o0 >= 0) {
+        double* d = Y + o0 + v * ldy;
+        const double val = u.x + yci[t0 * NV + v];
+        *d = alpha * val + (beta == 0.0 ? 0.0 : beta * *d);
+      }
+      if (o1 >= 0) {
+        double* d = Y + o1 + v * ldy;
+        const double val = u.y + yci[t1 * NV + v];
+        *d = alpha * val + (beta == 0.0 ? 0.0 : beta * *d);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// xc16[t][v] = X[perm[t] + v ldx] for every t (partitions: dense blocks read
+// the rows of remote leaves).  Thread per 16-byte output.
+__global__ void k_gather_mv(const int32_t* __restrict__ perm, const double* __restrict__ X, int64_t ldx, int nv,
+                            int64_t n, double* __restrict__ xc) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * (NV / 2);
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = e >> 3;
+    const int v = 2 * int(e & 7);
+    const int64_t o = __ldg(perm + t);
+    const double a = v < nv ? __ldg(X + o + v * ldx) : 0.0;
+    const double b = v + 1 < nv ? __ldg(X + o + (v + 1) * ldx) : 0.0;
+    reinterpret_cast<double2*>(xc)[e] = make_double2(a, b);
+  }
+}
+
+// Y[perm[t] + v ldy] = alpha yc[t][v] + beta Y[...] for every t (the
+// replicated-output scatter of a gathered cluster-order panel).
+__global__ void k_scatter_mv(const int32_t* __restrict__ perm, const double* __restrict__ yc, int64_t n, int nv,
+                             double* __restrict__ Y, int64_t ldy, double alpha, double beta) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * NV;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = e >> 4;
+    const int v = int(e & (NV - 1));
+    if (v >= nv) continue;
+    double* d = Y + __ldg(perm + t) + v * ldy;
+    *d = alpha * yc[e] + (beta == 0.0 ? 0.0 : beta * *d);
   }
 }
 
@@ -226,14 +518,28 @@ unsigned wgrid(int64_t items) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, int64_t(sms()) * 8)));
 }
 
+unsigned leaf_grid(int64_t items) {
+  return unsigned(
+      std::max<int64_t>(1, std::min<int64_t>((items + kLeafWarps - 1) / kLeafWarps, int64_t(sms()) * 16)));
+}
+
+unsigned persistent_grid_mv(const void* kernel) {
+  int per_sm = 0;
+  H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+  return unsigned(std::max(1, per_sm) * sms());
+}
+
 }  // namespace
 
-// Y (n x nv, ld ldy) <- alpha A X + beta Y for nv <= 16 vectors, device pointers.
-void hmv_multi_device(Matrix& A, Work& w, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
-                      double alpha, double beta, cudaStream_t s) {
-  require(nv >= 1 && nv <= NV, "hmv_multi: 1..16 vectors per pass");
+namespace {
+
+unsigned flat_grid_mv(int64_t items) {
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(sms()) * 16)));
+}
+
+void ensure_mv_work(Matrix& A, Work& w) {
+  const Matrix& C = A.col_basis();
   const int q = A.q;
-  const Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
   const int64_t nvec_pool = std::max<int64_t>({1, A.vec_off[q + 1], C.vec_off[q + 1]}) * NV;
   if (w.xc16.n < size_t(A.n) * NV) {
     w.xc16.alloc(size_t(A.n) * NV);
@@ -243,30 +549,95 @@ void hmv_multi_device(Matrix& A, Work& w, const double* X, int64_t ldx, double* 
     w.xh16.alloc(nvec_pool);
     w.yh16.alloc(nvec_pool);
   }
-  const int64_t n = A.n;
-  k_gather_mv<<<unsigned(std::min<int64_t>((n * NV + 255) / 256, int64_t(sms()) * 16)), 256, 0, s>>>(
-      A.perm.p, X, ldx, nv, n, w.xc16.p);
+}
+
+// Upsweep of the 16-vector pass over this handle's nodes: gather + leaves,
+// then levels q .. part_s + 1 (whole matrix: q .. 1) in one dataflow launch.
+template <int POL, int UNR>
+void mv_up_local(Matrix& A, Work& w, const double* X, int64_t ldx, int nv, cudaStream_t s) {
+  const int q = A.q;
+  const Matrix& C = A.col_basis();  // upsweep on the column basis (hmv.hpp:182)
+  double* xh = w.xh16.p;
+  const int64_t nl = C.own_count(q);
+  const bool part = A.part_s > 0;
+  if (part) {  // dense blocks crossing the partition read remote rows of xc
+    k_gather_mv<<<flat_grid_mv(int64_t(A.n) * (NV / 2)), 256, 0, s>>>(A.perm.p, X, ldx, nv, A.n, w.xc16.p);
+    H2B_CUDA(cudaGetLastError());
+  }
+  k_up_leaf_mv<POL, UNR><<<leaf_grid(nl), 32 * kLeafWarps, 0, s>>>(C.leaf.p, C.ldm, C.m, C.rank[q], nl,
+                                                                   C.own_begin(q), A.perm.p, X, ldx, nv,
+                                                                   part ? 0 : 1, w.xc16.p, xh + C.vec_off[q] * NV);
   H2B_CUDA(cudaGetLastError());
-  const int64_t nl = A.nodes(q);
+  if (q > A.part_s) {
+    SweepTableMV T{};
+    T.q = q;
+    int64_t tot = 0;
+    for (int l = q; l > A.part_s; --l) {
+      SweepLevelMV& L = T.L[T.nl];
+      L.T = C.transfer.p + C.tr_off[l];
+      L.stride = C.tr_stride(l);
+      L.cbegin = C.tr_begin(l);
+      L.ldc = C.ld(l);
+      L.kc = C.rank[l];
+      L.kp = C.rank[l - 1];
+      L.l = l;
+      L.in = xh + C.vec_off[l] * NV;
+      L.out = xh + C.vec_off[l - 1] * NV;
+      L.i0 = C.own_begin(l - 1);
+      L.n = C.own_count(l - 1);
+      T.start[T.nl++] = tot;
+      tot += L.n;
+    }
+    T.start[T.nl] = tot;
+    H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
+    k_up_fused_mv<POL, UNR><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR>), kThreads, 0, s>>>(
+        T, w.flag.p, 2 * w.epoch, w.ticket.p);
+    H2B_CUDA(cudaGetLastError());
+  }
+}
+
+// Replicated top of a partition: levels part_s .. 1, every node (level
+// part_s's x^ gathered from all partitions).
+template <int POL, int UNR>
+void mv_up_top(Matrix& A, Work& w, cudaStream_t s) {
+  if (A.part_s < 1) return;
+  double* xh = w.xh16.p;
+  SweepTableMV T{};
+  T.q = A.part_s;
+  int64_t tot = 0;
+  for (int l = A.part_s; l >= 1; --l) {
+    SweepLevelMV& L = T.L[T.nl];
+    L.T = A.transfer.p + A.tr_off[l];
+    L.stride = A.tr_stride(l);
+    L.cbegin = A.tr_begin(l);
+    L.ldc = A.ld(l);
+    L.kc = A.rank[l];
+    L.kp = A.rank[l - 1];
+    L.l = l;
+    L.in = xh + A.vec_off[l] * NV;
+    L.out = xh + A.vec_off[l - 1] * NV;
+    L.i0 = 0;
+    L.n = A.nodes(l - 1);
+    T.start[T.nl++] = tot;
+    tot += L.n;
+  }
+  T.start[T.nl] = tot;
+  H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
+  k_up_fused_mv<POL, UNR><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR>), kThreads, 0, s>>>(
+      T, w.flag.p, 2 * w.epoch, w.ticket.p);
+  H2B_CUDA(cudaGetLastError());
+}
+
+// Coupling + dense rows of this handle, downsweep (replicated top + own
+// subtree), leaf expansion: Y (original order, alpha / beta) or, when yslice,
+// the cluster-order vector-minor slice of the owned leaves.
+template <int POL, int UNR>
+void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha, double beta, double* yslice,
+               cudaStream_t s) {
+  const int q = A.q;
+  const Matrix& C = A.col_basis();
   double* xh = w.xh16.p;
   double* yh = w.yh16.p;
-  if (C.rank[q] > 0) {
-    k_up_leaf_mv<<<wgrid(nl), kThreads, 0, s>>>(C.leaf.p, C.ldm, C.m, C.rank[q], nl, w.xc16.p,
-                                               xh + C.vec_off[q] * NV);
-    H2B_CUDA(cudaGetLastError());
-  }
-  for (int l = q; l >= 1; --l) {
-    const int kc = C.rank[l], kp = C.rank[l - 1];
-    const int64_t np = A.nodes(l - 1);
-    if (kp == 0) continue;
-    if (kc == 0) {
-      H2B_CUDA(cudaMemsetAsync(xh + C.vec_off[l - 1] * NV, 0, size_t(np) * kp * NV * sizeof(double), s));
-      continue;
-    }
-    k_up_level_mv<<<wgrid(np), kThreads, 0, s>>>(C.transfer.p + C.tr_off[l], C.ld(l), kc, kp, np,
-                                                 xh + C.vec_off[l] * NV, xh + C.vec_off[l - 1] * NV);
-    H2B_CUDA(cudaGetLastError());
-  }
   LayerTableMV T{};
   for (int l = 0; l <= q; ++l) {
     const Layer& L = A.cpl[l];
@@ -292,20 +663,95 @@ void hmv_multi_device(Matrix& A, Work& w, const double* X, int64_t ldx, double* 
   d.bc = A.dense.bc;
   d.ld = std::max(2, A.dense.ld);
   if (A.nwork) {
-    k_bsr_mv<<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
+    // The LPT-ordered work list (make_work_list).  Layer / row order keeps
+    // neighbouring rows' x panels in L2 (DRAM read 75.4 -> 72.6 GB at C4) but
+    // loses the balance: 12.18 -> 12.71 ms.  16-byte paired-row loads
+    // (mma_N_pairs) instead of the 8-byte fragments: 17.3 ms (fewer loads in
+    // flight at 255 registers); non-coherent / L2::256B loads: 12.6 ms,
+    // 79.4 GB read.  The evict-first 8-byte form stays.
+    k_bsr_mv<0><<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
     H2B_CUDA(cudaGetLastError());
   }
-  for (int l = 1; l <= q; ++l) {
-    const int kc = A.rank[l], kp = A.rank[l - 1];
-    if (kc == 0 || kp == 0) continue;
-    const int64_t nc = A.nodes(l);
-    k_down_level_mv<<<wgrid(nc), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, nc,
-                                                   yh + A.vec_off[l - 1] * NV, yh + A.vec_off[l] * NV);
+  if (q >= 1) {  // levels 1..q in one dataflow launch (the root's y^ is final)
+    SweepTableMV S{};
+    S.q = 0;
+    int64_t tot = 0;
+    for (int l = 1; l <= q; ++l) {
+      SweepLevelMV& L = S.L[S.nl];
+      L.T = A.transfer.p + A.tr_off[l];
+      L.stride = A.tr_stride(l);
+      L.cbegin = A.tr_begin(l);
+      L.ldc = A.ld(l);
+      L.kc = A.rank[l];
+      L.kp = A.rank[l - 1];
+      L.l = l;
+      L.in = yh + A.vec_off[l - 1] * NV;
+      L.out = yh + A.vec_off[l] * NV;
+      L.i0 = A.own_begin(l);
+      L.n = A.own_count(l);
+      S.start[S.nl++] = tot;
+      tot += L.n;
+    }
+    S.start[S.nl] = tot;
+    H2B_CUDA(cudaMemsetAsync(w.ticket.p + 1, 0, sizeof(unsigned long long), s));
+    k_down_fused_mv<POL, UNR><<<persistent_grid_mv((const void*)k_down_fused_mv<POL, UNR>), kThreads, 0, s>>>(
+        S, w.flag.p, 2 * w.epoch + 1, w.ticket.p + 1);
     H2B_CUDA(cudaGetLastError());
   }
-  k_down_leaf_mv<<<wgrid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[q], nl,
-                                                yh + A.vec_off[q] * NV, w.yc16.p, A.perm.p, Y, ldy, nv,
-                                                alpha, beta);
+  const int64_t nl = A.own_count(q);
+  k_down_leaf_mv<POL, UNR><<<leaf_grid(nl), 32 * kLeafWarps, 0, s>>>(
+      A.leaf.p, A.ldm, A.m, A.rank[q], nl, A.own_begin(q), yh + A.vec_off[q] * NV, w.yc16.p, A.perm.p, Y, ldy, nv,
+      alpha, beta, yslice);
+  H2B_CUDA(cudaGetLastError());
+}
+
+// Load policy and unroll measured at C4 (n = 2^22, k = 64, 16 vectors; ncu
+// launch lists, tools/mv16_launches.sh): the evict-first 16-byte loads of the
+// transposed products fetched 1.5-1.8x their bytes from DRAM (the other half
+// of each 128-byte line was evicted before its second 64-byte piece was
+// used): k_up_fused_mv 2.13 ms / 8.73 GB read, k_up_leaf_mv 0.87 ms / 4.00 GB.
+// Non-coherent loads with the 256-byte L2 prefetch hint read exactly the
+// algorithmic bytes: 1.45 ms / 5.36 GB and 0.68 ms / 2.70 GB.  Two pair-steps
+// in flight beat four (registers / occupancy) except for the leaf (0.67 vs
+// 0.68 ms, noise).  The untransposed products are insensitive to the policy.
+constexpr int kPol = 2, kUnr = 2;
+
+}  // namespace
+
+// Y (n x nv, ld ldy) <- alpha A X + beta Y for nv <= 16 vectors, device pointers.
+void hmv_multi_device(Matrix& A, Work& w, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv,
+                      double alpha, double beta, cudaStream_t s) {
+  require(nv >= 1 && nv <= NV, "hmv_multi: 1..16 vectors per pass");
+  require(A.part_s == 0, "hmv_multi_device: partition handle");
+  ensure_mv_work(A, w);
+  sweep_begin(w, A, s);
+  mv_up_local<kPol, kUnr>(A, w, X, ldx, nv, s);
+  mv_finish<kPol, kUnr>(A, w, Y, ldy, nv, alpha, beta, nullptr, s);
+}
+
+// Partitioned 16-vector pass, phase 1: owned leaves and levels > part_s.
+// Level l >= part_s of the vector-minor x^ panel pool (xh16) then holds this
+// partition's nodes; the caller all-gathers them (part_exchange).
+void part_mv_upsweep(Matrix& A, Work& w, const double* X, int64_t ldx, int nv, cudaStream_t s) {
+  require(nv >= 1 && nv <= NV, "hmv_multi: 1..16 vectors per pass");
+  ensure_mv_work(A, w);
+  sweep_begin(w, A, s);
+  mv_up_local<kPol, kUnr>(A, w, X, ldx, nv, s);
+}
+
+// Phase 2: replicated top, owned rows, downsweep, leaf expansion into Y
+// (yslice == nullptr: owned rows of Y in original order) or the cluster-order
+// vector-minor slice.
+void part_mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha, double beta, double* yslice,
+                    cudaStream_t s) {
+  mv_up_top<kPol, kUnr>(A, w, s);
+  mv_finish<kPol, kUnr>(A, w, Y, ldy, nv, alpha, beta, yslice, s);
+}
+
+void launch_scatter_mv(const int32_t* perm, const double* yc, int64_t n, int nv, double* Y, int64_t ldy,
+                       double alpha, double beta, cudaStream_t s) {
+  if (n == 0) return;
+  k_scatter_mv<<<flat_grid_mv(n * NV), 256, 0, s>>>(perm, yc, n, nv, Y, ldy, alpha, beta);
   H2B_CUDA(cudaGetLastError());
 }
 

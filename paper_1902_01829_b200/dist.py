@@ -4,18 +4,23 @@ One process per GPU (torch.distributed, NCCL).  Each rank builds only its
 partition of the matrix in HBM (h2b_matrix_build_part: its top-level
 subtree's leaves, basis nodes and coupling/dense block rows, plus the
 replicated levels above the split), so an n = 2^22 matrix takes 1/P of the
-memory per GPU.  One mat-vec (DistributedH2Matrix.hmv):
+memory per GPU.  One mat-vec (DistributedH2Matrix.hmv) is ONE library call,
+h2b_part_hmv, which runs every step in libh2b.so on the caller's stream:
 
-  1. h2b_part_upsweep   local leaves -> x^ of the owned nodes, up to level s
-  2. all-gather x^      one NCCL all-gather per level >= s (the owned slice of a
-                        level is contiguous in the level-concatenated pool;
-                        in-place, nothing is copied)
-  3. h2b_part_finish    replicated top upsweep, coupling + dense rows of the
-                        owned subtree, downsweep, leaf expansion -> y slice
-  4. all-gather y       cluster-order slices, then y[perm] = a y_c + b y[perm]
+  1. owned leaves -> x^ of the owned nodes, up to level s (dataflow launch)
+  2. pack the owned x^ of every level >= s into one buffer, ONE stream-ordered
+     all-gather through the communicator (NCCL: ncclAllGather in place),
+     unpack the other ranks' slices
+  3. replicated top upsweep, coupling + dense rows of the owned subtree,
+     downsweep, leaf expansion
+  4. Y_REPLICATED: all-gather of the cluster-order y slices and the fused
+     owner-row scatter y[perm] = a y_c + b y[perm]; Y_OWNED: each rank writes
+     its own rows of y directly (no y collective)
 
-x̂ crossing the partition boundary is < 1 % of the matrix bytes at n = 2^22,
-so the collectives are a small fraction of the step.
+No torch compute op runs on this path; torch.distributed only provides the
+NCCL communicator (TorchComm).  A C++ host drives the same call with its own
+ncclComm_t (examples/part_hmv_nccl.cpp).  x^ crossing the partition boundary
+is < 1 % of the matrix bytes at n = 2^22.
 """
 from __future__ import annotations
 
@@ -51,6 +56,14 @@ def torch_stream_handle() -> int:
     import torch
     h = torch.cuda.current_stream().cuda_stream
     return h if h else _lib.CUDA_STREAM_LEGACY
+
+
+def _stream_of(handle: int):
+    """torch stream object for a cudaStream_t handed back by the library."""
+    import torch
+    if handle in (0, _lib.CUDA_STREAM_LEGACY):
+        return torch.cuda.default_stream()
+    return torch.cuda.ExternalStream(handle)
 
 
 def gather_xhat(plan: PartitionPlan, xhat, allgather):
@@ -98,6 +111,29 @@ class Communicator:
 
     def allreduce_sum(self, t):
         raise NotImplementedError
+
+    def allgather_stream(self, buf, stream: int):
+        """Stream-ordered form used by h2b_part_hmv: the all-gather must be
+        complete, in stream order, before the stream's next operation.  Default:
+        synchronise the stream, then the blocking allgather."""
+        _stream_of(stream).synchronize()
+        self.allgather(buf)
+
+    def as_dcomm(self) -> "_lib.DComm":
+        """ctypes h2b_dcomm (the partitioned mat-vec's device all-gather)."""
+
+        def ag(ctx, ptr, count, stream):
+            try:
+                self.allgather_stream(_wrap(ptr, int(count) * self.nparts, self.device), int(stream or 0))
+                return 0
+            except Exception as e:  # noqa: BLE001  (cannot propagate through C)
+                self.error = e
+                return 1
+
+        self.error = None
+        self._dfn = _lib.DALLGATHER_FN(ag)
+        self._dc = _lib.DComm(None, self._dfn)
+        return self._dc
 
     def as_c(self) -> "_lib.Comm":
         """ctypes h2b_comm whose callbacks call this object (kept alive by it)."""
@@ -158,6 +194,17 @@ class TorchComm(Communicator):
             parts = [torch.empty_like(mine) for _ in range(self.nparts)]
             dist.all_gather(parts, mine, group=self.group)
             buf.copy_(torch.cat(parts))
+
+    def allgather_stream(self, buf, stream: int):
+        """NCCL: enqueue the in-place all-gather on `stream` (no host sync);
+        the rank's own slice of buf is the send buffer."""
+        if not (self.nccl and buf.is_cuda):
+            return super().allgather_stream(buf, stream)
+        import torch
+        import torch.distributed as dist
+        chunk = buf.numel() // self.nparts
+        with torch.cuda.stream(_stream_of(stream)):
+            dist.all_gather_into_tensor(buf, buf.narrow(0, self.part * chunk, chunk), group=self.group)
 
     def _allreduce(self, t, op):
         import torch
@@ -307,28 +354,55 @@ class DistributedH2Matrix:
         self._refresh()
         return report_from_c(rep, self.depth)
 
-    def gather_xhat(self, allgather):
-        gather_xhat(self.plan, self.xhat, allgather)
-
-    def hmv(self, x, y=None, alpha: float = 1.0, beta: float = 0.0, allgather=None):
-        """y <- alpha A x + beta y for the full vectors x, y (original order,
-        replicated on every rank, CUDA float64)."""
+    def hmv(self, x, y=None, alpha: float = 1.0, beta: float = 0.0, comm: Communicator | None = None,
+            y_mode: int = _lib.Y_REPLICATED, stream: int | None = None):
+        """y <- alpha A x + beta y (hmv.hpp:175-188) with x, y full vectors in
+        original order (CUDA float64).  One library call (h2b_part_hmv): the
+        upsweep, the packed x^ all-gather (comm, default NCCL through this
+        matrix's process group), the coupling / dense rows, the downsweep and the
+        owner-row scatter all run in libh2b.so; y_mode Y_REPLICATED all-gathers
+        the cluster-order y slices so every rank ends with all of y, Y_OWNED
+        writes only this rank's rows."""
         import torch
-        import torch.distributed as dist
-        if allgather is None:
-            def allgather(out, inp):
-                dist.all_gather_into_tensor(out, inp, group=self.group)
-        st = torch_stream_handle()
-        lib = _lib.load()
-        _lib.check(lib.h2b_part_upsweep(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(st)))
-        self.gather_xhat(allgather)
-        _lib.check(lib.h2b_part_finish(self._h, C.c_void_p(self.y_slice.data_ptr()), C.c_void_p(st)))
-        allgather(self.y_cluster, self.y_slice)
+        if comm is None:
+            comm = self._default_comm()
         if y is None:
-            y = torch.empty_like(x)
+            y = torch.zeros_like(x)
             beta = 0.0
-        if beta == 0.0:
-            y[self.perm] = alpha * self.y_cluster
-        else:
-            y[self.perm] = alpha * self.y_cluster + beta * y[self.perm]
+        st = torch_stream_handle() if stream is None else stream
+        dc = comm.as_dcomm()
+        status = _lib.load().h2b_part_hmv(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                          float(alpha), float(beta), int(y_mode), C.byref(dc), C.c_void_p(st))
+        self._check_comm(status, comm)
         return y
+
+    def hmv_multi(self, X, Y=None, alpha: float = 1.0, beta: float = 0.0, comm: Communicator | None = None,
+                  y_mode: int = _lib.Y_REPLICATED, stream: int | None = None):
+        """Y <- alpha A X + beta Y for the columns of X (n x nvec, column-major:
+        a (nvec, n) row-major CUDA tensor), 16 per pass on the FP64 tensor cores
+        (h2b_part_hmv_multi)."""
+        import torch
+        if comm is None:
+            comm = self._default_comm()
+        if Y is None:
+            Y = torch.zeros_like(X)
+            beta = 0.0
+        nvec, n = X.shape
+        st = torch_stream_handle() if stream is None else stream
+        dc = comm.as_dcomm()
+        status = _lib.load().h2b_part_hmv_multi(self._h, int(nvec), C.c_void_p(X.data_ptr()), n,
+                                                C.c_void_p(Y.data_ptr()), n, float(alpha), float(beta),
+                                                int(y_mode), C.byref(dc), C.c_void_p(st))
+        self._check_comm(status, comm)
+        return Y
+
+    def _default_comm(self):
+        if not hasattr(self, "_comm"):
+            self._comm = TorchComm(self.group, self.device)
+        return self._comm
+
+    @staticmethod
+    def _check_comm(status, comm):
+        if status != _lib.H2B_OK and getattr(comm, "error", None) is not None:
+            raise RuntimeError(f"communicator failed: {comm.error!r}")
+        _lib.check(status)

@@ -98,6 +98,7 @@ def part0(steps=10):
     build_s = time.time() - t0
     n = D.n
     free, total = torch.cuda.mem_get_info()
+    fp_local, fp_global = D.footprint_local, D.footprint_global  # before compress() shrinks them
     lib = _lib.load()
     x = torch.rand(n, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream()
@@ -121,9 +122,9 @@ def part0(steps=10):
     torch.cuda.synchronize()
     comp_wall = time.time() - t0
     out = {"case": "3D n=2^24 k=64 (C5), partition 0 of 8, collectives stubbed",
-           "build_s": round(build_s, 1), "footprint_local_bytes": D.footprint_local,
-           "footprint_global_bytes": D.footprint_global, "hbm_used_gb": round((total - free) / 1e9, 1),
-           "local_hmv_ms": round(ms, 3), "local_hmv_GBs": round(D.footprint_local / ms / 1e6, 1),
+           "build_s": round(build_s, 1), "footprint_local_bytes": fp_local,
+           "footprint_global_bytes": fp_global, "hbm_used_gb": round((total - free) / 1e9, 1),
+           "local_hmv_ms": round(ms, 3), "local_hmv_GBs": round(fp_local / ms / 1e6, 1),
            "phase_ms_after_upsweep": [round(v, 4) for v in list(buf)[:3]],
            "xhat_allgather_bytes_per_gpu": gather,
            "compress_local": {"eps": 1e-6, "ms": round(rep.total_ms(), 1), "wall_s": round(comp_wall, 2),
