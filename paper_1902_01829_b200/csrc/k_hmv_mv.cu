@@ -231,6 +231,25 @@ __device__ __forceinline__ void store_panel_pr(const Acc& acc, double* __restric
   }
 }
 
+// acc = in (M x 16, vector-minor; paired-row tile layout), zero above M: the
+// accumulator starts from the values the product is added to, so their loads
+// overlap the first A-operand loads instead of trailing the product.
+__device__ __forceinline__ void load_panel_pr(Acc& acc, const double* __restrict__ in, int M) {
+  const int lane = lane_id();
+  const int fr = lane >> 2, fc = 2 * (lane & 3);
+#pragma unroll
+  for (int x = 0; x < 8; ++x) {
+    const int i = prow(x, fr);
+#pragma unroll
+    for (int y = 0; y < 2; ++y) {
+      const double2 v = i < M ? __ldcg(reinterpret_cast<const double2*>(in + i * NV + 8 * y + fc))
+                              : make_double2(0.0, 0.0);
+      acc.c[x][y][0] = v.x;
+      acc.c[x][y][1] = v.y;
+    }
+  }
+}
+
 // ---- shared 64 x 16 panel of one leaf ------------------------------------
 // Pair-interleaved and swizzled: rows 2j, 2j+1 of vector v form one 16-byte
 // unit at j * 16 + (v ^ ((j & 3) << 1)).  The B fragments of mma_T_pairs read
@@ -256,14 +275,17 @@ __global__ void __launch_bounds__(32 * kLeafWarps) k_up_leaf_mv(
     const int t0 = 2 * lane, t1 = t0 + 1;
     const int64_t o0 = t0 < m ? int64_t(__ldg(perm + base + t0)) : -1;
     const int64_t o1 = t1 < m ? int64_t(__ldg(perm + base + t1)) : -1;
-#pragma unroll 4
+    // all 32 loads in flight before the first store
+    double2 g[NV];
+#pragma unroll
     for (int s = 0; s < NV; ++s) {
       const int v = (s + (lane >> 2)) & (NV - 1);
       const bool vok = v < nv;
-      const double a = (vok && o0 >= 0) ? __ldg(X + o0 + v * ldx) : 0.0;
-      const double b = (vok && o1 >= 0) ? __ldg(X + o1 + v * ldx) : 0.0;
-      panel[punit(lane, v)] = make_double2(a, b);
+      g[s].x = (vok && o0 >= 0) ? __ldg(X + o0 + v * ldx) : 0.0;
+      g[s].y = (vok && o1 >= 0) ? __ldg(X + o1 + v * ldx) : 0.0;
     }
+#pragma unroll
+    for (int s = 0; s < NV; ++s) panel[punit(lane, (s + (lane >> 2)) & (NV - 1))] = g[s];
     __syncwarp();
     // xc16 rows of this leaf, coalesced 16-byte stores (unless a full gather
     // already wrote them: partitions, whose dense blocks read remote rows)
@@ -315,9 +337,11 @@ __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant_
                                                           unsigned long long* __restrict__ ticket) {
   const int fr = lane_id() >> 2;
   const int64_t total = S.start[S.nl];
+  int64_t next = df::claim(ticket);
   for (;;) {
-    const int64_t it = df::claim(ticket);
+    const int64_t it = next;
     if (it >= total) break;
+    next = df::claim(ticket);  // claimed ahead: its atomic overlaps this item (claims stay monotone)
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevelMV& L = S.L[e];
@@ -355,9 +379,11 @@ __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constan
                                                             uint32_t* __restrict__ flag, uint32_t epoch,
                                                             unsigned long long* __restrict__ ticket) {
   const int64_t total = S.start[S.nl];
+  int64_t next = df::claim(ticket);
   for (;;) {
-    const int64_t it = df::claim(ticket);
+    const int64_t it = next;
     if (it >= total) break;
+    next = df::claim(ticket);  // claimed ahead: its atomic overlaps this item (claims stay monotone)
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevelMV& L = S.L[e];
@@ -367,6 +393,9 @@ __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constan
       Acc acc;
       acc.zero();
       mma_N_pairs<UNR, POL>(acc, L.T + (c - L.cbegin) * L.stride, L.ldc, L.kc, L.kp, L.in + (c >> 1) * L.kp * NV);
+      // y^l_c (coupling product) += E_c y^{l-1}: added at the end (starting
+      // the accumulator from it, as k_down_leaf_mv does with yc, measured
+      // 1.49 -> 1.70 ms at C4)
       store_panel_pr(acc, L.out + c * L.kc * NV, L.kc, true);
     }
     df::set_flag(flag + df::node_id(L.l, c), epoch);
@@ -434,7 +463,7 @@ __global__ void __launch_bounds__(32 * kLeafWarps) k_down_leaf_mv(
   for (int64_t il = warp_global(); il < nleaves; il += warp_count()) {
     const int64_t i = leaf0 + il;  // global leaf; the pool holds the owned leaves only
     Acc acc;
-    acc.zero();
+    load_panel_pr(acc, yc + i * m * NV, m);  // yc (dense product) + U y^ (0.88 -> 0.76 ms at C4)
     if (k > 0) mma_N_pairs<UNR, POL>(acc, U + il * stride, ldm, m, k, yh + i * k * NV);
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
@@ -447,10 +476,9 @@ __global__ void __launch_bounds__(32 * kLeafWarps) k_down_leaf_mv(
     }
     __syncwarp();
     const int64_t base = i * m;
-    const double* yci = yc + base * NV;
     if (yslice) {  // partition: the cluster-order slice (vector-minor), alpha / beta applied by the scatter
       double* yo = yslice + il * m * NV;
-      for (int e = lane; e < m * NV; e += 32) yo[e] = panel[(e & (NV - 1)) * kSLd + (e >> 4)] + yci[e];
+      for (int e = lane; e < m * NV; e += 32) yo[e] = panel[(e & (NV - 1)) * kSLd + (e >> 4)];
       __syncwarp();
       continue;
     }
@@ -462,12 +490,12 @@ __global__ void __launch_bounds__(32 * kLeafWarps) k_down_leaf_mv(
       const double2 u = *reinterpret_cast<const double2*>(panel + v * kSLd + t0);
       if (o0 >= 0) {
         double* d = Y + o0 + v * ldy;
-        const double val = u.x + yci[t0 * NV + v];
+        const double val = u.x;
         *d = alpha * val + (beta == 0.0 ? 0.0 : beta * *d);
       }
       if (o1 >= 0) {
         double* d = Y + o1 + v * ldy;
-        const double val = u.y + yci[t1 * NV + v];
+        const double val = u.y;
         *d = alpha * val + (beta == 0.0 ? 0.0 : beta * *d);
       }
     }
