@@ -328,7 +328,25 @@ def compression_run(h2, torch, device, reps):
                          "project_trunc": round(rep.time_project_trunc_ms, 1)},
             "new_ranks": rep.new_ranks, "frobenius_error": rep.frobenius_error,
             "bytes": [rep.bytes_before, rep.bytes_after],
-            "pipe_utilisation_ncu": (load_pipes() or {}).get("compression_C3")}
+            "executed": executed_compress(dev_ms),
+            "pipe_utilisation_ncu_recorded": (load_pipes() or {}).get("compression_C3")}
+
+
+def executed_compress(dev_ms):
+    """Executed FP64 flops of one C3 compress (ncu SASS counters: 2 DFMA + DADD
+    + DMUL + 512 DMMA.8x8x4, tools/compress_exec_flops.py), RECORDED in
+    profiles/r02_compress_exec_flops_c3.json -- not measured by this run -- over
+    this run's device time.  The kernels execute ~79% of the reference model's
+    flops: unpadded weight stacks, upper blocks of symmetric levels, skipped
+    triangular fragments, ~6 Jacobi sweeps (but also the dead-lane FMAs)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_compress_exec_flops_c3.json")) as f:
+            ex = json.load(f)["executed_flops"]
+    except Exception:
+        return None
+    g = ex / (dev_ms * 1e-3) / 1e9
+    return {"flops": ex, "gflops": round(g, 1), "pct_fp64_peak": round(100 * g / 1e3 / FP64_PEAK_TFLOPS, 2),
+            "source": "profiles/r02_compress_exec_flops_c3.json (ncu, recorded)"}
 
 
 def compression_run_dist(torch, device, reps, world):
@@ -394,7 +412,23 @@ def multi16_run(A, torch, steps):
             "matrix_stream_GBs": round(fp / ms / 1e6, 1),
             "model_tflops": round(16 * flops / ms / 1e9, 2),
             "pct_fp64_peak": round(100 * 16 * flops / ms / 1e9 / FP64_PEAK_TFLOPS, 2),
-            "pipe_utilisation_ncu": (load_pipes() or {}).get("multi16_C4")}
+            "byte_bound": mv16_byte_bound(A, n, fp, ms),
+            "pipe_utilisation_ncu_recorded": (load_pipes() or {}).get("multi16_C4")}
+
+
+def mv16_byte_bound(A, n, fp, ms):
+    """Compulsory HBM bytes of one 16-vector pass: every matrix entry once, the
+    (symmetric) basis a second time in the downsweep, the 16-column panels of
+    x (read), y (written), xc / yc (written + read) and x^ / y^ (written +
+    read), over the measured copy peak."""
+    inf = A.info()
+    k = list(inf.ranks[:inf.depth + 1])
+    basis = 8 * (n * k[-1] + sum((1 << l) * k[l] * k[l - 1] for l in range(1, len(k))))
+    vec = sum((1 << l) * k[l] for l in range(len(k)))
+    byts = fp + basis + 128 * n * 6 + 128 * vec * 4
+    peak, _ = load_peaks()
+    bound = byts / (peak * 1e6)
+    return {"bytes": byts, "ms": round(bound, 3), "frac": round(bound / ms, 3), "peak_GBs": peak}
 
 
 def run_reference(args):

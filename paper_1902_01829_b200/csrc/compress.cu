@@ -1476,8 +1476,11 @@ void transpose_structure(const Layer& L, std::vector<int32_t>& cp, std::vector<i
 // Weight tree of basis B (generate_weight_tree, compression.hpp:213-256):
 // B = A (row basis, row stacks of S^T) or, with col, A's column basis over
 // the transposed layers (column stacks of S).
+// before(l), when set, is called right before level l's weight-tree launches
+// (after the parent products): the overlapped compression makes the chain
+// stream wait there for level l's projection only.
 void weights(Matrix& A, Matrix& B, bool col, TreePool& R, cudaStream_t s, Flops& fl, double& flops, const Part& pt,
-             double* tree_mem, Arena& ar) {
+             double* tree_mem, Arena& ar, const std::function<void(int)>& before = nullptr) {
   const int q = A.q;
   R.alloc(B, B.rank, B.rank, tree_mem);
   H2B_CUDA(cudaMemsetAsync(R.at(0), 0, sizeof(double) * B.rank[0] * B.rank[0], s));
@@ -1563,6 +1566,7 @@ void weights(Matrix& A, Matrix& B, bool col, TreePool& R, cudaStream_t s, Flops&
       }
       H2B_CUDA(cudaGetLastError());
     };
+    if (before) before(l);
     if (nseg == 1) {
       launch(src, Rl, 0, ditems, int64_t(items.size()), counters);
     } else {
@@ -1819,36 +1823,66 @@ struct ChainStream {
 // Side stream of compress(): fork(l) makes it wait for the main stream's
 // work issued so far (T(l) final), join() makes the main stream wait for it.
 // Disabled: b is the main stream itself and both are no-ops.
+// Lowest-priority side streams for the projections, ONE PER LEVEL: the
+// producers (orthogonalization, truncation) finish the levels bottom-up, the
+// weight tree consumes them top-down, so a small top level's projection must
+// not queue behind the big bottom levels' in one in-order stream.
 struct SideStream {
-  cudaStream_t s, b;
+  cudaStream_t s;
   bool on;
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t done = nullptr;
-  SideStream(bool enable, cudaStream_t main) : s(main), b(main), on(enable) {
+  int prio = 0;
+  std::vector<cudaStream_t> bs = std::vector<cudaStream_t>(kMaxLevels + 1, nullptr);
+  std::vector<cudaEvent_t> ev = std::vector<cudaEvent_t>(kMaxLevels + 1, nullptr);   // fork points
+  std::vector<cudaEvent_t> lev = std::vector<cudaEvent_t>(kMaxLevels + 1, nullptr);  // per-level completion
+  SideStream(bool enable, cudaStream_t main) : s(main), on(enable) {
     if (!on) return;
-    int lo = 0, hi = 0;
-    H2B_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    H2B_CUDA(cudaStreamCreateWithPriority(&b, cudaStreamNonBlocking, lo));  // lowest: fills the gaps
-    ev.resize(kMaxLevels + 1, nullptr);
-    for (auto& e : ev) H2B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    H2B_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    int hi = 0;
+    H2B_CUDA(cudaDeviceGetStreamPriorityRange(&prio, &hi));  // lowest: fills the gaps
   }
   ~SideStream() {
     if (!on) return;
-    cudaStreamSynchronize(b);
-    for (auto e : ev) cudaEventDestroy(e);
-    cudaEventDestroy(done);
-    cudaStreamDestroy(b);
+    for (int l = 0; l <= kMaxLevels; ++l) {
+      if (bs[l]) cudaStreamSynchronize(bs[l]);
+      if (lev[l]) cudaEventDestroy(lev[l]);
+      if (ev[l]) cudaEventDestroy(ev[l]);
+      if (bs[l]) cudaStreamDestroy(bs[l]);
+    }
   }
+  // the stream level l's side work goes to (the main stream when off)
+  cudaStream_t b(int l) {
+    if (!on) return s;
+    if (!bs[l]) {
+      H2B_CUDA(cudaStreamCreateWithPriority(&bs[l], cudaStreamNonBlocking, prio));
+      H2B_CUDA(cudaEventCreateWithFlags(&ev[l], cudaEventDisableTiming));
+      H2B_CUDA(cudaEventCreateWithFlags(&lev[l], cudaEventDisableTiming));
+    }
+    return bs[l];
+  }
+  // level l's side work starts after everything enqueued on the main stream so far
   void fork(int l) {
     if (!on) return;
+    cudaStream_t st = b(l);
     H2B_CUDA(cudaEventRecord(ev[l], s));
-    H2B_CUDA(cudaStreamWaitEvent(b, ev[l], 0));
+    H2B_CUDA(cudaStreamWaitEvent(st, ev[l], 0));
   }
+  // level l's side work is enqueued: mark its completion
+  void mark(int l) {
+    if (!on) return;
+    H2B_CUDA(cudaEventRecord(lev[l], b(l)));
+  }
+  // the main stream waits for level l's side work only
+  void wait(int l) {
+    if (!on || !bs[l]) return;
+    H2B_CUDA(cudaStreamWaitEvent(s, lev[l], 0));
+  }
+  // the main stream waits for all side work
   void join() {
     if (!on) return;
-    H2B_CUDA(cudaEventRecord(done, b));
-    H2B_CUDA(cudaStreamWaitEvent(s, done, 0));
+    for (int l = 0; l <= kMaxLevels; ++l)
+      if (bs[l]) {
+        H2B_CUDA(cudaEventRecord(lev[l], bs[l]));
+        H2B_CUDA(cudaStreamWaitEvent(s, lev[l], 0));
+      }
   }
 };
 
@@ -1977,7 +2011,8 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     double* fa = &fl_acc;
     return [Ap, Tp, fa, tri, want_sum, &PR, &fl, &pt, &side](int l) {
       side.fork(l);
-      project_level(*Ap, *Tp, *Tp, PR, l, tri, want_sum, fl, *fa, pt, side.b);
+      project_level(*Ap, *Tp, *Tp, PR, l, tri, want_sum, fl, *fa, pt, side.b(l));
+      side.mark(l);
     };
   };
   {
@@ -1988,27 +2023,44 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     if (!sym) orthogonalize(Cb, Toc, s, fl, r.flops_orthogonalize, pt, trees_col);
     r.time_orthogonalize_ms = t.stop();
   }
-  {
-    NvtxRange nv("h2b compress: project (orthogonal)");
+  if (!overlap) {
+    {
+      NvtxRange nv("h2b compress: project (orthogonal)");
+      Timer t(s);
+      for (int l = A.q; l >= 0; --l) project_level(A, To, To_c, PR, l, true, true, fl, r.flops_project_orth, pt, s);
+      n2 = project_rowsum(PR, pt, s);
+      project_finish(A, To, To_c, /*in_place=*/true, ar, s);
+      r.time_project_orth_ms = t.stop();
+    }
+    n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s, ws.arena);
+    pt.sum_f64(&n2, 1);
+    {
+      NvtxRange nv("h2b compress: weight tree");
+      Timer t(s);
+      weights(A, A, false, R, s, fl, r.flops_weights, pt, ws.rtree, ar);
+      if (!sym) weights(A, Cb, true, Rc, s, fl, r.flops_weights, pt, rtree_col, ar);  // transposed layers
+      r.time_weights_ms = t.stop();
+    }
+  } else {
+    // The weight tree goes top-down and level l needs only level l's projected
+    // blocks: its launches wait for that level's projection (side.wait), so
+    // the small, latency-bound top levels run while the big bottom levels are
+    // still being projected.  The projection phase then has no time of its
+    // own (reported as 0; its kernels run inside the orthogonalization and
+    // weight-tree phases).  The in-place orthogonal projection changes no
+    // layer shape, so project_finish and ||A||_F come after the weight tree.
+    NvtxRange nv("h2b compress: weight tree (overlapping the orthogonal projection)");
     Timer t(s);
-    if (!overlap)
-      for (int l = A.q; l >= 0; --l)
-        project_level(A, To, To_c, PR, l, true, true, fl, r.flops_project_orth, pt, s);
+    weights(A, A, false, R, s, fl, r.flops_weights, pt, ws.rtree, ar, [&side](int l) { side.wait(l); });
     side.join();
+    r.time_weights_ms = t.stop();
+    r.time_project_orth_ms = 0.0;
     n2 = project_rowsum(PR, pt, s);
     project_finish(A, To, To_c, /*in_place=*/true, ar, s);
-    r.time_project_orth_ms = t.stop();
+    n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s, ws.arena);
+    pt.sum_f64(&n2, 1);
   }
-  n2 += sumsq(A.dense.val, A.dense.nb * A.dense.block_stride(), s, ws.arena);
-  pt.sum_f64(&n2, 1);
   r.frobenius_norm = std::sqrt(n2);
-  {
-    NvtxRange nv("h2b compress: weight tree");
-    Timer t(s);
-    weights(A, A, false, R, s, fl, r.flops_weights, pt, ws.rtree, ar);
-    if (!sym) weights(A, Cb, true, Rc, s, fl, r.flops_weights, pt, rtree_col, ar);  // transposed layers
-    r.time_weights_ms = t.stop();
-  }
   for (int l = 0; l <= A.q; ++l) A.cpl[l].max_row = saved_max[l];
   double energy = 0.0;
   {
