@@ -12,7 +12,10 @@ RAW = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "dram__bytes.sum.per_second", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
        "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "sm__inst_executed_pipe_fp64.sum",
-       "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+       "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_tensor_subpipe_dmma.sum")
 
 
 def main(path):
