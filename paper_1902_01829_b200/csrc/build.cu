@@ -352,8 +352,8 @@ h2b_matrix* build_matrix(const h2b_build_config& cfg, int device, int nparts, in
   if (cfg.grid_order > kMaxOrder) throw Error(H2B_UNSUPPORTED, "grid_order > 16 not supported");
   int k = 1;
   for (int a = 0; a < cfg.dim; ++a) k *= cfg.grid_order;
-  if (k > kMaxDim || cfg.leaf_size > kMaxDim)
-    throw Error(H2B_UNSUPPORTED, "rank or leaf size > 64 not supported by the compiled kernels");
+  if (k > kMaxDimHmv || cfg.leaf_size > kMaxDimHmv)
+    throw Error(H2B_UNSUPPORTED, "rank or leaf size > 128 not supported by the compiled kernels");
 
   const std::vector<double> X = perturbed_grid(cfg.dim, cfg.n, cfg.perturbation, cfg.seed);
   const Tree T = cluster_tree(X, cfg.dim, cfg.n, cfg.leaf_size);

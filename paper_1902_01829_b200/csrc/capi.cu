@@ -429,10 +429,10 @@ void check_shape(int n, int m, int depth, const int32_t* ranks) {
   require(depth >= 0 && depth <= kMaxLevels - 1, "depth out of range");
   require(m >= 1, "leaf size must be positive");
   require(int64_t(m) << depth == n, "n must equal m * 2^depth");
-  if (m > kMaxDim) throw Error(H2B_UNSUPPORTED, "leaf size > 64 not supported by the compiled kernels");
+  if (m > kMaxDimHmv) throw Error(H2B_UNSUPPORTED, "leaf size > 128 not supported by the compiled kernels");
   for (int l = 0; l <= depth; ++l) {
     require(ranks[l] >= 0, "ranks must be non-negative");
-    if (ranks[l] > kMaxDim) throw Error(H2B_UNSUPPORTED, "rank > 64 not supported by the compiled kernels");
+    if (ranks[l] > kMaxDimHmv) throw Error(H2B_UNSUPPORTED, "rank > 128 not supported by the compiled kernels");
   }
   require(int64_t(1) << (depth + 1) < (int64_t(1) << kLayerShift), "tree too deep for the work-list encoding");
 }
@@ -872,8 +872,12 @@ h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx,
       Work& w = default_work(A);
       WorkUse u(w, s);
       ensure_work(A, w);
-      for (int v0 = 0; v0 < nvec; v0 += 16)
-        hmv_multi_device(A, w, xd + v0 * lx, lx, yd + v0 * ly, ly, std::min(16, nvec - v0), alpha, beta, s);
+      if (big_matrix(A)) {  // blocks > 64: the single-vector kernels, column by column
+        for (int v = 0; v < nvec; ++v) hmv_device(A, w, xd + v * lx, yd + v * ly, alpha, beta, s);
+      } else {
+        for (int v0 = 0; v0 < nvec; v0 += 16)
+          hmv_multi_device(A, w, xd + v0 * lx, lx, yd + v0 * ly, ly, std::min(16, nvec - v0), alpha, beta, s);
+      }
     }
     if (!dy)
       H2B_CUDA(cudaMemcpy2DAsync(Y, ldy * sizeof(double), ys.p, A.n * sizeof(double), A.n * sizeof(double),
@@ -1114,6 +1118,42 @@ void require_dcomm(const Matrix& A, const h2b_dcomm* comm) {
 }
 }  // namespace
 
+namespace {
+// One partitioned mat-vec on device vectors with workspace w (held by the caller).
+void part_hmv_device(Matrix& A, Work& w, const double* x, double* y, double alpha, double beta, int y_mode,
+                     const h2b_dcomm* comm, cudaStream_t s) {
+  const int nparts = 1 << A.part_s;
+  cudaEvent_t* ev = timing_slots(A);  // upsweep + exchange | coupling + dense | downsweep + y
+  if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
+  sweep_begin(w, A, s);
+  launch_up_leaf(A, x, w.xc.p, w.xhat.p, s);
+  if (A.part_s > 0) launch_gather(A.perm.p, x, w.xc.p, A.n, s);  // dense blocks read remote columns
+  if (A.q > A.part_s) launch_up_fused(w, A, w.xhat.p, s, A.q, A.part_s + 1, true);
+  if (nparts > 1) {  // one all-gather of every level >= s
+    const int64_t cnt = part_exchange_count(A, 1);
+    if (w.xg.n < size_t(cnt) * nparts) w.xg.alloc(size_t(cnt) * nparts);
+    launch_pack_xhat(A, 1, w.xhat.p, w.xg.p, s);
+    dcomm_allgather(comm, w.xg.p, cnt, s);
+    launch_unpack_xhat(A, 1, w.xg.p, w.xhat.p, s);
+  }
+  if (A.part_s >= 1) launch_up_fused(w, A, w.xhat.p, s, A.part_s, 1, false);  // replicated top
+  if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
+  launch_bsr(A, A.work.p, A.nwork, w.xc.p, w.yc.p, w.xhat.p, w.yhat.p, s);
+  if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
+  if (A.q >= 1) launch_down_fused(w, A, w.yhat.p, s, true);
+  if (y_mode == H2B_Y_OWNED || nparts == 1) {
+    launch_down_leaf(A, w.yhat.p, w.yc.p, y, alpha, beta, true, s);  // owned rows, original order
+  } else {
+    const int64_t slice = A.n / nparts;
+    if (w.yg.n < size_t(A.n)) w.yg.alloc(A.n);
+    launch_down_leaf(A, w.yhat.p, w.yc.p, w.yg.p + A.part_g * slice, 1.0, 0.0, false, s);
+    dcomm_allgather(comm, w.yg.p, slice, s);
+    launch_scatter(A.perm.p, w.yg.p, y, A.n, alpha, beta, s);
+  }
+  if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
+}
+}  // namespace
+
 h2b_status h2b_part_hmv(h2b_matrix* Ah, const double* x, double* y, double alpha, double beta, int y_mode,
                         const h2b_dcomm* comm, void* stream) {
   return guarded([&] {
@@ -1124,38 +1164,10 @@ h2b_status h2b_part_hmv(h2b_matrix* Ah, const double* x, double* y, double alpha
     DeviceGuard g(A.device);
     require(resolve_device(H2B_PTR_AUTO, x) && resolve_device(H2B_PTR_AUTO, y), "h2b_part_hmv: device vectors");
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
-    const int nparts = 1 << A.part_s;
     Work& w = default_work(A);
     WorkUse u(w, s);
     ensure_work(A, w);
-    cudaEvent_t* ev = timing_slots(A);  // upsweep + exchange | coupling + dense | downsweep + y
-    if (ev) H2B_CUDA(cudaEventRecord(ev[0], s));
-    sweep_begin(w, A, s);
-    launch_up_leaf(A, x, w.xc.p, w.xhat.p, s);
-    if (A.part_s > 0) launch_gather(A.perm.p, x, w.xc.p, A.n, s);  // dense blocks read remote columns
-    if (A.q > A.part_s) launch_up_fused(w, A, w.xhat.p, s, A.q, A.part_s + 1, true);
-    if (nparts > 1) {  // one all-gather of every level >= s
-      const int64_t cnt = part_exchange_count(A, 1);
-      if (w.xg.n < size_t(cnt) * nparts) w.xg.alloc(size_t(cnt) * nparts);
-      launch_pack_xhat(A, 1, w.xhat.p, w.xg.p, s);
-      dcomm_allgather(comm, w.xg.p, cnt, s);
-      launch_unpack_xhat(A, 1, w.xg.p, w.xhat.p, s);
-    }
-    if (A.part_s >= 1) launch_up_fused(w, A, w.xhat.p, s, A.part_s, 1, false);  // replicated top
-    if (ev) H2B_CUDA(cudaEventRecord(ev[1], s));
-    launch_bsr(A, A.work.p, A.nwork, w.xc.p, w.yc.p, w.xhat.p, w.yhat.p, s);
-    if (ev) H2B_CUDA(cudaEventRecord(ev[2], s));
-    if (A.q >= 1) launch_down_fused(w, A, w.yhat.p, s, true);
-    if (y_mode == H2B_Y_OWNED || nparts == 1) {
-      launch_down_leaf(A, w.yhat.p, w.yc.p, y, alpha, beta, true, s);  // owned rows, original order
-    } else {
-      const int64_t slice = A.n / nparts;
-      if (w.yg.n < size_t(A.n)) w.yg.alloc(A.n);
-      launch_down_leaf(A, w.yhat.p, w.yc.p, w.yg.p + A.part_g * slice, 1.0, 0.0, false, s);
-      dcomm_allgather(comm, w.yg.p, slice, s);
-      launch_scatter(A.perm.p, w.yg.p, y, A.n, alpha, beta, s);
-    }
-    if (ev) H2B_CUDA(cudaEventRecord(ev[3], s));
+    part_hmv_device(A, w, x, y, alpha, beta, y_mode, comm, s);
   });
 }
 
@@ -1177,6 +1189,10 @@ h2b_status h2b_part_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t
     Work& w = default_work(A);
     WorkUse u(w, s);
     ensure_work(A, w);
+    if (big_matrix(A)) {  // blocks > 64: the single-vector kernels, column by column
+      for (int v = 0; v < nvec; ++v) part_hmv_device(A, w, X + v * ldx, Y + v * ldy, alpha, beta, y_mode, comm, s);
+      return;
+    }
     for (int v0 = 0; v0 < nvec; v0 += NV) {
       const int nv = std::min(NV, nvec - v0);
       const double* Xv = X + v0 * ldx;

@@ -1937,8 +1937,18 @@ uint64_t counted_footprint(const Matrix& A, const Part& pt) {
   return e * sizeof(double);
 }
 
+// The compression kernels (register Householder, 64-thread Jacobi, 64 x 64
+// DMMA projection tiles) cover ranks and leaf sizes up to 64; the mat-vec
+// kernels go to 128 (k_hmv_big.cu).
+void require_compress_dims(const Matrix& B, const char* what) {
+  if (big_basis(B))
+    throw Error(H2B_UNSUPPORTED, std::string(what) + ": rank or leaf size > 64 not supported by the compression kernels");
+}
+
 void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_comm* comm) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
+  require_compress_dims(A, "compress");
+  if (!A.symmetric) require_compress_dims(*A.colb, "compress");
   DeviceGuard g(A.device);
   // The dependency chain (orthogonalization, weights, truncation) runs on a
   // highest-priority stream ordered after the handle's stream; the
@@ -2115,6 +2125,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
 
 // orthogonalize_basis(B) (compression.hpp:69-126): t_dev gets T (k_l x k_l per node).
 void phase_orthogonalize(Matrix& B, double* t_dev, cudaStream_t s) {
+  require_compress_dims(B, "orthogonalize_basis");
   Flops fl;
   double f = 0;
   TreePool T;
@@ -2167,6 +2178,7 @@ void phase_project(Matrix& S, const double* tr, const std::vector<int>& tr_rows,
 // generate_weight_tree(B, S) (compression.hpp:213-256): r_dev gets R (k_l x k_l
 // per node, upper triangular; R^0 = 0).
 void phase_weights(Matrix& S, Matrix& B, double* r_dev, cudaStream_t s) {
+  require_compress_dims(B, "generate_weight_tree");
   require(S.q == B.q, "generate_weight_tree: depth mismatch");
   for (int l = 1; l <= S.q; ++l)
     require(S.cpl[l].nb == 0 || S.cpl[l].br == B.rank[l], "generate_weight_tree: dim mismatch");
@@ -2187,6 +2199,7 @@ void phase_weights(Matrix& S, Matrix& B, double* r_dev, cudaStream_t s) {
 // energy[l] the discarded energy of level l.
 void phase_truncate(Matrix& B, const double* r_dev, double eps, double* t_dev, std::vector<double>& energy,
                     cudaStream_t s) {
+  require_compress_dims(B, "truncate_basis");
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
   const std::vector<int> old = B.rank;
   Flops fl;
@@ -2218,6 +2231,7 @@ void orthogonalize_matrix(Matrix& A, double* t_out, bool col) {
   DeviceGuard g(A.device);
   cudaStream_t s = A.stream;
   Matrix& B = col ? A.col_basis() : A;
+  require_compress_dims(B, "orthogonalize_basis");
   Flops fl;
   double f = 0;
   TreePool T;

@@ -57,9 +57,11 @@ struct NvtxRange {
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
-// Largest block dimension the compiled warp kernels cover (rows owned by a
-// lane pair: 2 * 32 lanes).
+// Largest block dimension the fast warp kernels cover (rows owned by a lane
+// pair: 2 * 32 lanes) and the compression kernels accept; mat-vec blocks up
+// to kMaxDimHmv take the k_hmv_big.cu kernels (two row pairs per lane).
 constexpr int kMaxDim = 64;
+constexpr int kMaxDimHmv = 128;
 constexpr int kMaxLevels = 31;
 
 // Device buffer (cudaMalloc / cudaFree).
@@ -262,6 +264,18 @@ void launch_gather(const int32_t* perm, const double* x, double* xc, int64_t n, 
 // a cluster-order y (partitioned mat-vec).
 void launch_scatter(const int32_t* perm, const double* ys, double* y, int64_t n, double alpha, double beta,
                     cudaStream_t s);
+
+// ---- blocks of 65..128 rows / columns (k_hmv_big.cu) ----
+bool big_basis(const Matrix& B);   // leaf size or some rank > kMaxDim
+bool big_matrix(const Matrix& A);  // ... of the row or the column basis
+void launch_up_leaf_big(const Matrix& B, const double* x, double* xc, double* xhat, cudaStream_t s,
+                        bool cluster_order);
+void launch_up_level_big(const Matrix& B, int l, double* xhat, cudaStream_t s, int64_t p0, int64_t p1);
+void launch_down_level_big(const Matrix& A, int l, double* yhat, cudaStream_t s, int64_t c0, int64_t c1);
+void launch_down_leaf_big(const Matrix& A, const double* yhat, const double* yc, double* y, double alpha,
+                          double beta, bool to_user, cudaStream_t s);
+void launch_bsr_big(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense, double* ydense,
+                    const double* xh, double* yh, cudaStream_t s, const Matrix* xb);
 
 // ---- workspaces (capi.cu) ----
 // (Re)size w for A's current layout; the default workspace of A.

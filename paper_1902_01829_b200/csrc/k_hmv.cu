@@ -14,6 +14,7 @@
 // (evict-first) 128-bit loads; node vectors stay L2-resident.
 #include "dataflow.cuh"
 #include "h2b_internal.hpp"
+#include "warp_gemv.cuh"
 
 #include <algorithm>
 #include <numeric>
@@ -21,114 +22,8 @@
 namespace h2b {
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;  // 8 warps per CTA
-
-__device__ __forceinline__ double2 ld_stream(const double* p) {
-  return __ldcs(reinterpret_cast<const double2*>(p));
-}
-
-__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
-__device__ __forceinline__ int64_t warp_global() {
-  return (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-}
-__device__ __forceinline__ int64_t warp_count() {
-  return (int64_t(gridDim.x) * blockDim.x) >> 5;
-}
-
-// Transposed product for the column group g in {0,1}:
-//   returns out[2*lane + g] = sum_r A[r, 2*lane+g] * v[r]  (+ B^T w when TWO)
-// A, B: column-major, leading dim ld (even), `cols` columns; the lane's row
-// pair (2*lane, 2*lane+1) is valid when row_ok.
-template <bool TWO>
-__device__ __forceinline__ double gemvT_group(const double* __restrict__ A,
-                                              const double* __restrict__ B, int ld, int cols,
-                                              int g, double v0, double v1, double w0, double w1,
-                                              bool row_ok) {
-  const int lane = lane_id();
-  const int r = 2 * lane;
-  // Streaming reduce-scatter: each chunk of 8 columns is reduced over lane
-  // bits 0..2 right away (7 shuffles), leaving one value per chunk; the 4
-  // chunk values are then reduced over lane bits 3..4 (3 shuffles).  Lane L
-  // ends with column index L of the group; 31 shuffles per 32 columns, and
-  // only one chunk of loads is live at a time.
-  double hv[4] = {0.0, 0.0, 0.0, 0.0};
-  const int64_t step = 2 * int64_t(ld);
-  const double* pa = A + int64_t(g) * ld + r;
-  const double* pb = TWO ? B + int64_t(g) * ld + r : nullptr;
-#pragma unroll 1
-  for (int h = 0; h < 4; ++h) {
-    double p[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int c = 2 * (8 * h + t) + g;
-      const bool ok = c < cols && row_ok;
-      const double2 a = ok ? ld_stream(pa) : make_double2(0.0, 0.0);
-      pa += step;
-      double acc = a.x * v0 + a.y * v1;
-      if (TWO) {
-        const double2 b = ok ? ld_stream(pb) : make_double2(0.0, 0.0);
-        pb += step;
-        acc += b.x * w0 + b.y * w1;
-      }
-      p[t] = acc;
-    }
-#pragma unroll
-    for (int s = 1, n = 8; s <= 4; s <<= 1, n >>= 1) {
-      const bool up = (lane & s) != 0;
-#pragma unroll
-      for (int i = 0; i < n / 2; ++i) {
-        const double keep = up ? p[2 * i + 1] : p[2 * i];
-        const double send = up ? p[2 * i] : p[2 * i + 1];
-        p[i] = keep + __shfl_xor_sync(kFull, send, s);
-      }
-    }
-    hv[0] = h == 0 ? p[0] : hv[0];
-    hv[1] = h == 1 ? p[0] : hv[1];
-    hv[2] = h == 2 ? p[0] : hv[2];
-    hv[3] = h == 3 ? p[0] : hv[3];
-    if (2 * (8 * h + 8) + g >= cols) break;  // remaining chunks are all padding
-  }
-#pragma unroll
-  for (int s = 8, n = 4; s <= 16; s <<= 1, n >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < n / 2; ++i) {
-      const double keep = up ? hv[2 * i + 1] : hv[2 * i];
-      const double send = up ? hv[2 * i] : hv[2 * i + 1];
-      hv[i] = keep + __shfl_xor_sync(kFull, send, s);
-    }
-  }
-  return hv[0];
-}
-
-// Non-transposed product: returns (acc0, acc1) for rows (2*lane, 2*lane+1)
-// of A (ld x cols) times v, where v is held in pair layout (lane L has
-// v[2L], v[2L+1]) and broadcast with shuffles.
-__device__ __forceinline__ void gemvN_pair(const double* __restrict__ A, int ld, int cols,
-                                           double a0, double a1, bool row_ok, double& acc0,
-                                           double& acc1) {
-  const int r = 2 * lane_id();
-  acc0 = 0.0;
-  acc1 = 0.0;
-  for (int c0 = 0; c0 < cols; c0 += 8) {
-    double2 col[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int c = c0 + u;
-      col[u] = (c < cols && row_ok) ? ld_stream(A + int64_t(c) * ld + r) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int c = c0 + u;  // warp-uniform
-      if (c < cols) {
-        const double s = __shfl_sync(kFull, (c & 1) ? a1 : a0, c >> 1);
-        acc0 += col[u].x * s;
-        acc1 += col[u].y * s;
-      }
-    }
-  }
-}
+using namespace wg;
 
 __global__ void __launch_bounds__(kThreads, 2) k_up_leaf(const double* __restrict__ x,
                                                       const int32_t* __restrict__ perm,
@@ -400,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
 }
 
 // block_sparse_mv(L, x, y, alpha, beta) for one generic layer (any block_rows x
-// block_cols, brows / bcols <= 64), in the reference's exact arithmetic
+// block_cols, brows / bcols <= 128), in the reference's exact arithmetic
 // (bsr.hpp:50-73): y_r = (beta == 0 ? 0 : beta y_r), then for every block in
 // col_idx order and every column j, y_r += col_j * (alpha x_j) -- unfused
 // multiply and add, so the result is bitwise the reference's.  Warp per block
@@ -413,9 +308,9 @@ __global__ void __launch_bounds__(kThreads) k_bsr_exact(const double* __restrict
   const int lane = lane_id();
   for (int64_t r = warp_global(); r < rows; r += warp_count()) {
     double* yr = y + r * br;
-    double acc[2];
+    double acc[4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < 4; ++h) {
       const int i = lane + 32 * h;
       acc[h] = (i < br && beta != 0.0) ? __dmul_rn(beta, yr[i]) : 0.0;
     }
@@ -425,14 +320,14 @@ __global__ void __launch_bounds__(kThreads) k_bsr_exact(const double* __restrict
       for (int j = 0; j < bc; ++j) {
         const double xv = __dmul_rn(alpha, __ldg(xs + j));
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 4; ++h) {
           const int i = lane + 32 * h;
           if (i < br) acc[h] = __dadd_rn(acc[h], __dmul_rn(blk[i + int64_t(j) * ld], xv));
         }
       }
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < 4; ++h)
       if (lane + 32 * h < br) yr[lane + 32 * h] = acc[h];
   }
 }
@@ -496,6 +391,7 @@ unsigned flat_grid(int64_t n) {
 
 void launch_up_leaf(const Matrix& B, const double* x, double* xc, double* xhat, cudaStream_t s,
                     bool cluster_order) {
+  if (big_basis(B)) return launch_up_leaf_big(B, x, xc, xhat, s, cluster_order);
   const int64_t nl = B.own_count(B.q);
   k_up_leaf<<<warp_grid(nl), kThreads, 0, s>>>(x, cluster_order ? nullptr : B.perm.p, B.leaf.p, B.m, B.ldm,
                                                B.rank[B.q], nl, B.own_begin(B.q), xc, xhat + B.vec_off[B.q]);
@@ -512,6 +408,7 @@ void launch_up_level(const Matrix& B, int l, double* xhat, cudaStream_t s, int64
     H2B_CUDA(cudaMemsetAsync(xp + p0 * kp, 0, size_t(np) * kp * sizeof(double), s));
     return;
   }
+  if (big_basis(B)) return launch_up_level_big(B, l, xhat, s, p0, p1);
   k_up_level<<<warp_grid(np), kThreads, 0, s>>>(B.transfer.p + B.tr_off[l], B.ld(l), kc, kp, p0, p1,
                                                 B.tr_begin(l), xhat + B.vec_off[l], xp);
   H2B_CUDA(cudaGetLastError());
@@ -539,6 +436,11 @@ void sweep_begin(Work& w, const Matrix& A, cudaStream_t s) {
 }
 
 void launch_up_fused(Work& w, const Matrix& B, double* xhat, cudaStream_t s, int l_hi, int l_lo, bool own) {
+  if (big_basis(B)) {  // blocks > 64: one launch per level (k_hmv_big.cu)
+    for (int l = l_hi; l >= l_lo; --l)
+      launch_up_level(B, l, xhat, s, own ? B.own_begin(l - 1) : 0, own ? B.own_end(l - 1) : B.nodes(l - 1));
+    return;
+  }
   SweepTable T{};
   T.q = l_hi;
   int64_t tot = 0;
@@ -569,6 +471,11 @@ void launch_up_fused(Work& w, const Matrix& B, double* xhat, cudaStream_t s, int
 }
 
 void launch_down_fused(Work& w, const Matrix& A, double* yhat, cudaStream_t s, bool own) {
+  if (big_basis(A)) {  // blocks > 64: one launch per level (k_hmv_big.cu)
+    for (int l = 1; l <= A.q; ++l)
+      launch_down_level(A, l, yhat, s, own ? A.own_begin(l) : 0, own ? A.own_end(l) : A.nodes(l));
+    return;
+  }
   const int q = A.q;
   SweepTable T{};
   T.q = 0;  // the root's y^ is final (after the coupling multiply)
@@ -604,6 +511,7 @@ void launch_down_level(const Matrix& A, int l, double* yhat, cudaStream_t s, int
   if (c1 < 0) c1 = A.nodes(l);
   const int64_t nc = c1 - c0;
   if (kc == 0 || kp == 0 || nc <= 0) return;
+  if (big_basis(A)) return launch_down_level_big(A, l, yhat, s, c0, c1);
   k_down_level<<<warp_grid(nc), kThreads, 0, s>>>(A.transfer.p + A.tr_off[l], A.ld(l), kc, kp, c0, c1,
                                                   A.tr_begin(l), yhat + A.vec_off[l - 1], yhat + A.vec_off[l]);
   H2B_CUDA(cudaGetLastError());
@@ -611,6 +519,7 @@ void launch_down_level(const Matrix& A, int l, double* yhat, cudaStream_t s, int
 
 void launch_down_leaf(const Matrix& A, const double* yhat, const double* yc, double* y, double alpha,
                       double beta, bool to_user, cudaStream_t s) {
+  if (big_basis(A)) return launch_down_leaf_big(A, yhat, yc, y, alpha, beta, to_user, s);
   const int64_t nl = A.own_count(A.q);
   k_down_leaf<<<warp_grid(nl), kThreads, 0, s>>>(A.leaf.p, A.ldm, A.m, A.rank[A.q], nl, A.own_begin(A.q),
                                                  yhat + A.vec_off[A.q], yc, A.perm.p, y, alpha, beta,
@@ -621,6 +530,7 @@ void launch_down_leaf(const Matrix& A, const double* yhat, const double* yc, dou
 void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const double* xdense,
                 double* ydense, const double* xh, double* yh, cudaStream_t s, const Matrix* xb) {
   if (nwork == 0) return;
+  if (big_matrix(A)) return launch_bsr_big(A, work, nwork, xdense, ydense, xh, yh, s, xb);
   const std::vector<int64_t>& xoff = xb ? xb->vec_off : A.vec_off;
   LayerTable T{};
   for (int l = 0; l <= A.q; ++l) {

@@ -116,9 +116,9 @@ h2b_matrix* make_basis(const h2b_basis_desc& d, int device) {
   require(d.ranks && (d.leaf || d.ranks[d.depth] == 0), "null pointer in basis descriptor");
   for (int l = 0; l <= d.depth; ++l) {
     require(d.ranks[l] >= 0, "ranks must be non-negative");
-    if (d.ranks[l] > kMaxDim) throw Error(H2B_UNSUPPORTED, "rank > 64 not supported by the compiled kernels");
+    if (d.ranks[l] > kMaxDimHmv) throw Error(H2B_UNSUPPORTED, "rank > 128 not supported by the compiled kernels");
   }
-  if (d.m > kMaxDim) throw Error(H2B_UNSUPPORTED, "leaf size > 64 not supported by the compiled kernels");
+  if (d.m > kMaxDimHmv) throw Error(H2B_UNSUPPORTED, "leaf size > 128 not supported by the compiled kernels");
   need_device_public(device);
   std::unique_ptr<h2b_matrix> A(new h2b_matrix);
   A->device = device;
@@ -154,8 +154,8 @@ void check_layer_desc(const h2b_layer_desc& L, int64_t want_rows, int64_t want_c
   if (want_rows >= 0) require(L.block_rows == want_rows && L.block_cols == want_cols,
                               "tree level: block_rows / block_cols must be 2^l");
   require(L.row_ptr != nullptr, "layer: null row_ptr");
-  if (L.brows > kMaxDim || L.bcols > kMaxDim)
-    throw Error(H2B_UNSUPPORTED, "block dimension > 64 not supported by the compiled kernels");
+  if (L.brows > kMaxDimHmv || L.bcols > kMaxDimHmv)
+    throw Error(H2B_UNSUPPORTED, "block dimension > 128 not supported by the compiled kernels");
 }
 
 // A coupling-only Matrix (MatrixTree): level l holds 2^l x 2^l blocks of
