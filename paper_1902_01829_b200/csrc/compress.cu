@@ -855,6 +855,7 @@ __global__ void __launch_bounds__(64) k_jacobi64(const double* __restrict__ Jall
   __shared__ __align__(16) double cols[64 * LD];
   __shared__ double nrm2[64];
   __shared__ double nrm[64];
+  __shared__ double dpart[64];  // half dot products of the round (rows of this lane's half)
   __shared__ int flag, big;
   const int c = threadIdx.x;
   const int n = r + (r & 1);  // zero pad column when odd
@@ -893,21 +894,29 @@ __global__ void __launch_bounds__(64) k_jacobi64(const double* __restrict__ Jall
     for (int rd = 0; rd < m1; ++rd) {
       __syncthreads();  // this round's columns are published
       bool rot = false;
+      // round-robin (circle) partner of column c in round rd
+      const int pt = c == m1 ? rd : (c == rd ? m1 : (2 * rd - c + 2 * m1) % m1);
+      const bool is_p = c < pt;
       if (c < n) {
-        // round-robin (circle) partner of column c in round rd
-        const int pt = c == m1 ? rd : (c == rd ? m1 : (2 * rd - c + 2 * m1) % m1);
-        const double2* pc = reinterpret_cast<const double2*>(cols + pt * LD);
+        // the pair's dot product in two halves: column p's lane reads rows
+        // 0..31 of the partner, column q's lane rows 32..63 (half the shared
+        // memory reads of the round's dot products; the kernel is bound by them)
+        const int h0 = is_p ? 0 : 32;
+        const double2* pc = reinterpret_cast<const double2*>(cols + pt * LD + h0);
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < 64; i += 2) {
+        for (int i = 0; i < 32; i += 2) {
           const double2 x = pc[i / 2];
-          d0 = fma(g[i], x.x, d0);
-          d1 = fma(g[i + 1], x.y, d1);
+          d0 = fma(is_p ? g[i] : g[i + 32], x.x, d0);
+          d1 = fma(is_p ? g[i + 1] : g[i + 33], x.y, d1);
         }
-        const double d = d0 + d1;
-        asm volatile("" ::: "memory");  // re-read the partner below: 64 registers saved
+        dpart[c] = d0 + d1;
+      }
+      __syncthreads();  // both halves of every pair's dot product
+      if (c < n) {
+        const double d = is_p ? dpart[c] + dpart[pt] : dpart[pt] + dpart[c];  // (rows 0..31) + (rows 32..63)
+        const double2* pc = reinterpret_cast<const double2*>(cols + pt * LD);
         const double b = nrm2[pt];
-        const bool is_p = c < pt;
         const double ap = is_p ? a : b, aq = is_p ? b : a;
         // skip rule of linalg.hpp:155-160 (sqrt(a) sqrt(b): no underflow)
         const double sab = sqrt(ap) * sqrt(aq);
