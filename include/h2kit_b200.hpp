@@ -32,10 +32,13 @@
 // address plus a fingerprint (shape, pool addresses, sampled values) -- the
 // role HmvContext plays on the CPU.  compress() refreshes the host object
 // from the device.  A caller that mutates unsampled entries of A in place
-// must call h2kit_b200::invalidate(A).
+// must call h2kit_b200::invalidate(A); with H2KIT_B200_STRICT=1 in the
+// environment the fingerprint covers every value instead (a host pass over
+// the whole matrix per call: for tests, not for production).
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -161,10 +164,14 @@ inline std::mutex& cache_mutex() {
 inline uint64_t fingerprint(const H2Matrix<double>& A) {
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+  static const bool strict = [] {
+    const char* e = std::getenv("H2KIT_B200_STRICT");
+    return e && *e && *e != '0';
+  }();
   auto sample = [&](const std::vector<double>& v) {
     mix(v.size());
     mix(reinterpret_cast<uintptr_t>(v.data()));
-    const size_t step = v.size() / 61 + 1;
+    const size_t step = strict ? 1 : v.size() / 1021 + 1;
     for (size_t i = 0; i < v.size(); i += step) {
       uint64_t b;
       std::memcpy(&b, &v[i], sizeof(b));
@@ -265,10 +272,14 @@ inline void pull(h2b_matrix* h, H2Matrix<double>& A) {
 
 // ---- component objects (BasisTree / MatrixTree / BSRLayer) ----------------
 inline void mix_sample(uint64_t& h, const std::vector<double>& v) {
+  static const bool strict = [] {
+    const char* e = std::getenv("H2KIT_B200_STRICT");
+    return e && *e && *e != '0';
+  }();
   auto mix = [&](uint64_t x) { h = (h ^ x) * 1099511628211ull; };
   mix(v.size());
   mix(reinterpret_cast<uintptr_t>(v.data()));
-  const size_t step = v.size() / 61 + 1;
+  const size_t step = strict ? 1 : v.size() / 1021 + 1;
   for (size_t i = 0; i < v.size(); i += step) {
     uint64_t b;
     std::memcpy(&b, &v[i], sizeof(b));

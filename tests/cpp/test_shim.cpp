@@ -359,6 +359,22 @@ void scalar_and_growing_projection() {
   CHECK(S2.levels[0].values == S3.levels[0].values);
 }
 
+// A host-side edit of an entry the default fingerprint does not sample:
+// invalidate(A) (or H2KIT_B200_STRICT=1, checked by the Python runner) makes
+// the next call see it.
+void mutation_then_invalidate() {
+  H2Matrix<double> A = kernel_matrix(2, 2048, 8);
+  std::vector<double> x(A.n, 1.0), y0(A.n), y1(A.n), yr(A.n);
+  h2kit_b200::hmv(A, x.data(), y0.data());
+  auto& v = A.coupling.levels[A.depth()].values;
+  v[v.size() / 2 + 3] += 1.0;  // off the sampling grid
+  h2kit_b200::invalidate(A);
+  h2kit_b200::hmv(A, x.data(), y1.data());
+  h2kit::hmv(A, x.data(), yr.data());
+  CHECK(rel(y1, yr) <= 1e-12);
+  CHECK(rel(y1, y0) > 0.0);
+}
+
 void errors_are_invalid_argument() {
   H2Matrix<double> A = kernel_matrix(2, 1024, 8);
   bool threw = false;
@@ -385,6 +401,7 @@ int main() {
   run("non-symmetric orthogonalize (row and column bases) matches the reference", nonsymmetric_orthogonalize);
   run("component phase API (BasisTree / MatrixTree / BSRLayer) matches the reference", component_phases_match_reference);
   run("scalar and growing projections", scalar_and_growing_projection);
+  run("host-side mutation + invalidate is seen by the next call", mutation_then_invalidate);
   run("invalid arguments throw std::invalid_argument", errors_are_invalid_argument);
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;

@@ -18,3 +18,13 @@ def test_cpp_shim_suite(gpu):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+def test_cpp_shim_suite_strict_fingerprint(gpu):
+    """The same suite with full-content fingerprints (H2KIT_B200_STRICT=1)."""
+    if not os.path.exists(BIN):
+        pytest.skip("tests/cpp/test_shim not built (needs the reference headers at build time)")
+    env = dict(os.environ, H2KIT_B200_STRICT="1")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
