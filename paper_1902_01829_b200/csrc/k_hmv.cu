@@ -423,7 +423,7 @@ unsigned persistent_grid(const void* kernel) {
 }  // namespace
 
 void sweep_begin(Work& w, const Matrix& A, cudaStream_t s) {
-  const int64_t nodes = int64_t(2) << A.q;
+  const int64_t nodes = int64_t(4) << A.q;  // 2^(q+1) - 1 nodes, x 2 for the split 16-vector sweeps
   if (w.flag.n < size_t(nodes) || !w.ticket.p) {
     // stream-ordered zeroing: the kernels of this mat-vec run after it
     w.flag.alloc(nodes);

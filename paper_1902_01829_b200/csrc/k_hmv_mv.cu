@@ -59,15 +59,18 @@ __device__ __forceinline__ double2 ld_stream2(const double* p) {
   return v;
 }
 
-struct Acc {
-  double c[8][2][2];  // 8 row tiles (M <= 64) x 2 column tiles (16 vectors)
+// 8 row tiles (M <= 64) x NY column tiles (8 NY vectors)
+template <int NY>
+struct AccT {
+  double c[8][NY][2];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int x = 0; x < 8; ++x)
 #pragma unroll
-      for (int y = 0; y < 2; ++y) c[x][y][0] = c[x][y][1] = 0.0;
+      for (int y = 0; y < NY; ++y) c[x][y][0] = c[x][y][1] = 0.0;
   }
 };
+using Acc = AccT<2>;  // 16 vectors
 
 // acc (M x 16) += op(A) (M x K) * B (K x 16), B vector-minor (B[p * 16 + v]).
 // op(A)(i, p) = TA ? A[p + i * lda] : A[i + p * lda]; A streamed (evict-first).
@@ -110,8 +113,9 @@ __device__ __forceinline__ void mma_panel(Acc& acc, const double* __restrict__ A
   }
 }
 
-// out (M x 16, vector-minor) = acc (+ out when add); natural tile layout.
-__device__ __forceinline__ void store_panel(const Acc& acc, double* __restrict__ out, int M, bool add) {
+// out (M x 8 NY of a vector-minor panel) = acc (+ out when add); natural tile layout.
+template <int NY>
+__device__ __forceinline__ void store_panel(const AccT<NY>& acc, double* __restrict__ out, int M, bool add) {
   const int lane = lane_id();
   const int fr = lane >> 2, fc = 2 * (lane & 3);
 #pragma unroll
@@ -119,7 +123,7 @@ __device__ __forceinline__ void store_panel(const Acc& acc, double* __restrict__
     const int i = 8 * x + fr;
     if (i >= M) continue;
 #pragma unroll
-    for (int y = 0; y < 2; ++y) {
+    for (int y = 0; y < NY; ++y) {
       double2* o = reinterpret_cast<double2*>(out + i * NV + 8 * y + fc);
       double2 v = make_double2(acc.c[x][y][0], acc.c[x][y][1]);
       if (add) {
@@ -139,8 +143,8 @@ __device__ __forceinline__ void store_panel(const Acc& acc, double* __restrict__
 // (j = j0 + fk): A by one 16-byte load per row tile, B by the callback
 // bpair(j, y) -> (B(2j, 8y + fr), B(2j + 1, 8y + fr)), which must return 0
 // for rows >= K.  UNROLL pair-steps (8 contraction rows each) in flight.
-template <int UNROLL, int POL, class BPair>
-__device__ __forceinline__ void mma_T_pairs(Acc& acc, const double* __restrict__ A, int lda, int M, int K,
+template <int UNROLL, int POL, int NY = 2, class BPair>
+__device__ __forceinline__ void mma_T_pairs(AccT<NY>& acc, const double* __restrict__ A, int lda, int M, int K,
                                             BPair bpair) {
   const int lane = lane_id();
   const int fr = lane >> 2, fk = lane & 3;
@@ -150,9 +154,9 @@ __device__ __forceinline__ void mma_T_pairs(Acc& acc, const double* __restrict__
     const int j = j0 + fk;
     const bool ok = j < np;
     const bool hi = 2 * j + 1 < K;
-    double2 b[2];
+    double2 b[NY];
 #pragma unroll
-    for (int y = 0; y < 2; ++y) b[y] = bpair(j, y, ok);
+    for (int y = 0; y < NY; ++y) b[y] = bpair(j, y, ok);
     double2 a[8];
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
@@ -163,10 +167,10 @@ __device__ __forceinline__ void mma_T_pairs(Acc& acc, const double* __restrict__
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
       if (8 * x < M) {  // warp-uniform
-        dmma(acc.c[x][0][0], acc.c[x][0][1], a[x].x, b[0].x);
-        dmma(acc.c[x][1][0], acc.c[x][1][1], a[x].x, b[1].x);
-        dmma(acc.c[x][0][0], acc.c[x][0][1], a[x].y, b[0].y);
-        dmma(acc.c[x][1][0], acc.c[x][1][1], a[x].y, b[1].y);
+#pragma unroll
+        for (int y = 0; y < NY; ++y) dmma(acc.c[x][y][0], acc.c[x][y][1], a[x].x, b[y].x);
+#pragma unroll
+        for (int y = 0; y < NY; ++y) dmma(acc.c[x][y][0], acc.c[x][y][1], a[x].y, b[y].y);
       }
     }
   }
@@ -178,8 +182,8 @@ __device__ __forceinline__ void mma_T_pairs(Acc& acc, const double* __restrict__
 // row fr): one 16-byte load per tile pair and k-step.
 __device__ __forceinline__ int prow(int x, int fr) { return 16 * (x >> 1) + 2 * fr + (x & 1); }
 
-template <int UNROLL, int POL>
-__device__ __forceinline__ void mma_N_pairs(Acc& acc, const double* __restrict__ A, int lda, int M, int K,
+template <int UNROLL, int POL, int NY = 2>
+__device__ __forceinline__ void mma_N_pairs(AccT<NY>& acc, const double* __restrict__ A, int lda, int M, int K,
                                             const double* __restrict__ B) {
   const int lane = lane_id();
   const int fr = lane >> 2, fk = lane & 3;
@@ -187,9 +191,9 @@ __device__ __forceinline__ void mma_N_pairs(Acc& acc, const double* __restrict__
   for (int p0 = 0; p0 < K; p0 += 4) {
     const int p = p0 + fk;
     const bool pk = p < K;
-    double b[2];
+    double b[NY];
 #pragma unroll
-    for (int y = 0; y < 2; ++y) b[y] = pk ? __ldcg(B + p * NV + 8 * y + fr) : 0.0;
+    for (int y = 0; y < NY; ++y) b[y] = pk ? __ldcg(B + p * NV + 8 * y + fr) : 0.0;
     double2 a[4];
 #pragma unroll
     for (int z = 0; z < 4; ++z) {
@@ -200,17 +204,18 @@ __device__ __forceinline__ void mma_N_pairs(Acc& acc, const double* __restrict__
 #pragma unroll
     for (int z = 0; z < 4; ++z) {
       if (16 * z < M) {  // warp-uniform
-        dmma(acc.c[2 * z][0][0], acc.c[2 * z][0][1], a[z].x, b[0]);
-        dmma(acc.c[2 * z][1][0], acc.c[2 * z][1][1], a[z].x, b[1]);
-        dmma(acc.c[2 * z + 1][0][0], acc.c[2 * z + 1][0][1], a[z].y, b[0]);
-        dmma(acc.c[2 * z + 1][1][0], acc.c[2 * z + 1][1][1], a[z].y, b[1]);
+#pragma unroll
+        for (int y = 0; y < NY; ++y) dmma(acc.c[2 * z][y][0], acc.c[2 * z][y][1], a[z].x, b[y]);
+#pragma unroll
+        for (int y = 0; y < NY; ++y) dmma(acc.c[2 * z + 1][y][0], acc.c[2 * z + 1][y][1], a[z].y, b[y]);
       }
     }
   }
 }
 
-// out (M x 16, vector-minor) = acc (+ out when add); paired-row tile layout.
-__device__ __forceinline__ void store_panel_pr(const Acc& acc, double* __restrict__ out, int M, bool add) {
+// out (M x 8 NY of a vector-minor panel) = acc (+ out when add); paired-row tile layout.
+template <int NY>
+__device__ __forceinline__ void store_panel_pr(const AccT<NY>& acc, double* __restrict__ out, int M, bool add) {
   const int lane = lane_id();
   const int fr = lane >> 2, fc = 2 * (lane & 3);
 #pragma unroll
@@ -218,7 +223,7 @@ __device__ __forceinline__ void store_panel_pr(const Acc& acc, double* __restric
     const int i = prow(x, fr);
     if (i >= M) continue;
 #pragma unroll
-    for (int y = 0; y < 2; ++y) {
+    for (int y = 0; y < NY; ++y) {
       double2* o = reinterpret_cast<double2*>(out + i * NV + 8 * y + fc);
       double2 v = make_double2(acc.c[x][y][0], acc.c[x][y][1]);
       if (add) {
@@ -330,11 +335,23 @@ struct SweepTableMV {
   int q;  // up: the deepest child level (input); down: the top parent level (input)
 };
 
+// The fused sweeps optionally split every node into two items, one per
+// 8-vector half (SPLIT = 1): the halves of the 16-vector pass are independent
+// dataflows (half h of a parent needs only half h of its children), a warp
+// holds half the accumulators and fragments, and twice as many warps fit an
+// SM (both halves stream the node's matrix; the second read hits L2).  Flags
+// are per (node, half).
+template <int SPLIT>
+__device__ __forceinline__ uint32_t* flag_of(uint32_t* flag, int level, int64_t node, int h) {
+  return flag + ((df::node_id(level, node) << SPLIT) + h);
+}
+
 // x^{l-1}_p = F_2p^T x^l_2p + F_2p+1^T x^l_2p+1 (hmv.hpp:98-110), levels q..1.
-template <int POL, int UNR>
+template <int POL, int UNR, int SPLIT>
 __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant__ SweepTableMV S,
                                                           uint32_t* __restrict__ flag, uint32_t epoch,
                                                           unsigned long long* __restrict__ ticket) {
+  constexpr int NY = SPLIT ? 1 : 2;
   const int fr = lane_id() >> 2;
   const int64_t total = S.start[S.nl];
   int64_t next = df::claim(ticket);
@@ -345,21 +362,23 @@ __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant_
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevelMV& L = S.L[e];
-    const int64_t p = L.i0 + (it - S.start[e]);
+    const int64_t loc = it - S.start[e];
+    const int64_t p = L.i0 + (loc >> SPLIT);
+    const int h = int(loc) & SPLIT, v0 = 8 * h;
     if (L.l < S.q) {
-      df::wait_flag(flag + df::node_id(L.l, 2 * p), epoch);
-      df::wait_flag(flag + df::node_id(L.l, 2 * p + 1), epoch);
+      df::wait_flag(flag_of<SPLIT>(flag, L.l, 2 * p, h), epoch);
+      df::wait_flag(flag_of<SPLIT>(flag, L.l, 2 * p + 1, h), epoch);
     }
     if (L.kp > 0) {
-      Acc acc;
+      AccT<NY> acc;
       acc.zero();
       if (L.kc > 0) {
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
-          const double* xin = L.in + (2 * p + c) * L.kc * NV;
+          const double* xin = L.in + (2 * p + c) * L.kc * NV + v0;
           const int kc = L.kc;
-          mma_T_pairs<UNR, POL>(acc, L.T + (2 * p + c - L.cbegin) * L.stride, L.ldc, L.kp, kc,
-                                [&](int j, int y, bool ok) {
+          mma_T_pairs<UNR, POL, NY>(acc, L.T + (2 * p + c - L.cbegin) * L.stride, L.ldc, L.kp, kc,
+                                    [&](int j, int y, bool ok) {
             const int r = 2 * j;
             const double lo = (ok && r < kc) ? __ldcg(xin + r * NV + 8 * y + fr) : 0.0;
             const double hi = (ok && r + 1 < kc) ? __ldcg(xin + (r + 1) * NV + 8 * y + fr) : 0.0;
@@ -367,17 +386,18 @@ __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant_
           });
         }
       }
-      store_panel(acc, L.out + p * L.kp * NV, L.kp, false);
+      store_panel(acc, L.out + p * L.kp * NV + v0, L.kp, false);
     }
-    df::set_flag(flag + df::node_id(L.l - 1, p), epoch);
+    df::set_flag(flag_of<SPLIT>(flag, L.l - 1, p, h), epoch);
   }
 }
 
 // y^l_c += E_c y^{l-1}_{c/2} (hmv.hpp:136-146), levels 1..q.
-template <int POL, int UNR>
+template <int POL, int UNR, int SPLIT>
 __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constant__ SweepTableMV S,
                                                             uint32_t* __restrict__ flag, uint32_t epoch,
                                                             unsigned long long* __restrict__ ticket) {
+  constexpr int NY = SPLIT ? 1 : 2;
   const int64_t total = S.start[S.nl];
   int64_t next = df::claim(ticket);
   for (;;) {
@@ -387,18 +407,21 @@ __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constan
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevelMV& L = S.L[e];
-    const int64_t c = L.i0 + (it - S.start[e]);
-    if (L.l - 1 > S.q) df::wait_flag(flag + df::node_id(L.l - 1, c >> 1), epoch);
+    const int64_t loc = it - S.start[e];
+    const int64_t c = L.i0 + (loc >> SPLIT);
+    const int h = int(loc) & SPLIT, v0 = 8 * h;
+    if (L.l - 1 > S.q) df::wait_flag(flag_of<SPLIT>(flag, L.l - 1, c >> 1, h), epoch);
     if (L.kc > 0 && L.kp > 0) {
-      Acc acc;
+      AccT<NY> acc;
       acc.zero();
-      mma_N_pairs<UNR, POL>(acc, L.T + (c - L.cbegin) * L.stride, L.ldc, L.kc, L.kp, L.in + (c >> 1) * L.kp * NV);
+      mma_N_pairs<UNR, POL, NY>(acc, L.T + (c - L.cbegin) * L.stride, L.ldc, L.kc, L.kp,
+                                L.in + (c >> 1) * L.kp * NV + v0);
       // y^l_c (coupling product) += E_c y^{l-1}: added at the end (starting
       // the accumulator from it, as k_down_leaf_mv does with yc, measured
       // 1.49 -> 1.70 ms at C4)
-      store_panel_pr(acc, L.out + c * L.kc * NV, L.kc, true);
+      store_panel_pr(acc, L.out + c * L.kc * NV + v0, L.kc, true);
     }
-    df::set_flag(flag + df::node_id(L.l, c), epoch);
+    df::set_flag(flag_of<SPLIT>(flag, L.l, c, h), epoch);
   }
 }
 
@@ -561,6 +584,12 @@ unsigned persistent_grid_mv(const void* kernel) {
 
 namespace {
 
+// Fused sweeps with one item per (node, 8-vector half) (kSplit = 1): 80
+// registers and twice the warps per SM, but measured slower at C4
+// (k_up_fused_mv 1.46 -> 1.56 ms, k_down_fused_mv 1.49 -> 1.94 ms: every
+// fragment load now feeds half the DMMAs).  Kept switchable.
+constexpr int kSplit = 0;
+
 unsigned flat_grid_mv(int64_t items) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(sms()) * 16)));
 }
@@ -614,11 +643,11 @@ void mv_up_local(Matrix& A, Work& w, const double* X, int64_t ldx, int nv, cudaS
       L.i0 = C.own_begin(l - 1);
       L.n = C.own_count(l - 1);
       T.start[T.nl++] = tot;
-      tot += L.n;
+      tot += L.n << kSplit;
     }
     T.start[T.nl] = tot;
     H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
-    k_up_fused_mv<POL, UNR><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR>), kThreads, 0, s>>>(
+    k_up_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
         T, w.flag.p, 2 * w.epoch, w.ticket.p);
     H2B_CUDA(cudaGetLastError());
   }
@@ -647,11 +676,11 @@ void mv_up_top(Matrix& A, Work& w, cudaStream_t s) {
     L.i0 = 0;
     L.n = A.nodes(l - 1);
     T.start[T.nl++] = tot;
-    tot += L.n;
+    tot += L.n << kSplit;
   }
   T.start[T.nl] = tot;
   H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
-  k_up_fused_mv<POL, UNR><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR>), kThreads, 0, s>>>(
+  k_up_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
       T, w.flag.p, 2 * w.epoch, w.ticket.p);
   H2B_CUDA(cudaGetLastError());
 }
@@ -718,11 +747,11 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
       L.i0 = A.own_begin(l);
       L.n = A.own_count(l);
       S.start[S.nl++] = tot;
-      tot += L.n;
+      tot += L.n << kSplit;
     }
     S.start[S.nl] = tot;
     H2B_CUDA(cudaMemsetAsync(w.ticket.p + 1, 0, sizeof(unsigned long long), s));
-    k_down_fused_mv<POL, UNR><<<persistent_grid_mv((const void*)k_down_fused_mv<POL, UNR>), kThreads, 0, s>>>(
+    k_down_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_down_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
         S, w.flag.p, 2 * w.epoch + 1, w.ticket.p + 1);
     H2B_CUDA(cudaGetLastError());
   }
