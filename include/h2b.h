@@ -70,7 +70,10 @@ typedef enum {
 typedef enum {
   H2B_PTR_AUTO = 0,   /* detect with cudaPointerGetAttributes */
   H2B_PTR_HOST = 1,   /* host memory (pinned or pageable); copies happen inside the call */
-  H2B_PTR_DEVICE = 2  /* device memory on the matrix's device */
+  H2B_PTR_DEVICE = 2, /* device memory on the matrix's device */
+  H2B_PTR_HOST_ASYNC = 3 /* PINNED host memory, stream-ordered: the copies are enqueued on the
+                            call's stream and the call returns without synchronising; the caller
+                            synchronises before reading y or rewriting x (h2b_hmv / h2b_hmv_ctx) */
 } h2b_ptr_kind;
 
 typedef struct h2b_matrix h2b_matrix;

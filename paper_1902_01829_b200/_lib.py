@@ -20,7 +20,7 @@ H2B_NO_DEVICE = 5
 H2B_INTERNAL = 6
 H2B_IO_ERROR = 7
 
-PTR_AUTO, PTR_HOST, PTR_DEVICE = 0, 1, 2
+PTR_AUTO, PTR_HOST, PTR_DEVICE, PTR_HOST_ASYNC = 0, 1, 2, 3
 WS_XHAT, WS_YHAT, WS_XC, WS_PERM = 0, 1, 2, 3
 CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
 

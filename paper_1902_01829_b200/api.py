@@ -249,8 +249,13 @@ class HmvContext:
 
 
 def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=None,
-        ctx: HmvContext | None = None):
-    """y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-194). Returns y."""
+        ctx: HmvContext | None = None, asynchronous: bool = False):
+    """y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-194). Returns y.
+    asynchronous: x and y are PINNED host arrays; the copies and the mat-vec
+    are enqueued on `stream` and the call returns at once (H2B_PTR_HOST_ASYNC):
+    synchronise the stream before reading y.  With one HmvContext and one
+    stream per in-flight call, the copies of one call overlap another's
+    kernels."""
     if y is None:
         if isinstance(x, np.ndarray):
             y = np.zeros_like(x)
@@ -262,6 +267,10 @@ def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=No
     py, ky = _vec(y, n, "hmv: y", writable=True)
     kind = _lib.PTR_DEVICE if (kx == ky == _lib.PTR_DEVICE) else (
         _lib.PTR_HOST if (kx == ky == _lib.PTR_HOST) else _lib.PTR_AUTO)
+    if asynchronous:
+        if not kx == ky == _lib.PTR_HOST:
+            raise _bad("hmv: asynchronous calls take pinned host arrays")
+        kind = _lib.PTR_HOST_ASYNC
     if stream is None and _lib.PTR_DEVICE in (kx, ky):
         # device tensors: run on torch's current stream (NULL would mean the
         # matrix's own non-blocking stream, unordered with torch's work)

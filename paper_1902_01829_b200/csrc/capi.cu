@@ -592,7 +592,10 @@ void hmv(Matrix& A, Work* wp, const double* x, double* y, double alpha, double b
   if (!s) s = A.stream;
   Work& w = wp ? *wp : default_work(A);
   require(w.device == A.device || w.owner == nullptr, "hmv: context belongs to another device");
-  const bool dx = resolve_device(kind, x), dy = resolve_device(kind, y);
+  const bool async_host = kind == H2B_PTR_HOST_ASYNC;
+  if (async_host)
+    require(is_pinned(x) && is_pinned(y), "hmv: H2B_PTR_HOST_ASYNC needs pinned (page-locked) host vectors");
+  const bool dx = !async_host && resolve_device(kind, x), dy = !async_host && resolve_device(kind, y);
   bool sync = false;
   {
     WorkUse u(w, s);
@@ -611,7 +614,7 @@ void hmv(Matrix& A, Work* wp, const double* x, double* y, double alpha, double b
     }
     hmv_device(A, w, xd, yd, alpha, beta, s);
     if (!dy) copy_out(y, w.ys.p, A.n, s);
-    sync = !dx || !dy;
+    sync = (!dx || !dy) && !async_host;
   }
   if (sync) H2B_CUDA(cudaStreamSynchronize(s));
 }

@@ -130,3 +130,25 @@ def test_python_argument_checks(gpu):
         h2.downsweep(A, np.zeros(A.vec_size() + 1), np.zeros(1024))
     with pytest.raises(ValueError):
         h2.validate_sampled(A, 0.1, points=np.zeros((1000, 2)))
+
+
+def test_async_pinned_host_calls(gpu, orc):
+    """H2B_PTR_HOST_ASYNC: pinned host vectors, stream-ordered, two calls in
+    flight on two contexts / streams; pageable host memory is refused."""
+    import torch
+    n = 4096
+    A = h2.H2Matrix.construct(2, n)
+    x = orc.random_vector(n, 1)
+    y_ref = h2.hmv(A, x)
+    xh = torch.from_numpy(x).pin_memory()
+    ys = [torch.zeros(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    ctxs = [h2.HmvContext(A), h2.HmvContext(A)]
+    sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for i in range(6):
+        k = i & 1
+        h2.hmv(A, xh.numpy(), ys[k].numpy(), stream=sts[k].cuda_stream, ctx=ctxs[k], asynchronous=True)
+    torch.cuda.synchronize()
+    for y in ys:
+        assert np.array_equal(y.numpy(), y_ref)
+    with pytest.raises(h2.H2bInvalidArgument):
+        h2.hmv(A, x, np.zeros(n), ctx=ctxs[0], asynchronous=True)  # pageable
