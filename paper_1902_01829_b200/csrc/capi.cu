@@ -397,6 +397,21 @@ void check_value_symmetry(Matrix& A) {
   for (int l = 0; l <= A.q; ++l) A.value_sym[l] = A.mirror_sym[l] && !h[l];
 }
 
+// The BSR work list for the current block shapes (LPT order), reusing the
+// device list when the row count is unchanged.
+void rebuild_work_list(Matrix& A) {
+  cudaStream_t s = A.stream;
+  std::vector<const Layer*> layers;
+  for (int l = 0; l <= A.q; ++l) layers.push_back(&A.cpl[l]);
+  layers.push_back(&A.dense);
+  const std::vector<uint32_t> w = make_work_list(layers);
+  if (A.work.n != w.size()) A.work.alloc(w.size());
+  A.nwork = int64_t(w.size());
+  if (!w.empty())
+    H2B_CUDA(cudaMemcpyAsync(A.work.p, w.data(), w.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  H2B_CUDA(cudaStreamSynchronize(s));
+}
+
 void upload_structure(Matrix& A) {
   cudaStream_t s = A.stream;
   build_mirror(A);

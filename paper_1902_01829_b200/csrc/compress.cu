@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -29,6 +30,7 @@
 namespace h2b {
 
 void upload_structure(Matrix& A);
+void rebuild_work_list(Matrix& A);
 
 namespace {
 
@@ -1838,61 +1840,96 @@ struct ChainStream {
 // producers (orthogonalization, truncation) finish the levels bottom-up, the
 // weight tree consumes them top-down, so a small top level's projection must
 // not queue behind the big bottom levels' in one in-order stream.
-struct SideStream {
-  cudaStream_t s;
-  bool on;
-  int prio = 0;
+// Lowest-priority side streams for the projections, ONE PER LEVEL: the
+// producers (orthogonalization, truncation) finish the levels bottom-up, the
+// weight tree consumes them top-down, so a small top level's projection must
+// not queue behind the big bottom levels' in one in-order stream.  The
+// stream sets are created on first use and recycled through a per-device
+// free list (creating 15 streams per call left the GPU idle for ms).
+struct SideSet {
   std::vector<cudaStream_t> bs = std::vector<cudaStream_t>(kMaxLevels + 1, nullptr);
   std::vector<cudaEvent_t> ev = std::vector<cudaEvent_t>(kMaxLevels + 1, nullptr);   // fork points
   std::vector<cudaEvent_t> lev = std::vector<cudaEvent_t>(kMaxLevels + 1, nullptr);  // per-level completion
+};
+struct SidePool {
+  std::mutex mu;
+  std::map<int, std::vector<SideSet*>> free;  // never destroyed: device teardown frees the streams
+};
+SidePool& side_pool() {
+  static SidePool p;
+  return p;
+}
+SideSet* side_acquire(int device) {
+  SidePool& p = side_pool();
+  std::lock_guard<std::mutex> g(p.mu);
+  auto& f = p.free[device];
+  if (f.empty()) return new SideSet;
+  SideSet* r = f.back();
+  f.pop_back();
+  return r;
+}
+void side_release(int device, SideSet* set) {
+  SidePool& p = side_pool();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.free[device].push_back(set);
+}
+
+struct SideStream {
+  cudaStream_t s;
+  bool on;
+  int device = 0;
+  SideSet* set = nullptr;
+  std::vector<char> used = std::vector<char>(kMaxLevels + 1, 0);
   SideStream(bool enable, cudaStream_t main) : s(main), on(enable) {
     if (!on) return;
-    int hi = 0;
-    H2B_CUDA(cudaDeviceGetStreamPriorityRange(&prio, &hi));  // lowest: fills the gaps
+    H2B_CUDA(cudaGetDevice(&device));
+    set = side_acquire(device);
   }
   ~SideStream() {
     if (!on) return;
-    for (int l = 0; l <= kMaxLevels; ++l) {
-      if (bs[l]) cudaStreamSynchronize(bs[l]);
-      if (lev[l]) cudaEventDestroy(lev[l]);
-      if (ev[l]) cudaEventDestroy(ev[l]);
-      if (bs[l]) cudaStreamDestroy(bs[l]);
-    }
+    for (int l = 0; l <= kMaxLevels; ++l)
+      if (used[l]) cudaStreamSynchronize(set->bs[l]);
+    side_release(device, set);
   }
+  SideStream(const SideStream&) = delete;
+  SideStream& operator=(const SideStream&) = delete;
   // the stream level l's side work goes to (the main stream when off)
   cudaStream_t b(int l) {
     if (!on) return s;
-    if (!bs[l]) {
-      H2B_CUDA(cudaStreamCreateWithPriority(&bs[l], cudaStreamNonBlocking, prio));
-      H2B_CUDA(cudaEventCreateWithFlags(&ev[l], cudaEventDisableTiming));
-      H2B_CUDA(cudaEventCreateWithFlags(&lev[l], cudaEventDisableTiming));
+    if (!set->bs[l]) {
+      int lo = 0, hi = 0;
+      H2B_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      H2B_CUDA(cudaStreamCreateWithPriority(&set->bs[l], cudaStreamNonBlocking, lo));
+      H2B_CUDA(cudaEventCreateWithFlags(&set->ev[l], cudaEventDisableTiming));
+      H2B_CUDA(cudaEventCreateWithFlags(&set->lev[l], cudaEventDisableTiming));
     }
-    return bs[l];
+    used[l] = 1;
+    return set->bs[l];
   }
   // level l's side work starts after everything enqueued on the main stream so far
   void fork(int l) {
     if (!on) return;
     cudaStream_t st = b(l);
-    H2B_CUDA(cudaEventRecord(ev[l], s));
-    H2B_CUDA(cudaStreamWaitEvent(st, ev[l], 0));
+    H2B_CUDA(cudaEventRecord(set->ev[l], s));
+    H2B_CUDA(cudaStreamWaitEvent(st, set->ev[l], 0));
   }
   // level l's side work is enqueued: mark its completion
   void mark(int l) {
     if (!on) return;
-    H2B_CUDA(cudaEventRecord(lev[l], b(l)));
+    H2B_CUDA(cudaEventRecord(set->lev[l], b(l)));
   }
   // the main stream waits for level l's side work only
   void wait(int l) {
-    if (!on || !bs[l]) return;
-    H2B_CUDA(cudaStreamWaitEvent(s, lev[l], 0));
+    if (!on || !used[l]) return;
+    H2B_CUDA(cudaStreamWaitEvent(s, set->lev[l], 0));
   }
   // the main stream waits for all side work
   void join() {
     if (!on) return;
     for (int l = 0; l <= kMaxLevels; ++l)
-      if (bs[l]) {
-        H2B_CUDA(cudaEventRecord(lev[l], bs[l]));
-        H2B_CUDA(cudaStreamWaitEvent(s, lev[l], 0));
+      if (used[l]) {
+        H2B_CUDA(cudaEventRecord(set->lev[l], set->bs[l]));
+        H2B_CUDA(cudaStreamWaitEvent(s, set->lev[l], 0));
       }
   }
 };
@@ -1909,7 +1946,10 @@ void relayout(Matrix& A) {
   }
   // every workspace (the handle's and any h2b_context) re-sizes on next use
   ++A.layout_version;
-  upload_structure(A);
+  // the block pattern (row_ptr / col_idx, the symmetric mirror map) is
+  // unchanged; only the work list's row costs changed with the ranks (the full
+  // upload_structure rebuilt the mirror map on the host: 16-19 ms of idle GPU)
+  rebuild_work_list(A);
 }
 
 struct DeviceGuard {
