@@ -31,12 +31,30 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int NV = 16;        // vectors per pass (2 DMMA column tiles)
 constexpr int kLeafWarps = 4; // leaf kernels: 4 warps x 8 KB shared panel
+#ifndef H2B_MV_PREFETCH
+#define H2B_MV_PREFETCH 1
+#endif
+// Bulk L2 prefetch of the downsweep's transfer block ahead of its flag wait
+// (C4: k_down_fused_mv 1.49 -> 1.41 ms).  The same for the upsweep and the
+// leaf kernels (the next leaf of the warp) raised their DRAM reads 1.5-1.7x
+// and their times (profiles/r02_mv16_launches.txt): not used there.
+constexpr bool kPrefetch = H2B_MV_PREFETCH;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int64_t warp_global() {
   return (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
 }
 __device__ __forceinline__ int64_t warp_count() { return (int64_t(gridDim.x) * blockDim.x) >> 5; }
+
+// Bulk L2 prefetch of a contiguous matrix block (16-byte aligned, size a
+// multiple of 16): the TMA unit streams it into L2 while the warp waits on
+// flags or works on the previous block, beyond what its registers can hold
+// in flight.
+__device__ __forceinline__ void prefetch_l2(const double* p, int64_t count) {
+  if ((threadIdx.x & 31) == 0 && count > 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(uint32_t(count * sizeof(double)))
+                 : "memory");
+}
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -410,6 +428,8 @@ __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constan
     const int64_t loc = it - S.start[e];
     const int64_t c = L.i0 + (loc >> SPLIT);
     const int h = int(loc) & SPLIT, v0 = 8 * h;
+    if (kPrefetch && L.kc > 0 && L.kp > 0 && h == 0)  // the transfer block, ahead of the flag wait
+      prefetch_l2(L.T + (c - L.cbegin) * L.stride, L.stride);
     if (L.l - 1 > S.q) df::wait_flag(flag_of<SPLIT>(flag, L.l - 1, c >> 1, h), epoch);
     if (L.kc > 0 && L.kp > 0) {
       AccT<NY> acc;
