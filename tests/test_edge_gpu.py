@@ -63,7 +63,7 @@ def test_invalid_arguments(gpu):
     with pytest.raises(h2.H2bInvalidArgument, match="perturbation"):
         h2.H2Matrix.construct(2, 1024, perturbation=0.5)
     with pytest.raises(h2.H2bError):
-        h2.H2Matrix.construct(2, 1024, grid_order=9)  # rank 81 > 64: outside the kernel envelope
+        h2.H2Matrix.construct(2, 1024, grid_order=12)  # rank 144 > 128: outside the kernel envelope
     A = h2.H2Matrix.construct(2, 1024)
     with pytest.raises(h2.H2bInvalidArgument, match="leading dimension"):
         h2.hmv_multi(A, np.zeros((2, 512)))  # columns shorter than n
