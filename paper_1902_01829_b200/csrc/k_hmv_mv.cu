@@ -93,7 +93,7 @@ using Acc = AccT<2>;  // 16 vectors
 // acc (M x 16) += op(A) (M x K) * B (K x 16), B vector-minor (B[p * 16 + v]).
 // op(A)(i, p) = TA ? A[p + i * lda] : A[i + p * lda]; A streamed (evict-first).
 // Natural tile layout (row tile x = rows 8x .. 8x+7).  Used by k_bsr_mv.
-template <bool TA, int UNROLL = 2, int POL = 0>
+template <bool TA, int UNROLL = 2>
 __device__ __forceinline__ void mma_panel(Acc& acc, const double* __restrict__ A, int lda, int M,
                                           int K, const double* __restrict__ B) {
   const int lane = lane_id();
@@ -109,17 +109,7 @@ __device__ __forceinline__ void mma_panel(Acc& acc, const double* __restrict__ A
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
       const int i = 8 * x + fr;
-      const double* pa = TA ? A + p + int64_t(i) * lda : A + i + int64_t(p) * lda;
-      double av = 0.0;
-      if (pk && i < M) {
-        if (POL == 0)
-          av = __ldcs(pa);
-        else if (POL == 1)
-          av = __ldg(pa);
-        else
-          asm("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(av) : "l"(pa));
-      }
-      a[x] = av;
+      a[x] = (pk && i < M) ? __ldcs(TA ? A + p + int64_t(i) * lda : A + i + int64_t(p) * lda) : 0.0;
     }
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
@@ -459,7 +449,6 @@ struct LayerTableMV {
 };
 
 // Y_r = sum_b B_b X_{col(b)} for every work item (row of one layer).
-template <int V>
 __global__ void __launch_bounds__(kThreads, 1) k_bsr_mv(const __grid_constant__ LayerTableMV T,
                                                      const uint32_t* __restrict__ work,
                                                      int64_t nwork) {
@@ -475,17 +464,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bsr_mv(const __grid_constant__ 
       // the whole 64-deep block unrolled: its 128 fragment loads per lane are
       // in flight together (measured at n = 2^22: 8 k-steps 19.35 ms per
       // 16 vectors, 16 k-steps 18.39 ms, 4 k-steps at 2 CTAs/SM 19.78 ms)
-      if (V < 3)
-        mma_panel<false, 16, V>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc,
-                                D.x + int64_t(col) * D.bc * NV);
-      else
-        mma_N_pairs<16, V - 3>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc,
-                               D.x + int64_t(col) * D.bc * NV);
+      mma_panel<false, 16>(acc, D.val + int64_t(b) * D.stride, D.ld, D.br, D.bc, D.x + int64_t(col) * D.bc * NV);
     }
-    if (V < 3)
-      store_panel(acc, D.y + int64_t(row) * D.br * NV, D.br, false);
-    else
-      store_panel_pr(acc, D.y + int64_t(row) * D.br * NV, D.br, false);
+    store_panel(acc, D.y + int64_t(row) * D.br * NV, D.br, false);
   }
 }
 
@@ -746,7 +727,7 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
     // (mma_N_pairs) instead of the 8-byte fragments: 17.3 ms (fewer loads in
     // flight at 255 registers); non-coherent / L2::256B loads: 12.6 ms,
     // 79.4 GB read.  The evict-first 8-byte form stays.
-    k_bsr_mv<0><<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
+    k_bsr_mv<<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
     H2B_CUDA(cudaGetLastError());
   }
   if (q >= 1) {  // levels 1..q in one dataflow launch (the root's y^ is final)
