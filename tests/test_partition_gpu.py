@@ -280,3 +280,29 @@ def test_part_hmv_c4_two_partitions(gpu, orc):
         assert float(np.linalg.norm(y)) == pytest.approx(meta["y_norm2"], rel=1e-12)
     for P in parts:
         P.close()
+
+
+def test_partitioned_compress_c3_two_partitions(gpu, orc):
+    """C3 (3D n = 2^20, k = 64, eps 1e-6) compressed as 2 subtree partitions
+    (each coupling pool ~2.8e9 elements, > 2^31) through the partitioned
+    protocol: the global report equals the REFERENCE's C3 compression (golden
+    from the reference on the GPU host), and the compressed partitions' mat-vec
+    matches the reference's compressed operator at the golden indices."""
+    import json
+    import os
+    from conftest import GOLDEN_DIR
+    with open(os.path.join(GOLDEN_DIR, "config", "C3.json")) as f:
+        meta = json.load(f)
+    arr = np.load(os.path.join(GOLDEN_DIR, "config", "C3.npz"))
+    g = meta["compress"]
+    parts, reps = compress_partitioned(meta["dim"], meta["n"], meta["grid_order"], meta["eps"], 2)
+    for r in reps:
+        assert r.new_ranks == g["new_ranks"]
+        assert r.bytes_before == int(g["bytes_before"]) and r.bytes_after == int(g["bytes_after"])
+        assert r.frobenius_error == pytest.approx(g["frobenius_error"], rel=1e-6)
+        assert r.total_flops() == pytest.approx(g["total_flops"], rel=1e-12)
+    x = orc.random_vector(meta["n"], 1)
+    y = partitioned_hmv(parts, x)
+    assert rel_err(y[arr["idx"]], arr["yc"]) <= 10 * meta["eps"]
+    for P in parts:
+        P.close()
