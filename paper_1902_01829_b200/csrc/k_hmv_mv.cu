@@ -590,6 +590,7 @@ namespace {
 // (k_up_fused_mv 1.46 -> 1.56 ms, k_down_fused_mv 1.49 -> 1.94 ms: every
 // fragment load now feeds half the DMMAs).  Kept switchable.
 constexpr int kSplit = 0;
+constexpr int kUnrDown = 2;  // pair-steps in flight of the fused downsweep (see kUnr)
 
 unsigned flat_grid_mv(int64_t items) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(sms()) * 16)));
@@ -752,7 +753,7 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
     }
     S.start[S.nl] = tot;
     H2B_CUDA(cudaMemsetAsync(w.ticket.p + 1, 0, sizeof(unsigned long long), s));
-    k_down_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_down_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
+    k_down_fused_mv<POL, kUnrDown, kSplit><<<persistent_grid_mv((const void*)k_down_fused_mv<POL, kUnrDown, kSplit>), kThreads, 0, s>>>(
         S, w.flag.p, 2 * w.epoch + 1, w.ticket.p + 1);
     H2B_CUDA(cudaGetLastError());
   }
@@ -772,7 +773,11 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
 // algorithmic bytes: 1.45 ms / 5.36 GB and 0.68 ms / 2.70 GB.  Two pair-steps
 // in flight beat four (registers / occupancy) except for the leaf (0.67 vs
 // 0.68 ms, noise).  The untransposed products are insensitive to the policy.
-constexpr int kPol = 2, kUnr = 2;
+// One pair-step in flight (kUnr = 1) beat two for the leaves and the upsweep
+// once the loads were non-coherent (k_up_fused_mv 1.46 -> 1.24 ms, the leaf
+// kernels 0.69 / 0.76 -> 0.64 / 0.68 ms); the downsweep keeps two (1.41 vs
+// 1.49 ms with its L2 prefetch).
+constexpr int kPol = 2, kUnr = 1;
 
 }  // namespace
 
