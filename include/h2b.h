@@ -210,6 +210,18 @@ H2B_API h2b_status h2b_hmv_ctx(h2b_matrix* A, h2b_context* ctx, const double* x,
                                double beta, h2b_ptr_kind kind, void* stream);
 
 /* nvec columns, leading dimensions ldx/ldy (>= n). */
+/* CUDA-graph replay of one mat-vec (for small matrices, where the launch
+ * sequence costs as much as the work): y <- alpha A x + beta y on the fixed
+ * DEVICE vectors x, y is captured once with the context's workspace (NULL: the
+ * matrix's own) and replayed by h2b_hmv_graph_launch on any stream, stream-
+ * ordered with the other users of that workspace.  A graph is tied to the
+ * matrix layout it was captured for: after compress() a launch returns
+ * H2B_INVALID_ARGUMENT.  Destroy graphs before their context / matrix. */
+typedef struct h2b_hmv_graph h2b_hmv_graph;
+H2B_API h2b_status h2b_hmv_graph_create(h2b_matrix* A, h2b_context* ctx, const double* x, double* y, double alpha,
+                                        double beta, h2b_hmv_graph** out);
+H2B_API h2b_status h2b_hmv_graph_launch(h2b_hmv_graph* g, void* stream);
+H2B_API h2b_status h2b_hmv_graph_destroy(h2b_hmv_graph* g);
 H2B_API h2b_status h2b_hmv_multi(h2b_matrix* A, int nvec, const double* X, int64_t ldx, double* Y,
                          int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream);
 

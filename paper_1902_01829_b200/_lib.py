@@ -140,6 +140,10 @@ _SIGS = {
     "h2b_workspace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "h2b_part_upsweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "h2b_part_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "h2b_hmv_graph_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                       C.POINTER(C.c_void_p)]),
+    "h2b_hmv_graph_launch": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "h2b_hmv_graph_destroy": (C.c_int, [C.c_void_p]),
     "h2b_part_hmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int,
                                C.POINTER(DComm), C.c_void_p]),
     "h2b_part_hmv_multi": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,

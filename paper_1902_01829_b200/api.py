@@ -248,6 +248,39 @@ class HmvContext:
             pass
 
 
+class HmvGraph:
+    """One mat-vec y <- alpha A x + beta y on fixed CUDA tensors x, y captured
+    as a CUDA graph (h2b_hmv_graph_create) and replayed by launch(): for small
+    matrices whose launch sequence costs as much as the work."""
+
+    def __init__(self, A: H2Matrix, x, y, alpha: float = 1.0, beta: float = 0.0, ctx: HmvContext | None = None):
+        px, kx = _vec(x, A.n, "hmv: x")
+        py, ky = _vec(y, A.n, "hmv: y", writable=True)
+        if not kx == ky == _lib.PTR_DEVICE:
+            raise _bad("HmvGraph: x and y must be CUDA tensors")
+        out = C.c_void_p()
+        _lib.check(_lib.load().h2b_hmv_graph_create(A._h, ctx._c if ctx is not None else None, px, py,
+                                                    float(alpha), float(beta), C.byref(out)))
+        self._g, self._keep = out, (A, x, y, ctx)
+
+    def launch(self, stream=None):
+        if stream is None:
+            from .dist import torch_stream_handle
+            stream = torch_stream_handle()
+        _lib.check(_lib.load().h2b_hmv_graph_launch(self._g, C.c_void_p(stream)))
+
+    def close(self):
+        if self._g and self._g.value:
+            _lib.check(_lib.load().h2b_hmv_graph_destroy(self._g))
+            self._g = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def hmv(A: H2Matrix, x, y=None, alpha: float = 1.0, beta: float = 0.0, stream=None,
         ctx: HmvContext | None = None, asynchronous: bool = False):
     """y <- alpha (A_D + A_LR) x + beta y (hmv.hpp:175-194). Returns y.

@@ -855,6 +855,93 @@ h2b_status h2b_hmv_ctx(h2b_matrix* Ah, h2b_context* ctx, const double* x, double
   });
 }
 
+}  // extern "C"
+
+struct h2b_hmv_graph {
+  h2b::Matrix* A = nullptr;
+  h2b::Work* w = nullptr;
+  uint64_t layout = 0;
+  int device = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" {
+
+h2b_status h2b_hmv_graph_create(h2b_matrix* Ah, h2b_context* ctx, const double* x, double* y, double alpha,
+                                double beta, h2b_hmv_graph** out) {
+  return guarded([&] {
+    require(Ah && x && y && out, "null argument");
+    Matrix& A = *Ah;
+    require(A.part_s == 0, "h2b_hmv_graph_create: partition handles use h2b_part_hmv");
+    DeviceGuard g(A.device);
+    require(resolve_device(H2B_PTR_AUTO, x) && resolve_device(H2B_PTR_AUTO, y),
+            "h2b_hmv_graph_create: x and y must be device vectors");
+    Work& w = ctx ? *static_cast<Work*>(ctx) : default_work(A);
+    require(w.device == A.device || w.owner == nullptr, "hmv: context belongs to another device");
+    std::unique_ptr<h2b_hmv_graph> G(new h2b_hmv_graph);
+    {
+      // size the workspace and its sweep flags outside the capture (no
+      // allocation may happen inside it), then capture with the workspace held
+      WorkUse u(w, A.stream);
+      ensure_work(A, w);
+      sweep_begin(w, A, A.stream);
+    }
+    H2B_CUDA(cudaStreamSynchronize(A.stream));
+    std::lock_guard<std::mutex> lk(w.mu);
+    cudaStream_t cs = nullptr;
+    H2B_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const bool timing = A.timing;
+    A.timing = false;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      try {
+        hmv_device(A, w, x, y, alpha, beta, cs);
+      } catch (...) {
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(cs, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        cudaStreamDestroy(cs);
+        A.timing = timing;
+        throw;
+      }
+      e = cudaStreamEndCapture(cs, &G->graph);
+    }
+    A.timing = timing;
+    cudaStreamDestroy(cs);
+    H2B_CUDA(e);
+    H2B_CUDA(cudaGraphInstantiate(&G->exec, G->graph, 0));
+    G->A = &A;
+    G->w = &w;
+    G->layout = A.layout_version;
+    G->device = A.device;
+    *out = G.release();
+  });
+}
+
+h2b_status h2b_hmv_graph_launch(h2b_hmv_graph* G, void* stream) {
+  return guarded([&] {
+    require(G && G->exec, "null graph");
+    Matrix& A = *G->A;
+    require(A.layout_version == G->layout,
+            "h2b_hmv_graph_launch: the matrix layout changed since the capture (compress); capture a new graph");
+    DeviceGuard g(G->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : A.stream;
+    WorkUse u(*G->w, s);
+    H2B_CUDA(cudaGraphLaunch(G->exec, s));
+  });
+}
+
+h2b_status h2b_hmv_graph_destroy(h2b_hmv_graph* G) {
+  return guarded([&] {
+    if (!G) return;
+    DeviceGuard g(G->device);
+    if (G->exec) cudaGraphExecDestroy(G->exec);
+    if (G->graph) cudaGraphDestroy(G->graph);
+    delete G;
+  });
+}
+
 h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx, double* Y,
                          int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream) {
   return guarded([&] {

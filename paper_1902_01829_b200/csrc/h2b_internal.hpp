@@ -139,8 +139,7 @@ struct Work {
   // Fused dataflow sweeps (launch_up_fused / launch_down_fused): per-node
   // completion flags (epoch-valued, never reset) and the work tickets.
   DevBuf<uint32_t> flag;
-  DevBuf<unsigned long long> ticket;  // [0] up, [1] down
-  uint32_t epoch = 0;
+  DevBuf<unsigned long long> ticket;  // [0] up ticket, [1] down ticket, [2] epoch (advanced on the device)
   std::mutex mu;
   cudaEvent_t done = nullptr;
   Work() = default;

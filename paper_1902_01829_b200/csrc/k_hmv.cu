@@ -154,9 +154,11 @@ __device__ __forceinline__ int claim(unsigned long long* ticket, unsigned long l
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant__ SweepTable S,
-                                                       uint32_t* __restrict__ flag, uint32_t epoch,
+                                                       uint32_t* __restrict__ flag,
+                                                       const unsigned long long* __restrict__ ep,
                                                        unsigned long long* __restrict__ ticket,
                                                        unsigned long long base) {
+  const uint32_t epoch = 2u * uint32_t(__ldcg(ep));  // up flags of this mat-vec
   const int r = 2 * lane_id();
   const int64_t total = S.start[S.nl];
   for (;;) {
@@ -189,9 +191,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant_
 }
 
 __global__ void __launch_bounds__(kThreads) k_down_fused(const __grid_constant__ SweepTable S,
-                                                         uint32_t* __restrict__ flag, uint32_t epoch,
+                                                         uint32_t* __restrict__ flag,
+                                                         const unsigned long long* __restrict__ ep,
                                                          unsigned long long* __restrict__ ticket,
                                                          unsigned long long base) {
+  const uint32_t epoch = 2u * uint32_t(__ldcg(ep)) + 1u;  // down flags of this mat-vec
   const int r = 2 * lane_id();
   const int64_t total = S.start[S.nl];
   for (;;) {
@@ -214,6 +218,8 @@ __global__ void __launch_bounds__(kThreads) k_down_fused(const __grid_constant__
     set_flag(flag + node_id(L.l, c), epoch);
   }
 }
+
+__global__ void k_epoch_next(unsigned long long* e) { *e += 1; }
 
 struct LayerDesc {
   const double* val;
@@ -428,11 +434,13 @@ void sweep_begin(Work& w, const Matrix& A, cudaStream_t s) {
     // stream-ordered zeroing: the kernels of this mat-vec run after it
     w.flag.alloc(nodes);
     H2B_CUDA(cudaMemsetAsync(w.flag.p, 0, nodes * sizeof(uint32_t), s));
-    w.ticket.alloc(2);
-    H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, 2 * sizeof(unsigned long long), s));
-    w.epoch = 0;
+    w.ticket.alloc(3);  // [0] up ticket, [1] down ticket, [2] epoch
+    H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, 3 * sizeof(unsigned long long), s));
   }
-  ++w.epoch;  // this hmv's epoch: up flags 2e, down flags 2e + 1
+  // this mat-vec's epoch (up flags 2e, down flags 2e + 1), advanced on the
+  // device so that a captured CUDA graph replays correctly
+  k_epoch_next<<<1, 1, 0, s>>>(w.ticket.p + 2);
+  H2B_CUDA(cudaGetLastError());
 }
 
 void launch_up_fused(Work& w, const Matrix& B, double* xhat, cudaStream_t s, int l_hi, int l_lo, bool own) {
@@ -465,7 +473,7 @@ void launch_up_fused(Work& w, const Matrix& B, double* xhat, cudaStream_t s, int
   if (tot == 0) return;
   require(w.flag.n >= (size_t(2) << B.q), "launch_up_fused: sweep_begin missing");
   H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
-  k_up_fused<<<persistent_grid((const void*)k_up_fused), kThreads, 0, s>>>(T, w.flag.p, 2 * w.epoch, w.ticket.p,
+  k_up_fused<<<persistent_grid((const void*)k_up_fused), kThreads, 0, s>>>(T, w.flag.p, w.ticket.p + 2, w.ticket.p,
                                                                           0ull);
   H2B_CUDA(cudaGetLastError());
 }
@@ -501,7 +509,7 @@ void launch_down_fused(Work& w, const Matrix& A, double* yhat, cudaStream_t s, b
   if (tot == 0) return;
   require(w.flag.n >= (size_t(2) << A.q), "launch_down_fused: sweep_begin missing");
   H2B_CUDA(cudaMemsetAsync(w.ticket.p + 1, 0, sizeof(unsigned long long), s));
-  k_down_fused<<<persistent_grid((const void*)k_down_fused), kThreads, 0, s>>>(T, w.flag.p, 2 * w.epoch + 1,
+  k_down_fused<<<persistent_grid((const void*)k_down_fused), kThreads, 0, s>>>(T, w.flag.p, w.ticket.p + 2,
                                                                               w.ticket.p + 1, 0ull);
   H2B_CUDA(cudaGetLastError());
 }

@@ -357,8 +357,10 @@ __device__ __forceinline__ uint32_t* flag_of(uint32_t* flag, int level, int64_t 
 // x^{l-1}_p = F_2p^T x^l_2p + F_2p+1^T x^l_2p+1 (hmv.hpp:98-110), levels q..1.
 template <int POL, int UNR, int SPLIT>
 __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant__ SweepTableMV S,
-                                                          uint32_t* __restrict__ flag, uint32_t epoch,
+                                                          uint32_t* __restrict__ flag,
+                                                          const unsigned long long* __restrict__ ep,
                                                           unsigned long long* __restrict__ ticket) {
+  const uint32_t epoch = 2u * uint32_t(__ldcg(ep));  // up flags of this pass
   constexpr int NY = SPLIT ? 1 : 2;
   const int fr = lane_id() >> 2;
   const int64_t total = S.start[S.nl];
@@ -403,8 +405,10 @@ __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant_
 // y^l_c += E_c y^{l-1}_{c/2} (hmv.hpp:136-146), levels 1..q.
 template <int POL, int UNR, int SPLIT>
 __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constant__ SweepTableMV S,
-                                                            uint32_t* __restrict__ flag, uint32_t epoch,
+                                                            uint32_t* __restrict__ flag,
+                                                            const unsigned long long* __restrict__ ep,
                                                             unsigned long long* __restrict__ ticket) {
+  const uint32_t epoch = 2u * uint32_t(__ldcg(ep)) + 1u;  // down flags of this pass
   constexpr int NY = SPLIT ? 1 : 2;
   const int64_t total = S.start[S.nl];
   int64_t next = df::claim(ticket);
@@ -650,7 +654,7 @@ void mv_up_local(Matrix& A, Work& w, const double* X, int64_t ldx, int nv, cudaS
     T.start[T.nl] = tot;
     H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
     k_up_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
-        T, w.flag.p, 2 * w.epoch, w.ticket.p);
+        T, w.flag.p, w.ticket.p + 2, w.ticket.p);
     H2B_CUDA(cudaGetLastError());
   }
 }
@@ -683,7 +687,7 @@ void mv_up_top(Matrix& A, Work& w, cudaStream_t s) {
   T.start[T.nl] = tot;
   H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
   k_up_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
-      T, w.flag.p, 2 * w.epoch, w.ticket.p);
+      T, w.flag.p, w.ticket.p + 2, w.ticket.p);
   H2B_CUDA(cudaGetLastError());
 }
 
@@ -754,7 +758,7 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
     S.start[S.nl] = tot;
     H2B_CUDA(cudaMemsetAsync(w.ticket.p + 1, 0, sizeof(unsigned long long), s));
     k_down_fused_mv<POL, kUnrDown, kSplit><<<persistent_grid_mv((const void*)k_down_fused_mv<POL, kUnrDown, kSplit>), kThreads, 0, s>>>(
-        S, w.flag.p, 2 * w.epoch + 1, w.ticket.p + 1);
+        S, w.flag.p, w.ticket.p + 2, w.ticket.p + 1);
     H2B_CUDA(cudaGetLastError());
   }
   const int64_t nl = A.own_count(q);

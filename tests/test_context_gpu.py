@@ -152,3 +152,37 @@ def test_async_pinned_host_calls(gpu, orc):
         assert np.array_equal(y.numpy(), y_ref)
     with pytest.raises(h2.H2bInvalidArgument):
         h2.hmv(A, x, np.zeros(n), ctx=ctxs[0], asynchronous=True)  # pageable
+
+
+def test_hmv_graph_replay(gpu, orc):
+    """h2b_hmv_graph_*: a captured mat-vec replays bitwise equal to the direct
+    call (the sweep epoch advances on the device, so replays stay ordered),
+    on a context and on the matrix's own workspace, and refuses to run after
+    compress() changed the layout."""
+    import torch
+    for dim, n, order in [(2, 4096, 8), (2, 8192, 10)]:  # 64 and 100 (k_hmv_big.cu)
+        A = h2.H2Matrix.construct(dim, n, grid_order=order)
+        x = torch.from_numpy(orc.random_vector(n, 1)).cuda()
+        y0 = torch.rand(n, dtype=torch.float64, device="cuda")
+        y_ref = y0.clone()
+        h2.hmv(A, x, y_ref, 1.5, 0.5)
+        ctx = h2.HmvContext(A)
+        for c in (ctx, None):
+            y = y0.clone()
+            g = h2.HmvGraph(A, x, y, 1.5, 0.0, ctx=c)
+            for _ in range(5):
+                g.launch()
+            torch.cuda.synchronize()
+            assert torch.equal(y, h2.hmv(A, x, torch.zeros_like(x), 1.5, 0.0))
+            g.close()
+        y = y0.clone()
+        g = h2.HmvGraph(A, x, y, 1.5, 0.5, ctx=ctx)
+        g.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref)
+        if order == 8:
+            h2.compress(A, 1e-6)
+            with pytest.raises(h2.H2bInvalidArgument, match="layout changed"):
+                g.launch()
+        g.close()
+        ctx.close()
