@@ -1208,8 +1208,18 @@ struct Part {
 // on_t(l) (optional): called once T(l) is final in stream order on s.
 using LevelHook = std::function<void(int)>;
 void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& flops, const Part& pt,
-                   double* tree_mem, const LevelHook& on_t = nullptr) {
+                   double* tree_mem, const LevelHook& on_t_user = nullptr) {
   const int q = A.q, m = A.m, kq = A.rank[q];
+  // partitioned: T(l) of a level >= s is complete (remote column bases
+  // included) only after the all-gather below, so its hook waits for it
+  std::vector<int> deferred;
+  bool gathered = !pt.dist();
+  const LevelHook on_t = !on_t_user ? LevelHook() : LevelHook([&](int l) {
+    if (!gathered && l >= pt.s)
+      deferred.push_back(l);
+    else
+      on_t_user(l);
+  });
   require(m >= kq, "orthogonalize_basis: leaf_dim must be >= leaf rank");
   T.alloc(A, A.rank, A.rank, tree_mem);
   const int64_t nl = A.nodes(q);
@@ -1249,6 +1259,8 @@ void orthogonalize(Matrix& A, TreePool& T, cudaStream_t s, Flops& fl, double& fl
   // the projection, the level-s roots for the replicated top
   for (int l = pt.s; l <= q; ++l)
     pt.allgather(T.at(l), (int64_t(1) << (l - pt.s)) * A.rank[l] * A.rank[l], s);
+  gathered = true;
+  for (int l : deferred) on_t_user(l);
   for (int l = pt.s; l >= 1; --l) level(l);
 }
 
@@ -1665,9 +1677,19 @@ TruncSizes truncate_sizes(const Matrix& A) {
 // on_t(l) (optional): called once Tt(l) (new x old per node) is final in
 // stream order on s; Tt.rows[l] holds the new rank by then.
 double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s, Flops& fl,
-                double& flops, const Part& pt, double* tree_mem, Arena& ar, const LevelHook& on_t = nullptr,
+                double& flops, const Part& pt, double* tree_mem, Arena& ar, const LevelHook& on_t_user = nullptr,
                 std::vector<double>* level_energy = nullptr) {
   require(eps >= 0.0, "truncate_basis: eps must be non-negative");
+  // partitioned: Tt(l) of a level > s gets its remote column bases from the
+  // all-gather after the loop, Tt(s) from the one at the top of level s
+  std::vector<int> deferred;
+  bool gathered_s = !pt.dist(), gathered_all = !pt.dist();
+  const LevelHook on_t = !on_t_user ? LevelHook() : LevelHook([&](int l) {
+    if ((l > pt.s && !gathered_all) || (l == pt.s && !gathered_s))
+      deferred.push_back(l);
+    else
+      on_t_user(l);
+  });
   Trace tr;
   const int q = A.q, m = A.m;
   const std::vector<int> old = A.rank;
@@ -1736,8 +1758,17 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
     const int sl = std::min(zr, kp);
     flops += fl.gemm(double(A.nodes(l)), ktc, kp, kc) + fl.gemm(double(np), zr, kp, kp) +
              fl.svd(double(np), zr, kp);
-    if (l == pt.s)  // the replicated top needs every level-s child's T
+    if (l == pt.s) {  // the replicated top needs every level-s child's T
       pt.allgather(Tt.at(l), int64_t(ktc) * kc, s);
+      gathered_s = true;
+      for (size_t d = 0; d < deferred.size();)
+        if (deferred[d] == pt.s) {
+          on_t_user(pt.s);
+          deferred.erase(deferred.begin() + d);
+        } else {
+          ++d;
+        }
+    }
     const int64_t p0 = A.own_begin(l - 1), npo = A.own_count(l - 1);  // parents here
     ar.off = lvl_base;
     double* Z = ar.take<double>(size_t(npo) * zr * kp);
@@ -1784,6 +1815,8 @@ double truncate(Matrix& A, TreePool& R, double eps, TreePool& Tt, cudaStream_t s
   // the projection with the rectangular T needs remote column bases too
   for (int l = pt.s + 1; l <= q; ++l)
     pt.allgather(Tt.at(l), (int64_t(1) << (l - pt.s)) * nr[l] * old[l], s);
+  gathered_all = gathered_s = true;
+  for (int l : deferred) on_t_user(l);
   Tt.rows = nr;  // per node: new x old, at the old-rank level offsets
   // new transfer pool with padded ld for the new ranks
   A.rank = nr;
@@ -2056,9 +2089,10 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   // the orthogonalization and of the truncation on the main stream.  Phase
   // times are therefore boundary to boundary on the main stream: a
   // projection phase is what remains of it after its producer phase.
-  // Partitioned compression (communicator callbacks between levels) runs
-  // the projections after their producers, on the main stream.
-  const bool overlap = !pt.dist() && sym;
+  // Partitioned compression: a partitioned level's projection starts once the
+  // all-gather has brought the remote column bases (orthogonalize / truncate
+  // defer its hook until then).
+  const bool overlap = sym;
   SideStream side(overlap, s);
   ProjRows PR;
   project_rows(A, par, PR, s);
