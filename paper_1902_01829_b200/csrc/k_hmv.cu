@@ -168,6 +168,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant_
     while (it >= S.start[e + 1]) ++e;
     const SweepLevel& L = S.L[e];
     const int64_t p = L.i0 + (it - S.start[e]);
+    // bulk L2 prefetch of both children's transfers ahead of the flag waits
+    // (C4 mat-vec 12.41 -> 12.34 ms, C2 1.850 -> 1.815 ms; three A/B pairs)
+    if (lane_id() == 0 && L.kc > 0 && L.kp > 0) {
+      const double* pf = L.T + (2 * p - L.cbegin) * L.stride;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(uint32_t(2 * L.stride * 8)) : "memory");
+    }
     if (L.l < S.q) {  // children computed by this launch (level q: input, e.g. by k_up_leaf)
       wait_flag(flag + node_id(L.l, 2 * p), epoch);
       wait_flag(flag + node_id(L.l, 2 * p + 1), epoch);
@@ -205,6 +211,10 @@ __global__ void __launch_bounds__(kThreads) k_down_fused(const __grid_constant__
     while (it >= S.start[e + 1]) ++e;
     const SweepLevel& L = S.L[e];
     const int64_t c = L.i0 + (it - S.start[e]);
+    if (lane_id() == 0 && L.kc > 0 && L.kp > 0) {  // the transfer block, ahead of the flag wait
+      const double* pf = L.T + (c - L.cbegin) * L.stride;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(uint32_t(L.stride * 8)) : "memory");
+    }
     if (L.l - 1 > S.q) wait_flag(flag + node_id(L.l - 1, c >> 1), epoch);  // (top parent level: input)
     if (L.kc > 0 && L.kp > 0) {
       const double* yp = L.in + (c >> 1) * L.kp;
