@@ -186,3 +186,19 @@ def test_hmv_graph_replay(gpu, orc):
                 g.launch()
         g.close()
         ctx.close()
+
+
+def test_async_pinned_host_alpha_beta(gpu, orc):
+    """H2B_PTR_HOST_ASYNC with beta != 0 reads the pinned y (stream-ordered)."""
+    import torch
+    n = 4096
+    A = h2.H2Matrix.construct(2, n)
+    x = orc.random_vector(n, 2)
+    y0 = np.random.default_rng(3).random(n)
+    y_ref = h2.hmv(A, x, y0.copy(), 2.0, -0.5)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.from_numpy(y0.copy()).pin_memory()
+    st = torch.cuda.Stream()
+    h2.hmv(A, xh.numpy(), yh.numpy(), 2.0, -0.5, stream=st.cuda_stream, asynchronous=True)
+    st.synchronize()
+    assert np.array_equal(yh.numpy(), y_ref)
