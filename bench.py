@@ -534,6 +534,23 @@ def run_distributed(args, cfg, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     # parity spot check against the replicated-input result
     assert torch.allclose(yh, y.cpu(), rtol=0, atol=0)
+    # 16-vector pass on the partitions (h2b_part_hmv_multi, BASELINE configs[3])
+    X = torch.rand(16, n, dtype=torch.float64, device="cuda", generator=gen)
+    Y = torch.zeros_like(X)
+    for _ in range(2):
+        D.hmv_multi(X, Y)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        D.hmv_multi(X, Y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    mv_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    multi = {"vectors": 16, "ms_per_pass": round(mv_ms, 3), "ms_per_vector": round(mv_ms / 16, 4),
+             "effective_GBs": round(16 * fp / mv_ms / 1e6, 1)}
+    del X, Y
     inf = D.info
     D.close()
     comp = None
@@ -570,6 +587,7 @@ def run_distributed(args, cfg, world, rank, local):
         # ours per step: up_leaf, gather, per-level up (q), bsr, per-level down (q), down_leaf
         "gpu_launches": (2 * q + 4) * args.steps,
         "clocks": clocks,
+        "multi16": multi,
         "compression": comp,
     }
     emit(line)
