@@ -117,3 +117,25 @@ def test_container_errors(gpu, tmp_path):
     with pytest.raises(h2.H2bIOError, match="missing section header"):
         h2.H2Matrix.load(bad)
     os.remove(bad)
+
+
+def test_big_blocks_roundtrip_with_reference(gpu, ref, tmp_path):
+    """Ranks / leaf sizes above 64 (leaf 128, rank 100) through the container:
+    the reference reads our device-built file and we read the reference's, with
+    the same mat-vec (k_hmv_big.cu on our side)."""
+    dim, n, leaf, order = 2, 1 << 13, 128, 10
+    A = h2.H2Matrix.construct(dim, n, leaf_size=leaf, grid_order=order)
+    p1 = tmp_path / "dev_big.h2"
+    A.save(p1)
+    R = ref.load(str(p1))
+    x = np.random.default_rng(31).random(n)
+    assert rel_err(R.hmv(x), h2.hmv(A, x)) <= 1e-12
+    R2 = ref.construct(dim, n, leaf_size=leaf, grid_order=order)
+    p2 = tmp_path / "ref_big.h2"
+    R2.save(str(p2))
+    B = h2.H2Matrix.load(p2)
+    assert rel_err(h2.hmv(B, x), R2.hmv(x)) <= 1e-12
+    U = h2.H2Matrix.from_host(R2.to_host())  # uploaded to HBM and saved from there
+    p3 = tmp_path / "up_big.h2"
+    U.save(p3, build_info=dict(dim=dim, seed=1, perturbation=0.25, ell=0.1, eta=2.0, grid_order=order))
+    assert p3.read_bytes() == p2.read_bytes()
