@@ -1381,7 +1381,11 @@ double project_rowsum(const ProjRows& R, const Part& pt, cudaStream_t s) {
 
 // After every level's launch completed (stream order on s): compaction of the
 // shrunken blocks (not in_place) and the new layer shapes.
-void project_finish(Matrix& A, const TreePool& T, const TreePool& Tc, bool in_place, Arena& ar, cudaStream_t s) {
+// level_done(l) (optional): makes s wait for level l's projection, so level
+// l is compacted while the projections of the levels after it still run
+// (compaction of level l touches only addresses below level l + 1's old slots).
+void project_finish(Matrix& A, const TreePool& T, const TreePool& Tc, bool in_place, Arena& ar, cudaStream_t s,
+                    const LevelHook& level_done = nullptr) {
   const int q = A.q;
   std::vector<int64_t> new_off(q + 2, 0);
   for (int l = 0; l <= q; ++l)
@@ -1393,6 +1397,7 @@ void project_finish(Matrix& A, const TreePool& T, const TreePool& Tc, bool in_pl
     for (int l = 0; l <= q; ++l) {
       const Layer& L = A.cpl[l];
       const int64_t bs_new = int64_t(pad2(T.rows[l])) * Tc.rows[l], bs_old = L.block_stride();
+      if (level_done) level_done(l);
       if (L.nb == 0 || bs_new == 0) continue;
       const int64_t per = std::max<int64_t>(1, cap / bs_new);
       const int64_t old_off = L.val - A.cpl_val.p;
@@ -1869,16 +1874,17 @@ struct ChainStream {
 // Side stream of compress(): fork(l) makes it wait for the main stream's
 // work issued so far (T(l) final), join() makes the main stream wait for it.
 // Disabled: b is the main stream itself and both are no-ops.
-// Lowest-priority side streams for the projections, ONE PER LEVEL: the
-// producers (orthogonalization, truncation) finish the levels bottom-up, the
-// weight tree consumes them top-down, so a small top level's projection must
-// not queue behind the big bottom levels' in one in-order stream.
-// Lowest-priority side streams for the projections, ONE PER LEVEL: the
-// producers (orthogonalization, truncation) finish the levels bottom-up, the
-// weight tree consumes them top-down, so a small top level's projection must
-// not queue behind the big bottom levels' in one in-order stream.  The
-// stream sets are created on first use and recycled through a per-device
-// free list (creating 15 streams per call left the GPU idle for ms).
+// Side streams for the projections, ONE PER LEVEL, below the main stream's
+// priority: the producers (orthogonalization, truncation) finish the levels
+// bottom-up, the weight tree consumes them top-down, so a small top level's
+// projection must not queue behind the big bottom levels' in one in-order
+// stream -- nor behind their CTAs in the block scheduler: the stream of the
+// level d above the leaves has priority lo - d (clamped one below the main
+// stream), so once the leaf level's projection (the biggest, issued first)
+// holds the GPU, every upper level's CTAs still go first as slots free up.
+// The stream sets are indexed by d, created on first use and recycled through
+// a per-device free list (creating 15 streams per call left the GPU idle for
+// ms).
 struct SideSet {
   std::vector<cudaStream_t> bs = std::vector<cudaStream_t>(kMaxLevels + 1, nullptr);
   std::vector<cudaEvent_t> ev = std::vector<cudaEvent_t>(kMaxLevels + 1, nullptr);   // fork points
@@ -1913,7 +1919,8 @@ struct SideStream {
   int device = 0;
   SideSet* set = nullptr;
   std::vector<char> used = std::vector<char>(kMaxLevels + 1, 0);
-  SideStream(bool enable, cudaStream_t main) : s(main), on(enable) {
+  int q = 0;  // leaf level: level l uses slot q - l
+  SideStream(bool enable, cudaStream_t main, int leaf_level) : s(main), on(enable), q(leaf_level) {
     if (!on) return;
     H2B_CUDA(cudaGetDevice(&device));
     set = side_acquire(device);
@@ -1929,32 +1936,35 @@ struct SideStream {
   // the stream level l's side work goes to (the main stream when off)
   cudaStream_t b(int l) {
     if (!on) return s;
-    if (!set->bs[l]) {
+    const int d = q - l;
+    if (!set->bs[d]) {
       int lo = 0, hi = 0;
       H2B_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      H2B_CUDA(cudaStreamCreateWithPriority(&set->bs[l], cudaStreamNonBlocking, lo));
-      H2B_CUDA(cudaEventCreateWithFlags(&set->ev[l], cudaEventDisableTiming));
-      H2B_CUDA(cudaEventCreateWithFlags(&set->lev[l], cudaEventDisableTiming));
+      const int prio = hi < lo ? std::max(hi + 1, lo - d) : lo;
+      H2B_CUDA(cudaStreamCreateWithPriority(&set->bs[d], cudaStreamNonBlocking, prio));
+      H2B_CUDA(cudaEventCreateWithFlags(&set->ev[d], cudaEventDisableTiming));
+      H2B_CUDA(cudaEventCreateWithFlags(&set->lev[d], cudaEventDisableTiming));
     }
-    used[l] = 1;
-    return set->bs[l];
+    used[d] = 1;
+    return set->bs[d];
   }
   // level l's side work starts after everything enqueued on the main stream so far
   void fork(int l) {
     if (!on) return;
     cudaStream_t st = b(l);
-    H2B_CUDA(cudaEventRecord(set->ev[l], s));
-    H2B_CUDA(cudaStreamWaitEvent(st, set->ev[l], 0));
+    H2B_CUDA(cudaEventRecord(set->ev[q - l], s));
+    H2B_CUDA(cudaStreamWaitEvent(st, set->ev[q - l], 0));
   }
   // level l's side work is enqueued: mark its completion
   void mark(int l) {
     if (!on) return;
-    H2B_CUDA(cudaEventRecord(set->lev[l], b(l)));
+    cudaStream_t st = b(l);
+    H2B_CUDA(cudaEventRecord(set->lev[q - l], st));
   }
   // the main stream waits for level l's side work only
   void wait(int l) {
-    if (!on || !used[l]) return;
-    H2B_CUDA(cudaStreamWaitEvent(s, set->lev[l], 0));
+    if (!on || !used[q - l]) return;
+    H2B_CUDA(cudaStreamWaitEvent(s, set->lev[q - l], 0));
   }
   // the main stream waits for all side work
   void join() {
@@ -2093,7 +2103,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   // all-gather has brought the remote column bases (orthogonalize / truncate
   // defer its hook until then).
   const bool overlap = sym;
-  SideStream side(overlap, s);
+  SideStream side(overlap, s, A.q);
   ProjRows PR;
   project_rows(A, par, PR, s);
   TreePool To, R, Tt, Toc, Rc, Ttc;  // row basis; column basis (non-symmetric)
@@ -2172,8 +2182,11 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
     if (!overlap)
       for (int l = A.q; l >= 0; --l)
         project_level(A, Tt, Tt_c, PR, l, false, false, fl, r.flops_project_trunc, pt, s);
+    // levels are compacted in address order as their projections complete:
+    // the upper levels (finished first, see SideStream) while the leaf
+    // level's projection still runs
+    project_finish(A, Tt, Tt_c, /*in_place=*/false, ar, s, [&side](int l) { side.wait(l); });
     side.join();
-    project_finish(A, Tt, Tt_c, /*in_place=*/false, ar, s);
     r.time_project_trunc_ms = t.stop();
   }
   relayout(A);

@@ -47,10 +47,9 @@ for _ in range(reps):
                           top_kernels=[(round(t, 2), k) for t, k in slow],
                           per_kernel={k: round(v, 1) for k, v in sorted(agg.items(), key=lambda kv: -kv[1])})), flush=True)
     if len(sys.argv) > 6:  # every launch in order: name, ms
-        seq = []
-        for e in ev:
-            k = e.name.replace("h2b::(anonymous namespace)::", "").replace("void ", "").split("(")[0][:24]
-            seq.append(f"{k}:{e.time_range.elapsed_us() / 1e3:.2f}")
-        print(" ".join(seq), flush=True)
+        t0 = ev[0].time_range.start
+        for e in ev:  # start offset, duration, kernel
+            k = e.name.replace("h2b::(anonymous namespace)::", "").replace("void ", "").split("(")[0][:28]
+            print(f"  {(e.time_range.start - t0) / 1e3:9.3f} {e.time_range.elapsed_us() / 1e3:8.3f}  {k}", flush=True)
     A.close()
     del A
