@@ -728,7 +728,8 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
   if (A.nwork) {
     // The LPT-ordered work list (make_work_list).  Layer / row order keeps
     // neighbouring rows' x panels in L2 (DRAM read 75.4 -> 72.6 GB at C4) but
-    // loses the balance: 12.18 -> 12.71 ms.  16-byte paired-row loads
+    // loses the balance: 12.18 -> 12.71 ms; claimed dynamically (atomic row
+    // ticket, claim-ahead) in that order: 72.8 GB but 15.6 ms.  16-byte paired-row loads
     // (mma_N_pairs) instead of the 8-byte fragments: 17.3 ms (fewer loads in
     // flight at 255 registers); non-coherent / L2::256B loads: 12.6 ms,
     // 79.4 GB read.  The evict-first 8-byte form stays.
