@@ -2046,7 +2046,7 @@ void compress_matrix(Matrix& A, double eps, h2b_compress_report* rep, const h2b_
   DeviceGuard g(A.device);
   // The dependency chain (orthogonalization, weights, truncation) runs on a
   // highest-priority stream ordered after the handle's stream; the
-  // projections on a lowest-priority side stream soak up the SMs it leaves
+  // projections on lower-priority per-level side streams soak up the SMs it leaves
   // idle (SideStream).
   ChainStream chain(A.stream);
   cudaStream_t s = chain.s;
