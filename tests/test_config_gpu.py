@@ -94,6 +94,24 @@ def test_config_hmv_and_compress(gpu, orc, case):
         h2.release_cached_memory(0)
 
 
+def check_multi16_and_properties(A, meta, arr, orc):
+    """The 16-vector DMMA pass (BASELINE configs[3]) at full size: vector 0 is
+    the golden's x, so its column is compared with the REFERENCE's y; other
+    columns with the single-vector path; linearity and symmetry
+    (test_hmv.cpp:103-142) at a size no dense check reaches."""
+    n = meta["n"]
+    rng = np.random.default_rng(41)
+    X = rng.uniform(-1.0, 1.0, (16, n))
+    X[0] = orc.random_vector(n, 1)
+    Y = h2.hmv_multi(A, X)
+    assert rel_err(Y[0][arr["idx"]], arr["y"]) <= 1e-12
+    for v in (1, 7, 15):
+        assert rel_err(Y[v], h2.hmv(A, X[v])) <= 1e-12
+    yw = h2.hmv(A, 2.0 * X[1] - 0.5 * X[2])
+    assert rel_err(yw, 2.0 * Y[1] - 0.5 * Y[2]) <= 1e-12
+    assert float(np.dot(X[2], Y[1])) == pytest.approx(float(np.dot(X[1], Y[2])), rel=1e-12)
+
+
 def test_config_C4_hmv_n2_22(gpu, orc):
     """C4: 2D n = 2^22, k = 64, 76.98 GB (coupling pool 6.4e9 elements)."""
     meta, arr = load_case("C4")
@@ -102,6 +120,7 @@ def test_config_C4_hmv_n2_22(gpu, orc):
         check_structure(A, meta)
         assert sum(b * 64 * 64 for b in meta["cpl_blocks"]) > 2 ** 31
         check_hmv(A, meta, arr, orc)
+        check_multi16_and_properties(A, meta, arr, orc)
     finally:
         A.close()
 
