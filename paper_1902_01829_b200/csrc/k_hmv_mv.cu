@@ -23,6 +23,16 @@
 #include "dataflow.cuh"
 #include "h2b_internal.hpp"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#ifndef H2B_TSTAGES
+#define H2B_TSTAGES 2
+#endif
+#ifndef H2B_TCTAS
+#define H2B_TCTAS 2
+#endif
+
 #include <algorithm>
 
 namespace h2b {
@@ -474,6 +484,193 @@ __global__ void __launch_bounds__(kThreads, 1) k_bsr_mv(const __grid_constant__ 
   }
 }
 
+// ---- TMA-fed coupling / dense product of the 16-vector pass ---------------
+// One CTA per SM walks its rows of the LPT list (static round robin).  A
+// producer warp streams every block of the row, and the x^ panel of its block
+// column, through a kTStages-deep ring in shared memory with tensor-map TMA
+// loads (cp.async.bulk.tensor.2d, 128-byte swizzle): a block is 4 boxes of
+// 16 rows x 64 columns, the panel one box of 64 rows x 16 vectors (8 KB each;
+// out-of-range rows / columns are zero-filled by the TMA unit), completion
+// signalled on the stage's mbarrier by the transaction bytes.  Four consumer
+// warps (one per SM sub-partition) each own one box, i.e. the 16 rows
+// [16w, 16w + 16) of the block row, as two DMMA row tiles (even / odd rows)
+// times two vector tiles (even / odd vectors): one 16-byte shared load gives
+// a lane its A values of both row tiles (rows 2fr, 2fr + 1 of a column) and
+// another its B values of both vector tiles (vectors 2fr, 2fr + 1).  The last
+// read of a stage arrives on its empty barrier.  The ring, not the registers,
+// holds the bytes in flight.
+//
+// Fragment k-order: in k-step kk lane (fr, fk) takes column
+//   p = 8 (kk / 2) + 2 fk + kk % 2,
+// a bijection onto 0..63 per block with p % 8 = 2 fk + kk % 2: under the
+// 128-byte swizzle (16-byte chunk ^= line % 8) the 8 lanes of a quarter warp
+// read 8 distinct chunks -- every 16-byte fragment load is 4 conflict-free
+// wavefronts.
+constexpr int kTStages = H2B_TSTAGES;
+constexpr int kTCtas = H2B_TCTAS;  // resident CTAs per SM
+constexpr int kTWarps = 4;
+constexpr int kTBox = 16 * 64;                      // doubles per box (8 KB)
+constexpr int kTStageDoubles = 5 * kTBox;           // 4 block boxes + the x^ panel
+constexpr size_t kTSmem = size_t(kTStages) * kTStageDoubles * sizeof(double) + 1024;  // + alignment
+
+struct TmaTableMV {
+  CUtensorMap S[kMaxLevels + 2];  // per layer: {ld, nb bc} column-major blocks, box {16, 64}
+  CUtensorMap X[2];               // [0] x^ pool, [1] xc (dense layer): {16, rows}, box {16, 64}
+  int64_t xrow0[kMaxLevels + 2];  // per layer: first row of its x panels in X
+  int dense;                      // the dense layer's index
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// L2 policies of the TMA loads: the matrix stream evict-first (read once),
+// the x^ panels evict-last (re-read by every block of their block column).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                       uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// Element (line, e) of a 128-byte-swizzled box of 16-double lines.
+__device__ __forceinline__ int swz(int line, int e) { return line * 16 + ((((e >> 1) ^ line) & 7) << 1) + (e & 1); }
+
+__global__ void __launch_bounds__(32 * (kTWarps + 1), kTCtas) k_bsr_mv_tma(const __grid_constant__ LayerTableMV T,
+                                                                     const __grid_constant__ TmaTableMV M,
+                                                                     const uint32_t* __restrict__ work,
+                                                                     int64_t nwork) {
+  extern __shared__ double ring_raw[];
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ring_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kTStages], empty[kTStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kTStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int stage = 0;
+  uint32_t phase = 0;
+  if (warp == kTWarps) {  // producer: one elected lane
+    if (lane == 0) {
+      const uint64_t pol_s = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
+      for (int64_t it = blockIdx.x; it < nwork; it += gridDim.x) {
+        const uint32_t u = __ldg(work + it);
+        const int li = int(u >> kLayerShift);
+        const LayerDescMV& D = T.L[li];
+        const int row = int(u & ((1u << kLayerShift) - 1));
+        const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
+        const CUtensorMap* xm = &M.X[li == M.dense ? 1 : 0];
+        for (int b = b0; b < b1; ++b) {
+          const int col = __ldg(D.ci + b);
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (D.br == 0 || D.bc == 0) {  // rank-0 blocks: nothing to load, the rows are zero
+            mbar_arrive(&full[stage]);
+            if (++stage == kTStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+            continue;
+          }
+          mbar_expect_tx(&full[stage], 5u * kTBox * sizeof(double));
+          double* dst = ring + stage * kTStageDoubles;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) tma_2d(dst + h * kTBox, &M.S[li], 16 * h, b * D.bc, &full[stage], pol_s);
+          tma_2d(dst + 4 * kTBox, xm, 0, int(M.xrow0[li] + int64_t(col) * D.bc), &full[stage], pol_x);
+          if (++stage == kTStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int fr = lane >> 2, fk = lane & 3;
+  const int r0 = 16 * warp + 2 * fr;  // this lane's A rows: r0 (even tile), r0 + 1 (odd tile)
+  for (int64_t it = blockIdx.x; it < nwork; it += gridDim.x) {
+    const uint32_t u = __ldg(work + it);
+    const LayerDescMV& D = T.L[u >> kLayerShift];
+    const int row = int(u & ((1u << kLayerShift) - 1));
+    const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
+    const int br = D.br, bc = D.bc;
+    const bool live = 16 * warp < br;  // warp-uniform
+    double c[2][2][2] = {};  // [row tile][vector tile][pair]
+    for (int b = b0; b < b1; ++b) {
+      mbar_wait(&full[stage], phase);
+      if (live) {
+        const double* S = ring + stage * kTStageDoubles + warp * kTBox;
+        const double* X = ring + stage * kTStageDoubles + 4 * kTBox;
+        double2 av[16], xv[16];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          const int p = 8 * (kk >> 1) + 2 * fk + (kk & 1);
+          const bool pk = p < bc;
+          av[kk] = pk ? *reinterpret_cast<const double2*>(S + swz(p, 2 * fr)) : make_double2(0.0, 0.0);
+          xv[kk] = pk ? *reinterpret_cast<const double2*>(X + swz(p, 2 * fr)) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          dmma(c[0][0][0], c[0][0][1], av[kk].x, xv[kk].x);
+          dmma(c[0][1][0], c[0][1][1], av[kk].x, xv[kk].y);
+          dmma(c[1][0][0], c[1][0][1], av[kk].y, xv[kk].x);
+          dmma(c[1][1][0], c[1][1][1], av[kk].y, xv[kk].y);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kTStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    // lane (fr, fk) of tile (t, y) holds rows r0 + t, vectors 2 (2 fk + j) + y:
+    // four consecutive vectors 4 fk .. 4 fk + 3 of each of its two rows
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (live && r0 + t < br) {
+        double* yo = D.y + (int64_t(row) * br + r0 + t) * NV + 4 * fk;
+        *reinterpret_cast<double2*>(yo) = make_double2(c[t][0][0], c[t][1][0]);
+        *reinterpret_cast<double2*>(yo + 2) = make_double2(c[t][0][1], c[t][1][1]);
+      }
+    }
+  }
+}
+
 // Leaf i: Y[perm[t] + v ldy] = alpha (U_i y^q_i + yc)[t][v] + beta Y[...]
 // (hmv.hpp:147-156, 184-187).  The result rows go through a shared [v][t]
 // panel so the scatter is coalesced along t.
@@ -594,10 +791,38 @@ namespace {
 // (k_up_fused_mv 1.46 -> 1.56 ms, k_down_fused_mv 1.49 -> 1.94 ms: every
 // fragment load now feeds half the DMMAs).  Kept switchable.
 constexpr int kSplit = 0;
+#ifndef H2B_TMA_BSR
+#define H2B_TMA_BSR 1
+#endif
+constexpr bool kTmaBsr = H2B_TMA_BSR;
 constexpr int kUnrDown = 2;  // pair-steps in flight of the fused downsweep (see kUnr)
 
 unsigned flat_grid_mv(int64_t items) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(sms()) * 16)));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    H2B_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    require(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2D f64 tensor {inner, outer} (outer stride `ld` doubles), boxes of 16 x 64
+// elements, 128-byte swizzle, out-of-range elements zero-filled.
+void encode_box16x64(CUtensorMap* m, const double* base, uint64_t inner, uint64_t outer, uint64_t ld) {
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * sizeof(double)};
+  const cuuint32_t box[2] = {16, 64};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(H2B_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
 }
 
 void ensure_mv_work(Matrix& A, Work& w) {
@@ -733,7 +958,24 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
     // (mma_N_pairs) instead of the 8-byte fragments: 17.3 ms (fewer loads in
     // flight at 255 registers); non-coherent / L2::256B loads: 12.6 ms,
     // 79.4 GB read.  The evict-first 8-byte form stays.
-    k_bsr_mv<<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
+    if (kTmaBsr) {
+      TmaTableMV M{};
+      const int64_t xrows = std::max<int64_t>(1, std::max(A.vec_off[q + 1], C.vec_off[q + 1]));
+      encode_box16x64(&M.X[0], xh, NV, uint64_t(xrows), NV);
+      encode_box16x64(&M.X[1], w.xc16.p, NV, uint64_t(std::max(1, A.n)), NV);
+      M.dense = q + 1;
+      for (int l = 0; l <= q + 1; ++l) {
+        const Layer& L = l <= q ? A.cpl[l] : A.dense;
+        M.xrow0[l] = l <= q ? C.vec_off[l] : 0;
+        if (L.nb > 0 && L.br > 0 && L.bc > 0)
+          encode_box16x64(&M.S[l], L.val, uint64_t(std::max(2, L.ld)), uint64_t(L.nb) * L.bc, uint64_t(std::max(2, L.ld)));
+      }
+      H2B_CUDA(cudaFuncSetAttribute(k_bsr_mv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTSmem)));
+      k_bsr_mv_tma<<<unsigned(std::min<int64_t>(A.nwork, int64_t(kTCtas) * sms())), 32 * (kTWarps + 1), kTSmem, s>>>(T, M, A.work.p,
+                                                                                                   A.nwork);
+    } else {
+      k_bsr_mv<<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
+    }
     H2B_CUDA(cudaGetLastError());
   }
   if (q >= 1) {  // levels 1..q in one dataflow launch (the root's y^ is final)

@@ -227,3 +227,16 @@ def test_fused_sweeps_repeat_bitwise(gpu, orc):
     assert rel_err(y1, y0) <= 1e-6
     for _ in range(8):
         assert np.array_equal(h2.hmv(A, x), y1)
+
+
+def test_hmv_multi_compressed_ranks(gpu):
+    """The 16-vector pass (TMA-fed coupling kernel) on compressed layouts: odd,
+    small and zero ranks per level, rectangular ld / rank blocks; every column
+    equals the single-vector mat-vec of the same handle."""
+    for dim, n, order, eps in [(3, 4096, 4, 1e-4), (2, 4096, 8, 1e-2), (2, 1 << 14, 8, 0.5)]:
+        A = h2.H2Matrix.construct(dim, n, grid_order=order)
+        h2.compress(A, eps)
+        X = np.random.default_rng(9).uniform(-1.0, 1.0, (16, n))
+        Y = h2.hmv_multi(A, X)
+        for v in (0, 5, 15):
+            assert rel_err(Y[v], h2.hmv(A, X[v])) <= TOL, (dim, order, eps, A.info().ranks)
