@@ -14,6 +14,7 @@
 // (evict-first) 128-bit loads; node vectors stay L2-resident.
 #include "dataflow.cuh"
 #include "h2b_internal.hpp"
+#include "tma.cuh"
 #include "warp_gemv.cuh"
 
 #include <algorithm>
@@ -21,6 +22,11 @@
 
 namespace h2b {
 namespace {
+
+#ifndef H2B_TMA_BSR1
+#define H2B_TMA_BSR1 1
+#endif
+constexpr bool kTmaBsr = H2B_TMA_BSR1;  // k_bsr_tma (else the register-fed k_bsr)
 
 constexpr int kThreads = 256;  // 8 warps per CTA
 using namespace wg;
@@ -310,6 +316,122 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
   }
 }
 
+// The same product with the blocks streamed by the tensor-memory accelerator
+// (k_bsr_tma): a read-only 64 GB stream measured 7.44 TB/s through a TMA ring
+// against 7.06-7.09 TB/s with 16-byte evict-first loads
+// (tools/microbench/tma_stream.cu).  One CTA walks its rows of the LPT list; a
+// producer lane loads each block as 4 tensor-map boxes of 16 rows x 64 columns
+// (128-byte swizzle; zero fill out of range) plus the 64-double x segment of
+// its block column (1D tensor map, from an even element: TMA boxes start
+// 16-byte aligned), completion on the stage's mbarrier; four
+// consumer warps own a box each: lane (i, h) accumulates row 16w + i over the
+// columns [32h, 32h + 32) from shared memory (a line of the box is the 16 rows
+// of one column: two conflict-free wavefronts per load), the halves meet by a
+// shuffle at the end of the row.
+#ifndef H2B_BSTAGES
+#define H2B_BSTAGES 2
+#endif
+constexpr int kBStages = H2B_BSTAGES, kBCtas = 2, kBWarps = 4;
+constexpr int kBBox = 16 * 64;
+constexpr int kBXBox = 66;  // x segment: 64 doubles from an even start (one more when it is odd)
+constexpr int kBStage = 4 * kBBox + 128;  // + the x segment, padded: every stage 1024-byte aligned (swizzle)
+constexpr size_t kBSmem = size_t(kBStages) * kBStage * sizeof(double) + 1024;
+struct TmaTable {
+  CUtensorMap S[kMaxLevels + 2];  // per layer: {ld, nb bc} column-major blocks, box {16, 64}
+  CUtensorMap X[2];               // [0] x^ pool, [1] x_c (dense layer): 1D, box 64
+  int64_t xrow0[kMaxLevels + 2];  // per layer: offset of its x^ in X[0]
+  int dense;                      // the dense layer's index
+};
+
+__global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __grid_constant__ LayerTable T,
+                                                                     const __grid_constant__ TmaTable M,
+                                                                     const uint32_t* __restrict__ work,
+                                                                     int64_t nwork) {
+  using namespace tma;
+  extern __shared__ double ring_raw[];
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ring_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kBStages], empty[kBStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kBStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int stage = 0;
+  uint32_t phase = 0;
+  if (warp == kBWarps) {  // producer: one elected lane
+    if (lane == 0) {
+      const uint64_t pol_s = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
+      for (int64_t it = blockIdx.x; it < nwork; it += gridDim.x) {
+        const uint32_t u = __ldg(work + it);
+        const int li = int(u >> kLayerShift);
+        const LayerDesc& D = T.L[li];
+        const int row = int(u & ((1u << kLayerShift) - 1));
+        const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
+        const CUtensorMap* xm = &M.X[li == M.dense ? 1 : 0];
+        for (int b = b0; b < b1; ++b) {
+          const int col = __ldg(D.ci + b);
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (D.br > 0 && D.bc > 0) {
+            // 4 boxes + the x segment; the segment starts at an even element
+            // (a TMA box must start 16-byte aligned): consumers skip x0 & 1
+            mbar_expect_tx(&full[stage], uint32_t((4 * kBBox + kBXBox) * sizeof(double)));
+            double* dst = ring + stage * kBStage;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) tma_2d(dst + h * kBBox, &M.S[li], 16 * h, b * D.bc, &full[stage], pol_s);
+            const int64_t x0 = M.xrow0[li] + int64_t(col) * D.bc;
+            tma_1d(dst + 4 * kBBox, xm, int(x0 & ~int64_t(1)), &full[stage], pol_x);
+          } else {  // rank-0 blocks: nothing to load
+            mbar_arrive(&full[stage]);
+          }
+          if (++stage == kBStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int i = lane & 15, hh = lane >> 4;
+  const int r = 16 * warp + i;
+  for (int64_t it = blockIdx.x; it < nwork; it += gridDim.x) {
+    const uint32_t u = __ldg(work + it);
+    const LayerDesc& D = T.L[u >> kLayerShift];
+    const int row = int(u & ((1u << kLayerShift) - 1));
+    const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
+    const int br = D.br, bc = D.bc;
+    const bool live = 16 * warp < br && bc > 0;  // warp-uniform
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // four FMA chains
+    for (int b = b0; b < b1; ++b) {
+      const int xo = int((M.xrow0[u >> kLayerShift] + int64_t(__ldg(D.ci + b)) * bc) & 1);
+      mbar_wait(&full[stage], phase);
+      if (live) {
+        const double* Sx = ring + stage * kBStage + warp * kBBox;
+        const double* xs = ring + stage * kBStage + 4 * kBBox + xo + 32 * hh;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const int j = 32 * hh + jj;
+          if (j < bc) acc[jj & 3] = fma(Sx[swz(j, i)], xs[jj], acc[jj & 3]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kBStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    a += __shfl_xor_sync(kFull, a, 16);
+    if (hh == 0 && r < br) D.y[int64_t(row) * br + r] = a;
+  }
+}
+
 // block_sparse_mv(L, x, y, alpha, beta) for one generic layer (any block_rows x
 // block_cols, brows / bcols <= 128), in the reference's exact arithmetic
 // (bsr.hpp:50-73): y_r = (beta == 0 ? 0 : beta y_r), then for every block in
@@ -574,7 +696,28 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
   d.br = A.dense.br;
   d.bc = A.dense.bc;
   d.ld = std::max(2, A.dense.ld);
-  k_bsr<<<warp_grid(nwork), kThreads, 0, s>>>(T, work, nwork);
+  // the tensor maps need 16-byte aligned bases (user device pointers of the
+  // phase API may not be): the register-fed kernel takes any alignment
+  const auto aligned = [](const double* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (kTmaBsr && aligned(xh) && aligned(xdense)) {
+    TmaTable M{};
+    if (xh) tma::encode_1d(&M.X[0], xh, uint64_t(std::max<int64_t>(1, xoff[A.q + 1])), kBXBox);
+    if (xdense) tma::encode_1d(&M.X[1], xdense, uint64_t(std::max(1, A.n)), kBXBox);
+    M.dense = A.q + 1;
+    for (int l = 0; l <= A.q + 1; ++l) {
+      const Layer& L = l <= A.q ? A.cpl[l] : A.dense;
+      M.xrow0[l] = l <= A.q ? xoff[l] : 0;
+      const bool xok = l <= A.q ? xh != nullptr : xdense != nullptr;
+      if (xok && L.nb > 0 && L.br > 0 && L.bc > 0)
+        tma::encode_box16x64(&M.S[l], L.val, uint64_t(std::max(2, L.ld)), uint64_t(L.nb) * L.bc,
+                             uint64_t(std::max(2, L.ld)));
+    }
+    H2B_CUDA(cudaFuncSetAttribute(k_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBSmem)));
+    k_bsr_tma<<<unsigned(std::min<int64_t>(nwork, int64_t(kBCtas) * sm_count())), 32 * (kBWarps + 1), kBSmem, s>>>(
+        T, M, work, nwork);
+  } else {
+    k_bsr<<<warp_grid(nwork), kThreads, 0, s>>>(T, work, nwork);
+  }
   H2B_CUDA(cudaGetLastError());
 }
 

@@ -22,9 +22,7 @@
 // k_down_leaf_mv (alpha/beta scatter fused, coalesced through shared memory).
 #include "dataflow.cuh"
 #include "h2b_internal.hpp"
-
-#include <cuda.h>
-#include <cudaTypedefs.h>
+#include "tma.cuh"
 
 #ifndef H2B_TSTAGES
 #define H2B_TSTAGES 2
@@ -37,6 +35,8 @@
 
 namespace h2b {
 namespace {
+
+using namespace tma;
 
 constexpr int kThreads = 256;
 constexpr int NV = 16;        // vectors per pass (2 DMMA column tiles)
@@ -520,52 +520,6 @@ struct TmaTableMV {
   int dense;                      // the dense layer's index
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return uint32_t(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-// L2 policies of the TMA loads: the matrix stream evict-first (read once),
-// the x^ panels evict-last (re-read by every block of their block column).
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                       uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
-      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-// Element (line, e) of a 128-byte-swizzled box of 16-double lines.
-__device__ __forceinline__ int swz(int line, int e) { return line * 16 + ((((e >> 1) ^ line) & 7) << 1) + (e & 1); }
-
 __global__ void __launch_bounds__(32 * (kTWarps + 1), kTCtas) k_bsr_mv_tma(const __grid_constant__ LayerTableMV T,
                                                                      const __grid_constant__ TmaTableMV M,
                                                                      const uint32_t* __restrict__ work,
@@ -799,30 +753,6 @@ constexpr int kUnrDown = 2;  // pair-steps in flight of the fused downsweep (see
 
 unsigned flat_grid_mv(int64_t items) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(sms()) * 16)));
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    H2B_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    require(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  return fn;
-}
-
-// 2D f64 tensor {inner, outer} (outer stride `ld` doubles), boxes of 16 x 64
-// elements, 128-byte swizzle, out-of-range elements zero-filled.
-void encode_box16x64(CUtensorMap* m, const double* base, uint64_t inner, uint64_t outer, uint64_t ld) {
-  const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {ld * sizeof(double)};
-  const cuuint32_t box[2] = {16, 64};
-  const cuuint32_t es[2] = {1, 1};
-  const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
-                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(H2B_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
 }
 
 void ensure_mv_work(Matrix& A, Work& w) {

@@ -240,3 +240,24 @@ def test_hmv_multi_compressed_ranks(gpu):
         Y = h2.hmv_multi(A, X)
         for v in (0, 5, 15):
             assert rel_err(Y[v], h2.hmv(A, X[v])) <= TOL, (dim, order, eps, A.info().ranks)
+
+
+def test_tree_multiply_misaligned_device_pointers(gpu):
+    """tree_multiply (the coupling product, hmv.hpp:114-125) on device x^ / y^
+    pointers that are 8 bytes off a 16-byte boundary: the TMA-streamed kernel
+    needs aligned tensor-map bases, so such calls take the register-fed
+    kernel -- same result as the aligned call."""
+    import ctypes as C
+    import torch
+    from paper_1902_01829_b200 import _lib
+    A = h2.H2Matrix.construct(2, 1 << 14)
+    nx, ny = A.col_vec_size(), A.vec_size()
+    xh = np.random.default_rng(5).random(nx)
+    ref = h2.tree_multiply(A, xh)
+    xb = torch.zeros(nx + 1, dtype=torch.float64, device="cuda")
+    yb = torch.zeros(ny + 1, dtype=torch.float64, device="cuda")
+    xb[1:] = torch.from_numpy(xh)
+    _lib.check(_lib.load().h2b_tree_multiply(A._h, C.c_void_p(xb[1:].data_ptr()), C.c_void_p(yb[1:].data_ptr()),
+                                             _lib.PTR_DEVICE))
+    torch.cuda.synchronize()
+    assert rel_err(yb[1:].cpu().numpy(), ref) <= 1e-14
