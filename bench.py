@@ -781,7 +781,7 @@ def main():
         "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
         "phase_ms": {"upsweep": round(phases[0], 4), "coupling_dense_bsr": round(phases[1], 4),
                      "downsweep_scatter": round(phases[2], 4)},
-        "roofline": {"bound": "hbm", "kernel": "k_bsr (coupling + dense blocks)",
+        "roofline": {"bound": "hbm", "kernel": "k_bsr_tma (coupling + dense blocks, TMA-streamed)",
                      "achieved": round(achieved, 1) if achieved else None, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
