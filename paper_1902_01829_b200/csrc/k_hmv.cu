@@ -323,11 +323,13 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
 // producer lane loads each block as 4 tensor-map boxes of 16 rows x 64 columns
 // (128-byte swizzle; zero fill out of range) plus the 64-double x segment of
 // its block column (1D tensor map, from an even element: TMA boxes start
-// 16-byte aligned), completion on the stage's mbarrier; four
-// consumer warps own a box each: lane (i, h) accumulates row 16w + i over the
-// columns [32h, 32h + 32) from shared memory (a line of the box is the 16 rows
-// of one column: two conflict-free wavefronts per load), the halves meet by a
-// shuffle at the end of the row.
+// 16-byte aligned), completion on the stage's mbarrier; four consumer warps
+// own a box each: lane (rp, cq) accumulates rows 16w + 2rp and 16w + 2rp + 1
+// over the columns [16cq, 16cq + 16), one 16-byte shared load per column (a
+// box line holds the 16 rows of one column; a quarter warp reads 8 distinct
+// swizzled chunks of a line: conflict-free), the column quarters meet by two
+// shuffles at the end of the row.  (One row per lane with 8-byte loads: 2-3%
+// slower, twice the shared loads.)
 #ifndef H2B_BSTAGES
 #define H2B_BSTAGES 2
 #endif
@@ -397,8 +399,10 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
     }
     return;
   }
-  const int i = lane & 15, hh = lane >> 4;
-  const int r = 16 * warp + i;
+  // lane = 8 cq + rp: rows 16w + 2rp, 16w + 2rp + 1 (one 16-byte load per
+  // column: two rows of a box line), columns [16cq, 16cq + 16)
+  const int rp = lane & 7, cq = lane >> 3;
+  const int r = 16 * warp + 2 * rp;
   for (int64_t it = blockIdx.x; it < nwork; it += gridDim.x) {
     const uint32_t u = __ldg(work + it);
     const LayerDesc& D = T.L[u >> kLayerShift];
@@ -406,17 +410,22 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
     const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
     const int br = D.br, bc = D.bc;
     const bool live = 16 * warp < br && bc > 0;  // warp-uniform
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // four FMA chains
+    double a0[2] = {0.0, 0.0}, a1[2] = {0.0, 0.0};  // rows r, r + 1; two FMA chains each
     for (int b = b0; b < b1; ++b) {
       const int xo = int((M.xrow0[u >> kLayerShift] + int64_t(__ldg(D.ci + b)) * bc) & 1);
       mbar_wait(&full[stage], phase);
       if (live) {
         const double* Sx = ring + stage * kBStage + warp * kBBox;
-        const double* xs = ring + stage * kBStage + 4 * kBBox + xo + 32 * hh;
+        const double* xs = ring + stage * kBStage + 4 * kBBox + xo + 16 * cq;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const int j = 32 * hh + jj;
-          if (j < bc) acc[jj & 3] = fma(Sx[swz(j, i)], xs[jj], acc[jj & 3]);
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = 16 * cq + jj;
+          if (j < bc) {
+            const double2 sv = *reinterpret_cast<const double2*>(Sx + swz(j, 2 * rp));
+            const double xj = xs[jj];
+            a0[jj & 1] = fma(sv.x, xj, a0[jj & 1]);
+            a1[jj & 1] = fma(sv.y, xj, a1[jj & 1]);
+          }
         }
       }
       __syncwarp();
@@ -426,9 +435,16 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
         phase ^= 1u;
       }
     }
-    double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    a += __shfl_xor_sync(kFull, a, 16);
-    if (hh == 0 && r < br) D.y[int64_t(row) * br + r] = a;
+    double y0 = a0[0] + a0[1], y1 = a1[0] + a1[1];
+    y0 += __shfl_xor_sync(kFull, y0, 8);
+    y1 += __shfl_xor_sync(kFull, y1, 8);
+    y0 += __shfl_xor_sync(kFull, y0, 16);
+    y1 += __shfl_xor_sync(kFull, y1, 16);
+    if (cq == 0) {
+      double* yr = D.y + int64_t(row) * br;
+      if (r < br) yr[r] = y0;
+      if (r + 1 < br) yr[r + 1] = y1;
+    }
   }
 }
 
