@@ -320,8 +320,8 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
 // (k_bsr_tma): a read-only 64 GB stream measured 7.44 TB/s through a TMA ring
 // against 7.06-7.09 TB/s with 16-byte evict-first loads
 // (tools/microbench/tma_stream.cu).  One CTA walks its rows of the LPT list; a
-// producer lane loads each block as 4 tensor-map boxes of 16 rows x 64 columns
-// (128-byte swizzle; zero fill out of range) plus the 64-double x segment of
+// producer lane loads each block as one tensor-map box of 64 x 64 (zero fill
+// out of range; column-major, 64-double column stride) plus the x segment of
 // its block column (1D tensor map, from an even element: TMA boxes start
 // 16-byte aligned), completion on the stage's mbarrier; four consumer warps
 // own a box each: lane (rp, cq) accumulates rows 16w + 2rp and 16w + 2rp + 1
@@ -329,11 +329,21 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
 // box line holds the 16 rows of one column; a quarter warp reads 8 distinct
 // swizzled chunks of a line: conflict-free), the column quarters meet by two
 // shuffles at the end of the row.  (One row per lane with 8-byte loads: 2-3%
-// slower, twice the shared loads.)
+// slower, twice the shared loads.)  Measured at C4, ms per mat-vec: one
+// unswizzled 64 x 64 box per block = four swizzled 16 x 64 boxes (11.94);
+// stages x CTAs/SM 2 x 2 12.0, 4 x 1 12.0, 1 x 4 12.04, 2 x 3 12.45, 3 x 2
+// 12.47 -- four blocks (128 KB) in flight per SM is the sweet spot.
 #ifndef H2B_BSTAGES
 #define H2B_BSTAGES 2
 #endif
-constexpr int kBStages = H2B_BSTAGES, kBCtas = 2, kBWarps = 4;
+#ifndef H2B_BBOX64
+#define H2B_BBOX64 1
+#endif
+constexpr bool kBBox64 = H2B_BBOX64;  // one unswizzled 64 x 64 box per block (else 4 swizzled 16 x 64)
+#ifndef H2B_BCTAS
+#define H2B_BCTAS 2
+#endif
+constexpr int kBStages = H2B_BSTAGES, kBCtas = H2B_BCTAS, kBWarps = 4;
 constexpr int kBBox = 16 * 64;
 constexpr int kBXBox = 66;  // x segment: 64 doubles from an even start (one more when it is odd)
 constexpr int kBStage = 4 * kBBox + 128;  // + the x segment, padded: every stage 1024-byte aligned (swizzle)
@@ -383,8 +393,11 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
             // (a TMA box must start 16-byte aligned): consumers skip x0 & 1
             mbar_expect_tx(&full[stage], uint32_t((4 * kBBox + kBXBox) * sizeof(double)));
             double* dst = ring + stage * kBStage;
+            if (kBBox64)
+              tma_2d(dst, &M.S[li], 0, b * D.bc, &full[stage], pol_s);
+            else
 #pragma unroll
-            for (int h = 0; h < 4; ++h) tma_2d(dst + h * kBBox, &M.S[li], 16 * h, b * D.bc, &full[stage], pol_s);
+              for (int h = 0; h < 4; ++h) tma_2d(dst + h * kBBox, &M.S[li], 16 * h, b * D.bc, &full[stage], pol_s);
             const int64_t x0 = M.xrow0[li] + int64_t(col) * D.bc;
             tma_1d(dst + 4 * kBBox, xm, int(x0 & ~int64_t(1)), &full[stage], pol_x);
           } else {  // rank-0 blocks: nothing to load
@@ -415,13 +428,13 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
       const int xo = int((M.xrow0[u >> kLayerShift] + int64_t(__ldg(D.ci + b)) * bc) & 1);
       mbar_wait(&full[stage], phase);
       if (live) {
-        const double* Sx = ring + stage * kBStage + warp * kBBox;
+        const double* Sx = ring + stage * kBStage + (kBBox64 ? 16 * warp : warp * kBBox);
         const double* xs = ring + stage * kBStage + 4 * kBBox + xo + 16 * cq;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
           const int j = 16 * cq + jj;
           if (j < bc) {
-            const double2 sv = *reinterpret_cast<const double2*>(Sx + swz(j, 2 * rp));
+            const double2 sv = *reinterpret_cast<const double2*>(Sx + (kBBox64 ? 64 * j + 2 * rp : swz(j, 2 * rp)));
             const double xj = xs[jj];
             a0[jj & 1] = fma(sv.x, xj, a0[jj & 1]);
             a1[jj & 1] = fma(sv.y, xj, a1[jj & 1]);
@@ -725,8 +738,8 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
       M.xrow0[l] = l <= A.q ? xoff[l] : 0;
       const bool xok = l <= A.q ? xh != nullptr : xdense != nullptr;
       if (xok && L.nb > 0 && L.br > 0 && L.bc > 0)
-        tma::encode_box16x64(&M.S[l], L.val, uint64_t(std::max(2, L.ld)), uint64_t(L.nb) * L.bc,
-                             uint64_t(std::max(2, L.ld)));
+        (kBBox64 ? tma::encode_box64x64 : tma::encode_box16x64)(&M.S[l], L.val, uint64_t(std::max(2, L.ld)),
+                                                                uint64_t(L.nb) * L.bc, uint64_t(std::max(2, L.ld)));
     }
     H2B_CUDA(cudaFuncSetAttribute(k_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBSmem)));
     k_bsr_tma<<<unsigned(std::min<int64_t>(nwork, int64_t(kBCtas) * sm_count())), 32 * (kBWarps + 1), kBSmem, s>>>(

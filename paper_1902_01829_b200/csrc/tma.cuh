@@ -96,6 +96,20 @@ inline void encode_box16x64(CUtensorMap* m, const double* base, uint64_t inner, 
   if (r != CUDA_SUCCESS) throw Error(H2B_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
 
+// 2D f64 tensor {inner, outer} (outer stride `ld` doubles), boxes of 64 x 64
+// elements without swizzle (one 32 KB block per load, column-major in shared
+// memory with a 64-double column stride), out-of-range elements zero-filled.
+inline void encode_box64x64(CUtensorMap* m, const double* base, uint64_t inner, uint64_t outer, uint64_t ld) {
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * sizeof(double)};
+  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(H2B_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
 // 1D f64 tensor of n elements, boxes of `box` elements (no swizzle), zero fill
 // beyond n.
 inline void encode_1d(CUtensorMap* m, const double* base, uint64_t n, uint32_t box) {
