@@ -222,6 +222,9 @@ H2B_API h2b_status h2b_hmv_graph_create(h2b_matrix* A, h2b_context* ctx, const d
                                         double beta, h2b_hmv_graph** out);
 H2B_API h2b_status h2b_hmv_graph_launch(h2b_hmv_graph* g, void* stream);
 H2B_API h2b_status h2b_hmv_graph_destroy(h2b_hmv_graph* g);
+/* Y <- alpha A X + beta Y for nvec columns (column v at X + v ldx / Y + v ldy),
+ * 16 columns per FP64-tensor-core pass.  Host pointers: synchronous; device
+ * pointers: stream-ordered on `stream` (NULL = the matrix's own stream). */
 H2B_API h2b_status h2b_hmv_multi(h2b_matrix* A, int nvec, const double* X, int64_t ldx, double* Y,
                          int64_t ldy, double alpha, double beta, h2b_ptr_kind kind, void* stream);
 

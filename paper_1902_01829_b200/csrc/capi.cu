@@ -987,7 +987,8 @@ h2b_status h2b_hmv_multi(h2b_matrix* Ah, int nvec, const double* X, int64_t ldx,
     if (!dy)
       H2B_CUDA(cudaMemcpy2DAsync(Y, ldy * sizeof(double), ys.p, A.n * sizeof(double), A.n * sizeof(double),
                                  nvec, cudaMemcpyDeviceToHost, s));
-    H2B_CUDA(cudaStreamSynchronize(s));
+    // host vectors: synchronous (like h2b_hmv); device vectors: stream-ordered
+    if (!dx || !dy) H2B_CUDA(cudaStreamSynchronize(s));
   });
 }
 
