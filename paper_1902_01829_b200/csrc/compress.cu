@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "cta_linalg.cuh"
+#include "tma.cuh"
 #include "h2b_internal.hpp"
 
 namespace h2b {
@@ -127,6 +128,12 @@ struct ProjLevel {
 };
 struct ProjTable {
   ProjLevel L[kMaxLevels + 1];
+  // TMA staging of the launched level (tma != 0): 3D views {ld, cols, blocks}
+  // of S, T_row and T_col, box {kPLd, 64, 1} -- one load lands a zero-padded
+  // 64 x kPLd tile exactly like stage64 (out-of-range rows / columns filled
+  // with zeros by the TMA unit)
+  CUtensorMap mS, mT, mTc;
+  int tma;
   int tri;          // T upper triangular (orthogonalization's R factors)
   double* rowsum;   // per block row: sum of squares of the projected blocks (or null)
   int max_row;      // longest block row over the levels (smem work list)
@@ -360,9 +367,23 @@ __device__ __forceinline__ void stage64(double* dst, const double* src, int lds,
 // The row's work list (symmetric levels: upper blocks only, each also writing
 // its mirror) is compacted into smem first: no dependent global index loads
 // between blocks.
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(tma::smem_u32(dst)),
+      "l"(map), "r"(0), "r"(0), "r"(c2), "r"(tma::smem_u32(bar))
+      : "memory");
+}
+constexpr uint32_t kTileBytes = 64 * kPLd * sizeof(double);
+#ifndef H2B_PROJ_TMA
+#define H2B_PROJ_TMA 1
+#endif
+constexpr bool kProjTma = H2B_PROJ_TMA;
+
 __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__ ProjTable P,
                                                          const ProjRow* __restrict__ rows) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[3];  // TMA staging: T_row, S, T_col
   const ProjRow pr = rows[blockIdx.x];
   const ProjLevel& L = P.L[pr.level];
   const int ro = L.ro, rn = L.rn, co = L.co, cn = L.cn;
@@ -373,7 +394,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   int* blist = wcnt + 32;  // blocks to project
   int* clist = blist + P.max_row;  // their block columns
   int* mlist = clist + P.max_row;  // their mirror block (or -1)
-  stage64(Tr, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
+  const bool tma = P.tma != 0;
+  uint32_t ph_s = 0, ph_t = 0;
+  // staging: TMA (one elected thread, mbarrier per buffer) or cp.async groups
+  auto issue = [&](int which, double* dst, int node) {
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of dst before
+      tma::mbar_expect_tx(&bar[which], kTileBytes);
+      tma_3d(dst, which == 0 ? &P.mT : which == 1 ? &P.mS : &P.mTc, node, &bar[which]);
+    }
+  };
+  auto stage_S = [&](int k) {
+    if (tma) issue(1, Sb, blist[k]);
+    else stage64(Sb, L.S + int64_t(blist[k]) * L.istride, L.ld_old, ro, co);
+  };
+  auto stage_Tc = [&](int k) {
+    if (tma) issue(2, Tc, clist[k]);
+    else stage64(Tc, L.Tc + int64_t(clist[k]) * cn * co, cn, cn, co);
+  };
+  if (tma) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 3; ++i) tma::mbar_init(&bar[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    issue(0, Tr, pr.row);
+  } else {
+    stage64(Tr, L.T + int64_t(pr.row) * rn * ro, rn, rn, ro);
+  }
   const int b0 = L.rp[pr.row], b1 = L.rp[pr.row + 1];
   // ---- ordered compaction of the row's work list ----
   int nk = 0;
@@ -406,13 +454,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
   }
   double ss = 0.0;
   if (nk > 0) {
-    stage64(Sb, L.S + int64_t(blist[0]) * L.istride, L.ld_old, ro, co);
+    stage_S(0);
     cp_async_commit();  // {T_row, S_0}
-    stage64(Tc, L.Tc + int64_t(clist[0]) * cn * co, cn, cn, co);
+    stage_Tc(0);
     cp_async_commit();  // {T_col,0}
   }
+  if (tma) tma::mbar_wait(&bar[0], 0);  // T_row
+  auto wait_S = [&](bool two_in_flight) {
+    if (tma) {
+      tma::mbar_wait(&bar[1], ph_s);
+      ph_s ^= 1u;
+    } else if (two_in_flight) {
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+  };
+  auto wait_Tc = [&](bool two_in_flight) {
+    if (tma) {
+      tma::mbar_wait(&bar[2], ph_t);
+      ph_t ^= 1u;
+    } else if (two_in_flight) {
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+  };
   for (int k = 0; k < nk; ++k) {
-    cp_async_wait<1>();  // S_k (T_col,k may still be in flight)
+    wait_S(true);  // S_k (T_col,k may still be in flight)
     __syncthreads();
     const int b = blist[k], mb = mlist[k];
     double* out = L.out + int64_t(b) * L.ostride;
@@ -426,14 +495,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
       const bool live = ts_cols<true>(Tr, Sb, ro, co, rn, acc);
       __syncthreads();  // S_k consumed
       if (live) ts_store(acc, Sb, rn);
-      cp_async_wait<0>();  // T_col,k
+      wait_Tc(false);  // T_col,k
       __syncthreads();
       out_rows<true>(Sb, Tc, out, outT, L.ld_new, co, rn, cn, s1);
       __syncthreads();  // TS, T_col,k consumed
       if (k + 1 < nk) {
-        stage64(Sb, L.S + int64_t(blist[k + 1]) * L.istride, L.ld_old, ro, co);
+        stage_S(k + 1);
         cp_async_commit();
-        stage64(Tc, L.Tc + int64_t(clist[k + 1]) * cn * co, cn, cn, co);
+        stage_Tc(k + 1);
         cp_async_commit();
       }
     } else {
@@ -441,13 +510,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_project(const __grid_constant__
       // under TS_{k+1}
       const bool live = ts_strip<false>(Tr, Sb, ro, co, rn, acc);
       __syncthreads();  // S_k consumed
-      if (k + 1 < nk) stage64(Sb, L.S + int64_t(blist[k + 1]) * L.istride, L.ld_old, ro, co);
+      if (k + 1 < nk) stage_S(k + 1);
       cp_async_commit();
-      cp_async_wait<1>();  // T_col,k
+      wait_Tc(true);  // T_col,k
       __syncthreads();
       if (live) out_strip<false>(acc, Tc, out, outT, L.ld_new, co, rn, cn, s1);
       __syncthreads();  // T_col,k consumed
-      if (k + 1 < nk) stage64(Tc, L.Tc + int64_t(clist[k + 1]) * cn * co, cn, cn, co);
+      if (k + 1 < nk) stage_Tc(k + 1);
       cp_async_commit();
     }
     ss += outT ? 2.0 * s1 : s1;
@@ -1359,6 +1428,17 @@ void project_level(const Matrix& A, const TreePool& T, const TreePool& Tc, const
   d.istride = L.block_stride();
   d.out = out ? out : L.val;  // default: in the old slots
   d.ostride = out ? ostride : L.block_stride();
+  // TMA staging when every tile source is a 16-byte aligned pool of even-ld
+  // blocks (odd ranks keep the 8-byte cp.async path)
+  const auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const int64_t nT = A.nodes(l), nTc = A.col_basis().nodes(l);
+  if (kProjTma && (L.ld & 1) == 0 && (rn & 1) == 0 && (cn & 1) == 0 && al(d.S) && al(d.T) && al(d.Tc) &&
+      L.nb > 0) {
+    tma::encode_blocks3d(&P.mS, d.S, uint64_t(L.ld), uint64_t(co), uint64_t(L.nb), kPLd, 64);
+    tma::encode_blocks3d(&P.mT, d.T, uint64_t(rn), uint64_t(ro), uint64_t(std::max<int64_t>(1, nT)), kPLd, 64);
+    tma::encode_blocks3d(&P.mTc, d.Tc, uint64_t(cn), uint64_t(co), uint64_t(std::max<int64_t>(1, nTc)), kPLd, 64);
+    P.tma = 1;
+  }
   const size_t smax = size_t(3) * 64 * kPLd * sizeof(double) + (32 + 3 * size_t(P.max_row)) * sizeof(int);
   check_smem(smax, "project_coupling");
   set_smem(k_project, smax);

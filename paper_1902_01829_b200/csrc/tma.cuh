@@ -110,6 +110,22 @@ inline void encode_box64x64(CUtensorMap* m, const double* base, uint64_t inner, 
   if (r != CUDA_SUCCESS) throw Error(H2B_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
 
+// 3D f64 view {ld, cols, blocks} of a pool of column-major blocks (ld x cols
+// each, consecutive), boxes {box_rows, box_cols, 1} without swizzle: one load
+// puts a block into a box_rows-strided shared tile, rows >= ld and columns >=
+// cols zero-filled.  Needs 16-byte aligned base and ld even.
+inline void encode_blocks3d(CUtensorMap* m, const double* base, uint64_t ld, uint64_t cols, uint64_t blocks,
+                            uint32_t box_rows, uint32_t box_cols) {
+  const cuuint64_t dims[3] = {ld, cols, blocks};
+  const cuuint64_t strides[2] = {ld * sizeof(double), ld * cols * sizeof(double)};
+  const cuuint32_t box[3] = {box_rows, box_cols, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(H2B_CUDA_ERROR, "cuTensorMapEncodeTiled (3D) failed: " + std::to_string(int(r)));
+}
+
 // 1D f64 tensor of n elements, boxes of `box` elements (no swizzle), zero fill
 // beyond n.
 inline void encode_1d(CUtensorMap* m, const double* base, uint64_t n, uint32_t box) {
