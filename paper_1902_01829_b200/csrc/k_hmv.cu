@@ -244,7 +244,8 @@ struct LayerDesc {
   const double* x;
   double* y;
   int64_t stride;
-  int br, bc, ld, pad;
+  int br, bc, ld;
+  int tma;  // rows of this layer go to k_bsr_tma (full 64 x 64 blocks), else to k_bsr
 };
 struct LayerTable {
   LayerDesc L[kMaxLevels + 2];
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_bsr(const __grid_constant__ LayerT
   for (int64_t it = warp_global(); it < nwork; it += warp_count()) {
     const uint32_t u = __ldg(work + it);
     const LayerDesc& D = T.L[u >> kLayerShift];
+    if (D.tma) continue;  // streamed by k_bsr_tma
     const int row = int(u & ((1u << kLayerShift) - 1));
     const int lpc = D.ld >> 1;
     const int G = 32 / lpc;
@@ -349,8 +351,8 @@ constexpr int kBXBox = 66;  // x segment: 64 doubles from an even start (one mor
 constexpr int kBStage = 4 * kBBox + 128;  // + the x segment, padded: every stage 1024-byte aligned (swizzle)
 constexpr size_t kBSmem = size_t(kBStages) * kBStage * sizeof(double) + 1024;
 struct TmaTable {
-  CUtensorMap S[kMaxLevels + 2];  // per layer: {ld, nb bc} column-major blocks, box {16, 64}
-  CUtensorMap X[2];               // [0] x^ pool, [1] x_c (dense layer): 1D, box 64
+  CUtensorMap S[kMaxLevels + 2];  // per layer: 3D {ld, bc, nb} blocks, box {64, 64, 1}
+  CUtensorMap X[2];               // [0] x^ pool, [1] x_c (dense layer): 1D, box 66
   int64_t xrow0[kMaxLevels + 2];  // per layer: offset of its x^ in X[0]
   int dense;                      // the dense layer's index
 };
@@ -382,6 +384,7 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
         const uint32_t u = __ldg(work + it);
         const int li = int(u >> kLayerShift);
         const LayerDesc& D = T.L[li];
+        if (!D.tma) continue;  // small blocks: k_bsr
         const int row = int(u & ((1u << kLayerShift) - 1));
         const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
         const CUtensorMap* xm = &M.X[li == M.dense ? 1 : 0];
@@ -394,10 +397,10 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
             mbar_expect_tx(&full[stage], uint32_t((4 * kBBox + kBXBox) * sizeof(double)));
             double* dst = ring + stage * kBStage;
             if (kBBox64)
-              tma_2d(dst, &M.S[li], 0, b * D.bc, &full[stage], pol_s);
+              tma_3d(dst, &M.S[li], 0, b, &full[stage], pol_s);
             else
 #pragma unroll
-              for (int h = 0; h < 4; ++h) tma_2d(dst + h * kBBox, &M.S[li], 16 * h, b * D.bc, &full[stage], pol_s);
+              for (int h = 0; h < 4; ++h) tma_3d(dst + h * kBBox, &M.S[li], 16 * h, b, &full[stage], pol_s);
             const int64_t x0 = M.xrow0[li] + int64_t(col) * D.bc;
             tma_1d(dst + 4 * kBBox, xm, int(x0 & ~int64_t(1)), &full[stage], pol_x);
           } else {  // rank-0 blocks: nothing to load
@@ -419,6 +422,7 @@ __global__ void __launch_bounds__(32 * (kBWarps + 1), kBCtas) k_bsr_tma(const __
   for (int64_t it = blockIdx.x; it < nwork; it += gridDim.x) {
     const uint32_t u = __ldg(work + it);
     const LayerDesc& D = T.L[u >> kLayerShift];
+    if (!D.tma) continue;
     const int row = int(u & ((1u << kLayerShift) - 1));
     const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
     const int br = D.br, bc = D.bc;
@@ -728,7 +732,27 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
   // the tensor maps need 16-byte aligned bases (user device pointers of the
   // phase API may not be): the register-fed kernel takes any alignment
   const auto aligned = [](const double* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (kTmaBsr && aligned(xh) && aligned(xdense)) {
+  // every layer with its x present streams through k_bsr_tma (3D block views:
+  // a compressed level's smaller blocks cost only their bytes).  C3, ms per
+  // mat-vec: uncompressed 8.55 vs 8.85 with k_bsr; compressed at 1e-6 (ranks
+  // 34-60) 5.96-6.08 for both, and 6.06-6.09 with only the full 64 x 64 levels
+  // on the ring.  k_bsr takes layers whose x is absent (phase calls) and
+  // misaligned phase-API pointers.
+  bool any_tma = false;
+  if (kTmaBsr && aligned(xh) && aligned(xdense))
+    for (int l = 0; l <= A.q + 1; ++l) {
+      const Layer& L = l <= A.q ? A.cpl[l] : A.dense;
+      T.L[l].tma = l <= A.q ? xh != nullptr : xdense != nullptr;
+      any_tma = any_tma || (T.L[l].tma && L.nb > 0);
+    }
+  if (!any_tma)
+    for (int l = 0; l <= A.q + 1; ++l) T.L[l].tma = 0;
+  bool any_reg = false;
+  for (int l = 0; l <= A.q + 1; ++l) {
+    const Layer& L = l <= A.q ? A.cpl[l] : A.dense;
+    any_reg = any_reg || (!T.L[l].tma && L.rows > 0);
+  }
+  if (any_tma) {
     TmaTable M{};
     if (xh) tma::encode_1d(&M.X[0], xh, uint64_t(std::max<int64_t>(1, xoff[A.q + 1])), kBXBox);
     if (xdense) tma::encode_1d(&M.X[1], xdense, uint64_t(std::max(1, A.n)), kBXBox);
@@ -736,17 +760,16 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
     for (int l = 0; l <= A.q + 1; ++l) {
       const Layer& L = l <= A.q ? A.cpl[l] : A.dense;
       M.xrow0[l] = l <= A.q ? xoff[l] : 0;
-      const bool xok = l <= A.q ? xh != nullptr : xdense != nullptr;
-      if (xok && L.nb > 0 && L.br > 0 && L.bc > 0)
-        (kBBox64 ? tma::encode_box64x64 : tma::encode_box16x64)(&M.S[l], L.val, uint64_t(std::max(2, L.ld)),
-                                                                uint64_t(L.nb) * L.bc, uint64_t(std::max(2, L.ld)));
+      if (T.L[l].tma && L.nb > 0)
+        tma::encode_blocks3d(&M.S[l], L.val, uint64_t(std::max(2, L.ld)), uint64_t(L.bc), uint64_t(L.nb),
+                             kBBox64 ? 64 : 16, 64, !kBBox64);
     }
     H2B_CUDA(cudaFuncSetAttribute(k_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBSmem)));
     k_bsr_tma<<<unsigned(std::min<int64_t>(nwork, int64_t(kBCtas) * sm_count())), 32 * (kBWarps + 1), kBSmem, s>>>(
         T, M, work, nwork);
-  } else {
-    k_bsr<<<warp_grid(nwork), kThreads, 0, s>>>(T, work, nwork);
+    H2B_CUDA(cudaGetLastError());
   }
+  if (any_reg) k_bsr<<<warp_grid(nwork), kThreads, 0, s>>>(T, work, nwork);
   H2B_CUDA(cudaGetLastError());
 }
 

@@ -456,7 +456,8 @@ struct LayerDescMV {
   const double* x;  // vector-minor panel base
   double* y;
   int64_t stride;
-  int br, bc, ld, pad;
+  int br, bc, ld;
+  int tma;  // rows of this layer go to k_bsr_mv_tma (full 64 x 64 blocks), else to k_bsr_mv
 };
 struct LayerTableMV {
   LayerDescMV L[kMaxLevels + 2];
@@ -469,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bsr_mv(const __grid_constant__ 
   for (int64_t it = warp_global(); it < nwork; it += warp_count()) {
     const uint32_t u = __ldg(work + it);
     const LayerDescMV& D = T.L[u >> kLayerShift];
+    if (D.tma) continue;  // streamed by k_bsr_mv_tma
     const int row = int(u & ((1u << kLayerShift) - 1));
     const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
     Acc acc;
@@ -514,7 +516,7 @@ constexpr int kTStageDoubles = 5 * kTBox;           // 4 block boxes + the x^ pa
 constexpr size_t kTSmem = size_t(kTStages) * kTStageDoubles * sizeof(double) + 1024;  // + alignment
 
 struct TmaTableMV {
-  CUtensorMap S[kMaxLevels + 2];  // per layer: {ld, nb bc} column-major blocks, box {16, 64}
+  CUtensorMap S[kMaxLevels + 2];  // per layer: 3D {ld, bc, nb} blocks, box {16, 64, 1}, 128-byte swizzle
   CUtensorMap X[2];               // [0] x^ pool, [1] xc (dense layer): {16, rows}, box {16, 64}
   int64_t xrow0[kMaxLevels + 2];  // per layer: first row of its x panels in X
   int dense;                      // the dense layer's index
@@ -546,6 +548,7 @@ __global__ void __launch_bounds__(32 * (kTWarps + 1), kTCtas) k_bsr_mv_tma(const
         const uint32_t u = __ldg(work + it);
         const int li = int(u >> kLayerShift);
         const LayerDescMV& D = T.L[li];
+        if (!D.tma) continue;  // small blocks: k_bsr_mv
         const int row = int(u & ((1u << kLayerShift) - 1));
         const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
         const CUtensorMap* xm = &M.X[li == M.dense ? 1 : 0];
@@ -563,7 +566,7 @@ __global__ void __launch_bounds__(32 * (kTWarps + 1), kTCtas) k_bsr_mv_tma(const
           mbar_expect_tx(&full[stage], 5u * kTBox * sizeof(double));
           double* dst = ring + stage * kTStageDoubles;
 #pragma unroll
-          for (int h = 0; h < 4; ++h) tma_2d(dst + h * kTBox, &M.S[li], 16 * h, b * D.bc, &full[stage], pol_s);
+          for (int h = 0; h < 4; ++h) tma_3d(dst + h * kTBox, &M.S[li], 16 * h, b, &full[stage], pol_s);
           tma_2d(dst + 4 * kTBox, xm, 0, int(M.xrow0[li] + int64_t(col) * D.bc), &full[stage], pol_x);
           if (++stage == kTStages) {
             stage = 0;
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(32 * (kTWarps + 1), kTCtas) k_bsr_mv_tma(const
   for (int64_t it = blockIdx.x; it < nwork; it += gridDim.x) {
     const uint32_t u = __ldg(work + it);
     const LayerDescMV& D = T.L[u >> kLayerShift];
+    if (!D.tma) continue;
     const int row = int(u & ((1u << kLayerShift) - 1));
     const int b0 = __ldg(D.rp + row), b1 = __ldg(D.rp + row + 1);
     const int br = D.br, bc = D.bc;
@@ -888,7 +892,22 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
     // (mma_N_pairs) instead of the 8-byte fragments: 17.3 ms (fewer loads in
     // flight at 255 registers); non-coherent / L2::256B loads: 12.6 ms,
     // 79.4 GB read.  The evict-first 8-byte form stays.
-    if (kTmaBsr) {
+    // every layer through the TMA ring (3D block views: a compressed level's
+    // smaller blocks cost only their bytes).  Measured on C3 compressed at
+    // 1e-6 (ranks 34-60, odd ld): 9.0-9.2 ms per pass against 12.9 ms with the
+    // register-fed k_bsr_mv, 12.8 ms with only the full 64 x 64 levels on the
+    // ring; uncompressed C3 10.4 vs 11.6 ms.  k_bsr_mv remains the H2B_TMA_BSR=0
+    // build's kernel.
+    bool any_tma = false, any_reg = false;
+    for (int l = 0; l <= q + 1; ++l) {
+      const Layer& L = l <= q ? A.cpl[l] : A.dense;
+      T.L[l].tma = kTmaBsr;
+      any_tma = any_tma || (T.L[l].tma && L.nb > 0);
+    }
+    if (!any_tma)
+      for (int l = 0; l <= q + 1; ++l) T.L[l].tma = 0;
+    for (int l = 0; l <= q + 1; ++l) any_reg = any_reg || (!T.L[l].tma && (l <= q ? A.cpl[l] : A.dense).rows > 0);
+    if (any_tma) {
       TmaTableMV M{};
       const int64_t xrows = std::max<int64_t>(1, std::max(A.vec_off[q + 1], C.vec_off[q + 1]));
       encode_box16x64(&M.X[0], xh, NV, uint64_t(xrows), NV);
@@ -897,15 +916,15 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
       for (int l = 0; l <= q + 1; ++l) {
         const Layer& L = l <= q ? A.cpl[l] : A.dense;
         M.xrow0[l] = l <= q ? C.vec_off[l] : 0;
-        if (L.nb > 0 && L.br > 0 && L.bc > 0)
-          encode_box16x64(&M.S[l], L.val, uint64_t(std::max(2, L.ld)), uint64_t(L.nb) * L.bc, uint64_t(std::max(2, L.ld)));
+        if (T.L[l].tma && L.nb > 0)
+          encode_blocks3d(&M.S[l], L.val, uint64_t(std::max(2, L.ld)), uint64_t(L.bc), uint64_t(L.nb), 16, 64, true);
       }
       H2B_CUDA(cudaFuncSetAttribute(k_bsr_mv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTSmem)));
       k_bsr_mv_tma<<<unsigned(std::min<int64_t>(A.nwork, int64_t(kTCtas) * sms())), 32 * (kTWarps + 1), kTSmem, s>>>(T, M, A.work.p,
                                                                                                    A.nwork);
-    } else {
-      k_bsr_mv<<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
+      H2B_CUDA(cudaGetLastError());
     }
+    if (any_reg) k_bsr_mv<<<wgrid(A.nwork), kThreads, 0, s>>>(T, A.work.p, A.nwork);
     H2B_CUDA(cudaGetLastError());
   }
   if (q >= 1) {  // levels 1..q in one dataflow launch (the root's y^ is final)

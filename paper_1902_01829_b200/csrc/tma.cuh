@@ -64,6 +64,15 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
 // Element (line, e) of a 128-byte-swizzled box of 16-double lines.
 __device__ __forceinline__ int swz(int line, int e) { return line * 16 + ((((e >> 1) ^ line) & 7) << 1) + (e & 1); }
 
+// Block b of a 3D view {ld, cols, blocks} (see encode_blocks3d): rows from r0.
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int r0, int b, uint64_t* bar,
+                                       uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "0, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(r0), "r"(b), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_1d(void* dst, const CUtensorMap* map, int c0, uint64_t* bar, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2}], "
@@ -113,15 +122,18 @@ inline void encode_box64x64(CUtensorMap* m, const double* base, uint64_t inner, 
 // 3D f64 view {ld, cols, blocks} of a pool of column-major blocks (ld x cols
 // each, consecutive), boxes {box_rows, box_cols, 1} without swizzle: one load
 // puts a block into a box_rows-strided shared tile, rows >= ld and columns >=
-// cols zero-filled.  Needs 16-byte aligned base and ld even.
+// cols zero-filled -- a block narrower than the box costs only its own bytes
+// (a 2D view would stream the next block's columns).  Needs 16-byte aligned
+// base and ld even.
 inline void encode_blocks3d(CUtensorMap* m, const double* base, uint64_t ld, uint64_t cols, uint64_t blocks,
-                            uint32_t box_rows, uint32_t box_cols) {
+                            uint32_t box_rows, uint32_t box_cols, bool swizzle128 = false) {
   const cuuint64_t dims[3] = {ld, cols, blocks};
   const cuuint64_t strides[2] = {ld * sizeof(double), ld * cols * sizeof(double)};
   const cuuint32_t box[3] = {box_rows, box_cols, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
-                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(H2B_CUDA_ERROR, "cuTensorMapEncodeTiled (3D) failed: " + std::to_string(int(r)));
 }
