@@ -22,3 +22,12 @@ ncu --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_
 python tools/compress_exec_flops.py sum gpurun_out/exec_flops_c3.csv        > gpurun_out/r02_compress_exec_flops_c3.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_launches.csv \
     python bench.py --steps 2 --warmup 1 --no-compress                      > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/r02_launches.csv                  > gpurun_out/r02_launches_summary.txt
+python tools/compress_timeline.py 3 1048576 4 1e-6 2 seq                    > gpurun_out/r02_compress_timeline_c3.txt 2>&1
+bash tools/ncu_bsr_mv_tma.sh                                                # -> gpurun_out/bsr_tma.ncu-rep
+ncu --set full --import-source on --clock-control none -k regex:k_bsr_tma -s 1 -c 1 -o gpurun_out/r02_k_bsr_tma \
+    python tools/microbench/c4_hmv.py 3                                     > /dev/null 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench/tma_stream tools/microbench/tma_stream.cu -lcuda \
+    && ./tools/microbench/tma_stream                                        > gpurun_out/r02_tma_stream.txt 2>&1
+python tools/microbench/compressed_hmv.py                                   > gpurun_out/r02_compressed_hmv.json 2>&1
+python tools/microbench/compressed_mv16.py                                  > gpurun_out/r02_compressed_mv16.json 2>&1
