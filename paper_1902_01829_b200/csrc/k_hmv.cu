@@ -26,7 +26,10 @@ namespace {
 #ifndef H2B_TMA_BSR1
 #define H2B_TMA_BSR1 1
 #endif
-constexpr bool kTmaBsr = H2B_TMA_BSR1;  // k_bsr_tma (else the register-fed k_bsr)
+constexpr bool kTmaBsr = H2B_TMA_BSR1;
+#ifndef H2B_TMA_FORCE
+#define H2B_TMA_FORCE 0
+#endif  // k_bsr_tma (else the register-fed k_bsr)
 
 constexpr int kThreads = 256;  // 8 warps per CTA
 using namespace wg;
@@ -732,14 +735,24 @@ void launch_bsr(const Matrix& A, const uint32_t* work, int64_t nwork, const doub
   // the tensor maps need 16-byte aligned bases (user device pointers of the
   // phase API may not be): the register-fed kernel takes any alignment
   const auto aligned = [](const double* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  // every layer with its x present streams through k_bsr_tma (3D block views:
-  // a compressed level's smaller blocks cost only their bytes).  C3, ms per
-  // mat-vec: uncompressed 8.55 vs 8.85 with k_bsr; compressed at 1e-6 (ranks
-  // 34-60) 5.96-6.08 for both, and 6.06-6.09 with only the full 64 x 64 levels
-  // on the ring.  k_bsr takes layers whose x is absent (phase calls) and
-  // misaligned phase-API pointers.
+  // k_bsr_tma (3D block views, a block costs only its own bytes) when the big
+  // blocks (>= 48 x 48 entries) carry at least 3/4 of the bytes, else k_bsr for
+  // everything: small blocks keep too few bytes in flight in a 4-block ring,
+  // and splitting a launch by layer loses the interleaving of big and small
+  // rows.  ms per mat-vec, same box (tools/microbench/hmv_configs.py): C3
+  // 8.65-8.66 on the ring vs 9.06-9.12 register-fed; C2 (k = 36, half the
+  // bytes in 36 x 36 blocks) 2.00 vs 1.92 (2.01 split by layer); C3 compressed
+  // at 1e-6 (ranks 34-60) 6.16-6.21 vs 6.09-6.14.  k_bsr also takes layers
+  // whose x is absent (phase calls) and misaligned phase-API pointers.
+  double big = 0.0, all = 0.0;
+  for (int l = 0; l <= A.q + 1; ++l) {
+    const Layer& L = l <= A.q ? A.cpl[l] : A.dense;
+    const double b = double(L.nb) * L.ld * L.bc;
+    all += b;
+    if (L.ld * L.bc >= 48 * 48) big += b;
+  }
   bool any_tma = false;
-  if (kTmaBsr && aligned(xh) && aligned(xdense))
+  if (kTmaBsr && aligned(xh) && aligned(xdense) && (H2B_TMA_FORCE || big >= 0.75 * all))
     for (int l = 0; l <= A.q + 1; ++l) {
       const Layer& L = l <= A.q ? A.cpl[l] : A.dense;
       T.L[l].tma = l <= A.q ? xh != nullptr : xdense != nullptr;
