@@ -195,3 +195,27 @@ def test_compress_eps_sweep_matches_reference(gpu, ref, dim, n, order, eps):
     tol = max(10 * eps, 1e-12)
     assert rel_err(h2.hmv(A, x), y0) <= tol
     assert rel_err(h2.hmv(A, x), R.hmv(x)) <= tol
+
+
+@pytest.mark.parametrize("dim,n,order,eps", [
+    (2, 1 << 14, 8, 3e-10),  # ranks 34, 50, 53, 60, 59, 53: odd big blocks (TMA-streamed)
+    (2, 1 << 15, 8, 1e-12),  # 61, 64, 64, 63, 64, 63
+    (3, 1 << 13, 4, 1e-9),   # 64 throughout
+    (2, 1 << 14, 6, 1e-7),   # 20, 29, 31, 35, 34, 32: small blocks (register-fed)
+])
+def test_compressed_hmv_matches_oracle_on_same_matrix(gpu, orc, dim, n, order, eps):
+    """The mat-vec of a COMPRESSED matrix (odd ranks, ld = rank + 1, narrow
+    blocks; the TMA-streamed or register-fed coupling kernel by block size)
+    against the oracle's hmv on the very same compressed matrix exported to the
+    host: equal to rounding, not just within the compression tolerance."""
+    A = h2.H2Matrix.construct(dim, n, grid_order=order)
+    h2.compress(A, eps)
+    O = orc.from_host(A.to_host())
+    rng = np.random.default_rng(17)
+    x, y0 = rng.uniform(-1.0, 1.0, n), rng.uniform(-1.0, 1.0, n)
+    assert rel_err(h2.hmv(A, x), O.hmv(x)) <= 1e-13, A.info().ranks
+    assert rel_err(h2.hmv(A, x, y0.copy(), 0.5, -2.0), O.hmv(x, y0.copy(), 0.5, -2.0)) <= 1e-13
+    X = rng.uniform(-1.0, 1.0, (16, n))
+    Y = h2.hmv_multi(A, X)
+    for v in (0, 9):
+        assert rel_err(Y[v], O.hmv(X[v])) <= 1e-13
