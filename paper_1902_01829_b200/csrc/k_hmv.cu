@@ -27,6 +27,14 @@ namespace {
 #define H2B_TMA_BSR1 1
 #endif
 constexpr bool kTmaBsr = H2B_TMA_BSR1;
+// fused sweeps: 0 claim an item after the previous one and prefetch its
+// transfers into L2 before its flag wait; 1 claim the next item ahead and
+// prefetch it while this one runs -- measured 1.10 -> 1.58 ms per sweep at C4
+// (an item claimed ahead holds back the items that wait on it); -1 no prefetch
+#ifndef H2B_SWEEP_AHEAD
+#define H2B_SWEEP_AHEAD 0
+#endif
+constexpr int kSweepAhead = H2B_SWEEP_AHEAD;
 #ifndef H2B_TMA_FORCE
 #define H2B_TMA_FORCE 0
 #endif  // k_bsr_tma (else the register-fed k_bsr)
@@ -170,19 +178,31 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant_
   const uint32_t epoch = 2u * uint32_t(__ldcg(ep));  // up flags of this mat-vec
   const int r = 2 * lane_id();
   const int64_t total = S.start[S.nl];
+  // bulk L2 prefetch of an item's two child transfers ahead of its flag waits
+  // (C4 mat-vec 12.41 -> 12.34 ms, C2 1.850 -> 1.815 ms; three A/B pairs)
+  auto prefetch = [&](int64_t i) {
+    if (kSweepAhead < 0 || i >= total || lane_id() != 0) return;
+    int e = 0;
+    while (i >= S.start[e + 1]) ++e;
+    const SweepLevel& L = S.L[e];
+    if (L.kc > 0 && L.kp > 0) {
+      const double* pf = L.T + (2 * (L.i0 + (i - S.start[e])) - L.cbegin) * L.stride;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(uint32_t(2 * L.stride * 8)) : "memory");
+    }
+  };
+  int64_t next = claim(ticket, base);
+  prefetch(next);
   for (;;) {
-    const int64_t it = claim(ticket, base);
+    const int64_t it = next;
     if (it >= total) break;
+    if (kSweepAhead > 0) {
+      next = claim(ticket, base);
+      prefetch(next);
+    }
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevel& L = S.L[e];
     const int64_t p = L.i0 + (it - S.start[e]);
-    // bulk L2 prefetch of both children's transfers ahead of the flag waits
-    // (C4 mat-vec 12.41 -> 12.34 ms, C2 1.850 -> 1.815 ms; three A/B pairs)
-    if (lane_id() == 0 && L.kc > 0 && L.kp > 0) {
-      const double* pf = L.T + (2 * p - L.cbegin) * L.stride;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(uint32_t(2 * L.stride * 8)) : "memory");
-    }
     if (L.l < S.q) {  // children computed by this launch (level q: input, e.g. by k_up_leaf)
       wait_flag(flag + node_id(L.l, 2 * p), epoch);
       wait_flag(flag + node_id(L.l, 2 * p + 1), epoch);
@@ -202,6 +222,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_up_fused(const __grid_constant_
       if (r + 1 < L.kp) L.out[p * L.kp + r + 1] = o1;
     }
     set_flag(flag + node_id(L.l - 1, p), epoch);
+    if (kSweepAhead <= 0) {
+      next = claim(ticket, base);
+      prefetch(next);
+    }
   }
 }
 
@@ -213,17 +237,29 @@ __global__ void __launch_bounds__(kThreads) k_down_fused(const __grid_constant__
   const uint32_t epoch = 2u * uint32_t(__ldcg(ep)) + 1u;  // down flags of this mat-vec
   const int r = 2 * lane_id();
   const int64_t total = S.start[S.nl];
+  auto prefetch = [&](int64_t i) {  // the transfer block, ahead of the flag wait (see k_up_fused)
+    if (kSweepAhead < 0 || i >= total || lane_id() != 0) return;
+    int e = 0;
+    while (i >= S.start[e + 1]) ++e;
+    const SweepLevel& L = S.L[e];
+    if (L.kc > 0 && L.kp > 0) {
+      const double* pf = L.T + (L.i0 + (i - S.start[e]) - L.cbegin) * L.stride;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(uint32_t(L.stride * 8)) : "memory");
+    }
+  };
+  int64_t next = claim(ticket, base);
+  prefetch(next);
   for (;;) {
-    const int64_t it = claim(ticket, base);
+    const int64_t it = next;
     if (it >= total) break;
+    if (kSweepAhead > 0) {
+      next = claim(ticket, base);
+      prefetch(next);
+    }
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevel& L = S.L[e];
     const int64_t c = L.i0 + (it - S.start[e]);
-    if (lane_id() == 0 && L.kc > 0 && L.kp > 0) {  // the transfer block, ahead of the flag wait
-      const double* pf = L.T + (c - L.cbegin) * L.stride;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(uint32_t(L.stride * 8)) : "memory");
-    }
     if (L.l - 1 > S.q) wait_flag(flag + node_id(L.l - 1, c >> 1), epoch);  // (top parent level: input)
     if (L.kc > 0 && L.kp > 0) {
       const double* yp = L.in + (c >> 1) * L.kp;
@@ -235,6 +271,10 @@ __global__ void __launch_bounds__(kThreads) k_down_fused(const __grid_constant__
       if (r + 1 < L.kc) y[r + 1] = acc1 + __ldcg(y + r + 1);
     }
     set_flag(flag + node_id(L.l, c), epoch);
+    if (kSweepAhead <= 0) {
+      next = claim(ticket, base);
+      prefetch(next);
+    }
   }
 }
 
