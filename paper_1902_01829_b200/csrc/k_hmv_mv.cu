@@ -49,6 +49,14 @@ constexpr int kLeafWarps = 4; // leaf kernels: 4 warps x 8 KB shared panel
 // leaf kernels (the next leaf of the warp) raised their DRAM reads 1.5-1.7x
 // and their times (profiles/r02_mv16_launches.txt): not used there.
 constexpr bool kPrefetch = H2B_MV_PREFETCH;
+// fused 16-vector sweeps: claim the next item before this one (1) or after it
+// (0).  C4, same box: k_down_fused_mv 1.50-1.53 ms claiming ahead, 1.37-1.38
+// after (an item claimed ahead holds back the items that wait on it);
+// k_up_fused_mv 1.25 either way.
+#ifndef H2B_MV_CLAIM_AHEAD
+#define H2B_MV_CLAIM_AHEAD 0
+#endif
+constexpr bool kMvClaimAhead = H2B_MV_CLAIM_AHEAD;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int64_t warp_global() {
@@ -378,7 +386,7 @@ __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant_
   for (;;) {
     const int64_t it = next;
     if (it >= total) break;
-    next = df::claim(ticket);  // claimed ahead: its atomic overlaps this item (claims stay monotone)
+    if (kMvClaimAhead) next = df::claim(ticket);  // claimed ahead: its atomic overlaps this item
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevelMV& L = S.L[e];
@@ -409,6 +417,7 @@ __global__ void __launch_bounds__(kThreads) k_up_fused_mv(const __grid_constant_
       store_panel(acc, L.out + p * L.kp * NV + v0, L.kp, false);
     }
     df::set_flag(flag_of<SPLIT>(flag, L.l - 1, p, h), epoch);
+    if (!kMvClaimAhead) next = df::claim(ticket);
   }
 }
 
@@ -425,7 +434,7 @@ __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constan
   for (;;) {
     const int64_t it = next;
     if (it >= total) break;
-    next = df::claim(ticket);  // claimed ahead: its atomic overlaps this item (claims stay monotone)
+    if (kMvClaimAhead) next = df::claim(ticket);  // claimed ahead: its atomic overlaps this item
     int e = 0;
     while (it >= S.start[e + 1]) ++e;
     const SweepLevelMV& L = S.L[e];
@@ -446,6 +455,7 @@ __global__ void __launch_bounds__(kThreads) k_down_fused_mv(const __grid_constan
       store_panel_pr(acc, L.out + c * L.kc * NV + v0, L.kc, true);
     }
     df::set_flag(flag_of<SPLIT>(flag, L.l, c, h), epoch);
+    if (!kMvClaimAhead) next = df::claim(ticket);
   }
 }
 
