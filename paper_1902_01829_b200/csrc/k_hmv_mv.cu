@@ -771,7 +771,10 @@ constexpr int kSplit = 0;
 #define H2B_TMA_BSR 1
 #endif
 constexpr bool kTmaBsr = H2B_TMA_BSR;
-constexpr int kUnrDown = 2;  // pair-steps in flight of the fused downsweep (see kUnr)
+#ifndef H2B_UNR_DOWN
+#define H2B_UNR_DOWN 2
+#endif
+constexpr int kUnrDown = H2B_UNR_DOWN;  // pair-steps in flight of the fused downsweep (see kUnr)
 
 unsigned flat_grid_mv(int64_t items) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(sms()) * 16)));
