@@ -774,7 +774,11 @@ constexpr bool kTmaBsr = H2B_TMA_BSR;
 #ifndef H2B_UNR_DOWN
 #define H2B_UNR_DOWN 2
 #endif
-constexpr int kUnrDown = H2B_UNR_DOWN;  // pair-steps in flight of the fused downsweep (see kUnr)
+constexpr int kUnrDown = H2B_UNR_DOWN;
+#ifndef H2B_UNR_UP
+#define H2B_UNR_UP 4  // C4: 1.25 ms at 1, 1.45 at 2, 1.22 at 4
+#endif
+constexpr int kUnrUp = H2B_UNR_UP;  // pair-steps in flight of the fused upsweep  // pair-steps in flight of the fused downsweep (see kUnr)
 
 unsigned flat_grid_mv(int64_t items) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(sms()) * 16)));
@@ -833,7 +837,7 @@ void mv_up_local(Matrix& A, Work& w, const double* X, int64_t ldx, int nv, cudaS
     }
     T.start[T.nl] = tot;
     H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
-    k_up_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
+    k_up_fused_mv<POL, kUnrUp, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, kUnrUp, kSplit>), kThreads, 0, s>>>(
         T, w.flag.p, w.ticket.p + 2, w.ticket.p);
     H2B_CUDA(cudaGetLastError());
   }
@@ -866,7 +870,7 @@ void mv_up_top(Matrix& A, Work& w, cudaStream_t s) {
   }
   T.start[T.nl] = tot;
   H2B_CUDA(cudaMemsetAsync(w.ticket.p, 0, sizeof(unsigned long long), s));
-  k_up_fused_mv<POL, UNR, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, UNR, kSplit>), kThreads, 0, s>>>(
+  k_up_fused_mv<POL, kUnrUp, kSplit><<<persistent_grid_mv((const void*)k_up_fused_mv<POL, kUnrUp, kSplit>), kThreads, 0, s>>>(
       T, w.flag.p, w.ticket.p + 2, w.ticket.p);
   H2B_CUDA(cudaGetLastError());
 }
@@ -993,7 +997,9 @@ void mv_finish(Matrix& A, Work& w, double* Y, int64_t ldy, int nv, double alpha,
 // One pair-step in flight (kUnr = 1) beat two for the leaves and the upsweep
 // once the loads were non-coherent (k_up_fused_mv 1.46 -> 1.24 ms, the leaf
 // kernels 0.69 / 0.76 -> 0.64 / 0.68 ms); the downsweep keeps two (1.41 vs
-// 1.49 ms with its L2 prefetch).
+// 1.49 ms with its L2 prefetch).  With the sweeps claiming items after the
+// current one, the fused upsweep runs best at four (1.22 vs 1.25 ms at one,
+// 1.45 at two; kUnrUp).
 constexpr int kPol = 2, kUnr = 1;
 
 }  // namespace
